@@ -1,0 +1,150 @@
+/*
+ * termesh_b200.h -- C ABI of the B200 (sm_100a) mesh -> polygons path.
+ *
+ * Drop-in boundary for the reference `termesh` package's phase functions
+ * (paths relative to /root/reference/pkg/src/termesh):
+ *
+ *   tm_label            replaces labeling.label_all        (labeling.py:118-145)
+ *                       + mesh_core.compute_trivertex      (mesh_core.py:171-178)
+ *                       + the twin/back-slot searches      (mesh_core.py:132-149,
+ *                         labeling.py:84,110, traversal.py:250-256)
+ *   tm_check_neighbors  the neighbor-reciprocity part of   mesh_core.validate (mesh_core.py:237-263)
+ *   tm_traverse         replaces traversal.build_polygon_mesh (traversal.py:303-347)
+ *   tm_repair           replaces reparation.repair_all     (reparation.py:343-377)
+ *   tm_mesh_to_polygons_host
+ *                       the timed part of pipeline.execute (pipeline.py:137-148)
+ *                       from host arrays in the reference dtypes.
+ *
+ * Conventions
+ *   - Pointers named d_* are device pointers owned by the caller (e.g. torch
+ *     tensors); the library never frees caller memory.  Internal scratch is
+ *     owned by the tm_ctx.  `stream` is a cudaStream_t (NULL = legacy stream).
+ *   - Triangles: corners CCW, half-edge h = 3t + j is the edge opposite corner
+ *     j, origin corner (j+1)%3, target (j+2)%3 (mesh_core.py:1-14).
+ *   - Packed half-edge word (int32[3T]): (twin << 1) | frontier, border = -1.
+ *   - Polygon meshes are CSR: offsets int64[P+1], verts int32[offsets[P]];
+ *     polygon i = verts[offsets[i] .. offsets[i+1]), CCW, in the reference's
+ *     SEQUENTIAL raw order and rotation.
+ *   - Every call returns a status code.  Messages: tm_ctx_last_error();
+ *     per-kind defect counts / first element: tm_ctx_defects().
+ *     Status codes map onto the reference's exceptions:
+ *       TM_ERR_STRUCTURAL -> errors.StructuralError  (errors.py:8-16)
+ *       TM_ERR_VALIDATION -> errors.ValidationError  (errors.py:19-25)
+ *       TM_ERR_ARGUMENT   -> ValueError
+ */
+#ifndef TERMESH_B200_H
+#define TERMESH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TM_OK 0
+#define TM_ERR_STRUCTURAL 1
+#define TM_ERR_VALIDATION 2
+#define TM_ERR_CAPACITY 3
+#define TM_ERR_CUDA 4
+#define TM_ERR_ARGUMENT 5
+
+/* defect kinds reported by tm_ctx_defects (index into the 16-entry arrays);
+ * 0..6 are the kinds of mesh_core.ValidationReport (mesh_core.py:28-35) */
+#define TM_KIND_INDEX_RANGE 0
+#define TM_KIND_ORIENTATION 1
+#define TM_KIND_DEGENERATE 2
+#define TM_KIND_DUPLICATE 3
+#define TM_KIND_RECIPROCITY 4
+#define TM_KIND_EDGE_COUNT 5
+#define TM_KIND_TRIVERTEX 6
+#define TM_KIND_NEIGHBORS 7
+#define TM_KIND_WALK 8
+#define TM_KIND_NO_FRONTIER 9
+#define TM_KIND_NO_CONVERGE 10
+#define TM_KIND_SPLIT_LAW 11
+#define TM_KIND_POOL 12
+#define TM_KIND_BARRIER 13
+#define TM_KIND_NO_INTERNAL 14
+#define TM_KIND_STRUCT 15
+#define TM_NUM_KINDS 16
+
+/* repair statistics (tm_repair / tm_mesh_to_polygons_host `stats`, int64[8]);
+ * 0..3 are repair_all's stats_out keys (reparation.py:372-376) */
+#define TM_STAT_ROUNDS 0
+#define TM_STAT_SPLITS 1
+#define TM_STAT_INITIAL_TIPS 2
+#define TM_STAT_UNREPAIRED 3
+#define TM_STAT_NONSIMPLE 4 /* pipeline.py:150 nonsimple_after_traversal */
+#define TM_STAT_TIP_SPLITS 5
+#define TM_STAT_PINCH_SPLITS 6
+#define TM_STAT_WORK_ITEMS 7
+#define TM_NUM_STATS 8
+
+typedef struct tm_ctx tm_ctx;
+
+int tm_version(void);
+int tm_ctx_create(tm_ctx **out);
+void tm_ctx_destroy(tm_ctx *ctx);
+const char *tm_ctx_last_error(const tm_ctx *ctx);
+int tm_ctx_defects(const tm_ctx *ctx, int64_t *counts, int64_t *first); /* TM_NUM_KINDS each */
+/* per-phase device milliseconds of the last tm_mesh_to_polygons* call:
+ * [0] label (K0+K1+K2), [1] traversal (K3), [2] reparation + stitch (K4) */
+int tm_ctx_phase_ms(const tm_ctx *ctx, double *ms3);
+
+/* Labels.  tri_bits = 32 or 64 (reference triangles are int64).  check != 0
+ * also reports index_range / orientation / degenerate / edge_count /
+ * reciprocity defects as TM_ERR_VALIDATION.
+ * Outputs (device): d_tri32 int32[3T] (may equal d_tri when tri_bits == 32),
+ * d_halfedge int32[3T], d_max_edge int8[T], d_seed uint8[T], d_trivertex int32[n]. */
+int tm_label(tm_ctx *ctx, const double *d_xy, int64_t n_vertices, const void *d_tri, int tri_bits, int64_t T,
+             int check, int32_t *d_tri32, int32_t *d_halfedge, int8_t *d_max_edge, uint8_t *d_seed,
+             int32_t *d_trivertex, void *stream);
+
+/* Recompute frontier bits and seeds from a caller max_edge (labeling.py:65-115
+ * with a given max_edge); d_halfedge must hold packed words from tm_label. */
+int tm_relabel(tm_ctx *ctx, int32_t *d_halfedge, const int8_t *d_max_edge, int64_t T, uint8_t *d_seed, void *stream);
+
+/* neighbors[h] must equal twin[h] / 3 (or -1): TM_ERR_VALIDATION otherwise */
+int tm_check_neighbors(tm_ctx *ctx, const int32_t *d_halfedge, const void *d_neighbors, int nb_bits, int64_t T,
+                       void *stream);
+
+/* expand packed words to the reference arrays (either output may be NULL) */
+int tm_unpack_halfedges(tm_ctx *ctx, const int32_t *d_halfedge, int64_t T, int32_t *d_twin, uint8_t *d_frontier,
+                        void *stream);
+/* overwrite the frontier bits from a caller frontier array (bool/uint8 [3T]) */
+int tm_pack_frontier(tm_ctx *ctx, int32_t *d_halfedge, const uint8_t *d_frontier, int64_t T, void *stream);
+
+/* Traversal.  Capacities: cap_polys >= #seeds, cap_slots >= #frontier
+ * half-edges (T and 3T always suffice).  *n_polys / *n_slots are host outputs;
+ * the call synchronizes `stream` before returning them. */
+int tm_traverse(tm_ctx *ctx, const int32_t *d_tri32, const int32_t *d_halfedge, const uint8_t *d_seed, int64_t T,
+                int64_t *d_offsets, int32_t *d_verts, int64_t cap_polys, int64_t cap_slots, int64_t *n_polys,
+                int64_t *n_slots, void *stream);
+
+/* Repair.  Mutates the frontier bits of d_halfedge exactly as repair_all
+ * mutates labels.frontier.  Capacities T and 3T always suffice.  stats: host
+ * int64[TM_NUM_STATS]. */
+int tm_repair(tm_ctx *ctx, const int32_t *d_tri32, int32_t *d_halfedge, const int32_t *d_trivertex, int64_t T,
+              const int64_t *d_offsets_in, const int32_t *d_verts_in, int64_t n_polys, int64_t *d_offsets_out,
+              int32_t *d_verts_out, int64_t cap_polys, int64_t cap_slots, int64_t *n_polys_out, int64_t *n_slots_out,
+              int64_t *stats, void *stream);
+
+/* Whole path from HOST arrays in the reference dtypes (Triangulation.vertices
+ * f64[2n], Triangulation.triangles i64[3T]); host->device copies, label,
+ * traversal, repair and the device->host copy of the final CSR all happen
+ * inside.  Output capacities T+1 / 3T always suffice.  Pinned host buffers
+ * give full PCIe bandwidth. */
+int tm_mesh_to_polygons_host(tm_ctx *ctx, const double *h_vertices, int64_t n_vertices, const int64_t *h_triangles,
+                             int64_t T, int check, int64_t *h_offsets, int32_t *h_verts, int64_t cap_polys,
+                             int64_t cap_slots, int64_t *n_polys, int64_t *n_slots, int64_t *stats);
+
+/* Same pipeline on caller device buffers (no host copies). */
+int tm_mesh_to_polygons(tm_ctx *ctx, const double *d_xy, int64_t n_vertices, const void *d_tri, int tri_bits,
+                        int64_t T, int check, int64_t *d_offsets, int32_t *d_verts, int64_t cap_polys,
+                        int64_t cap_slots, int64_t *n_polys, int64_t *n_slots, int64_t *stats, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

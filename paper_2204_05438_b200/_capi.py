@@ -1,0 +1,164 @@
+"""ctypes binding of libtermesh_b200.so (include/termesh_b200.h).
+
+The product path has exactly one implementation: the sm_100a kernels behind
+this C ABI.  If the library is missing or no CUDA device is visible, every
+entry point raises -- there is no CPU fallback.
+"""
+
+import ctypes
+import os
+import threading
+
+from .errors import CapacityError, StructuralError, TermeshError, ValidationError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtermesh_b200.so")
+
+TM_OK, TM_ERR_STRUCTURAL, TM_ERR_VALIDATION, TM_ERR_CAPACITY, TM_ERR_CUDA, TM_ERR_ARGUMENT = range(6)
+NUM_KINDS = 16
+NUM_STATS = 8
+KIND_NAMES = ("index_range", "orientation", "degenerate", "duplicate", "reciprocity", "edge_count",
+              "trivertex", "neighbors", "walk", "no_frontier", "no_converge", "split_law", "pool",
+              "barrier", "no_internal", "structural")
+STAT_NAMES = ("rounds", "splits", "initial_tips", "unrepaired", "nonsimple", "tip_splits",
+              "pinch_splits", "work_items")
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I = ctypes.c_int
+_PI64 = ctypes.POINTER(ctypes.c_int64)
+
+_lib = None
+_lock = threading.Lock()
+_ctxs = {}
+
+
+class ExtensionMissing(TermeshError, ImportError):
+    """libtermesh_b200.so is not built (run `python -m paper_2204_05438_b200.build`)."""
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ExtensionMissing(f"{LIB_PATH} not built; run `python -m paper_2204_05438_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        L.tm_version.restype = _I
+        L.tm_ctx_create.argtypes = [ctypes.POINTER(_P)]
+        L.tm_ctx_destroy.argtypes = [_P]
+        L.tm_ctx_destroy.restype = None
+        L.tm_ctx_last_error.argtypes = [_P]
+        L.tm_ctx_last_error.restype = ctypes.c_char_p
+        L.tm_ctx_defects.argtypes = [_P, _PI64, _PI64]
+        L.tm_ctx_phase_ms.argtypes = [_P, ctypes.POINTER(ctypes.c_double)]
+        L.tm_label.argtypes = [_P, _P, _I64, _P, _I, _I64, _I, _P, _P, _P, _P, _P, _P]
+        L.tm_relabel.argtypes = [_P, _P, _P, _I64, _P, _P]
+        L.tm_check_neighbors.argtypes = [_P, _P, _P, _I, _I64, _P]
+        L.tm_unpack_halfedges.argtypes = [_P, _P, _I64, _P, _P, _P]
+        L.tm_pack_frontier.argtypes = [_P, _P, _P, _I64, _P]
+        L.tm_traverse.argtypes = [_P, _P, _P, _P, _I64, _P, _P, _I64, _I64, _PI64, _PI64, _P]
+        L.tm_repair.argtypes = [_P, _P, _P, _P, _I64, _P, _P, _I64, _P, _P, _I64, _I64, _PI64, _PI64, _PI64, _P]
+        L.tm_mesh_to_polygons.argtypes = [_P, _P, _I64, _P, _I, _I64, _I, _P, _P, _I64, _I64, _PI64, _PI64,
+                                          _PI64, _P]
+        L.tm_mesh_to_polygons_host.argtypes = [_P, _P, _I64, _P, _I64, _I, _P, _P, _I64, _I64, _PI64, _PI64,
+                                               _PI64]
+        for name in ("tm_ctx_create", "tm_ctx_defects", "tm_ctx_phase_ms", "tm_label", "tm_relabel",
+                     "tm_check_neighbors",
+                     "tm_unpack_halfedges", "tm_pack_frontier", "tm_traverse", "tm_repair",
+                     "tm_mesh_to_polygons", "tm_mesh_to_polygons_host"):
+            getattr(L, name).restype = _I
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    """Names declared in include/termesh_b200.h (checked by the CPU tests)."""
+    return ("tm_version", "tm_ctx_create", "tm_ctx_destroy", "tm_ctx_last_error", "tm_ctx_defects",
+            "tm_ctx_phase_ms", "tm_label", "tm_relabel", "tm_check_neighbors", "tm_unpack_halfedges",
+            "tm_pack_frontier",
+            "tm_traverse", "tm_repair", "tm_mesh_to_polygons_host", "tm_mesh_to_polygons")
+
+
+def _require_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        raise TermeshError("termesh-b200 requires a CUDA device (sm_100a); no CPU fallback exists")
+    return torch
+
+
+class Context:
+    """One tm_ctx per CUDA device (owns the library's scratch buffers)."""
+
+    def __init__(self, device_index: int):
+        self.device_index = device_index
+        p = _P()
+        rc = lib().tm_ctx_create(ctypes.byref(p))
+        if rc != TM_OK:
+            raise TermeshError(f"tm_ctx_create failed with status {rc}")
+        self.ptr = p
+
+    def defects(self):
+        counts = (ctypes.c_int64 * NUM_KINDS)()
+        first = (ctypes.c_int64 * NUM_KINDS)()
+        lib().tm_ctx_defects(self.ptr, counts, first)
+        return [(KIND_NAMES[k], int(first[k]), int(counts[k])) for k in range(NUM_KINDS) if counts[k]]
+
+    def phase_ms(self):
+        ms = (ctypes.c_double * 3)()
+        lib().tm_ctx_phase_ms(self.ptr, ms)
+        return list(ms)
+
+    def last_error(self) -> str:
+        return lib().tm_ctx_last_error(self.ptr).decode()
+
+    def check(self, rc: int, phase: str | None = None):
+        if rc == TM_OK:
+            return
+        msg = self.last_error()
+        if rc == TM_ERR_VALIDATION:
+            from .mesh_core import ValidationReport
+            defects = [(kind, idx, f"{count} defect(s), first at element {idx}")
+                       for kind, idx, count in self.defects() if KIND_NAMES.index(kind) <= 7]
+            raise ValidationError("refusing to run on an invalid triangulation: " + msg,
+                                  ValidationReport(False, defects))
+        if rc == TM_ERR_STRUCTURAL:
+            raise StructuralError(msg)  # message already carries the [phase] tag
+        if rc == TM_ERR_CAPACITY:
+            raise CapacityError(msg)
+        if rc == TM_ERR_ARGUMENT:
+            raise ValueError(msg)
+        raise TermeshError(f"CUDA failure: {msg}")
+
+
+def context(device=None) -> Context:
+    torch = _require_cuda()
+    idx = torch.cuda.current_device() if device is None else torch.device(device).index
+    if idx is None:
+        idx = torch.cuda.current_device()
+    c = _ctxs.get(idx)
+    if c is None:
+        with _lock:
+            c = _ctxs.get(idx)
+            if c is None:
+                with torch.cuda.device(idx):
+                    c = Context(idx)
+                _ctxs[idx] = c
+    return c
+
+
+def stream_ptr(device=None):
+    torch = _require_cuda()
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def ptr(t):
+    """Device/host pointer of a torch tensor or numpy array as c_void_p (None -> NULL)."""
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        return ctypes.c_void_p(t.data_ptr())
+    return ctypes.c_void_p(t.ctypes.data)

@@ -1,0 +1,69 @@
+// tm_internal.h -- launch wrappers shared between the kernel translation units
+// and the C-ABI orchestration (tm_capi.cu).  Not part of the public ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tmb {
+
+struct DevStatus;
+
+// tm_label.cu
+uint64_t hash_capacity(int64_t T);
+void launch_label(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int check, int32_t* tri32,
+                  int32_t* hw, int8_t* max_edge, uint8_t* seed, int32_t* tv, uint32_t* slots, uint64_t cap,
+                  DevStatus* st, cudaStream_t s);
+void launch_relabel(const int8_t* max_edge, int64_t T, int32_t* hw, uint8_t* seed, cudaStream_t s);
+void launch_check_neighbors(const int32_t* hw, const void* nb, int nb_is64, int64_t T, DevStatus* st, cudaStream_t s);
+void launch_unpack(const int32_t* hw, int64_t T, int32_t* twin, uint8_t* fr, cudaStream_t s);
+void launch_pack_frontier(int32_t* hw, int64_t T, const uint8_t* fr, cudaStream_t s);
+
+// tm_traverse.cu
+size_t select_seeds_temp_bytes(int64_t T);
+void launch_select_seeds(const uint8_t* seed, int64_t T, int32_t* seeds, int64_t* n_seeds, void* temp,
+                         size_t temp_bytes, cudaStream_t s);
+size_t scan_temp_bytes(int64_t n);
+void launch_scan(const int64_t* in, int64_t* out, int64_t n, void* temp, size_t temp_bytes, cudaStream_t s);
+void launch_trav_start(const int32_t* hw, const int32_t* seeds, int64_t P, int32_t* start, int32_t* overflow,
+                       unsigned int* n_overflow, int32_t* queue, int32_t* stamp, DevStatus* st, cudaStream_t s);
+void launch_trav_len(const int32_t* hw, const int32_t* seeds, const int32_t* start, int64_t P, int64_t T,
+                     int64_t* len, DevStatus* st, cudaStream_t s);
+void launch_trav_write(const int32_t* tri, const int32_t* hw, const int32_t* start, int64_t P, int64_t T,
+                       const int64_t* offsets, int32_t* verts, cudaStream_t s);
+
+// tm_repair.cu
+struct RepairArgs {
+  const int32_t* tri;
+  int32_t* hw;
+  const int32_t* tv;
+  int64_t T;
+  int32_t* pool;
+  unsigned long long pool_cap;
+  unsigned long long* pool_top;
+  int32_t* undo;
+  unsigned long long* undo_top;
+  unsigned long long undo_cap;
+  DevStatus* st;
+  const int32_t* items;
+  const unsigned int* n_items;
+  const int64_t* off;
+  const int32_t* v;
+  int64_t* item_list;
+  int32_t* item_n;
+  int64_t* item_slots;
+  unsigned long long* stats;
+};
+void launch_classify(const int64_t* off, const int32_t* v, int64_t P, int32_t* item_of, int32_t* items,
+                     unsigned int* n_items, int32_t* long_list, unsigned int* n_long, unsigned long long* stats,
+                     cudaStream_t s);
+void launch_repair_items(const RepairArgs& a, cudaStream_t s);
+void launch_out_counts(const int64_t* off, int64_t P, const int32_t* item_of, const int32_t* item_n,
+                       const int64_t* item_slots, int64_t* cnt, int64_t* slots, cudaStream_t s);
+void launch_stitch(const int64_t* off, const int32_t* v, int64_t P, const int32_t* item_of, const int64_t* item_list,
+                   const int32_t* item_n, const int32_t* pool, const int64_t* pbase, const int64_t* sbase,
+                   int64_t* off_out, int32_t* v_out, cudaStream_t s);
+void launch_undo(int32_t* hw, const int32_t* undo, const unsigned long long* undo_top, unsigned long long cap,
+                 cudaStream_t s);
+
+}  // namespace tmb

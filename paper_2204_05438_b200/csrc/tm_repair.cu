@@ -1,0 +1,659 @@
+// tm_repair.cu -- K4: barrier-edge tip removal and pinch splitting, plus the
+// CSR stitch.  Replaces reparation.repair_all (reparation.py:343-377) and its
+// helpers: find_barrier_tip (59-71), the fan rotations (82-124),
+// middle_internal_edge (127-145), _pinch_candidates / _wedge_internal_edges
+// (148-205), _split_polygon (208-229) and the round driver (232-340).
+//
+// Schedule: one work item per non-simple input polygon.  The
+// item replays the reference's rounds on its own piece list (round r splits
+// every piece that still has a tip, pa before pb), which is exactly the
+// reference's global round schedule restricted to that polygon: distinct
+// polygons have disjoint interiors, so their frontier mutations never
+// interact.  Leaves come out in the reference's raw order.
+//
+// Tip splits do not re-walk the mesh: the two pieces are arcs
+// of the parent cycle cut at the tip v and at the occurrence j of u = target(e)
+// whose boundary wedge contains twin(e); each piece is then rotated to start at
+// origin(h0), h0 = smallest frontier slot of e/3 (resp. twin(e)/3), which is
+// where the reference's re-walk (poly_construction) starts.  If the wedge or
+// rotation search fails the split falls back to the re-walk.  Pinch trial splits
+// (rare) always re-walk, with revert on a broken length law.
+//
+// Piece records live in a device pool (bump allocated): {offset, len|flags}.
+// Every promoted half-edge is appended to an undo log, so a pool overflow can
+// be rolled back and retried by the host with a larger pool.
+#include <cub/device/device_scan.cuh>
+
+#include "tm_common.cuh"
+#include "tm_internal.h"
+
+namespace tmb {
+
+constexpr uint32_t F_TIP = 1u << 30;
+constexpr uint32_t F_REP = 1u << 31;
+constexpr uint32_t F_FAIL = 1u << 29;
+constexpr uint32_t LEN_MASK = (1u << 29) - 1;
+
+struct RepairCtx {
+  const int32_t* tri;
+  int32_t* hw;
+  const int32_t* tv;
+  int64_t T;
+  int32_t* pool;
+  unsigned long long pool_cap;
+  unsigned long long* pool_top;
+  int32_t* undo;
+  unsigned long long* undo_top;
+  unsigned long long undo_cap;
+  DevStatus* st;
+};
+
+__device__ __forceinline__ int64_t palloc(const RepairCtx& c, int64_t n) {
+  unsigned long long o = atomicAdd(c.pool_top, (unsigned long long)n);
+  if (o + (unsigned long long)n > c.pool_cap) return -1;
+  return (int64_t)o;
+}
+
+__device__ __forceinline__ void promote(const RepairCtx& c, int32_t e, int32_t te) {
+  c.hw[e] |= 1;
+  c.hw[te] |= 1;
+  unsigned long long k = atomicAdd(c.undo_top, 1ull);
+  if (k < c.undo_cap) c.undo[k] = e;
+}
+
+__device__ __forceinline__ void demote(const RepairCtx& c, int32_t e, int32_t te) {
+  c.hw[e] &= ~1;
+  c.hw[te] &= ~1;
+}
+
+// traversal.py:112-124 for one polygon
+__device__ bool poly_has_tip(const int32_t* s, int64_t n) {
+  for (int64_t pos = 0; pos < n; pos++) {
+    int64_t a = pos == 0 ? n - 1 : pos - 1, b = pos + 1 == n ? 0 : pos + 1;
+    if (s[a] == s[b]) return true;
+  }
+  return false;
+}
+
+// reparation.py:59-71
+__device__ int64_t first_tip(const int32_t* s, int64_t n) {
+  for (int64_t pos = 0; pos < n; pos++) {
+    int64_t a = pos == 0 ? n - 1 : pos - 1, b = pos + 1 == n ? 0 : pos + 1;
+    if (s[a] == s[b]) return pos;
+  }
+  return -1;
+}
+
+// (len - distinct) of one polygon (traversal.py:140-147).  Small polygons use a
+// quadratic scan; long ones an in-place heap sort of a scratch copy.
+__device__ void sift(int32_t* a, int64_t root, int64_t n) {
+  for (;;) {
+    int64_t ch = 2 * root + 1;
+    if (ch >= n) return;
+    if (ch + 1 < n && a[ch + 1] > a[ch]) ch++;
+    if (a[root] >= a[ch]) return;
+    int32_t t = a[root];
+    a[root] = a[ch];
+    a[ch] = t;
+    root = ch;
+  }
+}
+
+__device__ int64_t extra_visits(const int32_t* s, int64_t n, int32_t* scratch) {
+  if (n <= 48 || scratch == nullptr) {
+    int64_t extra = 0;
+    for (int64_t i = 1; i < n; i++) {
+      bool dup = false;
+      for (int64_t j = 0; j < i && !dup; j++) dup = s[j] == s[i];
+      extra += dup;
+    }
+    return extra;
+  }
+  for (int64_t i = 0; i < n; i++) scratch[i] = s[i];
+  for (int64_t r = n / 2 - 1; r >= 0; r--) sift(scratch, r, n);
+  for (int64_t e = n - 1; e > 0; e--) {
+    int32_t t = scratch[0];
+    scratch[0] = scratch[e];
+    scratch[e] = t;
+    sift(scratch, 0, e);
+  }
+  int64_t extra = 0;
+  for (int64_t i = 1; i < n; i++) extra += scratch[i] == scratch[i - 1];
+  return extra;
+}
+
+// ------------------------------------------------------------ classify
+// Per input polygon: tip flag, repeated flag, extra visits.  Work items are the
+// polygons with a repeated vertex (a tip implies one).
+__global__ void __launch_bounds__(256) k_classify(const int64_t* __restrict__ off, const int32_t* __restrict__ v,
+                                                  int64_t P, int32_t* __restrict__ item_of,
+                                                  int32_t* __restrict__ items, unsigned int* n_items,
+                                                  int32_t* __restrict__ long_list, unsigned int* n_long,
+                                                  unsigned long long* stats) {
+  unsigned long long extra_sum = 0, rep_cnt = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b = off[i], n = off[i + 1] - b;
+    item_of[i] = -1;
+    if (n > 48) {
+      long_list[atomicAdd(n_long, 1u)] = (int32_t)i;
+      continue;
+    }
+    int64_t ex = extra_visits(v + b, n, nullptr);
+    if (ex > 0) {
+      extra_sum += ex;
+      rep_cnt++;
+      unsigned int k = atomicAdd(n_items, 1u);
+      items[k] = (int32_t)i;
+      item_of[i] = (int32_t)k;
+    }
+  }
+  if (extra_sum) atomicAdd(stats + 2, extra_sum);
+  if (rep_cnt) atomicAdd(stats + 6, rep_cnt);
+}
+
+// long polygons: one warp each, quadratic duplicate count split over lanes
+__global__ void k_classify_long(const int64_t* __restrict__ off, const int32_t* __restrict__ v,
+                                const int32_t* __restrict__ long_list, const unsigned int* n_long,
+                                int32_t* __restrict__ item_of, int32_t* __restrict__ items, unsigned int* n_items,
+                                unsigned long long* stats) {
+  int lane = threadIdx.x & 31;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned int nl = *n_long;
+  for (int64_t w = warp; w < nl; w += nwarps) {
+    int32_t i = long_list[w];
+    int64_t b = off[i], n = off[i + 1] - b;
+    const int32_t* s = v + b;
+    unsigned long long ex = 0;
+    for (int64_t p = lane; p < n; p += 32) {
+      int32_t x = s[p];
+      bool dup = false;
+      for (int64_t q = 0; q < p && !dup; q++) dup = s[q] == x;
+      ex += dup;
+    }
+    for (int o = 16; o > 0; o >>= 1) ex += __shfl_xor_sync(0xffffffffu, ex, o);
+    if (lane == 0 && ex > 0) {
+      unsigned int k = atomicAdd(n_items, 1u);
+      items[k] = i;
+      item_of[i] = (int32_t)k;
+      atomicAdd(stats + 2, ex);
+      atomicAdd(stats + 6, 1ull);
+    }
+  }
+}
+
+// ------------------------------------------------------------ mesh helpers
+// reparation.py:127-145.  The fan order is cyclic (fan_step), so starting at
+// the barrier half-edge enumerates fan[barrier_at:] + fan[:barrier_at].
+__device__ int32_t middle_internal_edge(const RepairCtx& c, int32_t v, int32_t barrier, int32_t poly) {
+  int32_t t0 = c.tv[v];
+  int32_t g0 = t0 < 0 ? -1 : he_with_origin(c.tri, t0, v);
+  if (g0 < 0) { report(c.st, K_STRUCT, poly); return -1; }
+  int guard = (int)(3 * c.T + 3 < (1LL << 30) ? 3 * c.T + 3 : (1LL << 30));
+  int32_t g = g0, gb = -1;
+  int k = 0, deg = 0;
+  do {
+    int32_t w = c.hw[g];
+    if (gb < 0 && hw_front(w) && he_target(c.tri, g) == barrier) gb = g;
+    if (!hw_front(w)) k++;
+    deg++;
+    g = fan_step(c.hw, g, guard);
+    if (g < 0 || deg > guard) { report(c.st, K_STRUCT, poly); return -1; }
+  } while (g != g0);
+  if (gb < 0) { report(c.st, K_BARRIER, poly); return -1; }
+  if (k == 0) { report(c.st, K_NO_INTERNAL, poly); return -1; }
+  int want = (k - 1) / 2, cnt = 0;
+  g = gb;
+  for (int s = 0; s < deg; s++) {
+    if (!hw_front(c.hw[g])) {
+      if (cnt == want) return g;
+      cnt++;
+    }
+    g = fan_step(c.hw, g, guard);
+  }
+  report(c.st, K_STRUCT, poly);
+  return -1;
+}
+
+__device__ long long walk_len(const RepairCtx& c, int32_t h0) {
+  long long limit = 3 * c.T + 3, guard = 2 * 3 * c.T + 3, n = 0;
+  int32_t h = h0;
+  do {
+    if (++n > guard) return -1;
+    h = walk_next(c.hw, h, limit);
+    if (h < 0) return -1;
+  } while (h != h0);
+  return n;
+}
+
+__device__ void walk_write(const RepairCtx& c, int32_t h0, int32_t* out) {
+  long long limit = 3 * c.T + 3;
+  int32_t h = h0;
+  do {
+    *out++ = he_origin(c.tri, h);
+    h = walk_next(c.hw, h, limit);
+  } while (h != h0 && h >= 0);
+}
+
+// Re-walk split (reparation.py:216-229 after promotion).  Returns 1 on success
+// (pieces written), 0 when the length law fails (caller decides strictness),
+// -1 on error/capacity.
+__device__ int rewalk_split(const RepairCtx& c, int32_t e, int32_t te, int64_t plen, int32_t poly,
+                            int64_t* pa_off, int64_t* pa_len, int64_t* pb_off, int64_t* pb_len) {
+  int32_t ha = min_frontier_slot(c.hw, e / 3), hb = min_frontier_slot(c.hw, te / 3);
+  long long la = walk_len(c, ha), lb = walk_len(c, hb);
+  if (la < 0 || lb < 0) { report(c.st, K_STRUCT, poly); return -1; }
+  if (la + lb != plen + 2) return 0;
+  int64_t o = palloc(c, la + lb);
+  if (o < 0) { report(c.st, K_POOL, poly); return -1; }
+  walk_write(c, ha, c.pool + o);
+  walk_write(c, hb, c.pool + o + la);
+  *pa_off = o; *pa_len = la; *pb_off = o + la; *pb_len = lb;
+  return 1;
+}
+
+// Tip split of piece X (len L) at its first tip (reparation.py:294-312 splitter).
+__device__ bool split_tip(const RepairCtx& c, const int32_t* X, int64_t L, int32_t poly,
+                          int64_t* pa_off, int64_t* pa_len, int64_t* pb_off, int64_t* pb_len) {
+  int64_t pos = first_tip(X, L);
+  if (pos < 0) { report(c.st, K_STRUCT, poly); return false; }
+  int32_t v = X[pos], b = X[pos == 0 ? L - 1 : pos - 1];
+  int32_t e = middle_internal_edge(c, v, b, poly);
+  if (e < 0) return false;
+  int32_t te = hw_twin(c.hw[e]);
+  if (te < 0) { report(c.st, K_STRUCT, poly); return false; }
+  int32_t u = he_target(c.tri, e);
+  // incoming boundary vertex of the visit of u whose wedge holds twin(e):
+  // rotate CCW from twin(e) until the crossed edge prev(c) is frontier.
+  int32_t a_in = -1;
+  {
+    int32_t g = te;
+    long long guard = 3 * c.T + 3;
+    for (long long s = 0; s < guard; s++) {
+      int32_t p = he_prev(g);
+      int32_t w = c.hw[p];
+      if (hw_front(w)) { a_in = he_origin(c.tri, p); break; }
+      g = hw_twin(w);
+    }
+  }
+  int64_t j = -1;
+  if (a_in >= 0)
+    for (int64_t q = 0; q < L; q++)
+      if (X[q] == u && X[q == 0 ? L - 1 : q - 1] == a_in) { j = q; break; }
+  promote(c, e, te);
+  if (j >= 0) {
+    int64_t la = 1 + (pos - j + L) % L, lb = (j - pos + L) % L + 1;
+    // pa arc: A(0)=v, A(k)=X[(j+k-1)%L]; pb arc: B(k)=X[(pos+k)%L] (k<lb-1), B(lb-1)=u
+    int32_t ha = min_frontier_slot(c.hw, e / 3), hb = min_frontier_slot(c.hw, te / 3);
+    int32_t oa = he_origin(c.tri, ha), ga = he_target(c.tri, ha);
+    int32_t ob = he_origin(c.tri, hb), gb = he_target(c.tri, hb);
+    int64_t ka = -1, kb = -1;
+    for (int64_t k = 0; k < la && ka < 0; k++) {
+      int64_t k1 = k + 1 == la ? 0 : k + 1;
+      int32_t x0 = k == 0 ? v : X[(j + k - 1) % L];
+      int32_t x1 = k1 == 0 ? v : X[(j + k1 - 1) % L];
+      if (x0 == oa && x1 == ga) ka = k;
+    }
+    for (int64_t k = 0; k < lb && kb < 0; k++) {
+      int64_t k1 = k + 1 == lb ? 0 : k + 1;
+      int32_t x0 = k == lb - 1 ? u : X[(pos + k) % L];
+      int32_t x1 = k1 == lb - 1 ? u : X[(pos + k1) % L];
+      if (x0 == ob && x1 == gb) kb = k;
+    }
+    if (ka >= 0 && kb >= 0) {
+      int64_t o = palloc(c, la + lb);
+      if (o < 0) { report(c.st, K_POOL, poly); return false; }
+      int32_t* A = c.pool + o;
+      int32_t* B = A + la;
+      for (int64_t k = 0; k < la; k++) {
+        int64_t kk = (ka + k) % la;
+        A[k] = kk == 0 ? v : X[(j + kk - 1) % L];
+      }
+      for (int64_t k = 0; k < lb; k++) {
+        int64_t kk = (kb + k) % lb;
+        B[k] = kk == lb - 1 ? u : X[(pos + kk) % L];
+      }
+      *pa_off = o; *pa_len = la; *pb_off = o + la; *pb_len = lb;
+      return true;
+    }
+  }
+  int r = rewalk_split(c, e, te, L, poly, pa_off, pa_len, pb_off, pb_len);
+  if (r == 0) report(c.st, K_SPLIT_LAW, poly);
+  return r == 1;
+}
+
+__device__ __forceinline__ uint32_t tip_flag(const int32_t* s, int64_t n) { return poly_has_tip(s, n) ? F_TIP : 0u; }
+
+// ------------------------------------------------------------ tip phase
+// item_list[w] = pool offset of the item's record list, item_n[w] = #records.
+__global__ void __launch_bounds__(128) k_repair_tips(RepairCtx c, const int32_t* __restrict__ items,
+                                                     const unsigned int* n_items, const int64_t* __restrict__ off,
+                                                     const int32_t* __restrict__ v,
+                                                     int64_t* __restrict__ item_list, int32_t* __restrict__ item_n,
+                                                     unsigned long long* stats) {
+  unsigned int ni = *n_items;
+  // reparation.py:354-364: at most initial + 1 rounds, initial = extra visits of mesh0
+  long long max_rounds = (long long)stats[2] + 1;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < ni; w += (int64_t)gridDim.x * blockDim.x) {
+    int32_t i = items[w];
+    int64_t b = off[i], L = off[i + 1] - b;
+    item_list[w] = -1;
+    item_n[w] = 0;
+    int64_t base = palloc(c, L + 2);
+    if (base < 0) { report(c.st, K_POOL, i); continue; }
+    int32_t* P0 = c.pool + base;
+    for (int64_t k = 0; k < L; k++) P0[k] = v[b + k];
+    int64_t list = base + L;
+    c.pool[list] = (int32_t)base;
+    uint32_t f0 = tip_flag(P0, L);
+    c.pool[list + 1] = (int32_t)((uint32_t)L | f0);
+    int n = 1, ntips = f0 ? 1 : 0;
+    long long depth = 0, splits = 0;
+    bool bad = false;
+    while (ntips > 0 && !bad) {
+      depth++;
+      if (depth > max_rounds) { report(c.st, K_NO_CONVERGE, i); bad = true; break; }
+      int64_t nl = palloc(c, 2 * (int64_t)(n + ntips));
+      if (nl < 0) { report(c.st, K_POOL, i); bad = true; break; }
+      int m = 0, nt = 0;
+      for (int r = 0; r < n; r++) {
+        uint32_t ro = (uint32_t)c.pool[list + 2 * r], rl = (uint32_t)c.pool[list + 2 * r + 1];
+        if (!(rl & F_TIP)) {
+          c.pool[nl + 2 * m] = (int32_t)ro;
+          c.pool[nl + 2 * m + 1] = (int32_t)rl;
+          m++;
+          continue;
+        }
+        int64_t ao, al, bo, bl;
+        if (!split_tip(c, c.pool + ro, rl & LEN_MASK, i, &ao, &al, &bo, &bl)) { bad = true; break; }
+        uint32_t fa = tip_flag(c.pool + ao, al), fb = tip_flag(c.pool + bo, bl);
+        c.pool[nl + 2 * m] = (int32_t)ao;
+        c.pool[nl + 2 * m + 1] = (int32_t)((uint32_t)al | fa);
+        c.pool[nl + 2 * m + 2] = (int32_t)bo;
+        c.pool[nl + 2 * m + 3] = (int32_t)((uint32_t)bl | fb);
+        m += 2;
+        nt += (fa ? 1 : 0) + (fb ? 1 : 0);
+        splits++;
+      }
+      list = nl;
+      n = m;
+      ntips = nt;
+    }
+    if (bad) continue;
+    item_list[w] = list;
+    item_n[w] = n;
+    if (depth > 0) atomicMax(stats + 0, (unsigned long long)depth);
+    if (splits) atomicAdd(stats + 1, (unsigned long long)splits);
+    // repeated flags and extra visits of the leaves (pinch guard, reparation.py:322)
+    unsigned long long ex_sum = 0;
+    for (int r = 0; r < n; r++) {
+      uint32_t ro = (uint32_t)c.pool[list + 2 * r], rl = (uint32_t)c.pool[list + 2 * r + 1];
+      int64_t ln = rl & LEN_MASK;
+      int32_t* scratch = nullptr;
+      if (ln > 48) {
+        int64_t so = palloc(c, ln);
+        if (so < 0) { report(c.st, K_POOL, i); break; }
+        scratch = c.pool + so;
+      }
+      int64_t ex = extra_visits(c.pool + ro, ln, scratch);
+      if (ex > 0) c.pool[list + 2 * r + 1] = (int32_t)(rl | F_REP);
+      ex_sum += ex;
+    }
+    if (ex_sum) atomicAdd(stats + 5, ex_sum);
+  }
+}
+
+// ------------------------------------------------------------ pinch phase
+// Trial-split candidate g (reparation.py:326-332 with strict=False).
+__device__ int try_pinch(const RepairCtx& c, int32_t g, int64_t L, int32_t poly, int64_t* ao, int64_t* al,
+                         int64_t* bo, int64_t* bl) {
+  int32_t w = hw_twin(c.hw[g]);
+  if (w < 0) { report(c.st, K_STRUCT, poly); return -1; }
+  promote(c, g, w);
+  int r = rewalk_split(c, g, w, L, poly, ao, al, bo, bl);
+  if (r != 1) demote(c, g, w);
+  return r;
+}
+
+// _pinch_candidates (reparation.py:169-205) for one piece; returns 1 split, 0 none, -1 error
+__device__ int pinch_split(const RepairCtx& c, const int32_t* X, int64_t L, int32_t poly, int64_t* ao, int64_t* al,
+                           int64_t* bo, int64_t* bl) {
+  int32_t v = -1;
+  int64_t p1 = 0, p2 = 0;
+  for (int64_t idx = 1; idx < L && v < 0; idx++)
+    for (int64_t q = 0; q < idx; q++)
+      if (X[q] == X[idx]) { v = X[idx]; p1 = q; p2 = idx; break; }
+  if (v < 0) return 0;
+  int guard = (int)(3 * c.T + 3 < (1LL << 30) ? 3 * c.T + 3 : (1LL << 30));
+  int32_t t0 = c.tv[v];
+  int32_t g0 = t0 < 0 ? -1 : he_with_origin(c.tri, t0, v);
+  if (g0 < 0) { report(c.st, K_STRUCT, poly); return -1; }
+  int deg = 0;
+  {
+    int32_t g = g0;
+    do {
+      deg++;
+      g = fan_step(c.hw, g, guard);
+      if (g < 0 || deg > guard) { report(c.st, K_STRUCT, poly); return -1; }
+    } while (g != g0);
+  }
+  int64_t poss[2] = {p2, p1};
+  for (int q = 0; q < 2; q++) {
+    int32_t outv = X[(poss[q] + 1) % L];
+    int32_t g = g0, gout = -1;
+    for (int s = 0; s < deg; s++) {
+      if (hw_front(c.hw[g]) && he_target(c.tri, g) == outv) { gout = g; break; }
+      g = fan_step(c.hw, g, guard);
+    }
+    if (gout < 0) { report(c.st, K_STRUCT, poly); return -1; }
+    int k = 0;
+    g = fan_step(c.hw, gout, guard);
+    for (int s = 1; s < deg; s++) {
+      if (hw_front(c.hw[g])) break;
+      k++;
+      g = fan_step(c.hw, g, guard);
+    }
+    if (k == 0) continue;
+    int mid = (k - 1) / 2;
+    for (int ord = -1; ord < k; ord++) {
+      int idx = ord < 0 ? mid : ord;
+      if (ord == mid) continue;
+      int32_t cand = gout;
+      for (int s = 0; s <= idx; s++) cand = fan_step(c.hw, cand, guard);
+      int r = try_pinch(c, cand, L, poly, ao, al, bo, bl);
+      if (r != 0) return r;
+    }
+  }
+  for (int64_t idx = p1 + 1; idx < p2; idx++) {
+    int32_t x = X[idx];
+    int32_t tx = c.tv[x];
+    int32_t gx0 = tx < 0 ? -1 : he_with_origin(c.tri, tx, x);
+    if (gx0 < 0) { report(c.st, K_STRUCT, poly); return -1; }
+    int32_t g = gx0;
+    int cnt = 0;
+    do {
+      if (!hw_front(c.hw[g])) {
+        int r = try_pinch(c, g, L, poly, ao, al, bo, bl);
+        if (r != 0) return r;
+      }
+      g = fan_step(c.hw, g, guard);
+      if (g < 0 || ++cnt > guard) { report(c.st, K_STRUCT, poly); return -1; }
+    } while (g != gx0);
+  }
+  return 0;
+}
+
+__device__ uint32_t piece_flags(const RepairCtx& c, const int32_t* s, int64_t n, int32_t poly, bool* ok) {
+  uint32_t f = tip_flag(s, n);
+  int32_t* scratch = nullptr;
+  if (n > 48) {
+    int64_t so = palloc(c, n);
+    if (so < 0) { report(c.st, K_POOL, poly); *ok = false; return 0; }
+    scratch = c.pool + so;
+  }
+  if (extra_visits(s, n, scratch) > 0) f |= F_REP;
+  return f;
+}
+
+// Runs for every item: pinch rounds (bounded by the global guard, reparation.py:322-323),
+// then the item's output totals (#leaves, #slots, #unrepaired).
+__global__ void __launch_bounds__(128) k_repair_pinch(RepairCtx c, const int32_t* __restrict__ items,
+                                                      const unsigned int* n_items, int64_t* __restrict__ item_list,
+                                                      int32_t* __restrict__ item_n, int64_t* __restrict__ item_slots,
+                                                      unsigned long long* stats) {
+  unsigned int ni = *n_items;
+  long long guard = (long long)stats[5] + 1;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < ni; w += (int64_t)gridDim.x * blockDim.x) {
+    int32_t i = items[w];
+    int64_t list = item_list[w];
+    int n = item_n[w];
+    item_slots[w] = 0;
+    if (list < 0) continue;
+    int n0 = n;
+    bool ok = true;
+    for (long long r = 0; r < guard && ok; r++) {
+      int elig = 0;
+      for (int k = 0; k < n; k++) {
+        uint32_t rl = (uint32_t)c.pool[list + 2 * k + 1];
+        elig += (rl & F_REP) && !(rl & F_TIP) && !(rl & F_FAIL);
+      }
+      if (elig == 0) break;
+      int64_t nl = palloc(c, 2 * (int64_t)(n + elig));
+      if (nl < 0) { report(c.st, K_POOL, i); ok = false; break; }
+      int m = 0, did = 0;
+      for (int k = 0; k < n && ok; k++) {
+        uint32_t ro = (uint32_t)c.pool[list + 2 * k], rl = (uint32_t)c.pool[list + 2 * k + 1];
+        if ((rl & F_REP) && !(rl & F_TIP) && !(rl & F_FAIL)) {
+          int64_t ao, al, bo, bl;
+          int res = pinch_split(c, c.pool + ro, rl & LEN_MASK, i, &ao, &al, &bo, &bl);
+          if (res < 0) { ok = false; break; }
+          if (res == 1) {
+            uint32_t fa = piece_flags(c, c.pool + ao, al, i, &ok);
+            uint32_t fb = piece_flags(c, c.pool + bo, bl, i, &ok);
+            c.pool[nl + 2 * m] = (int32_t)ao;
+            c.pool[nl + 2 * m + 1] = (int32_t)((uint32_t)al | fa);
+            c.pool[nl + 2 * m + 2] = (int32_t)bo;
+            c.pool[nl + 2 * m + 3] = (int32_t)((uint32_t)bl | fb);
+            m += 2;
+            did++;
+            continue;
+          }
+          rl |= F_FAIL;  // a failed pinch fails identically in every later round
+        }
+        c.pool[nl + 2 * m] = (int32_t)ro;
+        c.pool[nl + 2 * m + 1] = (int32_t)rl;
+        m++;
+      }
+      list = nl;
+      n = m;
+      if (did == 0) break;
+    }
+    if (!ok) continue;
+    unsigned long long unrep = 0;
+    int64_t slots = 0;
+    for (int k = 0; k < n; k++) {
+      uint32_t rl = (uint32_t)c.pool[list + 2 * k + 1];
+      slots += rl & LEN_MASK;
+      unrep += (rl & F_REP) ? 1 : 0;
+    }
+    item_list[w] = list;
+    item_n[w] = n;
+    item_slots[w] = slots;
+    if (unrep) atomicAdd(stats + 3, unrep);
+    if (n != n0) atomicAdd(stats + 4, (unsigned long long)(n - n0));
+  }
+}
+
+// ------------------------------------------------------------ stitch
+__global__ void __launch_bounds__(256) k_out_counts(const int64_t* __restrict__ off, int64_t P,
+                                                    const int32_t* __restrict__ item_of, const int32_t* __restrict__ item_n,
+                                                    const int64_t* __restrict__ item_slots, int64_t* __restrict__ cnt,
+                                                    int64_t* __restrict__ slots) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= P; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i == P) { cnt[i] = 0; slots[i] = 0; continue; }
+    int32_t it = item_of[i];
+    if (it < 0) { cnt[i] = 1; slots[i] = off[i + 1] - off[i]; }
+    else { cnt[i] = item_n[it]; slots[i] = item_slots[it]; }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_stitch(const int64_t* __restrict__ off, const int32_t* __restrict__ v, int64_t P,
+                                                const int32_t* __restrict__ item_of, const int64_t* __restrict__ item_list,
+                                                const int32_t* __restrict__ item_n, const int32_t* __restrict__ pool,
+                                                const int64_t* __restrict__ pbase, const int64_t* __restrict__ sbase,
+                                                int64_t* __restrict__ off_out, int32_t* __restrict__ v_out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t it = item_of[i];
+    int64_t pb = pbase[i], sb = sbase[i];
+    if (it < 0) {
+      int64_t b = off[i], n = off[i + 1] - b;
+      off_out[pb] = sb;
+      for (int64_t k = 0; k < n; k++) v_out[sb + k] = v[b + k];
+      if (i == P - 1) off_out[pb + 1] = sb + n;
+      continue;
+    }
+    int64_t list = item_list[it];
+    int n = item_n[it];
+    for (int r = 0; r < n; r++) {
+      uint32_t ro = (uint32_t)pool[list + 2 * r], rl = (uint32_t)pool[list + 2 * r + 1];
+      int64_t ln = rl & LEN_MASK;
+      off_out[pb + r] = sb;
+      for (int64_t k = 0; k < ln; k++) v_out[sb + k] = pool[ro + k];
+      sb += ln;
+    }
+    if (i == P - 1) off_out[pb + n] = sb;
+  }
+}
+
+__global__ void k_undo(int32_t* hw, const int32_t* undo, const unsigned long long* undo_top, unsigned long long cap) {
+  unsigned long long n = *undo_top;
+  if (n > cap) n = cap;
+  for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < n;
+       k += (unsigned long long)gridDim.x * blockDim.x) {
+    int32_t e = undo[k];
+    int32_t te = hw_twin(hw[e]);
+    hw[e] &= ~1;
+    if (te >= 0) hw[te] &= ~1;
+  }
+}
+
+static inline int grid_for(int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  int64_t cap = (int64_t)kNumSMs * 16;
+  if (g > cap) g = cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+void launch_classify(const int64_t* off, const int32_t* v, int64_t P, int32_t* item_of, int32_t* items,
+                     unsigned int* n_items, int32_t* long_list, unsigned int* n_long, unsigned long long* stats,
+                     cudaStream_t s) {
+  if (P <= 0) return;
+  k_classify<<<grid_for(P, 256), 256, 0, s>>>(off, v, P, item_of, items, n_items, long_list, n_long, stats);
+  k_classify_long<<<kNumSMs * 2, 256, 0, s>>>(off, v, long_list, n_long, item_of, items, n_items, stats);
+}
+
+void launch_repair_items(const RepairArgs& a, cudaStream_t s) {
+  RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st};
+  int g = kNumSMs * 4;
+  k_repair_tips<<<g, 128, 0, s>>>(c, a.items, a.n_items, a.off, a.v, a.item_list, a.item_n, a.stats);
+  k_repair_pinch<<<g, 128, 0, s>>>(c, a.items, a.n_items, a.item_list, a.item_n, a.item_slots, a.stats);
+}
+
+void launch_out_counts(const int64_t* off, int64_t P, const int32_t* item_of, const int32_t* item_n,
+                       const int64_t* item_slots, int64_t* cnt, int64_t* slots, cudaStream_t s) {
+  k_out_counts<<<grid_for(P + 1, 256), 256, 0, s>>>(off, P, item_of, item_n, item_slots, cnt, slots);
+}
+
+void launch_stitch(const int64_t* off, const int32_t* v, int64_t P, const int32_t* item_of, const int64_t* item_list,
+                   const int32_t* item_n, const int32_t* pool, const int64_t* pbase, const int64_t* sbase,
+                   int64_t* off_out, int32_t* v_out, cudaStream_t s) {
+  if (P <= 0) return;
+  k_stitch<<<grid_for(P, 256), 256, 0, s>>>(off, v, P, item_of, item_list, item_n, pool, pbase, sbase, off_out, v_out);
+}
+
+void launch_undo(int32_t* hw, const int32_t* undo, const unsigned long long* undo_top, unsigned long long cap,
+                 cudaStream_t s) {
+  k_undo<<<kNumSMs, 256, 0, s>>>(hw, undo, undo_top, cap);
+}
+
+}  // namespace tmb

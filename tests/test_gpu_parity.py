@@ -1,0 +1,210 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's own
+outputs (golden cases from the Python reference), against the CPU oracle on
+freshly generated inputs, and against the reference's 1M golden hashes.
+
+Bar: bit-exact labels, raw polygon order + rotation, post-repair frontier,
+repair stats, canonical output.  No floating-point outputs exist on this path.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import CASE_NAMES, big_input, load_case, load_hashes
+
+pytestmark = pytest.mark.gpu
+
+
+def tm():
+    import paper_2204_05438_b200 as m
+    return m
+
+
+def _csr(pm):
+    off, v = pm.csr()
+    return off, v
+
+
+@pytest.mark.parametrize("name", CASE_NAMES)
+def test_labels_match_reference(cuda, name):
+    tri, g = load_case(name)
+    lab = tm().label_all(tri)
+    assert np.array_equal(lab.max_edge, g["max_edge"])
+    assert np.array_equal(lab.frontier, g["frontier_pre"])
+    assert np.array_equal(lab.seed, g["seed"])
+
+
+@pytest.mark.parametrize("name", CASE_NAMES)
+def test_twin_build_reproduces_neighbors_and_trivertex(cuda, name):
+    tri, g = load_case(name)
+    from paper_2204_05438_b200.device import DeviceMesh
+    dm = DeviceMesh.upload(tri, check=True, use_trivertex=False)
+    tw = dm.twin_host().astype(np.int64)
+    expect = np.where(tw < 0, -1, tw // 3)
+    assert np.array_equal(expect, tri.neighbors)
+    interior = tw >= 0
+    assert np.array_equal(tw[tw[interior]], np.flatnonzero(interior))  # involution
+    assert np.array_equal(dm.trivertex_host(), g["trivertex"].astype(np.int64))
+
+
+@pytest.mark.parametrize("name", CASE_NAMES)
+def test_traversal_raw_layout_matches_reference(cuda, name):
+    tri, g = load_case(name)
+    lab = tm().label_all(tri)
+    m0 = tm().build_polygon_mesh(tri, lab)
+    off, v = _csr(m0)
+    assert np.array_equal(off, g["mesh0_off"])
+    assert np.array_equal(v, g["mesh0_verts"])
+    assert np.array_equal(m0.mesh, g["mesh0_raw_mesh"])            # length-prefixed runs, byte for byte
+    assert np.array_equal(m0.positions, g["mesh0_raw_positions"])
+
+
+@pytest.mark.parametrize("name", CASE_NAMES)
+def test_repair_matches_reference(cuda, name):
+    tri, g = load_case(name)
+    lab = tm().label_all(tri)
+    fr_host = lab.frontier  # materialise: repair must mutate it in place
+    m0 = tm().build_polygon_mesh(tri, lab)
+    info = {}
+    fin = tm().repair_all(tri, lab, m0, stats_out=info)
+    off, v = _csr(fin)
+    assert np.array_equal(off, g["final_off"]), "polygon lengths / order differ"
+    assert np.array_equal(v, g["final_verts"]), "raw polygons differ"
+    assert np.array_equal(fr_host, g["frontier_post"])
+    assert [info[k] for k in ("rounds", "splits", "initial_tips", "unrepaired")] == g["stats"].tolist()
+
+
+@pytest.mark.parametrize("name", ["sun", "u1k_unit", "aniso2k_s1", "clust5k_s0"])
+def test_execute_and_canonical_output(cuda, name, tmp_path):
+    tri, g = load_case(name)
+    final, st = tm().execute(tri)
+    c = tm().canonicalize(final)
+    off, v = c.csr()
+    assert np.array_equal(off, g["canon_off"]) and np.array_equal(v, g["canon_verts"])
+    assert st.polygons_after_traversal == g["mesh0_off"].size - 1
+    assert st.final_polygons == g["final_off"].size - 1
+    assert st.reparation_rounds == int(g["stats"][0])
+    rec = st.to_record()
+    assert rec["schema_version"] == 1 and rec["input_triangles"] == tri.n_triangles
+    out = tmp_path / "m.polymesh"
+    tm().write_polymesh(final, tri.vertices, out)
+    verts, back = tm().read_polymesh(out)
+    assert np.array_equal(back.csr()[1], v)
+
+
+@pytest.mark.parametrize("name", ["u1k_unit", "aniso2k_s2", "clust5k_s3"])
+def test_host_c_abi_one_call(cuda, name):
+    """tm_mesh_to_polygons_host: host arrays in the reference dtypes in, final CSR out."""
+    from paper_2204_05438_b200 import _capi
+    tri, g = load_case(name)
+    T = tri.n_triangles
+    off = np.zeros(T + 1, dtype=np.int64)
+    verts = np.zeros(3 * T, dtype=np.int32)
+    npol, nsl = ctypes.c_int64(), ctypes.c_int64()
+    stats = (ctypes.c_int64 * 8)()
+    ctx = _capi.context()
+    rc = _capi.lib().tm_mesh_to_polygons_host(ctx.ptr, _capi.ptr(tri.vertices), tri.n_vertices,
+                                              _capi.ptr(tri.triangles), T, 1, _capi.ptr(off), _capi.ptr(verts),
+                                              T, 3 * T, ctypes.byref(npol), ctypes.byref(nsl), stats)
+    ctx.check(rc)
+    P, F = npol.value, nsl.value
+    assert np.array_equal(off[: P + 1], g["final_off"])
+    assert np.array_equal(verts[:F].astype(np.int64), g["final_verts"])
+    assert list(stats)[:4] == g["stats"].tolist()
+
+
+def _gpu_vs_oracle(tri):
+    r = oracle.execute(tri)
+    lab = tm().label_all(tri, check=False)
+    assert np.array_equal(lab.max_edge, r["labels"].max_edge)
+    assert np.array_equal(lab.frontier, r["frontier_pre"])
+    assert np.array_equal(lab.seed, r["labels"].seed)
+    m0 = tm().build_polygon_mesh(tri, lab)
+    assert all(np.array_equal(a, b) for a, b in zip(m0.csr(), r["mesh0"]))
+    info = {}
+    fin = tm().repair_all(tri, lab, m0, stats_out=info)
+    assert all(np.array_equal(a, b) for a, b in zip(fin.csr(), r["final"]))
+    assert np.array_equal(lab.frontier, r["labels"].frontier)
+    assert {k: info[k] for k in r["stats"]} == r["stats"]
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_random_uniform_vs_oracle(cuda, seed):
+    _gpu_vs_oracle(tm().generate_random_delaunay(20_000, seed=seed))
+
+
+@pytest.mark.parametrize("seed", [3, 4, 5, 6])
+def test_random_anisotropic_vs_oracle(cuda, seed):
+    _gpu_vs_oracle(tm().generate_anisotropic_delaunay(5_000, seed=seed))
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_random_clustered_vs_oracle(cuda, seed):
+    _gpu_vs_oracle(tm().generate_clustered_delaunay(30_000, clusters=16, sigma=0.002, seed=seed))
+
+
+# ------------------------------------------------------------------ validation
+def _bad(vertices, triangles, neighbors, trivertex=None):
+    return tm().Triangulation(vertices, triangles, neighbors, trivertex)
+
+
+def test_validation_rejects_clockwise(cuda):
+    with pytest.raises(tm().ValidationError):
+        tm().label_all(_bad([0, 0, 1, 0, 0, 1], [0, 2, 1], [-1, -1, -1]))
+
+
+def test_validation_reports_kinds(cuda):
+    flat = _bad([0, 0, 1, 0, 2, 0], [0, 1, 2], [-1, -1, -1])
+    assert any(k == "degenerate" for k, _, _ in tm().validate(flat).defects)
+    rng = _bad([0, 0, 1, 0, 0, 1], [0, 1, 7], [-1, -1, -1])
+    assert any(k == "index_range" for k, _, _ in tm().validate(rng).defects)
+    dup = _bad([0, 0, 1, 0, 0, 1], [0, 1, 2, 0, 1, 2], [-1] * 6)
+    assert not tm().validate(dup).ok
+    tri, _ = load_case("square")
+    nb = tri.neighbors.copy()
+    nb[tri.neighbors.tolist().index(0)] = -1
+    assert not tm().validate(_bad(tri.vertices, tri.triangles, nb)).ok
+    tv = tri.trivertex.copy()
+    tv[0] = 5
+    assert any(k == "trivertex" for k, _, _ in tm().validate(_bad(tri.vertices, tri.triangles, tri.neighbors, tv)).defects)
+    assert tm().validate(tri).ok
+
+
+def test_edge_shared_by_three_triangles(cuda):
+    v = [0, 0, 1, 0, 0.5, 1, 0.5, -1, 0.5, 2]
+    t = [0, 1, 2, 1, 0, 3, 0, 1, 4]
+    rep = tm().validate(_bad(v, t, [-1] * 9))
+    assert not rep.ok
+
+
+def test_empty_mesh(cuda):
+    tri = _bad([0, 0, 1, 0, 0, 1], np.empty(0, np.int64), np.empty(0, np.int64))
+    lab = tm().label_all(tri, check=False)
+    m0 = tm().build_polygon_mesh(tri, lab)
+    assert m0.count == 0
+    fin = tm().repair_all(tri, lab, m0)
+    assert fin.count == 0
+
+
+# ------------------------------------------------------------------ 1M golden
+@pytest.mark.slow
+def test_u1m_matches_reference_hashes(cuda):
+    h = load_hashes().get("u1m_unit")
+    if h is None:
+        pytest.skip("hashes.json has no u1m_unit entry")
+    from paper_2204_05438_b200.io_formats import array_hash as H
+    tri = big_input("u1m_unit")
+    assert H(tri.triangles) == h["input"]["triangles"], "regenerated input differs (scipy version?)"
+    lab = tm().label_all(tri, check=True)
+    assert H(lab.max_edge) == h["max_edge"]
+    assert H(lab.frontier) == h["frontier_pre"]
+    assert H(lab.seed) == h["seed"]
+    m0 = tm().build_polygon_mesh(tri, lab)
+    assert H(m0.mesh) == h["mesh0_raw_mesh"] and H(m0.positions) == h["mesh0_raw_positions"]
+    info = {}
+    fin = tm().repair_all(tri, lab, m0, stats_out=info)
+    off, v = fin.csr()
+    assert H(off) == h["final_off"] and H(v) == h["final_verts"]
+    assert H(lab.frontier) == h["frontier_post"]
+    assert [info[k] for k in ("rounds", "splits", "initial_tips", "unrepaired")] == h["stats"]
