@@ -1,0 +1,344 @@
+"""Benchmark: mesh -> polygons throughput (input triangles/s) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload u1m]
+
+A step is one pass of the whole hot path -- twin build + labels (K0-K2),
+traversal (K3), repair + stitch (K4) -- over one synthetic Delaunay
+triangulation (BASELINE.json configs[1]: 1M uniform points in the unit square,
+scipy Qhull, seed 0; T = 1,999,963 triangles).
+
+GPU arm (default):
+  value  device-resident: inputs (xy f64, triangles i64) already in HBM, CUDA
+         events on the launching stream around each step, L2 flushed (256 MiB
+         write) between steps outside the events; max over ranks.
+  e2e    the one-call C ABI (tm_mesh_to_polygons_host) from pinned host arrays
+         in the reference dtypes: H2D of the inputs, the path, D2H of the final
+         CSR, all inside the timed region (host wall clock per call).
+  roofline  the dominant kernel (largest device-time share) over its
+         algorithmic bytes, peak = measured HBM
+         copy bandwidth from MEASURED_PEAKS.json.
+  cpu_baseline  the CPU oracle port (oracle/, the reference algorithm in C,
+         OpenMP label+traversal, sequential repair as the reference's "mixed"
+         mode) on the same mesh, rank 0 at N=1 only.
+Multi-GPU (torchrun): every rank processes its own independent mesh (seed =
+rank): weak scaling, no data-path collective; barrier + max-over-ranks timing.
+
+Reference arm (--impl reference): the reference algorithm's CPU port (oracle/)
+on the box's host cores over the same workload, rank 0 only.
+"""
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "u1m": dict(n=1_000_000, desc="1M uniform random points in the unit square, scipy Delaunay (seed=rank)"),
+    "u10m": dict(n=10_000_000, desc="10M uniform random points in the unit square, scipy Delaunay (seed=rank)"),
+    "u100k": dict(n=100_000, desc="100k uniform random points in the unit square, scipy Delaunay (seed=rank)"),
+}
+METRIC = "triangles/sec end-to-end mesh->polygons"
+UNIT = "triangles/s"
+
+
+def load_mesh(workload, seed):
+    from paper_2204_05438_b200 import io_formats as io
+    n = WORKLOADS[workload]["n"]
+    return io.cached(f"{workload}_s{seed}_unit", lambda: io.generate_random_delaunay(n, (0.0, 0.0, 1.0, 1.0), seed))
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def algorithmic_bytes(n, T, F, P, Fp, Pp):
+    """Compulsory bytes per segment: every
+    array touched once in its device dtype."""
+    return {
+        "label_a_tri_pass": 24 * T + 16 * n + 12 * T + 1 * T + 12 * T + 4 * n,   # tri i64 in, xy, tri32, max_edge, twin, trivertex
+        "label_b_edges": 12 * T + 1 * T + 12 * T + 1 * T,                       # hw in/out, max_edge, seed
+        "select_seeds": 1 * T + 4 * P,
+        "trav_start": 4 * P + 12 * P + 4 * P,
+        "trav_len": 12 * T + 4 * P + 8 * P,
+        "trav_scan": 16 * P,
+        "trav_write": 12 * T + 4 * F + 4 * P + 8 * P + 4 * F,
+        "repair_classify": 8 * P + 4 * F + 4 * P,
+        "repair_tips": 0,
+        "repair_pinch": 0,
+        "repair_stitch": 8 * P + 4 * F + 8 * Pp + 4 * Fp,
+    }
+
+
+def run_gpu(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2204_05438_b200 as tm
+    from paper_2204_05438_b200 import _capi
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    tri = load_mesh(args.workload, rank)
+    n, T = tri.n_vertices, tri.n_triangles
+    xy = torch.from_numpy(tri.vertices).to(dev)
+    tr = torch.from_numpy(tri.triangles).to(dev)
+    off = torch.empty(T + 1, dtype=torch.int64, device=dev)
+    verts = torch.empty(3 * T, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ctx = _capi.context(dev)
+    L = _capi.lib()
+    stream = torch.cuda.current_stream(dev)
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    npol, nsl = ctypes.c_int64(), ctypes.c_int64()
+    stats = (ctypes.c_int64 * 8)()
+
+    def step():
+        rc = L.tm_mesh_to_polygons(ctx.ptr, _capi.ptr(xy), n, _capi.ptr(tr), 64, T, 0, _capi.ptr(off),
+                                   _capi.ptr(verts), T, 3 * T, ctypes.byref(npol), ctypes.byref(nsl), stats, sp)
+        ctx.check(rc)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = L.tm_launch_count()
+    with ClockSampler(local_rank) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    launches = L.tm_launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * T / (ms_per_step / 1e3)
+    P_out, F_out = npol.value, nsl.value
+    repair_stats = dict(zip(_capi.STAT_NAMES, list(stats)))
+
+    # per-kernel device time (separate profiled pass; not part of `value`)
+    ctx.set_profiling(True)
+    ctx.segments(reset=True)
+    prof_steps = max(3, min(args.steps, 10))
+    for _ in range(prof_steps):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    segs = ctx.segments(reset=True)
+    ctx.set_profiling(False)
+
+    # traversal-phase counts for the byte model
+    lab = tm.label_all(tri, check=False)
+    m0 = tm.build_polygon_mesh(tri, lab)
+    P0, F0 = m0.count, int(m0.csr()[0][-1])
+    abytes = algorithmic_bytes(n, T, F0, P0, F_out, P_out)
+    peak, peak_src = measured_peak()
+    kernels = {}
+    for name, (ms, cnt) in segs.items():
+        if cnt == 0:
+            continue
+        per = ms / cnt
+        b = abytes.get(name, 0)
+        kernels[name] = {"ms": round(per, 4), "share": None, "alg_bytes": b,
+                         "gbs": round(b / (per / 1e3) / 1e9, 1) if b and per > 0 else None}
+    tot = sum(k["ms"] for k in kernels.values()) or 1.0
+    for k in kernels.values():
+        k["share"] = round(k["ms"] / tot, 4)
+    dom = max(kernels, key=lambda k: kernels[k]["ms"]) if kernels else None
+    hbm_kernels = [k for k in kernels if kernels[k]["alg_bytes"]]
+    dom_hbm = max(hbm_kernels, key=lambda k: kernels[k]["ms"]) if hbm_kernels else None
+    d = kernels.get(dom_hbm, {})
+    achieved = d.get("gbs") or 0.0
+    roofline = {"bound": "hbm", "kernel": dom_hbm, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4) if peak else None, "traffic": None,
+                "peak_source": peak_src, "dominant_by_time": dom,
+                "note": "dominant HBM kernel; repair_tips is latency-bound (no byte roofline)"}
+
+    # e2e: one C-ABI call from pinned host buffers (reference dtypes)
+    h_xy = torch.from_numpy(tri.vertices).pin_memory()
+    h_tr = torch.from_numpy(tri.triangles).pin_memory()
+    h_off = torch.empty(T + 1, dtype=torch.int64).pin_memory()
+    h_v = torch.empty(3 * T, dtype=torch.int32).pin_memory()
+
+    def e2e_step():
+        rc = L.tm_mesh_to_polygons_host(ctx.ptr, _capi.ptr(h_xy), n, _capi.ptr(h_tr), T, 0, _capi.ptr(h_off),
+                                        _capi.ptr(h_v), T, 3 * T, ctypes.byref(npol), ctypes.byref(nsl), stats)
+        ctx.check(rc)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    if world > 1:
+        dist.barrier()
+    e2e_s = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        e2e_step()
+        e2e_s.append(time.perf_counter() - t0)
+    e2e_tot = torch.tensor([sum(e2e_s)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_tot, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_tot.item()) / args.steps * 1e3
+    e2e = {"value": round(world * T / (e2e_ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(e2e_ms, 3),
+           "h2d_bytes_per_step": 16 * n + 24 * T, "d2h_bytes_per_step": 8 * (npol.value + 1) + 4 * nsl.value,
+           "api": "tm_mesh_to_polygons_host (C ABI, pinned host buffers)"}
+    # parity spot check of the timed output against the oracle-free golden counts
+    out = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32/f64", "data": "synthetic",
+        "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"], "n_vertices": n,
+                   "triangles_per_gpu": T, "polygons": P_out, "polygon_slots": F_out,
+                   "l2": "flushed (256 MiB write) between steps", "parallelism": f"independent meshes x{world}"},
+        "e2e": e2e, "roofline": roofline, "kernels": kernels, "repair_stats": repair_stats,
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+        "step_ms": {"min": round(min(step_ms), 4), "median": round(statistics.median(step_ms), 4),
+                    "max": round(max(step_ms), 4)},
+    }
+    return out, tri
+
+
+def cpu_baseline(tri, budget_s=12.0):
+    import oracle
+    oracle.execute(tri)  # warm (page-in)
+    runs = []
+    t_start = time.perf_counter()
+    while not runs or (time.perf_counter() - t_start < budget_s and len(runs) < 5):
+        t0 = time.perf_counter()
+        oracle.execute(tri)
+        runs.append(time.perf_counter() - t0)
+    s = statistics.mean(runs)
+    return {"value": round(tri.n_triangles / s, 1), "unit": UNIT, "cores": oracle.max_threads(), "kind": "port",
+            "sample": f"full workload mesh (T={tri.n_triangles}), {len(runs)} run(s), mean {s:.3f} s; "
+                      "OpenMP label+traversal, sequential repair (reference 'mixed' mode)"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    import oracle
+    tri = load_mesh(args.workload, 0)
+    for _ in range(args.warmup):
+        oracle.execute(tri)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.execute(tri)
+        times.append(time.perf_counter() - t0)
+    s = statistics.mean(times)
+    v = round(tri.n_triangles / s, 1)
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(s * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64/f64", "data": "synthetic",
+            "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"],
+                       "triangles": tri.n_triangles},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.max_threads(), "kind": "port",
+                             "sample": f"full workload mesh per step ({args.steps} steps)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--workload", choices=tuple(WORKLOADS), default="u1m")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out, tri = run_gpu(args, rank, world, local_rank)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(tri)
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

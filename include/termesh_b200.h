@@ -92,6 +92,15 @@ int tm_ctx_defects(const tm_ctx *ctx, int64_t *counts, int64_t *first); /* TM_NU
  * [0] label (K0+K1+K2), [1] traversal (K3), [2] reparation + stitch (K4) */
 int tm_ctx_phase_ms(const tm_ctx *ctx, double *ms3);
 
+/* Optional per-kernel device timing: CUDA events around each kernel group on
+ * the launching stream.  tm_ctx_segment_ms flushes and returns the number of
+ * segments; names from tm_segment_name(k).  tm_launch_count() counts this
+ * library's own kernel launches (process-wide). */
+int tm_ctx_set_profiling(tm_ctx *ctx, int on);
+int tm_ctx_segment_ms(tm_ctx *ctx, double *ms, int64_t *counts, int n, int reset);
+const char *tm_segment_name(int k);
+int64_t tm_launch_count(void);
+
 /* Labels.  tri_bits = 32 or 64 (reference triangles are int64).  check != 0
  * also reports index_range / orientation / degenerate / edge_count /
  * reciprocity defects as TM_ERR_VALIDATION.

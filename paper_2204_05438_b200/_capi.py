@@ -29,7 +29,7 @@ _I = ctypes.c_int
 _PI64 = ctypes.POINTER(ctypes.c_int64)
 
 _lib = None
-_lock = threading.Lock()
+_lock = threading.RLock()
 _ctxs = {}
 
 
@@ -55,6 +55,11 @@ def lib():
         L.tm_ctx_last_error.restype = ctypes.c_char_p
         L.tm_ctx_defects.argtypes = [_P, _PI64, _PI64]
         L.tm_ctx_phase_ms.argtypes = [_P, ctypes.POINTER(ctypes.c_double)]
+        L.tm_ctx_set_profiling.argtypes = [_P, _I]
+        L.tm_ctx_segment_ms.argtypes = [_P, ctypes.POINTER(ctypes.c_double), _PI64, _I, _I]
+        L.tm_segment_name.argtypes = [_I]
+        L.tm_segment_name.restype = ctypes.c_char_p
+        L.tm_launch_count.restype = ctypes.c_int64
         L.tm_label.argtypes = [_P, _P, _I64, _P, _I, _I64, _I, _P, _P, _P, _P, _P, _P]
         L.tm_relabel.argtypes = [_P, _P, _P, _I64, _P, _P]
         L.tm_check_neighbors.argtypes = [_P, _P, _P, _I, _I64, _P]
@@ -66,7 +71,8 @@ def lib():
                                           _PI64, _P]
         L.tm_mesh_to_polygons_host.argtypes = [_P, _P, _I64, _P, _I64, _I, _P, _P, _I64, _I64, _PI64, _PI64,
                                                _PI64]
-        for name in ("tm_ctx_create", "tm_ctx_defects", "tm_ctx_phase_ms", "tm_label", "tm_relabel",
+        for name in ("tm_ctx_create", "tm_ctx_defects", "tm_ctx_phase_ms", "tm_ctx_set_profiling",
+                     "tm_ctx_segment_ms", "tm_label", "tm_relabel",
                      "tm_check_neighbors",
                      "tm_unpack_halfedges", "tm_pack_frontier", "tm_traverse", "tm_repair",
                      "tm_mesh_to_polygons", "tm_mesh_to_polygons_host"):
@@ -78,7 +84,8 @@ def lib():
 def exported_symbols():
     """Names declared in include/termesh_b200.h (checked by the CPU tests)."""
     return ("tm_version", "tm_ctx_create", "tm_ctx_destroy", "tm_ctx_last_error", "tm_ctx_defects",
-            "tm_ctx_phase_ms", "tm_label", "tm_relabel", "tm_check_neighbors", "tm_unpack_halfedges",
+            "tm_ctx_phase_ms", "tm_ctx_set_profiling", "tm_ctx_segment_ms", "tm_segment_name", "tm_launch_count",
+            "tm_label", "tm_relabel", "tm_check_neighbors", "tm_unpack_halfedges",
             "tm_pack_frontier",
             "tm_traverse", "tm_repair", "tm_mesh_to_polygons_host", "tm_mesh_to_polygons")
 
@@ -111,6 +118,16 @@ class Context:
         ms = (ctypes.c_double * 3)()
         lib().tm_ctx_phase_ms(self.ptr, ms)
         return list(ms)
+
+    def set_profiling(self, on: bool):
+        lib().tm_ctx_set_profiling(self.ptr, int(on))
+
+    def segments(self, reset: bool = True) -> dict:
+        """{segment name: (total device ms, launches)} since the last reset."""
+        ms = (ctypes.c_double * 32)()
+        cnt = (ctypes.c_int64 * 32)()
+        n = lib().tm_ctx_segment_ms(self.ptr, ms, cnt, 32, int(reset))
+        return {lib().tm_segment_name(k).decode(): (ms[k], int(cnt[k])) for k in range(n)}
 
     def last_error(self) -> str:
         return lib().tm_ctx_last_error(self.ptr).decode()

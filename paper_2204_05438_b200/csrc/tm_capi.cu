@@ -1,8 +1,10 @@
 // tm_capi.cu -- extern "C" entry points (include/termesh_b200.h) and the host
 // orchestration of the device phases: workspace management, status decoding
 // into the reference's error vocabulary, and the whole-path drivers.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <tuple>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -49,9 +51,33 @@ struct Counters {       // device scratch, zeroed per phase
   unsigned long long stats[8];
 };
 
+// timed segments (tm_ctx_segment_ms); names in kSegNames
+enum Seg {
+  S_LABEL_A, S_LABEL_B, S_SEEDS, S_TRAV_START, S_TRAV_LEN, S_TRAV_SCAN, S_TRAV_WRITE,
+  S_CLASSIFY, S_REPAIR_TIPS, S_REPAIR_PINCH, S_STITCH, S_NUM
+};
+const char* kSegNames[S_NUM] = {"label_a_tri_pass", "label_b_edges", "select_seeds", "trav_start", "trav_len",
+                                "trav_scan", "trav_write", "repair_classify", "repair_tips", "repair_pinch",
+                                "repair_stitch"};
+
+struct Prof {
+  bool on = false;
+  std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> pending;
+  std::vector<cudaEvent_t> free_ev;
+  double ms[S_NUM] = {0};
+  long long cnt[S_NUM] = {0};
+};
+
+std::atomic<long long> g_launches{0};
+
 }  // namespace
 
+namespace tmb {
+void note_launch(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+}  // namespace tmb
+
 struct tm_ctx {
+  Prof prof;
   std::string err;
   int64_t defect_count[K_NUM] = {0};
   int64_t defect_first[K_NUM] = {0};
@@ -96,6 +122,51 @@ static int cuda_fail(tm_ctx* c, cudaError_t e, const char* where) {
     if (!ctx->buf.ensure(bytes)) return set_err(ctx, TM_ERR_CUDA, "cudaMalloc of %zu bytes for %s failed", \
                                                 (size_t)(bytes), #buf);           \
   } while (0)
+
+static cudaEvent_t prof_event(tm_ctx* ctx) {
+  if (!ctx->prof.free_ev.empty()) {
+    cudaEvent_t e = ctx->prof.free_ev.back();
+    ctx->prof.free_ev.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Segment timers: CUDA events recorded on the launching stream around the kernels.
+struct SegTimer {
+  tm_ctx* ctx;
+  int seg;
+  cudaStream_t s;
+  cudaEvent_t b = nullptr;
+  SegTimer(tm_ctx* c, int sg, cudaStream_t st) : ctx(c), seg(sg), s(st) {
+    if (ctx->prof.on) {
+      b = prof_event(ctx);
+      cudaEventRecord(b, s);
+    }
+  }
+  ~SegTimer() {
+    if (b) {
+      cudaEvent_t e = prof_event(ctx);
+      cudaEventRecord(e, s);
+      ctx->prof.pending.emplace_back(seg, b, e);
+    }
+  }
+};
+
+static void prof_flush(tm_ctx* ctx) {
+  for (auto& t : ctx->prof.pending) {
+    float ms = 0;
+    cudaEventSynchronize(std::get<2>(t));
+    cudaEventElapsedTime(&ms, std::get<1>(t), std::get<2>(t));
+    ctx->prof.ms[std::get<0>(t)] += ms;
+    ctx->prof.cnt[std::get<0>(t)] += 1;
+    ctx->prof.free_ev.push_back(std::get<1>(t));
+    ctx->prof.free_ev.push_back(std::get<2>(t));
+  }
+  ctx->prof.pending.clear();
+}
 
 static Counters* dev_counters(tm_ctx* ctx) { return ctx->counters.as<Counters>(); }
 
@@ -208,6 +279,8 @@ void tm_ctx_destroy(tm_ctx* ctx) {
   if (ctx->pinned_counters.p) cudaFreeHost(ctx->pinned_counters.p);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  prof_flush(ctx);
+  for (auto e : ctx->prof.free_ev) cudaEventDestroy(e);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }
@@ -222,6 +295,28 @@ int tm_ctx_defects(const tm_ctx* ctx, int64_t* counts, int64_t* first) {
   }
   return TM_OK;
 }
+
+int tm_ctx_set_profiling(tm_ctx* ctx, int on) {
+  if (!ctx) return TM_ERR_ARGUMENT;
+  ctx->prof.on = on != 0;
+  return TM_OK;
+}
+
+int tm_ctx_segment_ms(tm_ctx* ctx, double* ms, int64_t* counts, int n, int reset) {
+  if (!ctx) return TM_ERR_ARGUMENT;
+  prof_flush(ctx);
+  for (int k = 0; k < n && k < S_NUM; k++) {
+    if (ms) ms[k] = ctx->prof.ms[k];
+    if (counts) counts[k] = ctx->prof.cnt[k];
+  }
+  if (reset)
+    for (int k = 0; k < S_NUM; k++) ctx->prof.ms[k] = 0, ctx->prof.cnt[k] = 0;
+  return S_NUM;
+}
+
+const char* tm_segment_name(int k) { return (k >= 0 && k < S_NUM) ? kSegNames[k] : ""; }
+
+int64_t tm_launch_count(void) { return g_launches.load(); }
 
 int tm_ctx_phase_ms(const tm_ctx* ctx, double* ms3) {
   if (!ctx || !ms3) return TM_ERR_ARGUMENT;
@@ -242,8 +337,15 @@ int tm_label(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_tri, int 
   if (rc) return rc;
   uint64_t cap = hash_capacity(T);
   ENSURE(slots, cap * sizeof(uint32_t));
-  launch_label(d_xy, n, d_tri, tri_bits == 64, T, check, d_tri32, d_hw, d_max_edge, d_seed, d_tv,
-               ctx->slots.as<uint32_t>(), cap, &dev_counters(ctx)->st, s);
+  {
+    SegTimer st_(ctx, S_LABEL_A, s);
+    launch_label_a(d_xy, n, d_tri, tri_bits == 64, T, check, d_tri32, d_hw, d_max_edge, d_tv,
+                   ctx->slots.as<uint32_t>(), cap, &dev_counters(ctx)->st, s);
+  }
+  {
+    SegTimer st_(ctx, S_LABEL_B, s);
+    launch_label_b(n, T, d_hw, d_max_edge, d_seed, d_tv, s);
+  }
   CK(cudaGetLastError());
   Counters h;
   if ((rc = read_counters(ctx, s, &h))) return rc;
@@ -300,7 +402,10 @@ int tm_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* d_hw, const 
   Counters h;
   int64_t P = 0;
   if (T > 0) {
-    launch_select_seeds(d_seed, T, ctx->seeds.as<int32_t>(), &dc->n_seeds, ctx->temp.p, ctx->temp.bytes, s);
+    {
+      SegTimer st_(ctx, S_SEEDS, s);
+      launch_select_seeds(d_seed, T, ctx->seeds.as<int32_t>(), &dc->n_seeds, ctx->temp.p, ctx->temp.bytes, s);
+    }
     CK(cudaGetLastError());
     if ((rc = read_counters(ctx, s, &h))) return rc;
     P = h.n_seeds;
@@ -318,11 +423,21 @@ int tm_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* d_hw, const 
   ENSURE(queue, Tn * sizeof(int32_t));
   ENSURE(stamp, Tn * sizeof(int32_t));
   CK(cudaMemsetAsync(ctx->stamp.p, 0xFF, Tn * sizeof(int32_t), s));
-  launch_trav_start(d_hw, ctx->seeds.as<int32_t>(), P, ctx->start.as<int32_t>(), ctx->overflow.as<int32_t>(),
-                    &dc->n_overflow, ctx->queue.as<int32_t>(), ctx->stamp.as<int32_t>(), &dc->st, s);
+  {
+    SegTimer st_(ctx, S_TRAV_START, s);
+    launch_trav_start(d_hw, ctx->seeds.as<int32_t>(), P, ctx->start.as<int32_t>(), ctx->overflow.as<int32_t>(),
+                      &dc->n_overflow, ctx->queue.as<int32_t>(), ctx->stamp.as<int32_t>(), &dc->st, s);
+  }
   CK(cudaMemsetAsync(ctx->len.as<int64_t>() + P, 0, sizeof(int64_t), s));
-  launch_trav_len(d_hw, ctx->seeds.as<int32_t>(), ctx->start.as<int32_t>(), P, T, ctx->len.as<int64_t>(), &dc->st, s);
-  launch_scan(ctx->len.as<int64_t>(), d_offsets, P + 1, ctx->temp.p, ctx->temp.bytes, s);
+  {
+    SegTimer st_(ctx, S_TRAV_LEN, s);
+    launch_trav_len(d_hw, ctx->seeds.as<int32_t>(), ctx->start.as<int32_t>(), P, T, ctx->len.as<int64_t>(), &dc->st,
+                    s);
+  }
+  {
+    SegTimer st_(ctx, S_TRAV_SCAN, s);
+    launch_scan(ctx->len.as<int64_t>(), d_offsets, P + 1, ctx->temp.p, ctx->temp.bytes, s);
+  }
   CK(cudaGetLastError());
   int64_t total = 0;
   CK(cudaMemcpyAsync(&dc->stats[0], d_offsets + P, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
@@ -331,7 +446,10 @@ int tm_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* d_hw, const 
   total = (int64_t)h.stats[0];
   if (total > cap_slots)
     return set_err(ctx, TM_ERR_STRUCTURAL, "[traversal] polygon storage capacity exceeded; labels are inconsistent");
-  launch_trav_write(d_tri32, d_hw, ctx->start.as<int32_t>(), P, T, d_offsets, d_verts, s);
+  {
+    SegTimer st_(ctx, S_TRAV_WRITE, s);
+    launch_trav_write(d_tri32, d_hw, ctx->start.as<int32_t>(), P, T, d_offsets, d_verts, s);
+  }
   CK(cudaGetLastError());
   *n_slots = total;
   return TM_OK;
@@ -364,8 +482,11 @@ int tm_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, const int32_t*
   ENSURE(item_list, Pn * sizeof(int64_t));
   ENSURE(item_n, Pn * sizeof(int32_t));
   ENSURE(item_slots, Pn * sizeof(int64_t));
-  launch_classify(d_off_in, d_v_in, P, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(), &dc->n_items,
-                  ctx->long_list.as<int32_t>(), &dc->n_long, dc->stats, s);
+  {
+    SegTimer st_(ctx, S_CLASSIFY, s);
+    launch_classify(d_off_in, d_v_in, P, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(), &dc->n_items,
+                    ctx->long_list.as<int32_t>(), &dc->n_long, dc->stats, s);
+  }
   CK(cudaGetLastError());
   int64_t in_slots = 0;
   CK(cudaMemcpyAsync(&dc->pool_top, d_off_in + P, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
@@ -387,7 +508,16 @@ int tm_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, const int32_t*
     RepairArgs a{d_tri32, d_hw, d_tv, T, ctx->pool.as<int32_t>(), pool_cap, &dc->pool_top, ctx->undo.as<int32_t>(),
                  &dc->undo_top, undo_cap, &dc->st, ctx->items.as<int32_t>(), &dc->n_items, d_off_in, d_v_in,
                  ctx->item_list.as<int64_t>(), ctx->item_n.as<int32_t>(), ctx->item_slots.as<int64_t>(), dc->stats};
-    if (n_items > 0) launch_repair_items(a, s);
+    if (n_items > 0) {
+      {
+        SegTimer st_(ctx, S_REPAIR_TIPS, s);
+        launch_repair_tips(a, s);
+      }
+      {
+        SegTimer st_(ctx, S_REPAIR_PINCH, s);
+        launch_repair_pinch(a, s);
+      }
+    }
     CK(cudaGetLastError());
     if ((rc = read_counters(ctx, s, &h))) return rc;
     if (h.st.count[K_POOL] && attempt < 6) {
@@ -415,6 +545,7 @@ int tm_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, const int32_t*
   ENSURE(sbase, (Pn + 1) * sizeof(int64_t));
   size_t tb = scan_temp_bytes(Pn + 1);
   ENSURE(temp, tb + 256);
+  SegTimer* stitch_timer = new SegTimer(ctx, S_STITCH, s);
   launch_out_counts(d_off_in, P, ctx->item_of.as<int32_t>(), ctx->item_n.as<int32_t>(),
                     ctx->item_slots.as<int64_t>(), ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), s);
   launch_scan(ctx->cnt.as<int64_t>(), ctx->pbase.as<int64_t>(), P + 1, ctx->temp.p, ctx->temp.bytes, s);
@@ -424,12 +555,15 @@ int tm_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, const int32_t*
   CK(cudaMemcpyAsync(&tot[0], ctx->pbase.as<int64_t>() + P, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(&tot[1], ctx->sbase.as<int64_t>() + P, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  if (tot[0] > cap_polys || tot[1] > cap_slots)
+  if (tot[0] > cap_polys || tot[1] > cap_slots) {
+    delete stitch_timer;
     return set_err(ctx, TM_ERR_CAPACITY, "[reparation] output capacity (%lld polygons, %lld slots) < (%lld, %lld)",
                    (long long)cap_polys, (long long)cap_slots, (long long)tot[0], (long long)tot[1]);
+  }
   launch_stitch(d_off_in, d_v_in, P, ctx->item_of.as<int32_t>(), ctx->item_list.as<int64_t>(),
                 ctx->item_n.as<int32_t>(), ctx->pool.as<int32_t>(), ctx->pbase.as<int64_t>(),
                 ctx->sbase.as<int64_t>(), d_off_out, d_v_out, s);
+  delete stitch_timer;
   CK(cudaGetLastError());
   *n_polys_out = tot[0];
   *n_slots_out = tot[1];

@@ -11,9 +11,13 @@ struct DevStatus;
 
 // tm_label.cu
 uint64_t hash_capacity(int64_t T);
-void launch_label(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int check, int32_t* tri32,
-                  int32_t* hw, int8_t* max_edge, uint8_t* seed, int32_t* tv, uint32_t* slots, uint64_t cap,
-                  DevStatus* st, cudaStream_t s);
+// counts kernels of this library launched (bench.py's gpu_launches)
+void note_launch(int k);
+void launch_label_a(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int check,
+                    int32_t* tri32, int32_t* hw, int8_t* max_edge, int32_t* tv, uint32_t* slots, uint64_t cap,
+                    DevStatus* st, cudaStream_t s);
+void launch_label_b(int64_t n, int64_t T, int32_t* hw, const int8_t* max_edge, uint8_t* seed, int32_t* tv,
+                    cudaStream_t s);
 void launch_relabel(const int8_t* max_edge, int64_t T, int32_t* hw, uint8_t* seed, cudaStream_t s);
 void launch_check_neighbors(const int32_t* hw, const void* nb, int nb_is64, int64_t T, DevStatus* st, cudaStream_t s);
 void launch_unpack(const int32_t* hw, int64_t T, int32_t* twin, uint8_t* fr, cudaStream_t s);
@@ -57,7 +61,8 @@ struct RepairArgs {
 void launch_classify(const int64_t* off, const int32_t* v, int64_t P, int32_t* item_of, int32_t* items,
                      unsigned int* n_items, int32_t* long_list, unsigned int* n_long, unsigned long long* stats,
                      cudaStream_t s);
-void launch_repair_items(const RepairArgs& a, cudaStream_t s);
+void launch_repair_tips(const RepairArgs& a, cudaStream_t s);
+void launch_repair_pinch(const RepairArgs& a, cudaStream_t s);
 void launch_out_counts(const int64_t* off, int64_t P, const int32_t* item_of, const int32_t* item_n,
                        const int64_t* item_slots, int64_t* cnt, int64_t* slots, cudaStream_t s);
 void launch_stitch(const int64_t* off, const int32_t* v, int64_t P, const int32_t* item_of, const int64_t* item_list,

@@ -202,9 +202,9 @@ uint64_t hash_capacity(int64_t T) {
   return c < 64 ? 64 : c;
 }
 
-void launch_label(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int check,
-                  int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed, int32_t* tv,
-                  uint32_t* slots, uint64_t cap, DevStatus* st, cudaStream_t s) {
+void launch_label_a(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int check,
+                    int32_t* tri32, int32_t* hw, int8_t* max_edge, int32_t* tv, uint32_t* slots, uint64_t cap,
+                    DevStatus* st, cudaStream_t s) {
   cudaMemsetAsync(slots, 0xFF, cap * sizeof(uint32_t), s);
   cudaMemsetAsync(hw, 0xFF, (size_t)(3 * T) * sizeof(int32_t), s);
   if (n > 0) {
@@ -220,13 +220,24 @@ void launch_label(const double* xy, int64_t n, const void* tri, int tri_is64, in
       k_tri_pass<int32_t><<<grid_for(T, B), B, 0, s>>>((const double2*)xy, n, (const int32_t*)tri, T,
                                                        tri32 == tri ? nullptr : tri32, max_edge, slots, cap, hw, tv,
                                                        check, st);
-    k_label_edges<<<grid_for(T, B), B, 0, s>>>(max_edge, T, hw, seed, 0);
+    note_launch(1);
   }
-  if (n > 0) k_trivertex_fix<<<grid_for(n, 256), 256, 0, s>>>(tv, n);
+}
+
+void launch_label_b(int64_t n, int64_t T, int32_t* hw, const int8_t* max_edge, uint8_t* seed, int32_t* tv,
+                    cudaStream_t s) {
+  if (T > 0) {
+    k_label_edges<<<grid_for(T, 256), 256, 0, s>>>(max_edge, T, hw, seed, 0);
+    note_launch(1);
+  }
+  if (n > 0) {
+    k_trivertex_fix<<<grid_for(n, 256), 256, 0, s>>>(tv, n);
+    note_launch(1);
+  }
 }
 
 void launch_relabel(const int8_t* max_edge, int64_t T, int32_t* hw, uint8_t* seed, cudaStream_t s) {
-  if (T > 0) k_label_edges<<<grid_for(T, 256), 256, 0, s>>>(max_edge, T, hw, seed, 1);
+  if (T > 0) k_label_edges<<<grid_for(T, 256), 256, 0, s>>>(max_edge, T, hw, seed, 1), note_launch(1);
 }
 
 void launch_check_neighbors(const int32_t* hw, const void* nb, int nb_is64, int64_t T, DevStatus* st, cudaStream_t s) {

@@ -629,19 +629,27 @@ void launch_classify(const int64_t* off, const int32_t* v, int64_t P, int32_t* i
                      cudaStream_t s) {
   if (P <= 0) return;
   k_classify<<<grid_for(P, 256), 256, 0, s>>>(off, v, P, item_of, items, n_items, long_list, n_long, stats);
+  note_launch(1);
   k_classify_long<<<kNumSMs * 2, 256, 0, s>>>(off, v, long_list, n_long, item_of, items, n_items, stats);
+  note_launch(1);
 }
 
-void launch_repair_items(const RepairArgs& a, cudaStream_t s) {
+void launch_repair_tips(const RepairArgs& a, cudaStream_t s) {
   RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st};
-  int g = kNumSMs * 4;
-  k_repair_tips<<<g, 128, 0, s>>>(c, a.items, a.n_items, a.off, a.v, a.item_list, a.item_n, a.stats);
-  k_repair_pinch<<<g, 128, 0, s>>>(c, a.items, a.n_items, a.item_list, a.item_n, a.item_slots, a.stats);
+  k_repair_tips<<<kNumSMs * 4, 128, 0, s>>>(c, a.items, a.n_items, a.off, a.v, a.item_list, a.item_n, a.stats);
+  note_launch(1);
+}
+
+void launch_repair_pinch(const RepairArgs& a, cudaStream_t s) {
+  RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st};
+  k_repair_pinch<<<kNumSMs * 4, 128, 0, s>>>(c, a.items, a.n_items, a.item_list, a.item_n, a.item_slots, a.stats);
+  note_launch(1);
 }
 
 void launch_out_counts(const int64_t* off, int64_t P, const int32_t* item_of, const int32_t* item_n,
                        const int64_t* item_slots, int64_t* cnt, int64_t* slots, cudaStream_t s) {
   k_out_counts<<<grid_for(P + 1, 256), 256, 0, s>>>(off, P, item_of, item_n, item_slots, cnt, slots);
+  note_launch(1);
 }
 
 void launch_stitch(const int64_t* off, const int32_t* v, int64_t P, const int32_t* item_of, const int64_t* item_list,
@@ -649,11 +657,13 @@ void launch_stitch(const int64_t* off, const int32_t* v, int64_t P, const int32_
                    int64_t* off_out, int32_t* v_out, cudaStream_t s) {
   if (P <= 0) return;
   k_stitch<<<grid_for(P, 256), 256, 0, s>>>(off, v, P, item_of, item_list, item_n, pool, pbase, sbase, off_out, v_out);
+  note_launch(1);
 }
 
 void launch_undo(int32_t* hw, const int32_t* undo, const unsigned long long* undo_top, unsigned long long cap,
                  cudaStream_t s) {
   k_undo<<<kNumSMs, 256, 0, s>>>(hw, undo, undo_top, cap);
+  note_launch(1);
 }
 
 }  // namespace tmb

@@ -151,19 +151,23 @@ void launch_trav_start(const int32_t* hw, const int32_t* seeds, int64_t P, int32
                        unsigned int* n_overflow, int32_t* queue, int32_t* stamp, DevStatus* st, cudaStream_t s) {
   if (P <= 0) return;
   k_trav_start<<<grid_for(P, 256), 256, 0, s>>>(hw, seeds, P, start, overflow, n_overflow, st);
+  note_launch(1);
   k_bfs_slow<<<1, 32, 0, s>>>(hw, seeds, start, overflow, n_overflow, queue, stamp, st);
+  note_launch(1);
 }
 
 void launch_trav_len(const int32_t* hw, const int32_t* seeds, const int32_t* start, int64_t P, int64_t T,
                      int64_t* len, DevStatus* st, cudaStream_t s) {
   if (P <= 0) return;
   k_trav_len<<<grid_for(P, 256), 256, 0, s>>>(hw, seeds, start, P, 3 * T + 3, len, st);
+  note_launch(1);
 }
 
 void launch_trav_write(const int32_t* tri, const int32_t* hw, const int32_t* start, int64_t P, int64_t T,
                        const int64_t* offsets, int32_t* verts, cudaStream_t s) {
   if (P <= 0) return;
   k_trav_write<<<grid_for(P, 256), 256, 0, s>>>(tri, hw, start, P, 3 * T + 3, offsets, verts);
+  note_launch(1);
 }
 
 }  // namespace tmb
