@@ -252,21 +252,136 @@ __device__ int rewalk_split(const RepairCtx& c, int32_t e, int32_t te, int64_t p
   return 1;
 }
 
-// Tip split of piece X (len L) at its first tip (reparation.py:294-312 splitter).
-__device__ bool split_tip(const RepairCtx& c, const int32_t* X, int64_t L, int32_t poly,
-                          int64_t* pa_off, int64_t* pa_len, int64_t* pb_off, int64_t* pb_len) {
-  int64_t pos = first_tip(X, L);
-  if (pos < 0) { report(c.st, K_STRUCT, poly); return false; }
+// ------------------------------------------------------------ warp helpers
+// One warp cooperates on one work item.  Lanes split O(len) scans and copies;
+// the inherently sequential mesh rotations (fan walk, wedge rotation) run on
+// lane 0 and are broadcast.  All control flow below is warp-uniform.
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kFanCap = 64;
+constexpr int kTipWarps = 4;  // warps per block of k_repair_tips
+
+__device__ __forceinline__ int wrap_idx(int x, int n) { return x >= n ? x - n : (x < 0 ? x + n : x); }
+
+// first position p (cyclic triple s[p-1] == s[p+1]) or -1 (reparation.py:59-71)
+__device__ int warp_first_tip(const int32_t* s, int n, int lane) {
+  for (int base = 0; base < n; base += 32) {
+    int p = base + lane;
+    bool t = false;
+    if (p < n) t = s[p == 0 ? n - 1 : p - 1] == s[p + 1 == n ? 0 : p + 1];
+    unsigned m = __ballot_sync(kFull, t);
+    if (m) return base + __ffs(m) - 1;
+  }
+  return -1;
+}
+
+// (len - distinct) of s[0..n) (traversal.py:140-147), quadratic over lanes
+__device__ int warp_extra_visits(const int32_t* s, int n, int lane) {
+  int extra = 0;
+  for (int pb = 0; pb < n; pb += 32) {
+    int p = pb + lane;
+    int32_t x = p < n ? s[p] : INT32_MIN;
+    bool dup = false;
+    for (int qb = 0; qb <= pb; qb += 32) {
+      int32_t y = qb + lane < n ? s[qb + lane] : INT32_MIN + 1;
+      int qmax = min(32, n - qb);
+      for (int k = 0; k < qmax; k++) {
+        int32_t yk = __shfl_sync(kFull, y, k);
+        dup |= (qb + k < p) && (yk == x);
+      }
+    }
+    extra += __popc(__ballot_sync(kFull, dup && p < n));
+  }
+  return extra;
+}
+
+// reparation.py:127-145 with the fan held in shared memory (deg <= kFanCap);
+// larger fans fall back to the sequential enumeration on lane 0.
+__device__ int32_t warp_middle_internal_edge(const RepairCtx& c, int32_t v, int32_t barrier, int32_t poly,
+                                             int32_t* fan, int lane) {
+  int deg = 0, status = 0;
+  if (lane == 0) {
+    int32_t t0 = c.tv[v];
+    int32_t g0 = t0 < 0 ? -1 : he_with_origin(c.tri, t0, v);
+    if (g0 < 0) {
+      status = 1;
+    } else {
+      int guard = (int)(3 * c.T + 3 < (1LL << 30) ? 3 * c.T + 3 : (1LL << 30));
+      int32_t g = g0;
+      do {
+        if (deg < kFanCap) fan[deg] = g;
+        deg++;
+        g = fan_step(c.hw, g, guard);
+        if (g < 0 || deg > guard) { status = 1; break; }
+      } while (g != g0);
+    }
+  }
+  deg = __shfl_sync(kFull, deg, 0);
+  status = __shfl_sync(kFull, status, 0);
+  __syncwarp();
+  if (status) {
+    if (lane == 0) report(c.st, K_STRUCT, poly);
+    return -1;
+  }
+  if (deg > kFanCap) {
+    int32_t e = -1;
+    if (lane == 0) e = middle_internal_edge(c, v, barrier, poly);
+    return __shfl_sync(kFull, e, 0);
+  }
+  unsigned long long imask = 0, bmask = 0;
+  for (int base = 0; base < deg; base += 32) {
+    int idx = base + lane;
+    bool fr = false, in_fan = idx < deg;
+    int32_t tg = -1;
+    if (in_fan) {
+      int32_t g = fan[idx];
+      fr = hw_front(c.hw[g]);
+      tg = he_target(c.tri, g);
+    }
+    unsigned bi = __ballot_sync(kFull, in_fan && fr && tg == barrier);
+    unsigned ii = __ballot_sync(kFull, in_fan && !fr);
+    bmask |= (unsigned long long)bi << base;
+    imask |= (unsigned long long)ii << base;
+  }
+  if (bmask == 0) {
+    if (lane == 0) report(c.st, K_BARRIER, poly);
+    return -1;
+  }
+  if (imask == 0) {
+    if (lane == 0) report(c.st, K_NO_INTERNAL, poly);
+    return -1;
+  }
+  int at = __ffsll((long long)bmask) - 1;
+  int k = __popcll(imask), want = (k - 1) / 2;
+  // rotated order fan[at:] + fan[:at]
+  unsigned long long hi = imask & (~0ull << at), lo = imask & ((1ull << at) - 1);
+  unsigned long long m = hi;
+  int cnt_hi = __popcll(hi);
+  if (want >= cnt_hi) { m = lo; want -= cnt_hi; }
+  for (int r = 0; r < want; r++) m &= m - 1;
+  return fan[__ffsll((long long)m) - 1];
+}
+
+// Tip split of piece X (len L) at its first tip, warp-cooperative arc copy
+// with the re-walk as fallback.
+__device__ bool warp_split_tip(const RepairCtx& c, const int32_t* X, int L, int32_t poly, int32_t* fan, int lane,
+                               int64_t* pa_off, int64_t* pa_len, int64_t* pb_off, int64_t* pb_len) {
+  int pos = warp_first_tip(X, L, lane);
+  if (pos < 0) {
+    if (lane == 0) report(c.st, K_STRUCT, poly);
+    return false;
+  }
   int32_t v = X[pos], b = X[pos == 0 ? L - 1 : pos - 1];
-  int32_t e = middle_internal_edge(c, v, b, poly);
+  int32_t e = warp_middle_internal_edge(c, v, b, poly, fan, lane);
   if (e < 0) return false;
   int32_t te = hw_twin(c.hw[e]);
-  if (te < 0) { report(c.st, K_STRUCT, poly); return false; }
+  if (te < 0) {
+    if (lane == 0) report(c.st, K_STRUCT, poly);
+    return false;
+  }
   int32_t u = he_target(c.tri, e);
-  // incoming boundary vertex of the visit of u whose wedge holds twin(e):
-  // rotate CCW from twin(e) until the crossed edge prev(c) is frontier.
+  // incoming boundary vertex of the visit of u whose wedge holds twin(e)
   int32_t a_in = -1;
-  {
+  if (lane == 0) {
     int32_t g = te;
     long long guard = 3 * c.T + 3;
     for (long long s = 0; s < guard; s++) {
@@ -276,130 +391,206 @@ __device__ bool split_tip(const RepairCtx& c, const int32_t* X, int64_t L, int32
       g = hw_twin(w);
     }
   }
-  int64_t j = -1;
-  if (a_in >= 0)
-    for (int64_t q = 0; q < L; q++)
-      if (X[q] == u && X[q == 0 ? L - 1 : q - 1] == a_in) { j = q; break; }
-  promote(c, e, te);
-  if (j >= 0) {
-    int64_t la = 1 + (pos - j + L) % L, lb = (j - pos + L) % L + 1;
-    // pa arc: A(0)=v, A(k)=X[(j+k-1)%L]; pb arc: B(k)=X[(pos+k)%L] (k<lb-1), B(lb-1)=u
-    int32_t ha = min_frontier_slot(c.hw, e / 3), hb = min_frontier_slot(c.hw, te / 3);
-    int32_t oa = he_origin(c.tri, ha), ga = he_target(c.tri, ha);
-    int32_t ob = he_origin(c.tri, hb), gb = he_target(c.tri, hb);
-    int64_t ka = -1, kb = -1;
-    for (int64_t k = 0; k < la && ka < 0; k++) {
-      int64_t k1 = k + 1 == la ? 0 : k + 1;
-      int32_t x0 = k == 0 ? v : X[(j + k - 1) % L];
-      int32_t x1 = k1 == 0 ? v : X[(j + k1 - 1) % L];
-      if (x0 == oa && x1 == ga) ka = k;
+  a_in = __shfl_sync(kFull, a_in, 0);
+  int j = -1;
+  if (a_in >= 0) {
+    for (int base = 0; base < L && j < 0; base += 32) {
+      int q = base + lane;
+      bool hit = q < L && X[q] == u && X[q == 0 ? L - 1 : q - 1] == a_in;
+      unsigned m = __ballot_sync(kFull, hit);
+      if (m) j = base + __ffs(m) - 1;
     }
-    for (int64_t k = 0; k < lb && kb < 0; k++) {
-      int64_t k1 = k + 1 == lb ? 0 : k + 1;
-      int32_t x0 = k == lb - 1 ? u : X[(pos + k) % L];
-      int32_t x1 = k1 == lb - 1 ? u : X[(pos + k1) % L];
-      if (x0 == ob && x1 == gb) kb = k;
+  }
+  int32_t oa = 0, ga = 0, ob = 0, gb = 0;
+  if (lane == 0) {
+    promote(c, e, te);
+    int32_t ha = min_frontier_slot(c.hw, e / 3), hb = min_frontier_slot(c.hw, te / 3);
+    oa = he_origin(c.tri, ha); ga = he_target(c.tri, ha);
+    ob = he_origin(c.tri, hb); gb = he_target(c.tri, hb);
+  }
+  __syncwarp();
+  oa = __shfl_sync(kFull, oa, 0); ga = __shfl_sync(kFull, ga, 0);
+  ob = __shfl_sync(kFull, ob, 0); gb = __shfl_sync(kFull, gb, 0);
+  if (j >= 0) {
+    int la = 1 + wrap_idx(pos - j, L), lb = wrap_idx(j - pos, L) + 1;
+    // pa arc: A(0) = v, A(k) = X[(j+k-1) % L]; pb arc: B(k) = X[(pos+k) % L] (k < lb-1), B(lb-1) = u
+    int ka = -1, kb = -1;
+    for (int base = 0; base < la && ka < 0; base += 32) {
+      int k = base + lane;
+      bool hit = false;
+      if (k < la) {
+        int k1 = k + 1 == la ? 0 : k + 1;
+        int32_t x0 = k == 0 ? v : X[wrap_idx(j + k - 1, L)];
+        int32_t x1 = k1 == 0 ? v : X[wrap_idx(j + k1 - 1, L)];
+        hit = x0 == oa && x1 == ga;
+      }
+      unsigned m = __ballot_sync(kFull, hit);
+      if (m) ka = base + __ffs(m) - 1;
+    }
+    for (int base = 0; base < lb && kb < 0; base += 32) {
+      int k = base + lane;
+      bool hit = false;
+      if (k < lb) {
+        int k1 = k + 1 == lb ? 0 : k + 1;
+        int32_t x0 = k == lb - 1 ? u : X[wrap_idx(pos + k, L)];
+        int32_t x1 = k1 == lb - 1 ? u : X[wrap_idx(pos + k1, L)];
+        hit = x0 == ob && x1 == gb;
+      }
+      unsigned m = __ballot_sync(kFull, hit);
+      if (m) kb = base + __ffs(m) - 1;
     }
     if (ka >= 0 && kb >= 0) {
-      int64_t o = palloc(c, la + lb);
-      if (o < 0) { report(c.st, K_POOL, poly); return false; }
+      long long o = 0;
+      if (lane == 0) o = palloc(c, la + lb);
+      o = __shfl_sync(kFull, o, 0);
+      if (o < 0) {
+        if (lane == 0) report(c.st, K_POOL, poly);
+        return false;
+      }
       int32_t* A = c.pool + o;
       int32_t* B = A + la;
-      for (int64_t k = 0; k < la; k++) {
-        int64_t kk = (ka + k) % la;
-        A[k] = kk == 0 ? v : X[(j + kk - 1) % L];
+      for (int k = lane; k < la; k += 32) {
+        int kk = wrap_idx(ka + k, la);
+        A[k] = kk == 0 ? v : X[wrap_idx(j + kk - 1, L)];
       }
-      for (int64_t k = 0; k < lb; k++) {
-        int64_t kk = (kb + k) % lb;
-        B[k] = kk == lb - 1 ? u : X[(pos + kk) % L];
+      for (int k = lane; k < lb; k += 32) {
+        int kk = wrap_idx(kb + k, lb);
+        B[k] = kk == lb - 1 ? u : X[wrap_idx(pos + kk, L)];
       }
+      __syncwarp();
       *pa_off = o; *pa_len = la; *pb_off = o + la; *pb_len = lb;
       return true;
     }
   }
-  int r = rewalk_split(c, e, te, L, poly, pa_off, pa_len, pb_off, pb_len);
-  if (r == 0) report(c.st, K_SPLIT_LAW, poly);
+  int r = 0;
+  long long ao = 0, al = 0, bo = 0, bl = 0;
+  if (lane == 0) {
+    int64_t a1, a2, a3, a4;
+    r = rewalk_split(c, e, te, L, poly, &a1, &a2, &a3, &a4);
+    if (r == 0) report(c.st, K_SPLIT_LAW, poly);
+    ao = a1; al = a2; bo = a3; bl = a4;
+  }
+  __syncwarp();
+  r = __shfl_sync(kFull, r, 0);
+  ao = __shfl_sync(kFull, ao, 0); al = __shfl_sync(kFull, al, 0);
+  bo = __shfl_sync(kFull, bo, 0); bl = __shfl_sync(kFull, bl, 0);
+  *pa_off = ao; *pa_len = al; *pb_off = bo; *pb_len = bl;
   return r == 1;
 }
 
-__device__ __forceinline__ uint32_t tip_flag(const int32_t* s, int64_t n) { return poly_has_tip(s, n) ? F_TIP : 0u; }
+__device__ __forceinline__ uint32_t warp_tip_flag(const int32_t* s, int n, int lane) {
+  return warp_first_tip(s, n, lane) >= 0 ? F_TIP : 0u;
+}
 
 // ------------------------------------------------------------ tip phase
-// item_list[w] = pool offset of the item's record list, item_n[w] = #records.
-__global__ void __launch_bounds__(128) k_repair_tips(RepairCtx c, const int32_t* __restrict__ items,
-                                                     const unsigned int* n_items, const int64_t* __restrict__ off,
-                                                     const int32_t* __restrict__ v,
-                                                     int64_t* __restrict__ item_list, int32_t* __restrict__ item_n,
-                                                     unsigned long long* stats) {
+// One warp per work item.  item_list[w] = pool offset of the item's record
+// list, item_n[w] = #records (leaves in the reference's raw order).
+__global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, const int32_t* __restrict__ items,
+                                                                const unsigned int* n_items,
+                                                                const int64_t* __restrict__ off,
+                                                                const int32_t* __restrict__ v,
+                                                                int64_t* __restrict__ item_list,
+                                                                int32_t* __restrict__ item_n,
+                                                                unsigned long long* stats) {
+  __shared__ int32_t s_fan[kTipWarps][kFanCap];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int32_t* fan = s_fan[wib];
   unsigned int ni = *n_items;
   // reparation.py:354-364: at most initial + 1 rounds, initial = extra visits of mesh0
   long long max_rounds = (long long)stats[2] + 1;
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < ni; w += (int64_t)gridDim.x * blockDim.x) {
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = warp; w < ni; w += nwarps) {
     int32_t i = items[w];
-    int64_t b = off[i], L = off[i + 1] - b;
-    item_list[w] = -1;
-    item_n[w] = 0;
-    int64_t base = palloc(c, L + 2);
-    if (base < 0) { report(c.st, K_POOL, i); continue; }
+    int64_t b = off[i];
+    int L = (int)(off[i + 1] - b);
+    long long base = 0;
+    if (lane == 0) base = palloc(c, L + 2);
+    base = __shfl_sync(kFull, base, 0);
+    if (base < 0) {
+      if (lane == 0) { report(c.st, K_POOL, i); item_list[w] = -1; item_n[w] = 0; }
+      continue;
+    }
     int32_t* P0 = c.pool + base;
-    for (int64_t k = 0; k < L; k++) P0[k] = v[b + k];
-    int64_t list = base + L;
-    c.pool[list] = (int32_t)base;
-    uint32_t f0 = tip_flag(P0, L);
-    c.pool[list + 1] = (int32_t)((uint32_t)L | f0);
+    for (int k = lane; k < L; k += 32) P0[k] = v[b + k];
+    __syncwarp();
+    long long list = base + L;
+    uint32_t f0 = warp_tip_flag(P0, L, lane);
+    if (lane == 0) {
+      c.pool[list] = (int32_t)base;
+      c.pool[list + 1] = (int32_t)((uint32_t)L | f0);
+    }
+    __syncwarp();
     int n = 1, ntips = f0 ? 1 : 0;
     long long depth = 0, splits = 0;
     bool bad = false;
     while (ntips > 0 && !bad) {
       depth++;
-      if (depth > max_rounds) { report(c.st, K_NO_CONVERGE, i); bad = true; break; }
-      int64_t nl = palloc(c, 2 * (int64_t)(n + ntips));
-      if (nl < 0) { report(c.st, K_POOL, i); bad = true; break; }
+      if (depth > max_rounds) {
+        if (lane == 0) report(c.st, K_NO_CONVERGE, i);
+        bad = true;
+        break;
+      }
+      long long nl = 0;
+      if (lane == 0) nl = palloc(c, 2 * (int64_t)(n + ntips));
+      nl = __shfl_sync(kFull, nl, 0);
+      if (nl < 0) {
+        if (lane == 0) report(c.st, K_POOL, i);
+        bad = true;
+        break;
+      }
       int m = 0, nt = 0;
       for (int r = 0; r < n; r++) {
         uint32_t ro = (uint32_t)c.pool[list + 2 * r], rl = (uint32_t)c.pool[list + 2 * r + 1];
         if (!(rl & F_TIP)) {
-          c.pool[nl + 2 * m] = (int32_t)ro;
-          c.pool[nl + 2 * m + 1] = (int32_t)rl;
+          if (lane == 0) {
+            c.pool[nl + 2 * m] = (int32_t)ro;
+            c.pool[nl + 2 * m + 1] = (int32_t)rl;
+          }
           m++;
           continue;
         }
         int64_t ao, al, bo, bl;
-        if (!split_tip(c, c.pool + ro, rl & LEN_MASK, i, &ao, &al, &bo, &bl)) { bad = true; break; }
-        uint32_t fa = tip_flag(c.pool + ao, al), fb = tip_flag(c.pool + bo, bl);
-        c.pool[nl + 2 * m] = (int32_t)ao;
-        c.pool[nl + 2 * m + 1] = (int32_t)((uint32_t)al | fa);
-        c.pool[nl + 2 * m + 2] = (int32_t)bo;
-        c.pool[nl + 2 * m + 3] = (int32_t)((uint32_t)bl | fb);
+        if (!warp_split_tip(c, c.pool + ro, (int)(rl & LEN_MASK), i, fan, lane, &ao, &al, &bo, &bl)) {
+          bad = true;
+          break;
+        }
+        uint32_t fa = warp_tip_flag(c.pool + ao, (int)al, lane), fb = warp_tip_flag(c.pool + bo, (int)bl, lane);
+        if (lane == 0) {
+          c.pool[nl + 2 * m] = (int32_t)ao;
+          c.pool[nl + 2 * m + 1] = (int32_t)((uint32_t)al | fa);
+          c.pool[nl + 2 * m + 2] = (int32_t)bo;
+          c.pool[nl + 2 * m + 3] = (int32_t)((uint32_t)bl | fb);
+        }
         m += 2;
         nt += (fa ? 1 : 0) + (fb ? 1 : 0);
         splits++;
       }
+      __syncwarp();
       list = nl;
       n = m;
       ntips = nt;
     }
-    if (bad) continue;
-    item_list[w] = list;
-    item_n[w] = n;
-    if (depth > 0) atomicMax(stats + 0, (unsigned long long)depth);
-    if (splits) atomicAdd(stats + 1, (unsigned long long)splits);
+    if (bad) {
+      if (lane == 0) { item_list[w] = -1; item_n[w] = 0; }
+      continue;
+    }
     // repeated flags and extra visits of the leaves (pinch guard, reparation.py:322)
     unsigned long long ex_sum = 0;
     for (int r = 0; r < n; r++) {
       uint32_t ro = (uint32_t)c.pool[list + 2 * r], rl = (uint32_t)c.pool[list + 2 * r + 1];
-      int64_t ln = rl & LEN_MASK;
-      int32_t* scratch = nullptr;
-      if (ln > 48) {
-        int64_t so = palloc(c, ln);
-        if (so < 0) { report(c.st, K_POOL, i); break; }
-        scratch = c.pool + so;
-      }
-      int64_t ex = extra_visits(c.pool + ro, ln, scratch);
-      if (ex > 0) c.pool[list + 2 * r + 1] = (int32_t)(rl | F_REP);
+      int ex = warp_extra_visits(c.pool + ro, (int)(rl & LEN_MASK), lane);
+      if (ex > 0 && lane == 0) c.pool[list + 2 * r + 1] = (int32_t)(rl | F_REP);
       ex_sum += ex;
     }
-    if (ex_sum) atomicAdd(stats + 5, ex_sum);
+    __syncwarp();
+    if (lane == 0) {
+      item_list[w] = list;
+      item_n[w] = n;
+      if (depth > 0) atomicMax(stats + 0, (unsigned long long)depth);
+      if (splits) atomicAdd(stats + 1, (unsigned long long)splits);
+      if (ex_sum) atomicAdd(stats + 5, ex_sum);
+    }
   }
 }
 
@@ -484,7 +675,7 @@ __device__ int pinch_split(const RepairCtx& c, const int32_t* X, int64_t L, int3
 }
 
 __device__ uint32_t piece_flags(const RepairCtx& c, const int32_t* s, int64_t n, int32_t poly, bool* ok) {
-  uint32_t f = tip_flag(s, n);
+  uint32_t f = poly_has_tip(s, n) ? F_TIP : 0u;
   int32_t* scratch = nullptr;
   if (n > 48) {
     int64_t so = palloc(c, n);
@@ -636,7 +827,7 @@ void launch_classify(const int64_t* off, const int32_t* v, int64_t P, int32_t* i
 
 void launch_repair_tips(const RepairArgs& a, cudaStream_t s) {
   RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st};
-  k_repair_tips<<<kNumSMs * 4, 128, 0, s>>>(c, a.items, a.n_items, a.off, a.v, a.item_list, a.item_n, a.stats);
+  k_repair_tips<<<kNumSMs * 8, 32 * kTipWarps, 0, s>>>(c, a.items, a.n_items, a.off, a.v, a.item_list, a.item_n, a.stats);
   note_launch(1);
 }
 
