@@ -53,10 +53,11 @@ struct Counters {       // device scratch, zeroed per phase
 
 // timed segments (tm_ctx_segment_ms); names in kSegNames
 enum Seg {
-  S_LABEL_A, S_LABEL_B, S_SEEDS, S_TRAV_START, S_TRAV_LEN, S_TRAV_SCAN, S_TRAV_WRITE,
+  S_LABEL_A, S_LABEL_B, S_SEEDS, S_TRAV_START, S_TRAV_RULERS, S_TRAV_LEN, S_TRAV_SCAN, S_TRAV_WRITE,
   S_CLASSIFY, S_REPAIR_TIPS, S_REPAIR_PINCH, S_STITCH, S_NUM
 };
-const char* kSegNames[S_NUM] = {"label_a_tri_pass", "label_b_edges", "select_seeds", "trav_start", "trav_len",
+const char* kSegNames[S_NUM] = {"label_a_tri_pass", "label_b_edges", "select_seeds", "trav_start", "trav_rulers",
+                                "trav_chain",
                                 "trav_scan", "trav_write", "repair_classify", "repair_tips", "repair_pinch",
                                 "repair_stitch"};
 
@@ -86,7 +87,7 @@ struct tm_ctx {
   // label
   Buf slots;
   // traversal
-  Buf seeds, start, len, overflow, queue, stamp, temp;
+  Buf seeds, start, len, overflow, queue, stamp, temp, nrul, eoff, rnext, rdist, startbits, ent_r, ent_base;
   // repair
   Buf item_of, items, long_list, item_list, item_n, item_slots, cnt, slotsz, pbase, sbase, pool, undo;
   // whole-path buffers
@@ -271,7 +272,8 @@ int tm_ctx_create(tm_ctx** out) {
 void tm_ctx_destroy(tm_ctx* ctx) {
   if (!ctx) return;
   Buf* bufs[] = {&ctx->counters, &ctx->slots, &ctx->seeds, &ctx->start, &ctx->len, &ctx->overflow, &ctx->queue,
-                 &ctx->stamp, &ctx->temp, &ctx->item_of, &ctx->items, &ctx->long_list, &ctx->item_list,
+                 &ctx->stamp, &ctx->temp, &ctx->nrul, &ctx->eoff, &ctx->rnext, &ctx->rdist, &ctx->startbits,
+                 &ctx->ent_r, &ctx->ent_base, &ctx->item_of, &ctx->items, &ctx->long_list, &ctx->item_list,
                  &ctx->item_n, &ctx->item_slots, &ctx->cnt, &ctx->slotsz, &ctx->pbase, &ctx->sbase, &ctx->pool,
                  &ctx->undo, &ctx->xy, &ctx->tri, &ctx->tri32, &ctx->hw, &ctx->max_edge, &ctx->seed, &ctx->tv,
                  &ctx->off0, &ctx->v0, &ctx->fin_off, &ctx->fin_v};
@@ -419,36 +421,59 @@ int tm_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* d_hw, const 
   }
   ENSURE(start, P * sizeof(int32_t));
   ENSURE(len, (P + 1) * sizeof(int64_t));
+  ENSURE(nrul, (P + 1) * sizeof(int64_t));
+  ENSURE(eoff, (P + 1) * sizeof(int64_t));
   ENSURE(overflow, P * sizeof(int32_t));
   ENSURE(queue, Tn * sizeof(int32_t));
   ENSURE(stamp, Tn * sizeof(int32_t));
+  ENSURE(rnext, 3 * Tn * sizeof(int32_t));
+  ENSURE(rdist, 3 * Tn * sizeof(int32_t));
+  const int64_t nbits = (3 * Tn + 31) / 32;
+  ENSURE(startbits, nbits * sizeof(uint32_t));
+  // ruler entries: seed starts + the 1/8 hash sample of half-edges (+ slack)
+  const int64_t ecap = P + (3 * Tn) / 8 + (3 * Tn) / 16 + 1024;
+  ENSURE(ent_r, ecap * sizeof(int32_t));
+  ENSURE(ent_base, ecap * sizeof(int64_t));
   CK(cudaMemsetAsync(ctx->stamp.p, 0xFF, Tn * sizeof(int32_t), s));
+  CK(cudaMemsetAsync(ctx->startbits.p, 0, nbits * sizeof(uint32_t), s));
   {
     SegTimer st_(ctx, S_TRAV_START, s);
     launch_trav_start(d_hw, ctx->seeds.as<int32_t>(), P, ctx->start.as<int32_t>(), ctx->overflow.as<int32_t>(),
-                      &dc->n_overflow, ctx->queue.as<int32_t>(), ctx->stamp.as<int32_t>(), &dc->st, s);
+                      &dc->n_overflow, ctx->queue.as<int32_t>(), ctx->stamp.as<int32_t>(),
+                      ctx->startbits.as<uint32_t>(), &dc->st, s);
+  }
+  {
+    SegTimer st_(ctx, S_TRAV_RULERS, s);
+    launch_ruler_walk(d_hw, ctx->startbits.as<uint32_t>(), T, ctx->rnext.as<int32_t>(), ctx->rdist.as<int32_t>(),
+                      &dc->st, s);
   }
   CK(cudaMemsetAsync(ctx->len.as<int64_t>() + P, 0, sizeof(int64_t), s));
+  CK(cudaMemsetAsync(ctx->nrul.as<int64_t>() + P, 0, sizeof(int64_t), s));
   {
     SegTimer st_(ctx, S_TRAV_LEN, s);
-    launch_trav_len(d_hw, ctx->seeds.as<int32_t>(), ctx->start.as<int32_t>(), P, T, ctx->len.as<int64_t>(), &dc->st,
-                    s);
+    launch_chain_count(ctx->seeds.as<int32_t>(), ctx->start.as<int32_t>(), P, T, ctx->rnext.as<int32_t>(),
+                       ctx->rdist.as<int32_t>(), ctx->len.as<int64_t>(), ctx->nrul.as<int64_t>(), &dc->st, s);
   }
   {
     SegTimer st_(ctx, S_TRAV_SCAN, s);
     launch_scan(ctx->len.as<int64_t>(), d_offsets, P + 1, ctx->temp.p, ctx->temp.bytes, s);
+    launch_scan(ctx->nrul.as<int64_t>(), ctx->eoff.as<int64_t>(), P + 1, ctx->temp.p, ctx->temp.bytes, s);
   }
   CK(cudaGetLastError());
-  int64_t total = 0;
   CK(cudaMemcpyAsync(&dc->stats[0], d_offsets + P, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(&dc->stats[1], ctx->eoff.as<int64_t>() + P, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
   if ((rc = read_counters(ctx, s, &h))) return rc;
   if ((rc = decode_status(ctx, h.st, "traversal"))) return rc;
-  total = (int64_t)h.stats[0];
+  int64_t total = (int64_t)h.stats[0], n_ent = (int64_t)h.stats[1];
   if (total > cap_slots)
     return set_err(ctx, TM_ERR_STRUCTURAL, "[traversal] polygon storage capacity exceeded; labels are inconsistent");
+  if (n_ent > ecap) return set_err(ctx, TM_ERR_CAPACITY, "[traversal] ruler entry capacity exceeded");
   {
     SegTimer st_(ctx, S_TRAV_WRITE, s);
-    launch_trav_write(d_tri32, d_hw, ctx->start.as<int32_t>(), P, T, d_offsets, d_verts, s);
+    launch_chain_emit(ctx->start.as<int32_t>(), P, ctx->rnext.as<int32_t>(), ctx->rdist.as<int32_t>(), d_offsets,
+                      ctx->eoff.as<int64_t>(), ctx->ent_r.as<int32_t>(), ctx->ent_base.as<int64_t>(), s);
+    launch_ruler_write(d_tri32, d_hw, ctx->eoff.as<int64_t>() + P, ctx->ent_r.as<int32_t>(),
+                       ctx->ent_base.as<int64_t>(), ctx->rdist.as<int32_t>(), T, d_verts, s);
   }
   CK(cudaGetLastError());
   *n_slots = total;

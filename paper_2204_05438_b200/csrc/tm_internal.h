@@ -30,11 +30,17 @@ void launch_select_seeds(const uint8_t* seed, int64_t T, int32_t* seeds, int64_t
 size_t scan_temp_bytes(int64_t n);
 void launch_scan(const int64_t* in, int64_t* out, int64_t n, void* temp, size_t temp_bytes, cudaStream_t s);
 void launch_trav_start(const int32_t* hw, const int32_t* seeds, int64_t P, int32_t* start, int32_t* overflow,
-                       unsigned int* n_overflow, int32_t* queue, int32_t* stamp, DevStatus* st, cudaStream_t s);
-void launch_trav_len(const int32_t* hw, const int32_t* seeds, const int32_t* start, int64_t P, int64_t T,
-                     int64_t* len, DevStatus* st, cudaStream_t s);
-void launch_trav_write(const int32_t* tri, const int32_t* hw, const int32_t* start, int64_t P, int64_t T,
-                       const int64_t* offsets, int32_t* verts, cudaStream_t s);
+                       unsigned int* n_overflow, int32_t* queue, int32_t* stamp, uint32_t* bits, DevStatus* st,
+                       cudaStream_t s);
+void launch_ruler_walk(const int32_t* hw, const uint32_t* bits, int64_t T, int32_t* rnext, int32_t* rdist,
+                       DevStatus* st, cudaStream_t s);
+void launch_chain_count(const int32_t* seeds, const int32_t* start, int64_t P, int64_t T, const int32_t* rnext,
+                        const int32_t* rdist, int64_t* len, int64_t* nrul, DevStatus* st, cudaStream_t s);
+void launch_chain_emit(const int32_t* start, int64_t P, const int32_t* rnext, const int32_t* rdist,
+                       const int64_t* offsets, const int64_t* eoff, int32_t* ent_r, int64_t* ent_base,
+                       cudaStream_t s);
+void launch_ruler_write(const int32_t* tri, const int32_t* hw, const int64_t* n_entries, const int32_t* ent_r,
+                        const int64_t* ent_base, const int32_t* rdist, int64_t T, int32_t* verts, cudaStream_t s);
 
 // tm_repair.cu
 struct RepairArgs {

@@ -151,34 +151,58 @@ __global__ void __launch_bounds__(256) k_classify(const int64_t* __restrict__ of
   if (rep_cnt) atomicAdd(stats + 6, rep_cnt);
 }
 
-// long polygons: one warp each, quadratic duplicate count split over lanes
-__global__ void k_classify_long(const int64_t* __restrict__ off, const int32_t* __restrict__ v,
-                                const int32_t* __restrict__ long_list, const unsigned int* n_long,
-                                int32_t* __restrict__ item_of, int32_t* __restrict__ items, unsigned int* n_items,
-                                unsigned long long* stats) {
-  int lane = threadIdx.x & 31;
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+// long polygons: one block each; distinct vertices counted with a shared-memory
+// open-addressing set (len <= kSetCap/2), else a block-parallel quadratic scan.
+constexpr int kSetCap = 8192;
+__global__ void __launch_bounds__(256) k_classify_long(const int64_t* __restrict__ off, const int32_t* __restrict__ v,
+                                                       const int32_t* __restrict__ long_list,
+                                                       const unsigned int* n_long, int32_t* __restrict__ item_of,
+                                                       int32_t* __restrict__ items, unsigned int* n_items,
+                                                       unsigned long long* stats) {
+  __shared__ int32_t tab[kSetCap];
+  __shared__ unsigned int dups;
   unsigned int nl = *n_long;
-  for (int64_t w = warp; w < nl; w += nwarps) {
+  for (unsigned int w = blockIdx.x; w < nl; w += gridDim.x) {
     int32_t i = long_list[w];
-    int64_t b = off[i], n = off[i + 1] - b;
+    int64_t b = off[i];
+    int n = (int)(off[i + 1] - b);
     const int32_t* s = v + b;
-    unsigned long long ex = 0;
-    for (int64_t p = lane; p < n; p += 32) {
-      int32_t x = s[p];
-      bool dup = false;
-      for (int64_t q = 0; q < p && !dup; q++) dup = s[q] == x;
-      ex += dup;
+    if (threadIdx.x == 0) dups = 0;
+    unsigned int my = 0;
+    if (2 * n <= kSetCap) {
+      int cap = 64;
+      while (cap < 2 * n) cap <<= 1;
+      for (int k = threadIdx.x; k < cap; k += blockDim.x) tab[k] = -1;
+      __syncthreads();
+      for (int p = threadIdx.x; p < n; p += blockDim.x) {
+        int32_t x = s[p];
+        uint32_t slot = ((uint32_t)x * 0x9E3779B1u) >> (32 - __ffs(cap) + 1);
+        for (;;) {
+          int32_t prev = atomicCAS(&tab[slot], -1, x);
+          if (prev == -1) break;
+          if (prev == x) { my++; break; }
+          slot = (slot + 1) & (cap - 1);
+        }
+      }
+    } else {
+      __syncthreads();
+      for (int p = threadIdx.x; p < n; p += blockDim.x) {
+        int32_t x = s[p];
+        bool dup = false;
+        for (int q = 0; q < p && !dup; q++) dup = s[q] == x;
+        my += dup;
+      }
     }
-    for (int o = 16; o > 0; o >>= 1) ex += __shfl_xor_sync(0xffffffffu, ex, o);
-    if (lane == 0 && ex > 0) {
+    atomicAdd(&dups, my);
+    __syncthreads();
+    if (threadIdx.x == 0 && dups > 0) {
       unsigned int k = atomicAdd(n_items, 1u);
       items[k] = i;
       item_of[i] = (int32_t)k;
-      atomicAdd(stats + 2, ex);
+      atomicAdd(stats + 2, (unsigned long long)dups);
       atomicAdd(stats + 6, 1ull);
     }
+    __syncthreads();
   }
 }
 
@@ -821,7 +845,7 @@ void launch_classify(const int64_t* off, const int32_t* v, int64_t P, int32_t* i
   if (P <= 0) return;
   k_classify<<<grid_for(P, 256), 256, 0, s>>>(off, v, P, item_of, items, n_items, long_list, n_long, stats);
   note_launch(1);
-  k_classify_long<<<kNumSMs * 2, 256, 0, s>>>(off, v, long_list, n_long, item_of, items, n_items, stats);
+  k_classify_long<<<kNumSMs * 4, 256, 0, s>>>(off, v, long_list, n_long, item_of, items, n_items, stats);
   note_launch(1);
 }
 

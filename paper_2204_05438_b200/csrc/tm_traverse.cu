@@ -6,6 +6,14 @@
 // Output order is ascending seed order with a count -> exclusive scan -> write
 // layout, which reproduces the reference's SEQUENTIAL `mesh`/`positions` byte
 // for byte instead of the paper's unordered AtomicAdd append.
+//
+// The walks are split at "rulers" so no thread walks a whole long polygon
+// (hull-sliver regions reach 902 boundary vertices at 1M, 3210 at 10M): the
+// rulers are every seed's start half-edge plus a hash-sampled 1/8 of all
+// frontier half-edges.  (1) every ruler walks to the next ruler (expected 8
+// boundary steps); (2) every seed follows its ruler chain (L/8 links) for the
+// polygon length and the ruler offsets; (3) scan; (4) every ruler on a seed
+// cycle writes its run.  Critical path ~ max ruler gap + L/8 instead of L.
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <thrust/iterator/counting_iterator.h>
@@ -44,15 +52,22 @@ __device__ int32_t seed_start(const int32_t* __restrict__ hw, int32_t t) {
   return -1;
 }
 
+__device__ __forceinline__ void mark_start(uint32_t* bits, int32_t h) { atomicOr(bits + (h >> 5), 1u << (h & 31)); }
+__device__ __forceinline__ bool is_start(const uint32_t* bits, int32_t h) { return (__ldg(bits + (h >> 5)) >> (h & 31)) & 1u; }
+// 1 in 8 half-edges, by a multiplicative hash of the id
+__device__ __forceinline__ bool sampled(int32_t h) { return ((uint32_t)h * 0x9E3779B1u) < (1u << 29); }
+__device__ __forceinline__ bool is_ruler(const uint32_t* bits, int32_t h) { return sampled(h) || is_start(bits, h); }
+
 __global__ void __launch_bounds__(256) k_trav_start(const int32_t* __restrict__ hw, const int32_t* __restrict__ seeds,
                                                     int64_t P, int32_t* __restrict__ start,
                                                     int32_t* __restrict__ overflow, unsigned int* n_overflow,
-                                                    DevStatus* st) {
+                                                    uint32_t* __restrict__ bits, DevStatus* st) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t t = seeds[i];
     int32_t h = seed_start(hw, t);
     if (h == -2) overflow[atomicAdd(n_overflow, 1u)] = (int32_t)i;
     else if (h < 0) report(st, K_NO_FRONTIER, t);
+    else mark_start(bits, h);
     start[i] = h;
   }
 }
@@ -62,7 +77,7 @@ __global__ void __launch_bounds__(256) k_trav_start(const int32_t* __restrict__ 
 __global__ void k_bfs_slow(const int32_t* __restrict__ hw, const int32_t* __restrict__ seeds,
                            int32_t* __restrict__ start, const int32_t* __restrict__ overflow,
                            const unsigned int* n_overflow, int32_t* __restrict__ queue, int32_t* __restrict__ stamp,
-                           DevStatus* st) {
+                           uint32_t* __restrict__ bits, DevStatus* st) {
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
   unsigned int no = *n_overflow;
   for (unsigned int k = 0; k < no; k++) {
@@ -80,40 +95,83 @@ __global__ void k_bfs_slow(const int32_t* __restrict__ hw, const int32_t* __rest
       }
     }
     if (res < 0) report(st, K_NO_FRONTIER, t);
+    else mark_start(bits, res);
     start[i] = res;
   }
 }
 
-__global__ void __launch_bounds__(256) k_trav_len(const int32_t* __restrict__ hw, const int32_t* __restrict__ seeds,
-                                                  const int32_t* __restrict__ start, int64_t P, long long limit,
-                                                  int64_t* __restrict__ len, DevStatus* st) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t h0 = start[i], h = h0;
-    long long n = 0;
-    if (h0 >= 0) {
-      for (;;) {
-        if (++n > limit) { n = -1; break; }
-        h = walk_next(hw, h, limit);
-        if (h < 0) { n = -1; break; }
-        if (h == h0) break;
-      }
-      if (n < 0) report(st, K_WALK, seeds[i]);
-    }
-    len[i] = n > 0 ? n : 0;
+// (1) every ruler walks to the next ruler: rnext/rdist indexed by half-edge id
+__global__ void __launch_bounds__(256) k_ruler_walk(const int32_t* __restrict__ hw, const uint32_t* __restrict__ bits,
+                                                    int64_t H, long long limit, int32_t* __restrict__ rnext,
+                                                    int32_t* __restrict__ rdist, DevStatus* st) {
+  for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < H; h += (int64_t)gridDim.x * blockDim.x) {
+    if (!hw_front(hw[h]) || !is_ruler(bits, (int32_t)h)) continue;
+    int32_t g = (int32_t)h;
+    long long d = 0;
+    do {
+      d++;
+      g = walk_next(hw, g, limit);
+      if (g < 0 || d > limit) { report(st, K_WALK, h / 3); g = (int32_t)h; break; }
+    } while (!is_ruler(bits, g));
+    rnext[h] = g;
+    rdist[h] = (int32_t)d;
   }
 }
 
-__global__ void __launch_bounds__(256) k_trav_write(const int32_t* __restrict__ tri, const int32_t* __restrict__ hw,
-                                                    const int32_t* __restrict__ start, int64_t P, long long limit,
-                                                    const int64_t* __restrict__ offsets, int32_t* __restrict__ verts) {
+// (2a) polygon length and ruler count per seed (traversal.py:264-281)
+__global__ void __launch_bounds__(256) k_chain_count(const int32_t* __restrict__ seeds, const int32_t* __restrict__ start,
+                                                     int64_t P, long long limit, const int32_t* __restrict__ rnext,
+                                                     const int32_t* __restrict__ rdist, int64_t* __restrict__ len,
+                                                     int64_t* __restrict__ nrul, DevStatus* st) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t w = offsets[i], end = offsets[i + 1];
-    int32_t h0 = start[i], h = h0;
-    if (h0 < 0 || end == w) continue;
-    do {
-      verts[w++] = he_origin(tri, h);
-      h = walk_next(hw, h, limit);
-    } while (h != h0 && h >= 0 && w < end);
+    int32_t h0 = start[i], r = h0;
+    long long L = 0, cnt = 0;
+    if (h0 >= 0) {
+      do {
+        L += rdist[r];
+        cnt++;
+        r = rnext[r];
+        if (L > limit) { report(st, K_WALK, seeds[i]); L = 0; cnt = 0; break; }
+      } while (r != h0);
+    }
+    len[i] = L;
+    nrul[i] = cnt;
+  }
+}
+
+// (2b) emit (ruler, absolute output offset) entries in chain order
+__global__ void __launch_bounds__(256) k_chain_emit(const int32_t* __restrict__ start, int64_t P,
+                                                    const int32_t* __restrict__ rnext, const int32_t* __restrict__ rdist,
+                                                    const int64_t* __restrict__ offsets, const int64_t* __restrict__ eoff,
+                                                    int32_t* __restrict__ ent_r, int64_t* __restrict__ ent_base) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t k = eoff[i], kend = eoff[i + 1], pos = offsets[i];
+    int32_t r = start[i];
+    for (; k < kend; k++) {
+      ent_r[k] = r;
+      ent_base[k] = pos;
+      pos += rdist[r];
+      r = rnext[r];
+    }
+  }
+}
+
+// (4) every ruler run writes origin(h) for its boundary half-edges (traversal.py:284-300)
+__global__ void __launch_bounds__(256) k_ruler_write(const int32_t* __restrict__ tri, const int32_t* __restrict__ hw,
+                                                     const int64_t* __restrict__ n_entries,
+                                                     const int32_t* __restrict__ ent_r,
+                                                     const int64_t* __restrict__ ent_base,
+                                                     const int32_t* __restrict__ rdist, long long limit,
+                                                     int32_t* __restrict__ verts) {
+  int64_t E = *n_entries;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < E; k += (int64_t)gridDim.x * blockDim.x) {
+    int32_t g = ent_r[k];
+    int64_t w = ent_base[k];
+    int d = rdist[g];
+    for (int s = 0; s < d; s++) {
+      verts[w + s] = he_origin(tri, g);
+      g = walk_next(hw, g, limit);
+    }
   }
 }
 
@@ -148,25 +206,39 @@ void launch_scan(const int64_t* in, int64_t* out, int64_t n, void* temp, size_t 
 }
 
 void launch_trav_start(const int32_t* hw, const int32_t* seeds, int64_t P, int32_t* start, int32_t* overflow,
-                       unsigned int* n_overflow, int32_t* queue, int32_t* stamp, DevStatus* st, cudaStream_t s) {
+                       unsigned int* n_overflow, int32_t* queue, int32_t* stamp, uint32_t* bits, DevStatus* st,
+                       cudaStream_t s) {
   if (P <= 0) return;
-  k_trav_start<<<grid_for(P, 256), 256, 0, s>>>(hw, seeds, P, start, overflow, n_overflow, st);
-  note_launch(1);
-  k_bfs_slow<<<1, 32, 0, s>>>(hw, seeds, start, overflow, n_overflow, queue, stamp, st);
+  k_trav_start<<<grid_for(P, 256), 256, 0, s>>>(hw, seeds, P, start, overflow, n_overflow, bits, st);
+  k_bfs_slow<<<1, 32, 0, s>>>(hw, seeds, start, overflow, n_overflow, queue, stamp, bits, st);
+  note_launch(2);
+}
+
+void launch_ruler_walk(const int32_t* hw, const uint32_t* bits, int64_t T, int32_t* rnext, int32_t* rdist,
+                       DevStatus* st, cudaStream_t s) {
+  if (T <= 0) return;
+  k_ruler_walk<<<grid_for(3 * T, 256), 256, 0, s>>>(hw, bits, 3 * T, 3 * T + 3, rnext, rdist, st);
   note_launch(1);
 }
 
-void launch_trav_len(const int32_t* hw, const int32_t* seeds, const int32_t* start, int64_t P, int64_t T,
-                     int64_t* len, DevStatus* st, cudaStream_t s) {
+void launch_chain_count(const int32_t* seeds, const int32_t* start, int64_t P, int64_t T, const int32_t* rnext,
+                        const int32_t* rdist, int64_t* len, int64_t* nrul, DevStatus* st, cudaStream_t s) {
   if (P <= 0) return;
-  k_trav_len<<<grid_for(P, 256), 256, 0, s>>>(hw, seeds, start, P, 3 * T + 3, len, st);
+  k_chain_count<<<grid_for(P, 256), 256, 0, s>>>(seeds, start, P, 3 * T + 3, rnext, rdist, len, nrul, st);
   note_launch(1);
 }
 
-void launch_trav_write(const int32_t* tri, const int32_t* hw, const int32_t* start, int64_t P, int64_t T,
-                       const int64_t* offsets, int32_t* verts, cudaStream_t s) {
+void launch_chain_emit(const int32_t* start, int64_t P, const int32_t* rnext, const int32_t* rdist,
+                       const int64_t* offsets, const int64_t* eoff, int32_t* ent_r, int64_t* ent_base,
+                       cudaStream_t s) {
   if (P <= 0) return;
-  k_trav_write<<<grid_for(P, 256), 256, 0, s>>>(tri, hw, start, P, 3 * T + 3, offsets, verts);
+  k_chain_emit<<<grid_for(P, 256), 256, 0, s>>>(start, P, rnext, rdist, offsets, eoff, ent_r, ent_base);
+  note_launch(1);
+}
+
+void launch_ruler_write(const int32_t* tri, const int32_t* hw, const int64_t* n_entries, const int32_t* ent_r,
+                        const int64_t* ent_base, const int32_t* rdist, int64_t T, int32_t* verts, cudaStream_t s) {
+  k_ruler_write<<<kNumSMs * 16, 256, 0, s>>>(tri, hw, n_entries, ent_r, ent_base, rdist, 3 * T + 3, verts);
   note_launch(1);
 }
 
