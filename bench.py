@@ -112,19 +112,21 @@ class ClockSampler:
 
 def algorithmic_bytes(n, T, F, P, Fp, Pp):
     """Compulsory bytes per segment: every
-    array touched once in its device dtype."""
+    array touched once in its device dtype.  R = rulers = seeds + F/8."""
+    R = P + F // 8
     return {
         "label_a_tri_pass": 24 * T + 16 * n + 12 * T + 1 * T + 12 * T + 4 * n,   # tri i64 in, xy, tri32, max_edge, twin, trivertex
         "label_b_edges": 12 * T + 1 * T + 12 * T + 1 * T,                       # hw in/out, max_edge, seed
         "select_seeds": 1 * T + 4 * P,
         "trav_start": 4 * P + 12 * P + 4 * P,
-        "trav_len": 12 * T + 4 * P + 8 * P,
-        "trav_scan": 16 * P,
-        "trav_write": 12 * T + 4 * F + 4 * P + 8 * P + 4 * F,
+        "trav_rulers": 12 * T + 12 * T + 8 * R,                                 # hw scan + rotations, rnext/rdist
+        "trav_chain": 4 * P + 8 * R + 16 * P,
+        "trav_scan": 32 * P,
+        "trav_write": 4 * P + 8 * R + 24 * R + 12 * T + 4 * F + 4 * F,
         "repair_classify": 8 * P + 4 * F + 4 * P,
         "repair_tips": 0,
         "repair_pinch": 0,
-        "repair_stitch": 8 * P + 4 * F + 8 * Pp + 4 * Fp,
+        "repair_stitch": 8 * P + 4 * F + 8 * Pp + 4 * Fp + 48 * P,
     }
 
 

@@ -1,12 +1,18 @@
 // tm_capi.cu -- extern "C" entry points (include/termesh_b200.h) and the host
-// orchestration of the device phases: workspace management, status decoding
-// into the reference's error vocabulary, and the whole-path drivers.
+// orchestration of the device phases.
+//
+// Every phase is *enqueued* without host round trips: element counts stay in
+// device memory (a Counters block) and every kernel reads them from there, with
+// host-known upper bounds (T, 3T) sizing the grids.  The whole mesh -> polygons
+// path is therefore captured once as a CUDA graph and replayed; the host reads
+// the counters (status, counts, repair stats) once at the end.
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
-#include <tuple>
+#include <cstdlib>
 #include <cstring>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/termesh_b200.h"
@@ -39,27 +45,27 @@ struct Buf {
   T* as() const { return static_cast<T*>(p); }
 };
 
-struct Counters {       // device scratch, zeroed per phase
+// Device-side counters of one pipeline run (reset at the start of a run).
+struct Counters {
   DevStatus st;
-  int64_t n_seeds;
-  unsigned int n_overflow;
-  unsigned int n_items;
-  unsigned int n_long;
-  unsigned int pad;
-  unsigned long long pool_top;
-  unsigned long long undo_top;
+  int64_t n_seeds;     // P: polygons after traversal
+  int64_t n_slots0;    // F: vertex slots after traversal
+  int64_t n_entries;   // ruler entries
+  int64_t p_in;        // repair input polygon count (tm_repair called with a host count)
+  int64_t p_out;       // P': polygons after repair
+  int64_t f_out;       // F': vertex slots after repair
+  unsigned int n_overflow, n_items, n_long, pad;
+  unsigned long long pool_top, undo_top;
   unsigned long long stats[8];
 };
 
-// timed segments (tm_ctx_segment_ms); names in kSegNames
 enum Seg {
   S_LABEL_A, S_LABEL_B, S_SEEDS, S_TRAV_START, S_TRAV_RULERS, S_TRAV_LEN, S_TRAV_SCAN, S_TRAV_WRITE,
   S_CLASSIFY, S_REPAIR_TIPS, S_REPAIR_PINCH, S_STITCH, S_NUM
 };
 const char* kSegNames[S_NUM] = {"label_a_tri_pass", "label_b_edges", "select_seeds", "trav_start", "trav_rulers",
-                                "trav_chain",
-                                "trav_scan", "trav_write", "repair_classify", "repair_tips", "repair_pinch",
-                                "repair_stitch"};
+                                "trav_chain", "trav_scan", "trav_write", "repair_classify", "repair_tips",
+                                "repair_pinch", "repair_stitch"};
 
 struct Prof {
   bool on = false;
@@ -70,6 +76,20 @@ struct Prof {
 };
 
 std::atomic<long long> g_launches{0};
+
+struct GraphKey {
+  const void* xy = nullptr;
+  const void* tri = nullptr;
+  void* off = nullptr;
+  void* v = nullptr;
+  int64_t n = -1, T = -1;
+  int bits = 0, check = 0;
+  unsigned long long pool_cap = 0;
+  bool operator==(const GraphKey& o) const {
+    return xy == o.xy && tri == o.tri && off == o.off && v == o.v && n == o.n && T == o.T && bits == o.bits &&
+           check == o.check && pool_cap == o.pool_cap;
+  }
+};
 
 }  // namespace
 
@@ -83,19 +103,26 @@ struct tm_ctx {
   int64_t defect_count[K_NUM] = {0};
   int64_t defect_first[K_NUM] = {0};
   double phase_ms[3] = {0, 0, 0};
-  Buf counters, pinned_counters;
+  Buf counters;
+  Counters* h_reset = nullptr;   // pinned, constant reset image
+  Counters* h_result = nullptr;  // pinned, D2H target
+  int64_t* h_pin = nullptr;      // pinned scratch (host counts for tm_repair)
   // label
   Buf slots;
   // traversal
-  Buf seeds, start, len, overflow, queue, stamp, temp, nrul, eoff, rnext, rdist, startbits, ent_r, ent_base;
+  Buf seeds, start, len, overflow, queue, stamp, tiles, nrul, eoff, rnext, rdist, startbits, ent_r, ent_base;
   // repair
   Buf item_of, items, long_list, item_list, item_n, item_slots, cnt, slotsz, pbase, sbase, pool, undo;
   // whole-path buffers
   Buf xy, tri, tri32, hw, max_edge, seed, tv, off0, v0, fin_off, fin_v;
-  Buf h_pin_in, h_pin_out;
-  cudaStream_t own_stream = nullptr;
+  cudaStream_t gstream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  unsigned long long pool_cap_hint = 0;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  GraphKey gkey;
+  unsigned long long pool_cap = 0;
+  int64_t ecap = 0;
+  int use_graph = 1;
 };
 
 static int set_err(tm_ctx* c, int code, const char* fmt, ...) {
@@ -112,18 +139,21 @@ static int cuda_fail(tm_ctx* c, cudaError_t e, const char* where) {
   return set_err(c, TM_ERR_CUDA, "CUDA error in %s: %s", where, cudaGetErrorString(e));
 }
 
-#define CK(call)                                                         \
-  do {                                                                   \
-    cudaError_t _e = (call);                                             \
-    if (_e != cudaSuccess) return cuda_fail(ctx, _e, #call);             \
+#define CK(call)                                             \
+  do {                                                       \
+    cudaError_t _e = (call);                                 \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, #call); \
   } while (0)
 
-#define ENSURE(buf, bytes)                                                        \
-  do {                                                                            \
-    if (!ctx->buf.ensure(bytes)) return set_err(ctx, TM_ERR_CUDA, "cudaMalloc of %zu bytes for %s failed", \
-                                                (size_t)(bytes), #buf);           \
+#define ENSURE(buf, bytes)                                                                                   \
+  do {                                                                                                       \
+    if (!ctx->buf.ensure(bytes))                                                                             \
+      return set_err(ctx, TM_ERR_CUDA, "cudaMalloc of %zu bytes for %s failed", (size_t)(bytes), #buf);     \
   } while (0)
 
+static Counters* dc_of(tm_ctx* ctx) { return ctx->counters.as<Counters>(); }
+
+// ---------------------------------------------------------------- profiling
 static cudaEvent_t prof_event(tm_ctx* ctx) {
   if (!ctx->prof.free_ev.empty()) {
     cudaEvent_t e = ctx->prof.free_ev.back();
@@ -135,8 +165,7 @@ static cudaEvent_t prof_event(tm_ctx* ctx) {
   return e;
 }
 
-// Segment timers: CUDA events recorded on the launching stream around the kernels.
-struct SegTimer {
+struct SegTimer {  // CUDA events on the launching stream around a kernel group
   tm_ctx* ctx;
   int seg;
   cudaStream_t s;
@@ -169,30 +198,29 @@ static void prof_flush(tm_ctx* ctx) {
   ctx->prof.pending.clear();
 }
 
-static Counters* dev_counters(tm_ctx* ctx) { return ctx->counters.as<Counters>(); }
-
-static int reset_counters(tm_ctx* ctx, cudaStream_t s) {
+// ---------------------------------------------------------------- counters
+static int init_counters(tm_ctx* ctx) {
   if (!ctx->counters.ensure(sizeof(Counters))) return set_err(ctx, TM_ERR_CUDA, "cudaMalloc failed (counters)");
-  if (!ctx->pinned_counters.p) {
+  if (!ctx->h_reset) {
     void* p = nullptr;
-    if (cudaMallocHost(&p, sizeof(Counters)) != cudaSuccess) return set_err(ctx, TM_ERR_CUDA, "cudaMallocHost failed");
-    ctx->pinned_counters.p = p;
-    ctx->pinned_counters.bytes = sizeof(Counters);
+    if (cudaMallocHost(&p, 2 * sizeof(Counters) + 64) != cudaSuccess)
+      return set_err(ctx, TM_ERR_CUDA, "cudaMallocHost failed");
+    ctx->h_reset = static_cast<Counters*>(p);
+    ctx->h_result = ctx->h_reset + 1;
+    ctx->h_pin = reinterpret_cast<int64_t*>(ctx->h_result + 1);
+    memset(ctx->h_reset, 0, sizeof(Counters));
+    for (int k = 0; k < K_NUM; k++) ctx->h_reset->st.first[k] = ~0ull;
   }
-  Counters h;
-  memset(&h, 0, sizeof h);
-  for (int k = 0; k < K_NUM; k++) h.st.first[k] = ~0ull;
-  memcpy(ctx->pinned_counters.p, &h, sizeof h);
-  CK(cudaMemcpyAsync(ctx->counters.p, ctx->pinned_counters.p, sizeof h, cudaMemcpyHostToDevice, s));
   return TM_OK;
 }
 
-// fetch the counters to host (synchronizes s)
-static int read_counters(tm_ctx* ctx, cudaStream_t s, Counters* out) {
-  CK(cudaMemcpyAsync(ctx->pinned_counters.p, ctx->counters.p, sizeof(Counters), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  CK(cudaGetLastError());
-  memcpy(out, ctx->pinned_counters.p, sizeof(Counters));
+static int enqueue_reset(tm_ctx* ctx, cudaStream_t s) {
+  CK(cudaMemcpyAsync(ctx->counters.p, ctx->h_reset, sizeof(Counters), cudaMemcpyHostToDevice, s));
+  return TM_OK;
+}
+
+static int enqueue_readback(tm_ctx* ctx, cudaStream_t s) {
+  CK(cudaMemcpyAsync(ctx->h_result, ctx->counters.p, sizeof(Counters), cudaMemcpyDeviceToHost, s));
   return TM_OK;
 }
 
@@ -203,9 +231,10 @@ static const char* kind_name(int k) {
   return names[k];
 }
 
-// Decode device status.  Validation kinds (0..7) -> TM_ERR_VALIDATION,
-// structural kinds -> TM_ERR_STRUCTURAL with the reference's message wording.
-static int decode_status(tm_ctx* ctx, const DevStatus& st, const char* phase, const Counters* cn = nullptr) {
+// Device status -> the reference's error vocabulary.  Validation kinds (0..7)
+// -> TM_ERR_VALIDATION; structural kinds -> TM_ERR_STRUCTURAL.
+static int decode_status(tm_ctx* ctx, const Counters& h) {
+  const DevStatus& st = h.st;
   bool any = false;
   for (int k = 0; k < K_NUM; k++) {
     ctx->defect_count[k] = st.count[k];
@@ -229,61 +258,255 @@ static int decode_status(tm_ctx* ctx, const DevStatus& st, const char* phase, co
     long long f = (long long)st.first[k];
     switch (k) {
       case K_WALK:
-        return set_err(ctx, TM_ERR_STRUCTURAL, "[%s] boundary walk from seed triangle %lld did not terminate", phase, f);
+        return set_err(ctx, TM_ERR_STRUCTURAL, "[traversal] boundary walk from seed triangle %lld did not terminate", f);
       case K_NO_FRONTIER:
-        return set_err(ctx, TM_ERR_STRUCTURAL, "[%s] no frontier edge reachable from triangle %lld", phase, f);
+        return set_err(ctx, TM_ERR_STRUCTURAL, "[traversal] no frontier edge reachable from triangle %lld", f);
       case K_NO_CONVERGE:
         return set_err(ctx, TM_ERR_STRUCTURAL,
-                       "[%s] tip removal did not converge (polygon %lld; initial repeated-vertex count %llu)", phase,
-                       f, cn ? cn->stats[2] : 0ull);
+                       "[reparation] tip removal did not converge (polygon %lld; initial repeated-vertex count %llu)",
+                       f, h.stats[2]);
       case K_SPLIT_LAW:
-        return set_err(ctx, TM_ERR_STRUCTURAL, "[%s] polygon %lld: split broke the length law |pa|+|pb| = |P|+2",
-                       phase, f);
+        return set_err(ctx, TM_ERR_STRUCTURAL,
+                       "[reparation] polygon %lld: split broke the length law |pa|+|pb| = |P|+2", f);
       case K_POOL:
-        return set_err(ctx, TM_ERR_CAPACITY, "[%s] repair scratch pool exhausted (polygon %lld)", phase, f);
+        return set_err(ctx, TM_ERR_CAPACITY, "[reparation] repair scratch pool exhausted (polygon %lld)", f);
       case K_BARRIER:
-        return set_err(ctx, TM_ERR_STRUCTURAL, "[%s] polygon %lld: barrier edge not found around tip vertex", phase, f);
-      case K_NO_INTERNAL:
-        return set_err(ctx, TM_ERR_STRUCTURAL, "[%s] polygon %lld: tip vertex has no internal edge to split on", phase,
+        return set_err(ctx, TM_ERR_STRUCTURAL, "[reparation] polygon %lld: barrier edge not found around tip vertex",
                        f);
+      case K_NO_INTERNAL:
+        return set_err(ctx, TM_ERR_STRUCTURAL,
+                       "[reparation] polygon %lld: tip vertex has no internal edge to split on", f);
       default:
-        return set_err(ctx, TM_ERR_STRUCTURAL, "[%s] structural failure at element %lld", phase, f);
+        return set_err(ctx, TM_ERR_STRUCTURAL, "structural failure at element %lld", f);
     }
   }
   return TM_OK;
 }
 
+// ---------------------------------------------------------------- buffers
+static int prepare(tm_ctx* ctx, int64_t T) {
+  int rc = init_counters(ctx);
+  if (rc) return rc;
+  int64_t Tn = T > 0 ? T : 1;
+  ENSURE(slots, hash_capacity(Tn) * sizeof(uint32_t));
+  ENSURE(seeds, Tn * sizeof(int32_t));
+  ENSURE(start, Tn * sizeof(int32_t));
+  ENSURE(len, (Tn + 1) * sizeof(int64_t));
+  ENSURE(nrul, (Tn + 1) * sizeof(int64_t));
+  ENSURE(eoff, (Tn + 1) * sizeof(int64_t));
+  ENSURE(overflow, Tn * sizeof(int32_t));
+  ENSURE(queue, Tn * sizeof(int32_t));
+  ENSURE(stamp, Tn * sizeof(int32_t));
+  ENSURE(tiles, (scan_scratch_elems(3 * Tn) + 8) * sizeof(int64_t));
+  ENSURE(rnext, 3 * Tn * sizeof(int32_t));
+  ENSURE(rdist, 3 * Tn * sizeof(int32_t));
+  ENSURE(startbits, ((3 * Tn + 31) / 32) * sizeof(uint32_t));
+  // ruler entries: seed starts + the 1/8 hash sample of half-edges (+ slack)
+  ctx->ecap = Tn + (3 * Tn) / 8 + (3 * Tn) / 16 + 1024;
+  ENSURE(ent_r, ctx->ecap * sizeof(int32_t));
+  ENSURE(ent_base, ctx->ecap * sizeof(int64_t));
+  ENSURE(item_of, Tn * sizeof(int32_t));
+  ENSURE(items, Tn * sizeof(int32_t));
+  ENSURE(long_list, Tn * sizeof(int32_t));
+  ENSURE(item_list, Tn * sizeof(int64_t));
+  ENSURE(item_n, Tn * sizeof(int32_t));
+  ENSURE(item_slots, Tn * sizeof(int64_t));
+  ENSURE(cnt, (Tn + 1) * sizeof(int64_t));
+  ENSURE(slotsz, (Tn + 1) * sizeof(int64_t));
+  ENSURE(pbase, (Tn + 1) * sizeof(int64_t));
+  ENSURE(sbase, (Tn + 1) * sizeof(int64_t));
+  unsigned long long want = 6ull * (unsigned long long)Tn + (1ull << 20);
+  if (ctx->pool_cap < want) ctx->pool_cap = want;
+  if (ctx->pool_cap >= (1ull << 32)) return set_err(ctx, TM_ERR_CAPACITY, "repair scratch pool exceeds 2^32 slots");
+  ENSURE(pool, ctx->pool_cap * sizeof(int32_t));
+  ENSURE(undo, ((unsigned long long)Tn + 1024) * sizeof(int32_t));
+  return TM_OK;
+}
+
+// ---------------------------------------------------------------- enqueue (no host syncs)
+static int enqueue_label(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_tri, int tri_bits, int64_t T,
+                         int check, int32_t* d_tri32, int32_t* d_hw, int8_t* d_me, uint8_t* d_seed, int32_t* d_tv,
+                         cudaStream_t s) {
+  uint64_t cap = hash_capacity(T > 0 ? T : 1);
+  Counters* dc = dc_of(ctx);
+  {
+    SegTimer t_(ctx, S_LABEL_A, s);
+    launch_label_a(d_xy, n, d_tri, tri_bits == 64, T, check, d_tri32, d_hw, d_me, d_tv, ctx->slots.as<uint32_t>(),
+                   cap, &dc->st, s);
+  }
+  {
+    SegTimer t_(ctx, S_LABEL_B, s);
+    launch_label_b(n, T, d_hw, d_me, d_seed, d_tv, s);
+  }
+  CK(cudaGetLastError());
+  return TM_OK;
+}
+
+static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* d_hw, const uint8_t* d_seed,
+                            int64_t T, int64_t* d_off, int32_t* d_v, cudaStream_t s) {
+  Counters* dc = dc_of(ctx);
+  int64_t Tn = T > 0 ? T : 1;
+  int64_t* tiles = ctx->tiles.as<int64_t>();
+  {
+    SegTimer t_(ctx, S_SEEDS, s);
+    launch_select_flags(d_seed, T, ctx->seeds.as<int32_t>(), &dc->n_seeds, tiles, s);
+  }
+  CK(cudaMemsetAsync(ctx->stamp.p, 0xFF, Tn * sizeof(int32_t), s));
+  CK(cudaMemsetAsync(ctx->startbits.p, 0, ((3 * Tn + 31) / 32) * sizeof(uint32_t), s));
+  {
+    SegTimer t_(ctx, S_TRAV_START, s);
+    launch_trav_start(d_hw, ctx->seeds.as<int32_t>(), &dc->n_seeds, Tn, ctx->start.as<int32_t>(),
+                      ctx->overflow.as<int32_t>(), &dc->n_overflow, ctx->queue.as<int32_t>(),
+                      ctx->stamp.as<int32_t>(), ctx->startbits.as<uint32_t>(), &dc->st, s);
+  }
+  {
+    SegTimer t_(ctx, S_TRAV_RULERS, s);
+    launch_ruler_walk(d_hw, ctx->startbits.as<uint32_t>(), T, ctx->rnext.as<int32_t>(), ctx->rdist.as<int32_t>(),
+                      &dc->st, s);
+  }
+  {
+    SegTimer t_(ctx, S_TRAV_LEN, s);
+    launch_chain_count(ctx->seeds.as<int32_t>(), ctx->start.as<int32_t>(), &dc->n_seeds, Tn, T,
+                       ctx->rnext.as<int32_t>(), ctx->rdist.as<int32_t>(), ctx->len.as<int64_t>(),
+                       ctx->nrul.as<int64_t>(), &dc->st, s);
+  }
+  {
+    SegTimer t_(ctx, S_TRAV_SCAN, s);
+    launch_scan_dev(ctx->len.as<int64_t>(), d_off, &dc->n_seeds, Tn, tiles, s);
+    launch_scan_dev(ctx->nrul.as<int64_t>(), ctx->eoff.as<int64_t>(), &dc->n_seeds, Tn, tiles, s);
+    launch_gather_at(d_off, &dc->n_seeds, &dc->n_slots0, s);
+    launch_gather_at(ctx->eoff.as<int64_t>(), &dc->n_seeds, &dc->n_entries, s);
+  }
+  {
+    SegTimer t_(ctx, S_TRAV_WRITE, s);
+    launch_chain_emit(ctx->start.as<int32_t>(), &dc->n_seeds, Tn, ctx->rnext.as<int32_t>(), ctx->rdist.as<int32_t>(),
+                      d_off, ctx->eoff.as<int64_t>(), ctx->ent_r.as<int32_t>(), ctx->ent_base.as<int64_t>(),
+                      ctx->ecap, &dc->st, s);
+    launch_ruler_write(d_tri32, d_hw, &dc->n_entries, ctx->ent_r.as<int32_t>(), ctx->ent_base.as<int64_t>(),
+                       ctx->rdist.as<int32_t>(), T, ctx->ecap, d_v, s);
+  }
+  CK(cudaGetLastError());
+  return TM_OK;
+}
+
+// Repair phase.  Pp: device polygon count of the input CSR.
+static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, const int32_t* d_tv, int64_t T,
+                          const int64_t* d_off_in, const int32_t* d_v_in, const int64_t* Pp, int64_t* d_off_out,
+                          int32_t* d_v_out, cudaStream_t s) {
+  Counters* dc = dc_of(ctx);
+  int64_t Tn = T > 0 ? T : 1;
+  int64_t* tiles = ctx->tiles.as<int64_t>();
+  {
+    SegTimer t_(ctx, S_CLASSIFY, s);
+    launch_classify(d_off_in, d_v_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(), &dc->n_items,
+                    ctx->long_list.as<int32_t>(), &dc->n_long, dc->stats, s);
+  }
+  RepairArgs a{d_tri32, d_hw, d_tv, T, ctx->pool.as<int32_t>(), ctx->pool_cap, &dc->pool_top, ctx->undo.as<int32_t>(),
+               &dc->undo_top, (unsigned long long)Tn + 1024, &dc->st, ctx->items.as<int32_t>(), &dc->n_items,
+               d_off_in, d_v_in, ctx->item_list.as<int64_t>(), ctx->item_n.as<int32_t>(),
+               ctx->item_slots.as<int64_t>(), dc->stats};
+  {
+    SegTimer t_(ctx, S_REPAIR_TIPS, s);
+    launch_repair_tips(a, s);
+  }
+  {
+    SegTimer t_(ctx, S_REPAIR_PINCH, s);
+    launch_repair_pinch(a, s);
+  }
+  {
+    SegTimer t_(ctx, S_STITCH, s);
+    launch_out_counts(d_off_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->item_n.as<int32_t>(),
+                      ctx->item_slots.as<int64_t>(), ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), s);
+    launch_scan_dev(ctx->cnt.as<int64_t>(), ctx->pbase.as<int64_t>(), Pp, Tn, tiles, s);
+    launch_scan_dev(ctx->slotsz.as<int64_t>(), ctx->sbase.as<int64_t>(), Pp, Tn, tiles, s);
+    launch_finalize(Pp, ctx->pbase.as<int64_t>(), ctx->sbase.as<int64_t>(), d_off_out, &dc->p_out, &dc->f_out, s);
+    launch_stitch(d_off_in, d_v_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->item_list.as<int64_t>(),
+                  ctx->item_n.as<int32_t>(), ctx->pool.as<int32_t>(), ctx->pbase.as<int64_t>(),
+                  ctx->sbase.as<int64_t>(), d_off_out, d_v_out, s);
+  }
+  CK(cudaGetLastError());
+  return TM_OK;
+}
+
+// read back the counters (synchronizes s) and decode the status
+static int finish(tm_ctx* ctx, cudaStream_t s, Counters* out) {
+  int rc = enqueue_readback(ctx, s);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(s));
+  CK(cudaGetLastError());
+  *out = *ctx->h_result;
+  return decode_status(ctx, *out);
+}
+
+static void fill_stats(const Counters& h, int64_t* stats) {
+  if (!stats) return;
+  stats[TM_STAT_ROUNDS] = h.stats[0] > 0 ? (int64_t)h.stats[0] : 1;
+  stats[TM_STAT_SPLITS] = (int64_t)(h.stats[1] + h.stats[4]);
+  stats[TM_STAT_INITIAL_TIPS] = (int64_t)h.stats[2];
+  stats[TM_STAT_UNREPAIRED] = (int64_t)h.stats[3];
+  stats[TM_STAT_NONSIMPLE] = (int64_t)h.stats[6];
+  stats[TM_STAT_TIP_SPLITS] = (int64_t)h.stats[1];
+  stats[TM_STAT_PINCH_SPLITS] = (int64_t)h.stats[4];
+  stats[TM_STAT_WORK_ITEMS] = (int64_t)h.n_items;
+}
+
+// Pool overflow: roll back the promotions of the failed attempt, grow the
+// pool, and re-run the repair phase (outside any graph).
+static int retry_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, const int32_t* d_tv, int64_t T,
+                        const int64_t* d_off_in, const int32_t* d_v_in, const int64_t* Pp, int64_t* d_off_out,
+                        int32_t* d_v_out, cudaStream_t s, Counters* h, int rc) {
+  for (int attempt = 0; attempt < 6 && rc == TM_ERR_CAPACITY && h->st.count[K_POOL]; attempt++) {
+    unsigned long long ucap = (unsigned long long)(T > 0 ? T : 1) + 1024;
+    if (h->undo_top > ucap) return set_err(ctx, TM_ERR_CAPACITY, "[reparation] pool and promotion log overflowed");
+    Counters* dc = dc_of(ctx);
+    launch_undo(d_hw, ctx->undo.as<int32_t>(), &dc->undo_top, ucap, s);
+    CK(cudaStreamSynchronize(s));
+    ctx->pool_cap *= 4;
+    if (ctx->pool_cap >= (1ull << 32)) return set_err(ctx, TM_ERR_CAPACITY, "repair pool exceeds 2^32 slots");
+    ENSURE(pool, ctx->pool_cap * sizeof(int32_t));
+    // reset the repair-side counters and the status; keep the traversal counts
+    CK(cudaMemcpyAsync(&dc->st, &ctx->h_reset->st, sizeof(DevStatus), cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(&dc->n_items, 0, 2 * sizeof(unsigned int), s));
+    CK(cudaMemsetAsync(&dc->pool_top, 0, 10 * sizeof(unsigned long long), s));
+    int r = enqueue_repair(ctx, d_tri32, d_hw, d_tv, T, d_off_in, d_v_in, Pp, d_off_out, d_v_out, s);
+    if (r) return r;
+    rc = finish(ctx, s, h);
+  }
+  return rc;
+}
+
 extern "C" {
 
-int tm_version(void) { return 1; }
+int tm_version(void) { return 2; }
 
 int tm_ctx_create(tm_ctx** out) {
   if (!out) return TM_ERR_ARGUMENT;
-  *out = new tm_ctx();
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) {
-    delete *out;
-    *out = nullptr;
-    return TM_ERR_CUDA;
-  }
+  if (cudaGetDevice(&dev) != cudaSuccess) return TM_ERR_CUDA;
+  *out = new tm_ctx();
+  const char* g = getenv("TERMESH_NO_GRAPH");
+  if (g && *g && *g != '0') (*out)->use_graph = 0;
   return TM_OK;
 }
 
 void tm_ctx_destroy(tm_ctx* ctx) {
   if (!ctx) return;
   Buf* bufs[] = {&ctx->counters, &ctx->slots, &ctx->seeds, &ctx->start, &ctx->len, &ctx->overflow, &ctx->queue,
-                 &ctx->stamp, &ctx->temp, &ctx->nrul, &ctx->eoff, &ctx->rnext, &ctx->rdist, &ctx->startbits,
+                 &ctx->stamp, &ctx->tiles, &ctx->nrul, &ctx->eoff, &ctx->rnext, &ctx->rdist, &ctx->startbits,
                  &ctx->ent_r, &ctx->ent_base, &ctx->item_of, &ctx->items, &ctx->long_list, &ctx->item_list,
                  &ctx->item_n, &ctx->item_slots, &ctx->cnt, &ctx->slotsz, &ctx->pbase, &ctx->sbase, &ctx->pool,
                  &ctx->undo, &ctx->xy, &ctx->tri, &ctx->tri32, &ctx->hw, &ctx->max_edge, &ctx->seed, &ctx->tv,
                  &ctx->off0, &ctx->v0, &ctx->fin_off, &ctx->fin_v};
   for (Buf* b : bufs) b->release();
-  if (ctx->pinned_counters.p) cudaFreeHost(ctx->pinned_counters.p);
+  if (ctx->h_reset) cudaFreeHost(ctx->h_reset);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+  if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
   prof_flush(ctx);
   for (auto e : ctx->prof.free_ev) cudaEventDestroy(e);
-  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+  if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
   delete ctx;
 }
 
@@ -326,32 +549,25 @@ int tm_ctx_phase_ms(const tm_ctx* ctx, double* ms3) {
   return TM_OK;
 }
 
+static int check_sizes(tm_ctx* ctx, int64_t n, int64_t T) {
+  if (T < 0 || n < 0) return set_err(ctx, TM_ERR_ARGUMENT, "sizes must be non-negative");
+  if (3 * T >= (int64_t)0x7FFFFFFF) return set_err(ctx, TM_ERR_ARGUMENT, "3T must fit in 31 bits");
+  if (n >= (int64_t)0x7F7F7F7F) return set_err(ctx, TM_ERR_ARGUMENT, "vertex count must fit in 31 bits");
+  return TM_OK;
+}
+
 int tm_label(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_tri, int tri_bits, int64_t T, int check,
              int32_t* d_tri32, int32_t* d_hw, int8_t* d_max_edge, uint8_t* d_seed, int32_t* d_tv, void* stream) {
   if (!ctx) return TM_ERR_ARGUMENT;
-  if ((tri_bits != 32 && tri_bits != 64) || T < 0 || n < 0)
-    return set_err(ctx, TM_ERR_ARGUMENT, "tri_bits must be 32 or 64 and sizes non-negative");
-  if (3 * T >= (int64_t)0x7FFFFFFF) return set_err(ctx, TM_ERR_ARGUMENT, "3T must fit in 31 bits");
-  if (n >= (int64_t)0x7F7F7F7F) return set_err(ctx, TM_ERR_ARGUMENT, "vertex count must fit in 31 bits");
-  cudaStream_t s = (cudaStream_t)stream;
-  for (int k = 0; k < K_NUM; k++) ctx->defect_count[k] = 0, ctx->defect_first[k] = -1;
-  int rc = reset_counters(ctx, s);
+  if (tri_bits != 32 && tri_bits != 64) return set_err(ctx, TM_ERR_ARGUMENT, "tri_bits must be 32 or 64");
+  int rc = check_sizes(ctx, n, T);
   if (rc) return rc;
-  uint64_t cap = hash_capacity(T);
-  ENSURE(slots, cap * sizeof(uint32_t));
-  {
-    SegTimer st_(ctx, S_LABEL_A, s);
-    launch_label_a(d_xy, n, d_tri, tri_bits == 64, T, check, d_tri32, d_hw, d_max_edge, d_tv,
-                   ctx->slots.as<uint32_t>(), cap, &dev_counters(ctx)->st, s);
-  }
-  {
-    SegTimer st_(ctx, S_LABEL_B, s);
-    launch_label_b(n, T, d_hw, d_max_edge, d_seed, d_tv, s);
-  }
-  CK(cudaGetLastError());
+  cudaStream_t s = (cudaStream_t)stream;
+  if ((rc = prepare(ctx, T)) || (rc = enqueue_reset(ctx, s))) return rc;
+  if ((rc = enqueue_label(ctx, d_xy, n, d_tri, tri_bits, T, check, d_tri32, d_hw, d_max_edge, d_seed, d_tv, s)))
+    return rc;
   Counters h;
-  if ((rc = read_counters(ctx, s, &h))) return rc;
-  return decode_status(ctx, h.st, "label");
+  return finish(ctx, s, &h);
 }
 
 int tm_relabel(tm_ctx* ctx, int32_t* d_hw, const int8_t* d_max_edge, int64_t T, uint8_t* d_seed, void* stream) {
@@ -365,13 +581,12 @@ int tm_check_neighbors(tm_ctx* ctx, const int32_t* d_hw, const void* d_nb, int n
   if (!ctx) return TM_ERR_ARGUMENT;
   if (nb_bits != 32 && nb_bits != 64) return set_err(ctx, TM_ERR_ARGUMENT, "nb_bits must be 32 or 64");
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = reset_counters(ctx, s);
-  if (rc) return rc;
-  launch_check_neighbors(d_hw, d_nb, nb_bits == 64, T, &dev_counters(ctx)->st, s);
+  int rc = init_counters(ctx);
+  if (rc || (rc = enqueue_reset(ctx, s))) return rc;
+  launch_check_neighbors(d_hw, d_nb, nb_bits == 64, T, &dc_of(ctx)->st, s);
   CK(cudaGetLastError());
   Counters h;
-  if ((rc = read_counters(ctx, s, &h))) return rc;
-  return decode_status(ctx, h.st, "validate");
+  return finish(ctx, s, &h);
 }
 
 int tm_unpack_halfedges(tm_ctx* ctx, const int32_t* d_hw, int64_t T, int32_t* d_twin, uint8_t* d_fr, void* stream) {
@@ -392,91 +607,16 @@ int tm_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* d_hw, const 
                 int64_t* d_offsets, int32_t* d_verts, int64_t cap_polys, int64_t cap_slots, int64_t* n_polys,
                 int64_t* n_slots, void* stream) {
   if (!ctx || !n_polys || !n_slots) return TM_ERR_ARGUMENT;
+  if (cap_polys < T || cap_slots < 3 * T)
+    return set_err(ctx, TM_ERR_ARGUMENT, "tm_traverse needs cap_polys >= T and cap_slots >= 3T");
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = reset_counters(ctx, s);
-  if (rc) return rc;
-  Counters* dc = dev_counters(ctx);
-  int64_t Tn = T > 0 ? T : 1;
-  ENSURE(seeds, Tn * sizeof(int32_t));
-  size_t tb = select_seeds_temp_bytes(Tn);
-  size_t tb2 = scan_temp_bytes(Tn + 1);
-  ENSURE(temp, (tb > tb2 ? tb : tb2) + 256);
+  int rc = prepare(ctx, T);
+  if (rc || (rc = enqueue_reset(ctx, s))) return rc;
+  if ((rc = enqueue_traverse(ctx, d_tri32, d_hw, d_seed, T, d_offsets, d_verts, s))) return rc;
   Counters h;
-  int64_t P = 0;
-  if (T > 0) {
-    {
-      SegTimer st_(ctx, S_SEEDS, s);
-      launch_select_seeds(d_seed, T, ctx->seeds.as<int32_t>(), &dc->n_seeds, ctx->temp.p, ctx->temp.bytes, s);
-    }
-    CK(cudaGetLastError());
-    if ((rc = read_counters(ctx, s, &h))) return rc;
-    P = h.n_seeds;
-  }
-  if (P > cap_polys) return set_err(ctx, TM_ERR_CAPACITY, "polygon capacity %lld < %lld seeds", (long long)cap_polys, (long long)P);
-  *n_polys = P;
-  CK(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t), s));
-  if (P == 0) {
-    *n_slots = 0;
-    return TM_OK;
-  }
-  ENSURE(start, P * sizeof(int32_t));
-  ENSURE(len, (P + 1) * sizeof(int64_t));
-  ENSURE(nrul, (P + 1) * sizeof(int64_t));
-  ENSURE(eoff, (P + 1) * sizeof(int64_t));
-  ENSURE(overflow, P * sizeof(int32_t));
-  ENSURE(queue, Tn * sizeof(int32_t));
-  ENSURE(stamp, Tn * sizeof(int32_t));
-  ENSURE(rnext, 3 * Tn * sizeof(int32_t));
-  ENSURE(rdist, 3 * Tn * sizeof(int32_t));
-  const int64_t nbits = (3 * Tn + 31) / 32;
-  ENSURE(startbits, nbits * sizeof(uint32_t));
-  // ruler entries: seed starts + the 1/8 hash sample of half-edges (+ slack)
-  const int64_t ecap = P + (3 * Tn) / 8 + (3 * Tn) / 16 + 1024;
-  ENSURE(ent_r, ecap * sizeof(int32_t));
-  ENSURE(ent_base, ecap * sizeof(int64_t));
-  CK(cudaMemsetAsync(ctx->stamp.p, 0xFF, Tn * sizeof(int32_t), s));
-  CK(cudaMemsetAsync(ctx->startbits.p, 0, nbits * sizeof(uint32_t), s));
-  {
-    SegTimer st_(ctx, S_TRAV_START, s);
-    launch_trav_start(d_hw, ctx->seeds.as<int32_t>(), P, ctx->start.as<int32_t>(), ctx->overflow.as<int32_t>(),
-                      &dc->n_overflow, ctx->queue.as<int32_t>(), ctx->stamp.as<int32_t>(),
-                      ctx->startbits.as<uint32_t>(), &dc->st, s);
-  }
-  {
-    SegTimer st_(ctx, S_TRAV_RULERS, s);
-    launch_ruler_walk(d_hw, ctx->startbits.as<uint32_t>(), T, ctx->rnext.as<int32_t>(), ctx->rdist.as<int32_t>(),
-                      &dc->st, s);
-  }
-  CK(cudaMemsetAsync(ctx->len.as<int64_t>() + P, 0, sizeof(int64_t), s));
-  CK(cudaMemsetAsync(ctx->nrul.as<int64_t>() + P, 0, sizeof(int64_t), s));
-  {
-    SegTimer st_(ctx, S_TRAV_LEN, s);
-    launch_chain_count(ctx->seeds.as<int32_t>(), ctx->start.as<int32_t>(), P, T, ctx->rnext.as<int32_t>(),
-                       ctx->rdist.as<int32_t>(), ctx->len.as<int64_t>(), ctx->nrul.as<int64_t>(), &dc->st, s);
-  }
-  {
-    SegTimer st_(ctx, S_TRAV_SCAN, s);
-    launch_scan(ctx->len.as<int64_t>(), d_offsets, P + 1, ctx->temp.p, ctx->temp.bytes, s);
-    launch_scan(ctx->nrul.as<int64_t>(), ctx->eoff.as<int64_t>(), P + 1, ctx->temp.p, ctx->temp.bytes, s);
-  }
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(&dc->stats[0], d_offsets + P, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
-  CK(cudaMemcpyAsync(&dc->stats[1], ctx->eoff.as<int64_t>() + P, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
-  if ((rc = read_counters(ctx, s, &h))) return rc;
-  if ((rc = decode_status(ctx, h.st, "traversal"))) return rc;
-  int64_t total = (int64_t)h.stats[0], n_ent = (int64_t)h.stats[1];
-  if (total > cap_slots)
-    return set_err(ctx, TM_ERR_STRUCTURAL, "[traversal] polygon storage capacity exceeded; labels are inconsistent");
-  if (n_ent > ecap) return set_err(ctx, TM_ERR_CAPACITY, "[traversal] ruler entry capacity exceeded");
-  {
-    SegTimer st_(ctx, S_TRAV_WRITE, s);
-    launch_chain_emit(ctx->start.as<int32_t>(), P, ctx->rnext.as<int32_t>(), ctx->rdist.as<int32_t>(), d_offsets,
-                      ctx->eoff.as<int64_t>(), ctx->ent_r.as<int32_t>(), ctx->ent_base.as<int64_t>(), s);
-    launch_ruler_write(d_tri32, d_hw, ctx->eoff.as<int64_t>() + P, ctx->ent_r.as<int32_t>(),
-                       ctx->ent_base.as<int64_t>(), ctx->rdist.as<int32_t>(), T, d_verts, s);
-  }
-  CK(cudaGetLastError());
-  *n_slots = total;
+  if ((rc = finish(ctx, s, &h))) return rc;
+  *n_polys = h.n_seeds;
+  *n_slots = h.n_slots0;
   return TM_OK;
 }
 
@@ -485,129 +625,37 @@ int tm_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, const int32_t*
               int64_t cap_polys, int64_t cap_slots, int64_t* n_polys_out, int64_t* n_slots_out, int64_t* stats,
               void* stream) {
   if (!ctx || !n_polys_out || !n_slots_out) return TM_ERR_ARGUMENT;
+  if (cap_polys < T || cap_slots < 3 * T)
+    return set_err(ctx, TM_ERR_ARGUMENT, "tm_repair needs cap_polys >= T and cap_slots >= 3T");
+  if (P < 0 || P > (T > 0 ? T : 0)) return set_err(ctx, TM_ERR_ARGUMENT, "polygon count out of range");
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = reset_counters(ctx, s);
-  if (rc) return rc;
-  Counters* dc = dev_counters(ctx);
+  int rc = prepare(ctx, T);
+  if (rc || (rc = enqueue_reset(ctx, s))) return rc;
+  *ctx->h_pin = P;
+  Counters* dc = dc_of(ctx);
+  CK(cudaMemcpyAsync(&dc->p_in, ctx->h_pin, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  if ((rc = enqueue_repair(ctx, d_tri32, d_hw, d_tv, T, d_off_in, d_v_in, &dc->p_in, d_off_out, d_v_out, s)))
+    return rc;
   Counters h;
-  int64_t Pn = P > 0 ? P : 1;
-  if (stats)
-    for (int k = 0; k < TM_NUM_STATS; k++) stats[k] = 0;
-  if (P <= 0) {
-    CK(cudaMemsetAsync(d_off_out, 0, sizeof(int64_t), s));
-    CK(cudaStreamSynchronize(s));
-    *n_polys_out = 0;
-    *n_slots_out = 0;
-    if (stats) stats[TM_STAT_ROUNDS] = 1;
-    return TM_OK;
-  }
-  ENSURE(item_of, Pn * sizeof(int32_t));
-  ENSURE(items, Pn * sizeof(int32_t));
-  ENSURE(long_list, Pn * sizeof(int32_t));
-  ENSURE(item_list, Pn * sizeof(int64_t));
-  ENSURE(item_n, Pn * sizeof(int32_t));
-  ENSURE(item_slots, Pn * sizeof(int64_t));
-  {
-    SegTimer st_(ctx, S_CLASSIFY, s);
-    launch_classify(d_off_in, d_v_in, P, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(), &dc->n_items,
-                    ctx->long_list.as<int32_t>(), &dc->n_long, dc->stats, s);
-  }
-  CK(cudaGetLastError());
-  int64_t in_slots = 0;
-  CK(cudaMemcpyAsync(&dc->pool_top, d_off_in + P, sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
-  if ((rc = read_counters(ctx, s, &h))) return rc;
-  in_slots = (int64_t)h.pool_top;
-  unsigned int n_items = h.n_items;
-  unsigned long long pool_cap = ctx->pool_cap_hint;
-  unsigned long long want = 4ull * (unsigned long long)in_slots + 64ull * n_items + (1ull << 20);
-  if (pool_cap < want) pool_cap = want;
-  unsigned long long undo_cap = (unsigned long long)T + 1024;
-  ENSURE(undo, undo_cap * sizeof(int32_t));
-  for (int attempt = 0;; attempt++) {
-    if (pool_cap >= (1ull << 32)) return set_err(ctx, TM_ERR_CAPACITY, "[reparation] scratch pool exceeds 2^32 slots");
-    ENSURE(pool, pool_cap * sizeof(int32_t));
-    // reset repair-phase counters but keep classify results (stats[2], stats[6], n_items)
-    CK(cudaMemsetAsync(&dc->pool_top, 0, sizeof(unsigned long long) * 2, s));
-    CK(cudaMemsetAsync(&dc->stats[0], 0, sizeof(unsigned long long) * 2, s));
-    CK(cudaMemsetAsync(&dc->stats[3], 0, sizeof(unsigned long long) * 3, s));
-    RepairArgs a{d_tri32, d_hw, d_tv, T, ctx->pool.as<int32_t>(), pool_cap, &dc->pool_top, ctx->undo.as<int32_t>(),
-                 &dc->undo_top, undo_cap, &dc->st, ctx->items.as<int32_t>(), &dc->n_items, d_off_in, d_v_in,
-                 ctx->item_list.as<int64_t>(), ctx->item_n.as<int32_t>(), ctx->item_slots.as<int64_t>(), dc->stats};
-    if (n_items > 0) {
-      {
-        SegTimer st_(ctx, S_REPAIR_TIPS, s);
-        launch_repair_tips(a, s);
-      }
-      {
-        SegTimer st_(ctx, S_REPAIR_PINCH, s);
-        launch_repair_pinch(a, s);
-      }
-    }
-    CK(cudaGetLastError());
-    if ((rc = read_counters(ctx, s, &h))) return rc;
-    if (h.st.count[K_POOL] && attempt < 6) {
-      if (h.undo_top > undo_cap)
-        return set_err(ctx, TM_ERR_CAPACITY, "[reparation] scratch pool and promotion log both overflowed");
-      launch_undo(d_hw, ctx->undo.as<int32_t>(), &dc->undo_top, undo_cap, s);
-      CK(cudaMemsetAsync(&dc->st, 0, sizeof(DevStatus), s));
-      // DevStatus.first must be ~0: re-reset only the status block
-      Counters z;
-      memset(&z, 0, sizeof z);
-      for (int k = 0; k < K_NUM; k++) z.st.first[k] = ~0ull;
-      memcpy(ctx->pinned_counters.p, &z.st, sizeof z.st);
-      CK(cudaMemcpyAsync(&dc->st, ctx->pinned_counters.p, sizeof z.st, cudaMemcpyHostToDevice, s));
-      CK(cudaStreamSynchronize(s));
-      pool_cap *= 4;
-      ctx->pool_cap_hint = pool_cap;
-      continue;
-    }
-    if ((rc = decode_status(ctx, h.st, "reparation", &h))) return rc;
-    break;
-  }
-  ENSURE(cnt, (Pn + 1) * sizeof(int64_t));
-  ENSURE(slotsz, (Pn + 1) * sizeof(int64_t));
-  ENSURE(pbase, (Pn + 1) * sizeof(int64_t));
-  ENSURE(sbase, (Pn + 1) * sizeof(int64_t));
-  size_t tb = scan_temp_bytes(Pn + 1);
-  ENSURE(temp, tb + 256);
-  SegTimer* stitch_timer = new SegTimer(ctx, S_STITCH, s);
-  launch_out_counts(d_off_in, P, ctx->item_of.as<int32_t>(), ctx->item_n.as<int32_t>(),
-                    ctx->item_slots.as<int64_t>(), ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), s);
-  launch_scan(ctx->cnt.as<int64_t>(), ctx->pbase.as<int64_t>(), P + 1, ctx->temp.p, ctx->temp.bytes, s);
-  launch_scan(ctx->slotsz.as<int64_t>(), ctx->sbase.as<int64_t>(), P + 1, ctx->temp.p, ctx->temp.bytes, s);
-  CK(cudaGetLastError());
-  int64_t tot[2];
-  CK(cudaMemcpyAsync(&tot[0], ctx->pbase.as<int64_t>() + P, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(&tot[1], ctx->sbase.as<int64_t>() + P, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  if (tot[0] > cap_polys || tot[1] > cap_slots) {
-    delete stitch_timer;
-    return set_err(ctx, TM_ERR_CAPACITY, "[reparation] output capacity (%lld polygons, %lld slots) < (%lld, %lld)",
-                   (long long)cap_polys, (long long)cap_slots, (long long)tot[0], (long long)tot[1]);
-  }
-  launch_stitch(d_off_in, d_v_in, P, ctx->item_of.as<int32_t>(), ctx->item_list.as<int64_t>(),
-                ctx->item_n.as<int32_t>(), ctx->pool.as<int32_t>(), ctx->pbase.as<int64_t>(),
-                ctx->sbase.as<int64_t>(), d_off_out, d_v_out, s);
-  delete stitch_timer;
-  CK(cudaGetLastError());
-  *n_polys_out = tot[0];
-  *n_slots_out = tot[1];
-  if (stats) {
-    stats[TM_STAT_ROUNDS] = h.stats[0] > 0 ? (int64_t)h.stats[0] : 1;
-    stats[TM_STAT_SPLITS] = (int64_t)(h.stats[1] + h.stats[4]);
-    stats[TM_STAT_INITIAL_TIPS] = (int64_t)h.stats[2];
-    stats[TM_STAT_UNREPAIRED] = (int64_t)h.stats[3];
-    stats[TM_STAT_NONSIMPLE] = (int64_t)h.stats[6];
-    stats[TM_STAT_TIP_SPLITS] = (int64_t)h.stats[1];
-    stats[TM_STAT_PINCH_SPLITS] = (int64_t)h.stats[4];
-    stats[TM_STAT_WORK_ITEMS] = (int64_t)h.n_items;
-  }
+  rc = finish(ctx, s, &h);
+  if (rc == TM_ERR_CAPACITY)
+    rc = retry_repair(ctx, d_tri32, d_hw, d_tv, T, d_off_in, d_v_in, &dc->p_in, d_off_out, d_v_out, s, &h, rc);
+  if (rc) return rc;
+  *n_polys_out = h.p_out;
+  *n_slots_out = h.f_out;
+  fill_stats(h, stats);
   return TM_OK;
 }
 
+// Whole path on device buffers: one CUDA graph (captured on first use for a
+// given set of pointers/sizes) on the context's stream, ordered after the
+// caller's stream by events.  With profiling on, launches go to the caller's
+// stream one by one so each kernel group can be timed.
 static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_tri, int tri_bits, int64_t T,
-                      int check, int64_t* d_off, int32_t* d_v, int64_t cap_polys, int64_t cap_slots, int64_t* n_polys,
-                      int64_t* n_slots, int64_t* stats, cudaStream_t s) {
+                      int check, int64_t* d_off, int32_t* d_v, int64_t* n_polys, int64_t* n_slots, int64_t* stats,
+                      cudaStream_t user) {
+  int rc = check_sizes(ctx, n, T);
+  if (rc || (rc = prepare(ctx, T))) return rc;
   int64_t Tn = T > 0 ? T : 1, nn = n > 0 ? n : 1;
   ENSURE(tri32, 3 * Tn * sizeof(int32_t));
   ENSURE(hw, 3 * Tn * sizeof(int32_t));
@@ -616,29 +664,79 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
   ENSURE(tv, nn * sizeof(int32_t));
   ENSURE(off0, (Tn + 1) * sizeof(int64_t));
   ENSURE(v0, 3 * Tn * sizeof(int32_t));
+  if (!ctx->gstream) CK(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
   for (auto& e : ctx->ev)
     if (!e) CK(cudaEventCreate(&e));
-  CK(cudaEventRecord(ctx->ev[0], s));
-  int rc = tm_label(ctx, d_xy, n, d_tri, tri_bits, T, check, ctx->tri32.as<int32_t>(), ctx->hw.as<int32_t>(),
-                    ctx->max_edge.as<int8_t>(), ctx->seed.as<uint8_t>(), ctx->tv.as<int32_t>(), s);
+  if (!ctx->ev_in) CK(cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming));
+  if (!ctx->ev_out) CK(cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming));
+  int32_t* tri32 = ctx->tri32.as<int32_t>();
+  int32_t* hw = ctx->hw.as<int32_t>();
+  int32_t* tv = ctx->tv.as<int32_t>();
+  int64_t* off0 = ctx->off0.as<int64_t>();
+  int32_t* v0 = ctx->v0.as<int32_t>();
+  Counters* dc = dc_of(ctx);
+
+  auto body = [&](cudaStream_t s) -> int {
+    int r;
+    if ((r = enqueue_reset(ctx, s))) return r;
+    CK(cudaEventRecordWithFlags(ctx->ev[0], s, cudaEventRecordExternal));
+    if ((r = enqueue_label(ctx, d_xy, n, d_tri, tri_bits, T, check, tri32, hw, ctx->max_edge.as<int8_t>(),
+                           ctx->seed.as<uint8_t>(), tv, s)))
+      return r;
+    CK(cudaEventRecordWithFlags(ctx->ev[1], s, cudaEventRecordExternal));
+    if ((r = enqueue_traverse(ctx, tri32, hw, ctx->seed.as<uint8_t>(), T, off0, v0, s))) return r;
+    CK(cudaEventRecordWithFlags(ctx->ev[2], s, cudaEventRecordExternal));
+    if ((r = enqueue_repair(ctx, tri32, hw, tv, T, off0, v0, &dc->n_seeds, d_off, d_v, s))) return r;
+    CK(cudaEventRecordWithFlags(ctx->ev[3], s, cudaEventRecordExternal));
+    return enqueue_readback(ctx, s);
+  };
+
+  cudaStream_t s = user;
+  if (ctx->use_graph && !ctx->prof.on) {
+    GraphKey key{d_xy, d_tri, d_off, d_v, n, T, tri_bits, check, ctx->pool_cap};
+    if (!ctx->graph || !(key == ctx->gkey)) {
+      if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+      ctx->graph = nullptr;
+      cudaGraph_t g = nullptr;
+      CK(cudaStreamBeginCapture(ctx->gstream, cudaStreamCaptureModeThreadLocal));
+      int r = body(ctx->gstream);
+      cudaError_t e = cudaStreamEndCapture(ctx->gstream, &g);
+      if (r) {
+        if (g) cudaGraphDestroy(g);
+        return r;
+      }
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamEndCapture");
+      e = cudaGraphInstantiate(&ctx->graph, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate");
+      ctx->gkey = key;
+    }
+    CK(cudaEventRecord(ctx->ev_in, user));
+    CK(cudaStreamWaitEvent(ctx->gstream, ctx->ev_in, 0));
+    CK(cudaGraphLaunch(ctx->graph, ctx->gstream));
+    CK(cudaEventRecord(ctx->ev_out, ctx->gstream));
+    CK(cudaStreamWaitEvent(user, ctx->ev_out, 0));
+    s = ctx->gstream;
+  } else {
+    if ((rc = body(s))) return rc;
+  }
+  CK(cudaStreamSynchronize(s));
+  CK(cudaGetLastError());
+  Counters h = *ctx->h_result;
+  rc = decode_status(ctx, h);
+  if (rc == TM_ERR_CAPACITY) {
+    rc = retry_repair(ctx, tri32, hw, tv, T, off0, v0, &dc->n_seeds, d_off, d_v, s, &h, rc);
+    if (ctx->graph) cudaGraphExecDestroy(ctx->graph);  // pool size changed
+    ctx->graph = nullptr;
+  }
   if (rc) return rc;
-  CK(cudaEventRecord(ctx->ev[1], s));
-  int64_t P = 0, F = 0;
-  rc = tm_traverse(ctx, ctx->tri32.as<int32_t>(), ctx->hw.as<int32_t>(), ctx->seed.as<uint8_t>(), T,
-                   ctx->off0.as<int64_t>(), ctx->v0.as<int32_t>(), Tn, 3 * Tn, &P, &F, s);
-  if (rc) return rc;
-  CK(cudaEventRecord(ctx->ev[2], s));
-  rc = tm_repair(ctx, ctx->tri32.as<int32_t>(), ctx->hw.as<int32_t>(), ctx->tv.as<int32_t>(), T,
-                 ctx->off0.as<int64_t>(), ctx->v0.as<int32_t>(), P, d_off, d_v, cap_polys, cap_slots, n_polys, n_slots,
-                 stats, s);
-  if (rc) return rc;
-  CK(cudaEventRecord(ctx->ev[3], s));
-  CK(cudaEventSynchronize(ctx->ev[3]));
   for (int k = 0; k < 3; k++) {
     float ms = 0;
-    CK(cudaEventElapsedTime(&ms, ctx->ev[k], ctx->ev[k + 1]));
-    ctx->phase_ms[k] = ms;
+    if (cudaEventElapsedTime(&ms, ctx->ev[k], ctx->ev[k + 1]) == cudaSuccess) ctx->phase_ms[k] = ms;
   }
+  *n_polys = h.p_out;
+  *n_slots = h.f_out;
+  fill_stats(h, stats);
   return TM_OK;
 }
 
@@ -646,39 +744,38 @@ int tm_mesh_to_polygons(tm_ctx* ctx, const double* d_xy, int64_t n, const void* 
                         int check, int64_t* d_off, int32_t* d_v, int64_t cap_polys, int64_t cap_slots,
                         int64_t* n_polys, int64_t* n_slots, int64_t* stats, void* stream) {
   if (!ctx || !n_polys || !n_slots) return TM_ERR_ARGUMENT;
-  return run_device(ctx, d_xy, n, d_tri, tri_bits, T, check, d_off, d_v, cap_polys, cap_slots, n_polys, n_slots,
-                    stats, (cudaStream_t)stream);
+  if (tri_bits != 32 && tri_bits != 64) return set_err(ctx, TM_ERR_ARGUMENT, "tri_bits must be 32 or 64");
+  if (cap_polys < T || cap_slots < 3 * T)
+    return set_err(ctx, TM_ERR_ARGUMENT, "output capacities must be at least T polygons and 3T slots");
+  return run_device(ctx, d_xy, n, d_tri, tri_bits, T, check, d_off, d_v, n_polys, n_slots, stats,
+                    (cudaStream_t)stream);
 }
 
 int tm_mesh_to_polygons_host(tm_ctx* ctx, const double* h_xy, int64_t n, const int64_t* h_tri, int64_t T, int check,
                              int64_t* h_off, int32_t* h_v, int64_t cap_polys, int64_t cap_slots, int64_t* n_polys,
                              int64_t* n_slots, int64_t* stats) {
   if (!ctx || !n_polys || !n_slots || (!h_xy && n) || (!h_tri && T)) return TM_ERR_ARGUMENT;
-  if (!ctx->own_stream) CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
-  cudaStream_t s = ctx->own_stream;
+  int rc = check_sizes(ctx, n, T);
+  if (rc) return rc;
+  if (!ctx->gstream) CK(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
+  cudaStream_t s = ctx->gstream;
   int64_t Tn = T > 0 ? T : 1, nn = n > 0 ? n : 1;
   ENSURE(xy, 2 * nn * sizeof(double));
   ENSURE(tri, 3 * Tn * sizeof(int64_t));
-  CK(cudaMemcpyAsync(ctx->xy.p, h_xy, 2 * n * sizeof(double), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(ctx->tri.p, h_tri, 3 * T * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-  // final CSR goes to device buffers sized by the bounds, then to host
   ENSURE(fin_off, (Tn + 1) * sizeof(int64_t));
   ENSURE(fin_v, 3 * Tn * sizeof(int32_t));
-  Buf& out_off = ctx->fin_off;
-  Buf& out_v = ctx->fin_v;
-  int rc = run_device(ctx, ctx->xy.as<double>(), n, ctx->tri.p, 64, T, check, out_off.as<int64_t>(),
-                      out_v.as<int32_t>(), Tn, 3 * Tn, n_polys, n_slots, stats, s);
-  if (rc == TM_OK) {
-    if (*n_polys + 1 > cap_polys + 1 || *n_slots > cap_slots) {
-      rc = set_err(ctx, TM_ERR_CAPACITY, "host output capacity too small");
-    } else {
-      cudaError_t e1 = cudaMemcpyAsync(h_off, out_off.p, (*n_polys + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-      cudaError_t e2 = cudaMemcpyAsync(h_v, out_v.p, *n_slots * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-      cudaError_t e3 = cudaStreamSynchronize(s);
-      if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) rc = cuda_fail(ctx, e3 != cudaSuccess ? e3 : (e1 != cudaSuccess ? e1 : e2), "D2H");
-    }
-  }
-  return rc;
+  CK(cudaMemcpyAsync(ctx->xy.p, h_xy, 2 * n * sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ctx->tri.p, h_tri, 3 * T * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  rc = run_device(ctx, ctx->xy.as<double>(), n, ctx->tri.p, 64, T, check, ctx->fin_off.as<int64_t>(),
+                  ctx->fin_v.as<int32_t>(), n_polys, n_slots, stats, s);
+  if (rc) return rc;
+  if (*n_polys > cap_polys || *n_slots > cap_slots)
+    return set_err(ctx, TM_ERR_CAPACITY, "host output capacity too small (%lld polygons, %lld slots needed)",
+                   (long long)*n_polys, (long long)*n_slots);
+  CK(cudaMemcpyAsync(h_off, ctx->fin_off.p, (*n_polys + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h_v, ctx->fin_v.p, *n_slots * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return TM_OK;
 }
 
 }  // extern "C"

@@ -23,24 +23,29 @@ void launch_check_neighbors(const int32_t* hw, const void* nb, int nb_is64, int6
 void launch_unpack(const int32_t* hw, int64_t T, int32_t* twin, uint8_t* fr, cudaStream_t s);
 void launch_pack_frontier(int32_t* hw, int64_t T, const uint8_t* fr, cudaStream_t s);
 
-// tm_traverse.cu
-size_t select_seeds_temp_bytes(int64_t T);
-void launch_select_seeds(const uint8_t* seed, int64_t T, int32_t* seeds, int64_t* n_seeds, void* temp,
-                         size_t temp_bytes, cudaStream_t s);
-size_t scan_temp_bytes(int64_t n);
-void launch_scan(const int64_t* in, int64_t* out, int64_t n, void* temp, size_t temp_bytes, cudaStream_t s);
-void launch_trav_start(const int32_t* hw, const int32_t* seeds, int64_t P, int32_t* start, int32_t* overflow,
-                       unsigned int* n_overflow, int32_t* queue, int32_t* stamp, uint32_t* bits, DevStatus* st,
-                       cudaStream_t s);
+// tm_scan.cu (device-count scans / compaction)
+size_t scan_scratch_elems(int64_t n_cap);
+void launch_scan_dev(const int64_t* in, int64_t* out, const int64_t* n_dev, int64_t n_cap, int64_t* tile_sums,
+                     cudaStream_t s);
+void launch_gather_at(const int64_t* arr, const int64_t* idx, int64_t* dst, cudaStream_t s);
+void launch_select_flags(const uint8_t* flag, int64_t n, int32_t* out, int64_t* n_out, int64_t* tile_sums,
+                         cudaStream_t s);
+
+// tm_traverse.cu (Pp = device count, Pcap = host bound for the grid)
+void launch_trav_start(const int32_t* hw, const int32_t* seeds, const int64_t* Pp, int64_t Pcap, int32_t* start,
+                       int32_t* overflow, unsigned int* n_overflow, int32_t* queue, int32_t* stamp, uint32_t* bits,
+                       DevStatus* st, cudaStream_t s);
 void launch_ruler_walk(const int32_t* hw, const uint32_t* bits, int64_t T, int32_t* rnext, int32_t* rdist,
                        DevStatus* st, cudaStream_t s);
-void launch_chain_count(const int32_t* seeds, const int32_t* start, int64_t P, int64_t T, const int32_t* rnext,
-                        const int32_t* rdist, int64_t* len, int64_t* nrul, DevStatus* st, cudaStream_t s);
-void launch_chain_emit(const int32_t* start, int64_t P, const int32_t* rnext, const int32_t* rdist,
-                       const int64_t* offsets, const int64_t* eoff, int32_t* ent_r, int64_t* ent_base,
-                       cudaStream_t s);
+void launch_chain_count(const int32_t* seeds, const int32_t* start, const int64_t* Pp, int64_t Pcap, int64_t T,
+                        const int32_t* rnext, const int32_t* rdist, int64_t* len, int64_t* nrul, DevStatus* st,
+                        cudaStream_t s);
+void launch_chain_emit(const int32_t* start, const int64_t* Pp, int64_t Pcap, const int32_t* rnext,
+                       const int32_t* rdist, const int64_t* offsets, const int64_t* eoff, int32_t* ent_r,
+                       int64_t* ent_base, int64_t ecap, DevStatus* st, cudaStream_t s);
 void launch_ruler_write(const int32_t* tri, const int32_t* hw, const int64_t* n_entries, const int32_t* ent_r,
-                        const int64_t* ent_base, const int32_t* rdist, int64_t T, int32_t* verts, cudaStream_t s);
+                        const int64_t* ent_base, const int32_t* rdist, int64_t T, int64_t ecap, int32_t* verts,
+                        cudaStream_t s);
 
 // tm_repair.cu
 struct RepairArgs {
@@ -64,16 +69,19 @@ struct RepairArgs {
   int64_t* item_slots;
   unsigned long long* stats;
 };
-void launch_classify(const int64_t* off, const int32_t* v, int64_t P, int32_t* item_of, int32_t* items,
-                     unsigned int* n_items, int32_t* long_list, unsigned int* n_long, unsigned long long* stats,
-                     cudaStream_t s);
+void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, int32_t* item_of,
+                     int32_t* items, unsigned int* n_items, int32_t* long_list, unsigned int* n_long,
+                     unsigned long long* stats, cudaStream_t s);
 void launch_repair_tips(const RepairArgs& a, cudaStream_t s);
 void launch_repair_pinch(const RepairArgs& a, cudaStream_t s);
-void launch_out_counts(const int64_t* off, int64_t P, const int32_t* item_of, const int32_t* item_n,
-                       const int64_t* item_slots, int64_t* cnt, int64_t* slots, cudaStream_t s);
-void launch_stitch(const int64_t* off, const int32_t* v, int64_t P, const int32_t* item_of, const int64_t* item_list,
-                   const int32_t* item_n, const int32_t* pool, const int64_t* pbase, const int64_t* sbase,
-                   int64_t* off_out, int32_t* v_out, cudaStream_t s);
+void launch_out_counts(const int64_t* off, const int64_t* Pp, int64_t Pcap, const int32_t* item_of,
+                       const int32_t* item_n, const int64_t* item_slots, int64_t* cnt, int64_t* slots,
+                       cudaStream_t s);
+void launch_stitch(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, const int32_t* item_of,
+                   const int64_t* item_list, const int32_t* item_n, const int32_t* pool, const int64_t* pbase,
+                   const int64_t* sbase, int64_t* off_out, int32_t* v_out, cudaStream_t s);
+void launch_finalize(const int64_t* Pp, const int64_t* pbase, const int64_t* sbase, int64_t* off_out,
+                     int64_t* p_out, int64_t* f_out, cudaStream_t s);
 void launch_undo(int32_t* hw, const int32_t* undo, const unsigned long long* undo_top, unsigned long long cap,
                  cudaStream_t s);
 

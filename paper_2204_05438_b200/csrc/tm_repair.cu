@@ -22,8 +22,6 @@
 // Piece records live in a device pool (bump allocated): {offset, len|flags}.
 // Every promoted half-edge is appended to an undo log, so a pool overflow can
 // be rolled back and retried by the host with a larger pool.
-#include <cub/device/device_scan.cuh>
-
 #include "tm_common.cuh"
 #include "tm_internal.h"
 
@@ -126,10 +124,11 @@ __device__ int64_t extra_visits(const int32_t* s, int64_t n, int32_t* scratch) {
 // Per input polygon: tip flag, repeated flag, extra visits.  Work items are the
 // polygons with a repeated vertex (a tip implies one).
 __global__ void __launch_bounds__(256) k_classify(const int64_t* __restrict__ off, const int32_t* __restrict__ v,
-                                                  int64_t P, int32_t* __restrict__ item_of,
+                                                  const int64_t* __restrict__ Pp, int32_t* __restrict__ item_of,
                                                   int32_t* __restrict__ items, unsigned int* n_items,
                                                   int32_t* __restrict__ long_list, unsigned int* n_long,
                                                   unsigned long long* stats) {
+  const int64_t P = *Pp;
   unsigned long long extra_sum = 0, rep_cnt = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t b = off[i], n = off[i + 1] - b;
@@ -780,10 +779,11 @@ __global__ void __launch_bounds__(128) k_repair_pinch(RepairCtx c, const int32_t
 }
 
 // ------------------------------------------------------------ stitch
-__global__ void __launch_bounds__(256) k_out_counts(const int64_t* __restrict__ off, int64_t P,
+__global__ void __launch_bounds__(256) k_out_counts(const int64_t* __restrict__ off, const int64_t* __restrict__ Pp,
                                                     const int32_t* __restrict__ item_of, const int32_t* __restrict__ item_n,
                                                     const int64_t* __restrict__ item_slots, int64_t* __restrict__ cnt,
                                                     int64_t* __restrict__ slots) {
+  const int64_t P = *Pp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= P; i += (int64_t)gridDim.x * blockDim.x) {
     if (i == P) { cnt[i] = 0; slots[i] = 0; continue; }
     int32_t it = item_of[i];
@@ -792,11 +792,12 @@ __global__ void __launch_bounds__(256) k_out_counts(const int64_t* __restrict__ 
   }
 }
 
-__global__ void __launch_bounds__(256) k_stitch(const int64_t* __restrict__ off, const int32_t* __restrict__ v, int64_t P,
+__global__ void __launch_bounds__(256) k_stitch(const int64_t* __restrict__ off, const int32_t* __restrict__ v, const int64_t* __restrict__ Pp,
                                                 const int32_t* __restrict__ item_of, const int64_t* __restrict__ item_list,
                                                 const int32_t* __restrict__ item_n, const int32_t* __restrict__ pool,
                                                 const int64_t* __restrict__ pbase, const int64_t* __restrict__ sbase,
                                                 int64_t* __restrict__ off_out, int32_t* __restrict__ v_out) {
+  const int64_t P = *Pp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t it = item_of[i];
     int64_t pb = pbase[i], sb = sbase[i];
@@ -820,6 +821,16 @@ __global__ void __launch_bounds__(256) k_stitch(const int64_t* __restrict__ off,
   }
 }
 
+__global__ void k_finalize(const int64_t* __restrict__ Pp, const int64_t* __restrict__ pbase,
+                           const int64_t* __restrict__ sbase, int64_t* __restrict__ off_out, int64_t* p_out,
+                           int64_t* f_out) {
+  if (threadIdx.x || blockIdx.x) return;
+  int64_t P = *Pp;
+  off_out[pbase[P]] = sbase[P];
+  *p_out = pbase[P];
+  *f_out = sbase[P];
+}
+
 __global__ void k_undo(int32_t* hw, const int32_t* undo, const unsigned long long* undo_top, unsigned long long cap) {
   unsigned long long n = *undo_top;
   if (n > cap) n = cap;
@@ -839,11 +850,10 @@ static inline int grid_for(int64_t n, int block) {
   return (int)(g < 1 ? 1 : g);
 }
 
-void launch_classify(const int64_t* off, const int32_t* v, int64_t P, int32_t* item_of, int32_t* items,
-                     unsigned int* n_items, int32_t* long_list, unsigned int* n_long, unsigned long long* stats,
-                     cudaStream_t s) {
-  if (P <= 0) return;
-  k_classify<<<grid_for(P, 256), 256, 0, s>>>(off, v, P, item_of, items, n_items, long_list, n_long, stats);
+void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, int32_t* item_of,
+                     int32_t* items, unsigned int* n_items, int32_t* long_list, unsigned int* n_long,
+                     unsigned long long* stats, cudaStream_t s) {
+  k_classify<<<grid_for(Pcap, 256), 256, 0, s>>>(off, v, Pp, item_of, items, n_items, long_list, n_long, stats);
   note_launch(1);
   k_classify_long<<<kNumSMs * 4, 256, 0, s>>>(off, v, long_list, n_long, item_of, items, n_items, stats);
   note_launch(1);
@@ -861,17 +871,24 @@ void launch_repair_pinch(const RepairArgs& a, cudaStream_t s) {
   note_launch(1);
 }
 
-void launch_out_counts(const int64_t* off, int64_t P, const int32_t* item_of, const int32_t* item_n,
-                       const int64_t* item_slots, int64_t* cnt, int64_t* slots, cudaStream_t s) {
-  k_out_counts<<<grid_for(P + 1, 256), 256, 0, s>>>(off, P, item_of, item_n, item_slots, cnt, slots);
+void launch_out_counts(const int64_t* off, const int64_t* Pp, int64_t Pcap, const int32_t* item_of,
+                       const int32_t* item_n, const int64_t* item_slots, int64_t* cnt, int64_t* slots,
+                       cudaStream_t s) {
+  k_out_counts<<<grid_for(Pcap + 1, 256), 256, 0, s>>>(off, Pp, item_of, item_n, item_slots, cnt, slots);
   note_launch(1);
 }
 
-void launch_stitch(const int64_t* off, const int32_t* v, int64_t P, const int32_t* item_of, const int64_t* item_list,
-                   const int32_t* item_n, const int32_t* pool, const int64_t* pbase, const int64_t* sbase,
-                   int64_t* off_out, int32_t* v_out, cudaStream_t s) {
-  if (P <= 0) return;
-  k_stitch<<<grid_for(P, 256), 256, 0, s>>>(off, v, P, item_of, item_list, item_n, pool, pbase, sbase, off_out, v_out);
+void launch_stitch(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, const int32_t* item_of,
+                   const int64_t* item_list, const int32_t* item_n, const int32_t* pool, const int64_t* pbase,
+                   const int64_t* sbase, int64_t* off_out, int32_t* v_out, cudaStream_t s) {
+  k_stitch<<<grid_for(Pcap, 256), 256, 0, s>>>(off, v, Pp, item_of, item_list, item_n, pool, pbase, sbase, off_out,
+                                               v_out);
+  note_launch(1);
+}
+
+void launch_finalize(const int64_t* Pp, const int64_t* pbase, const int64_t* sbase, int64_t* off_out,
+                     int64_t* p_out, int64_t* f_out, cudaStream_t s) {
+  k_finalize<<<1, 32, 0, s>>>(Pp, pbase, sbase, off_out, p_out, f_out);
   note_launch(1);
 }
 

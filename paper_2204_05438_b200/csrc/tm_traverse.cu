@@ -14,10 +14,6 @@
 // boundary steps); (2) every seed follows its ruler chain (L/8 links) for the
 // polygon length and the ruler offsets; (3) scan; (4) every ruler on a seed
 // cycle writes its run.  Critical path ~ max ruler gap + L/8 instead of L.
-#include <cub/device/device_scan.cuh>
-#include <cub/device/device_select.cuh>
-#include <thrust/iterator/counting_iterator.h>
-
 #include "tm_common.cuh"
 #include "tm_internal.h"
 
@@ -59,9 +55,10 @@ __device__ __forceinline__ bool sampled(int32_t h) { return ((uint32_t)h * 0x9E3
 __device__ __forceinline__ bool is_ruler(const uint32_t* bits, int32_t h) { return sampled(h) || is_start(bits, h); }
 
 __global__ void __launch_bounds__(256) k_trav_start(const int32_t* __restrict__ hw, const int32_t* __restrict__ seeds,
-                                                    int64_t P, int32_t* __restrict__ start,
+                                                    const int64_t* __restrict__ Pp, int32_t* __restrict__ start,
                                                     int32_t* __restrict__ overflow, unsigned int* n_overflow,
                                                     uint32_t* __restrict__ bits, DevStatus* st) {
+  const int64_t P = *Pp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t t = seeds[i];
     int32_t h = seed_start(hw, t);
@@ -120,9 +117,10 @@ __global__ void __launch_bounds__(256) k_ruler_walk(const int32_t* __restrict__ 
 
 // (2a) polygon length and ruler count per seed (traversal.py:264-281)
 __global__ void __launch_bounds__(256) k_chain_count(const int32_t* __restrict__ seeds, const int32_t* __restrict__ start,
-                                                     int64_t P, long long limit, const int32_t* __restrict__ rnext,
+                                                     const int64_t* __restrict__ Pp, long long limit, const int32_t* __restrict__ rnext,
                                                      const int32_t* __restrict__ rdist, int64_t* __restrict__ len,
                                                      int64_t* __restrict__ nrul, DevStatus* st) {
+  const int64_t P = *Pp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t h0 = start[i], r = h0;
     long long L = 0, cnt = 0;
@@ -140,13 +138,16 @@ __global__ void __launch_bounds__(256) k_chain_count(const int32_t* __restrict__
 }
 
 // (2b) emit (ruler, absolute output offset) entries in chain order
-__global__ void __launch_bounds__(256) k_chain_emit(const int32_t* __restrict__ start, int64_t P,
+__global__ void __launch_bounds__(256) k_chain_emit(const int32_t* __restrict__ start, const int64_t* __restrict__ Pp,
                                                     const int32_t* __restrict__ rnext, const int32_t* __restrict__ rdist,
                                                     const int64_t* __restrict__ offsets, const int64_t* __restrict__ eoff,
-                                                    int32_t* __restrict__ ent_r, int64_t* __restrict__ ent_base) {
+                                                    int32_t* __restrict__ ent_r, int64_t* __restrict__ ent_base,
+                                                    int64_t ecap, DevStatus* st) {
+  const int64_t P = *Pp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t k = eoff[i], kend = eoff[i + 1], pos = offsets[i];
     int32_t r = start[i];
+    if (kend > ecap) { report(st, K_STRUCT, i); continue; }
     for (; k < kend; k++) {
       ent_r[k] = r;
       ent_base[k] = pos;
@@ -162,8 +163,9 @@ __global__ void __launch_bounds__(256) k_ruler_write(const int32_t* __restrict__
                                                      const int32_t* __restrict__ ent_r,
                                                      const int64_t* __restrict__ ent_base,
                                                      const int32_t* __restrict__ rdist, long long limit,
-                                                     int32_t* __restrict__ verts) {
+                                                     int64_t ecap, int32_t* __restrict__ verts) {
   int64_t E = *n_entries;
+  if (E > ecap) E = ecap;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < E; k += (int64_t)gridDim.x * blockDim.x) {
     int32_t g = ent_r[k];
     int64_t w = ent_base[k];
@@ -182,34 +184,11 @@ static inline int grid_for(int64_t n, int block) {
   return (int)(g < 1 ? 1 : g);
 }
 
-size_t select_seeds_temp_bytes(int64_t T) {
-  size_t bytes = 0;
-  thrust::counting_iterator<int32_t> it(0);
-  cub::DeviceSelect::Flagged(nullptr, bytes, it, (const uint8_t*)nullptr, (int32_t*)nullptr, (int64_t*)nullptr, (int)T);
-  return bytes;
-}
-
-void launch_select_seeds(const uint8_t* seed, int64_t T, int32_t* seeds, int64_t* n_seeds, void* temp, size_t temp_bytes,
-                         cudaStream_t s) {
-  thrust::counting_iterator<int32_t> it(0);
-  cub::DeviceSelect::Flagged(temp, temp_bytes, it, seed, seeds, n_seeds, (int)T, s);
-}
-
-size_t scan_temp_bytes(int64_t n) {
-  size_t bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const int64_t*)nullptr, (int64_t*)nullptr, (int)n);
-  return bytes;
-}
-
-void launch_scan(const int64_t* in, int64_t* out, int64_t n, void* temp, size_t temp_bytes, cudaStream_t s) {
-  cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, out, (int)n, s);
-}
-
-void launch_trav_start(const int32_t* hw, const int32_t* seeds, int64_t P, int32_t* start, int32_t* overflow,
-                       unsigned int* n_overflow, int32_t* queue, int32_t* stamp, uint32_t* bits, DevStatus* st,
-                       cudaStream_t s) {
-  if (P <= 0) return;
-  k_trav_start<<<grid_for(P, 256), 256, 0, s>>>(hw, seeds, P, start, overflow, n_overflow, bits, st);
+// Pp: device polygon (seed) count; Pcap: host upper bound used for the grid.
+void launch_trav_start(const int32_t* hw, const int32_t* seeds, const int64_t* Pp, int64_t Pcap, int32_t* start,
+                       int32_t* overflow, unsigned int* n_overflow, int32_t* queue, int32_t* stamp, uint32_t* bits,
+                       DevStatus* st, cudaStream_t s) {
+  k_trav_start<<<grid_for(Pcap, 256), 256, 0, s>>>(hw, seeds, Pp, start, overflow, n_overflow, bits, st);
   k_bfs_slow<<<1, 32, 0, s>>>(hw, seeds, start, overflow, n_overflow, queue, stamp, bits, st);
   note_launch(2);
 }
@@ -221,24 +200,25 @@ void launch_ruler_walk(const int32_t* hw, const uint32_t* bits, int64_t T, int32
   note_launch(1);
 }
 
-void launch_chain_count(const int32_t* seeds, const int32_t* start, int64_t P, int64_t T, const int32_t* rnext,
-                        const int32_t* rdist, int64_t* len, int64_t* nrul, DevStatus* st, cudaStream_t s) {
-  if (P <= 0) return;
-  k_chain_count<<<grid_for(P, 256), 256, 0, s>>>(seeds, start, P, 3 * T + 3, rnext, rdist, len, nrul, st);
+void launch_chain_count(const int32_t* seeds, const int32_t* start, const int64_t* Pp, int64_t Pcap, int64_t T,
+                        const int32_t* rnext, const int32_t* rdist, int64_t* len, int64_t* nrul, DevStatus* st,
+                        cudaStream_t s) {
+  k_chain_count<<<grid_for(Pcap, 256), 256, 0, s>>>(seeds, start, Pp, 3 * T + 3, rnext, rdist, len, nrul, st);
   note_launch(1);
 }
 
-void launch_chain_emit(const int32_t* start, int64_t P, const int32_t* rnext, const int32_t* rdist,
-                       const int64_t* offsets, const int64_t* eoff, int32_t* ent_r, int64_t* ent_base,
-                       cudaStream_t s) {
-  if (P <= 0) return;
-  k_chain_emit<<<grid_for(P, 256), 256, 0, s>>>(start, P, rnext, rdist, offsets, eoff, ent_r, ent_base);
+void launch_chain_emit(const int32_t* start, const int64_t* Pp, int64_t Pcap, const int32_t* rnext,
+                       const int32_t* rdist, const int64_t* offsets, const int64_t* eoff, int32_t* ent_r,
+                       int64_t* ent_base, int64_t ecap, DevStatus* st, cudaStream_t s) {
+  k_chain_emit<<<grid_for(Pcap, 256), 256, 0, s>>>(start, Pp, rnext, rdist, offsets, eoff, ent_r, ent_base, ecap,
+                                                   st);
   note_launch(1);
 }
 
 void launch_ruler_write(const int32_t* tri, const int32_t* hw, const int64_t* n_entries, const int32_t* ent_r,
-                        const int64_t* ent_base, const int32_t* rdist, int64_t T, int32_t* verts, cudaStream_t s) {
-  k_ruler_write<<<kNumSMs * 16, 256, 0, s>>>(tri, hw, n_entries, ent_r, ent_base, rdist, 3 * T + 3, verts);
+                        const int64_t* ent_base, const int32_t* rdist, int64_t T, int64_t ecap, int32_t* verts,
+                        cudaStream_t s) {
+  k_ruler_write<<<kNumSMs * 16, 256, 0, s>>>(tri, hw, n_entries, ent_r, ent_base, rdist, 3 * T + 3, ecap, verts);
   note_launch(1);
 }
 
