@@ -123,6 +123,7 @@ struct tm_ctx {
   unsigned long long pool_cap = 0;
   int64_t ecap = 0;
   int use_graph = 1;
+  long long graph_kernels = 0;  // kernels per graph replay (counted at capture)
 };
 
 static int set_err(tm_ctx* c, int code, const char* fmt, ...) {
@@ -676,18 +677,23 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
   int32_t* v0 = ctx->v0.as<int32_t>();
   Counters* dc = dc_of(ctx);
 
+  bool capturing = false;
+  // external event nodes inside a capture, plain records otherwise
+  auto rec = [&](cudaEvent_t e, cudaStream_t s) {
+    return capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s);
+  };
   auto body = [&](cudaStream_t s) -> int {
     int r;
     if ((r = enqueue_reset(ctx, s))) return r;
-    CK(cudaEventRecordWithFlags(ctx->ev[0], s, cudaEventRecordExternal));
+    CK(rec(ctx->ev[0], s));
     if ((r = enqueue_label(ctx, d_xy, n, d_tri, tri_bits, T, check, tri32, hw, ctx->max_edge.as<int8_t>(),
                            ctx->seed.as<uint8_t>(), tv, s)))
       return r;
-    CK(cudaEventRecordWithFlags(ctx->ev[1], s, cudaEventRecordExternal));
+    CK(rec(ctx->ev[1], s));
     if ((r = enqueue_traverse(ctx, tri32, hw, ctx->seed.as<uint8_t>(), T, off0, v0, s))) return r;
-    CK(cudaEventRecordWithFlags(ctx->ev[2], s, cudaEventRecordExternal));
+    CK(rec(ctx->ev[2], s));
     if ((r = enqueue_repair(ctx, tri32, hw, tv, T, off0, v0, &dc->n_seeds, d_off, d_v, s))) return r;
-    CK(cudaEventRecordWithFlags(ctx->ev[3], s, cudaEventRecordExternal));
+    CK(rec(ctx->ev[3], s));
     return enqueue_readback(ctx, s);
   };
 
@@ -698,9 +704,14 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
       if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
       ctx->graph = nullptr;
       cudaGraph_t g = nullptr;
+      long long k0 = g_launches.load();
       CK(cudaStreamBeginCapture(ctx->gstream, cudaStreamCaptureModeThreadLocal));
+      capturing = true;
       int r = body(ctx->gstream);
+      capturing = false;
       cudaError_t e = cudaStreamEndCapture(ctx->gstream, &g);
+      ctx->graph_kernels = g_launches.load() - k0;
+      g_launches.fetch_sub(ctx->graph_kernels);  // captured, not launched
       if (r) {
         if (g) cudaGraphDestroy(g);
         return r;
@@ -714,6 +725,7 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
     CK(cudaEventRecord(ctx->ev_in, user));
     CK(cudaStreamWaitEvent(ctx->gstream, ctx->ev_in, 0));
     CK(cudaGraphLaunch(ctx->graph, ctx->gstream));
+    g_launches.fetch_add(ctx->graph_kernels);
     CK(cudaEventRecord(ctx->ev_out, ctx->gstream));
     CK(cudaStreamWaitEvent(user, ctx->ev_out, 0));
     s = ctx->gstream;
