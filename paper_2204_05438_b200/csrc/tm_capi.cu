@@ -421,9 +421,9 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
     launch_scan_dev(ctx->cnt.as<int64_t>(), ctx->pbase.as<int64_t>(), Pp, Tn, tiles, s);
     launch_scan_dev(ctx->slotsz.as<int64_t>(), ctx->sbase.as<int64_t>(), Pp, Tn, tiles, s);
     launch_finalize(Pp, ctx->pbase.as<int64_t>(), ctx->sbase.as<int64_t>(), d_off_out, &dc->p_out, &dc->f_out, s);
-    launch_stitch(d_off_in, d_v_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->item_list.as<int64_t>(),
-                  ctx->item_n.as<int32_t>(), ctx->pool.as<int32_t>(), ctx->pbase.as<int64_t>(),
-                  ctx->sbase.as<int64_t>(), d_off_out, d_v_out, s);
+    launch_stitch(d_off_in, d_v_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(), &dc->n_items,
+                  ctx->item_list.as<int64_t>(), ctx->item_n.as<int32_t>(), ctx->pool.as<int32_t>(),
+                  ctx->pbase.as<int64_t>(), ctx->sbase.as<int64_t>(), d_off_out, d_v_out, s);
   }
   CK(cudaGetLastError());
   return TM_OK;

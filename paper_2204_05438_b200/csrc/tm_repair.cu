@@ -285,16 +285,49 @@ constexpr int kTipWarps = 4;  // warps per block of k_repair_tips
 
 __device__ __forceinline__ int wrap_idx(int x, int n) { return x >= n ? x - n : (x < 0 ? x + n : x); }
 
-// first position p (cyclic triple s[p-1] == s[p+1]) or -1 (reparation.py:59-71)
-__device__ int warp_first_tip(const int32_t* s, int n, int lane) {
-  for (int base = 0; base < n; base += 32) {
-    int p = base + lane;
-    bool t = false;
-    if (p < n) t = s[p == 0 ? n - 1 : p - 1] == s[p + 1 == n ? 0 : p + 1];
-    unsigned m = __ballot_sync(kFull, t);
-    if (m) return base + __ffs(m) - 1;
+// Smallest p in [0, n) with pred(p), or -1.  Eight 32-wide chunks per round
+// so their loads are in flight together (one memory round trip per 256).
+constexpr int kScanUnroll = 8;
+template <typename Pred>
+__device__ __forceinline__ int warp_find_first(int n, int lane, Pred pred) {
+  for (int base = 0; base < n; base += 32 * kScanUnroll) {
+    bool hit[kScanUnroll];
+#pragma unroll
+    for (int c = 0; c < kScanUnroll; c++) {
+      int p = base + c * 32 + lane;
+      hit[c] = p < n && pred(p);
+    }
+#pragma unroll
+    for (int c = 0; c < kScanUnroll; c++) {
+      unsigned m = __ballot_sync(kFull, hit[c]);
+      if (m) return base + c * 32 + __ffs(m) - 1;
+    }
   }
   return -1;
+}
+
+// dst[k] = src(k) for k in [0, n), values staged in registers so the loads of
+// eight elements per lane are in flight together.
+template <typename Src>
+__device__ __forceinline__ void warp_copy(int32_t* dst, int n, int lane, Src src) {
+  for (int base = 0; base < n; base += 32 * kScanUnroll) {
+    int32_t buf[kScanUnroll];
+#pragma unroll
+    for (int c = 0; c < kScanUnroll; c++) {
+      int k = base + c * 32 + lane;
+      if (k < n) buf[c] = src(k);
+    }
+#pragma unroll
+    for (int c = 0; c < kScanUnroll; c++) {
+      int k = base + c * 32 + lane;
+      if (k < n) dst[k] = buf[c];
+    }
+  }
+}
+
+// first position p (cyclic triple s[p-1] == s[p+1]) or -1 (reparation.py:59-71)
+__device__ int warp_first_tip(const int32_t* s, int n, int lane) {
+  return warp_find_first(n, lane, [&](int p) { return s[p == 0 ? n - 1 : p - 1] == s[p + 1 == n ? 0 : p + 1]; });
 }
 
 // (len - distinct) of s[0..n) (traversal.py:140-147), quadratic over lanes
@@ -416,14 +449,8 @@ __device__ bool warp_split_tip(const RepairCtx& c, const int32_t* X, int L, int3
   }
   a_in = __shfl_sync(kFull, a_in, 0);
   int j = -1;
-  if (a_in >= 0) {
-    for (int base = 0; base < L && j < 0; base += 32) {
-      int q = base + lane;
-      bool hit = q < L && X[q] == u && X[q == 0 ? L - 1 : q - 1] == a_in;
-      unsigned m = __ballot_sync(kFull, hit);
-      if (m) j = base + __ffs(m) - 1;
-    }
-  }
+  if (a_in >= 0)
+    j = warp_find_first(L, lane, [&](int q) { return X[q] == u && X[q == 0 ? L - 1 : q - 1] == a_in; });
   int32_t oa = 0, ga = 0, ob = 0, gb = 0;
   if (lane == 0) {
     promote(c, e, te);
@@ -437,31 +464,10 @@ __device__ bool warp_split_tip(const RepairCtx& c, const int32_t* X, int L, int3
   if (j >= 0) {
     int la = 1 + wrap_idx(pos - j, L), lb = wrap_idx(j - pos, L) + 1;
     // pa arc: A(0) = v, A(k) = X[(j+k-1) % L]; pb arc: B(k) = X[(pos+k) % L] (k < lb-1), B(lb-1) = u
-    int ka = -1, kb = -1;
-    for (int base = 0; base < la && ka < 0; base += 32) {
-      int k = base + lane;
-      bool hit = false;
-      if (k < la) {
-        int k1 = k + 1 == la ? 0 : k + 1;
-        int32_t x0 = k == 0 ? v : X[wrap_idx(j + k - 1, L)];
-        int32_t x1 = k1 == 0 ? v : X[wrap_idx(j + k1 - 1, L)];
-        hit = x0 == oa && x1 == ga;
-      }
-      unsigned m = __ballot_sync(kFull, hit);
-      if (m) ka = base + __ffs(m) - 1;
-    }
-    for (int base = 0; base < lb && kb < 0; base += 32) {
-      int k = base + lane;
-      bool hit = false;
-      if (k < lb) {
-        int k1 = k + 1 == lb ? 0 : k + 1;
-        int32_t x0 = k == lb - 1 ? u : X[wrap_idx(pos + k, L)];
-        int32_t x1 = k1 == lb - 1 ? u : X[wrap_idx(pos + k1, L)];
-        hit = x0 == ob && x1 == gb;
-      }
-      unsigned m = __ballot_sync(kFull, hit);
-      if (m) kb = base + __ffs(m) - 1;
-    }
+    auto A_at = [&](int k) { return k == 0 ? v : X[wrap_idx(j + k - 1, L)]; };
+    auto B_at = [&](int k) { return k == lb - 1 ? u : X[wrap_idx(pos + k, L)]; };
+    int ka = warp_find_first(la, lane, [&](int k) { return A_at(k) == oa && A_at(k + 1 == la ? 0 : k + 1) == ga; });
+    int kb = warp_find_first(lb, lane, [&](int k) { return B_at(k) == ob && B_at(k + 1 == lb ? 0 : k + 1) == gb; });
     if (ka >= 0 && kb >= 0) {
       long long o = 0;
       if (lane == 0) o = palloc(c, la + lb);
@@ -472,14 +478,8 @@ __device__ bool warp_split_tip(const RepairCtx& c, const int32_t* X, int L, int3
       }
       int32_t* A = c.pool + o;
       int32_t* B = A + la;
-      for (int k = lane; k < la; k += 32) {
-        int kk = wrap_idx(ka + k, la);
-        A[k] = kk == 0 ? v : X[wrap_idx(j + kk - 1, L)];
-      }
-      for (int k = lane; k < lb; k += 32) {
-        int kk = wrap_idx(kb + k, lb);
-        B[k] = kk == lb - 1 ? u : X[wrap_idx(pos + kk, L)];
-      }
+      warp_copy(A, la, lane, [&](int k) { return A_at(wrap_idx(ka + k, la)); });
+      warp_copy(B, lb, lane, [&](int k) { return B_at(wrap_idx(kb + k, lb)); });
       __syncwarp();
       *pa_off = o; *pa_len = la; *pb_off = o + la; *pb_len = lb;
       return true;
@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, con
       continue;
     }
     int32_t* P0 = c.pool + base;
-    for (int k = lane; k < L; k += 32) P0[k] = v[b + k];
+    warp_copy(P0, L, lane, [&](int k) { return v[b + k]; });
     __syncwarp();
     long long list = base + L;
     uint32_t f0 = warp_tip_flag(P0, L, lane);
@@ -792,32 +792,79 @@ __global__ void __launch_bounds__(256) k_out_counts(const int64_t* __restrict__ 
   }
 }
 
-__global__ void __launch_bounds__(256) k_stitch(const int64_t* __restrict__ off, const int32_t* __restrict__ v, const int64_t* __restrict__ Pp,
-                                                const int32_t* __restrict__ item_of, const int64_t* __restrict__ item_list,
-                                                const int32_t* __restrict__ item_n, const int32_t* __restrict__ pool,
-                                                const int64_t* __restrict__ pbase, const int64_t* __restrict__ sbase,
-                                                int64_t* __restrict__ off_out, int32_t* __restrict__ v_out) {
+// untouched polygons: one thread each, up to 16 independent loads in flight
+__global__ void __launch_bounds__(256) k_stitch_plain(const int64_t* __restrict__ off, const int32_t* __restrict__ v,
+                                                      const int64_t* __restrict__ Pp,
+                                                      const int32_t* __restrict__ item_of,
+                                                      const int64_t* __restrict__ pbase,
+                                                      const int64_t* __restrict__ sbase,
+                                                      int64_t* __restrict__ off_out, int32_t* __restrict__ v_out) {
   const int64_t P = *Pp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t it = item_of[i];
+    if (item_of[i] >= 0) continue;
+    int64_t b = off[i], n = off[i + 1] - b, sb = sbase[i];
+    off_out[pbase[i]] = sb;
+    for (int64_t k0 = 0; k0 < n; k0 += 16) {
+      int32_t buf[16];
+#pragma unroll
+      for (int k = 0; k < 16; k++)
+        if (k0 + k < n) buf[k] = v[b + k0 + k];
+#pragma unroll
+      for (int k = 0; k < 16; k++)
+        if (k0 + k < n) v_out[sb + k0 + k] = buf[k];
+    }
+  }
+}
+
+// repaired polygons: one warp per work item, leaves flattened across lanes
+__global__ void __launch_bounds__(256) k_stitch_items(const int32_t* __restrict__ items,
+                                                      const unsigned int* n_items,
+                                                      const int64_t* __restrict__ item_list,
+                                                      const int32_t* __restrict__ item_n,
+                                                      const int32_t* __restrict__ pool,
+                                                      const int64_t* __restrict__ pbase,
+                                                      const int64_t* __restrict__ sbase,
+                                                      int64_t* __restrict__ off_out, int32_t* __restrict__ v_out) {
+  const int lane = threadIdx.x & 31;
+  const unsigned int ni = *n_items;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = warp; w < ni; w += nwarps) {
+    int32_t i = items[w];
+    int64_t list = item_list[w];
+    int n = item_n[w];
+    if (list < 0) continue;
     int64_t pb = pbase[i], sb = sbase[i];
-    if (it < 0) {
-      int64_t b = off[i], n = off[i + 1] - b;
-      off_out[pb] = sb;
-      for (int64_t k = 0; k < n; k++) v_out[sb + k] = v[b + k];
-      if (i == P - 1) off_out[pb + 1] = sb + n;
-      continue;
+    for (int c = 0; c < n; c += 32) {
+      int r = c + lane;
+      uint32_t ro = 0;
+      int ln = 0;
+      if (r < n) {
+        ro = (uint32_t)pool[list + 2 * r];
+        ln = (int)((uint32_t)pool[list + 2 * r + 1] & LEN_MASK);
+      }
+      int inc = ln;
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      int start = inc - ln, total = __shfl_sync(0xffffffffu, inc, 31);
+      if (r < n) off_out[pb + r] = sb + start;
+      for (int kb = 0; kb < total; kb += 32) {
+        int k = kb + lane;  // all lanes stay converged for the shuffles
+        // leaf owning flattened element k: last leaf whose start <= k
+        int lo = 0;
+        for (int step = 16; step > 0; step >>= 1) {
+          int cand = lo + step;
+          int cs = __shfl_sync(0xffffffffu, start, cand < 32 ? cand : 31);
+          if (cand < 32 && cand + c < n && cs <= k) lo = cand;
+        }
+        uint32_t lro = __shfl_sync(0xffffffffu, ro, lo);
+        int ls = __shfl_sync(0xffffffffu, start, lo);
+        if (k < total) v_out[sb + k] = pool[lro + (k - ls)];
+      }
+      sb += total;
     }
-    int64_t list = item_list[it];
-    int n = item_n[it];
-    for (int r = 0; r < n; r++) {
-      uint32_t ro = (uint32_t)pool[list + 2 * r], rl = (uint32_t)pool[list + 2 * r + 1];
-      int64_t ln = rl & LEN_MASK;
-      off_out[pb + r] = sb;
-      for (int64_t k = 0; k < ln; k++) v_out[sb + k] = pool[ro + k];
-      sb += ln;
-    }
-    if (i == P - 1) off_out[pb + n] = sb;
   }
 }
 
@@ -879,11 +926,12 @@ void launch_out_counts(const int64_t* off, const int64_t* Pp, int64_t Pcap, cons
 }
 
 void launch_stitch(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, const int32_t* item_of,
-                   const int64_t* item_list, const int32_t* item_n, const int32_t* pool, const int64_t* pbase,
-                   const int64_t* sbase, int64_t* off_out, int32_t* v_out, cudaStream_t s) {
-  k_stitch<<<grid_for(Pcap, 256), 256, 0, s>>>(off, v, Pp, item_of, item_list, item_n, pool, pbase, sbase, off_out,
-                                               v_out);
-  note_launch(1);
+                   const int32_t* items, const unsigned int* n_items, const int64_t* item_list, const int32_t* item_n,
+                   const int32_t* pool, const int64_t* pbase, const int64_t* sbase, int64_t* off_out, int32_t* v_out,
+                   cudaStream_t s) {
+  k_stitch_plain<<<grid_for(Pcap, 256), 256, 0, s>>>(off, v, Pp, item_of, pbase, sbase, off_out, v_out);
+  k_stitch_items<<<kNumSMs * 8, 256, 0, s>>>(items, n_items, item_list, item_n, pool, pbase, sbase, off_out, v_out);
+  note_launch(2);
 }
 
 void launch_finalize(const int64_t* Pp, const int64_t* pbase, const int64_t* sbase, int64_t* off_out,
