@@ -114,7 +114,7 @@ struct tm_ctx {
   // repair
   Buf item_of, items, long_list, item_list, item_n, item_slots, cnt, slotsz, pbase, sbase, pool, undo;
   // whole-path buffers
-  Buf xy, tri, tri32, hw, max_edge, seed, tv, off0, v0, fin_off, fin_v;
+  Buf xy, tri, tri32, hw, max_edge, seed, tv, off0, v0, fin_off, fin_v, hw_snap;
   cudaStream_t gstream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
@@ -316,7 +316,10 @@ static int prepare(tm_ctx* ctx, int64_t T) {
   ENSURE(slotsz, (Tn + 1) * sizeof(int64_t));
   ENSURE(pbase, (Tn + 1) * sizeof(int64_t));
   ENSURE(sbase, (Tn + 1) * sizeof(int64_t));
-  unsigned long long want = 6ull * (unsigned long long)Tn + (1ull << 20);
+  // item copies + pieces + per-warp arena slack
+  unsigned long long want = 8ull * (unsigned long long)Tn + (1ull << 22);
+  const char* forced = getenv("TERMESH_POOL_INIT");  // testing hook: start small, exercise the retry path
+  if (forced && *forced) want = strtoull(forced, nullptr, 10);
   if (ctx->pool_cap < want) ctx->pool_cap = want;
   if (ctx->pool_cap >= (1ull << 32)) return set_err(ctx, TM_ERR_CAPACITY, "repair scratch pool exceeds 2^32 slots");
   ENSURE(pool, ctx->pool_cap * sizeof(int32_t));
@@ -451,16 +454,16 @@ static void fill_stats(const Counters& h, int64_t* stats) {
   stats[TM_STAT_WORK_ITEMS] = (int64_t)h.n_items;
 }
 
-// Pool overflow: roll back the promotions of the failed attempt, grow the
+// Pool overflow: restore the pre-repair frontier bits (restore()), grow the
 // pool, and re-run the repair phase (outside any graph).
+template <typename Restore>
 static int retry_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, const int32_t* d_tv, int64_t T,
                         const int64_t* d_off_in, const int32_t* d_v_in, const int64_t* Pp, int64_t* d_off_out,
-                        int32_t* d_v_out, cudaStream_t s, Counters* h, int rc) {
+                        int32_t* d_v_out, cudaStream_t s, Counters* h, int rc, Restore restore) {
   for (int attempt = 0; attempt < 6 && rc == TM_ERR_CAPACITY && h->st.count[K_POOL]; attempt++) {
-    unsigned long long ucap = (unsigned long long)(T > 0 ? T : 1) + 1024;
-    if (h->undo_top > ucap) return set_err(ctx, TM_ERR_CAPACITY, "[reparation] pool and promotion log overflowed");
     Counters* dc = dc_of(ctx);
-    launch_undo(d_hw, ctx->undo.as<int32_t>(), &dc->undo_top, ucap, s);
+    int r = restore(s);
+    if (r) return r;
     CK(cudaStreamSynchronize(s));
     ctx->pool_cap *= 4;
     if (ctx->pool_cap >= (1ull << 32)) return set_err(ctx, TM_ERR_CAPACITY, "repair pool exceeds 2^32 slots");
@@ -469,7 +472,7 @@ static int retry_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, cons
     CK(cudaMemcpyAsync(&dc->st, &ctx->h_reset->st, sizeof(DevStatus), cudaMemcpyHostToDevice, s));
     CK(cudaMemsetAsync(&dc->n_items, 0, 2 * sizeof(unsigned int), s));
     CK(cudaMemsetAsync(&dc->pool_top, 0, 10 * sizeof(unsigned long long), s));
-    int r = enqueue_repair(ctx, d_tri32, d_hw, d_tv, T, d_off_in, d_v_in, Pp, d_off_out, d_v_out, s);
+    r = enqueue_repair(ctx, d_tri32, d_hw, d_tv, T, d_off_in, d_v_in, Pp, d_off_out, d_v_out, s);
     if (r) return r;
     rc = finish(ctx, s, h);
   }
@@ -497,7 +500,7 @@ void tm_ctx_destroy(tm_ctx* ctx) {
                  &ctx->ent_r, &ctx->ent_base, &ctx->item_of, &ctx->items, &ctx->long_list, &ctx->item_list,
                  &ctx->item_n, &ctx->item_slots, &ctx->cnt, &ctx->slotsz, &ctx->pbase, &ctx->sbase, &ctx->pool,
                  &ctx->undo, &ctx->xy, &ctx->tri, &ctx->tri32, &ctx->hw, &ctx->max_edge, &ctx->seed, &ctx->tv,
-                 &ctx->off0, &ctx->v0, &ctx->fin_off, &ctx->fin_v};
+                 &ctx->off0, &ctx->v0, &ctx->fin_off, &ctx->fin_v, &ctx->hw_snap};
   for (Buf* b : bufs) b->release();
   if (ctx->h_reset) cudaFreeHost(ctx->h_reset);
   for (auto& e : ctx->ev)
@@ -635,12 +638,20 @@ int tm_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, const int32_t*
   *ctx->h_pin = P;
   Counters* dc = dc_of(ctx);
   CK(cudaMemcpyAsync(&dc->p_in, ctx->h_pin, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  // caller-supplied frontier bits: keep a copy so a pool overflow can be rolled back
+  ENSURE(hw_snap, 3 * (T > 0 ? T : 1) * sizeof(int32_t));
+  CK(cudaMemcpyAsync(ctx->hw_snap.p, d_hw, 3 * T * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
   if ((rc = enqueue_repair(ctx, d_tri32, d_hw, d_tv, T, d_off_in, d_v_in, &dc->p_in, d_off_out, d_v_out, s)))
     return rc;
   Counters h;
   rc = finish(ctx, s, &h);
   if (rc == TM_ERR_CAPACITY)
-    rc = retry_repair(ctx, d_tri32, d_hw, d_tv, T, d_off_in, d_v_in, &dc->p_in, d_off_out, d_v_out, s, &h, rc);
+    rc = retry_repair(ctx, d_tri32, d_hw, d_tv, T, d_off_in, d_v_in, &dc->p_in, d_off_out, d_v_out, s, &h, rc,
+                      [&](cudaStream_t st) -> int {
+                        CK(cudaMemcpyAsync(d_hw, ctx->hw_snap.p, 3 * T * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                                           st));
+                        return TM_OK;
+                      });
   if (rc) return rc;
   *n_polys_out = h.p_out;
   *n_slots_out = h.f_out;
@@ -737,7 +748,13 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
   Counters h = *ctx->h_result;
   rc = decode_status(ctx, h);
   if (rc == TM_ERR_CAPACITY) {
-    rc = retry_repair(ctx, tri32, hw, tv, T, off0, v0, &dc->n_seeds, d_off, d_v, s, &h, rc);
+    // labels are ours: relabeling restores the pre-repair frontier exactly
+    rc = retry_repair(ctx, tri32, hw, tv, T, off0, v0, &dc->n_seeds, d_off, d_v, s, &h, rc,
+                      [&](cudaStream_t st) -> int {
+                        launch_relabel(ctx->max_edge.as<int8_t>(), T, hw, ctx->seed.as<uint8_t>(), st);
+                        CK(cudaGetLastError());
+                        return TM_OK;
+                      });
     if (ctx->graph) cudaGraphExecDestroy(ctx->graph);  // pool size changed
     ctx->graph = nullptr;
   }

@@ -19,9 +19,11 @@
 // rotation search fails the split falls back to the re-walk.  Pinch trial splits
 // (rare) always re-walk, with revert on a broken length law.
 //
-// Piece records live in a device pool (bump allocated): {offset, len|flags}.
-// Every promoted half-edge is appended to an undo log, so a pool overflow can
-// be rolled back and retried by the host with a larger pool.
+// Piece records live in a device pool: {offset, len|flags}.  Each warp
+// allocates from its own arena (one global atomic per arena, not per piece),
+// so the bump counter is not a serialisation point.  A pool overflow is
+// reported; the host restores the pre-repair frontier bits and retries with a
+// larger pool.
 #include "tm_common.cuh"
 #include "tm_internal.h"
 
@@ -55,8 +57,34 @@ __device__ __forceinline__ int64_t palloc(const RepairCtx& c, int64_t n) {
 __device__ __forceinline__ void promote(const RepairCtx& c, int32_t e, int32_t te) {
   c.hw[e] |= 1;
   c.hw[te] |= 1;
-  unsigned long long k = atomicAdd(c.undo_top, 1ull);
-  if (k < c.undo_cap) c.undo[k] = e;
+}
+
+// Per-warp bump arena carved from the pool (state held by lane 0).
+struct WarpArena {
+  long long cur = 0, end = 0;
+};
+
+// Warp-uniform allocation of n slots; returns -1 when the pool is exhausted.
+__device__ __forceinline__ long long warp_alloc(const RepairCtx& c, WarpArena& a, long long n, long long refill,
+                                                int lane) {
+  long long o = 0;
+  if (lane == 0) {
+    if (a.cur + n > a.end) {
+      long long want = n > refill ? n : refill;
+      long long base = palloc(c, want);
+      if (base < 0) {
+        o = -1;
+      } else {
+        a.cur = base;
+        a.end = base + want;
+      }
+    }
+    if (o == 0) {
+      o = a.cur;
+      a.cur += n;
+    }
+  }
+  return __shfl_sync(0xffffffffu, o, 0);
 }
 
 __device__ __forceinline__ void demote(const RepairCtx& c, int32_t e, int32_t te) {
@@ -420,7 +448,7 @@ __device__ int32_t warp_middle_internal_edge(const RepairCtx& c, int32_t v, int3
 // Tip split of piece X (len L) at its first tip, warp-cooperative arc copy
 // with the re-walk as fallback.
 __device__ bool warp_split_tip(const RepairCtx& c, const int32_t* X, int L, int32_t poly, int32_t* fan, int lane,
-                               int64_t* pa_off, int64_t* pa_len, int64_t* pb_off, int64_t* pb_len) {
+                               WarpArena& arena, int64_t* pa_off, int64_t* pa_len, int64_t* pb_off, int64_t* pb_len) {
   int pos = warp_first_tip(X, L, lane);
   if (pos < 0) {
     if (lane == 0) report(c.st, K_STRUCT, poly);
@@ -469,9 +497,7 @@ __device__ bool warp_split_tip(const RepairCtx& c, const int32_t* X, int L, int3
     int ka = warp_find_first(la, lane, [&](int k) { return A_at(k) == oa && A_at(k + 1 == la ? 0 : k + 1) == ga; });
     int kb = warp_find_first(lb, lane, [&](int k) { return B_at(k) == ob && B_at(k + 1 == lb ? 0 : k + 1) == gb; });
     if (ka >= 0 && kb >= 0) {
-      long long o = 0;
-      if (lane == 0) o = palloc(c, la + lb);
-      o = __shfl_sync(kFull, o, 0);
+      long long o = warp_alloc(c, arena, la + lb, 2 * (long long)L + 512, lane);
       if (o < 0) {
         if (lane == 0) report(c.st, K_POOL, poly);
         return false;
@@ -527,9 +553,8 @@ __global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, con
     int32_t i = items[w];
     int64_t b = off[i];
     int L = (int)(off[i + 1] - b);
-    long long base = 0;
-    if (lane == 0) base = palloc(c, L + 2);
-    base = __shfl_sync(kFull, base, 0);
+    WarpArena arena;
+    long long base = warp_alloc(c, arena, L + 2, 4 * (long long)L + 512, lane);
     if (base < 0) {
       if (lane == 0) { report(c.st, K_POOL, i); item_list[w] = -1; item_n[w] = 0; }
       continue;
@@ -554,9 +579,7 @@ __global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, con
         bad = true;
         break;
       }
-      long long nl = 0;
-      if (lane == 0) nl = palloc(c, 2 * (int64_t)(n + ntips));
-      nl = __shfl_sync(kFull, nl, 0);
+      long long nl = warp_alloc(c, arena, 2 * (long long)(n + ntips), 2 * (long long)L + 512, lane);
       if (nl < 0) {
         if (lane == 0) report(c.st, K_POOL, i);
         bad = true;
@@ -574,7 +597,7 @@ __global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, con
           continue;
         }
         int64_t ao, al, bo, bl;
-        if (!warp_split_tip(c, c.pool + ro, (int)(rl & LEN_MASK), i, fan, lane, &ao, &al, &bo, &bl)) {
+        if (!warp_split_tip(c, c.pool + ro, (int)(rl & LEN_MASK), i, fan, lane, arena, &ao, &al, &bo, &bl)) {
           bad = true;
           break;
         }

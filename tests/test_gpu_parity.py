@@ -208,3 +208,29 @@ def test_u1m_matches_reference_hashes(cuda):
     assert H(off) == h["final_off"] and H(v) == h["final_verts"]
     assert H(lab.frontier) == h["frontier_post"]
     assert [info[k] for k in ("rounds", "splits", "initial_tips", "unrepaired")] == h["stats"]
+
+
+def test_pool_overflow_retry_is_exact(cuda):
+    """A deliberately tiny repair pool forces the overflow -> restore -> retry
+    path (pipeline and phase-level API); results must not change."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, 'tests'); sys.path.insert(0, '.')\n"
+        "from conftest import load_case\n"
+        "import paper_2204_05438_b200 as tm\n"
+        "for name in ('aniso2k_s1', 'aniso2k_s2', 'clust5k_s0'):\n"
+        "    tri, g = load_case(name)\n"
+        "    lab = tm.label_all(tri, check=False); m0 = tm.build_polygon_mesh(tri, lab); info = {}\n"
+        "    fin = tm.repair_all(tri, lab, m0, stats_out=info)\n"
+        "    off, v = fin.csr()\n"
+        "    assert np.array_equal(off, g['final_off']) and np.array_equal(v, g['final_verts']), name\n"
+        "    assert np.array_equal(lab.frontier, g['frontier_post']), name\n"
+        "    f2, st = tm.execute(tri)\n"
+        "    assert np.array_equal(f2.csr()[1], g['final_verts']), name\n"
+        "print('ok')\n")
+    import os
+    env = dict(os.environ, TERMESH_POOL_INIT="2048")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
