@@ -112,7 +112,8 @@ struct tm_ctx {
   // traversal
   Buf seeds, start, len, overflow, queue, stamp, tiles, nrul, eoff, rnext, rdist, startbits, ent_r, ent_base;
   // repair
-  Buf item_of, items, long_list, item_list, item_n, item_slots, cnt, slotsz, pbase, sbase, pool, undo;
+  Buf item_of, items, long_list, item_list, item_n, item_slots, item_state, item_depth, cnt, slotsz, pbase, sbase, pool,
+      undo;
   // whole-path buffers
   Buf xy, tri, tri32, hw, max_edge, seed, tv, off0, v0, fin_off, fin_v, hw_snap;
   cudaStream_t gstream = nullptr;
@@ -312,6 +313,8 @@ static int prepare(tm_ctx* ctx, int64_t T) {
   ENSURE(item_list, Tn * sizeof(int64_t));
   ENSURE(item_n, Tn * sizeof(int32_t));
   ENSURE(item_slots, Tn * sizeof(int64_t));
+  ENSURE(item_state, Tn * sizeof(int32_t));
+  ENSURE(item_depth, Tn * sizeof(int32_t));
   ENSURE(cnt, (Tn + 1) * sizeof(int64_t));
   ENSURE(slotsz, (Tn + 1) * sizeof(int64_t));
   ENSURE(pbase, (Tn + 1) * sizeof(int64_t));
@@ -405,10 +408,12 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
     launch_classify(d_off_in, d_v_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(), &dc->n_items,
                     ctx->long_list.as<int32_t>(), &dc->n_long, dc->stats, s);
   }
+  CK(cudaMemsetAsync(ctx->item_state.p, 0, Tn * sizeof(int32_t), s));
   RepairArgs a{d_tri32, d_hw, d_tv, T, ctx->pool.as<int32_t>(), ctx->pool_cap, &dc->pool_top, ctx->undo.as<int32_t>(),
                &dc->undo_top, (unsigned long long)Tn + 1024, &dc->st, ctx->items.as<int32_t>(), &dc->n_items,
                d_off_in, d_v_in, ctx->item_list.as<int64_t>(), ctx->item_n.as<int32_t>(),
-               ctx->item_slots.as<int64_t>(), dc->stats};
+               ctx->item_slots.as<int64_t>(), ctx->item_state.as<int32_t>(), ctx->item_depth.as<int32_t>(),
+               dc->stats};
   {
     SegTimer t_(ctx, S_REPAIR_TIPS, s);
     launch_repair_tips(a, s);
@@ -498,7 +503,7 @@ void tm_ctx_destroy(tm_ctx* ctx) {
   Buf* bufs[] = {&ctx->counters, &ctx->slots, &ctx->seeds, &ctx->start, &ctx->len, &ctx->overflow, &ctx->queue,
                  &ctx->stamp, &ctx->tiles, &ctx->nrul, &ctx->eoff, &ctx->rnext, &ctx->rdist, &ctx->startbits,
                  &ctx->ent_r, &ctx->ent_base, &ctx->item_of, &ctx->items, &ctx->long_list, &ctx->item_list,
-                 &ctx->item_n, &ctx->item_slots, &ctx->cnt, &ctx->slotsz, &ctx->pbase, &ctx->sbase, &ctx->pool,
+                 &ctx->item_n, &ctx->item_slots, &ctx->item_state, &ctx->item_depth, &ctx->cnt, &ctx->slotsz, &ctx->pbase, &ctx->sbase, &ctx->pool,
                  &ctx->undo, &ctx->xy, &ctx->tri, &ctx->tri32, &ctx->hw, &ctx->max_edge, &ctx->seed, &ctx->tv,
                  &ctx->off0, &ctx->v0, &ctx->fin_off, &ctx->fin_v, &ctx->hw_snap};
   for (Buf* b : bufs) b->release();

@@ -67,6 +67,8 @@ struct RepairArgs {
   int64_t* item_list;
   int32_t* item_n;
   int64_t* item_slots;
+  int32_t* item_state;   // 0 todo, 1 done (shared-memory kernel), 2 resume, 3 warp kernel from scratch
+  int32_t* item_depth;
   unsigned long long* stats;
 };
 void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, int32_t* item_of,

@@ -24,6 +24,8 @@
 // so the bump counter is not a serialisation point.  A pool overflow is
 // reported; the host restores the pre-repair frontier bits and retries with a
 // larger pool.
+#include <cstdlib>
+
 #include "tm_common.cuh"
 #include "tm_internal.h"
 
@@ -304,9 +306,9 @@ __device__ int rewalk_split(const RepairCtx& c, int32_t e, int32_t te, int64_t p
 }
 
 // ------------------------------------------------------------ warp helpers
-// One warp cooperates on one work item.  Lanes split O(len) scans and copies;
-// the inherently sequential mesh rotations (fan walk, wedge rotation) run on
-// lane 0 and are broadcast.  All control flow below is warp-uniform.
+// One warp cooperates on one piece.  Lanes split O(len) scans and copies; the
+// sequential mesh rotations run on one or two lanes and are broadcast.  All
+// control flow below is warp-uniform.
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kFanCap = 64;
 constexpr int kTipWarps = 4;  // warps per block of k_repair_tips
@@ -334,8 +336,7 @@ __device__ __forceinline__ int warp_find_first(int n, int lane, Pred pred) {
   return -1;
 }
 
-// dst[k] = src(k) for k in [0, n), values staged in registers so the loads of
-// eight elements per lane are in flight together.
+// dst[k] = src(k) for k in [0, n), staged in registers (8 loads in flight per lane)
 template <typename Src>
 __device__ __forceinline__ void warp_copy(int32_t* dst, int n, int lane, Src src) {
   for (int base = 0; base < n; base += 32 * kScanUnroll) {
@@ -358,6 +359,10 @@ __device__ int warp_first_tip(const int32_t* s, int n, int lane) {
   return warp_find_first(n, lane, [&](int p) { return s[p == 0 ? n - 1 : p - 1] == s[p + 1 == n ? 0 : p + 1]; });
 }
 
+__device__ __forceinline__ uint32_t warp_tip_flag(const int32_t* s, int n, int lane) {
+  return warp_first_tip(s, n, lane) >= 0 ? F_TIP : 0u;
+}
+
 // (len - distinct) of s[0..n) (traversal.py:140-147), quadratic over lanes
 __device__ int warp_extra_visits(const int32_t* s, int n, int lane) {
   int extra = 0;
@@ -378,31 +383,74 @@ __device__ int warp_extra_visits(const int32_t* s, int n, int lane) {
   return extra;
 }
 
-// reparation.py:127-145 with the fan held in shared memory (deg <= kFanCap);
-// larger fans fall back to the sequential enumeration on lane 0.
-__device__ int32_t warp_middle_internal_edge(const RepairCtx& c, int32_t v, int32_t barrier, int32_t poly,
-                                             int32_t* fan, int lane) {
-  int deg = 0, status = 0;
+// Fan of v in the reference order (_fan_around from the trivertex half-edge
+// g0, reparation.py:91-124) collected into fan[0..deg) by two walkers: lane 0
+// rotates CCW from g0, lane 1 rotates CW.  A closed fan ends where the walkers
+// meet; an open fan is the CCW run followed by the reversed CW run.  Half the
+// dependent loads of a one-sided walk.  Returns deg, -1 on a structural
+// failure, or kFanCap + 1 when the fan does not fit (caller falls back).
+__device__ int warp_collect_fan(const RepairCtx& c, int32_t v, int32_t* fan, int32_t* back, int lane) {
+  int32_t g0 = -1;
   if (lane == 0) {
     int32_t t0 = c.tv[v];
-    int32_t g0 = t0 < 0 ? -1 : he_with_origin(c.tri, t0, v);
-    if (g0 < 0) {
-      status = 1;
-    } else {
-      int guard = (int)(3 * c.T + 3 < (1LL << 30) ? 3 * c.T + 3 : (1LL << 30));
-      int32_t g = g0;
-      do {
-        if (deg < kFanCap) fan[deg] = g;
-        deg++;
-        g = fan_step(c.hw, g, guard);
-        if (g < 0 || deg > guard) { status = 1; break; }
-      } while (g != g0);
-    }
+    g0 = t0 < 0 ? -1 : he_with_origin(c.tri, t0, v);
+    if (g0 >= 0) fan[0] = g0;
   }
-  deg = __shfl_sync(kFull, deg, 0);
-  status = __shfl_sync(kFull, status, 0);
+  g0 = __shfl_sync(kFull, g0, 0);
+  if (g0 < 0) return -1;
+  int32_t cur = g0;                 // lane 0: CCW walker, lane 1: CW walker
+  bool stop = false;
+  int a = 0, b = 0;                 // fan[1..a] from lane 0, back[0..b) from lane 1
+  int deg = kFanCap + 1, mode = 0;  // mode 1: append the meeting element
+  for (int step = 0; step < kFanCap; step++) {
+    int32_t nxt = -1;
+    if (lane == 0 && !stop) nxt = rot_ccw(c.hw, cur);
+    if (lane == 1 && !stop) nxt = rot_cw(c.hw, cur);
+    int32_t n0 = __shfl_sync(kFull, nxt, 0), n1 = __shfl_sync(kFull, nxt, 1);
+    int32_t c1 = __shfl_sync(kFull, cur, 1);
+    bool s0 = __shfl_sync(kFull, stop, 0), s1 = __shfl_sync(kFull, stop, 1);
+    int aa = __shfl_sync(kFull, a, 0), bb = __shfl_sync(kFull, b, 1);
+    if (!s0 && !s1 && n0 >= 0) {
+      if (n0 == c1) { deg = 1 + aa + bb; break; }            // CCW reached the CW walker's element
+      if (n0 == n1) { deg = 2 + aa + bb; mode = 1; break; }  // both stepped onto the same element
+    }
+    if (lane == 0 && !stop) {
+      if (nxt < 0) stop = true;
+      else { a++; if (a < kFanCap) fan[a] = nxt; cur = nxt; }
+    }
+    if (lane == 1 && !stop) {
+      if (nxt < 0) stop = true;
+      else { if (b < kFanCap) back[b] = nxt; b++; cur = nxt; }
+    }
+    s0 = __shfl_sync(kFull, stop, 0);
+    s1 = __shfl_sync(kFull, stop, 1);
+    aa = __shfl_sync(kFull, a, 0);
+    bb = __shfl_sync(kFull, b, 1);
+    if (s0 && s1) { deg = 1 + aa + bb; break; }              // open fan: both walkers at the border
+    if (1 + aa + bb + 1 > kFanCap) break;
+  }
+  a = __shfl_sync(kFull, a, 0);
+  b = __shfl_sync(kFull, b, 1);
+  if (deg > kFanCap) return kFanCap + 1;
   __syncwarp();
-  if (status) {
+  if (mode == 1) {
+    int32_t m = -1;
+    if (lane == 0) m = rot_ccw(c.hw, fan[a]);
+    if (lane == 0) fan[a + 1] = m;
+    a++;
+  }
+  __syncwarp();
+  for (int k = lane; k < b; k += 32) fan[1 + a + k] = back[b - 1 - k];
+  __syncwarp();
+  return deg;
+}
+
+// reparation.py:127-145: the ((k-1)//2)-th non-frontier half-edge of the fan
+// rotated to start at the barrier half-edge (target == barrier, frontier).
+__device__ int32_t warp_middle_internal_edge(const RepairCtx& c, int32_t v, int32_t barrier, int32_t poly,
+                                             int32_t* fan, int32_t* back, int lane) {
+  int deg = warp_collect_fan(c, v, fan, back, lane);
+  if (deg < 0) {
     if (lane == 0) report(c.st, K_STRUCT, poly);
     return -1;
   }
@@ -436,7 +484,6 @@ __device__ int32_t warp_middle_internal_edge(const RepairCtx& c, int32_t v, int3
   }
   int at = __ffsll((long long)bmask) - 1;
   int k = __popcll(imask), want = (k - 1) / 2;
-  // rotated order fan[at:] + fan[:at]
   unsigned long long hi = imask & (~0ull << at), lo = imask & ((1ull << at) - 1);
   unsigned long long m = hi;
   int cnt_hi = __popcll(hi);
@@ -445,17 +492,57 @@ __device__ int32_t warp_middle_internal_edge(const RepairCtx& c, int32_t v, int3
   return fan[__ffsll((long long)m) - 1];
 }
 
-// Tip split of piece X (len L) at its first tip, warp-cooperative arc copy
-// with the re-walk as fallback.
-__device__ bool warp_split_tip(const RepairCtx& c, const int32_t* X, int L, int32_t poly, int32_t* fan, int lane,
-                               WarpArena& arena, int64_t* pa_off, int64_t* pa_len, int64_t* pb_off, int64_t* pb_len) {
+// Re-walk split (reparation.py:216-229 after promotion), warp-uniform result:
+// 1 = pieces written through alloc, 0 = length law failed, -1 = error.
+template <typename Alloc>
+__device__ int warp_rewalk_split(const RepairCtx& c, int32_t e, int32_t te, int L, int32_t poly, Alloc alloc,
+                                 int lane, int32_t** A, int* la_out, int32_t** B, int* lb_out) {
+  long long la = 0, lb = 0;
+  int32_t ha = -1, hb = -1;
+  if (lane == 0) {
+    ha = min_frontier_slot(c.hw, e / 3);
+    hb = min_frontier_slot(c.hw, te / 3);
+    la = walk_len(c, ha);
+    lb = walk_len(c, hb);
+  }
+  la = __shfl_sync(kFull, la, 0);
+  lb = __shfl_sync(kFull, lb, 0);
+  if (la < 0 || lb < 0) {
+    if (lane == 0) report(c.st, K_STRUCT, poly);
+    return -1;
+  }
+  if (la + lb != (long long)L + 2) return 0;
+  int32_t* p = alloc(la + lb);
+  if (p == nullptr) {
+    if (lane == 0) report(c.st, K_POOL, poly);
+    return -1;
+  }
+  if (lane == 0) {
+    walk_write(c, ha, p);
+    walk_write(c, hb, p + la);
+  }
+  __syncwarp();
+  *A = p;
+  *la_out = (int)la;
+  *B = p + la;
+  *lb_out = (int)lb;
+  return 1;
+}
+
+// Tip split of piece X (len L) at its first tip (reparation.py:294-312
+// splitter), warp-cooperative arc copy with the re-walk as
+// fallback.  Pieces are written through alloc (global pool or shared arena).
+template <typename Alloc>
+__device__ bool warp_split_tip(const RepairCtx& c, const int32_t* X, int L, int32_t poly, int32_t* fan,
+                               int32_t* back, int lane, Alloc alloc, int32_t** A_out, int* la_out, int32_t** B_out,
+                               int* lb_out) {
   int pos = warp_first_tip(X, L, lane);
   if (pos < 0) {
     if (lane == 0) report(c.st, K_STRUCT, poly);
     return false;
   }
   int32_t v = X[pos], b = X[pos == 0 ? L - 1 : pos - 1];
-  int32_t e = warp_middle_internal_edge(c, v, b, poly, fan, lane);
+  int32_t e = warp_middle_internal_edge(c, v, b, poly, fan, back, lane);
   if (e < 0) return false;
   int32_t te = hw_twin(c.hw[e]);
   if (te < 0) {
@@ -463,7 +550,8 @@ __device__ bool warp_split_tip(const RepairCtx& c, const int32_t* X, int L, int3
     return false;
   }
   int32_t u = he_target(c.tri, e);
-  // incoming boundary vertex of the visit of u whose wedge holds twin(e)
+  // incoming boundary vertex of the visit of u whose wedge holds twin(e):
+  // rotate CCW from twin(e) until the crossed edge prev(g) is frontier
   int32_t a_in = -1;
   if (lane == 0) {
     int32_t g = te;
@@ -497,41 +585,49 @@ __device__ bool warp_split_tip(const RepairCtx& c, const int32_t* X, int L, int3
     int ka = warp_find_first(la, lane, [&](int k) { return A_at(k) == oa && A_at(k + 1 == la ? 0 : k + 1) == ga; });
     int kb = warp_find_first(lb, lane, [&](int k) { return B_at(k) == ob && B_at(k + 1 == lb ? 0 : k + 1) == gb; });
     if (ka >= 0 && kb >= 0) {
-      long long o = warp_alloc(c, arena, la + lb, 2 * (long long)L + 512, lane);
-      if (o < 0) {
+      int32_t* A = alloc(la + lb);
+      if (A == nullptr) {
         if (lane == 0) report(c.st, K_POOL, poly);
         return false;
       }
-      int32_t* A = c.pool + o;
       int32_t* B = A + la;
       warp_copy(A, la, lane, [&](int k) { return A_at(wrap_idx(ka + k, la)); });
       warp_copy(B, lb, lane, [&](int k) { return B_at(wrap_idx(kb + k, lb)); });
       __syncwarp();
-      *pa_off = o; *pa_len = la; *pb_off = o + la; *pb_len = lb;
+      *A_out = A; *la_out = la; *B_out = B; *lb_out = lb;
       return true;
     }
   }
-  int r = 0;
-  long long ao = 0, al = 0, bo = 0, bl = 0;
-  if (lane == 0) {
-    int64_t a1, a2, a3, a4;
-    r = rewalk_split(c, e, te, L, poly, &a1, &a2, &a3, &a4);
-    if (r == 0) report(c.st, K_SPLIT_LAW, poly);
-    ao = a1; al = a2; bo = a3; bl = a4;
-  }
-  __syncwarp();
-  r = __shfl_sync(kFull, r, 0);
-  ao = __shfl_sync(kFull, ao, 0); al = __shfl_sync(kFull, al, 0);
-  bo = __shfl_sync(kFull, bo, 0); bl = __shfl_sync(kFull, bl, 0);
-  *pa_off = ao; *pa_len = al; *pb_off = bo; *pb_len = bl;
+  int r = warp_rewalk_split(c, e, te, L, poly, alloc, lane, A_out, la_out, B_out, lb_out);
+  if (r == 0 && lane == 0) report(c.st, K_SPLIT_LAW, poly);
   return r == 1;
 }
 
-__device__ __forceinline__ uint32_t warp_tip_flag(const int32_t* s, int n, int lane) {
-  return warp_first_tip(s, n, lane) >= 0 ? F_TIP : 0u;
+// ------------------------------------------------------------ tip phase, global pool
+// Item states (item_state[w]): 0 = not started, 1 = finished by the shared-
+// memory kernel, 2 = resume from item_list/item_n/item_depth in the pool.
+constexpr int kLongMin = 96;  // items longer than this go to k_repair_tips_long first
+
+__device__ void finish_item(const RepairCtx& c, int64_t w, long long list, int n, long long depth, long long splits,
+                            int lane, int64_t* item_list, int32_t* item_n, unsigned long long* stats) {
+  // repeated flags and extra visits of the leaves (pinch guard, reparation.py:322)
+  unsigned long long ex_sum = 0;
+  for (int r = 0; r < n; r++) {
+    uint32_t ro = (uint32_t)c.pool[list + 2 * r], rl = (uint32_t)c.pool[list + 2 * r + 1];
+    int ex = warp_extra_visits(c.pool + ro, (int)(rl & LEN_MASK), lane);
+    if (ex > 0 && lane == 0) c.pool[list + 2 * r + 1] = (int32_t)(rl | F_REP);
+    ex_sum += ex;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    item_list[w] = list;
+    item_n[w] = n;
+    if (depth > 0) atomicMax(stats + 0, (unsigned long long)depth);
+    if (splits) atomicAdd(stats + 1, (unsigned long long)splits);
+    if (ex_sum) atomicAdd(stats + 5, ex_sum);
+  }
 }
 
-// ------------------------------------------------------------ tip phase
 // One warp per work item.  item_list[w] = pool offset of the item's record
 // list, item_n[w] = #records (leaves in the reference's raw order).
 __global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, const int32_t* __restrict__ items,
@@ -540,37 +636,57 @@ __global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, con
                                                                 const int32_t* __restrict__ v,
                                                                 int64_t* __restrict__ item_list,
                                                                 int32_t* __restrict__ item_n,
+                                                                const int32_t* __restrict__ item_state,
+                                                                const int32_t* __restrict__ item_depth,
                                                                 unsigned long long* stats) {
   __shared__ int32_t s_fan[kTipWarps][kFanCap];
+  __shared__ int32_t s_back[kTipWarps][kFanCap];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   int32_t* fan = s_fan[wib];
+  int32_t* back = s_back[wib];
   unsigned int ni = *n_items;
   // reparation.py:354-364: at most initial + 1 rounds, initial = extra visits of mesh0
   long long max_rounds = (long long)stats[2] + 1;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t w = warp; w < ni; w += nwarps) {
+    int st = item_state[w];
+    if (st == 1) continue;
     int32_t i = items[w];
     int64_t b = off[i];
     int L = (int)(off[i + 1] - b);
+    if (st == 0 && L > kLongMin) continue;  // handled by k_repair_tips_long (state 1/2/3)
     WarpArena arena;
-    long long base = warp_alloc(c, arena, L + 2, 4 * (long long)L + 512, lane);
-    if (base < 0) {
-      if (lane == 0) { report(c.st, K_POOL, i); item_list[w] = -1; item_n[w] = 0; }
-      continue;
-    }
-    int32_t* P0 = c.pool + base;
-    warp_copy(P0, L, lane, [&](int k) { return v[b + k]; });
-    __syncwarp();
-    long long list = base + L;
-    uint32_t f0 = warp_tip_flag(P0, L, lane);
-    if (lane == 0) {
-      c.pool[list] = (int32_t)base;
-      c.pool[list + 1] = (int32_t)((uint32_t)L | f0);
-    }
-    __syncwarp();
-    int n = 1, ntips = f0 ? 1 : 0;
+    auto alloc = [&](long long n) -> int32_t* {
+      long long o = warp_alloc(c, arena, n, 2 * (long long)L + 512, lane);
+      return o < 0 ? nullptr : c.pool + o;
+    };
+    long long list;
+    int n, ntips = 0;
     long long depth = 0, splits = 0;
+    if (st == 2) {
+      list = item_list[w];
+      n = item_n[w];
+      depth = item_depth[w];
+      for (int r = 0; r < n; r++) ntips += (((uint32_t)c.pool[list + 2 * r + 1]) & F_TIP) ? 1 : 0;
+    } else {
+      int32_t* P0 = alloc(L + 2);
+      if (P0 == nullptr) {
+        if (lane == 0) { report(c.st, K_POOL, i); item_list[w] = -1; item_n[w] = 0; }
+        continue;
+      }
+      warp_copy(P0, L, lane, [&](int k) { return v[b + k]; });
+      __syncwarp();
+      list = (P0 - c.pool) + L;
+      uint32_t f0 = warp_tip_flag(P0, L, lane);
+      if (lane == 0) {
+        c.pool[list] = (int32_t)(P0 - c.pool);
+        c.pool[list + 1] = (int32_t)((uint32_t)L | f0);
+      }
+      __syncwarp();
+      n = 1;
+      ntips = f0 ? 1 : 0;
+    }
     bool bad = false;
     while (ntips > 0 && !bad) {
       depth++;
@@ -579,12 +695,13 @@ __global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, con
         bad = true;
         break;
       }
-      long long nl = warp_alloc(c, arena, 2 * (long long)(n + ntips), 2 * (long long)L + 512, lane);
-      if (nl < 0) {
+      int32_t* nlp = alloc(2 * (long long)(n + ntips));
+      if (nlp == nullptr) {
         if (lane == 0) report(c.st, K_POOL, i);
         bad = true;
         break;
       }
+      long long nl = nlp - c.pool;
       int m = 0, nt = 0;
       for (int r = 0; r < n; r++) {
         uint32_t ro = (uint32_t)c.pool[list + 2 * r], rl = (uint32_t)c.pool[list + 2 * r + 1];
@@ -596,16 +713,17 @@ __global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, con
           m++;
           continue;
         }
-        int64_t ao, al, bo, bl;
-        if (!warp_split_tip(c, c.pool + ro, (int)(rl & LEN_MASK), i, fan, lane, arena, &ao, &al, &bo, &bl)) {
+        int32_t *A, *B;
+        int al, bl;
+        if (!warp_split_tip(c, c.pool + ro, (int)(rl & LEN_MASK), i, fan, back, lane, alloc, &A, &al, &B, &bl)) {
           bad = true;
           break;
         }
-        uint32_t fa = warp_tip_flag(c.pool + ao, (int)al, lane), fb = warp_tip_flag(c.pool + bo, (int)bl, lane);
+        uint32_t fa = warp_tip_flag(A, al, lane), fb = warp_tip_flag(B, bl, lane);
         if (lane == 0) {
-          c.pool[nl + 2 * m] = (int32_t)ao;
+          c.pool[nl + 2 * m] = (int32_t)(A - c.pool);
           c.pool[nl + 2 * m + 1] = (int32_t)((uint32_t)al | fa);
-          c.pool[nl + 2 * m + 2] = (int32_t)bo;
+          c.pool[nl + 2 * m + 2] = (int32_t)(B - c.pool);
           c.pool[nl + 2 * m + 3] = (int32_t)((uint32_t)bl | fb);
         }
         m += 2;
@@ -621,22 +739,212 @@ __global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, con
       if (lane == 0) { item_list[w] = -1; item_n[w] = 0; }
       continue;
     }
-    // repeated flags and extra visits of the leaves (pinch guard, reparation.py:322)
-    unsigned long long ex_sum = 0;
-    for (int r = 0; r < n; r++) {
-      uint32_t ro = (uint32_t)c.pool[list + 2 * r], rl = (uint32_t)c.pool[list + 2 * r + 1];
-      int ex = warp_extra_visits(c.pool + ro, (int)(rl & LEN_MASK), lane);
-      if (ex > 0 && lane == 0) c.pool[list + 2 * r + 1] = (int32_t)(rl | F_REP);
-      ex_sum += ex;
+    finish_item(c, w, list, n, depth, splits, lane, item_list, item_n, stats);
+  }
+}
+
+// ------------------------------------------------------------ tip phase, shared memory
+// Long items (hull slivers: 902 vertices / 70 tips / 41 rounds at 1M): one
+// block each, pieces in a shared-memory bump arena, the tipped pieces of a
+// round split concurrently by the block's warps (distinct pieces have
+// disjoint interiors).  Scans run at shared-memory latency; only the mesh
+// rotations touch global memory.  If the arena or the record list fills up,
+// the current pieces are written to the global pool and the warp kernel
+// resumes the item (item_state = 2).
+constexpr int kLongWarps = 8;
+constexpr int kLongArena = 36 * 1024;  // ints (144 KiB)
+constexpr int kLongRec = 1024;         // records per list
+size_t long_smem_bytes() {
+  return (size_t)kLongArena * 4 + 2 * (size_t)kLongRec * 8 + 2 * (size_t)kLongWarps * kFanCap * 4 + 64;
+}
+
+__global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx c, const int32_t* __restrict__ items,
+                                                                      const unsigned int* n_items,
+                                                                      const int64_t* __restrict__ off,
+                                                                      const int32_t* __restrict__ v,
+                                                                      int64_t* __restrict__ item_list,
+                                                                      int32_t* __restrict__ item_n,
+                                                                      int32_t* __restrict__ item_state,
+                                                                      int32_t* __restrict__ item_depth,
+                                                                      unsigned long long* stats, int arena_cap) {
+  extern __shared__ __align__(16) int32_t smem[];
+  int32_t* arena = smem;
+  int2* recs = reinterpret_cast<int2*>(arena + kLongArena);  // layout uses the full size  // [2][kLongRec] {offset, len|flags}
+  int32_t* fans = reinterpret_cast<int32_t*>(recs + 2 * kLongRec);
+  __shared__ int s_top, s_fail, s_ntips;
+  __shared__ int s_out[kLongRec];  // output index of each input record
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int32_t* fan = fans + wib * kFanCap;
+  int32_t* back = fans + (kLongWarps + wib) * kFanCap;
+  unsigned int ni = *n_items;
+  long long max_rounds = (long long)stats[2] + 1;
+  for (unsigned int w = blockIdx.x; w < ni; w += gridDim.x) {
+    int32_t i = items[w];
+    int64_t b = off[i];
+    int L = (int)(off[i + 1] - b);
+    if (L <= kLongMin) continue;
+    if (L + 2 > arena_cap) {  // does not fit: the warp kernel does it from scratch
+      if (threadIdx.x == 0) item_state[w] = 3;
+      continue;
     }
-    __syncwarp();
-    if (lane == 0) {
-      item_list[w] = list;
-      item_n[w] = n;
-      if (depth > 0) atomicMax(stats + 0, (unsigned long long)depth);
-      if (splits) atomicAdd(stats + 1, (unsigned long long)splits);
-      if (ex_sum) atomicAdd(stats + 5, ex_sum);
+    __syncthreads();
+    for (int k = threadIdx.x; k < L; k += blockDim.x) arena[k] = v[b + k];
+    if (threadIdx.x == 0) { s_top = L; s_fail = 0; }
+    __syncthreads();
+    int cur = 0, n = 1;
+    if (wib == 0) {
+      uint32_t f0 = warp_tip_flag(arena, L, lane);
+      if (lane == 0) { recs[0] = make_int2(0, (int)((uint32_t)L | f0)); s_ntips = f0 ? 1 : 0; }
     }
+    __syncthreads();
+    int ntips = s_ntips;
+    long long depth = 0, splits = 0;
+    bool bad = false, spill = false;
+    while (ntips > 0) {
+      if (depth + 1 > max_rounds) {
+        if (threadIdx.x == 0) report(c.st, K_NO_CONVERGE, i);
+        bad = true;
+        break;
+      }
+      int2* in = recs + cur * kLongRec;
+      int2* out = recs + (cur ^ 1) * kLongRec;
+      // output slot of every input record (prefix over tip flags) and the arena
+      // the round needs (a split writes |piece| + 2 slots), warp 0
+      __shared__ int s_need;
+      if (wib == 0) {
+        int carry = 0, need = 0;
+        for (int base = 0; base < n; base += 32) {
+          int r = base + lane;
+          int t = (r < n && ((uint32_t)in[r].y & F_TIP)) ? 1 : 0;
+          int inc = t;
+          for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(kFull, inc, o);
+            if (lane >= o) inc += y;
+          }
+          if (r < n) s_out[r] = r + carry + inc - t;
+          carry += __shfl_sync(kFull, inc, 31);
+          int nd = t ? (int)((uint32_t)in[r].y & LEN_MASK) + 2 : 0;
+          for (int o = 16; o > 0; o >>= 1) nd += __shfl_xor_sync(kFull, nd, o);
+          need += nd;
+        }
+        if (lane == 0) s_need = need;
+      }
+      if (threadIdx.x == 0) s_ntips = 0;
+      __syncthreads();
+      if (n + ntips > kLongRec || s_top + s_need > arena_cap) { spill = true; break; }  // uniform
+      depth++;
+      __syncthreads();
+      // untouched records are pointer copies; tipped ones are split by a warp each
+      for (int r = threadIdx.x; r < n; r += blockDim.x)
+        if (!((uint32_t)in[r].y & F_TIP)) out[s_out[r]] = in[r];
+      int t_idx = 0;
+      for (int r = 0; r < n; r++) {
+        if (!((uint32_t)in[r].y & F_TIP)) continue;
+        int mine = (t_idx++ % kLongWarps) == wib;
+        if (!mine) continue;
+        auto alloc = [&](long long m) -> int32_t* {
+          int o = 0;
+          if (lane == 0) o = atomicAdd(&s_top, (int)m);
+          o = __shfl_sync(kFull, o, 0);
+          if (o + m > arena_cap) return nullptr;
+          return arena + o;
+        };
+        int32_t *A, *B;
+        int al, bl;
+        bool ok = warp_split_tip(c, arena + in[r].x, (int)((uint32_t)in[r].y & LEN_MASK), i, fan, back, lane, alloc,
+                                 &A, &al, &B, &bl);
+        if (!ok) {
+          if (lane == 0) atomicCAS(&s_fail, 0, 1);
+          continue;
+        }
+        uint32_t fa = warp_tip_flag(A, al, lane), fb = warp_tip_flag(B, bl, lane);
+        if (lane == 0) {
+          int o = s_out[r];
+          out[o] = make_int2((int)(A - arena), (int)((uint32_t)al | fa));
+          out[o + 1] = make_int2((int)(B - arena), (int)((uint32_t)bl | fb));
+          atomicAdd(&s_ntips, (fa ? 1 : 0) + (fb ? 1 : 0));
+        }
+      }
+      __syncthreads();
+      splits += ntips;
+      n += ntips;
+      ntips = s_ntips;
+      cur ^= 1;
+      if (s_fail) {
+        bad = true;  // (the arena cannot overflow: capacity was checked before the round)
+        break;
+      }
+    }
+    if (bad) {
+      if (threadIdx.x == 0) { item_state[w] = 1; item_list[w] = -1; item_n[w] = 0; }
+      continue;
+    }
+    // leaves (or the state before an unsplit round) -> global pool
+    int2* fin = recs + cur * kLongRec;
+    __shared__ long long s_base;
+    __shared__ int s_tot;
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int r = 0; r < n; r++) tot += (int)((uint32_t)fin[r].y & LEN_MASK);
+      s_tot = tot;
+      s_base = palloc(c, tot + 2 * (long long)n);
+    }
+    __syncthreads();
+    if (s_base < 0) {
+      if (threadIdx.x == 0) { report(c.st, K_POOL, i); item_state[w] = 1; item_list[w] = -1; item_n[w] = 0; }
+      continue;
+    }
+    long long list = s_base + s_tot;
+    if (wib == 0) {
+      int carry = 0;
+      for (int base = 0; base < n; base += 32) {
+        int r = base + lane;
+        int ln = r < n ? (int)((uint32_t)fin[r].y & LEN_MASK) : 0;
+        int inc = ln;
+        for (int o = 1; o < 32; o <<= 1) {
+          int y = __shfl_up_sync(kFull, inc, o);
+          if (lane >= o) inc += y;
+        }
+        if (r < n) {
+          c.pool[list + 2 * r] = (int32_t)(s_base + carry + inc - ln);
+          c.pool[list + 2 * r + 1] = fin[r].y;
+        }
+        carry += __shfl_sync(kFull, inc, 31);
+      }
+    }
+    __syncthreads();
+    for (int r = wib; r < n; r += kLongWarps) {
+      uint32_t ro = (uint32_t)c.pool[list + 2 * r];
+      int ln = (int)((uint32_t)fin[r].y & LEN_MASK);
+      const int32_t* src = arena + fin[r].x;
+      warp_copy(c.pool + ro, ln, lane, [&](int k) { return src[k]; });
+    }
+    __syncthreads();
+    if (spill) {
+      // record list too long for shared memory: the warp kernel continues
+      if (threadIdx.x == 0) { item_state[w] = 2; item_list[w] = list; item_n[w] = n; item_depth[w] = (int)depth; }
+      if (threadIdx.x == 0 && splits) atomicAdd(stats + 1, (unsigned long long)splits);
+      continue;
+    }
+    if (wib == 0) {
+      // leaf flags from shared memory (fast), then the common epilogue
+      unsigned long long ex_sum = 0;
+      for (int r = 0; r < n; r++) {
+        int ln = (int)((uint32_t)fin[r].y & LEN_MASK);
+        int ex = warp_extra_visits(arena + fin[r].x, ln, lane);
+        if (ex > 0 && lane == 0) c.pool[list + 2 * r + 1] = (int32_t)((uint32_t)fin[r].y | F_REP);
+        ex_sum += ex;
+      }
+      if (lane == 0) {
+        item_state[w] = 1;
+        item_list[w] = list;
+        item_n[w] = n;
+        if (depth > 0) atomicMax(stats + 0, (unsigned long long)depth);
+        if (splits) atomicAdd(stats + 1, (unsigned long long)splits);
+        if (ex_sum) atomicAdd(stats + 5, ex_sum);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -931,8 +1239,24 @@ void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, in
 
 void launch_repair_tips(const RepairArgs& a, cudaStream_t s) {
   RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st};
-  k_repair_tips<<<kNumSMs * 8, 32 * kTipWarps, 0, s>>>(c, a.items, a.n_items, a.off, a.v, a.item_list, a.item_n, a.stats);
-  note_launch(1);
+  static bool attr = false;
+  size_t smem = long_smem_bytes();
+  if (!attr) {
+    cudaFuncSetAttribute(k_repair_tips_long, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  static int arena_cap = -1;
+  if (arena_cap < 0) {  // testing hook: TERMESH_LONG_ARENA shrinks the shared arena to exercise spills
+    const char* e = getenv("TERMESH_LONG_ARENA");
+    arena_cap = (e && *e) ? atoi(e) : kLongArena;
+    if (arena_cap > kLongArena) arena_cap = kLongArena;
+  }
+  k_repair_tips_long<<<kNumSMs, 32 * kLongWarps, smem, s>>>(c, a.items, a.n_items, a.off, a.v, a.item_list,
+                                                             a.item_n, a.item_state, a.item_depth, a.stats,
+                                                             arena_cap);
+  k_repair_tips<<<kNumSMs * 8, 32 * kTipWarps, 0, s>>>(c, a.items, a.n_items, a.off, a.v, a.item_list, a.item_n,
+                                                       a.item_state, a.item_depth, a.stats);
+  note_launch(2);
 }
 
 void launch_repair_pinch(const RepairArgs& a, cudaStream_t s) {
