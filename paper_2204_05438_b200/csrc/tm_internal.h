@@ -48,6 +48,13 @@ void launch_ruler_write(const int32_t* tri, const int32_t* hw, const int64_t* n_
                         cudaStream_t s);
 
 // tm_repair.cu
+struct LongQueue {       // work items longer than kLongMin, longest class first
+  int32_t* huge;
+  int32_t* longq;
+  unsigned int* n_huge;
+  unsigned int* n_long;
+  unsigned int* next;
+};
 struct RepairArgs {
   const int32_t* tri;
   int32_t* hw;
@@ -70,10 +77,11 @@ struct RepairArgs {
   int32_t* item_state;   // 0 todo, 1 done (shared-memory kernel), 2 resume, 3 warp kernel from scratch
   int32_t* item_depth;
   unsigned long long* stats;
+  LongQueue q;
 };
 void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, int32_t* item_of,
                      int32_t* items, unsigned int* n_items, int32_t* long_list, unsigned int* n_long,
-                     unsigned long long* stats, cudaStream_t s);
+                     unsigned long long* stats, LongQueue q, cudaStream_t s);
 void launch_repair_tips(const RepairArgs& a, cudaStream_t s);
 void launch_repair_pinch(const RepairArgs& a, cudaStream_t s);
 void launch_out_counts(const int64_t* off, const int64_t* Pp, int64_t Pcap, const int32_t* item_of,

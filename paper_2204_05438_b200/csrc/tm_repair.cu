@@ -31,6 +31,8 @@
 
 namespace tmb {
 
+constexpr int kLongMin = 96;    // items longer than this go to k_repair_tips_long first
+constexpr int kHugeMin = 512;   // ... and the longest ones are dequeued first
 constexpr uint32_t F_TIP = 1u << 30;
 constexpr uint32_t F_REP = 1u << 31;
 constexpr uint32_t F_FAIL = 1u << 29;
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(256) k_classify_long(const int64_t* __restrict
                                                        const int32_t* __restrict__ long_list,
                                                        const unsigned int* n_long, int32_t* __restrict__ item_of,
                                                        int32_t* __restrict__ items, unsigned int* n_items,
-                                                       unsigned long long* stats) {
+                                                       unsigned long long* stats, LongQueue q) {
   __shared__ int32_t tab[kSetCap];
   __shared__ unsigned int dups;
   unsigned int nl = *n_long;
@@ -230,6 +232,8 @@ __global__ void __launch_bounds__(256) k_classify_long(const int64_t* __restrict
       item_of[i] = (int32_t)k;
       atomicAdd(stats + 2, (unsigned long long)dups);
       atomicAdd(stats + 6, 1ull);
+      if (n > kHugeMin) q.huge[atomicAdd(q.n_huge, 1u)] = (int32_t)k;
+      else if (n > kLongMin) q.longq[atomicAdd(q.n_long, 1u)] = (int32_t)k;
     }
     __syncthreads();
   }
@@ -606,7 +610,6 @@ __device__ bool warp_split_tip(const RepairCtx& c, const int32_t* X, int L, int3
 // ------------------------------------------------------------ tip phase, global pool
 // Item states (item_state[w]): 0 = not started, 1 = finished by the shared-
 // memory kernel, 2 = resume from item_list/item_n/item_depth in the pool.
-constexpr int kLongMin = 96;  // items longer than this go to k_repair_tips_long first
 
 __device__ void finish_item(const RepairCtx& c, int64_t w, long long list, int n, long long depth, long long splits,
                             int lane, int64_t* item_list, int32_t* item_n, unsigned long long* stats) {
@@ -766,7 +769,8 @@ __global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx 
                                                                       int32_t* __restrict__ item_n,
                                                                       int32_t* __restrict__ item_state,
                                                                       int32_t* __restrict__ item_depth,
-                                                                      unsigned long long* stats, int arena_cap) {
+                                                                      unsigned long long* stats, int arena_cap,
+                                                                      LongQueue q) {
   extern __shared__ __align__(16) int32_t smem[];
   int32_t* arena = smem;
   int2* recs = reinterpret_cast<int2*>(arena + kLongArena);  // layout uses the full size  // [2][kLongRec] {offset, len|flags}
@@ -776,13 +780,21 @@ __global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx 
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   int32_t* fan = fans + wib * kFanCap;
   int32_t* back = fans + (kLongWarps + wib) * kFanCap;
-  unsigned int ni = *n_items;
+  (void)n_items;
   long long max_rounds = (long long)stats[2] + 1;
-  for (unsigned int w = blockIdx.x; w < ni; w += gridDim.x) {
+  // dynamic queue, longest class first (the hull-sliver lineage sets the critical path)
+  const unsigned int nh = *q.n_huge, nq = nh + *q.n_long;
+  __shared__ unsigned int s_w;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_w = atomicAdd(q.next, 1u);
+    __syncthreads();
+    unsigned int qi = s_w;
+    if (qi >= nq) break;
+    unsigned int w = qi < nh ? (unsigned int)q.huge[qi] : (unsigned int)q.longq[qi - nh];
     int32_t i = items[w];
     int64_t b = off[i];
     int L = (int)(off[i + 1] - b);
-    if (L <= kLongMin) continue;
     if (L + 2 > arena_cap) {  // does not fit: the warp kernel does it from scratch
       if (threadIdx.x == 0) item_state[w] = 3;
       continue;
@@ -1230,10 +1242,10 @@ static inline int grid_for(int64_t n, int block) {
 
 void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, int32_t* item_of,
                      int32_t* items, unsigned int* n_items, int32_t* long_list, unsigned int* n_long,
-                     unsigned long long* stats, cudaStream_t s) {
+                     unsigned long long* stats, LongQueue q, cudaStream_t s) {
   k_classify<<<grid_for(Pcap, 256), 256, 0, s>>>(off, v, Pp, item_of, items, n_items, long_list, n_long, stats);
   note_launch(1);
-  k_classify_long<<<kNumSMs * 4, 256, 0, s>>>(off, v, long_list, n_long, item_of, items, n_items, stats);
+  k_classify_long<<<kNumSMs * 4, 256, 0, s>>>(off, v, long_list, n_long, item_of, items, n_items, stats, q);
   note_launch(1);
 }
 
@@ -1253,7 +1265,7 @@ void launch_repair_tips(const RepairArgs& a, cudaStream_t s) {
   }
   k_repair_tips_long<<<kNumSMs, 32 * kLongWarps, smem, s>>>(c, a.items, a.n_items, a.off, a.v, a.item_list,
                                                              a.item_n, a.item_state, a.item_depth, a.stats,
-                                                             arena_cap);
+                                                             arena_cap, a.q);
   k_repair_tips<<<kNumSMs * 8, 32 * kTipWarps, 0, s>>>(c, a.items, a.n_items, a.off, a.v, a.item_list, a.item_n,
                                                        a.item_state, a.item_depth, a.stats);
   note_launch(2);
