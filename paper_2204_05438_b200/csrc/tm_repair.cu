@@ -452,13 +452,14 @@ __device__ int warp_collect_fan(const RepairCtx& c, int32_t v, int32_t* fan, int
 // reparation.py:127-145: the ((k-1)//2)-th non-frontier half-edge of the fan
 // rotated to start at the barrier half-edge (target == barrier, frontier).
 __device__ int32_t warp_middle_internal_edge(const RepairCtx& c, int32_t v, int32_t barrier, int32_t poly,
-                                             int32_t* fan, int32_t* back, int lane) {
+                                             int32_t* fan, int32_t* back, int lane, bool quiet = false) {
   int deg = warp_collect_fan(c, v, fan, back, lane);
   if (deg < 0) {
-    if (lane == 0) report(c.st, K_STRUCT, poly);
+    if (lane == 0 && !quiet) report(c.st, K_STRUCT, poly);
     return -1;
   }
   if (deg > kFanCap) {
+    if (quiet) return -1;  // precompute: leave it to the exact on-the-fly path
     int32_t e = -1;
     if (lane == 0) e = middle_internal_edge(c, v, barrier, poly);
     return __shfl_sync(kFull, e, 0);
@@ -479,11 +480,11 @@ __device__ int32_t warp_middle_internal_edge(const RepairCtx& c, int32_t v, int3
     imask |= (unsigned long long)ii << base;
   }
   if (bmask == 0) {
-    if (lane == 0) report(c.st, K_BARRIER, poly);
+    if (lane == 0 && !quiet) report(c.st, K_BARRIER, poly);
     return -1;
   }
   if (imask == 0) {
-    if (lane == 0) report(c.st, K_NO_INTERNAL, poly);
+    if (lane == 0 && !quiet) report(c.st, K_NO_INTERNAL, poly);
     return -1;
   }
   int at = __ffsll((long long)bmask) - 1;
@@ -533,61 +534,86 @@ __device__ int warp_rewalk_split(const RepairCtx& c, int32_t e, int32_t te, int 
   return 1;
 }
 
-// Tip split of piece X (len L) at its first tip (reparation.py:294-312
-// splitter), warp-cooperative arc copy with the re-walk as
-// fallback.  Pieces are written through alloc (global pool or shared arena).
-template <typename Alloc>
-__device__ bool warp_split_tip(const RepairCtx& c, const int32_t* X, int L, int32_t poly, int32_t* fan,
-                               int32_t* back, int lane, Alloc alloc, int32_t** A_out, int* la_out, int32_t** B_out,
-                               int* lb_out) {
-  int pos = warp_first_tip(X, L, lane);
-  if (pos < 0) {
-    if (lane == 0) report(c.st, K_STRUCT, poly);
-    return false;
-  }
-  int32_t v = X[pos], b = X[pos == 0 ? L - 1 : pos - 1];
-  int32_t e = warp_middle_internal_edge(c, v, b, poly, fan, back, lane);
+// Everything a tip split needs from the mesh (reparation.py:127-145, 216-220):
+// the promoted edge e = v->u and its twin, the incoming boundary vertex a_in of
+// the visit of u whose wedge holds twin(e), and the directed boundary pairs
+// (oa,ga) / (ob,gb) of h0 = smallest frontier slot of e/3 and twin(e)/3 after
+// the promotion (where the reference re-walks start).
+struct SplitInfo {
+  int32_t e, te, u, a_in, oa, ga, ob, gb;
+};
+
+// smallest frontier slot of triangle t when slot `forced` counts as frontier
+__device__ __forceinline__ int32_t min_slot_with(const int32_t* hw, int32_t t, int32_t forced) {
+  int32_t b = 3 * t;
+  int32_t w0 = hw[b], w1 = hw[b + 1], w2 = hw[b + 2];
+  if (hw_front(w0) || forced == b) return b;
+  if (hw_front(w1) || forced == b + 1) return b + 1;
+  if (hw_front(w2) || forced == b + 2) return b + 2;
+  return -1;
+}
+
+// Computes the split of tip vertex v (barrier b) from the current frontier.
+// promote_now: also set the frontier bits of e and twin(e).  quiet: do not
+// report failures (precomputation).  Warp-uniform result.
+__device__ bool warp_split_info(const RepairCtx& c, int32_t v, int32_t b, int32_t poly, int32_t* fan, int32_t* back,
+                                int lane, bool promote_now, bool quiet, SplitInfo* out) {
+  int32_t e = warp_middle_internal_edge(c, v, b, poly, fan, back, lane, quiet);
   if (e < 0) return false;
-  int32_t te = hw_twin(c.hw[e]);
-  if (te < 0) {
-    if (lane == 0) report(c.st, K_STRUCT, poly);
-    return false;
-  }
-  int32_t u = he_target(c.tri, e);
-  // incoming boundary vertex of the visit of u whose wedge holds twin(e):
-  // rotate CCW from twin(e) until the crossed edge prev(g) is frontier
-  int32_t a_in = -1;
+  SplitInfo s{};
   if (lane == 0) {
-    int32_t g = te;
-    long long guard = 3 * c.T + 3;
-    for (long long s = 0; s < guard; s++) {
-      int32_t p = he_prev(g);
-      int32_t w = c.hw[p];
-      if (hw_front(w)) { a_in = he_origin(c.tri, p); break; }
-      g = hw_twin(w);
+    s.e = e;
+    s.te = hw_twin(c.hw[e]);
+    s.u = he_target(c.tri, e);
+    s.a_in = -1;
+    if (s.te >= 0) {
+      // rotate CCW from twin(e) until the crossed edge prev(g) is frontier
+      int32_t g = s.te;
+      long long guard = 3 * c.T + 3;
+      for (long long k = 0; k < guard; k++) {
+        int32_t p = he_prev(g);
+        int32_t w = c.hw[p];
+        if (hw_front(w)) { s.a_in = he_origin(c.tri, p); break; }
+        g = hw_twin(w);
+      }
+      if (promote_now) promote(c, e, s.te);
+      int32_t ha = min_slot_with(c.hw, e / 3, e), hb = min_slot_with(c.hw, s.te / 3, s.te);
+      s.oa = he_origin(c.tri, ha); s.ga = he_target(c.tri, ha);
+      s.ob = he_origin(c.tri, hb); s.gb = he_target(c.tri, hb);
     }
   }
-  a_in = __shfl_sync(kFull, a_in, 0);
+  __syncwarp();
+  s.e = __shfl_sync(kFull, s.e, 0); s.te = __shfl_sync(kFull, s.te, 0);
+  s.u = __shfl_sync(kFull, s.u, 0); s.a_in = __shfl_sync(kFull, s.a_in, 0);
+  s.oa = __shfl_sync(kFull, s.oa, 0); s.ga = __shfl_sync(kFull, s.ga, 0);
+  s.ob = __shfl_sync(kFull, s.ob, 0); s.gb = __shfl_sync(kFull, s.gb, 0);
+  if (s.te < 0) {
+    if (lane == 0 && !quiet) report(c.st, K_STRUCT, poly);
+    return false;
+  }
+  *out = s;
+  return true;
+}
+
+// Arc split of piece X at tip position pos with the (already promoted) split
+// info, re-walk fallback with the strict length law.
+template <typename Alloc>
+__device__ bool warp_split_arcs(const RepairCtx& c, const int32_t* X, int L, int pos, const SplitInfo& s,
+                                int32_t poly, int lane, Alloc alloc, int32_t** A_out, int* la_out, int32_t** B_out,
+                                int* lb_out) {
+  const int32_t v = X[pos], u = s.u, a_in = s.a_in;
   int j = -1;
   if (a_in >= 0)
     j = warp_find_first(L, lane, [&](int q) { return X[q] == u && X[q == 0 ? L - 1 : q - 1] == a_in; });
-  int32_t oa = 0, ga = 0, ob = 0, gb = 0;
-  if (lane == 0) {
-    promote(c, e, te);
-    int32_t ha = min_frontier_slot(c.hw, e / 3), hb = min_frontier_slot(c.hw, te / 3);
-    oa = he_origin(c.tri, ha); ga = he_target(c.tri, ha);
-    ob = he_origin(c.tri, hb); gb = he_target(c.tri, hb);
-  }
-  __syncwarp();
-  oa = __shfl_sync(kFull, oa, 0); ga = __shfl_sync(kFull, ga, 0);
-  ob = __shfl_sync(kFull, ob, 0); gb = __shfl_sync(kFull, gb, 0);
   if (j >= 0) {
     int la = 1 + wrap_idx(pos - j, L), lb = wrap_idx(j - pos, L) + 1;
     // pa arc: A(0) = v, A(k) = X[(j+k-1) % L]; pb arc: B(k) = X[(pos+k) % L] (k < lb-1), B(lb-1) = u
     auto A_at = [&](int k) { return k == 0 ? v : X[wrap_idx(j + k - 1, L)]; };
     auto B_at = [&](int k) { return k == lb - 1 ? u : X[wrap_idx(pos + k, L)]; };
-    int ka = warp_find_first(la, lane, [&](int k) { return A_at(k) == oa && A_at(k + 1 == la ? 0 : k + 1) == ga; });
-    int kb = warp_find_first(lb, lane, [&](int k) { return B_at(k) == ob && B_at(k + 1 == lb ? 0 : k + 1) == gb; });
+    int ka = warp_find_first(la, lane,
+                             [&](int k) { return A_at(k) == s.oa && A_at(k + 1 == la ? 0 : k + 1) == s.ga; });
+    int kb = warp_find_first(lb, lane,
+                             [&](int k) { return B_at(k) == s.ob && B_at(k + 1 == lb ? 0 : k + 1) == s.gb; });
     if (ka >= 0 && kb >= 0) {
       int32_t* A = alloc(la + lb);
       if (A == nullptr) {
@@ -602,9 +628,25 @@ __device__ bool warp_split_tip(const RepairCtx& c, const int32_t* X, int L, int3
       return true;
     }
   }
-  int r = warp_rewalk_split(c, e, te, L, poly, alloc, lane, A_out, la_out, B_out, lb_out);
+  int r = warp_rewalk_split(c, s.e, s.te, L, poly, alloc, lane, A_out, la_out, B_out, lb_out);
   if (r == 0 && lane == 0) report(c.st, K_SPLIT_LAW, poly);
   return r == 1;
+}
+
+// Tip split of piece X (len L) at its first tip (reparation.py:294-312 splitter).
+template <typename Alloc>
+__device__ bool warp_split_tip(const RepairCtx& c, const int32_t* X, int L, int32_t poly, int32_t* fan,
+                               int32_t* back, int lane, Alloc alloc, int32_t** A_out, int* la_out, int32_t** B_out,
+                               int* lb_out) {
+  int pos = warp_first_tip(X, L, lane);
+  if (pos < 0) {
+    if (lane == 0) report(c.st, K_STRUCT, poly);
+    return false;
+  }
+  int32_t v = X[pos], b = X[pos == 0 ? L - 1 : pos - 1];
+  SplitInfo s;
+  if (!warp_split_info(c, v, b, poly, fan, back, lane, true, false, &s)) return false;
+  return warp_split_arcs(c, X, L, pos, s, poly, lane, alloc, A_out, la_out, B_out, lb_out);
 }
 
 // ------------------------------------------------------------ tip phase, global pool
@@ -755,10 +797,13 @@ __global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, con
 // the current pieces are written to the global pool and the warp kernel
 // resumes the item (item_state = 2).
 constexpr int kLongWarps = 8;
-constexpr int kLongArena = 36 * 1024;  // ints (144 KiB)
+constexpr int kLongArena = 32 * 1024;  // ints (128 KiB)
 constexpr int kLongRec = 1024;         // records per list
+constexpr int kMaxTips = 1024;         // precomputed tips per item
+constexpr int kMaxTouch = 2048;        // promoted-edge endpoints per item
 size_t long_smem_bytes() {
-  return (size_t)kLongArena * 4 + 2 * (size_t)kLongRec * 8 + 2 * (size_t)kLongWarps * kFanCap * 4 + 64;
+  return (size_t)kLongArena * 4 + 2 * (size_t)kLongRec * 8 + 2 * (size_t)kLongWarps * kFanCap * 4 +
+         (size_t)kMaxTips * 4 * 2 + (size_t)kMaxTips * sizeof(SplitInfo) + (size_t)kMaxTouch * 4 + 64;
 }
 
 __global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx c, const int32_t* __restrict__ items,
@@ -773,8 +818,13 @@ __global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx 
                                                                       LongQueue q) {
   extern __shared__ __align__(16) int32_t smem[];
   int32_t* arena = smem;
-  int2* recs = reinterpret_cast<int2*>(arena + kLongArena);  // layout uses the full size  // [2][kLongRec] {offset, len|flags}
+  int2* recs = reinterpret_cast<int2*>(arena + kLongArena);  // [2][kLongRec] {offset, len|flags}
   int32_t* fans = reinterpret_cast<int32_t*>(recs + 2 * kLongRec);
+  int32_t* tipv = fans + 2 * kLongWarps * kFanCap;  // tip vertex (or -1 when its info is unusable)
+  int32_t* tipb = tipv + kMaxTips;                  // barrier vertex
+  SplitInfo* tipinfo = reinterpret_cast<SplitInfo*>(tipb + kMaxTips);
+  int32_t* touched = reinterpret_cast<int32_t*>(tipinfo + kMaxTips);
+  __shared__ int s_ntip, s_ntouch;
   __shared__ int s_top, s_fail, s_ntips;
   __shared__ int s_out[kLongRec];  // output index of each input record
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -804,8 +854,31 @@ __global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx 
     if (threadIdx.x == 0) { s_top = L; s_fail = 0; }
     __syncthreads();
     int cur = 0, n = 1;
+    if (threadIdx.x == 0) { s_ntip = 0; s_ntouch = 0; }
+    __syncthreads();
+    // Every tip of the item is a tip of its initial polygon (an arc split only
+    // removes the split tip), and its split edge depends only on the frontier
+    // around v and u.  So the mesh rotations for all tips run up front, in
+    // parallel; a round reuses them unless an earlier promotion touched v or u.
+    for (int p = threadIdx.x; p < L; p += blockDim.x) {
+      int32_t a = arena[p == 0 ? L - 1 : p - 1];
+      if (a == arena[p + 1 == L ? 0 : p + 1]) {
+        int k = atomicAdd(&s_ntip, 1);
+        if (k < kMaxTips) { tipv[k] = arena[p]; tipb[k] = a; }
+      }
+    }
+    __syncthreads();
+    const int ntip_pre = s_ntip < kMaxTips ? s_ntip : kMaxTips;
+    for (int k = wib; k < ntip_pre; k += kLongWarps) {
+      SplitInfo si;
+      bool ok = warp_split_info(c, tipv[k], tipb[k], i, fan, back, lane, false, true, &si);
+      if (lane == 0) {
+        tipinfo[k] = si;
+        if (!ok) tipv[k] = -1;
+      }
+    }
     if (wib == 0) {
-      uint32_t f0 = warp_tip_flag(arena, L, lane);
+      uint32_t f0 = s_ntip > 0 ? F_TIP : 0u;
       if (lane == 0) { recs[0] = make_int2(0, (int)((uint32_t)L | f0)); s_ntips = f0 ? 1 : 0; }
     }
     __syncthreads();
@@ -845,6 +918,7 @@ __global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx 
       __syncthreads();
       if (n + ntips > kLongRec || s_top + s_need > arena_cap) { spill = true; break; }  // uniform
       depth++;
+      const int ntouch0 = s_ntouch < kMaxTouch ? s_ntouch : -1;  // -1: overflowed, always recompute
       __syncthreads();
       // untouched records are pointer copies; tipped ones are split by a warp each
       for (int r = threadIdx.x; r < n; r += blockDim.x)
@@ -863,8 +937,40 @@ __global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx 
         };
         int32_t *A, *B;
         int al, bl;
-        bool ok = warp_split_tip(c, arena + in[r].x, (int)((uint32_t)in[r].y & LEN_MASK), i, fan, back, lane, alloc,
-                                 &A, &al, &B, &bl);
+        const int32_t* X = arena + in[r].x;
+        const int Lr = (int)((uint32_t)in[r].y & LEN_MASK);
+        bool ok = false;
+        int pos = warp_first_tip(X, Lr, lane);
+        if (pos < 0) {
+          if (lane == 0) report(c.st, K_STRUCT, i);
+        } else {
+          int32_t v = X[pos], bv = X[pos == 0 ? Lr - 1 : pos - 1];
+          int k = warp_find_first(ntip_pre, lane, [&](int q) { return tipv[q] == v; });
+          SplitInfo si;
+          bool use = k >= 0 && ntouch0 >= 0;
+          if (use) {
+            si = tipinfo[k];
+            bool stale = warp_find_first(ntouch0, lane, [&](int q) {
+                           int32_t x = touched[q];
+                           return x == v || x == si.u;
+                         }) >= 0;
+            use = !stale;
+          }
+          if (use) {
+            if (lane == 0) promote(c, si.e, si.te);
+            __syncwarp();
+            ok = true;
+          } else {
+            ok = warp_split_info(c, v, bv, i, fan, back, lane, true, false, &si);
+          }
+          if (ok) {
+            if (lane == 0) {
+              int tk = atomicAdd(&s_ntouch, 2);
+              if (tk + 2 <= kMaxTouch) { touched[tk] = v; touched[tk + 1] = si.u; }
+            }
+            ok = warp_split_arcs(c, X, Lr, pos, si, i, lane, alloc, &A, &al, &B, &bl);
+          }
+        }
         if (!ok) {
           if (lane == 0) atomicCAS(&s_fail, 0, 1);
           continue;
