@@ -100,6 +100,8 @@ int tm_ctx_set_profiling(tm_ctx *ctx, int on);
 int tm_ctx_segment_ms(tm_ctx *ctx, double *ms, int64_t *counts, int n, int reset);
 const char *tm_segment_name(int k);
 int64_t tm_launch_count(void);
+/* kernel debug timestamps (ns, %globaltimer) of the last run: repair lineage trace */
+int tm_ctx_debug(const tm_ctx *ctx, uint64_t *out, int n);
 
 /* Labels.  tri_bits = 32 or 64 (reference triangles are int64).  check != 0
  * also reports index_range / orientation / degenerate / edge_count /

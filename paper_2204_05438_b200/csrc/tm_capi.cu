@@ -58,6 +58,7 @@ struct Counters {
   unsigned int q_huge, q_long, q_next, pad2;
   unsigned long long pool_top, undo_top;
   unsigned long long stats[8];
+  unsigned long long dbg[64];  // optional kernel timestamps (tm_ctx_debug)
 };
 
 enum Seg {
@@ -417,7 +418,7 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
                &dc->undo_top, (unsigned long long)Tn + 1024, &dc->st, ctx->items.as<int32_t>(), &dc->n_items,
                d_off_in, d_v_in, ctx->item_list.as<int64_t>(), ctx->item_n.as<int32_t>(),
                ctx->item_slots.as<int64_t>(), ctx->item_state.as<int32_t>(), ctx->item_depth.as<int32_t>(),
-               dc->stats, q};
+               dc->stats, q, dc->dbg};
   {
     SegTimer t_(ctx, S_REPAIR_TIPS, s);
     launch_repair_tips(a, s);
@@ -556,6 +557,13 @@ int tm_ctx_segment_ms(tm_ctx* ctx, double* ms, int64_t* counts, int n, int reset
 const char* tm_segment_name(int k) { return (k >= 0 && k < S_NUM) ? kSegNames[k] : ""; }
 
 int64_t tm_launch_count(void) { return g_launches.load(); }
+
+// debug timestamps written by kernels into Counters.dbg during the last run
+int tm_ctx_debug(const tm_ctx* ctx, uint64_t* out, int n) {
+  if (!ctx || !ctx->h_result) return TM_ERR_ARGUMENT;
+  for (int k = 0; k < n && k < 64; k++) out[k] = ctx->h_result->dbg[k];
+  return TM_OK;
+}
 
 int tm_ctx_phase_ms(const tm_ctx* ctx, double* ms3) {
   if (!ctx || !ms3) return TM_ERR_ARGUMENT;

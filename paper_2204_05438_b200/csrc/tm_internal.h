@@ -78,6 +78,7 @@ struct RepairArgs {
   int32_t* item_depth;
   unsigned long long* stats;
   LongQueue q;
+  unsigned long long* dbg;  // 64 timestamp slots (debug)
 };
 void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, int32_t* item_of,
                      int32_t* items, unsigned int* n_items, int32_t* long_list, unsigned int* n_long,

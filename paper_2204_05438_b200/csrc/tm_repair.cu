@@ -815,7 +815,7 @@ __global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx 
                                                                       int32_t* __restrict__ item_state,
                                                                       int32_t* __restrict__ item_depth,
                                                                       unsigned long long* stats, int arena_cap,
-                                                                      LongQueue q) {
+                                                                      LongQueue q, unsigned long long* dbg) {
   extern __shared__ __align__(16) int32_t smem[];
   int32_t* arena = smem;
   int2* recs = reinterpret_cast<int2*>(arena + kLongArena);  // [2][kLongRec] {offset, len|flags}
@@ -842,6 +842,9 @@ __global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx 
     unsigned int qi = s_w;
     if (qi >= nq) break;
     unsigned int w = qi < nh ? (unsigned int)q.huge[qi] : (unsigned int)q.longq[qi - nh];
+    const bool trace = qi == 0 && threadIdx.x == 0;
+    unsigned long long t_ns;
+    if (trace) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ns)); dbg[0] = t_ns; }
     int32_t i = items[w];
     int64_t b = off[i];
     int L = (int)(off[i + 1] - b);
@@ -877,6 +880,8 @@ __global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx 
         if (!ok) tipv[k] = -1;
       }
     }
+    __syncthreads();
+    if (trace) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ns)); dbg[1] = t_ns; dbg[2] = L; dbg[3] = s_ntip; }
     if (wib == 0) {
       uint32_t f0 = s_ntip > 0 ? F_TIP : 0u;
       if (lane == 0) { recs[0] = make_int2(0, (int)((uint32_t)L | f0)); s_ntips = f0 ? 1 : 0; }
@@ -988,6 +993,7 @@ __global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx 
       n += ntips;
       ntips = s_ntips;
       cur ^= 1;
+      if (trace && depth < 56) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ns)); dbg[4 + depth] = t_ns; }
       if (s_fail) {
         bad = true;  // (the arena cannot overflow: capacity was checked before the round)
         break;
@@ -1371,7 +1377,7 @@ void launch_repair_tips(const RepairArgs& a, cudaStream_t s) {
   }
   k_repair_tips_long<<<kNumSMs, 32 * kLongWarps, smem, s>>>(c, a.items, a.n_items, a.off, a.v, a.item_list,
                                                              a.item_n, a.item_state, a.item_depth, a.stats,
-                                                             arena_cap, a.q);
+                                                             arena_cap, a.q, a.dbg);
   k_repair_tips<<<kNumSMs * 8, 32 * kTipWarps, 0, s>>>(c, a.items, a.n_items, a.off, a.v, a.item_list, a.item_n,
                                                        a.item_state, a.item_depth, a.stats);
   note_launch(2);
