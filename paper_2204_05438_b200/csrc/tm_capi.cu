@@ -288,11 +288,11 @@ static int decode_status(tm_ctx* ctx, const Counters& h) {
 }
 
 // ---------------------------------------------------------------- buffers
-static int prepare(tm_ctx* ctx, int64_t T) {
+static int prepare(tm_ctx* ctx, int64_t T, int64_t n = -1) {
   int rc = init_counters(ctx);
   if (rc) return rc;
   int64_t Tn = T > 0 ? T : 1;
-  ENSURE(slots, hash_capacity(Tn) * sizeof(uint32_t));
+  if (n >= 0) ENSURE(slots, hash_bytes(n, Tn));
   ENSURE(seeds, Tn * sizeof(int32_t));
   ENSURE(start, Tn * sizeof(int32_t));
   ENSURE(len, (Tn + 1) * sizeof(int64_t));
@@ -338,16 +338,16 @@ static int prepare(tm_ctx* ctx, int64_t T) {
 static int enqueue_label(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_tri, int tri_bits, int64_t T,
                          int check, int32_t* d_tri32, int32_t* d_hw, int8_t* d_me, uint8_t* d_seed, int32_t* d_tv,
                          cudaStream_t s) {
-  uint64_t cap = hash_capacity(T > 0 ? T : 1);
   Counters* dc = dc_of(ctx);
   {
     SegTimer t_(ctx, S_LABEL_A, s);
-    launch_label_a(d_xy, n, d_tri, tri_bits == 64, T, check, d_tri32, d_hw, d_me, d_tv, ctx->slots.as<uint32_t>(),
-                   cap, &dc->st, s);
+    launch_label_a(d_xy, n, d_tri, tri_bits == 64, T, check, d_tri32, d_hw, d_me, d_seed, d_tv, ctx->slots.p,
+                   &dc->st, s);
   }
   {
     SegTimer t_(ctx, S_LABEL_B, s);
-    launch_label_b(n, T, d_hw, d_me, d_seed, d_tv, s);
+    launch_label_b(tri_bits == 32 && d_tri32 == nullptr ? (const int32_t*)d_tri : d_tri32, n, T, d_hw, d_me, d_seed,
+                   d_tv, ctx->slots.p, check, &dc->st, s);
   }
   CK(cudaGetLastError());
   return TM_OK;
@@ -585,7 +585,7 @@ int tm_label(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_tri, int 
   int rc = check_sizes(ctx, n, T);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  if ((rc = prepare(ctx, T)) || (rc = enqueue_reset(ctx, s))) return rc;
+  if ((rc = prepare(ctx, T, n)) || (rc = enqueue_reset(ctx, s))) return rc;
   if ((rc = enqueue_label(ctx, d_xy, n, d_tri, tri_bits, T, check, d_tri32, d_hw, d_max_edge, d_seed, d_tv, s)))
     return rc;
   Counters h;
@@ -685,7 +685,7 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
                       int check, int64_t* d_off, int32_t* d_v, int64_t* n_polys, int64_t* n_slots, int64_t* stats,
                       cudaStream_t user) {
   int rc = check_sizes(ctx, n, T);
-  if (rc || (rc = prepare(ctx, T))) return rc;
+  if (rc || (rc = prepare(ctx, T, n))) return rc;
   int64_t Tn = T > 0 ? T : 1, nn = n > 0 ? n : 1;
   ENSURE(tri32, 3 * Tn * sizeof(int32_t));
   ENSURE(hw, 3 * Tn * sizeof(int32_t));

@@ -10,14 +10,14 @@ namespace tmb {
 struct DevStatus;
 
 // tm_label.cu
-uint64_t hash_capacity(int64_t T);
+size_t hash_bytes(int64_t n, int64_t T);
 // counts kernels of this library launched (bench.py's gpu_launches)
 void note_launch(int k);
 void launch_label_a(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int check,
-                    int32_t* tri32, int32_t* hw, int8_t* max_edge, int32_t* tv, uint32_t* slots, uint64_t cap,
+                    int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed, int32_t* tv, void* table,
                     DevStatus* st, cudaStream_t s);
-void launch_label_b(int64_t n, int64_t T, int32_t* hw, const int8_t* max_edge, uint8_t* seed, int32_t* tv,
-                    cudaStream_t s);
+void launch_label_b(const int32_t* tri32, int64_t n, int64_t T, int32_t* hw, const int8_t* max_edge, uint8_t* seed,
+                    int32_t* tv, void* table, int check, DevStatus* st, cudaStream_t s);
 void launch_relabel(const int8_t* max_edge, int64_t T, int32_t* hw, uint8_t* seed, cudaStream_t s);
 void launch_check_neighbors(const int32_t* hw, const void* nb, int nb_is64, int64_t T, DevStatus* st, cudaStream_t s);
 void launch_unpack(const int32_t* hw, int64_t T, int32_t* twin, uint8_t* fr, cudaStream_t s);

@@ -6,32 +6,128 @@
 // label_seeds / label_frontiers (labeling.py:46-115).  The reference receives
 // `neighbors` from Qhull; here adjacency is derived from the triangle list.
 //
-// Pass A (per triangle, HBM-bound gather): corners -> tri32, three fp64 squared
-//   lengths computed UNFUSED (__dmul_rn/__dadd_rn; numpy's ((b-c)**2).sum is
-//   dx*dx + dy*dy with two roundings), first-max argmax -> max_edge;
-//   signed-area validation; atomicMin trivertex; and insertion of the three
-//   undirected edge keys into an open-addressing hash table of int32 half-edge
-//   ids (linear probing, load <= 0.5).  The second arrival of a key claims the
-//   slot with a MATCHED bit and writes both twins.  A third arrival is an
-//   edge shared by >2 triangles (validate's "edge_count"); equal direction is a
-//   reciprocity/orientation defect.
-// Pass B (per triangle): frontier / seed from max_edge of both sides, written
-//   as packed words hw = (twin << 1) | frontier (in place over the twin array).
+// Two passes over the triangles, no sort:
+// Pass A (per triangle): corners -> tri32, three fp64 squared lengths computed
+//   UNFUSED (__dmul_rn/__dadd_rn; numpy's ((b-c)**2).sum is dx*dx + dy*dy with
+//   two roundings), first-max argmax -> max_edge; signed-area
+//   validation; atomicMin trivertex; and insertion of every ASCENDING
+//   half-edge (origin < target) into an open-addressing table keyed by the
+//   packed (min, max) vertex pair (u64 keys, u32 half-edge values, linear
+//   probing, load <= 0.75).  One CAS per undirected edge, no contention: in a
+//   valid mesh each key has exactly one ascending half-edge.
+// Pass B (per triangle): every DESCENDING half-edge looks its partner up
+//   (read-only probes) and writes the packed words hw = (twin << 1) | frontier
+//   of both half-edges plus the seed flags of both triangles, so K0's twin
+//   build and K2's labels finish in the same pass.
 #include "tm_common.cuh"
 #include "tm_internal.h"
 
 namespace tmb {
 
-constexpr uint32_t kEmpty = 0xFFFFFFFFu;
-constexpr uint32_t kMatched = 0x80000000u;
+// ---------------------------------------------------------------- twin table
+// Bucketed open addressing with quotienting.  The undirected edge key
+// (lo << b) | hi (K = 2b bits) goes through an invertible K-bit mix x; the top
+// q bits of x pick the home bucket, the low R = K - q bits ("remainder") plus
+// the bucket displacement d identify the key exactly, so a slot holds the
+// whole entry in 64 bits:  [ remainder | d (kDispBits) | half-edge (hb) ].
+// A bucket is 4 slots = one 32-byte sector, so a probe is one sector load.
+// Slots of a bucket fill in order and are never cleared, so a lookup may stop
+// at the first bucket with an empty slot.
+constexpr unsigned long long kEmptySlot = ~0ull;
+constexpr unsigned long long kClaimBit = 1ull << 63;
+constexpr int kDispBits = 6;
+constexpr int kMaxDisp = (1 << kDispBits) - 1;
 
-__device__ __forceinline__ uint64_t mix64(uint64_t k) {
-  k ^= k >> 33;
-  k *= 0xff51afd7ed558ccdULL;
-  k ^= k >> 33;
-  k *= 0xc4ceb9fe1a85ec53ULL;
-  k ^= k >> 33;
-  return k;
+struct TwinTable {
+  unsigned long long* slots;  // 4 * nb
+  uint64_t nb_mask;           // nb - 1 (nb = 2^q buckets)
+  int K, b, R, hb;
+};
+
+__device__ __forceinline__ uint64_t mixK(uint64_t x, int K) {
+  const uint64_t M = (K >= 64) ? ~0ull : ((1ull << K) - 1);
+  const int s = (K + 1) >> 1;
+  x = (x * 0x9E3779B97F4A7C15ull) & M;
+  x ^= x >> s;
+  x = (x * 0xD6E8FEB86659FD93ull) & M;
+  x ^= x >> s;
+  return x;
+}
+
+struct Probe {
+  uint64_t home;
+  uint64_t tag;  // (remainder << kDispBits) at displacement 0
+};
+
+__device__ __forceinline__ Probe probe_of(const TwinTable& tb, int32_t lo, int32_t hi) {
+  uint64_t key = ((uint64_t)(uint32_t)lo << tb.b) | (uint32_t)hi;
+  uint64_t x = mixK(key, tb.K);
+  Probe p;
+  p.home = (x >> tb.R) & tb.nb_mask;
+  p.tag = (x & ((1ull << tb.R) - 1)) << kDispBits;
+  return p;
+}
+
+__device__ __forceinline__ void load_bucket_cg(const unsigned long long* s, unsigned long long (&v)[4]) {
+  ulonglong2 a = __ldcg(reinterpret_cast<const ulonglong2*>(s));
+  ulonglong2 b = __ldcg(reinterpret_cast<const ulonglong2*>(s) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+
+__device__ __forceinline__ void load_bucket_nc(const unsigned long long* s, unsigned long long (&v)[4]) {
+  ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(s));
+  ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(s) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+
+// Insert ascending half-edge h = lo -> hi.  In a valid mesh each key has one
+// ascending half-edge; a second one is an orientation / reciprocity defect.
+__device__ __forceinline__ void table_insert(const TwinTable& tb, DevStatus* st, int32_t h, int32_t lo, int32_t hi) {
+  Probe p = probe_of(tb, lo, hi);
+  for (int d = 0; d <= kMaxDisp; d++) {
+    unsigned long long* bk = tb.slots + 4 * ((p.home + d) & tb.nb_mask);
+    const uint64_t tag = p.tag | (uint64_t)d;
+    const unsigned long long mine = (tag << tb.hb) | (uint32_t)h;
+    unsigned long long v[4];
+    load_bucket_cg(bk, v);
+    int s = 0;
+    while (s < 4) {
+      if (v[s] == kEmptySlot) {
+        unsigned long long prev = atomicCAS(bk + s, kEmptySlot, mine);
+        if (prev == kEmptySlot) return;
+        v[s] = prev;  // lost the race: examine the winner, stay on this slot
+        continue;
+      }
+      if (((v[s] & ~kClaimBit) >> tb.hb) == tag) { report(st, K_RECIPROCITY, h / 3); return; }
+      s++;
+    }
+  }
+  report(st, K_STRUCT, h / 3);  // displacement overflow (> 63 buckets): not seen at load <= 0.7
+}
+
+// Partner of descending half-edge o -> g (key (g, o)); -1 when border.
+__device__ __forceinline__ int32_t table_lookup(const TwinTable& tb, DevStatus* st, int check, int32_t lo, int32_t hi,
+                                                int64_t elem) {
+  Probe p = probe_of(tb, lo, hi);
+  const uint64_t hmask = (1ull << tb.hb) - 1;
+  for (int d = 0; d <= kMaxDisp; d++) {
+    unsigned long long* bk = tb.slots + 4 * ((p.home + d) & tb.nb_mask);
+    const uint64_t tag = p.tag | (uint64_t)d;
+    unsigned long long v[4];
+    load_bucket_nc(bk, v);
+#pragma unroll
+    for (int s = 0; s < 4; s++) {
+      if (v[s] == kEmptySlot) return -1;
+      if (((v[s] & ~kClaimBit) >> tb.hb) == tag) {
+        if (check) {  // a second descending partner: edge shared by > 2 triangles
+          unsigned long long old = atomicOr(bk + s, kClaimBit);
+          if (old & kClaimBit) report(st, K_EDGE_COUNT, elem);
+        }
+        return (int32_t)(v[s] & hmask);
+      }
+    }
+  }
+  return -1;
 }
 
 __device__ __forceinline__ double sqlen(double2 p, double2 q) {
@@ -54,78 +150,144 @@ __device__ __forceinline__ int argmax3(double l0, double l1, double l2) {
   return m;
 }
 
-template <typename TI>
-__device__ __forceinline__ int32_t corner(const TI* tri, int64_t s) { return (int32_t)__ldg(tri + s); }
+constexpr int kLabelThreads = 256;
+constexpr int kLabelWarps = kLabelThreads / 32;
 
-template <typename TI>
-__device__ __forceinline__ void insert_edge(const TI* __restrict__ tri, uint32_t* __restrict__ slots,
-                                            uint64_t cap, int32_t* __restrict__ twin, DevStatus* st,
-                                            int32_t h, int32_t o, int32_t g) {
-  uint32_t lo = (uint32_t)min(o, g), hi = (uint32_t)max(o, g);
-  uint64_t key = ((uint64_t)lo << 32) | hi;
-  uint64_t i = __umul64hi(mix64(key), cap);
-  for (uint64_t probe = 0; probe < cap; probe++) {
-    uint32_t cur = slots[i];
-    if (cur == kEmpty) {
-      uint32_t prev = atomicCAS(slots + i, kEmpty, (uint32_t)h);
-      if (prev == kEmpty) return;
-      cur = prev;
+// Per-warp compaction of up to 96 half-edge items (3 per lane) so the table
+// probes run on dense lanes: lane l's items with flag bit j set get queue
+// positions in (slot j, lane) order.  Returns the item count.
+__device__ __forceinline__ int warp_compact3(unsigned flags, int lane, int32_t* q_h, int32_t* q_o, int32_t* q_g,
+                                             const int32_t (&h)[3], const int32_t (&o)[3], const int32_t (&g)[3]) {
+  const unsigned lt = (1u << lane) - 1u;
+  int base = 0;
+#pragma unroll
+  for (int j = 0; j < 3; j++) {
+    unsigned m = __ballot_sync(0xffffffffu, (flags >> j) & 1u);
+    if ((flags >> j) & 1u) {
+      int pos = base + __popc(m & lt);
+      q_h[pos] = h[j];
+      q_o[pos] = o[j];
+      q_g[pos] = g[j];
     }
-    int32_t hc = (int32_t)(cur & ~kMatched);
-    int64_t tc = hc / 3, jc = hc % 3;
-    int32_t oc = corner(tri, 3 * tc + (jc + 1) % 3);
-    int32_t gc = corner(tri, 3 * tc + (jc + 2) % 3);
-    if ((uint32_t)min(oc, gc) == lo && (uint32_t)max(oc, gc) == hi) {
-      if (cur & kMatched) { report(st, K_EDGE_COUNT, h / 3); return; }
-      if (oc != g || gc != o) { report(st, K_RECIPROCITY, h / 3); return; }
-      uint32_t prev = atomicCAS(slots + i, cur, cur | kMatched);
-      if (prev != cur) { report(st, K_EDGE_COUNT, h / 3); return; }
-      twin[h] = hc;
-      twin[hc] = h;
-      return;
-    }
-    i = (i + 1 == cap) ? 0 : i + 1;
+    base += __popc(m);
   }
-  report(st, K_STRUCT, h / 3);  // table full: impossible at load <= 0.5
+  __syncwarp();
+  return base;
 }
 
+// Pass A (K1 + first half of K0), one thread per triangle: corners -> tri32,
+// fp64 longest edge -> max_edge, orientation check, trivertex (atomicMin, a
+// fire-and-forget RED), provisional labels (hw = border, seed = 1); then the
+// warp's ascending half-edges (origin < target) go into the twin table on
+// dense lanes.
 template <typename TI>
-__global__ void __launch_bounds__(256) k_tri_pass(const double2* __restrict__ xy, int64_t n,
-                                                  const TI* __restrict__ tri, int64_t T,
-                                                  int32_t* __restrict__ tri32, int8_t* __restrict__ max_edge,
-                                                  uint32_t* __restrict__ slots, uint64_t cap,
-                                                  int32_t* __restrict__ twin, int32_t* __restrict__ tv,
-                                                  int check, DevStatus* st) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t a = (int64_t)__ldg(tri + 3 * t), b = (int64_t)__ldg(tri + 3 * t + 1), c = (int64_t)__ldg(tri + 3 * t + 2);
-    if (a < 0 || a >= n || b < 0 || b >= n || c < 0 || c >= n) {
-      report(st, K_INDEX_RANGE, t);
-      max_edge[t] = 0;
-      continue;
+__global__ void __launch_bounds__(kLabelThreads) k_tri_pass(const double2* __restrict__ xy, int64_t n,
+                                                            const TI* __restrict__ tri, int64_t T,
+                                                            int32_t* __restrict__ tri32, int8_t* __restrict__ max_edge,
+                                                            TwinTable tb, int32_t* __restrict__ hw,
+                                                            uint8_t* __restrict__ seed, int32_t* __restrict__ tv,
+                                                            int check, DevStatus* st) {
+  __shared__ int32_t sq[kLabelWarps][3][96];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t - lane < T; t += stride) {
+    unsigned flags = 0;
+    int32_t hh[3], oo[3], gg[3];
+    if (t < T) {
+      int64_t a = (int64_t)__ldg(tri + 3 * t), b = (int64_t)__ldg(tri + 3 * t + 1), c = (int64_t)__ldg(tri + 3 * t + 2);
+      hw[3 * t] = -1;
+      hw[3 * t + 1] = -1;
+      hw[3 * t + 2] = -1;
+      seed[t] = 1;
+      if (a < 0 || a >= n || b < 0 || b >= n || c < 0 || c >= n) {
+        report(st, K_INDEX_RANGE, t);
+        max_edge[t] = 0;
+        if (tri32 != nullptr) tri32[3 * t] = tri32[3 * t + 1] = tri32[3 * t + 2] = -1;
+      } else {
+        if (tri32 != nullptr) {
+          tri32[3 * t] = (int32_t)a;
+          tri32[3 * t + 1] = (int32_t)b;
+          tri32[3 * t + 2] = (int32_t)c;
+        }
+        double2 pa = xy[a], pb = xy[b], pc = xy[c];
+        // labeling.py:55-59: edge 0 joins corners 1-2, edge 1 joins 2-0, edge 2 joins 0-1
+        max_edge[t] = (int8_t)argmax3(sqlen(pb, pc), sqlen(pc, pa), sqlen(pa, pb));
+        if (check) {
+          // mesh_core.signed_areas (160-168), sign only, unfused
+          double d = __dsub_rn(__dmul_rn(__dsub_rn(pb.x, pa.x), __dsub_rn(pc.y, pa.y)),
+                               __dmul_rn(__dsub_rn(pb.y, pa.y), __dsub_rn(pc.x, pa.x)));
+          if (d < 0.0) report(st, K_ORIENTATION, t);
+          else if (d == 0.0) report(st, K_DEGENERATE, t);
+        }
+        atomicMin(tv + a, (int32_t)t);
+        atomicMin(tv + b, (int32_t)t);
+        atomicMin(tv + c, (int32_t)t);
+        // half-edge j: origin corner (j+1)%3, target corner (j+2)%3
+        const int32_t cv[3] = {(int32_t)a, (int32_t)b, (int32_t)c};
+#pragma unroll
+        for (int j = 0; j < 3; j++) {
+          hh[j] = (int32_t)(3 * t + j);
+          oo[j] = cv[(j + 1) % 3];
+          gg[j] = cv[(j + 2) % 3];
+          if (oo[j] < gg[j]) flags |= 1u << j;
+        }
+      }
     }
-    if (tri32 != nullptr) {
-      tri32[3 * t] = (int32_t)a;
-      tri32[3 * t + 1] = (int32_t)b;
-      tri32[3 * t + 2] = (int32_t)c;
-    }
-    double2 pa = xy[a], pb = xy[b], pc = xy[c];
-    // labeling.py:55-59: edge 0 joins corners 1-2, edge 1 joins 2-0, edge 2 joins 0-1
-    max_edge[t] = (int8_t)argmax3(sqlen(pb, pc), sqlen(pc, pa), sqlen(pa, pb));
-    if (check) {
-      // mesh_core.signed_areas (160-168), sign only, unfused
-      double d = __dsub_rn(__dmul_rn(__dsub_rn(pb.x, pa.x), __dsub_rn(pc.y, pa.y)),
-                           __dmul_rn(__dsub_rn(pb.y, pa.y), __dsub_rn(pc.x, pa.x)));
-      if (d < 0.0) report(st, K_ORIENTATION, t);
-      else if (d == 0.0) report(st, K_DEGENERATE, t);
-    }
-    atomicMin(tv + a, (int32_t)t);
-    atomicMin(tv + b, (int32_t)t);
-    atomicMin(tv + c, (int32_t)t);
-    int32_t h = (int32_t)(3 * t);
-    insert_edge(tri, slots, cap, twin, st, h + 0, (int32_t)b, (int32_t)c);
-    insert_edge(tri, slots, cap, twin, st, h + 1, (int32_t)c, (int32_t)a);
-    insert_edge(tri, slots, cap, twin, st, h + 2, (int32_t)a, (int32_t)b);
+    int m = warp_compact3(flags, lane, sq[wid][0], sq[wid][1], sq[wid][2], hh, oo, gg);
+    for (int i = lane; i < m; i += 32) table_insert(tb, st, sq[wid][0][i], sq[wid][1][i], sq[wid][2][i]);
+    __syncwarp();
   }
+}
+
+// Pass B (second half of K0 + K2), one thread per triangle (and per vertex for
+// the trivertex sentinel).  The warp's descending half-edges h = o -> g
+// (o > g) look their ascending partner up under key (g, o) on dense lanes and
+// label the edge pair from both sides at once: frontier = neither side's
+// longest edge (labeling.py:92-115), terminal = both (labeling.py:65-89, seed
+// on the lower triangle).  k = twin % 3 replaces the reference's back-slot
+// searches.  A half-edge without a partner stays border as pass A wrote it
+// (an ascending one keeps its provisional seed flag).
+__global__ void __launch_bounds__(kLabelThreads) k_pair_pass(const int32_t* __restrict__ tri32, int64_t T,
+                                                             const int8_t* __restrict__ max_edge, TwinTable tb,
+                                                             int32_t* __restrict__ hw, uint8_t* __restrict__ seed,
+                                                             int32_t* __restrict__ tv, int64_t n, int check,
+                                                             DevStatus* st) {
+  __shared__ int32_t sq[kLabelWarps][3][96];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t - lane < T; t += stride) {
+    unsigned flags = 0;
+    int32_t hh[3], oo[3], gg[3];
+    if (t < T) {
+      const int32_t cv[3] = {__ldg(tri32 + 3 * t), __ldg(tri32 + 3 * t + 1), __ldg(tri32 + 3 * t + 2)};
+      if ((uint32_t)cv[0] < (uint32_t)n && (uint32_t)cv[1] < (uint32_t)n && (uint32_t)cv[2] < (uint32_t)n) {
+#pragma unroll
+        for (int j = 0; j < 3; j++) {
+          hh[j] = (int32_t)(3 * t + j);
+          oo[j] = cv[(j + 1) % 3];
+          gg[j] = cv[(j + 2) % 3];
+          if (oo[j] > gg[j]) flags |= 1u << j;
+        }
+      }
+    }
+    int m = warp_compact3(flags, lane, sq[wid][0], sq[wid][1], sq[wid][2], hh, oo, gg);
+    for (int i = lane; i < m; i += 32) {
+      const int32_t h = sq[wid][0][i];
+      const int32_t hc = table_lookup(tb, st, check, sq[wid][2][i], sq[wid][1][i], h / 3);
+      if (hc < 0) continue;  // border
+      const int32_t tt = h / 3, j = h - 3 * tt;
+      const int32_t tc = hc / 3, k = hc - 3 * tc;
+      const bool own = __ldg(max_edge + tt) == j, other = __ldg(max_edge + tc) == k;
+      const int32_t fr = (!own && !other) ? 1 : 0;
+      hw[h] = (hc << 1) | fr;
+      hw[hc] = (h << 1) | fr;
+      if (own) seed[tt] = (other && tt < tc) ? 1 : 0;
+      if (other) seed[tc] = (own && tc < tt) ? 1 : 0;
+    }
+    __syncwarp();
+  }
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride)
+    if (tv[v] == 0x7F7F7F7F) tv[v] = -1;
 }
 
 // labeling.py:65-115 fused.  k = twin % 3 replaces the back-slot search.
@@ -158,11 +320,6 @@ __global__ void __launch_bounds__(256) k_label_edges(const int8_t* __restrict__ 
   }
 }
 
-__global__ void k_trivertex_fix(int32_t* tv, int64_t n) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
-    if (tv[v] == 0x7F7F7F7F) tv[v] = -1;
-}
-
 // Compare a caller-supplied neighbor array (reference layout, -1 border)
 // against the twin build: neighbors[h] == twin[h] // 3.
 template <typename TI>
@@ -189,6 +346,7 @@ __global__ void k_pack_frontier(int32_t* __restrict__ hw, int64_t H, const uint8
   }
 }
 
+
 static inline int grid_for(int64_t n, int block) {
   int64_t g = (n + block - 1) / block;
   int64_t cap = (int64_t)kNumSMs * 16;
@@ -196,42 +354,64 @@ static inline int grid_for(int64_t n, int block) {
   return (int)(g < 1 ? 1 : g);
 }
 
-uint64_t hash_capacity(int64_t T) {
-  // at most 3T/2 + border distinct keys; capacity 3T keeps the load <= 0.5
-  uint64_t c = (uint64_t)(3 * T);
-  return c < 64 ? 64 : c;
+static int bit_length(uint64_t v) {
+  int b = 0;
+  while (v) { b++; v >>= 1; }
+  return b;
+}
+
+// Geometry of the twin table for a mesh of n vertices / T triangles.
+static TwinTable table_geometry(int64_t n, int64_t T, void* mem) {
+  TwinTable tb{};
+  tb.b = bit_length((uint64_t)(n > 1 ? n - 1 : 1));
+  tb.K = 2 * tb.b;
+  tb.hb = bit_length((uint64_t)(3 * (T > 0 ? T : 1)));  // 2^hb > 3T: the all-ones field is never a half-edge
+  // ascending half-edges <= 3T/2 + border; 4-slot buckets at load in [0.35, 0.7)
+  // (measured: a fuller table costs more in probe/CAS conflicts than it saves in L2)
+  uint64_t keys = (uint64_t)(3 * (T > 0 ? T : 1)) / 2 + 64;
+  int q = bit_length((keys * 10 / 28) | 1);
+  if (q > tb.K) q = tb.K;
+  while (tb.K - q + kDispBits + tb.hb > 63 && q < tb.K) q++;  // the slot must hold remainder|d|h in 63 bits
+  tb.R = tb.K - q;
+  tb.nb_mask = (1ull << q) - 1;
+  tb.slots = static_cast<unsigned long long*>(mem);
+  return tb;
+}
+
+size_t hash_bytes(int64_t n, int64_t T) {
+  TwinTable tb = table_geometry(n, T, nullptr);
+  return (size_t)(tb.nb_mask + 1) * 4 * sizeof(unsigned long long);
 }
 
 void launch_label_a(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int check,
-                    int32_t* tri32, int32_t* hw, int8_t* max_edge, int32_t* tv, uint32_t* slots, uint64_t cap,
+                    int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed, int32_t* tv, void* table,
                     DevStatus* st, cudaStream_t s) {
-  cudaMemsetAsync(slots, 0xFF, cap * sizeof(uint32_t), s);
-  cudaMemsetAsync(hw, 0xFF, (size_t)(3 * T) * sizeof(int32_t), s);
+  TwinTable tb = table_geometry(n, T, table);
+  cudaMemsetAsync(table, 0xFF, hash_bytes(n, T), s);
   if (n > 0) {
-    // sentinel 0x7F7F7F7F (> any triangle index), mapped to -1 after the atomicMin pass
+    // sentinel 0x7F7F7F7F (> any triangle index), mapped to -1 by pass B
     cudaMemsetAsync(tv, 0x7F, (size_t)n * sizeof(int32_t), s);
   }
   if (T > 0) {
-    const int B = 256;
+    const int B = kLabelThreads;
     if (tri_is64)
       k_tri_pass<int64_t><<<grid_for(T, B), B, 0, s>>>((const double2*)xy, n, (const int64_t*)tri, T, tri32, max_edge,
-                                                       slots, cap, hw, tv, check, st);
+                                                       tb, hw, seed, tv, check, st);
     else
       k_tri_pass<int32_t><<<grid_for(T, B), B, 0, s>>>((const double2*)xy, n, (const int32_t*)tri, T,
-                                                       tri32 == tri ? nullptr : tri32, max_edge, slots, cap, hw, tv,
+                                                       tri32 == tri ? nullptr : tri32, max_edge, tb, hw, seed, tv,
                                                        check, st);
     note_launch(1);
   }
 }
 
-void launch_label_b(int64_t n, int64_t T, int32_t* hw, const int8_t* max_edge, uint8_t* seed, int32_t* tv,
-                    cudaStream_t s) {
-  if (T > 0) {
-    k_label_edges<<<grid_for(T, 256), 256, 0, s>>>(max_edge, T, hw, seed, 0);
-    note_launch(1);
-  }
-  if (n > 0) {
-    k_trivertex_fix<<<grid_for(n, 256), 256, 0, s>>>(tv, n);
+void launch_label_b(const int32_t* tri32, int64_t n, int64_t T, int32_t* hw, const int8_t* max_edge, uint8_t* seed,
+                    int32_t* tv, void* table, int check, DevStatus* st, cudaStream_t s) {
+  TwinTable tb = table_geometry(n, T, table);
+  int64_t m = T > n ? T : n;
+  if (m > 0) {
+    k_pair_pass<<<grid_for(m, kLabelThreads), kLabelThreads, 0, s>>>(tri32, T, max_edge, tb, hw, seed, tv, n, check,
+                                                                     st);
     note_launch(1);
   }
 }
