@@ -119,6 +119,8 @@ struct tm_ctx {
   // whole-path buffers
   Buf xy, tri, tri32, hw, max_edge, seed, tv, off0, v0, fin_off, fin_v, hw_snap;
   cudaStream_t gstream = nullptr;
+  cudaStream_t aux = nullptr;                            // long repair items run beside the short ones
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cudaGraphExec_t graph = nullptr;
@@ -291,6 +293,9 @@ static int decode_status(tm_ctx* ctx, const Counters& h) {
 static int prepare(tm_ctx* ctx, int64_t T, int64_t n = -1) {
   int rc = init_counters(ctx);
   if (rc) return rc;
+  if (!ctx->aux) CK(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+  if (!ctx->ev_fork) CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+  if (!ctx->ev_join) CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
   int64_t Tn = T > 0 ? T : 1;
   if (n >= 0) ENSURE(slots, hash_bytes(n, Tn));
   ENSURE(seeds, Tn * sizeof(int32_t));
@@ -421,7 +426,21 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
                dc->stats, q, dc->dbg};
   {
     SegTimer t_(ctx, S_REPAIR_TIPS, s);
-    launch_repair_tips(a, s);
+    // fork: the long items (one block each) on ctx->aux beside the short ones
+    static int serial = -1;
+    if (serial < 0) serial = getenv("TERMESH_SERIAL_REPAIR") != nullptr;  // debug: no fork
+    cudaStream_t sl = serial ? s : ctx->aux;
+    if (!serial) {
+      CK(cudaEventRecord(ctx->ev_fork, s));
+      CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
+    }
+    launch_repair_tips_long(a, sl);
+    launch_repair_tips(a, 0, s);
+    if (!serial) {
+      CK(cudaEventRecord(ctx->ev_join, ctx->aux));
+      CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
+    }
+    launch_repair_tips(a, 1, s);  // long items the shared-memory kernel handed back
   }
   {
     SegTimer t_(ctx, S_REPAIR_PINCH, s);

@@ -83,7 +83,9 @@ struct RepairArgs {
 void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, int32_t* item_of,
                      int32_t* items, unsigned int* n_items, int32_t* long_list, unsigned int* n_long,
                      unsigned long long* stats, LongQueue q, cudaStream_t s);
-void launch_repair_tips(const RepairArgs& a, cudaStream_t s);
+void launch_repair_tips_long(const RepairArgs& a, cudaStream_t s);
+// mode 0: items of length <= kLongMin; mode 1: long items handed back (state 2/3)
+void launch_repair_tips(const RepairArgs& a, int mode, cudaStream_t s);
 void launch_repair_pinch(const RepairArgs& a, cudaStream_t s);
 void launch_out_counts(const int64_t* off, const int64_t* Pp, int64_t Pcap, const int32_t* item_of,
                        const int32_t* item_n, const int64_t* item_slots, int64_t* cnt, int64_t* slots,

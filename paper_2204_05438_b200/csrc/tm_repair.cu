@@ -58,9 +58,11 @@ __device__ __forceinline__ int64_t palloc(const RepairCtx& c, int64_t n) {
   return (int64_t)o;
 }
 
+// both loads issued before the stores: one memory round trip
 __device__ __forceinline__ void promote(const RepairCtx& c, int32_t e, int32_t te) {
-  c.hw[e] |= 1;
-  c.hw[te] |= 1;
+  const int32_t we = c.hw[e], wt = c.hw[te];
+  c.hw[e] = we | 1;
+  c.hw[te] = wt | 1;
 }
 
 // Per-warp bump arena carved from the pool (state held by lane 0).
@@ -683,24 +685,30 @@ __global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, con
                                                                 int32_t* __restrict__ item_n,
                                                                 const int32_t* __restrict__ item_state,
                                                                 const int32_t* __restrict__ item_depth,
-                                                                unsigned long long* stats) {
+                                                                unsigned long long* stats, LongQueue q, int mode) {
   __shared__ int32_t s_fan[kTipWarps][kFanCap];
   __shared__ int32_t s_back[kTipWarps][kFanCap];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   int32_t* fan = s_fan[wib];
   int32_t* back = s_back[wib];
-  unsigned int ni = *n_items;
+  const unsigned int nh = mode ? *q.n_huge : 0u;
+  const unsigned int ni = mode ? nh + *q.n_long : *n_items;
   // reparation.py:354-364: at most initial + 1 rounds, initial = extra visits of mesh0
   long long max_rounds = (long long)stats[2] + 1;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t w = warp; w < ni; w += nwarps) {
-    int st = item_state[w];
-    if (st == 1) continue;
+  for (int64_t wq = warp; wq < ni; wq += nwarps) {
+    const int64_t w = !mode ? wq : (wq < nh ? q.huge[wq] : q.longq[wq - nh]);
     int32_t i = items[w];
     int64_t b = off[i];
     int L = (int)(off[i + 1] - b);
-    if (st == 0 && L > kLongMin) continue;  // handled by k_repair_tips_long (state 1/2/3)
+    int st = 0;
+    if (!mode) {
+      if (L > kLongMin) continue;  // k_repair_tips_long runs it concurrently
+    } else {
+      st = item_state[w];
+      if (st != 2 && st != 3) continue;
+    }
     WarpArena arena;
     auto alloc = [&](long long n) -> int32_t* {
       long long o = warp_alloc(c, arena, n, 2 * (long long)L + 512, lane);
@@ -788,91 +796,397 @@ __global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, con
   }
 }
 
-// ------------------------------------------------------------ tip phase, shared memory
-// Long items (hull slivers: 902 vertices / 70 tips / 41 rounds at 1M): one
-// block each, pieces in a shared-memory bump arena, the tipped pieces of a
-// round split concurrently by the block's warps (distinct pieces have
-// disjoint interiors).  Scans run at shared-memory latency; only the mesh
-// rotations touch global memory.  If the arena or the record list fills up,
-// the current pieces are written to the global pool and the warp kernel
-// resumes the item (item_state = 2).
-constexpr int kLongWarps = 8;
-constexpr int kLongArena = 32 * 1024;  // ints (128 KiB)
-constexpr int kLongRec = 1024;         // records per list
-constexpr int kMaxTips = 1024;         // precomputed tips per item
-constexpr int kMaxTouch = 2048;        // promoted-edge endpoints per item
-size_t long_smem_bytes() {
-  return (size_t)kLongArena * 4 + 2 * (size_t)kLongRec * 8 + 2 * (size_t)kLongWarps * kFanCap * 4 +
-         (size_t)kMaxTips * 4 * 2 + (size_t)kMaxTips * sizeof(SplitInfo) + (size_t)kMaxTouch * 4 + 64;
+// ------------------------------------------------------------ tip phase, segment pieces
+// Long items (hull slivers: 902 vertices / 70 tips / 41 rounds at 1M, 3210 /
+// 219 / 142 at 10M): one block each.  The item's original cycle P stays in
+// shared memory and every piece is a short list of SEGMENTS -- a cyclic range
+// of P or one inserted vertex -- because a tip split only cuts its parent into
+// two arcs and adds one vertex to each.  All per-round queries
+// run over segments instead of vertices:
+//   first tip      tip bitmap of P for segment interiors, explicit checks at the
+//                  (few) segment junctions;
+//   cut / rotation the directed boundary pair (x, y) is unique in a piece: a
+//                  hash map pair -> index of P answers it for segment interiors,
+//                  junctions again explicitly.
+// So a split costs O(#segments), not O(|piece|).  The mesh rotations of every
+// tip of P (split edge, wedge vertex, re-walk start pairs) run up front, in
+// parallel; a round reuses them unless an earlier promotion touched v or u.
+// Leaves are expanded into the global pool at the end.  If the segment arena
+// or the record list would overflow, the current pieces go to the pool and the
+// warp kernel resumes the item (item_state = 2).
+constexpr int kSegWarps = 16;
+constexpr int kSegMaxL = 8192;   // longer items: the warp kernel from scratch (state 3)
+constexpr int kPairCap = 16384;  // pair-map slots (>= 2 kSegMaxL); reused as leaf hash sets
+constexpr int kSegRec = 1024;    // piece records per round list
+constexpr int kSegTips = 512;    // precomputed tips per item
+constexpr int kSegTouch = 1024;  // promoted-edge endpoints per item
+constexpr int kSmemMax = 226 * 1024;  // dynamic; leaves room for the static __shared__ words
+
+struct Seg {
+  int32_t base, len, loff;  // base >= 0: P[(base + i) mod L], i < len; base < 0: the vertex ~base (len 1)
+};
+struct SPiece {
+  int32_t soff, nseg, len, ftip;  // segments [soff, soff + nseg), first tip position (-1: none)
+};
+
+constexpr size_t kSegFixed = (size_t)kSegMaxL * 4 + (kSegMaxL / 32) * 4 + (size_t)kPairCap * 4 +
+                             2 * (size_t)kSegRec * sizeof(SPiece) + (size_t)kSegRec * 4 +
+                             2 * (size_t)kSegWarps * kFanCap * 4 + 2 * (size_t)kSegTips * 4 +
+                             (size_t)kSegTips * sizeof(SplitInfo) + (size_t)kSegTouch * 4 + 128;
+constexpr int kSegCap = (int)((kSmemMax - kSegFixed) / sizeof(Seg));
+size_t seg_smem_bytes() { return kSegFixed + (size_t)kSegCap * sizeof(Seg); }
+
+struct SegView {
+  const int32_t* P;
+  int L;
+  const uint32_t* tipbits;
+  const int32_t* pmap;
+  int pmask;
+  Seg* segs;
+};
+
+__device__ __forceinline__ int wrapL(int x, int L) { return x >= L ? x - L : x; }
+__device__ __forceinline__ int wrapN(int x, int n) { x %= n; return x < 0 ? x + n : x; }
+__device__ __forceinline__ int32_t sval(const SegView& g, const Seg& s, int i) {
+  return s.base < 0 ? ~s.base : g.P[wrapL(s.base + i, g.L)];
+}
+__device__ __forceinline__ uint32_t pair_hash(int32_t x, int32_t y) {
+  uint32_t h = (uint32_t)x * 0x9E3779B1u ^ (uint32_t)y * 0x85EBCA77u;
+  return h ^ (h >> 15);
+}
+// index k of P with P[k-1] == x and P[k] == y, or -1
+__device__ __forceinline__ int pmap_lookup(const SegView& g, int32_t x, int32_t y) {
+  uint32_t i = pair_hash(x, y) & g.pmask;
+  for (int probe = 0; probe <= g.pmask; probe++) {
+    int k = g.pmap[i];
+    if (k < 0) return -1;
+    if (g.P[k] == y && g.P[k == 0 ? g.L - 1 : k - 1] == x) return k;
+    i = (i + 1) & g.pmask;
+  }
+  return -1;
 }
 
-__global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx c, const int32_t* __restrict__ items,
-                                                                      const unsigned int* n_items,
-                                                                      const int64_t* __restrict__ off,
-                                                                      const int32_t* __restrict__ v,
-                                                                      int64_t* __restrict__ item_list,
-                                                                      int32_t* __restrict__ item_n,
-                                                                      int32_t* __restrict__ item_state,
-                                                                      int32_t* __restrict__ item_depth,
-                                                                      unsigned long long* stats, int arena_cap,
-                                                                      LongQueue q, unsigned long long* dbg) {
-  extern __shared__ __align__(16) int32_t smem[];
-  int32_t* arena = smem;
-  int2* recs = reinterpret_cast<int2*>(arena + kLongArena);  // [2][kLongRec] {offset, len|flags}
-  int32_t* fans = reinterpret_cast<int32_t*>(recs + 2 * kLongRec);
-  int32_t* tipv = fans + 2 * kLongWarps * kFanCap;  // tip vertex (or -1 when its info is unusable)
-  int32_t* tipb = tipv + kMaxTips;                  // barrier vertex
-  SplitInfo* tipinfo = reinterpret_cast<SplitInfo*>(tipb + kMaxTips);
-  int32_t* touched = reinterpret_cast<int32_t*>(tipinfo + kMaxTips);
-  __shared__ int s_ntip, s_ntouch;
-  __shared__ int s_top, s_fail, s_ntips;
-  __shared__ int s_out[kLongRec];  // output index of each input record
+// first set bit of the cyclic index range [a, a + cnt) of bits (over L), as an offset, or -1
+__device__ int bits_first(const uint32_t* bits, int L, int a, int cnt) {
+  int d = 0;
+  while (d < cnt) {
+    int k = wrapL(a + d, L);
+    int bo = k & 31;
+    int span = min(min(32 - bo, cnt - d), L - k);
+    uint32_t word = bits[k >> 5] >> bo;
+    uint32_t m = span >= 32 ? word : (word & ((1u << span) - 1u));
+    if (m) return d + __ffs(m) - 1;
+    d += span;
+  }
+  return -1;
+}
+
+// segment of X holding local position p (warp-uniform)
+__device__ __forceinline__ int seg_of(const SegView& g, const SPiece& X, int p, int lane) {
+  for (int c0 = 0; c0 < X.nseg; c0 += 32) {
+    int s = c0 + lane;
+    bool hit = false;
+    if (s < X.nseg) {
+      Seg sg = g.segs[X.soff + s];
+      hit = sg.loff <= p && p < sg.loff + sg.len;
+    }
+    unsigned m = __ballot_sync(kFull, hit);
+    if (m) return c0 + __ffs(m) - 1;
+  }
+  return -1;
+}
+__device__ __forceinline__ int32_t selem(const SegView& g, const SPiece& X, int p, int lane) {
+  Seg sg = g.segs[X.soff + seg_of(g, X, p, lane)];
+  return sval(g, sg, p - sg.loff);
+}
+// one lane, linear (tiny pieces)
+__device__ int32_t selem1(const SegView& g, const SPiece& X, int p) {
+  for (int s = 0; s < X.nseg; s++) {
+    Seg sg = g.segs[X.soff + s];
+    if (sg.loff <= p && p < sg.loff + sg.len) return sval(g, sg, p - sg.loff);
+  }
+  return -1;
+}
+
+// reparation.py:59-71 on a segment piece: the first position p with
+// s[p-1] == s[p+1] (cyclic), or -1.  Warp-uniform.
+__device__ int seg_first_tip(const SegView& g, const SPiece& X, int lane) {
+  if (X.len < 4) {
+    int r = -1;
+    if (lane == 0)
+      for (int p = 0; p < X.len && r < 0; p++)
+        if (selem1(g, X, p == 0 ? X.len - 1 : p - 1) == selem1(g, X, p + 1 == X.len ? 0 : p + 1)) r = p;
+    return __shfl_sync(kFull, r, 0);
+  }
+  for (int c0 = 0; c0 < X.nseg; c0 += 32) {
+    int s = c0 + lane, best = -1;
+    if (s < X.nseg) {
+      Seg sg = g.segs[X.soff + s];
+      Seg sp = g.segs[X.soff + (s == 0 ? X.nseg - 1 : s - 1)];
+      Seg sn = g.segs[X.soff + (s + 1 == X.nseg ? 0 : s + 1)];
+      int32_t pv = sval(g, sp, sp.len - 1), nv = sval(g, sn, 0);
+      const int l = sg.len;
+      if (pv == (l >= 2 ? sval(g, sg, 1) : nv)) {
+        best = sg.loff;
+      } else {
+        if (l >= 3) {
+          int d = bits_first(g.tipbits, g.L, wrapL(sg.base + 1, g.L), l - 2);
+          if (d >= 0) best = sg.loff + 1 + d;
+        }
+        if (best < 0 && l >= 2 && sval(g, sg, l - 2) == nv) best = sg.loff + l - 1;
+      }
+    }
+    unsigned m = __ballot_sync(kFull, best >= 0);
+    if (m) return __shfl_sync(kFull, best, __ffs(m) - 1);
+  }
+  return -1;
+}
+
+// local position q of X with X[q-1] == x and X[q] == y (a directed boundary
+// pair is unique in a piece), or -1.  Warp-uniform.
+__device__ int seg_pairfind(const SegView& g, const SPiece& X, int32_t x, int32_t y, int lane) {
+  const int k = pmap_lookup(g, x, y);
+  for (int c0 = 0; c0 < X.nseg; c0 += 32) {
+    int s = c0 + lane, q = -1;
+    if (s < X.nseg) {
+      Seg sg = g.segs[X.soff + s];
+      if (k >= 0 && sg.base >= 0) {
+        int i = k - sg.base;
+        if (i < 0) i += g.L;
+        if (i >= 1 && i < sg.len) q = sg.loff + i;
+      }
+      if (q < 0) {
+        Seg sp = g.segs[X.soff + (s == 0 ? X.nseg - 1 : s - 1)];
+        if (sval(g, sg, 0) == y && sval(g, sp, sp.len - 1) == x) q = sg.loff;
+      }
+    }
+    unsigned m = __ballot_sync(kFull, q >= 0);
+    if (m) return __shfl_sync(kFull, q, __ffs(m) - 1);
+  }
+  return -1;
+}
+
+// Appends X's local positions [start, start + cnt) (cyclic, cnt <= |X|) to
+// out[n..] as segments with local offsets from lo; returns the new count.
+// Lane s clips segment s; parts land in range order (the segment holding
+// `start` first, then the following ones cyclically, then -- when the range
+// wraps all the way around -- that segment's head).  X's segments are maximal
+// runs of P except across X's own wrap point, so at most one pair of parts
+// needs merging.  Warp-uniform.
+__device__ int emit_range_warp(const SegView& g, const SPiece& X, int start, int cnt, Seg* out, int n, int lo,
+                               int lane) {
+  if (cnt <= 0) return n;
+  const int Lx = X.len, ns = X.nseg;
+  const int s0 = seg_of(g, X, start, lane);
+  int count = 0;
+  for (int c0 = 0; c0 < ns; c0 += 32) {
+    const int s = c0 + lane;
+    bool inc = false, tail = false;
+    if (s < ns) {
+      const Seg sg = g.segs[X.soff + s];
+      int r0, skip;
+      if (s == s0) { r0 = 0; skip = start - sg.loff; }
+      else { r0 = wrapN(sg.loff - start, Lx); skip = 0; }
+      if (r0 < cnt) {
+        inc = true;
+        int idx = s - s0;
+        if (idx < 0) idx += ns;
+        out[n + idx] = Seg{sg.base >= 0 ? wrapL(sg.base + skip, g.L) : sg.base, min(sg.len - skip, cnt - r0), lo + r0};
+      }
+      if (s == s0 && start > sg.loff) {
+        int rt = Lx - (start - sg.loff);
+        if (rt < cnt) {
+          tail = true;
+          out[n + ns] = Seg{sg.base, min(start - sg.loff, cnt - rt), lo + rt};
+        }
+      }
+    }
+    count += __popc(__ballot_sync(kFull, inc)) + __popc(__ballot_sync(kFull, tail));
+  }
+  __syncwarp();
+  // merge the one possible contiguous pair
+  int mpos = -1;
+  for (int c0 = 1; c0 < count; c0 += 32) {
+    const int k = c0 + lane;
+    bool m = false;
+    if (k < count) {
+      const Seg a = out[n + k - 1], b = out[n + k];
+      m = a.base >= 0 && b.base >= 0 && wrapL(a.base + a.len, g.L) == b.base && a.len + b.len <= g.L;
+    }
+    unsigned bm = __ballot_sync(kFull, m);
+    if (bm && mpos < 0) mpos = c0 + __ffs(bm) - 1;
+  }
+  if (mpos < 0) return n + count;
+  const int add = out[n + mpos].len;
+  __syncwarp();
+  for (int c0 = mpos; c0 < count - 1; c0 += 32) {
+    const int k = c0 + lane;
+    Seg nx;
+    if (k < count - 1) nx = out[n + k + 1];
+    __syncwarp();
+    if (k < count - 1) out[n + k] = nx;
+    __syncwarp();
+  }
+  if (lane == 0) out[n + mpos - 1].len += add;
+  __syncwarp();
+  return n + count - 1;
+}
+
+// Arc split of piece X at tip position pos with split info si
+// (not yet promoted).  On success the children are written (rotated to the
+// re-walk start pairs) and the edge is promoted; returns false without side
+// effects when a search fails (the caller falls back to the re-walk).
+__device__ bool seg_split_arcs(const RepairCtx& c, const SegView& g, const SPiece& X, int pos, int32_t v,
+                               const SplitInfo& si, int* s_stop, int seg_cap, int lane, SPiece* A, SPiece* B,
+                               unsigned long long* prof) {
+  const int Lx = X.len;
+  if (si.a_in < 0) return false;
+  long long c0 = clock64();
+  const int j = seg_pairfind(g, X, si.a_in, si.u, lane);
+  long long c1 = clock64();
+  if (j < 0 || j == pos) return false;
+  const int la = wrapN(pos - j, Lx) + 1, lb = wrapN(j - pos, Lx) + 1;
+  // pa = [v, X[j .. pos-1]], pb = [X[pos .. j-1], u]; their re-walk start pairs
+  int ka = -1, kb = -1;
+  const int32_t xj = selem(g, X, j, lane), xpm = selem(g, X, wrapN(pos - 1, Lx), lane);
+  const int32_t xpos = v, xjm = selem(g, X, wrapN(j - 1, Lx), lane);
+  if (v == si.oa && (la >= 2 ? xj : v) == si.ga) ka = 0;
+  else if (la >= 2 && xpm == si.oa && v == si.ga) ka = la - 1;
+  else {
+    int q = seg_pairfind(g, X, si.oa, si.ga, lane);
+    if (q >= 0) {
+      int d = wrapN(q - j, Lx);
+      if (d >= 1 && d <= la - 2) ka = d;
+    }
+  }
+  if (si.u == si.ob && xpos == si.gb) kb = lb - 1;
+  else if (lb >= 2 && xjm == si.ob && si.u == si.gb) kb = lb - 2;
+  else {
+    int q = seg_pairfind(g, X, si.ob, si.gb, lane);
+    if (q >= 0) {
+      int d = wrapN(q - pos, Lx);
+      if (d >= 1 && d <= lb - 2) kb = d - 1;
+    }
+  }
+  if (ka < 0 || kb < 0) return false;
+  long long c2 = clock64();
+  int base = 0;
+  const int need = 2 * (X.nseg + 4);
+  if (lane == 0) base = atomicAdd(s_stop, need);
+  base = __shfl_sync(kFull, base, 0);
+  if (base + need > seg_cap) return false;  // (capacity is checked per round; defensive)
+  int32_t we = 0, wt = 0;
+  if (lane == 0) { we = c.hw[si.e]; wt = c.hw[si.te]; }  // promotion loads overlap the emission
+  Seg* oa = g.segs + base;
+  Seg* ob = g.segs + base + X.nseg + 4;
+  int na = 0, nb = 0;
+  if (ka == 0) {
+    if (lane == 0) oa[0] = Seg{~v, 1, 0};
+    na = emit_range_warp(g, X, j, la - 1, oa, 1, 1, lane);
+  } else {
+    na = emit_range_warp(g, X, wrapN(j + ka - 1, Lx), la - ka, oa, 0, 0, lane);
+    if (lane == 0) oa[na] = Seg{~v, 1, la - ka};
+    na = emit_range_warp(g, X, j, ka - 1, oa, na + 1, la - ka + 1, lane);
+  }
+  nb = emit_range_warp(g, X, wrapN(pos + kb, Lx), lb - 1 - kb, ob, 0, 0, lane);
+  if (lane == 0) ob[nb] = Seg{~si.u, 1, lb - 1 - kb};
+  nb = emit_range_warp(g, X, pos, kb, ob, nb + 1, lb - kb, lane);
+  if (lane == 0) {
+    c.hw[si.e] = we | 1;
+    c.hw[si.te] = wt | 1;
+    A->soff = base; A->nseg = na; A->len = la;
+    B->soff = base + X.nseg + 4; B->nseg = nb; B->len = lb;
+    if (prof) {
+      long long c3 = clock64();
+      atomicAdd(prof + 0, (unsigned long long)(c1 - c0));
+      atomicAdd(prof + 1, (unsigned long long)(c2 - c1));
+      atomicAdd(prof + 2, (unsigned long long)(c3 - c2));
+      atomicAdd(prof + 3, (unsigned long long)X.nseg);
+    }
+  }
+  __syncwarp();
+  A->soff = __shfl_sync(kFull, A->soff, 0); A->nseg = __shfl_sync(kFull, A->nseg, 0);
+  A->len = __shfl_sync(kFull, A->len, 0);
+  B->soff = __shfl_sync(kFull, B->soff, 0); B->nseg = __shfl_sync(kFull, B->nseg, 0);
+  B->len = __shfl_sync(kFull, B->len, 0);
+  return true;
+}
+
+__global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c, const int32_t* __restrict__ items,
+                                                                    const int64_t* __restrict__ off,
+                                                                    const int32_t* __restrict__ v,
+                                                                    int64_t* __restrict__ item_list,
+                                                                    int32_t* __restrict__ item_n,
+                                                                    int32_t* __restrict__ item_state,
+                                                                    int32_t* __restrict__ item_depth,
+                                                                    unsigned long long* stats, LongQueue q,
+                                                                    unsigned long long* dbg, unsigned int trace_qi,
+                                                                    int seg_cap) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int32_t* P = reinterpret_cast<int32_t*>(smem_raw);
+  uint32_t* tipbits = reinterpret_cast<uint32_t*>(P + kSegMaxL);
+  int32_t* pmap = reinterpret_cast<int32_t*>(tipbits + kSegMaxL / 32);
+  SPiece* recs = reinterpret_cast<SPiece*>(pmap + kPairCap);  // [2][kSegRec]
+  int32_t* s_out = reinterpret_cast<int32_t*>(recs + 2 * kSegRec);
+  int32_t* fans = s_out + kSegRec;
+  int32_t* tipv = fans + 2 * kSegWarps * kFanCap;  // tip vertex (or -1 when its info is unusable)
+  int32_t* tipb = tipv + kSegTips;                 // barrier vertex
+  SplitInfo* tipinfo = reinterpret_cast<SplitInfo*>(tipb + kSegTips);
+  int32_t* touched = reinterpret_cast<int32_t*>(tipinfo + kSegTips);
+  Seg* segs = reinterpret_cast<Seg*>(touched + kSegTouch);
+  __shared__ int s_ntip, s_ntouch, s_stop, s_fail, s_ntips, s_need, s_tot;
+  __shared__ long long s_base;
+  __shared__ unsigned int s_w;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   int32_t* fan = fans + wib * kFanCap;
-  int32_t* back = fans + (kLongWarps + wib) * kFanCap;
-  (void)n_items;
-  long long max_rounds = (long long)stats[2] + 1;
-  // dynamic queue, longest class first (the hull-sliver lineage sets the critical path)
+  int32_t* back = fans + (kSegWarps + wib) * kFanCap;
+  const long long max_rounds = (long long)stats[2] + 1;
   const unsigned int nh = *q.n_huge, nq = nh + *q.n_long;
-  __shared__ unsigned int s_w;
   for (;;) {
     __syncthreads();
     if (threadIdx.x == 0) s_w = atomicAdd(q.next, 1u);
     __syncthreads();
-    unsigned int qi = s_w;
+    const unsigned int qi = s_w;
     if (qi >= nq) break;
-    unsigned int w = qi < nh ? (unsigned int)q.huge[qi] : (unsigned int)q.longq[qi - nh];
-    const bool trace = qi == 0 && threadIdx.x == 0;
-    unsigned long long t_ns;
-    if (trace) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ns)); dbg[0] = t_ns; }
-    int32_t i = items[w];
-    int64_t b = off[i];
-    int L = (int)(off[i + 1] - b);
-    if (L + 2 > arena_cap) {  // does not fit: the warp kernel does it from scratch
+    const unsigned int w = qi < nh ? (unsigned int)q.huge[qi] : (unsigned int)q.longq[qi - nh];
+    // debug timeline (tm_ctx_debug): item trace_qi's rounds in dbg[0..59],
+    // slowest item in dbg[60], stale / reused split infos in dbg[61] / dbg[62],
+    // re-walk fallbacks in dbg[63]
+    const bool trace = qi == trace_qi && threadIdx.x == 0;
+    unsigned long long t_ns, t_item;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_item));
+    if (trace) dbg[0] = t_item;
+    const int32_t i = items[w];
+    const int64_t b0 = off[i];
+    const int L = (int)(off[i + 1] - b0);
+    if (L > kSegMaxL || L < 3) {
       if (threadIdx.x == 0) item_state[w] = 3;
       continue;
     }
+    int pcap = 64;
+    while (pcap < 2 * L) pcap <<= 1;
+    for (int k = threadIdx.x; k < L; k += blockDim.x) P[k] = v[b0 + k];
+    for (int k = threadIdx.x; k < pcap; k += blockDim.x) pmap[k] = -1;
+    for (int k = threadIdx.x; k < (L + 31) / 32; k += blockDim.x) tipbits[k] = 0;
+    if (threadIdx.x == 0) { s_ntip = 0; s_ntouch = 0; s_fail = 0; s_stop = 1; }
     __syncthreads();
-    for (int k = threadIdx.x; k < L; k += blockDim.x) arena[k] = v[b + k];
-    if (threadIdx.x == 0) { s_top = L; s_fail = 0; }
-    __syncthreads();
-    int cur = 0, n = 1;
-    if (threadIdx.x == 0) { s_ntip = 0; s_ntouch = 0; }
-    __syncthreads();
-    // Every tip of the item is a tip of its initial polygon (an arc split only
-    // removes the split tip), and its split edge depends only on the frontier
-    // around v and u.  So the mesh rotations for all tips run up front, in
-    // parallel; a round reuses them unless an earlier promotion touched v or u.
-    for (int p = threadIdx.x; p < L; p += blockDim.x) {
-      int32_t a = arena[p == 0 ? L - 1 : p - 1];
-      if (a == arena[p + 1 == L ? 0 : p + 1]) {
-        int k = atomicAdd(&s_ntip, 1);
-        if (k < kMaxTips) { tipv[k] = arena[p]; tipb[k] = a; }
+    const SegView g{P, L, tipbits, pmap, pcap - 1, segs};
+    // tips of P (bitmap + list) and the pair map
+    for (int k = threadIdx.x; k < L; k += blockDim.x) {
+      int32_t a = P[k == 0 ? L - 1 : k - 1], y = P[k];
+      if (a == P[k + 1 == L ? 0 : k + 1]) {
+        atomicOr(&tipbits[k >> 5], 1u << (k & 31));
+        int t = atomicAdd(&s_ntip, 1);
+        if (t < kSegTips) { tipv[t] = y; tipb[t] = a; }
       }
+      uint32_t h = pair_hash(a, y) & (pcap - 1);
+      while (atomicCAS(&pmap[h], -1, k) != -1) h = (h + 1) & (pcap - 1);
     }
     __syncthreads();
-    const int ntip_pre = s_ntip < kMaxTips ? s_ntip : kMaxTips;
-    for (int k = wib; k < ntip_pre; k += kLongWarps) {
+    // every tip of the item is a tip of P (an arc split only removes the split
+    // tip); its split edge depends only on the frontier around v and u
+    const int ntip_pre = s_ntip < kSegTips ? s_ntip : kSegTips;
+    for (int k = wib; k < ntip_pre; k += kSegWarps) {
       SplitInfo si;
       bool ok = warp_split_info(c, tipv[k], tipb[k], i, fan, back, lane, false, true, &si);
       if (lane == 0) {
@@ -880,14 +1194,16 @@ __global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx 
         if (!ok) tipv[k] = -1;
       }
     }
+    if (threadIdx.x == 0) segs[0] = Seg{0, L, 0};
     __syncthreads();
     if (trace) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ns)); dbg[1] = t_ns; dbg[2] = L; dbg[3] = s_ntip; }
     if (wib == 0) {
-      uint32_t f0 = s_ntip > 0 ? F_TIP : 0u;
-      if (lane == 0) { recs[0] = make_int2(0, (int)((uint32_t)L | f0)); s_ntips = f0 ? 1 : 0; }
+      SPiece X0{0, 1, L, -1};
+      X0.ftip = s_ntip > 0 ? seg_first_tip(g, X0, lane) : -1;
+      if (lane == 0) { recs[0] = X0; s_ntips = X0.ftip >= 0 ? 1 : 0; }
     }
     __syncthreads();
-    int ntips = s_ntips;
+    int cur = 0, n = 1, ntips = s_ntips;
     long long depth = 0, splits = 0;
     bool bad = false, spill = false;
     while (ntips > 0) {
@@ -896,16 +1212,15 @@ __global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx 
         bad = true;
         break;
       }
-      int2* in = recs + cur * kLongRec;
-      int2* out = recs + (cur ^ 1) * kLongRec;
-      // output slot of every input record (prefix over tip flags) and the arena
-      // the round needs (a split writes |piece| + 2 slots), warp 0
-      __shared__ int s_need;
+      SPiece* in = recs + cur * kSegRec;
+      SPiece* out = recs + (cur ^ 1) * kSegRec;
+      // output slot of every input record (prefix over tip flags) and the
+      // segments the round may need, warp 0
       if (wib == 0) {
         int carry = 0, need = 0;
         for (int base = 0; base < n; base += 32) {
           int r = base + lane;
-          int t = (r < n && ((uint32_t)in[r].y & F_TIP)) ? 1 : 0;
+          int t = (r < n && in[r].ftip >= 0) ? 1 : 0;
           int inc = t;
           for (int o = 1; o < 32; o <<= 1) {
             int y = __shfl_up_sync(kFull, inc, o);
@@ -913,7 +1228,7 @@ __global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx 
           }
           if (r < n) s_out[r] = r + carry + inc - t;
           carry += __shfl_sync(kFull, inc, 31);
-          int nd = t ? (int)((uint32_t)in[r].y & LEN_MASK) + 2 : 0;
+          int nd = t ? 2 * (in[r].nseg + 4) : 0;
           for (int o = 16; o > 0; o >>= 1) nd += __shfl_xor_sync(kFull, nd, o);
           need += nd;
         }
@@ -921,71 +1236,90 @@ __global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx 
       }
       if (threadIdx.x == 0) s_ntips = 0;
       __syncthreads();
-      if (n + ntips > kLongRec || s_top + s_need > arena_cap) { spill = true; break; }  // uniform
+      if (n + ntips > kSegRec || s_stop + s_need > seg_cap) { spill = true; break; }  // uniform
       depth++;
-      const int ntouch0 = s_ntouch < kMaxTouch ? s_ntouch : -1;  // -1: overflowed, always recompute
+      const int ntouch0 = s_ntouch < kSegTouch ? s_ntouch : -1;  // -1: overflowed, always recompute
       __syncthreads();
-      // untouched records are pointer copies; tipped ones are split by a warp each
       for (int r = threadIdx.x; r < n; r += blockDim.x)
-        if (!((uint32_t)in[r].y & F_TIP)) out[s_out[r]] = in[r];
+        if (in[r].ftip < 0) out[s_out[r]] = in[r];
       int t_idx = 0;
       for (int r = 0; r < n; r++) {
-        if (!((uint32_t)in[r].y & F_TIP)) continue;
-        int mine = (t_idx++ % kLongWarps) == wib;
-        if (!mine) continue;
-        auto alloc = [&](long long m) -> int32_t* {
-          int o = 0;
-          if (lane == 0) o = atomicAdd(&s_top, (int)m);
-          o = __shfl_sync(kFull, o, 0);
-          if (o + m > arena_cap) return nullptr;
-          return arena + o;
-        };
-        int32_t *A, *B;
-        int al, bl;
-        const int32_t* X = arena + in[r].x;
-        const int Lr = (int)((uint32_t)in[r].y & LEN_MASK);
-        bool ok = false;
-        int pos = warp_first_tip(X, Lr, lane);
-        if (pos < 0) {
-          if (lane == 0) report(c.st, K_STRUCT, i);
-        } else {
-          int32_t v = X[pos], bv = X[pos == 0 ? Lr - 1 : pos - 1];
-          int k = warp_find_first(ntip_pre, lane, [&](int q) { return tipv[q] == v; });
-          SplitInfo si;
-          bool use = k >= 0 && ntouch0 >= 0;
-          if (use) {
-            si = tipinfo[k];
-            bool stale = warp_find_first(ntouch0, lane, [&](int q) {
-                           int32_t x = touched[q];
-                           return x == v || x == si.u;
-                         }) >= 0;
-            use = !stale;
-          }
-          if (use) {
-            if (lane == 0) promote(c, si.e, si.te);
-            __syncwarp();
-            ok = true;
-          } else {
-            ok = warp_split_info(c, v, bv, i, fan, back, lane, true, false, &si);
-          }
+        if (in[r].ftip < 0) continue;
+        if ((t_idx++ % kSegWarps) != wib) continue;
+        const SPiece X = in[r];
+        const int pos = X.ftip;
+        long long ck0 = clock64();
+        const int32_t tv_ = selem(g, X, pos, lane), bv = selem(g, X, pos == 0 ? X.len - 1 : pos - 1, lane);
+        int k = warp_find_first(ntip_pre, lane, [&](int qq) { return tipv[qq] == tv_; });
+        SplitInfo si;
+        bool use = k >= 0 && ntouch0 >= 0;
+        if (use) {
+          si = tipinfo[k];
+          bool stale = warp_find_first(ntouch0, lane, [&](int qq) {
+                         int32_t x = touched[qq];
+                         return x == tv_ || x == si.u;
+                       }) >= 0;
+          use = !stale;
+        }
+        if (lane == 0) atomicAdd(dbg + (use ? 62 : 61), 1ull);
+        bool ok = use || warp_split_info(c, tv_, bv, i, fan, back, lane, false, false, &si);
+        SPiece A{0, 0, 0, -1}, B{0, 0, 0, -1};
+        long long ck1 = clock64();
+        if (ok && !seg_split_arcs(c, g, X, pos, tv_, si, &s_stop, seg_cap, lane, &A, &B, qi == trace_qi ? dbg + 52 : nullptr)) {
+          // re-walk fallback (reparation.py:216-229) with the strict length law;
+          // the pieces come back as one-vertex segments
+          if (lane == 0) { promote(c, si.e, si.te); atomicAdd(dbg + 63, 1ull); }
+          __syncwarp();
+          int32_t *pa = nullptr, *pb = nullptr;
+          int la = 0, lb = 0;
+          auto galloc = [&](long long m) -> int32_t* {
+            long long o = 0;
+            if (lane == 0) o = palloc(c, m);
+            o = __shfl_sync(kFull, o, 0);
+            return o < 0 ? nullptr : c.pool + o;
+          };
+          int rr = warp_rewalk_split(c, si.e, si.te, X.len, i, galloc, lane, &pa, &la, &pb, &lb);
+          if (rr == 0 && lane == 0) report(c.st, K_SPLIT_LAW, i);
+          ok = rr == 1;
           if (ok) {
-            if (lane == 0) {
-              int tk = atomicAdd(&s_ntouch, 2);
-              if (tk + 2 <= kMaxTouch) { touched[tk] = v; touched[tk + 1] = si.u; }
+            int sb = 0;
+            if (lane == 0) sb = atomicAdd(&s_stop, la + lb);
+            sb = __shfl_sync(kFull, sb, 0);
+            if (sb + la + lb > seg_cap) {
+              if (lane == 0) report(c.st, K_STRUCT, i);
+              ok = false;
+            } else {
+              for (int x = lane; x < la; x += 32) segs[sb + x] = Seg{~pa[x], 1, x};
+              for (int x = lane; x < lb; x += 32) segs[sb + la + x] = Seg{~pb[x], 1, x};
+              A = SPiece{sb, la, la, -1};
+              B = SPiece{sb + la, lb, lb, -1};
             }
-            ok = warp_split_arcs(c, X, Lr, pos, si, i, lane, alloc, &A, &al, &B, &bl);
           }
         }
+        __syncwarp();
         if (!ok) {
           if (lane == 0) atomicCAS(&s_fail, 0, 1);
           continue;
         }
-        uint32_t fa = warp_tip_flag(A, al, lane), fb = warp_tip_flag(B, bl, lane);
+        if (lane == 0) {
+          int tk = atomicAdd(&s_ntouch, 2);
+          if (tk + 2 <= kSegTouch) { touched[tk] = tv_; touched[tk + 1] = si.u; }
+        }
+        long long ck2 = clock64();
+        A.ftip = seg_first_tip(g, A, lane);
+        B.ftip = seg_first_tip(g, B, lane);
+        long long ck3 = clock64();
+        if (qi == trace_qi && lane == 0) {
+          atomicAdd(dbg + 56, (unsigned long long)(ck1 - ck0));
+          atomicAdd(dbg + 57, (unsigned long long)(ck2 - ck1));
+          atomicAdd(dbg + 58, (unsigned long long)(ck3 - ck2));
+          atomicAdd(dbg + 59, 1ull);
+        }
         if (lane == 0) {
           int o = s_out[r];
-          out[o] = make_int2((int)(A - arena), (int)((uint32_t)al | fa));
-          out[o + 1] = make_int2((int)(B - arena), (int)((uint32_t)bl | fb));
-          atomicAdd(&s_ntips, (fa ? 1 : 0) + (fb ? 1 : 0));
+          out[o] = A;
+          out[o + 1] = B;
+          atomicAdd(&s_ntips, (A.ftip >= 0 ? 1 : 0) + (B.ftip >= 0 ? 1 : 0));
         }
       }
       __syncthreads();
@@ -993,9 +1327,9 @@ __global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx 
       n += ntips;
       ntips = s_ntips;
       cur ^= 1;
-      if (trace && depth < 56) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ns)); dbg[4 + depth] = t_ns; }
+      if (trace && depth < 48) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ns)); dbg[4 + depth] = t_ns; }
       if (s_fail) {
-        bad = true;  // (the arena cannot overflow: capacity was checked before the round)
+        bad = true;
         break;
       }
     }
@@ -1003,13 +1337,11 @@ __global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx 
       if (threadIdx.x == 0) { item_state[w] = 1; item_list[w] = -1; item_n[w] = 0; }
       continue;
     }
-    // leaves (or the state before an unsplit round) -> global pool
-    int2* fin = recs + cur * kLongRec;
-    __shared__ long long s_base;
-    __shared__ int s_tot;
+    // leaves (or the pieces before an unsplit round) -> global pool
+    const SPiece* fin = recs + cur * kSegRec;
     if (threadIdx.x == 0) {
       int tot = 0;
-      for (int r = 0; r < n; r++) tot += (int)((uint32_t)fin[r].y & LEN_MASK);
+      for (int r = 0; r < n; r++) tot += fin[r].len;
       s_tot = tot;
       s_base = palloc(c, tot + 2 * (long long)n);
     }
@@ -1018,12 +1350,12 @@ __global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx 
       if (threadIdx.x == 0) { report(c.st, K_POOL, i); item_state[w] = 1; item_list[w] = -1; item_n[w] = 0; }
       continue;
     }
-    long long list = s_base + s_tot;
+    const long long list = s_base + s_tot;
     if (wib == 0) {
       int carry = 0;
       for (int base = 0; base < n; base += 32) {
         int r = base + lane;
-        int ln = r < n ? (int)((uint32_t)fin[r].y & LEN_MASK) : 0;
+        int ln = r < n ? fin[r].len : 0;
         int inc = ln;
         for (int o = 1; o < 32; o <<= 1) {
           int y = __shfl_up_sync(kFull, inc, o);
@@ -1031,44 +1363,77 @@ __global__ void __launch_bounds__(32 * kLongWarps) k_repair_tips_long(RepairCtx 
         }
         if (r < n) {
           c.pool[list + 2 * r] = (int32_t)(s_base + carry + inc - ln);
-          c.pool[list + 2 * r + 1] = fin[r].y;
+          c.pool[list + 2 * r + 1] = (int32_t)((uint32_t)ln | (fin[r].ftip >= 0 ? F_TIP : 0u));
         }
         carry += __shfl_sync(kFull, inc, 31);
       }
     }
     __syncthreads();
-    for (int r = wib; r < n; r += kLongWarps) {
-      uint32_t ro = (uint32_t)c.pool[list + 2 * r];
-      int ln = (int)((uint32_t)fin[r].y & LEN_MASK);
-      const int32_t* src = arena + fin[r].x;
-      warp_copy(c.pool + ro, ln, lane, [&](int k) { return src[k]; });
+    for (int r = wib; r < n; r += kSegWarps) {
+      int32_t* dst = c.pool + (uint32_t)c.pool[list + 2 * r];
+      const SPiece X = fin[r];
+      for (int s = 0; s < X.nseg; s++) {
+        Seg sg = segs[X.soff + s];
+        for (int x = lane; x < sg.len; x += 32) dst[sg.loff + x] = sval(g, sg, x);
+      }
     }
     __syncthreads();
     if (spill) {
-      // record list too long for shared memory: the warp kernel continues
+      // record list or segment arena too small: the warp kernel continues
       if (threadIdx.x == 0) { item_state[w] = 2; item_list[w] = list; item_n[w] = n; item_depth[w] = (int)depth; }
       if (threadIdx.x == 0 && splits) atomicAdd(stats + 1, (unsigned long long)splits);
       continue;
     }
-    if (wib == 0) {
-      // leaf flags from shared memory (fast), then the common epilogue
-      unsigned long long ex_sum = 0;
-      for (int r = 0; r < n; r++) {
-        int ln = (int)((uint32_t)fin[r].y & LEN_MASK);
-        int ex = warp_extra_visits(arena + fin[r].x, ln, lane);
-        if (ex > 0 && lane == 0) c.pool[list + 2 * r + 1] = (int32_t)((uint32_t)fin[r].y | F_REP);
-        ex_sum += ex;
+    // repeated flags and extra visits of the leaves (pinch guard,
+    // reparation.py:322): per-warp hash sets in the (now free) pair map
+    __shared__ unsigned long long s_ex;
+    if (threadIdx.x == 0) s_ex = 0;
+    __syncthreads();
+    int32_t* set = pmap + wib * (kPairCap / kSegWarps);
+    for (int r = wib; r < n; r += kSegWarps) {
+      const uint32_t ro = (uint32_t)c.pool[list + 2 * r];
+      const int ln = fin[r].len;
+      const int32_t* s = c.pool + ro;
+      int ex;
+      if (2 * ln <= kPairCap / kSegWarps) {
+        int cap = 64;
+        while (cap < 2 * ln) cap <<= 1;
+        for (int x = lane; x < cap; x += 32) set[x] = -1;
+        __syncwarp();
+        int mine = 0;
+        for (int x = lane; x < ln; x += 32) {
+          int32_t val = s[x];
+          uint32_t slot = ((uint32_t)val * 0x9E3779B1u) & (cap - 1);
+          for (;;) {
+            int32_t prev = atomicCAS(&set[slot], -1, val);
+            if (prev == -1) break;
+            if (prev == val) { mine++; break; }
+            slot = (slot + 1) & (cap - 1);
+          }
+        }
+        for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(kFull, mine, o);
+        ex = mine;
+        __syncwarp();
+      } else {
+        ex = warp_extra_visits(s, ln, lane);
       }
-      if (lane == 0) {
-        item_state[w] = 1;
-        item_list[w] = list;
-        item_n[w] = n;
-        if (depth > 0) atomicMax(stats + 0, (unsigned long long)depth);
-        if (splits) atomicAdd(stats + 1, (unsigned long long)splits);
-        if (ex_sum) atomicAdd(stats + 5, ex_sum);
+      if (lane == 0 && ex > 0) {
+        c.pool[list + 2 * r + 1] = (int32_t)((uint32_t)c.pool[list + 2 * r + 1] | F_REP);
+        atomicAdd(&s_ex, (unsigned long long)ex);
       }
     }
     __syncthreads();
+    if (threadIdx.x == 0) {
+      item_state[w] = 1;
+      item_list[w] = list;
+      item_n[w] = n;
+      if (depth > 0) atomicMax(stats + 0, (unsigned long long)depth);
+      if (splits) atomicAdd(stats + 1, (unsigned long long)splits);
+      if (s_ex) atomicAdd(stats + 5, s_ex);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ns));
+      unsigned long long dur = (t_ns - t_item) / 100;  // 0.1 us units
+      atomicMax(dbg + 60, (dur << 32) | ((unsigned long long)(depth & 0xFFFF) << 16) | (qi & 0xFFFF));
+    }
   }
 }
 
@@ -1361,26 +1726,36 @@ void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, in
   note_launch(1);
 }
 
-void launch_repair_tips(const RepairArgs& a, cudaStream_t s) {
+void launch_repair_tips_long(const RepairArgs& a, cudaStream_t s) {
   RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st};
   static bool attr = false;
-  size_t smem = long_smem_bytes();
+  size_t smem = seg_smem_bytes();
   if (!attr) {
-    cudaFuncSetAttribute(k_repair_tips_long, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_repair_tips_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  static int arena_cap = -1;
-  if (arena_cap < 0) {  // testing hook: TERMESH_LONG_ARENA shrinks the shared arena to exercise spills
-    const char* e = getenv("TERMESH_LONG_ARENA");
-    arena_cap = (e && *e) ? atoi(e) : kLongArena;
-    if (arena_cap > kLongArena) arena_cap = kLongArena;
+  static int trace_qi = -1;
+  if (trace_qi < 0) {  // debug: which long item's rounds are timestamped
+    const char* e = getenv("TERMESH_TRACE_QI");
+    trace_qi = (e && *e) ? atoi(e) : 0;
   }
-  k_repair_tips_long<<<kNumSMs, 32 * kLongWarps, smem, s>>>(c, a.items, a.n_items, a.off, a.v, a.item_list,
-                                                             a.item_n, a.item_state, a.item_depth, a.stats,
-                                                             arena_cap, a.q, a.dbg);
-  k_repair_tips<<<kNumSMs * 8, 32 * kTipWarps, 0, s>>>(c, a.items, a.n_items, a.off, a.v, a.item_list, a.item_n,
-                                                       a.item_state, a.item_depth, a.stats);
-  note_launch(2);
+  static int seg_cap = -1;
+  if (seg_cap < 0) {  // testing hook: TERMESH_SEG_CAP shrinks the segment arena to exercise spills
+    const char* e = getenv("TERMESH_SEG_CAP");
+    seg_cap = (e && *e) ? atoi(e) : kSegCap;
+    if (seg_cap > kSegCap) seg_cap = kSegCap;
+  }
+  k_repair_tips_seg<<<kNumSMs, 32 * kSegWarps, smem, s>>>(c, a.items, a.off, a.v, a.item_list, a.item_n,
+                                                           a.item_state, a.item_depth, a.stats, a.q, a.dbg,
+                                                           (unsigned int)trace_qi, seg_cap);
+  note_launch(1);
+}
+
+void launch_repair_tips(const RepairArgs& a, int mode, cudaStream_t s) {
+  RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st};
+  k_repair_tips<<<mode ? kNumSMs : kNumSMs * 8, 32 * kTipWarps, 0, s>>>(
+      c, a.items, a.n_items, a.off, a.v, a.item_list, a.item_n, a.item_state, a.item_depth, a.stats, a.q, mode);
+  note_launch(1);
 }
 
 void launch_repair_pinch(const RepairArgs& a, cudaStream_t s) {

@@ -212,7 +212,7 @@ def test_u1m_matches_reference_hashes(cuda):
 
 def test_pool_overflow_retry_is_exact(cuda):
     """A deliberately tiny repair pool forces the overflow -> restore -> retry
-    path (pipeline and phase-level API), and a tiny shared arena forces long
+    path (pipeline and phase-level API), and a tiny segment arena forces long
     items to spill to the global pool mid-lineage; results must not change."""
     import subprocess
     import sys
@@ -231,7 +231,7 @@ def test_pool_overflow_retry_is_exact(cuda):
         "    assert np.array_equal(f2.csr()[1], g['final_verts']), name\n"
         "print('ok')\n")
     import os
-    env = dict(os.environ, TERMESH_POOL_INIT="2048", TERMESH_LONG_ARENA="600")
+    env = dict(os.environ, TERMESH_POOL_INIT="2048", TERMESH_SEG_CAP="48")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
