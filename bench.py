@@ -20,8 +20,11 @@ GPU arm (default):
   cpu_baseline  the CPU oracle port (oracle/, the reference algorithm in C,
          OpenMP label+traversal, sequential repair as the reference's "mixed"
          mode) on the same mesh, rank 0 at N=1 only.
-Multi-GPU (torchrun): every rank processes its own independent mesh (seed =
-rank): weak scaling, no data-path collective; barrier + max-over-ranks timing.
+Multi-GPU (torchrun): the mesh is replicated on every rank and
+the seeds are partitioned (rank r owns triangles [rT/G, (r+1)T/G)); each step
+ends with the exchange -- NCCL all-gather of the per-rank (polygons, slots)
+counts and the shift of the local CSR to its global base.  Strong scaling:
+value = T / (slowest rank's step time); barrier + max-over-ranks timing.
 
 Reference arm (--impl reference): the reference algorithm's CPU port (oracle/)
 on the box's host cores over the same workload, rank 0 only.
@@ -42,9 +45,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    "u1m": dict(n=1_000_000, desc="1M uniform random points in the unit square, scipy Delaunay (seed=rank)"),
-    "u10m": dict(n=10_000_000, desc="10M uniform random points in the unit square, scipy Delaunay (seed=rank)"),
-    "u100k": dict(n=100_000, desc="100k uniform random points in the unit square, scipy Delaunay (seed=rank)"),
+    "u1m": dict(n=1_000_000, desc="1M uniform random points in the unit square, scipy Delaunay (seed 0)"),
+    "u10m": dict(n=10_000_000, desc="10M uniform random points in the unit square, scipy Delaunay (seed 0)"),
+    "u100k": dict(n=100_000, desc="100k uniform random points in the unit square, scipy Delaunay (seed 0)"),
 }
 METRIC = "triangles/sec end-to-end mesh->polygons"
 UNIT = "triangles/s"
@@ -115,8 +118,10 @@ def algorithmic_bytes(n, T, F, P, Fp, Pp):
     array touched once in its device dtype.  R = rulers = seeds + F/8."""
     R = P + F // 8
     return {
-        "label_a_tri_pass": 24 * T + 16 * n + 12 * T + 1 * T + 12 * T + 4 * n,   # tri i64 in, xy, tri32, max_edge, twin, trivertex
-        "label_b_edges": 12 * T + 1 * T + 12 * T + 1 * T,                       # hw in/out, max_edge, seed
+        # pass A: tri i64 in, xy gathers, tri32 + max_edge + trivertex out, 1.5 ascending keys (8 B) in the twin table
+        "label_a_tri_pass": 24 * T + 16 * n + 12 * T + 1 * T + 4 * n + 12 * T,
+        # pass B: tri32 + max_edge in, 1.5 key probes, packed half-edge words + seeds out
+        "label_b_edges": 12 * T + 1 * T + 12 * T + 12 * T + 1 * T,
         "select_seeds": 1 * T + 4 * P,
         "trav_start": 4 * P + 12 * P + 4 * P,
         "trav_rulers": 12 * T + 12 * T + 8 * R,                                 # hw scan + rotations, rnext/rdist
@@ -139,8 +144,10 @@ def run_gpu(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    tri = load_mesh(args.workload, rank)
+    from paper_2204_05438_b200 import distributed as D
+    tri = load_mesh(args.workload, 0)  # one mesh, replicated on every rank
     n, T = tri.n_vertices, tri.n_triangles
+    t_begin, t_end = D.partition(T, world)[rank]  # this rank's seed range
     xy = torch.from_numpy(tri.vertices).to(dev)
     tr = torch.from_numpy(tri.triangles).to(dev)
     off = torch.empty(T + 1, dtype=torch.int64, device=dev)
@@ -153,10 +160,14 @@ def run_gpu(args, rank, world, local_rank):
     npol, nsl = ctypes.c_int64(), ctypes.c_int64()
     stats = (ctypes.c_int64 * 8)()
 
+    ctx.check(L.tm_ctx_set_partition(ctx.ptr, t_begin, t_end))
+
     def step():
         rc = L.tm_mesh_to_polygons(ctx.ptr, _capi.ptr(xy), n, _capi.ptr(tr), 64, T, 0, _capi.ptr(off),
                                    _capi.ptr(verts), T, 3 * T, ctypes.byref(npol), ctypes.byref(nsl), stats, sp)
         ctx.check(rc)
+        if world > 1:  # the exchange step: all-gather counts (NCCL), shift to the global slot base
+            D.stitch(off, verts, npol.value, nsl.value)
 
     for _ in range(args.warmup):
         step()
@@ -184,7 +195,7 @@ def run_gpu(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = world * T / (ms_per_step / 1e3)
+    value = T / (ms_per_step / 1e3)  # the one mesh's triangles over the slowest rank's time
     P_out, F_out = npol.value, nsl.value
     repair_stats = dict(zip(_capi.STAT_NAMES, list(stats)))
 
@@ -199,7 +210,7 @@ def run_gpu(args, rank, world, local_rank):
     segs = ctx.segments(reset=True)
     ctx.set_profiling(False)
 
-    # traversal-phase counts for the byte model
+    # traversal-phase counts for the byte model (this rank's seed range)
     lab = tm.label_all(tri, check=False)
     m0 = tm.build_polygon_mesh(tri, lab)
     P0, F0 = m0.count, int(m0.csr()[0][-1])
@@ -236,6 +247,8 @@ def run_gpu(args, rank, world, local_rank):
         rc = L.tm_mesh_to_polygons_host(ctx.ptr, _capi.ptr(h_xy), n, _capi.ptr(h_tr), T, 0, _capi.ptr(h_off),
                                         _capi.ptr(h_v), T, 3 * T, ctypes.byref(npol), ctypes.byref(nsl), stats)
         ctx.check(rc)
+        if world > 1:
+            D.stitch(h_off, h_v, npol.value, nsl.value)
 
     for _ in range(args.warmup):
         e2e_step()
@@ -250,17 +263,18 @@ def run_gpu(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(e2e_tot, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_tot.item()) / args.steps * 1e3
-    e2e = {"value": round(world * T / (e2e_ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(e2e_ms, 3),
+    e2e = {"value": round(T / (e2e_ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(e2e_ms, 3),
            "h2d_bytes_per_step": 16 * n + 24 * T, "d2h_bytes_per_step": 8 * (npol.value + 1) + 4 * nsl.value,
            "api": "tm_mesh_to_polygons_host (C ABI, pinned host buffers)"}
     # parity spot check of the timed output against the oracle-free golden counts
     out = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32/f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "int32/f64", "data": "synthetic",
         "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"], "n_vertices": n,
-                   "triangles_per_gpu": T, "polygons": P_out, "polygon_slots": F_out,
-                   "l2": "flushed (256 MiB write) between steps", "parallelism": f"independent meshes x{world}"},
+                   "triangles": T, "seed_range_rank0": [t_begin, t_end], "polygons_rank0": P_out,
+                   "polygon_slots_rank0": F_out, "l2": "flushed (256 MiB write) between steps",
+                   "parallelism": f"replicated mesh, seeds partitioned x{world}, NCCL all-gather of counts"},
         "e2e": e2e, "roofline": roofline, "kernels": kernels, "repair_stats": repair_stats,
         "gpu_launches": int(launches), "clocks": clk.summary(),
         "step_ms": {"min": round(min(step_ms), 4), "median": round(statistics.median(step_ms), 4),

@@ -100,6 +100,15 @@ int tm_ctx_set_profiling(tm_ctx *ctx, int on);
 int tm_ctx_segment_ms(tm_ctx *ctx, double *ms, int64_t *counts, int n, int reset);
 const char *tm_segment_name(int k);
 int64_t tm_launch_count(void);
+/* Seed partition for multi-GPU runs: traversal, repair and
+ * stitch of this context only cover the polygons whose seed triangle lies in
+ * [t_begin, t_end) (t_end = -1: up to T); labels always cover the whole mesh.
+ * With ranks owning consecutive ranges, the concatenation of their outputs in
+ * rank order is the single-GPU output (seed order = raw order, F13). */
+int tm_ctx_set_partition(tm_ctx *ctx, int64_t t_begin, int64_t t_end);
+/* d_offsets[0..n_polys] += delta: places a rank's CSR at its global slot base
+ * (the exclusive prefix of the all-gathered per-rank slot counts). */
+int tm_shift_offsets(int64_t *d_offsets, int64_t n_polys, int64_t delta, void *stream);
 /* kernel debug timestamps (ns, %globaltimer) of the last run: repair lineage trace */
 int tm_ctx_debug(const tm_ctx *ctx, uint64_t *out, int n);
 

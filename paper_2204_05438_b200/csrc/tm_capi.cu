@@ -84,12 +84,12 @@ struct GraphKey {
   const void* tri = nullptr;
   void* off = nullptr;
   void* v = nullptr;
-  int64_t n = -1, T = -1;
+  int64_t n = -1, T = -1, tb = 0, te = 0;
   int bits = 0, check = 0;
   unsigned long long pool_cap = 0;
   bool operator==(const GraphKey& o) const {
-    return xy == o.xy && tri == o.tri && off == o.off && v == o.v && n == o.n && T == o.T && bits == o.bits &&
-           check == o.check && pool_cap == o.pool_cap;
+    return xy == o.xy && tri == o.tri && off == o.off && v == o.v && n == o.n && T == o.T && tb == o.tb &&
+           te == o.te && bits == o.bits && check == o.check && pool_cap == o.pool_cap;
   }
 };
 
@@ -128,6 +128,7 @@ struct tm_ctx {
   unsigned long long pool_cap = 0;
   int64_t ecap = 0;
   int use_graph = 1;
+  int64_t part_begin = 0, part_end = -1;  // seed partition [begin, end) in triangles (-1: T)
   long long graph_kernels = 0;  // kernels per graph replay (counted at capture)
 };
 
@@ -358,14 +359,27 @@ static int enqueue_label(tm_ctx* ctx, const double* d_xy, int64_t n, const void*
   return TM_OK;
 }
 
+// the seed partition of this context clipped to [0, T]
+static void part_range(const tm_ctx* ctx, int64_t T, int64_t* tb, int64_t* te) {
+  int64_t b = ctx->part_begin, e = ctx->part_end < 0 ? T : ctx->part_end;
+  if (b < 0) b = 0;
+  if (b > T) b = T;
+  if (e > T) e = T;
+  if (e < b) e = b;
+  *tb = b;
+  *te = e;
+}
+
 static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* d_hw, const uint8_t* d_seed,
                             int64_t T, int64_t* d_off, int32_t* d_v, cudaStream_t s) {
   Counters* dc = dc_of(ctx);
   int64_t Tn = T > 0 ? T : 1;
   int64_t* tiles = ctx->tiles.as<int64_t>();
+  int64_t tb = 0, te = 0;
+  part_range(ctx, T, &tb, &te);
   {
     SegTimer t_(ctx, S_SEEDS, s);
-    launch_select_flags(d_seed, T, ctx->seeds.as<int32_t>(), &dc->n_seeds, tiles, s);
+    launch_select_flags(d_seed + tb, te - tb, ctx->seeds.as<int32_t>(), &dc->n_seeds, tiles, s, tb);
   }
   CK(cudaMemsetAsync(ctx->stamp.p, 0xFF, Tn * sizeof(int32_t), s));
   CK(cudaMemsetAsync(ctx->startbits.p, 0, ((3 * Tn + 31) / 32) * sizeof(uint32_t), s));
@@ -377,8 +391,8 @@ static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* 
   }
   {
     SegTimer t_(ctx, S_TRAV_RULERS, s);
-    launch_ruler_walk(d_hw, ctx->startbits.as<uint32_t>(), T, ctx->rnext.as<int32_t>(), ctx->rdist.as<int32_t>(),
-                      &dc->st, s);
+    launch_ruler_walk(d_hw, ctx->startbits.as<uint32_t>(), T, tb, te, ctx->start.as<int32_t>(), &dc->n_seeds, Tn,
+                      ctx->rnext.as<int32_t>(), ctx->rdist.as<int32_t>(), &dc->st, s);
   }
   {
     SegTimer t_(ctx, S_TRAV_LEN, s);
@@ -584,6 +598,20 @@ int tm_ctx_debug(const tm_ctx* ctx, uint64_t* out, int n) {
   return TM_OK;
 }
 
+int tm_ctx_set_partition(tm_ctx* ctx, int64_t t_begin, int64_t t_end) {
+  if (!ctx) return TM_ERR_ARGUMENT;
+  if (t_begin < 0 || (t_end >= 0 && t_end < t_begin)) return set_err(ctx, TM_ERR_ARGUMENT, "bad seed partition");
+  ctx->part_begin = t_begin;
+  ctx->part_end = t_end;
+  return TM_OK;
+}
+
+int tm_shift_offsets(int64_t* d_offsets, int64_t n_polys, int64_t delta, void* stream) {
+  if (n_polys < 0) return TM_ERR_ARGUMENT;
+  if (delta != 0) launch_shift(d_offsets, n_polys, delta, (cudaStream_t)stream);
+  return cudaGetLastError() == cudaSuccess ? TM_OK : TM_ERR_CUDA;
+}
+
 int tm_ctx_phase_ms(const tm_ctx* ctx, double* ms3) {
   if (!ctx || !ms3) return TM_ERR_ARGUMENT;
   for (int k = 0; k < 3; k++) ms3[k] = ctx->phase_ms[k];
@@ -747,7 +775,8 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
 
   cudaStream_t s = user;
   if (ctx->use_graph && !ctx->prof.on) {
-    GraphKey key{d_xy, d_tri, d_off, d_v, n, T, tri_bits, check, ctx->pool_cap};
+    GraphKey key{d_xy, d_tri, d_off, d_v, n, T, 0, 0, tri_bits, check, ctx->pool_cap};
+    part_range(ctx, T, &key.tb, &key.te);
     if (!ctx->graph || !(key == ctx->gkey)) {
       if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
       ctx->graph = nullptr;

@@ -27,15 +27,18 @@ void launch_pack_frontier(int32_t* hw, int64_t T, const uint8_t* fr, cudaStream_
 size_t scan_scratch_elems(int64_t n_cap);
 void launch_scan_dev(const int64_t* in, int64_t* out, const int64_t* n_dev, int64_t n_cap, int64_t* tile_sums,
                      cudaStream_t s);
+void launch_shift(int64_t* a, int64_t n, int64_t delta, cudaStream_t s);
 void launch_gather_at(const int64_t* arr, const int64_t* idx, int64_t* dst, cudaStream_t s);
 void launch_select_flags(const uint8_t* flag, int64_t n, int32_t* out, int64_t* n_out, int64_t* tile_sums,
-                         cudaStream_t s);
+                         cudaStream_t s, int64_t base_index = 0);
 
 // tm_traverse.cu (Pp = device count, Pcap = host bound for the grid)
 void launch_trav_start(const int32_t* hw, const int32_t* seeds, const int64_t* Pp, int64_t Pcap, int32_t* start,
                        int32_t* overflow, unsigned int* n_overflow, int32_t* queue, int32_t* stamp, uint32_t* bits,
                        DevStatus* st, cudaStream_t s);
-void launch_ruler_walk(const int32_t* hw, const uint32_t* bits, int64_t T, int32_t* rnext, int32_t* rdist,
+// rulers: starts of the selected seeds + sampled half-edges of triangles [t_begin, t_end)
+void launch_ruler_walk(const int32_t* hw, const uint32_t* bits, int64_t T, int64_t t_begin, int64_t t_end,
+                       const int32_t* start, const int64_t* Pp, int64_t Pcap, int32_t* rnext, int32_t* rdist,
                        DevStatus* st, cudaStream_t s);
 void launch_chain_count(const int32_t* seeds, const int32_t* start, const int64_t* Pp, int64_t Pcap, int64_t T,
                         const int32_t* rnext, const int32_t* rdist, int64_t* len, int64_t* nrul, DevStatus* st,

@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_final(const int64_t* __re
   }
 }
 
-// ---- ascending indices t with flag[t] != 0 (seed compaction), count -> *n_out
+// ---- ascending indices base_index + t with flag[t] != 0 (seed compaction), count -> *n_out
 __global__ void __launch_bounds__(kScanThreads) k_flag_reduce(const uint8_t* __restrict__ flag, int64_t n,
                                                               int64_t* __restrict__ tile_sums) {
   int64_t base = (int64_t)blockIdx.x * kTile;
@@ -130,7 +130,8 @@ __global__ void __launch_bounds__(kScanThreads) k_flag_reduce(const uint8_t* __r
 
 __global__ void __launch_bounds__(kScanThreads) k_flag_scatter(const uint8_t* __restrict__ flag, int64_t n,
                                                                const int64_t* __restrict__ tile_sums,
-                                                               int32_t* __restrict__ out, int64_t* n_out) {
+                                                               int32_t* __restrict__ out, int64_t* n_out,
+                                                               int64_t base_index) {
   int64_t base = (int64_t)blockIdx.x * kTile;
   int64_t first = base + (int64_t)threadIdx.x * kScanItems;
   uint8_t f[kScanItems];
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(kScanThreads) k_flag_scatter(const uint8_t* __
   int64_t pos = block_exclusive_scan<int64_t>(s, &tot) + tile_sums[blockIdx.x];
 #pragma unroll
   for (int k = 0; k < kScanItems; k++)
-    if (f[k]) out[pos++] = (int32_t)(first + k);
+    if (f[k]) out[pos++] = (int32_t)(base_index + first + k);
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kScanThreads - 1) *n_out = pos;
 }
 
@@ -162,12 +163,12 @@ void launch_scan_dev(const int64_t* in, int64_t* out, const int64_t* n_dev, int6
 }
 
 void launch_select_flags(const uint8_t* flag, int64_t n, int32_t* out, int64_t* n_out, int64_t* tile_sums,
-                         cudaStream_t s) {
+                         cudaStream_t s, int64_t base_index) {
   int nt = (int)((n + kTile - 1) / kTile);
   if (nt < 1) nt = 1;
   k_flag_reduce<<<nt, kScanThreads, 0, s>>>(flag, n, tile_sums);
   k_scan_tiles<<<1, kScanThreads, 0, s>>>(tile_sums, nullptr, n);
-  k_flag_scatter<<<nt, kScanThreads, 0, s>>>(flag, n, tile_sums, out, n_out);
+  k_flag_scatter<<<nt, kScanThreads, 0, s>>>(flag, n, tile_sums, out, n_out, base_index);
   note_launch(3);
 }
 
@@ -178,6 +179,19 @@ __global__ void k_gather_at(const int64_t* __restrict__ arr, const int64_t* __re
 // *dst = arr[*idx] on the device (no host round trip)
 void launch_gather_at(const int64_t* arr, const int64_t* idx, int64_t* dst, cudaStream_t s) {
   k_gather_at<<<1, 32, 0, s>>>(arr, idx, dst);
+  note_launch(1);
+}
+
+// offsets[i] += delta for i in [0, n] (stitching a rank's CSR into the global one)
+__global__ void k_shift(int64_t* __restrict__ a, int64_t n, int64_t delta) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] += delta;
+}
+
+void launch_shift(int64_t* a, int64_t n, int64_t delta, cudaStream_t s) {
+  int64_t g = (n + 1 + 255) / 256;
+  if (g > kNumSMs * 8) g = kNumSMs * 8;
+  k_shift<<<(int)(g < 1 ? 1 : g), 256, 0, s>>>(a, n, delta);
   note_launch(1);
 }
 

@@ -52,7 +52,17 @@ __device__ __forceinline__ void mark_start(uint32_t* bits, int32_t h) { atomicOr
 __device__ __forceinline__ bool is_start(const uint32_t* bits, int32_t h) { return (__ldg(bits + (h >> 5)) >> (h & 31)) & 1u; }
 // 1 in 8 half-edges, by a multiplicative hash of the id
 __device__ __forceinline__ bool sampled(int32_t h) { return ((uint32_t)h * 0x9E3779B1u) < (1u << 29); }
-__device__ __forceinline__ bool is_ruler(const uint32_t* bits, int32_t h) { return sampled(h) || is_start(bits, h); }
+// Rulers of this run: the start half-edges of its seeds, plus the sampled
+// half-edges of its own half-edge range [hb, he) (the whole mesh on one GPU;
+// a rank's triangle range when the seeds are partitioned, so the ruler walks
+// are partitioned too and other ranks' rulers never end a walk).
+struct RulerSet {
+  const uint32_t* bits;
+  int32_t hb, he;
+};
+__device__ __forceinline__ bool is_ruler(const RulerSet& rs, int32_t h) {
+  return (sampled(h) && h >= rs.hb && h < rs.he) || is_start(rs.bits, h);
+}
 
 __global__ void __launch_bounds__(256) k_trav_start(const int32_t* __restrict__ hw, const int32_t* __restrict__ seeds,
                                                     const int64_t* __restrict__ Pp, int32_t* __restrict__ start,
@@ -98,20 +108,41 @@ __global__ void k_bfs_slow(const int32_t* __restrict__ hw, const int32_t* __rest
 }
 
 // (1) every ruler walks to the next ruler: rnext/rdist indexed by half-edge id
-__global__ void __launch_bounds__(256) k_ruler_walk(const int32_t* __restrict__ hw, const uint32_t* __restrict__ bits,
-                                                    int64_t H, long long limit, int32_t* __restrict__ rnext,
-                                                    int32_t* __restrict__ rdist, DevStatus* st) {
-  for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < H; h += (int64_t)gridDim.x * blockDim.x) {
-    if (!hw_front(hw[h]) || !is_ruler(bits, (int32_t)h)) continue;
-    int32_t g = (int32_t)h;
-    long long d = 0;
-    do {
-      d++;
-      g = walk_next(hw, g, limit);
-      if (g < 0 || d > limit) { report(st, K_WALK, h / 3); g = (int32_t)h; break; }
-    } while (!is_ruler(bits, g));
-    rnext[h] = g;
-    rdist[h] = (int32_t)d;
+__device__ __forceinline__ void walk_ruler(const int32_t* __restrict__ hw, const RulerSet& rs, int32_t h,
+                                           long long limit, int32_t* __restrict__ rnext,
+                                           int32_t* __restrict__ rdist, DevStatus* st) {
+  int32_t g = h;
+  long long d = 0;
+  do {
+    d++;
+    g = walk_next(hw, g, limit);
+    if (g < 0 || d > limit) { report(st, K_WALK, h / 3); g = h; break; }
+  } while (!is_ruler(rs, g));
+  rnext[h] = g;
+  rdist[h] = (int32_t)d;
+}
+
+__global__ void __launch_bounds__(256) k_ruler_walk(const int32_t* __restrict__ hw, RulerSet rs, long long limit,
+                                                    int32_t* __restrict__ rnext, int32_t* __restrict__ rdist,
+                                                    DevStatus* st) {
+  for (int64_t h = rs.hb + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < rs.he;
+       h += (int64_t)gridDim.x * blockDim.x) {
+    if (!hw_front(hw[h]) || !is_ruler(rs, (int32_t)h)) continue;
+    walk_ruler(hw, rs, (int32_t)h, limit, rnext, rdist, st);
+  }
+}
+
+// partitioned runs: the start rulers that lie outside the own half-edge range
+__global__ void __launch_bounds__(256) k_ruler_walk_starts(const int32_t* __restrict__ hw, RulerSet rs,
+                                                           const int32_t* __restrict__ start,
+                                                           const int64_t* __restrict__ Pp, long long limit,
+                                                           int32_t* __restrict__ rnext, int32_t* __restrict__ rdist,
+                                                           DevStatus* st) {
+  const int64_t P = *Pp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t h = start[i];
+    if (h < 0 || (h >= rs.hb && h < rs.he)) continue;
+    walk_ruler(hw, rs, h, limit, rnext, rdist, st);
   }
 }
 
@@ -193,11 +224,17 @@ void launch_trav_start(const int32_t* hw, const int32_t* seeds, const int64_t* P
   note_launch(2);
 }
 
-void launch_ruler_walk(const int32_t* hw, const uint32_t* bits, int64_t T, int32_t* rnext, int32_t* rdist,
+void launch_ruler_walk(const int32_t* hw, const uint32_t* bits, int64_t T, int64_t t_begin, int64_t t_end,
+                       const int32_t* start, const int64_t* Pp, int64_t Pcap, int32_t* rnext, int32_t* rdist,
                        DevStatus* st, cudaStream_t s) {
   if (T <= 0) return;
-  k_ruler_walk<<<grid_for(3 * T, 256), 256, 0, s>>>(hw, bits, 3 * T, 3 * T + 3, rnext, rdist, st);
+  RulerSet rs{bits, (int32_t)(3 * t_begin), (int32_t)(3 * t_end)};
+  k_ruler_walk<<<grid_for(3 * (t_end - t_begin), 256), 256, 0, s>>>(hw, rs, 3 * T + 3, rnext, rdist, st);
   note_launch(1);
+  if (t_begin > 0 || t_end < T) {
+    k_ruler_walk_starts<<<grid_for(Pcap, 256), 256, 0, s>>>(hw, rs, start, Pp, 3 * T + 3, rnext, rdist, st);
+    note_launch(1);
+  }
 }
 
 void launch_chain_count(const int32_t* seeds, const int32_t* start, const int64_t* Pp, int64_t Pcap, int64_t T,

@@ -1,0 +1,169 @@
+"""Multi-GPU mesh -> polygons: replicated mesh, seed-partitioned.
+
+Every rank holds the whole (read-only) half-edge mesh on its own GPU and
+labels all of it -- a boundary walk may leave the rank's triangle range, and
+K0-K2 are streaming passes.  Rank r then traverses and repairs only the
+polygons whose seed triangle lies in its range
+
+    [r * T // G, (r + 1) * T // G)          (partition(T, G)[r])
+
+(tm_ctx_set_partition: seed selection, the sampled ruler walks, repair and
+the stitch are all restricted to that range).  Distinct polygons have
+disjoint interiors, so the ranks' frontier promotions never interact
+ and no label exchange is needed afterwards.
+
+The one exchange step is an all-gather of each rank's (polygon count, slot
+count) -- 16 bytes per rank, NCCL over NVLink on GPUs, gloo in the CPU tests.
+Its exclusive prefix gives every rank its global polygon / slot base; shifting
+the local CSR offsets by the slot base (tm_shift_offsets) stitches the global
+CSR, whose rank-ordered concatenation is exactly the single-GPU output
+(ascending seed order = the reference's raw order).  The CSR
+can stay sharded (ShardedCSR) or be gathered to one rank (gather_csr).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def partition(T: int, world: int) -> list[tuple[int, int]]:
+    """Consecutive seed-triangle ranges, one per rank, covering [0, T)."""
+    if world < 1:
+        raise ValueError("world size must be >= 1")
+    return [(r * T // world, (r + 1) * T // world) for r in range(world)]
+
+
+def exclusive_bases(counts) -> tuple[np.ndarray, np.ndarray]:
+    """counts[r] = (polygons, slots) of rank r -> (polygon base, slot base) per rank."""
+    c = np.asarray(counts, dtype=np.int64).reshape(-1, 2)
+    pb = np.concatenate([[0], np.cumsum(c[:, 0])[:-1]]).astype(np.int64)
+    sb = np.concatenate([[0], np.cumsum(c[:, 1])[:-1]]).astype(np.int64)
+    return pb, sb
+
+
+def exchange_counts(n_polys: int, n_slots: int, device, group=None) -> np.ndarray:
+    """All-gather (polygons, slots) of every rank: int64[world, 2] on every rank."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    if dist.get_backend(group) == "nccl":
+        device = torch.device("cuda", torch.cuda.current_device())
+    mine = torch.tensor([n_polys, n_slots], dtype=torch.int64, device=device)
+    allc = torch.empty(world * 2, dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(allc, mine, group=group)
+    return allc.view(world, 2).cpu().numpy()
+
+
+@dataclass
+class ShardedCSR:
+    """This rank's slice of the global polygon CSR.  offsets are GLOBAL slot
+    offsets (already shifted): polygon poly_base + i of the global mesh is
+    verts[offsets[i] - offsets[0] : offsets[i + 1] - offsets[0]]."""
+    offsets: object     # int64[P_r + 1] (device tensor)
+    verts: object       # int32[F_r] (device tensor)
+    poly_base: int
+    slot_base: int
+    counts: np.ndarray  # int64[world, 2]
+
+    @property
+    def n_polys(self) -> int:
+        return int(self.offsets.numel() - 1)
+
+
+def stitch(local_off, local_verts, n_polys: int, n_slots: int, group=None, shift=None) -> ShardedCSR:
+    """Exchange counts and place this rank's CSR at its global base.  `shift`
+    adds the slot base to the offsets in place (default: the C ABI kernel on
+    a CUDA tensor, a plain add on CPU tensors)."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    counts = exchange_counts(n_polys, n_slots, local_off.device if local_off.is_cuda else "cpu", group)
+    pb, sb = exclusive_bases(counts)
+    off = local_off[: n_polys + 1]
+    if shift is None:
+        shift = _shift_device if off.is_cuda else _shift_host
+    shift(off, n_polys, int(sb[rank]))
+    return ShardedCSR(off, local_verts[:n_slots], int(pb[rank]), int(sb[rank]), counts)
+
+
+def _shift_host(off, n_polys, delta):
+    off += delta
+
+
+def _shift_device(off, n_polys, delta):
+    from . import _capi
+    rc = _capi.lib().tm_shift_offsets(_capi.ptr(off), n_polys, delta, _capi.stream_ptr(off.device))
+    if rc != 0:
+        raise _capi.TermeshError(f"tm_shift_offsets failed with status {rc}")
+
+
+def gather_csr(shard: ShardedCSR, dst: int = 0, group=None):
+    """Global CSR (numpy offsets int64[P+1], verts int32[F]) on rank `dst`,
+    None elsewhere.  Padded all-gather, so it works on NCCL and gloo alike."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    counts = shard.counts
+    maxp, maxf = int(counts[:, 0].max()), int(counts[:, 1].max())
+    dev = shard.offsets.device
+    po = torch.zeros(maxp + 1, dtype=torch.int64, device=dev)
+    pv = torch.zeros(max(maxf, 1), dtype=torch.int32, device=dev)
+    po[: shard.n_polys + 1] = shard.offsets
+    pv[: shard.verts.numel()] = shard.verts
+    go = [torch.empty_like(po) for _ in range(world)]
+    gv = [torch.empty_like(pv) for _ in range(world)]
+    dist.all_gather(go, po, group=group)
+    dist.all_gather(gv, pv, group=group)
+    if rank != dst:
+        return None
+    offs, verts = [], []
+    for r in range(world):
+        p, f = int(counts[r, 0]), int(counts[r, 1])
+        offs.append(go[r][:p].cpu().numpy())
+        verts.append(gv[r][:f].cpu().numpy())
+    total = int(counts[:, 1].sum())
+    return (np.concatenate(offs + [np.array([total], dtype=np.int64)]).astype(np.int64),
+            np.concatenate(verts).astype(np.int32) if verts else np.zeros(0, np.int32))
+
+
+def run_partition(xy, tri, n: int, T: int, t_begin: int, t_end: int, ctx=None, off=None, verts=None):
+    """Device path of one rank: the whole pipeline restricted to the seeds in
+    [t_begin, t_end).  xy float64 / tri int64 device tensors.  Returns
+    (offsets, verts, n_polys, n_slots, stats) with LOCAL offsets (from 0)."""
+    import torch
+    from . import _capi
+    dev = xy.device
+    ctx = ctx or _capi.context(dev)
+    off = off if off is not None else torch.empty(T + 1, dtype=torch.int64, device=dev)
+    verts = verts if verts is not None else torch.empty(max(3 * T, 1), dtype=torch.int32, device=dev)
+    L = _capi.lib()
+    ctx.check(L.tm_ctx_set_partition(ctx.ptr, t_begin, t_end))
+    npol, nsl = ctypes.c_int64(), ctypes.c_int64()
+    stats = (ctypes.c_int64 * 8)()
+    try:
+        rc = L.tm_mesh_to_polygons(ctx.ptr, _capi.ptr(xy), n, _capi.ptr(tri), 64 if tri.dtype == torch.int64 else 32,
+                                   T, 0, _capi.ptr(off), _capi.ptr(verts), T, 3 * T, ctypes.byref(npol),
+                                   ctypes.byref(nsl), stats, _capi.stream_ptr(dev))
+        ctx.check(rc, "traversal")
+    finally:
+        L.tm_ctx_set_partition(ctx.ptr, 0, -1)
+    return off, verts, npol.value, nsl.value, dict(zip(_capi.STAT_NAMES, list(stats)))
+
+
+def execute_distributed(tri, group=None, gather: bool = True):
+    """Drop-in multi-GPU execute: every rank passes the same Triangulation; the
+    global final CSR comes back on rank 0 (gather=True) or as shards."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    n, T = tri.n_vertices, tri.n_triangles
+    dev = torch.device("cuda", torch.cuda.current_device())
+    xy = torch.from_numpy(np.ascontiguousarray(tri.vertices)).to(dev)
+    tr = torch.from_numpy(np.ascontiguousarray(tri.triangles)).to(dev)
+    b, e = partition(T, world)[rank]
+    off, verts, p, f, stats = run_partition(xy, tr, n, T, b, e)
+    shard = stitch(off, verts, p, f, group)
+    if not gather:
+        return shard, stats
+    return gather_csr(shard, 0, group), stats

@@ -1,0 +1,107 @@
+"""Multi-GPU path: replicated mesh, seed-partitioned ranks,
+one all-gather of per-rank counts to stitch the global CSR.
+
+CPU (gloo, world_size 2 and 3): the product's partition / exchange / stitch /
+gather code (paper_2204_05438_b200.distributed) with each rank's local result
+produced by the CPU oracle restricted to the rank's seed range -- the
+concatenation must equal the reference's single-process output byte for byte.
+GPU: the same partitions run through the C ABI (tm_ctx_set_partition) as
+logical ranks on one device (the G-way partitioned path on one
+GPU), stitched with the same bases."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import load_case
+from paper_2204_05438_b200 import distributed as D
+
+CASES = ("aniso2k_s1", "clust5k_s0", "sun", "u1k_unit")
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def oracle_partition(tri, b, e):
+    """The reference algorithm on the polygons whose seed lies in [b, e)."""
+    lab = oracle.label_all(tri)
+    off, v = oracle.build_polygon_mesh(tri, lab)
+    seeds = np.flatnonzero(lab.seed)
+    i0, i1 = np.searchsorted(seeds, b), np.searchsorted(seeds, e)
+    sub = (off[i0:i1 + 1] - off[i0], v[off[i0]:off[i1]])
+    (fo, fv), _ = oracle.repair_all(tri, lab, sub)
+    return fo, fv
+
+
+def test_partition_covers_range():
+    for T in (0, 1, 7, 1000, 1999963):
+        for G in (1, 2, 3, 8):
+            parts = D.partition(T, G)
+            assert parts[0][0] == 0 and parts[-1][1] == T
+            assert all(parts[k][1] == parts[k + 1][0] for k in range(G - 1))
+            assert max(e - b for b, e in parts) - min(e - b for b, e in parts) <= 1
+
+
+def test_exclusive_bases():
+    pb, sb = D.exclusive_bases([[3, 10], [0, 0], [2, 7]])
+    assert pb.tolist() == [0, 3, 3] and sb.tolist() == [0, 10, 10]
+
+
+def _worker(rank, world, port, names, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        for name in names:
+            tri, g = load_case(name)
+            b, e = D.partition(tri.n_triangles, world)[rank]
+            fo, fv = oracle_partition(tri, b, e)
+            p, f = fo.size - 1, int(fo[-1])
+            shard = D.stitch(torch.from_numpy(fo.copy()), torch.from_numpy(fv.astype(np.int32)), p, f)
+            out = D.gather_csr(shard, 0)
+            if rank == 0:
+                ok = np.array_equal(out[0], g["final_off"]) and np.array_equal(out[1], g["final_verts"])
+                q.put((name, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_stitch_gloo(world):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    mp.start_processes(_worker, args=(world, _free_port(), CASES, q), nprocs=world, join=True,
+                       start_method="spawn")
+    res = [q.get() for _ in CASES]
+    assert all(ok for _, ok in res), res
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("name", CASES)
+def test_partitioned_device_path(cuda, name, world):
+    import torch
+    tri, g = load_case(name)
+    n, T = tri.n_vertices, tri.n_triangles
+    xy = torch.from_numpy(tri.vertices).to(cuda)
+    tr = torch.from_numpy(tri.triangles).to(cuda)
+    locs = []
+    for b, e in D.partition(T, world):
+        off, v, p, f, _ = D.run_partition(xy, tr, n, T, b, e)
+        locs.append((off[: p + 1].clone(), v[:f].clone(), p, f))
+    pb, sb = D.exclusive_bases([[p, f] for _, _, p, f in locs])
+    for (off, _, p, _), base in zip(locs, sb):
+        D._shift_device(off, p, int(base))
+    torch.cuda.synchronize()
+    got_off = np.concatenate([o[:-1].cpu().numpy() for o, _, _, _ in locs] + [np.array([int(sb[-1]) + locs[-1][3]])])
+    got_v = np.concatenate([v.cpu().numpy() for _, v, _, _ in locs])
+    assert np.array_equal(got_off, g["final_off"]) and np.array_equal(got_v, g["final_verts"])
