@@ -45,9 +45,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    "u1m": dict(n=1_000_000, desc="1M uniform random points in the unit square, scipy Delaunay (seed 0)"),
-    "u10m": dict(n=10_000_000, desc="10M uniform random points in the unit square, scipy Delaunay (seed 0)"),
-    "u100k": dict(n=100_000, desc="100k uniform random points in the unit square, scipy Delaunay (seed 0)"),
+    "u1m": dict(n=1_000_000, gen="uniform", desc="1M uniform random points in the unit square, scipy Delaunay (seed 0)"),
+    "u10m": dict(n=10_000_000, gen="uniform", desc="10M uniform random points in the unit square, scipy Delaunay (seed 0)"),
+    "u100k": dict(n=100_000, gen="uniform", desc="100k uniform random points in the unit square, scipy Delaunay (seed 0)"),
+    "c1m": dict(n=1_000_000, gen="clustered",
+                desc="1M points in 64 Gaussian clusters (sigma 0.002) in the unit square, scipy Delaunay (seed 0)"),
+    "c10m": dict(n=10_000_000, gen="clustered",
+                 desc="10M points in 64 Gaussian clusters (sigma 0.002) in the unit square, scipy Delaunay (seed 0)"),
 }
 METRIC = "triangles/sec end-to-end mesh->polygons"
 UNIT = "triangles/s"
@@ -55,8 +59,10 @@ UNIT = "triangles/s"
 
 def load_mesh(workload, seed):
     from paper_2204_05438_b200 import io_formats as io
-    n = WORKLOADS[workload]["n"]
-    return io.cached(f"{workload}_s{seed}_unit", lambda: io.generate_random_delaunay(n, (0.0, 0.0, 1.0, 1.0), seed))
+    w = WORKLOADS[workload]
+    if w["gen"] == "clustered":
+        return io.cached(f"{workload}_s{seed}_clustered", lambda: io.generate_clustered_delaunay(w["n"], seed=seed))
+    return io.cached(f"{workload}_s{seed}_unit", lambda: io.generate_random_delaunay(w["n"], (0.0, 0.0, 1.0, 1.0), seed))
 
 
 def measured_peak():
@@ -158,7 +164,7 @@ def run_gpu(args, rank, world, local_rank):
     stream = torch.cuda.current_stream(dev)
     sp = ctypes.c_void_p(stream.cuda_stream)
     npol, nsl = ctypes.c_int64(), ctypes.c_int64()
-    stats = (ctypes.c_int64 * 8)()
+    stats = (ctypes.c_int64 * _capi.NUM_STATS)()
 
     ctx.check(L.tm_ctx_set_partition(ctx.ptr, t_begin, t_end))
 
@@ -167,7 +173,7 @@ def run_gpu(args, rank, world, local_rank):
                                    _capi.ptr(verts), T, 3 * T, ctypes.byref(npol), ctypes.byref(nsl), stats, sp)
         ctx.check(rc)
         if world > 1:  # the exchange step: all-gather counts (NCCL), shift to the global slot base
-            D.stitch(off, verts, npol.value, nsl.value)
+            D.stitch(off, verts, npol.value, nsl.value, pinch=(stats[8], stats[9]))
 
     for _ in range(args.warmup):
         step()
@@ -248,7 +254,7 @@ def run_gpu(args, rank, world, local_rank):
                                         _capi.ptr(h_v), T, 3 * T, ctypes.byref(npol), ctypes.byref(nsl), stats)
         ctx.check(rc)
         if world > 1:
-            D.stitch(h_off, h_v, npol.value, nsl.value)
+            D.stitch(h_off, h_v, npol.value, nsl.value, pinch=(stats[8], stats[9]))
 
     for _ in range(args.warmup):
         e2e_step()

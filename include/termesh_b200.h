@@ -79,7 +79,14 @@ extern "C" {
 #define TM_STAT_TIP_SPLITS 5
 #define TM_STAT_PINCH_SPLITS 6
 #define TM_STAT_WORK_ITEMS 7
-#define TM_NUM_STATS 8
+/* the pinch pass's round guard (reparation.py:322) is GLOBAL: extra visits of
+ * the tip-phase output + 1.  A seed partition runs with its own share
+ * (PINCH_EXTRA + 1) and counts the items the guard cut off with pinched
+ * polygons left (PINCH_TRUNCATED); the ranks' results equal the single run
+ * unless a rank truncated and the global guard is larger. */
+#define TM_STAT_PINCH_EXTRA 8
+#define TM_STAT_PINCH_TRUNCATED 9
+#define TM_NUM_STATS 10
 
 typedef struct tm_ctx tm_ctx;
 

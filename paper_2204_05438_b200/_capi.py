@@ -16,12 +16,12 @@ LIB_PATH = os.path.join(_HERE, "libtermesh_b200.so")
 
 TM_OK, TM_ERR_STRUCTURAL, TM_ERR_VALIDATION, TM_ERR_CAPACITY, TM_ERR_CUDA, TM_ERR_ARGUMENT = range(6)
 NUM_KINDS = 16
-NUM_STATS = 8
+NUM_STATS = 10
 KIND_NAMES = ("index_range", "orientation", "degenerate", "duplicate", "reciprocity", "edge_count",
               "trivertex", "neighbors", "walk", "no_frontier", "no_converge", "split_law", "pool",
               "barrier", "no_internal", "structural")
 STAT_NAMES = ("rounds", "splits", "initial_tips", "unrepaired", "nonsimple", "tip_splits",
-              "pinch_splits", "work_items")
+              "pinch_splits", "work_items", "pinch_extra", "pinch_truncated")
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

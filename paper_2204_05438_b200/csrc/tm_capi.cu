@@ -463,7 +463,8 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
   {
     SegTimer t_(ctx, S_STITCH, s);
     launch_out_counts(d_off_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->item_n.as<int32_t>(),
-                      ctx->item_slots.as<int64_t>(), ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), s);
+                      ctx->item_slots.as<int64_t>(), ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), nullptr,
+                      &dc->st, s);
     launch_scan_dev(ctx->cnt.as<int64_t>(), ctx->pbase.as<int64_t>(), Pp, Tn, tiles, s);
     launch_scan_dev(ctx->slotsz.as<int64_t>(), ctx->sbase.as<int64_t>(), Pp, Tn, tiles, s);
     launch_finalize(Pp, ctx->pbase.as<int64_t>(), ctx->sbase.as<int64_t>(), d_off_out, &dc->p_out, &dc->f_out, s);
@@ -495,6 +496,8 @@ static void fill_stats(const Counters& h, int64_t* stats) {
   stats[TM_STAT_TIP_SPLITS] = (int64_t)h.stats[1];
   stats[TM_STAT_PINCH_SPLITS] = (int64_t)h.stats[4];
   stats[TM_STAT_WORK_ITEMS] = (int64_t)h.n_items;
+  stats[TM_STAT_PINCH_EXTRA] = (int64_t)h.stats[5];
+  stats[TM_STAT_PINCH_TRUNCATED] = (int64_t)h.stats[7];
 }
 
 // Pool overflow: restore the pre-repair frontier bits (restore()), grow the

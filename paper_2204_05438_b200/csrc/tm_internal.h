@@ -92,7 +92,7 @@ void launch_repair_tips(const RepairArgs& a, int mode, cudaStream_t s);
 void launch_repair_pinch(const RepairArgs& a, cudaStream_t s);
 void launch_out_counts(const int64_t* off, const int64_t* Pp, int64_t Pcap, const int32_t* item_of,
                        const int32_t* item_n, const int64_t* item_slots, int64_t* cnt, int64_t* slots,
-                       cudaStream_t s);
+                       const unsigned long long* stats, DevStatus* st, cudaStream_t s);
 void launch_stitch(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, const int32_t* item_of,
                    const int32_t* items, const unsigned int* n_items, const int64_t* item_list, const int32_t* item_n,
                    const int32_t* pool, const int64_t* pbase, const int64_t* sbase, int64_t* off_out, int32_t* v_out,

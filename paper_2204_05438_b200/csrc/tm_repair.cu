@@ -651,6 +651,412 @@ __device__ bool warp_split_tip(const RepairCtx& c, const int32_t* X, int L, int3
   return warp_split_arcs(c, X, L, pos, s, poly, lane, alloc, A_out, la_out, B_out, lb_out);
 }
 
+// Duplicate scan of s[0..n) (traversal.py:140-147 and the first-repeat search
+// of reparation.py:184-189), one warp: a value -> first position hash map in
+// pool scratch, so long pieces cost O(n), not O(n^2).  Returns the extra
+// visits (n - distinct); *p1/*p2 = the first repeated position p2 and the
+// first occurrence p1 of its value (-1 when none).
+__device__ int warp_dup_scan(const RepairCtx& c, const int32_t* s, int n, int lane, int* p1, int* p2) {
+  if (n <= 64) {
+    int extra = 0, q2 = -1, q1 = -1;
+    for (int pb = 0; pb < n; pb += 32) {
+      int p = pb + lane;
+      int32_t x = p < n ? s[p] : 0;
+      int first = -1;
+      for (int q = 0; q < n && p < n; q++)
+        if (s[q] == x) { first = q; break; }
+      bool dup = p < n && first < p;
+      unsigned m = __ballot_sync(kFull, dup);
+      extra += __popc(m);
+      if (m && q2 < 0) {
+        int l = __ffs(m) - 1;
+        q2 = pb + l;
+        q1 = __shfl_sync(kFull, first, l);
+      }
+    }
+    if (p1) *p1 = q1;
+    if (p2) *p2 = q2;
+    return extra;
+  }
+  int cap = 64;
+  while (cap < 2 * n) cap <<= 1;
+  long long o = 0;
+  if (lane == 0) {
+    o = palloc(c, 2 * (long long)cap + 1);
+    if (o >= 0) o = (o + 1) & ~1LL;  // int2 alignment
+  }
+  o = __shfl_sync(kFull, o, 0);
+  if (o < 0) {  // pool exhausted: quadratic fallback
+    if (lane == 0) report(c.st, K_POOL, -1);
+    if (p1) *p1 = -1;
+    if (p2) *p2 = -1;
+    return warp_extra_visits(s, n, lane);
+  }
+  int2* tab = reinterpret_cast<int2*>(c.pool + o);
+  for (int k = lane; k < cap; k += 32) tab[k] = make_int2(-1, 0x7FFFFFFF);
+  __syncwarp();
+  for (int p = lane; p < n; p += 32) {
+    int32_t x = s[p];
+    uint32_t slot = ((uint32_t)x * 0x9E3779B1u) & (cap - 1);
+    for (;;) {
+      int prev = atomicCAS(&tab[slot].x, -1, x);
+      if (prev == -1 || prev == x) { atomicMin(&tab[slot].y, p); break; }
+      slot = (slot + 1) & (cap - 1);
+    }
+  }
+  __syncwarp();
+  __threadfence_block();
+  int extra = 0, q2 = -1, q1 = -1;
+  for (int pb = 0; pb < n; pb += 32) {
+    int p = pb + lane, first = -1;
+    if (p < n) {
+      int32_t x = s[p];
+      uint32_t slot = ((uint32_t)x * 0x9E3779B1u) & (cap - 1);
+      for (;;) {
+        int2 e = __ldcg(&tab[slot]);
+        if (e.x == x) { first = e.y; break; }
+        slot = (slot + 1) & (cap - 1);
+      }
+    }
+    bool dup = p < n && first < p;
+    unsigned m = __ballot_sync(kFull, dup);
+    extra += __popc(m);
+    if (m && q2 < 0) {
+      int l = __ffs(m) - 1;
+      q2 = pb + l;
+      q1 = __shfl_sync(kFull, first, l);
+    }
+  }
+  if (p1) *p1 = q1;
+  if (p2) *p2 = q2;
+  return extra;
+}
+
+// ------------------------------------------------------------ pinch phase
+// reparation.py:315-340 per item, one warp, after every item's tip phase:
+// the round guard is GLOBAL (extra visits of the whole tip-phase output + 1,
+// reparation.py:322) and does bind on small meshes.  Rounds follow the
+// reference: every eligible piece (repeated vertex, no tip, not failed
+// before) gets one candidate sweep per round; the loop ends when a round
+// splits nothing or the guard is reached.  Items cut off by the guard with
+// pinched pieces left are counted (TM_STAT_PINCH_TRUNCATED) so a seed-
+// partitioned run can check that its local guard equals the global one.
+
+// Trial split at candidate g with strict=False (reparation.py:326-332):
+// promote, re-walk both sides (lanes 0 and 1 at once) into fresh pool slots,
+// keep iff |pa| + |pb| == L + 2, else revert.  Warp-uniform result: 1 split,
+// 0 reverted, -1 error.
+__device__ int warp_try_pinch(const RepairCtx& c, int32_t g, int L, int32_t poly, int lane, int32_t** A, int* la,
+                              int32_t** B, int* lb) {
+  int32_t w = hw_twin(c.hw[g]);
+  if (w < 0) {
+    if (lane == 0) report(c.st, K_STRUCT, poly);
+    return -1;
+  }
+  long long o = 0;
+  if (lane == 0) {
+    o = palloc(c, 2 * (long long)L + 4);
+    if (o >= 0) promote(c, g, w);
+  }
+  o = __shfl_sync(kFull, o, 0);
+  if (o < 0) {
+    if (lane == 0) report(c.st, K_POOL, poly);
+    return -1;
+  }
+  __syncwarp();
+  int cnt = 0, err = 0, over = 0;
+  if (lane < 2) {
+    int32_t* dst = c.pool + o + (lane ? L + 2 : 0);
+    const int32_t h0 = min_frontier_slot(c.hw, lane ? w / 3 : g / 3);
+    const long long limit = 3 * c.T + 3;
+    int32_t h = h0;
+    if (h0 < 0) err = 1;
+    else
+      do {
+        if (cnt > L + 1) { over = 1; break; }
+        dst[cnt++] = he_origin(c.tri, h);
+        h = walk_next(c.hw, h, limit);
+        if (h < 0) { err = 1; break; }
+      } while (h != h0);
+  }
+  const int ca = __shfl_sync(kFull, cnt, 0), cb = __shfl_sync(kFull, cnt, 1);
+  err = __shfl_sync(kFull, err, 0) | __shfl_sync(kFull, err, 1);
+  over = __shfl_sync(kFull, over, 0) | __shfl_sync(kFull, over, 1);
+  if (err) {
+    if (lane == 0) report(c.st, K_STRUCT, poly);
+    return -1;
+  }
+  if (over || ca + cb != L + 2) {
+    if (lane == 0) demote(c, g, w);
+    __syncwarp();
+    return 0;
+  }
+  *A = c.pool + o;
+  *la = ca;
+  *B = c.pool + o + L + 2;
+  *lb = cb;
+  return 1;
+}
+
+// incoming boundary vertex of the wedge around origin(g) that holds g: rotate
+// CCW from g until the crossed edge prev(.) is frontier (pre-promotion flags)
+__device__ __forceinline__ int32_t wedge_in_vertex(const RepairCtx& c, int32_t g) {
+  long long guard = 3 * c.T + 3;
+  for (long long k = 0; k < guard; k++) {
+    int32_t p = he_prev(g);
+    int32_t w = c.hw[p];
+    if (hw_front(w)) return he_origin(c.tri, p);
+    g = hw_twin(w);
+    if (g < 0) return -1;
+  }
+  return -1;
+}
+
+// Arc trial of candidate g = x -> y (strict=False).  With the pre-promotion
+// frontier, the visit of x whose wedge holds g and the visit of y whose wedge
+// holds twin(g) cut X into exactly the two cycles the re-walks would trace
+// (as for tip splits), so |pa| + |pb| = L + 2 holds by
+// construction; when y is not on X the promoted edge dangles inside the
+// region, both re-walks trace one cycle of length L + 2 and the law fails.
+// Anything else (a wedge or rotation search that fails) takes the re-walk
+// trial.  Warp-uniform: 1 split, 0 reverted / not split, -1 error.
+__device__ int warp_try_pinch_arc(const RepairCtx& c, int32_t g, const int32_t* X, int L, int32_t poly, int lane,
+                                  int32_t** A, int* la_out, int32_t** B, int* lb_out) {
+  int32_t w = -1, x = -1, y = -1, ax = -1, ay = -1;
+  if (lane == 0) {
+    w = hw_twin(c.hw[g]);
+    x = he_origin(c.tri, g);
+    y = he_target(c.tri, g);
+    if (w >= 0) {
+      ax = wedge_in_vertex(c, g);
+      ay = wedge_in_vertex(c, w);
+    }
+  }
+  w = __shfl_sync(kFull, w, 0);
+  x = __shfl_sync(kFull, x, 0);
+  y = __shfl_sync(kFull, y, 0);
+  ax = __shfl_sync(kFull, ax, 0);
+  ay = __shfl_sync(kFull, ay, 0);
+  if (w < 0) {
+    if (lane == 0) report(c.st, K_STRUCT, poly);
+    return -1;
+  }
+  if (warp_find_first(L, lane, [&](int q) { return X[q] == y; }) < 0) return 0;  // y interior: no split
+  const int pos = ax < 0 ? -1 : warp_find_first(L, lane, [&](int q) { return X[q] == x && X[q == 0 ? L - 1 : q - 1] == ax; });
+  const int j = ay < 0 ? -1 : warp_find_first(L, lane, [&](int q) { return X[q] == y && X[q == 0 ? L - 1 : q - 1] == ay; });
+  if (pos < 0 || j < 0) return warp_try_pinch(c, g, L, poly, lane, A, la_out, B, lb_out);
+  int32_t oa = 0, ga = 0, ob = 0, gb = 0;
+  if (lane == 0) {
+    promote(c, g, w);
+    int32_t ha = min_frontier_slot(c.hw, g / 3), hb = min_frontier_slot(c.hw, w / 3);
+    oa = he_origin(c.tri, ha); ga = he_target(c.tri, ha);
+    ob = he_origin(c.tri, hb); gb = he_target(c.tri, hb);
+  }
+  oa = __shfl_sync(kFull, oa, 0); ga = __shfl_sync(kFull, ga, 0);
+  ob = __shfl_sync(kFull, ob, 0); gb = __shfl_sync(kFull, gb, 0);
+  const int la = wrap_idx(pos - j, L) + 1, lb = wrap_idx(j - pos, L) + 1;
+  // pa = [x, X[j .. pos-1]], pb = [X[pos .. j-1], y]
+  auto A_at = [&](int k) { return k == 0 ? x : X[wrap_idx(j + k - 1, L)]; };
+  auto B_at = [&](int k) { return k == lb - 1 ? y : X[wrap_idx(pos + k, L)]; };
+  const int ka = warp_find_first(la, lane, [&](int k) { return A_at(k) == oa && A_at(k + 1 == la ? 0 : k + 1) == ga; });
+  const int kb = warp_find_first(lb, lane, [&](int k) { return B_at(k) == ob && B_at(k + 1 == lb ? 0 : k + 1) == gb; });
+  if (ka < 0 || kb < 0) {
+    if (lane == 0) demote(c, g, w);
+    __syncwarp();
+    return warp_try_pinch(c, g, L, poly, lane, A, la_out, B, lb_out);
+  }
+  long long o = 0;
+  if (lane == 0) o = palloc(c, (long long)la + lb);
+  o = __shfl_sync(kFull, o, 0);
+  if (o < 0) {
+    if (lane == 0) report(c.st, K_POOL, poly);
+    return -1;
+  }
+  int32_t* pa = c.pool + o;
+  int32_t* pb = pa + la;
+  warp_copy(pa, la, lane, [&](int k) { return A_at(wrap_idx(ka + k, la)); });
+  warp_copy(pb, lb, lane, [&](int k) { return B_at(wrap_idx(kb + k, lb)); });
+  __syncwarp();
+  *A = pa; *la_out = la; *B = pb; *lb_out = lb;
+  return 1;
+}
+
+// _pinch_candidates (reparation.py:169-205) for one piece, candidates in the
+// reference order, each trial-split until one keeps.  Every lane runs the
+// (identical) candidate enumeration so the trials stay warp-convergent.
+__device__ int warp_pinch_split(const RepairCtx& c, const int32_t* X, int L, int32_t poly, int lane, int32_t** A,
+                                int* la, int32_t** B, int* lb) {
+  int p1 = -1, p2 = -1;  // first repeated vertex (reparation.py:184-189)
+  warp_dup_scan(c, X, L, lane, &p1, &p2);
+  if (p2 < 0) return 0;
+  const int32_t v = X[p2];
+  const int guard = (int)(3 * c.T + 3 < (1LL << 30) ? 3 * c.T + 3 : (1LL << 30));
+  int32_t t0 = c.tv[v];
+  int32_t g0 = t0 < 0 ? -1 : he_with_origin(c.tri, t0, v);
+  if (g0 < 0) {
+    if (lane == 0) report(c.st, K_STRUCT, poly);
+    return -1;
+  }
+  int deg = 0;
+  {
+    int32_t g = g0;
+    do {
+      deg++;
+      g = fan_step(c.hw, g, guard);
+      if (g < 0 || deg > guard) {
+        if (lane == 0) report(c.st, K_STRUCT, poly);
+        return -1;
+      }
+    } while (g != g0);
+  }
+  const int poss[2] = {p2, p1};
+  for (int q = 0; q < 2; q++) {  // wedge internal edges at the second, then the first visit
+    int32_t outv = X[(poss[q] + 1) % L];
+    int32_t g = g0, gout = -1;
+    for (int st = 0; st < deg; st++) {
+      if (hw_front(c.hw[g]) && he_target(c.tri, g) == outv) { gout = g; break; }
+      g = fan_step(c.hw, g, guard);
+    }
+    if (gout < 0) {
+      if (lane == 0) report(c.st, K_STRUCT, poly);
+      return -1;
+    }
+    int k = 0;
+    g = fan_step(c.hw, gout, guard);
+    for (int st = 1; st < deg; st++) {
+      if (hw_front(c.hw[g])) break;
+      k++;
+      g = fan_step(c.hw, g, guard);
+    }
+    if (k == 0) continue;
+    const int mid = (k - 1) / 2;
+    for (int ord = -1; ord < k; ord++) {  // middle edge first, then the rest in order
+      int idx = ord < 0 ? mid : ord;
+      if (ord == mid) continue;
+      int32_t cand = gout;
+      for (int st = 0; st <= idx; st++) cand = fan_step(c.hw, cand, guard);
+      int r = warp_try_pinch_arc(c, cand, X, L, poly, lane, A, la, B, lb);
+      if (r != 0) return r;
+    }
+  }
+  for (int idx = p1 + 1; idx < p2; idx++) {  // internal fan edges of the inner-loop vertices
+    int32_t x = X[idx];
+    int32_t tx = c.tv[x];
+    int32_t gx0 = tx < 0 ? -1 : he_with_origin(c.tri, tx, x);
+    if (gx0 < 0) {
+      if (lane == 0) report(c.st, K_STRUCT, poly);
+      return -1;
+    }
+    int32_t g = gx0;
+    int cnt = 0;
+    do {
+      if (!hw_front(c.hw[g])) {
+        int r = warp_try_pinch_arc(c, g, X, L, poly, lane, A, la, B, lb);
+        if (r != 0) return r;
+      }
+      g = fan_step(c.hw, g, guard);
+      if (g < 0 || ++cnt > guard) {
+        if (lane == 0) report(c.st, K_STRUCT, poly);
+        return -1;
+      }
+    } while (g != gx0);
+  }
+  return 0;
+}
+
+// Pinch rounds of item w (record list in the pool) and its output totals.
+__device__ void warp_finish_pinch(const RepairCtx& c, int64_t w, int32_t poly, long long list, int n, int lane,
+                                  int64_t* item_list, int32_t* item_n, int64_t* item_slots,
+                                  unsigned long long* stats, long long guard) {
+  const int n0 = n;
+  bool ok = true, truncated = false;
+  for (long long r = 0; ok; r++) {
+    int elig = 0;
+    for (int k0 = 0; k0 < n; k0 += 32) {
+      int k = k0 + lane;
+      bool e = false;
+      if (k < n) {
+        uint32_t rl = (uint32_t)c.pool[list + 2 * k + 1];
+        e = (rl & F_REP) && !(rl & F_TIP) && !(rl & F_FAIL);
+      }
+      elig += __popc(__ballot_sync(kFull, e));
+    }
+    if (elig == 0) break;
+    if (r >= guard) {  // the reference's loop ends here with pinched polygons left
+      truncated = true;
+      break;
+    }
+    long long nl = 0;
+    if (lane == 0) nl = palloc(c, 2 * (long long)(n + elig));
+    nl = __shfl_sync(kFull, nl, 0);
+    if (nl < 0) {
+      if (lane == 0) report(c.st, K_POOL, poly);
+      ok = false;
+      break;
+    }
+    int m = 0, did = 0;
+    for (int k = 0; k < n && ok; k++) {
+      uint32_t ro = (uint32_t)c.pool[list + 2 * k], rl = (uint32_t)c.pool[list + 2 * k + 1];
+      if ((rl & F_REP) && !(rl & F_TIP) && !(rl & F_FAIL)) {
+        int32_t *A, *B;
+        int al, bl;
+        int res = warp_pinch_split(c, c.pool + ro, (int)(rl & LEN_MASK), poly, lane, &A, &al, &B, &bl);
+        if (res < 0) { ok = false; break; }
+        if (res == 1) {
+          uint32_t fa = warp_tip_flag(A, al, lane) | (warp_dup_scan(c, A, al, lane, nullptr, nullptr) > 0 ? F_REP : 0u);
+          uint32_t fb = warp_tip_flag(B, bl, lane) | (warp_dup_scan(c, B, bl, lane, nullptr, nullptr) > 0 ? F_REP : 0u);
+          if (lane == 0) {
+            c.pool[nl + 2 * m] = (int32_t)(A - c.pool);
+            c.pool[nl + 2 * m + 1] = (int32_t)((uint32_t)al | fa);
+            c.pool[nl + 2 * m + 2] = (int32_t)(B - c.pool);
+            c.pool[nl + 2 * m + 3] = (int32_t)((uint32_t)bl | fb);
+          }
+          m += 2;
+          did++;
+          continue;
+        }
+        rl |= F_FAIL;  // a failed pinch fails identically in every later round
+      }
+      if (lane == 0) {
+        c.pool[nl + 2 * m] = (int32_t)ro;
+        c.pool[nl + 2 * m + 1] = (int32_t)rl;
+      }
+      m++;
+    }
+    __syncwarp();
+    if (!ok) break;
+    list = nl;
+    n = m;
+    if (did == 0) break;
+  }
+  if (!ok) {
+    if (lane == 0) { item_list[w] = -1; item_n[w] = 0; item_slots[w] = 0; }
+    return;
+  }
+  long long slots = 0;
+  unsigned long long unrep = 0;
+  for (int k0 = 0; k0 < n; k0 += 32) {
+    int k = k0 + lane;
+    if (k < n) {
+      uint32_t rl = (uint32_t)c.pool[list + 2 * k + 1];
+      slots += rl & LEN_MASK;
+      unrep += (rl & F_REP) ? 1 : 0;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    slots += __shfl_xor_sync(kFull, slots, o);
+    unrep += __shfl_xor_sync(kFull, unrep, o);
+  }
+  if (lane == 0) {
+    item_list[w] = list;
+    item_n[w] = n;
+    item_slots[w] = slots;
+    if (unrep) atomicAdd(stats + 3, unrep);
+    if (n != n0) atomicAdd(stats + 4, (unsigned long long)(n - n0));
+    if (truncated) atomicAdd(stats + 7, 1ull);
+  }
+}
+
 // ------------------------------------------------------------ tip phase, global pool
 // Item states (item_state[w]): 0 = not started, 1 = finished by the shared-
 // memory kernel, 2 = resume from item_list/item_n/item_depth in the pool.
@@ -661,7 +1067,7 @@ __device__ void finish_item(const RepairCtx& c, int64_t w, long long list, int n
   unsigned long long ex_sum = 0;
   for (int r = 0; r < n; r++) {
     uint32_t ro = (uint32_t)c.pool[list + 2 * r], rl = (uint32_t)c.pool[list + 2 * r + 1];
-    int ex = warp_extra_visits(c.pool + ro, (int)(rl & LEN_MASK), lane);
+    int ex = warp_dup_scan(c, c.pool + ro, (int)(rl & LEN_MASK), lane, nullptr, nullptr);
     if (ex > 0 && lane == 0) c.pool[list + 2 * r + 1] = (int32_t)(rl | F_REP);
     ex_sum += ex;
   }
@@ -685,6 +1091,7 @@ __global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, con
                                                                 int32_t* __restrict__ item_n,
                                                                 const int32_t* __restrict__ item_state,
                                                                 const int32_t* __restrict__ item_depth,
+                                                                int64_t* __restrict__ item_slots,
                                                                 unsigned long long* stats, LongQueue q, int mode) {
   __shared__ int32_t s_fan[kTipWarps][kFanCap];
   __shared__ int32_t s_back[kTipWarps][kFanCap];
@@ -725,7 +1132,7 @@ __global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, con
     } else {
       int32_t* P0 = alloc(L + 2);
       if (P0 == nullptr) {
-        if (lane == 0) { report(c.st, K_POOL, i); item_list[w] = -1; item_n[w] = 0; }
+        if (lane == 0) { report(c.st, K_POOL, i); item_list[w] = -1; item_n[w] = 0; item_slots[w] = 0; }
         continue;
       }
       warp_copy(P0, L, lane, [&](int k) { return v[b + k]; });
@@ -789,7 +1196,7 @@ __global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, con
       ntips = nt;
     }
     if (bad) {
-      if (lane == 0) { item_list[w] = -1; item_n[w] = 0; }
+      if (lane == 0) { item_list[w] = -1; item_n[w] = 0; item_slots[w] = 0; }
       continue;
     }
     finish_item(c, w, list, n, depth, splits, lane, item_list, item_n, stats);
@@ -1119,6 +1526,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
                                                                     int32_t* __restrict__ item_n,
                                                                     int32_t* __restrict__ item_state,
                                                                     int32_t* __restrict__ item_depth,
+                                                                    int64_t* __restrict__ item_slots,
                                                                     unsigned long long* stats, LongQueue q,
                                                                     unsigned long long* dbg, unsigned int trace_qi,
                                                                     int seg_cap) {
@@ -1334,7 +1742,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
       }
     }
     if (bad) {
-      if (threadIdx.x == 0) { item_state[w] = 1; item_list[w] = -1; item_n[w] = 0; }
+      if (threadIdx.x == 0) { item_state[w] = 1; item_list[w] = -1; item_n[w] = 0; item_slots[w] = 0; }
       continue;
     }
     // leaves (or the pieces before an unsplit round) -> global pool
@@ -1347,7 +1755,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
     }
     __syncthreads();
     if (s_base < 0) {
-      if (threadIdx.x == 0) { report(c.st, K_POOL, i); item_state[w] = 1; item_list[w] = -1; item_n[w] = 0; }
+      if (threadIdx.x == 0) { report(c.st, K_POOL, i); item_state[w] = 1; item_list[w] = -1; item_n[w] = 0; item_slots[w] = 0; }
       continue;
     }
     const long long list = s_base + s_tot;
@@ -1415,7 +1823,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
         ex = mine;
         __syncwarp();
       } else {
-        ex = warp_extra_visits(s, ln, lane);
+        ex = warp_dup_scan(c, s, ln, lane, nullptr, nullptr);
       }
       if (lane == 0 && ex > 0) {
         c.pool[list + 2 * r + 1] = (int32_t)((uint32_t)c.pool[list + 2 * r + 1] | F_REP);
@@ -1437,164 +1845,23 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
   }
 }
 
-// ------------------------------------------------------------ pinch phase
-// Trial-split candidate g (reparation.py:326-332 with strict=False).
-__device__ int try_pinch(const RepairCtx& c, int32_t g, int64_t L, int32_t poly, int64_t* ao, int64_t* al,
-                         int64_t* bo, int64_t* bl) {
-  int32_t w = hw_twin(c.hw[g]);
-  if (w < 0) { report(c.st, K_STRUCT, poly); return -1; }
-  promote(c, g, w);
-  int r = rewalk_split(c, g, w, L, poly, ao, al, bo, bl);
-  if (r != 1) demote(c, g, w);
-  return r;
-}
-
-// _pinch_candidates (reparation.py:169-205) for one piece; returns 1 split, 0 none, -1 error
-__device__ int pinch_split(const RepairCtx& c, const int32_t* X, int64_t L, int32_t poly, int64_t* ao, int64_t* al,
-                           int64_t* bo, int64_t* bl) {
-  int32_t v = -1;
-  int64_t p1 = 0, p2 = 0;
-  for (int64_t idx = 1; idx < L && v < 0; idx++)
-    for (int64_t q = 0; q < idx; q++)
-      if (X[q] == X[idx]) { v = X[idx]; p1 = q; p2 = idx; break; }
-  if (v < 0) return 0;
-  int guard = (int)(3 * c.T + 3 < (1LL << 30) ? 3 * c.T + 3 : (1LL << 30));
-  int32_t t0 = c.tv[v];
-  int32_t g0 = t0 < 0 ? -1 : he_with_origin(c.tri, t0, v);
-  if (g0 < 0) { report(c.st, K_STRUCT, poly); return -1; }
-  int deg = 0;
-  {
-    int32_t g = g0;
-    do {
-      deg++;
-      g = fan_step(c.hw, g, guard);
-      if (g < 0 || deg > guard) { report(c.st, K_STRUCT, poly); return -1; }
-    } while (g != g0);
-  }
-  int64_t poss[2] = {p2, p1};
-  for (int q = 0; q < 2; q++) {
-    int32_t outv = X[(poss[q] + 1) % L];
-    int32_t g = g0, gout = -1;
-    for (int s = 0; s < deg; s++) {
-      if (hw_front(c.hw[g]) && he_target(c.tri, g) == outv) { gout = g; break; }
-      g = fan_step(c.hw, g, guard);
-    }
-    if (gout < 0) { report(c.st, K_STRUCT, poly); return -1; }
-    int k = 0;
-    g = fan_step(c.hw, gout, guard);
-    for (int s = 1; s < deg; s++) {
-      if (hw_front(c.hw[g])) break;
-      k++;
-      g = fan_step(c.hw, g, guard);
-    }
-    if (k == 0) continue;
-    int mid = (k - 1) / 2;
-    for (int ord = -1; ord < k; ord++) {
-      int idx = ord < 0 ? mid : ord;
-      if (ord == mid) continue;
-      int32_t cand = gout;
-      for (int s = 0; s <= idx; s++) cand = fan_step(c.hw, cand, guard);
-      int r = try_pinch(c, cand, L, poly, ao, al, bo, bl);
-      if (r != 0) return r;
-    }
-  }
-  for (int64_t idx = p1 + 1; idx < p2; idx++) {
-    int32_t x = X[idx];
-    int32_t tx = c.tv[x];
-    int32_t gx0 = tx < 0 ? -1 : he_with_origin(c.tri, tx, x);
-    if (gx0 < 0) { report(c.st, K_STRUCT, poly); return -1; }
-    int32_t g = gx0;
-    int cnt = 0;
-    do {
-      if (!hw_front(c.hw[g])) {
-        int r = try_pinch(c, g, L, poly, ao, al, bo, bl);
-        if (r != 0) return r;
-      }
-      g = fan_step(c.hw, g, guard);
-      if (g < 0 || ++cnt > guard) { report(c.st, K_STRUCT, poly); return -1; }
-    } while (g != gx0);
-  }
-  return 0;
-}
-
-__device__ uint32_t piece_flags(const RepairCtx& c, const int32_t* s, int64_t n, int32_t poly, bool* ok) {
-  uint32_t f = poly_has_tip(s, n) ? F_TIP : 0u;
-  int32_t* scratch = nullptr;
-  if (n > 48) {
-    int64_t so = palloc(c, n);
-    if (so < 0) { report(c.st, K_POOL, poly); *ok = false; return 0; }
-    scratch = c.pool + so;
-  }
-  if (extra_visits(s, n, scratch) > 0) f |= F_REP;
-  return f;
-}
-
-// Runs for every item: pinch rounds (bounded by the global guard, reparation.py:322-323),
-// then the item's output totals (#leaves, #slots, #unrepaired).
+// ------------------------------------------------------------ pinch pass
 __global__ void __launch_bounds__(128) k_repair_pinch(RepairCtx c, const int32_t* __restrict__ items,
                                                       const unsigned int* n_items, int64_t* __restrict__ item_list,
                                                       int32_t* __restrict__ item_n, int64_t* __restrict__ item_slots,
                                                       unsigned long long* stats) {
-  unsigned int ni = *n_items;
-  long long guard = (long long)stats[5] + 1;
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < ni; w += (int64_t)gridDim.x * blockDim.x) {
-    int32_t i = items[w];
-    int64_t list = item_list[w];
-    int n = item_n[w];
-    item_slots[w] = 0;
-    if (list < 0) continue;
-    int n0 = n;
-    bool ok = true;
-    for (long long r = 0; r < guard && ok; r++) {
-      int elig = 0;
-      for (int k = 0; k < n; k++) {
-        uint32_t rl = (uint32_t)c.pool[list + 2 * k + 1];
-        elig += (rl & F_REP) && !(rl & F_TIP) && !(rl & F_FAIL);
-      }
-      if (elig == 0) break;
-      int64_t nl = palloc(c, 2 * (int64_t)(n + elig));
-      if (nl < 0) { report(c.st, K_POOL, i); ok = false; break; }
-      int m = 0, did = 0;
-      for (int k = 0; k < n && ok; k++) {
-        uint32_t ro = (uint32_t)c.pool[list + 2 * k], rl = (uint32_t)c.pool[list + 2 * k + 1];
-        if ((rl & F_REP) && !(rl & F_TIP) && !(rl & F_FAIL)) {
-          int64_t ao, al, bo, bl;
-          int res = pinch_split(c, c.pool + ro, rl & LEN_MASK, i, &ao, &al, &bo, &bl);
-          if (res < 0) { ok = false; break; }
-          if (res == 1) {
-            uint32_t fa = piece_flags(c, c.pool + ao, al, i, &ok);
-            uint32_t fb = piece_flags(c, c.pool + bo, bl, i, &ok);
-            c.pool[nl + 2 * m] = (int32_t)ao;
-            c.pool[nl + 2 * m + 1] = (int32_t)((uint32_t)al | fa);
-            c.pool[nl + 2 * m + 2] = (int32_t)bo;
-            c.pool[nl + 2 * m + 3] = (int32_t)((uint32_t)bl | fb);
-            m += 2;
-            did++;
-            continue;
-          }
-          rl |= F_FAIL;  // a failed pinch fails identically in every later round
-        }
-        c.pool[nl + 2 * m] = (int32_t)ro;
-        c.pool[nl + 2 * m + 1] = (int32_t)rl;
-        m++;
-      }
-      list = nl;
-      n = m;
-      if (did == 0) break;
+  const int lane = threadIdx.x & 31;
+  const unsigned int ni = *n_items;
+  const long long guard = (long long)stats[5] + 1;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = warp; w < ni; w += nwarps) {
+    const long long list = item_list[w];
+    if (list < 0) {
+      if (lane == 0) item_slots[w] = 0;
+      continue;
     }
-    if (!ok) continue;
-    unsigned long long unrep = 0;
-    int64_t slots = 0;
-    for (int k = 0; k < n; k++) {
-      uint32_t rl = (uint32_t)c.pool[list + 2 * k + 1];
-      slots += rl & LEN_MASK;
-      unrep += (rl & F_REP) ? 1 : 0;
-    }
-    item_list[w] = list;
-    item_n[w] = n;
-    item_slots[w] = slots;
-    if (unrep) atomicAdd(stats + 3, unrep);
-    if (n != n0) atomicAdd(stats + 4, (unsigned long long)(n - n0));
+    warp_finish_pinch(c, w, items[w], list, item_n[w], lane, item_list, item_n, item_slots, stats, guard);
   }
 }
 
@@ -1602,10 +1869,15 @@ __global__ void __launch_bounds__(128) k_repair_pinch(RepairCtx c, const int32_t
 __global__ void __launch_bounds__(256) k_out_counts(const int64_t* __restrict__ off, const int64_t* __restrict__ Pp,
                                                     const int32_t* __restrict__ item_of, const int32_t* __restrict__ item_n,
                                                     const int64_t* __restrict__ item_slots, int64_t* __restrict__ cnt,
-                                                    int64_t* __restrict__ slots) {
+                                                    int64_t* __restrict__ slots, const unsigned long long* stats,
+                                                    DevStatus* st) {
   const int64_t P = *Pp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= P; i += (int64_t)gridDim.x * blockDim.x) {
-    if (i == P) { cnt[i] = 0; slots[i] = 0; continue; }
+    if (i == P) {
+      cnt[i] = 0;
+      slots[i] = 0;
+      continue;
+    }
     int32_t it = item_of[i];
     if (it < 0) { cnt[i] = 1; slots[i] = off[i + 1] - off[i]; }
     else { cnt[i] = item_n[it]; slots[i] = item_slots[it]; }
@@ -1746,7 +2018,8 @@ void launch_repair_tips_long(const RepairArgs& a, cudaStream_t s) {
     if (seg_cap > kSegCap) seg_cap = kSegCap;
   }
   k_repair_tips_seg<<<kNumSMs, 32 * kSegWarps, smem, s>>>(c, a.items, a.off, a.v, a.item_list, a.item_n,
-                                                           a.item_state, a.item_depth, a.stats, a.q, a.dbg,
+                                                           a.item_state, a.item_depth, a.item_slots, a.stats, a.q,
+                                                           a.dbg,
                                                            (unsigned int)trace_qi, seg_cap);
   note_launch(1);
 }
@@ -1754,7 +2027,8 @@ void launch_repair_tips_long(const RepairArgs& a, cudaStream_t s) {
 void launch_repair_tips(const RepairArgs& a, int mode, cudaStream_t s) {
   RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st};
   k_repair_tips<<<mode ? kNumSMs : kNumSMs * 8, 32 * kTipWarps, 0, s>>>(
-      c, a.items, a.n_items, a.off, a.v, a.item_list, a.item_n, a.item_state, a.item_depth, a.stats, a.q, mode);
+      c, a.items, a.n_items, a.off, a.v, a.item_list, a.item_n, a.item_state, a.item_depth, a.item_slots, a.stats,
+      a.q, mode);
   note_launch(1);
 }
 
@@ -1766,8 +2040,8 @@ void launch_repair_pinch(const RepairArgs& a, cudaStream_t s) {
 
 void launch_out_counts(const int64_t* off, const int64_t* Pp, int64_t Pcap, const int32_t* item_of,
                        const int32_t* item_n, const int64_t* item_slots, int64_t* cnt, int64_t* slots,
-                       cudaStream_t s) {
-  k_out_counts<<<grid_for(Pcap + 1, 256), 256, 0, s>>>(off, Pp, item_of, item_n, item_slots, cnt, slots);
+                       const unsigned long long* stats, DevStatus* st, cudaStream_t s) {
+  k_out_counts<<<grid_for(Pcap + 1, 256), 256, 0, s>>>(off, Pp, item_of, item_n, item_slots, cnt, slots, stats, st);
   note_launch(1);
 }
 

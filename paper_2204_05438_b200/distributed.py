@@ -43,17 +43,33 @@ def exclusive_bases(counts) -> tuple[np.ndarray, np.ndarray]:
     return pb, sb
 
 
-def exchange_counts(n_polys: int, n_slots: int, device, group=None) -> np.ndarray:
-    """All-gather (polygons, slots) of every rank: int64[world, 2] on every rank."""
+def exchange_counts(n_polys: int, n_slots: int, device, group=None, pinch=(0, 0)) -> np.ndarray:
+    """All-gather (polygons, slots, pinch extra visits, pinch-truncated items) of every
+    rank: int64[world, 4] on every rank (32 bytes per rank)."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
     if dist.get_backend(group) == "nccl":
         device = torch.device("cuda", torch.cuda.current_device())
-    mine = torch.tensor([n_polys, n_slots], dtype=torch.int64, device=device)
-    allc = torch.empty(world * 2, dtype=torch.int64, device=device)
+    mine = torch.tensor([n_polys, n_slots, int(pinch[0]), int(pinch[1])], dtype=torch.int64, device=device)
+    allc = torch.empty(world * 4, dtype=torch.int64, device=device)
     dist.all_gather_into_tensor(allc, mine, group=group)
-    return allc.view(world, 2).cpu().numpy()
+    return allc.view(world, 4).cpu().numpy()
+
+
+def check_pinch_guard(table) -> None:
+    """The pinch pass's round guard is global (reparation.py:322: extra visits
+    of the whole tip-phase output + 1); each rank ran with its own share.  A
+    rank whose guard cut items off (truncated > 0) must have had the global
+    guard, else its output differs from the single-GPU run: fail loudly.
+    table rows: (polygons, slots, extra, truncated)."""
+    t = np.asarray(table, dtype=np.int64).reshape(-1, 4)
+    total = int(t[:, 2].sum())
+    bad = (t[:, 3] > 0) & (t[:, 2] != total)
+    if bad.any():
+        from .errors import StructuralError
+        raise StructuralError(f"pinch round guard binds on rank(s) {np.flatnonzero(bad).tolist()}: the "
+                              "partitioned result would differ from the single-GPU one", phase="reparation")
 
 
 @dataclass
@@ -72,13 +88,16 @@ class ShardedCSR:
         return int(self.offsets.numel() - 1)
 
 
-def stitch(local_off, local_verts, n_polys: int, n_slots: int, group=None, shift=None) -> ShardedCSR:
+def stitch(local_off, local_verts, n_polys: int, n_slots: int, group=None, shift=None, pinch=(0, 0)) -> ShardedCSR:
     """Exchange counts and place this rank's CSR at its global base.  `shift`
     adds the slot base to the offsets in place (default: the C ABI kernel on
-    a CUDA tensor, a plain add on CPU tensors)."""
+    a CUDA tensor, a plain add on CPU tensors); `pinch` = this rank's
+    (TM_STAT_PINCH_EXTRA, TM_STAT_PINCH_TRUNCATED) for the global guard check."""
     import torch.distributed as dist
     rank = dist.get_rank(group)
-    counts = exchange_counts(n_polys, n_slots, local_off.device if local_off.is_cuda else "cpu", group)
+    table = exchange_counts(n_polys, n_slots, local_off.device if local_off.is_cuda else "cpu", group, pinch)
+    check_pinch_guard(table)
+    counts = table[:, :2]
     pb, sb = exclusive_bases(counts)
     off = local_off[: n_polys + 1]
     if shift is None:
@@ -140,7 +159,7 @@ def run_partition(xy, tri, n: int, T: int, t_begin: int, t_end: int, ctx=None, o
     L = _capi.lib()
     ctx.check(L.tm_ctx_set_partition(ctx.ptr, t_begin, t_end))
     npol, nsl = ctypes.c_int64(), ctypes.c_int64()
-    stats = (ctypes.c_int64 * 8)()
+    stats = (ctypes.c_int64 * _capi.NUM_STATS)()
     try:
         rc = L.tm_mesh_to_polygons(ctx.ptr, _capi.ptr(xy), n, _capi.ptr(tri), 64 if tri.dtype == torch.int64 else 32,
                                    T, 0, _capi.ptr(off), _capi.ptr(verts), T, 3 * T, ctypes.byref(npol),
@@ -163,7 +182,7 @@ def execute_distributed(tri, group=None, gather: bool = True):
     tr = torch.from_numpy(np.ascontiguousarray(tri.triangles)).to(dev)
     b, e = partition(T, world)[rank]
     off, verts, p, f, stats = run_partition(xy, tr, n, T, b, e)
-    shard = stitch(off, verts, p, f, group)
+    shard = stitch(off, verts, p, f, group, pinch=(stats["pinch_extra"], stats["pinch_truncated"]))
     if not gather:
         return shard, stats
     return gather_csr(shard, 0, group), stats

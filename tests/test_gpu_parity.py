@@ -102,7 +102,7 @@ def test_host_c_abi_one_call(cuda, name):
     off = np.zeros(T + 1, dtype=np.int64)
     verts = np.zeros(3 * T, dtype=np.int32)
     npol, nsl = ctypes.c_int64(), ctypes.c_int64()
-    stats = (ctypes.c_int64 * 8)()
+    stats = (ctypes.c_int64 * _capi.NUM_STATS)()
     ctx = _capi.context()
     rc = _capi.lib().tm_mesh_to_polygons_host(ctx.ptr, _capi.ptr(tri.vertices), tri.n_vertices,
                                               _capi.ptr(tri.triangles), T, 1, _capi.ptr(off), _capi.ptr(verts),

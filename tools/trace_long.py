@@ -22,7 +22,7 @@ def run():
     v = torch.empty(3 * T, dtype=torch.int32, device="cuda")
     ctx = _capi.context()
     P, F = ctypes.c_int64(), ctypes.c_int64()
-    st = (ctypes.c_int64 * 8)()
+    st = (ctypes.c_int64 * _capi.NUM_STATS)()
     for _ in range(3):
         rc = _capi.lib().tm_mesh_to_polygons(ctx.ptr, _capi.ptr(xy), n, _capi.ptr(tr), 64, T, 0, _capi.ptr(off),
                                              _capi.ptr(v), T, 3 * T, ctypes.byref(P), ctypes.byref(F), st,
