@@ -117,7 +117,7 @@ struct tm_ctx {
   Buf item_of, items, long_list, item_list, item_n, item_slots, item_state, item_depth, cnt, slotsz, pbase, sbase, pool,
       undo, hugeq, longq;
   // whole-path buffers
-  Buf xy, tri, tri32, hw, max_edge, seed, tv, off0, v0, fin_off, fin_v, hw_snap;
+  Buf xy, tri, tri32, hw, max_edge, seed, tv, off0, v0, fin_off, fin_v, hw_snap, hv;
   cudaStream_t gstream = nullptr;
   cudaStream_t aux = nullptr;                            // long repair items run beside the short ones
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -129,6 +129,9 @@ struct tm_ctx {
   int64_t ecap = 0;
   int use_graph = 1;
   int64_t part_begin = 0, part_end = -1;  // seed partition [begin, end) in triangles (-1: T)
+  // whole-path runs: the traversal records each slot's boundary half-edge
+  // (hv) and repair derives its fan starts from it instead of a trivertex
+  int32_t* path_hv = nullptr;
   long long graph_kernels = 0;  // kernels per graph replay (counted at capture)
 };
 
@@ -413,7 +416,7 @@ static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* 
                       d_off, ctx->eoff.as<int64_t>(), ctx->ent_r.as<int32_t>(), ctx->ent_base.as<int64_t>(),
                       ctx->ecap, &dc->st, s);
     launch_ruler_write(d_tri32, d_hw, &dc->n_entries, ctx->ent_r.as<int32_t>(), ctx->ent_base.as<int64_t>(),
-                       ctx->rdist.as<int32_t>(), T, ctx->ecap, d_v, s);
+                       ctx->rdist.as<int32_t>(), T, ctx->ecap, d_v, ctx->path_hv, s);
   }
   CK(cudaGetLastError());
   return TM_OK;
@@ -433,7 +436,11 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
                     ctx->long_list.as<int32_t>(), &dc->n_long, dc->stats, q, s);
   }
   CK(cudaMemsetAsync(ctx->item_state.p, 0, Tn * sizeof(int32_t), s));
-  RepairArgs a{d_tri32, d_hw, d_tv, T, ctx->pool.as<int32_t>(), ctx->pool_cap, &dc->pool_top, ctx->undo.as<int32_t>(),
+  const int tv_exact = ctx->path_hv == nullptr;
+  if (!tv_exact)  // fan starts for the work items' vertices (d_tv is scratch here)
+    launch_tv_items(d_off_in, d_v_in, ctx->path_hv, ctx->items.as<int32_t>(), &dc->n_items, Tn,
+                    const_cast<int32_t*>(d_tv), s);
+  RepairArgs a{d_tri32, d_hw, d_tv, tv_exact, T, ctx->pool.as<int32_t>(), ctx->pool_cap, &dc->pool_top, ctx->undo.as<int32_t>(),
                &dc->undo_top, (unsigned long long)Tn + 1024, &dc->st, ctx->items.as<int32_t>(), &dc->n_items,
                d_off_in, d_v_in, ctx->item_list.as<int64_t>(), ctx->item_n.as<int32_t>(),
                ctx->item_slots.as<int64_t>(), ctx->item_state.as<int32_t>(), ctx->item_depth.as<int32_t>(),
@@ -744,6 +751,7 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
   ENSURE(tv, nn * sizeof(int32_t));
   ENSURE(off0, (Tn + 1) * sizeof(int64_t));
   ENSURE(v0, 3 * Tn * sizeof(int32_t));
+  ENSURE(hv, 3 * Tn * sizeof(int32_t));
   if (!ctx->gstream) CK(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
   for (auto& e : ctx->ev)
     if (!e) CK(cudaEventCreate(&e));
@@ -766,12 +774,16 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
     if ((r = enqueue_reset(ctx, s))) return r;
     CK(rec(ctx->ev[0], s));
     if ((r = enqueue_label(ctx, d_xy, n, d_tri, tri_bits, T, check, tri32, hw, ctx->max_edge.as<int8_t>(),
-                           ctx->seed.as<uint8_t>(), tv, s)))
+                           ctx->seed.as<uint8_t>(), nullptr, s)))
       return r;
     CK(rec(ctx->ev[1], s));
-    if ((r = enqueue_traverse(ctx, tri32, hw, ctx->seed.as<uint8_t>(), T, off0, v0, s))) return r;
+    ctx->path_hv = ctx->hv.as<int32_t>();
+    r = enqueue_traverse(ctx, tri32, hw, ctx->seed.as<uint8_t>(), T, off0, v0, s);
+    if (r) { ctx->path_hv = nullptr; return r; }
     CK(rec(ctx->ev[2], s));
-    if ((r = enqueue_repair(ctx, tri32, hw, tv, T, off0, v0, &dc->n_seeds, d_off, d_v, s))) return r;
+    r = enqueue_repair(ctx, tri32, hw, tv, T, off0, v0, &dc->n_seeds, d_off, d_v, s);
+    ctx->path_hv = nullptr;
+    if (r) return r;
     CK(rec(ctx->ev[3], s));
     return enqueue_readback(ctx, s);
   };
@@ -818,12 +830,14 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
   rc = decode_status(ctx, h);
   if (rc == TM_ERR_CAPACITY) {
     // labels are ours: relabeling restores the pre-repair frontier exactly
+    ctx->path_hv = ctx->hv.as<int32_t>();  // the traversal's slot half-edges are still in place
     rc = retry_repair(ctx, tri32, hw, tv, T, off0, v0, &dc->n_seeds, d_off, d_v, s, &h, rc,
                       [&](cudaStream_t st) -> int {
                         launch_relabel(ctx->max_edge.as<int8_t>(), T, hw, ctx->seed.as<uint8_t>(), st);
                         CK(cudaGetLastError());
                         return TM_OK;
                       });
+    ctx->path_hv = nullptr;
     if (ctx->graph) cudaGraphExecDestroy(ctx->graph);  // pool size changed
     ctx->graph = nullptr;
   }

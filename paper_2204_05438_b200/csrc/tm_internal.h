@@ -48,7 +48,7 @@ void launch_chain_emit(const int32_t* start, const int64_t* Pp, int64_t Pcap, co
                        int64_t* ent_base, int64_t ecap, DevStatus* st, cudaStream_t s);
 void launch_ruler_write(const int32_t* tri, const int32_t* hw, const int64_t* n_entries, const int32_t* ent_r,
                         const int64_t* ent_base, const int32_t* rdist, int64_t T, int64_t ecap, int32_t* verts,
-                        cudaStream_t s);
+                        int32_t* hv, cudaStream_t s);
 
 // tm_repair.cu
 struct LongQueue {       // work items longer than kLongMin, longest class first
@@ -61,7 +61,8 @@ struct LongQueue {       // work items longer than kLongMin, longest class first
 struct RepairArgs {
   const int32_t* tri;
   int32_t* hw;
-  const int32_t* tv;
+  const int32_t* tv;     // a triangle incident to each polygon vertex (exact lowest iff tv_exact)
+  int tv_exact;
   int64_t T;
   int32_t* pool;
   unsigned long long pool_cap;
@@ -83,6 +84,9 @@ struct RepairArgs {
   LongQueue q;
   unsigned long long* dbg;  // 64 timestamp slots (debug)
 };
+// tv[verts[k]] = hv[k] / 3 for every slot of the work items (any incident triangle)
+void launch_tv_items(const int64_t* off, const int32_t* v, const int32_t* hv, const int32_t* items,
+                     const unsigned int* n_items, int64_t Pcap, int32_t* tv, cudaStream_t s);
 void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, int32_t* item_of,
                      int32_t* items, unsigned int* n_items, int32_t* long_list, unsigned int* n_long,
                      unsigned long long* stats, LongQueue q, cudaStream_t s);

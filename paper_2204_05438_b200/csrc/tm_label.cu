@@ -219,9 +219,11 @@ __global__ void __launch_bounds__(kLabelThreads) k_tri_pass(const double2* __res
           if (d < 0.0) report(st, K_ORIENTATION, t);
           else if (d == 0.0) report(st, K_DEGENERATE, t);
         }
-        atomicMin(tv + a, (int32_t)t);
-        atomicMin(tv + b, (int32_t)t);
-        atomicMin(tv + c, (int32_t)t);
+        if (tv != nullptr) {  // phase API only; the whole path derives fan starts from the polygons
+          atomicMin(tv + a, (int32_t)t);
+          atomicMin(tv + b, (int32_t)t);
+          atomicMin(tv + c, (int32_t)t);
+        }
         // half-edge j: origin corner (j+1)%3, target corner (j+2)%3
         const int32_t cv[3] = {(int32_t)a, (int32_t)b, (int32_t)c};
 #pragma unroll
@@ -287,7 +289,7 @@ __global__ void __launch_bounds__(kLabelThreads) k_pair_pass(const int32_t* __re
     __syncwarp();
   }
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride)
-    if (tv[v] == 0x7F7F7F7F) tv[v] = -1;
+    if (tv != nullptr && tv[v] == 0x7F7F7F7F) tv[v] = -1;
 }
 
 // labeling.py:65-115 fused.  k = twin % 3 replaces the back-slot search.
@@ -388,7 +390,7 @@ void launch_label_a(const double* xy, int64_t n, const void* tri, int tri_is64, 
                     DevStatus* st, cudaStream_t s) {
   TwinTable tb = table_geometry(n, T, table);
   cudaMemsetAsync(table, 0xFF, hash_bytes(n, T), s);
-  if (n > 0) {
+  if (n > 0 && tv != nullptr) {
     // sentinel 0x7F7F7F7F (> any triangle index), mapped to -1 by pass B
     cudaMemsetAsync(tv, 0x7F, (size_t)n * sizeof(int32_t), s);
   }
@@ -408,7 +410,7 @@ void launch_label_a(const double* xy, int64_t n, const void* tri, int tri_is64, 
 void launch_label_b(const int32_t* tri32, int64_t n, int64_t T, int32_t* hw, const int8_t* max_edge, uint8_t* seed,
                     int32_t* tv, void* table, int check, DevStatus* st, cudaStream_t s) {
   TwinTable tb = table_geometry(n, T, table);
-  int64_t m = T > n ? T : n;
+  int64_t m = (T > n || tv == nullptr) ? T : n;
   if (m > 0) {
     k_pair_pass<<<grid_for(m, kLabelThreads), kLabelThreads, 0, s>>>(tri32, T, max_edge, tb, hw, seed, tv, n, check,
                                                                      st);

@@ -41,7 +41,7 @@ constexpr uint32_t LEN_MASK = (1u << 29) - 1;
 struct RepairCtx {
   const int32_t* tri;
   int32_t* hw;
-  const int32_t* tv;
+  const int32_t* tv;  // a triangle incident to each polygon vertex: fan starts (tip fans are rotation-invariant)
   int64_t T;
   int32_t* pool;
   unsigned long long pool_cap;
@@ -50,6 +50,7 @@ struct RepairCtx {
   unsigned long long* undo_top;
   unsigned long long undo_cap;
   DevStatus* st;
+  int tv_exact;       // tv is the reference trivertex (lowest incident triangle, mesh_core.py:171-178)
 };
 
 __device__ __forceinline__ int64_t palloc(const RepairCtx& c, int64_t n) {
@@ -881,6 +882,24 @@ __device__ int warp_try_pinch_arc(const RepairCtx& c, int32_t g, const int32_t* 
   return 1;
 }
 
+// Half-edge with origin v in the reference's trivertex triangle (the lowest
+// incident one, mesh_core.py:171-178): the pinch candidates iterate the fan
+// from there.  Without an exact trivertex the full fan is walked
+// once from any incident triangle and its minimum taken.
+__device__ int32_t trivertex_he(const RepairCtx& c, int32_t v, int guard) {
+  int32_t t0 = c.tv[v];
+  int32_t g0 = t0 < 0 ? -1 : he_with_origin(c.tri, t0, v);
+  if (g0 < 0 || c.tv_exact) return g0;
+  int32_t g = g0, best = g0;
+  int k = 0;
+  do {
+    if (g / 3 < best / 3) best = g;
+    g = fan_step(c.hw, g, guard);
+    if (g < 0 || ++k > guard) return -1;
+  } while (g != g0);
+  return best;
+}
+
 // _pinch_candidates (reparation.py:169-205) for one piece, candidates in the
 // reference order, each trial-split until one keeps.  Every lane runs the
 // (identical) candidate enumeration so the trials stay warp-convergent.
@@ -891,8 +910,7 @@ __device__ int warp_pinch_split(const RepairCtx& c, const int32_t* X, int L, int
   if (p2 < 0) return 0;
   const int32_t v = X[p2];
   const int guard = (int)(3 * c.T + 3 < (1LL << 30) ? 3 * c.T + 3 : (1LL << 30));
-  int32_t t0 = c.tv[v];
-  int32_t g0 = t0 < 0 ? -1 : he_with_origin(c.tri, t0, v);
+  int32_t g0 = trivertex_he(c, v, guard);
   if (g0 < 0) {
     if (lane == 0) report(c.st, K_STRUCT, poly);
     return -1;
@@ -941,8 +959,7 @@ __device__ int warp_pinch_split(const RepairCtx& c, const int32_t* X, int L, int
   }
   for (int idx = p1 + 1; idx < p2; idx++) {  // internal fan edges of the inner-loop vertices
     int32_t x = X[idx];
-    int32_t tx = c.tv[x];
-    int32_t gx0 = tx < 0 ? -1 : he_with_origin(c.tri, tx, x);
+    int32_t gx0 = trivertex_he(c, x, guard);
     if (gx0 < 0) {
       if (lane == 0) report(c.st, K_STRUCT, poly);
       return -1;
@@ -1226,20 +1243,24 @@ constexpr int kSegMaxL = 8192;   // longer items: the warp kernel from scratch (
 constexpr int kPairCap = 16384;  // pair-map slots (>= 2 kSegMaxL); reused as leaf hash sets
 constexpr int kSegRec = 1024;    // piece records per round list
 constexpr int kSegTips = 512;    // precomputed tips per item
-constexpr int kSegTouch = 1024;  // promoted-edge endpoints per item
+constexpr int kSegTouch = 2048;  // hash set of promoted-edge endpoints (load <= 1/2)
 constexpr int kSmemMax = 226 * 1024;  // dynamic; leaves room for the static __shared__ words
 
 struct Seg {
-  int32_t base, len, loff;  // base >= 0: P[(base + i) mod L], i < len; base < 0: the vertex ~base (len 1)
+  int32_t base;        // >= 0: P[(base + i) mod L], i < len; < 0: the vertex ~base (len 1)
+  uint16_t len, loff;  // pieces are shorter than 3 kSegMaxL < 2^16
 };
+__device__ __forceinline__ Seg mkseg(int32_t base, int len, int loff) { Seg r; r.base = base; r.len = (uint16_t)len; r.loff = (uint16_t)loff; return r; }
 struct SPiece {
   int32_t soff, nseg, len, ftip;  // segments [soff, soff + nseg), first tip position (-1: none)
+  int32_t fk;                     // index in P of the first tip's vertex (-1: not a range element)
 };
 
 constexpr size_t kSegFixed = (size_t)kSegMaxL * 4 + (kSegMaxL / 32) * 4 + (size_t)kPairCap * 4 +
                              2 * (size_t)kSegRec * sizeof(SPiece) + (size_t)kSegRec * 4 +
                              2 * (size_t)kSegWarps * kFanCap * 4 + 2 * (size_t)kSegTips * 4 +
-                             (size_t)kSegTips * sizeof(SplitInfo) + (size_t)kSegTouch * 4 + 128;
+                             (size_t)kSegTips * sizeof(SplitInfo) + (size_t)kSegTouch * 4 +
+                             (kSegMaxL / 32 + 1) * 4 + 128;
 constexpr int kSegCap = (int)((kSmemMax - kSegFixed) / sizeof(Seg));
 size_t seg_smem_bytes() { return kSegFixed + (size_t)kSegCap * sizeof(Seg); }
 
@@ -1317,7 +1338,8 @@ __device__ int32_t selem1(const SegView& g, const SPiece& X, int p) {
 
 // reparation.py:59-71 on a segment piece: the first position p with
 // s[p-1] == s[p+1] (cyclic), or -1.  Warp-uniform.
-__device__ int seg_first_tip(const SegView& g, const SPiece& X, int lane) {
+__device__ int seg_first_tip(const SegView& g, const SPiece& X, int lane, int* fk_out) {
+  *fk_out = -1;
   if (X.len < 4) {
     int r = -1;
     if (lane == 0)
@@ -1326,7 +1348,7 @@ __device__ int seg_first_tip(const SegView& g, const SPiece& X, int lane) {
     return __shfl_sync(kFull, r, 0);
   }
   for (int c0 = 0; c0 < X.nseg; c0 += 32) {
-    int s = c0 + lane, best = -1;
+    int s = c0 + lane, best = -1, fk = -1;
     if (s < X.nseg) {
       Seg sg = g.segs[X.soff + s];
       Seg sp = g.segs[X.soff + (s == 0 ? X.nseg - 1 : s - 1)];
@@ -1342,9 +1364,13 @@ __device__ int seg_first_tip(const SegView& g, const SPiece& X, int lane) {
         }
         if (best < 0 && l >= 2 && sval(g, sg, l - 2) == nv) best = sg.loff + l - 1;
       }
+      if (best >= 0 && sg.base >= 0) fk = wrapL(sg.base + (best - sg.loff), g.L);
     }
     unsigned m = __ballot_sync(kFull, best >= 0);
-    if (m) return __shfl_sync(kFull, best, __ffs(m) - 1);
+    if (m) {
+      *fk_out = __shfl_sync(kFull, fk, __ffs(m) - 1);
+      return __shfl_sync(kFull, best, __ffs(m) - 1);
+    }
   }
   return -1;
 }
@@ -1398,13 +1424,13 @@ __device__ int emit_range_warp(const SegView& g, const SPiece& X, int start, int
         inc = true;
         int idx = s - s0;
         if (idx < 0) idx += ns;
-        out[n + idx] = Seg{sg.base >= 0 ? wrapL(sg.base + skip, g.L) : sg.base, min(sg.len - skip, cnt - r0), lo + r0};
+        out[n + idx] = mkseg(sg.base >= 0 ? wrapL(sg.base + skip, g.L) : sg.base, min(sg.len - skip, cnt - r0), lo + r0);
       }
       if (s == s0 && start > sg.loff) {
         int rt = Lx - (start - sg.loff);
         if (rt < cnt) {
           tail = true;
-          out[n + ns] = Seg{sg.base, min(start - sg.loff, cnt - rt), lo + rt};
+          out[n + ns] = mkseg(sg.base, min(start - sg.loff, cnt - rt), lo + rt);
         }
       }
     }
@@ -1444,7 +1470,8 @@ __device__ int emit_range_warp(const SegView& g, const SPiece& X, int start, int
 // re-walk start pairs) and the edge is promoted; returns false without side
 // effects when a search fails (the caller falls back to the re-walk).
 __device__ bool seg_split_arcs(const RepairCtx& c, const SegView& g, const SPiece& X, int pos, int32_t v,
-                               const SplitInfo& si, int* s_stop, int seg_cap, int lane, SPiece* A, SPiece* B,
+                               const SplitInfo& si, int* s_stop, int seg_base, int seg_cap, int lane, SPiece* A,
+                               SPiece* B,
                                unsigned long long* prof) {
   const int Lx = X.len;
   if (si.a_in < 0) return false;
@@ -1482,21 +1509,22 @@ __device__ bool seg_split_arcs(const RepairCtx& c, const SegView& g, const SPiec
   if (lane == 0) base = atomicAdd(s_stop, need);
   base = __shfl_sync(kFull, base, 0);
   if (base + need > seg_cap) return false;  // (capacity is checked per round; defensive)
+  base += seg_base;
   int32_t we = 0, wt = 0;
   if (lane == 0) { we = c.hw[si.e]; wt = c.hw[si.te]; }  // promotion loads overlap the emission
   Seg* oa = g.segs + base;
   Seg* ob = g.segs + base + X.nseg + 4;
   int na = 0, nb = 0;
   if (ka == 0) {
-    if (lane == 0) oa[0] = Seg{~v, 1, 0};
+    if (lane == 0) oa[0] = mkseg(~v, 1, 0);
     na = emit_range_warp(g, X, j, la - 1, oa, 1, 1, lane);
   } else {
     na = emit_range_warp(g, X, wrapN(j + ka - 1, Lx), la - ka, oa, 0, 0, lane);
-    if (lane == 0) oa[na] = Seg{~v, 1, la - ka};
+    if (lane == 0) oa[na] = mkseg(~v, 1, la - ka);
     na = emit_range_warp(g, X, j, ka - 1, oa, na + 1, la - ka + 1, lane);
   }
   nb = emit_range_warp(g, X, wrapN(pos + kb, Lx), lb - 1 - kb, ob, 0, 0, lane);
-  if (lane == 0) ob[nb] = Seg{~si.u, 1, lb - 1 - kb};
+  if (lane == 0) ob[nb] = mkseg(~si.u, 1, lb - 1 - kb);
   nb = emit_range_warp(g, X, pos, kb, ob, nb + 1, lb - kb, lane);
   if (lane == 0) {
     c.hw[si.e] = we | 1;
@@ -1517,6 +1545,25 @@ __device__ bool seg_split_arcs(const RepairCtx& c, const SegView& g, const SPiec
   B->soff = __shfl_sync(kFull, B->soff, 0); B->nseg = __shfl_sync(kFull, B->nseg, 0);
   B->len = __shfl_sync(kFull, B->len, 0);
   return true;
+}
+
+__device__ __forceinline__ void tset_add(int32_t* set, int32_t x) {
+  uint32_t h = ((uint32_t)x * 0x9E3779B1u) & (kSegTouch - 1);
+  for (int k = 0; k < kSegTouch; k++) {
+    int32_t prev = atomicCAS(&set[h], -1, x);
+    if (prev == -1 || prev == x) return;
+    h = (h + 1) & (kSegTouch - 1);
+  }
+}
+__device__ __forceinline__ bool tset_has(const int32_t* set, int32_t x) {
+  uint32_t h = ((uint32_t)x * 0x9E3779B1u) & (kSegTouch - 1);
+  for (int k = 0; k < kSegTouch; k++) {
+    int32_t y = set[h];
+    if (y == x) return true;
+    if (y == -1) return false;
+    h = (h + 1) & (kSegTouch - 1);
+  }
+  return false;
 }
 
 __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c, const int32_t* __restrict__ items,
@@ -1540,8 +1587,9 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
   int32_t* tipv = fans + 2 * kSegWarps * kFanCap;  // tip vertex (or -1 when its info is unusable)
   int32_t* tipb = tipv + kSegTips;                 // barrier vertex
   SplitInfo* tipinfo = reinterpret_cast<SplitInfo*>(tipb + kSegTips);
-  int32_t* touched = reinterpret_cast<int32_t*>(tipinfo + kSegTips);
-  Seg* segs = reinterpret_cast<Seg*>(touched + kSegTouch);
+  int32_t* tset = reinterpret_cast<int32_t*>(tipinfo + kSegTips);  // promoted-edge endpoints (hash set)
+  int32_t* tiprank = tset + kSegTouch;                              // tips of P before word w
+  Seg* segs = reinterpret_cast<Seg*>(tiprank + kSegMaxL / 32 + 1);
   __shared__ int s_ntip, s_ntouch, s_stop, s_fail, s_ntips, s_need, s_tot;
   __shared__ long long s_base;
   __shared__ unsigned int s_w;
@@ -1576,19 +1624,41 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
     for (int k = threadIdx.x; k < L; k += blockDim.x) P[k] = v[b0 + k];
     for (int k = threadIdx.x; k < pcap; k += blockDim.x) pmap[k] = -1;
     for (int k = threadIdx.x; k < (L + 31) / 32; k += blockDim.x) tipbits[k] = 0;
-    if (threadIdx.x == 0) { s_ntip = 0; s_ntouch = 0; s_fail = 0; s_stop = 1; }
+    for (int k = threadIdx.x; k < kSegTouch; k += blockDim.x) tset[k] = -1;
+    if (threadIdx.x == 0) { s_ntip = 0; s_ntouch = 0; s_fail = 0; s_stop = 1; }  // segs[0]: the item
     __syncthreads();
     const SegView g{P, L, tipbits, pmap, pcap - 1, segs};
-    // tips of P (bitmap + list) and the pair map
+    // tips of P (bitmap) and the pair map
     for (int k = threadIdx.x; k < L; k += blockDim.x) {
       int32_t a = P[k == 0 ? L - 1 : k - 1], y = P[k];
-      if (a == P[k + 1 == L ? 0 : k + 1]) {
-        atomicOr(&tipbits[k >> 5], 1u << (k & 31));
-        int t = atomicAdd(&s_ntip, 1);
-        if (t < kSegTips) { tipv[t] = y; tipb[t] = a; }
-      }
+      if (a == P[k + 1 == L ? 0 : k + 1]) atomicOr(&tipbits[k >> 5], 1u << (k & 31));
       uint32_t h = pair_hash(a, y) & (pcap - 1);
       while (atomicCAS(&pmap[h], -1, k) != -1) h = (h + 1) & (pcap - 1);
+    }
+    __syncthreads();
+    // tip slots in P order: tip k lives at tiprank[k / 32] + (tips below k in its word)
+    const int nwords = (L + 31) / 32;
+    if (wib == 0) {
+      int carry = 0;
+      for (int base = 0; base < nwords; base += 32) {
+        int wd = base + lane;
+        int cnt = wd < nwords ? __popc(tipbits[wd]) : 0, inc = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+          int y = __shfl_up_sync(kFull, inc, o);
+          if (lane >= o) inc += y;
+        }
+        if (wd < nwords) tiprank[wd] = carry + inc - cnt;
+        carry += __shfl_sync(kFull, inc, 31);
+      }
+      if (lane == 0) s_ntip = carry;
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < L; k += blockDim.x) {
+      uint32_t wbits = tipbits[k >> 5];
+      if ((wbits >> (k & 31)) & 1u) {
+        int t = tiprank[k >> 5] + __popc(wbits & ((1u << (k & 31)) - 1u));
+        if (t < kSegTips) { tipv[t] = P[k]; tipb[t] = P[k == 0 ? L - 1 : k - 1]; }
+      }
     }
     __syncthreads();
     // every tip of the item is a tip of P (an arc split only removes the split
@@ -1602,16 +1672,16 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
         if (!ok) tipv[k] = -1;
       }
     }
-    if (threadIdx.x == 0) segs[0] = Seg{0, L, 0};
+    if (threadIdx.x == 0) segs[0] = mkseg(0, L, 0);
     __syncthreads();
     if (trace) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ns)); dbg[1] = t_ns; dbg[2] = L; dbg[3] = s_ntip; }
     if (wib == 0) {
-      SPiece X0{0, 1, L, -1};
-      X0.ftip = s_ntip > 0 ? seg_first_tip(g, X0, lane) : -1;
+      SPiece X0{0, 1, L, -1, -1};
+      X0.ftip = s_ntip > 0 ? seg_first_tip(g, X0, lane, &X0.fk) : -1;
       if (lane == 0) { recs[0] = X0; s_ntips = X0.ftip >= 0 ? 1 : 0; }
     }
     __syncthreads();
-    int cur = 0, n = 1, ntips = s_ntips;
+    int cur = 0, n = 1, ntips = s_ntips, hbase = 0;
     long long depth = 0, splits = 0;
     bool bad = false, spill = false;
     while (ntips > 0) {
@@ -1644,10 +1714,31 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
       }
       if (threadIdx.x == 0) s_ntips = 0;
       __syncthreads();
-      if (n + ntips > kSegRec || s_stop + s_need > seg_cap) { spill = true; break; }  // uniform
+      // Segments are bump-allocated in one half of the arena; when a round
+      // would overflow it, the live pieces are first compacted into the other
+      // half, so the arena only ever has to hold the live pieces.
+      const int half = seg_cap / 2;
+      if (n + ntips > kSegRec) { spill = true; break; }  // uniform
+      if (s_stop + s_need > half) {
+        const int nb = hbase == 0 ? half : 0;
+        __syncthreads();
+        if (threadIdx.x == 0) s_stop = 0;
+        __syncthreads();
+        for (int r = wib; r < n; r += kSegWarps) {
+          SPiece X = in[r];
+          int rel = 0;
+          if (lane == 0) rel = atomicAdd(&s_stop, X.nseg);
+          rel = __shfl_sync(kFull, rel, 0);
+          for (int k = lane; k < X.nseg; k += 32) segs[nb + rel + k] = segs[X.soff + k];
+          if (lane == 0) in[r].soff = nb + rel;
+        }
+        hbase = nb;
+        __syncthreads();
+        if (s_stop + s_need > half) { spill = true; break; }  // uniform
+      }
+      const int tb = hbase;
       depth++;
-      const int ntouch0 = s_ntouch < kSegTouch ? s_ntouch : -1;  // -1: overflowed, always recompute
-      __syncthreads();
+      const bool tset_ok = s_ntouch <= kSegTouch / 2;  // else: always recompute
       for (int r = threadIdx.x; r < n; r += blockDim.x)
         if (in[r].ftip < 0) out[s_out[r]] = in[r];
       int t_idx = 0;
@@ -1658,22 +1749,24 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
         const int pos = X.ftip;
         long long ck0 = clock64();
         const int32_t tv_ = selem(g, X, pos, lane), bv = selem(g, X, pos == 0 ? X.len - 1 : pos - 1, lane);
-        int k = warp_find_first(ntip_pre, lane, [&](int qq) { return tipv[qq] == tv_; });
+        int k = -1;
+        if (X.fk >= 0) {  // the precomputed slot of this tip of P
+          uint32_t wbits = tipbits[X.fk >> 5];
+          k = tiprank[X.fk >> 5] + __popc(wbits & ((1u << (X.fk & 31)) - 1u));
+          if (k >= ntip_pre || tipv[k] != tv_) k = -1;
+        }
         SplitInfo si;
-        bool use = k >= 0 && ntouch0 >= 0;
+        bool use = k >= 0 && tset_ok;
         if (use) {
           si = tipinfo[k];
-          bool stale = warp_find_first(ntouch0, lane, [&](int qq) {
-                         int32_t x = touched[qq];
-                         return x == tv_ || x == si.u;
-                       }) >= 0;
-          use = !stale;
+          use = !tset_has(tset, tv_) && !tset_has(tset, si.u);  // no promotion touched v or u
         }
         if (lane == 0) atomicAdd(dbg + (use ? 62 : 61), 1ull);
         bool ok = use || warp_split_info(c, tv_, bv, i, fan, back, lane, false, false, &si);
-        SPiece A{0, 0, 0, -1}, B{0, 0, 0, -1};
+        SPiece A{0, 0, 0, -1, -1}, B{0, 0, 0, -1, -1};
         long long ck1 = clock64();
-        if (ok && !seg_split_arcs(c, g, X, pos, tv_, si, &s_stop, seg_cap, lane, &A, &B, qi == trace_qi ? dbg + 52 : nullptr)) {
+        if (ok && !seg_split_arcs(c, g, X, pos, tv_, si, &s_stop, tb, half, lane, &A, &B,
+                                   qi == trace_qi ? dbg + 52 : nullptr)) {
           // re-walk fallback (reparation.py:216-229) with the strict length law;
           // the pieces come back as one-vertex segments
           if (lane == 0) { promote(c, si.e, si.te); atomicAdd(dbg + 63, 1ull); }
@@ -1693,14 +1786,15 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
             int sb = 0;
             if (lane == 0) sb = atomicAdd(&s_stop, la + lb);
             sb = __shfl_sync(kFull, sb, 0);
-            if (sb + la + lb > seg_cap) {
+            if (sb + la + lb > half) {
               if (lane == 0) report(c.st, K_STRUCT, i);
               ok = false;
             } else {
-              for (int x = lane; x < la; x += 32) segs[sb + x] = Seg{~pa[x], 1, x};
-              for (int x = lane; x < lb; x += 32) segs[sb + la + x] = Seg{~pb[x], 1, x};
-              A = SPiece{sb, la, la, -1};
-              B = SPiece{sb + la, lb, lb, -1};
+              sb += tb;
+              for (int x = lane; x < la; x += 32) segs[sb + x] = mkseg(~pa[x], 1, x);
+              for (int x = lane; x < lb; x += 32) segs[sb + la + x] = mkseg(~pb[x], 1, x);
+              A = SPiece{sb, la, la, -1, -1};
+              B = SPiece{sb + la, lb, lb, -1, -1};
             }
           }
         }
@@ -1710,12 +1804,13 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
           continue;
         }
         if (lane == 0) {
-          int tk = atomicAdd(&s_ntouch, 2);
-          if (tk + 2 <= kSegTouch) { touched[tk] = tv_; touched[tk + 1] = si.u; }
+          atomicAdd(&s_ntouch, 2);
+          tset_add(tset, tv_);
+          tset_add(tset, si.u);
         }
         long long ck2 = clock64();
-        A.ftip = seg_first_tip(g, A, lane);
-        B.ftip = seg_first_tip(g, B, lane);
+        A.ftip = seg_first_tip(g, A, lane, &A.fk);
+        B.ftip = seg_first_tip(g, B, lane, &B.fk);
         long long ck3 = clock64();
         if (qi == trace_qi && lane == 0) {
           atomicAdd(dbg + 56, (unsigned long long)(ck1 - ck0));
@@ -1989,6 +2084,25 @@ static inline int grid_for(int64_t n, int block) {
   return (int)(g < 1 ? 1 : g);
 }
 
+__global__ void __launch_bounds__(256) k_tv_items(const int64_t* __restrict__ off, const int32_t* __restrict__ v,
+                                                  const int32_t* __restrict__ hv, const int32_t* __restrict__ items,
+                                                  const unsigned int* n_items, int32_t* __restrict__ tv) {
+  const int lane = threadIdx.x & 31;
+  const unsigned int ni = *n_items;
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < ni;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int32_t i = items[w];
+    const int64_t b = off[i], e = off[i + 1];
+    for (int64_t k = b + lane; k < e; k += 32) tv[v[k]] = hv[k] / 3;
+  }
+}
+
+void launch_tv_items(const int64_t* off, const int32_t* v, const int32_t* hv, const int32_t* items,
+                     const unsigned int* n_items, int64_t Pcap, int32_t* tv, cudaStream_t s) {
+  k_tv_items<<<kNumSMs * 8, 256, 0, s>>>(off, v, hv, items, n_items, tv);
+  note_launch(1);
+}
+
 void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, int32_t* item_of,
                      int32_t* items, unsigned int* n_items, int32_t* long_list, unsigned int* n_long,
                      unsigned long long* stats, LongQueue q, cudaStream_t s) {
@@ -1999,7 +2113,7 @@ void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, in
 }
 
 void launch_repair_tips_long(const RepairArgs& a, cudaStream_t s) {
-  RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st};
+  RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st, a.tv_exact};
   static bool attr = false;
   size_t smem = seg_smem_bytes();
   if (!attr) {
@@ -2025,7 +2139,7 @@ void launch_repair_tips_long(const RepairArgs& a, cudaStream_t s) {
 }
 
 void launch_repair_tips(const RepairArgs& a, int mode, cudaStream_t s) {
-  RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st};
+  RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st, a.tv_exact};
   k_repair_tips<<<mode ? kNumSMs : kNumSMs * 8, 32 * kTipWarps, 0, s>>>(
       c, a.items, a.n_items, a.off, a.v, a.item_list, a.item_n, a.item_state, a.item_depth, a.item_slots, a.stats,
       a.q, mode);
@@ -2033,7 +2147,7 @@ void launch_repair_tips(const RepairArgs& a, int mode, cudaStream_t s) {
 }
 
 void launch_repair_pinch(const RepairArgs& a, cudaStream_t s) {
-  RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st};
+  RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st, a.tv_exact};
   k_repair_pinch<<<kNumSMs * 4, 128, 0, s>>>(c, a.items, a.n_items, a.item_list, a.item_n, a.item_slots, a.stats);
   note_launch(1);
 }

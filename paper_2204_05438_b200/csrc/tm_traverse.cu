@@ -194,7 +194,8 @@ __global__ void __launch_bounds__(256) k_ruler_write(const int32_t* __restrict__
                                                      const int32_t* __restrict__ ent_r,
                                                      const int64_t* __restrict__ ent_base,
                                                      const int32_t* __restrict__ rdist, long long limit,
-                                                     int64_t ecap, int32_t* __restrict__ verts) {
+                                                     int64_t ecap, int32_t* __restrict__ verts,
+                                                     int32_t* __restrict__ hv) {
   int64_t E = *n_entries;
   if (E > ecap) E = ecap;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < E; k += (int64_t)gridDim.x * blockDim.x) {
@@ -203,6 +204,7 @@ __global__ void __launch_bounds__(256) k_ruler_write(const int32_t* __restrict__
     int d = rdist[g];
     for (int s = 0; s < d; s++) {
       verts[w + s] = he_origin(tri, g);
+      if (hv) hv[w + s] = g;  // the boundary half-edge of each slot (fan starts for repair)
       g = walk_next(hw, g, limit);
     }
   }
@@ -254,8 +256,8 @@ void launch_chain_emit(const int32_t* start, const int64_t* Pp, int64_t Pcap, co
 
 void launch_ruler_write(const int32_t* tri, const int32_t* hw, const int64_t* n_entries, const int32_t* ent_r,
                         const int64_t* ent_base, const int32_t* rdist, int64_t T, int64_t ecap, int32_t* verts,
-                        cudaStream_t s) {
-  k_ruler_write<<<kNumSMs * 16, 256, 0, s>>>(tri, hw, n_entries, ent_r, ent_base, rdist, 3 * T + 3, ecap, verts);
+                        int32_t* hv, cudaStream_t s) {
+  k_ruler_write<<<kNumSMs * 16, 256, 0, s>>>(tri, hw, n_entries, ent_r, ent_base, rdist, 3 * T + 3, ecap, verts, hv);
   note_launch(1);
 }
 

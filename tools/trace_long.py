@@ -10,11 +10,14 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
+WORKLOAD = os.environ.get("TRACE_WORKLOAD", "u1m")
+
+
 def run():
     import torch
     import bench
     from paper_2204_05438_b200 import _capi
-    tri = bench.load_mesh("u1m", 0)
+    tri = bench.load_mesh(WORKLOAD, 0)
     n, T = tri.n_vertices, tri.n_triangles
     xy = torch.from_numpy(tri.vertices).cuda()
     tr = torch.from_numpy(tri.triangles).cuda()
