@@ -554,7 +554,7 @@ void tm_ctx_destroy(tm_ctx* ctx) {
                  &ctx->ent_r, &ctx->ent_base, &ctx->item_of, &ctx->items, &ctx->long_list, &ctx->item_list,
                  &ctx->item_n, &ctx->item_slots, &ctx->item_state, &ctx->item_depth, &ctx->hugeq, &ctx->longq, &ctx->cnt, &ctx->slotsz, &ctx->pbase, &ctx->sbase, &ctx->pool,
                  &ctx->undo, &ctx->xy, &ctx->tri, &ctx->tri32, &ctx->hw, &ctx->max_edge, &ctx->seed, &ctx->tv,
-                 &ctx->off0, &ctx->v0, &ctx->fin_off, &ctx->fin_v, &ctx->hw_snap};
+                 &ctx->off0, &ctx->v0, &ctx->fin_off, &ctx->fin_v, &ctx->hw_snap, &ctx->hv};
   for (Buf* b : bufs) b->release();
   if (ctx->h_reset) cudaFreeHost(ctx->h_reset);
   for (auto& e : ctx->ev)

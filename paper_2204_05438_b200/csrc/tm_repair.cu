@@ -59,11 +59,11 @@ __device__ __forceinline__ int64_t palloc(const RepairCtx& c, int64_t n) {
   return (int64_t)o;
 }
 
-// both loads issued before the stores: one memory round trip
+// The packed word is (twin << 1) | frontier and the twins are known, so a
+// promotion is two plain stores -- no load, nothing to wait for.
 __device__ __forceinline__ void promote(const RepairCtx& c, int32_t e, int32_t te) {
-  const int32_t we = c.hw[e], wt = c.hw[te];
-  c.hw[e] = we | 1;
-  c.hw[te] = wt | 1;
+  c.hw[e] = (te << 1) | 1;
+  c.hw[te] = (e << 1) | 1;
 }
 
 // Per-warp bump arena carved from the pool (state held by lane 0).
@@ -95,8 +95,8 @@ __device__ __forceinline__ long long warp_alloc(const RepairCtx& c, WarpArena& a
 }
 
 __device__ __forceinline__ void demote(const RepairCtx& c, int32_t e, int32_t te) {
-  c.hw[e] &= ~1;
-  c.hw[te] &= ~1;
+  c.hw[e] = te << 1;
+  c.hw[te] = e << 1;
 }
 
 // traversal.py:112-124 for one polygon
@@ -1510,8 +1510,6 @@ __device__ bool seg_split_arcs(const RepairCtx& c, const SegView& g, const SPiec
   base = __shfl_sync(kFull, base, 0);
   if (base + need > seg_cap) return false;  // (capacity is checked per round; defensive)
   base += seg_base;
-  int32_t we = 0, wt = 0;
-  if (lane == 0) { we = c.hw[si.e]; wt = c.hw[si.te]; }  // promotion loads overlap the emission
   Seg* oa = g.segs + base;
   Seg* ob = g.segs + base + X.nseg + 4;
   int na = 0, nb = 0;
@@ -1527,8 +1525,7 @@ __device__ bool seg_split_arcs(const RepairCtx& c, const SegView& g, const SPiec
   if (lane == 0) ob[nb] = mkseg(~si.u, 1, lb - 1 - kb);
   nb = emit_range_warp(g, X, pos, kb, ob, nb + 1, lb - kb, lane);
   if (lane == 0) {
-    c.hw[si.e] = we | 1;
-    c.hw[si.te] = wt | 1;
+    promote(c, si.e, si.te);
     A->soff = base; A->nseg = na; A->len = la;
     B->soff = base + X.nseg + 4; B->nseg = nb; B->len = lb;
     if (prof) {
