@@ -454,9 +454,31 @@ __device__ int warp_collect_fan(const RepairCtx& c, int32_t v, int32_t* fan, int
 
 // reparation.py:127-145: the ((k-1)//2)-th non-frontier half-edge of the fan
 // rotated to start at the barrier half-edge (target == barrier, frontier).
+// A fan collected once can be reused while the mesh topology is unchanged (a
+// promotion only flips frontier bits): `in` supplies a cached fan (global
+// memory, in_deg entries), `out`/`out_deg` receive the collected one.
+struct FanCache {
+  const int32_t* in = nullptr;
+  int in_deg = 0;
+  int32_t* out = nullptr;
+  int* out_deg = nullptr;
+};
+
 __device__ int32_t warp_middle_internal_edge(const RepairCtx& c, int32_t v, int32_t barrier, int32_t poly,
-                                             int32_t* fan, int32_t* back, int lane, bool quiet = false) {
-  int deg = warp_collect_fan(c, v, fan, back, lane);
+                                             int32_t* fan, int32_t* back, int lane, bool quiet = false,
+                                             FanCache fc = FanCache()) {
+  int deg;
+  if (fc.in) {
+    deg = fc.in_deg;
+    fan = const_cast<int32_t*>(fc.in);
+  } else {
+    deg = warp_collect_fan(c, v, fan, back, lane);
+    if (fc.out_deg) {
+      if (deg >= 0 && deg <= kFanCap)
+        for (int k = lane; k < deg; k += 32) fc.out[k] = fan[k];
+      if (lane == 0) *fc.out_deg = (deg >= 0 && deg <= kFanCap) ? deg : -1;
+    }
+  }
   if (deg < 0) {
     if (lane == 0 && !quiet) report(c.st, K_STRUCT, poly);
     return -1;
@@ -560,8 +582,8 @@ __device__ __forceinline__ int32_t min_slot_with(const int32_t* hw, int32_t t, i
 // promote_now: also set the frontier bits of e and twin(e).  quiet: do not
 // report failures (precomputation).  Warp-uniform result.
 __device__ bool warp_split_info(const RepairCtx& c, int32_t v, int32_t b, int32_t poly, int32_t* fan, int32_t* back,
-                                int lane, bool promote_now, bool quiet, SplitInfo* out) {
-  int32_t e = warp_middle_internal_edge(c, v, b, poly, fan, back, lane, quiet);
+                                int lane, bool promote_now, bool quiet, SplitInfo* out, FanCache fc = FanCache()) {
+  int32_t e = warp_middle_internal_edge(c, v, b, poly, fan, back, lane, quiet, fc);
   if (e < 0) return false;
   SplitInfo s{};
   if (lane == 0) {
@@ -1260,7 +1282,8 @@ constexpr size_t kSegFixed = (size_t)kSegMaxL * 4 + (kSegMaxL / 32) * 4 + (size_
                              2 * (size_t)kSegRec * sizeof(SPiece) + (size_t)kSegRec * 4 +
                              2 * (size_t)kSegWarps * kFanCap * 4 + 2 * (size_t)kSegTips * 4 +
                              (size_t)kSegTips * sizeof(SplitInfo) + (size_t)kSegTouch * 4 +
-                             (kSegMaxL / 32 + 1) * 4 + 128;
+                             2 * (kSegMaxL / 32 + 1) * 4 + (size_t)kSegMaxL * 2 + (size_t)kSegTips * 4 +
+                             (size_t)kSegRec * 4 + 128;
 constexpr int kSegCap = (int)((kSmemMax - kSegFixed) / sizeof(Seg));
 size_t seg_smem_bytes() { return kSegFixed + (size_t)kSegCap * sizeof(Seg); }
 
@@ -1268,6 +1291,7 @@ struct SegView {
   const int32_t* P;
   int L;
   const uint32_t* tipbits;
+  const uint16_t* nexttip;
   const int32_t* pmap;
   int pmask;
   Seg* segs;
@@ -1307,6 +1331,19 @@ __device__ int bits_first(const uint32_t* bits, int L, int a, int cnt) {
     d += span;
   }
   return -1;
+}
+
+// first tip of P in the cyclic index range [a, a + cnt), as an offset, or -1
+// (O(1): nexttip[k] = smallest tip index >= k, 0xFFFF when none)
+__device__ __forceinline__ int next_tip(const SegView& g, int a, int cnt) {
+  int t = g.nexttip[a];
+  if (t != 0xFFFF) {
+    if (t < a + cnt) return t - a;
+    return -1;
+  }
+  if (a + cnt <= g.L) return -1;
+  t = g.nexttip[0];
+  return (t != 0xFFFF && t < a + cnt - g.L) ? t + g.L - a : -1;
 }
 
 // segment of X holding local position p (warp-uniform)
@@ -1359,7 +1396,7 @@ __device__ int seg_first_tip(const SegView& g, const SPiece& X, int lane, int* f
         best = sg.loff;
       } else {
         if (l >= 3) {
-          int d = bits_first(g.tipbits, g.L, wrapL(sg.base + 1, g.L), l - 2);
+          int d = next_tip(g, wrapL(sg.base + 1, g.L), l - 2);
           if (d >= 0) best = sg.loff + 1 + d;
         }
         if (best < 0 && l >= 2 && sval(g, sg, l - 2) == nv) best = sg.loff + l - 1;
@@ -1411,6 +1448,16 @@ __device__ int emit_range_warp(const SegView& g, const SPiece& X, int start, int
   if (cnt <= 0) return n;
   const int Lx = X.len, ns = X.nseg;
   const int s0 = seg_of(g, X, start, lane);
+  // X's segments are maximal runs of P except across X's own wrap point
+  // (segment ns-1, then segment 0): when the range crosses local position 0
+  // strictly inside and the two runs are contiguous in P, their parts merge
+  // (decided up front, so the parts are written once, in place).
+  const Seg sl = g.segs[X.soff + ns - 1], sf = g.segs[X.soff];
+  const int rj = start == 0 ? 0 : Lx - start;  // range offset of local position 0
+  const bool merge = ns > 1 && rj > 0 && rj < cnt && sl.base >= 0 && sf.base >= 0 &&
+                     wrapL(sl.base + sl.len, g.L) == sf.base && sl.len + sf.len <= g.L;
+  const int ia = ns - 1 - s0;  // part index of segment ns-1; the part starting at local 0 is ia + 1
+  const int len0 = merge ? min(s0 == 0 ? start : (int)sf.len, cnt - rj) : 0;
   int count = 0;
   for (int c0 = 0; c0 < ns; c0 += 32) {
     const int s = c0 + lane;
@@ -1424,45 +1471,25 @@ __device__ int emit_range_warp(const SegView& g, const SPiece& X, int start, int
         inc = true;
         int idx = s - s0;
         if (idx < 0) idx += ns;
-        out[n + idx] = mkseg(sg.base >= 0 ? wrapL(sg.base + skip, g.L) : sg.base, min(sg.len - skip, cnt - r0), lo + r0);
+        int len = min(sg.len - skip, cnt - r0);
+        if (merge && idx == ia) len += len0;
+        if (!(merge && idx == ia + 1))
+          out[n + idx - (merge && idx > ia + 1 ? 1 : 0)] =
+              mkseg(sg.base >= 0 ? wrapL(sg.base + skip, g.L) : sg.base, len, lo + r0);
       }
       if (s == s0 && start > sg.loff) {
         int rt = Lx - (start - sg.loff);
         if (rt < cnt) {
           tail = true;
-          out[n + ns] = mkseg(sg.base, min(start - sg.loff, cnt - rt), lo + rt);
+          if (!(merge && ns == ia + 1))
+            out[n + ns - (merge ? 1 : 0)] = mkseg(sg.base, min(start - sg.loff, cnt - rt), lo + rt);
         }
       }
     }
     count += __popc(__ballot_sync(kFull, inc)) + __popc(__ballot_sync(kFull, tail));
   }
   __syncwarp();
-  // merge the one possible contiguous pair
-  int mpos = -1;
-  for (int c0 = 1; c0 < count; c0 += 32) {
-    const int k = c0 + lane;
-    bool m = false;
-    if (k < count) {
-      const Seg a = out[n + k - 1], b = out[n + k];
-      m = a.base >= 0 && b.base >= 0 && wrapL(a.base + a.len, g.L) == b.base && a.len + b.len <= g.L;
-    }
-    unsigned bm = __ballot_sync(kFull, m);
-    if (bm && mpos < 0) mpos = c0 + __ffs(bm) - 1;
-  }
-  if (mpos < 0) return n + count;
-  const int add = out[n + mpos].len;
-  __syncwarp();
-  for (int c0 = mpos; c0 < count - 1; c0 += 32) {
-    const int k = c0 + lane;
-    Seg nx;
-    if (k < count - 1) nx = out[n + k + 1];
-    __syncwarp();
-    if (k < count - 1) out[n + k] = nx;
-    __syncwarp();
-  }
-  if (lane == 0) out[n + mpos - 1].len += add;
-  __syncwarp();
-  return n + count - 1;
+  return n + count - (merge ? 1 : 0);
 }
 
 // Arc split of piece X at tip position pos with split info si
@@ -1586,7 +1613,11 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
   SplitInfo* tipinfo = reinterpret_cast<SplitInfo*>(tipb + kSegTips);
   int32_t* tset = reinterpret_cast<int32_t*>(tipinfo + kSegTips);  // promoted-edge endpoints (hash set)
   int32_t* tiprank = tset + kSegTouch;                              // tips of P before word w
-  Seg* segs = reinterpret_cast<Seg*>(tiprank + kSegMaxL / 32 + 1);
+  int32_t* nextw = tiprank + kSegMaxL / 32 + 1;                      // first non-empty tip word >= w
+  uint16_t* nexttip = reinterpret_cast<uint16_t*>(nextw + kSegMaxL / 32 + 1);
+  int* tipdeg = reinterpret_cast<int*>(nexttip + kSegMaxL);  // cached fan sizes (-1: none)
+  int* tlist = tipdeg + kSegTips;                              // tipped records of the round
+  Seg* segs = reinterpret_cast<Seg*>(tlist + kSegRec);
   __shared__ int s_ntip, s_ntouch, s_stop, s_fail, s_ntips, s_need, s_tot;
   __shared__ long long s_base;
   __shared__ unsigned int s_w;
@@ -1624,7 +1655,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
     for (int k = threadIdx.x; k < kSegTouch; k += blockDim.x) tset[k] = -1;
     if (threadIdx.x == 0) { s_ntip = 0; s_ntouch = 0; s_fail = 0; s_stop = 1; }  // segs[0]: the item
     __syncthreads();
-    const SegView g{P, L, tipbits, pmap, pcap - 1, segs};
+    const SegView g{P, L, tipbits, nexttip, pmap, pcap - 1, segs};
     // tips of P (bitmap) and the pair map
     for (int k = threadIdx.x; k < L; k += blockDim.x) {
       int32_t a = P[k == 0 ? L - 1 : k - 1], y = P[k];
@@ -1650,6 +1681,20 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
       if (lane == 0) s_ntip = carry;
     }
     __syncthreads();
+    if (wib == 1) {  // nextw: suffix scan over the tip words (first non-empty word at or after w)
+      int carry = 0x7FFFFFFF;
+      for (int top = ((nwords + 31) & ~31) - 32; top >= 0; top -= 32) {
+        int wd = top + lane;
+        int x = (wd < nwords && tipbits[wd] != 0) ? wd : 0x7FFFFFFF;
+        for (int o = 1; o < 32; o <<= 1) {
+          int y = __shfl_down_sync(kFull, x, o);
+          if (lane + o < 32) x = min(x, y);
+        }
+        x = min(x, carry);
+        if (wd < nwords) nextw[wd] = x;
+        carry = __shfl_sync(kFull, x, 0);
+      }
+    }
     for (int k = threadIdx.x; k < L; k += blockDim.x) {
       uint32_t wbits = tipbits[k >> 5];
       if ((wbits >> (k & 31)) & 1u) {
@@ -1658,12 +1703,31 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
       }
     }
     __syncthreads();
+    for (int k = threadIdx.x; k < L; k += blockDim.x) {
+      const int wd = k >> 5;
+      const uint32_t hi = tipbits[wd] & (~0u << (k & 31));
+      int t;
+      if (hi) t = (wd << 5) + __ffs(hi) - 1;
+      else {
+        const int w2 = wd + 1 < nwords ? nextw[wd + 1] : 0x7FFFFFFF;
+        t = w2 == 0x7FFFFFFF ? 0xFFFF : (w2 << 5) + __ffs(tipbits[w2]) - 1;
+      }
+      nexttip[k] = (uint16_t)t;
+    }
+    __syncthreads();
     // every tip of the item is a tip of P (an arc split only removes the split
     // tip); its split edge depends only on the frontier around v and u
     const int ntip_pre = s_ntip < kSegTips ? s_ntip : kSegTips;
+    // fans of the tips, cached in the pool for the stale-info recomputes
+    if (threadIdx.x == 0) s_base = palloc(c, (long long)ntip_pre * kFanCap);
+    __syncthreads();
+    int32_t* fcache = s_base >= 0 ? c.pool + s_base : nullptr;
     for (int k = wib; k < ntip_pre; k += kSegWarps) {
       SplitInfo si;
-      bool ok = warp_split_info(c, tipv[k], tipb[k], i, fan, back, lane, false, true, &si);
+      FanCache fc;
+      if (fcache) { fc.out = fcache + (long long)k * kFanCap; fc.out_deg = tipdeg + k; }
+      else if (lane == 0) tipdeg[k] = -1;
+      bool ok = warp_split_info(c, tipv[k], tipb[k], i, fan, back, lane, false, true, &si, fc);
       if (lane == 0) {
         tipinfo[k] = si;
         if (!ok) tipv[k] = -1;
@@ -1702,6 +1766,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
             if (lane >= o) inc += y;
           }
           if (r < n) s_out[r] = r + carry + inc - t;
+          if (t) tlist[carry + inc - 1] = r;  // the tipped records, in order
           carry += __shfl_sync(kFull, inc, 31);
           int nd = t ? 2 * (in[r].nseg + 4) : 0;
           for (int o = 16; o > 0; o >>= 1) nd += __shfl_xor_sync(kFull, nd, o);
@@ -1738,10 +1803,8 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
       const bool tset_ok = s_ntouch <= kSegTouch / 2;  // else: always recompute
       for (int r = threadIdx.x; r < n; r += blockDim.x)
         if (in[r].ftip < 0) out[s_out[r]] = in[r];
-      int t_idx = 0;
-      for (int r = 0; r < n; r++) {
-        if (in[r].ftip < 0) continue;
-        if ((t_idx++ % kSegWarps) != wib) continue;
+      for (int t = wib; t < ntips; t += kSegWarps) {
+        const int r = tlist[t];
         const SPiece X = in[r];
         const int pos = X.ftip;
         long long ck0 = clock64();
@@ -1759,7 +1822,9 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
           use = !tset_has(tset, tv_) && !tset_has(tset, si.u);  // no promotion touched v or u
         }
         if (lane == 0) atomicAdd(dbg + (use ? 62 : 61), 1ull);
-        bool ok = use || warp_split_info(c, tv_, bv, i, fan, back, lane, false, false, &si);
+        FanCache fc;
+        if (k >= 0 && fcache && tipdeg[k] >= 0) { fc.in = fcache + (long long)k * kFanCap; fc.in_deg = tipdeg[k]; }
+        bool ok = use || warp_split_info(c, tv_, bv, i, fan, back, lane, false, false, &si, fc);
         SPiece A{0, 0, 0, -1, -1}, B{0, 0, 0, -1, -1};
         long long ck1 = clock64();
         if (ok && !seg_split_arcs(c, g, X, pos, tv_, si, &s_stop, tb, half, lane, &A, &B,
