@@ -31,6 +31,7 @@
 
 namespace tmb {
 
+constexpr unsigned kFull = 0xffffffffu;
 constexpr int kLongMin = 96;    // items longer than this go to k_repair_tips_long first
 constexpr int kHugeMin = 512;   // ... and the longest ones are dequeued first
 constexpr uint32_t F_TIP = 1u << 30;
@@ -158,31 +159,87 @@ __device__ int64_t extra_visits(const int32_t* s, int64_t n, int32_t* scratch) {
 // ------------------------------------------------------------ classify
 // Per input polygon: tip flag, repeated flag, extra visits.  Work items are the
 // polygons with a repeated vertex (a tip implies one).
+// (len - distinct) of a polygon of n <= N vertices held in registers
+template <int N>
+__device__ __forceinline__ int extra_visits_reg(const int32_t* __restrict__ s, int n) {
+  int32_t r[N];
+#pragma unroll
+  for (int k = 0; k < N; k++) r[k] = k < n ? __ldg(s + k) : (int32_t)(0x80000000u + (uint32_t)k);
+  int ex = 0;
+#pragma unroll
+  for (int k = 1; k < N; k++) {
+    bool dup = false;
+#pragma unroll
+    for (int q = 0; q < k; q++) dup |= r[q] == r[k];
+    ex += dup;
+  }
+  return ex;
+}
+
+// Block-aggregated append: one global atomic per block and list instead of
+// one per element (a single hot counter serialises thousands of returning
+// atomics).  All threads of the block must call it.
+__device__ __forceinline__ int block_append(bool want, unsigned int* counter, int* s_cnt, unsigned int* s_base) {
+  const int lane = threadIdx.x & 31;
+  const unsigned m = __ballot_sync(kFull, want);
+  int wbase = 0;
+  if (lane == 0 && m) wbase = atomicAdd(s_cnt, __popc(m));
+  wbase = __shfl_sync(kFull, wbase, 0);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int c = *s_cnt;
+    *s_cnt = 0;  // ready for the next call (its adds follow the barrier below)
+    *s_base = c ? atomicAdd(counter, (unsigned)c) : 0u;
+  }
+  __syncthreads();
+  return want ? (int)*s_base + wbase + __popc(m & ((1u << lane) - 1u)) : -1;
+}
+
 __global__ void __launch_bounds__(256) k_classify(const int64_t* __restrict__ off, const int32_t* __restrict__ v,
                                                   const int64_t* __restrict__ Pp, int32_t* __restrict__ item_of,
                                                   int32_t* __restrict__ items, unsigned int* n_items,
                                                   int32_t* __restrict__ long_list, unsigned int* n_long,
                                                   unsigned long long* stats) {
+  __shared__ int s_cnt;
+  __shared__ unsigned int s_base;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
   const int64_t P = *Pp;
   unsigned long long extra_sum = 0, rep_cnt = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t b = off[i], n = off[i + 1] - b;
-    item_of[i] = -1;
-    if (n > 48) {
-      long_list[atomicAdd(n_long, 1u)] = (int32_t)i;
-      continue;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < P; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    bool is_long = false, is_item = false;
+    if (i < P) {
+      int64_t b = off[i], n = off[i + 1] - b;
+      item_of[i] = -1;
+      if (n > 48) {
+        is_long = true;
+      } else {
+        // registers: all loads in flight at once, compares without reloads
+        const int64_t ex = n <= 16 ? extra_visits_reg<16>(v + b, (int)n) : extra_visits_reg<48>(v + b, (int)n);
+        if (ex > 0) {
+          extra_sum += ex;
+          rep_cnt++;
+          is_item = true;
+        }
+      }
     }
-    int64_t ex = extra_visits(v + b, n, nullptr);
-    if (ex > 0) {
-      extra_sum += ex;
-      rep_cnt++;
-      unsigned int k = atomicAdd(n_items, 1u);
-      items[k] = (int32_t)i;
-      item_of[i] = (int32_t)k;
+    const int pl = block_append(is_long, n_long, &s_cnt, &s_base);
+    if (is_long) long_list[pl] = (int32_t)i;
+    const int pi = block_append(is_item, n_items, &s_cnt, &s_base);
+    if (is_item) {
+      items[pi] = (int32_t)i;
+      item_of[i] = pi;
     }
   }
-  if (extra_sum) atomicAdd(stats + 2, extra_sum);
-  if (rep_cnt) atomicAdd(stats + 6, rep_cnt);
+  for (int o = 16; o > 0; o >>= 1) {
+    extra_sum += __shfl_xor_sync(kFull, extra_sum, o);
+    rep_cnt += __shfl_xor_sync(kFull, rep_cnt, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (extra_sum) atomicAdd(stats + 2, extra_sum);
+    if (rep_cnt) atomicAdd(stats + 6, rep_cnt);
+  }
 }
 
 // long polygons: one block each; distinct vertices counted with a shared-memory
@@ -316,7 +373,6 @@ __device__ int rewalk_split(const RepairCtx& c, int32_t e, int32_t te, int64_t p
 // One warp cooperates on one piece.  Lanes split O(len) scans and copies; the
 // sequential mesh rotations run on one or two lanes and are broadcast.  All
 // control flow below is warp-uniform.
-constexpr unsigned kFull = 0xffffffffu;
 constexpr int kFanCap = 64;
 constexpr int kTipWarps = 4;  // warps per block of k_repair_tips
 
