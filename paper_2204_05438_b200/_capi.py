@@ -134,8 +134,8 @@ class Context:
         return {lib().tm_segment_name(k).decode(): (ms[k], int(cnt[k])) for k in range(n)}
 
     def debug(self):
-        out = (ctypes.c_uint64 * 64)()
-        lib().tm_ctx_debug(self.ptr, out, 64)
+        out = (ctypes.c_uint64 * 128)()
+        lib().tm_ctx_debug(self.ptr, out, 128)
         return list(out)
 
     def last_error(self) -> str:

@@ -55,10 +55,10 @@ struct Counters {
   int64_t p_out;       // P': polygons after repair
   int64_t f_out;       // F': vertex slots after repair
   unsigned int n_overflow, n_items, n_long, pad;
-  unsigned int q_huge, q_long, q_next, pad2;
+  unsigned int q_huge, q_long, q_next, n_parked;
   unsigned long long pool_top, undo_top;
   unsigned long long stats[8];
-  unsigned long long dbg[64];  // optional kernel timestamps (tm_ctx_debug)
+  unsigned long long dbg[128];  // optional kernel timestamps / counters (tm_ctx_debug)
 };
 
 enum Seg {
@@ -115,7 +115,7 @@ struct tm_ctx {
   Buf seeds, start, len, overflow, queue, stamp, tiles, nrul, eoff, rnext, rdist, startbits, ent_r, ent_base;
   // repair
   Buf item_of, items, long_list, item_list, item_n, item_slots, item_state, item_depth, cnt, slotsz, pbase, sbase, pool,
-      undo, hugeq, longq;
+      undo, hugeq, longq, parked;
   // whole-path buffers
   Buf xy, tri, tri32, hw, max_edge, seed, tv, off0, v0, fin_off, fin_v, hw_snap, hv;
   cudaStream_t gstream = nullptr;
@@ -327,6 +327,7 @@ static int prepare(tm_ctx* ctx, int64_t T, int64_t n = -1) {
   ENSURE(item_state, Tn * sizeof(int32_t));
   ENSURE(item_depth, Tn * sizeof(int32_t));
   ENSURE(hugeq, Tn * sizeof(int32_t));
+  ENSURE(parked, Tn * sizeof(int32_t));
   ENSURE(longq, Tn * sizeof(int32_t));
   ENSURE(cnt, (Tn + 1) * sizeof(int64_t));
   ENSURE(slotsz, (Tn + 1) * sizeof(int64_t));
@@ -429,7 +430,8 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
   Counters* dc = dc_of(ctx);
   int64_t Tn = T > 0 ? T : 1;
   int64_t* tiles = ctx->tiles.as<int64_t>();
-  LongQueue q{ctx->hugeq.as<int32_t>(), ctx->longq.as<int32_t>(), &dc->q_huge, &dc->q_long, &dc->q_next};
+  LongQueue q{ctx->hugeq.as<int32_t>(), ctx->longq.as<int32_t>(), &dc->q_huge,        &dc->q_long,
+              &dc->q_next,           ctx->parked.as<int32_t>(), &dc->n_parked};
   {
     SegTimer t_(ctx, S_CLASSIFY, s);
     launch_classify(d_off_in, d_v_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(), &dc->n_items,
@@ -457,6 +459,10 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
     }
     launch_repair_tips_long(a, sl);
     launch_repair_tips(a, 0, s);
+    {
+      SegTimer t_(ctx, S_REPAIR_PINCH, s);
+      launch_repair_pinch(a, 0, s);  // short items' pinch pass, still beside the long items
+    }
     if (!serial) {
       CK(cudaEventRecord(ctx->ev_join, ctx->aux));
       CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
@@ -465,7 +471,7 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
   }
   {
     SegTimer t_(ctx, S_REPAIR_PINCH, s);
-    launch_repair_pinch(a, s);
+    launch_repair_pinch(a, 1, s);
   }
   {
     SegTimer t_(ctx, S_STITCH, s);
@@ -552,7 +558,7 @@ void tm_ctx_destroy(tm_ctx* ctx) {
   Buf* bufs[] = {&ctx->counters, &ctx->slots, &ctx->seeds, &ctx->start, &ctx->len, &ctx->overflow, &ctx->queue,
                  &ctx->stamp, &ctx->tiles, &ctx->nrul, &ctx->eoff, &ctx->rnext, &ctx->rdist, &ctx->startbits,
                  &ctx->ent_r, &ctx->ent_base, &ctx->item_of, &ctx->items, &ctx->long_list, &ctx->item_list,
-                 &ctx->item_n, &ctx->item_slots, &ctx->item_state, &ctx->item_depth, &ctx->hugeq, &ctx->longq, &ctx->cnt, &ctx->slotsz, &ctx->pbase, &ctx->sbase, &ctx->pool,
+                 &ctx->item_n, &ctx->item_slots, &ctx->item_state, &ctx->item_depth, &ctx->hugeq, &ctx->longq, &ctx->parked, &ctx->cnt, &ctx->slotsz, &ctx->pbase, &ctx->sbase, &ctx->pool,
                  &ctx->undo, &ctx->xy, &ctx->tri, &ctx->tri32, &ctx->hw, &ctx->max_edge, &ctx->seed, &ctx->tv,
                  &ctx->off0, &ctx->v0, &ctx->fin_off, &ctx->fin_v, &ctx->hw_snap, &ctx->hv};
   for (Buf* b : bufs) b->release();
@@ -604,7 +610,7 @@ int64_t tm_launch_count(void) { return g_launches.load(); }
 // debug timestamps written by kernels into Counters.dbg during the last run
 int tm_ctx_debug(const tm_ctx* ctx, uint64_t* out, int n) {
   if (!ctx || !ctx->h_result) return TM_ERR_ARGUMENT;
-  for (int k = 0; k < n && k < 64; k++) out[k] = ctx->h_result->dbg[k];
+  for (int k = 0; k < n && k < 128; k++) out[k] = ctx->h_result->dbg[k];
   return TM_OK;
 }
 

@@ -57,6 +57,8 @@ struct LongQueue {       // work items longer than kLongMin, longest class first
   unsigned int* n_huge;
   unsigned int* n_long;
   unsigned int* next;
+  int32_t* parked;         // short items whose pinch pass waits for the global guard
+  unsigned int* n_parked;
 };
 struct RepairArgs {
   const int32_t* tri;
@@ -93,7 +95,10 @@ void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, in
 void launch_repair_tips_long(const RepairArgs& a, cudaStream_t s);
 // mode 0: items of length <= kLongMin; mode 1: long items handed back (state 2/3)
 void launch_repair_tips(const RepairArgs& a, int mode, cudaStream_t s);
-void launch_repair_pinch(const RepairArgs& a, cudaStream_t s);
+// mode 0: short items, beside the long-item kernel, under the extra visits known
+// so far (a lower bound of the global guard; items reaching it are parked);
+// mode 1: long items and parked ones, under the global guard
+void launch_repair_pinch(const RepairArgs& a, int mode, cudaStream_t s);
 void launch_out_counts(const int64_t* off, const int64_t* Pp, int64_t Pcap, const int32_t* item_of,
                        const int32_t* item_n, const int64_t* item_slots, int64_t* cnt, int64_t* slots,
                        const unsigned long long* stats, DevStatus* st, cudaStream_t s);

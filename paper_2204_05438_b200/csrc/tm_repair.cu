@@ -52,6 +52,7 @@ struct RepairCtx {
   unsigned long long undo_cap;
   DevStatus* st;
   int tv_exact;       // tv is the reference trivertex (lowest incident triangle, mesh_core.py:171-178)
+  unsigned long long* dbg;  // debug counters (tm_ctx_debug), may be null
 };
 
 __device__ __forceinline__ int64_t palloc(const RepairCtx& c, int64_t n) {
@@ -735,7 +736,10 @@ __device__ bool warp_split_tip(const RepairCtx& c, const int32_t* X, int L, int3
 // pool scratch, so long pieces cost O(n), not O(n^2).  Returns the extra
 // visits (n - distinct); *p1/*p2 = the first repeated position p2 and the
 // first occurrence p1 of its value (-1 when none).
-__device__ int warp_dup_scan(const RepairCtx& c, const int32_t* s, int n, int lane, int* p1, int* p2) {
+constexpr int kDupCap = 512;         // per-warp shared table in k_repair_tips (pieces up to 256 vertices)
+constexpr int kPinchDupCap = 4096;   // per-warp shared table in k_repair_pinch (pieces up to 2048 vertices)
+__device__ int warp_dup_scan(const RepairCtx& c, const int32_t* s, int n, int lane, int* p1, int* p2,
+                             int2* stab = nullptr, int scap = kDupCap) {
   if (n <= 64) {
     int extra = 0, q2 = -1, q1 = -1;
     for (int pb = 0; pb < n; pb += 32) {
@@ -759,19 +763,23 @@ __device__ int warp_dup_scan(const RepairCtx& c, const int32_t* s, int n, int la
   }
   int cap = 64;
   while (cap < 2 * n) cap <<= 1;
-  long long o = 0;
-  if (lane == 0) {
-    o = palloc(c, 2 * (long long)cap + 1);
-    if (o >= 0) o = (o + 1) & ~1LL;  // int2 alignment
+  const bool shared = stab != nullptr && cap <= scap;
+  int2* tab = stab;
+  if (!shared) {
+    long long o = 0;
+    if (lane == 0) {
+      o = palloc(c, 2 * (long long)cap + 1);
+      if (o >= 0) o = (o + 1) & ~1LL;  // int2 alignment
+    }
+    o = __shfl_sync(kFull, o, 0);
+    if (o < 0) {  // pool exhausted: quadratic fallback
+      if (lane == 0) report(c.st, K_POOL, -1);
+      if (p1) *p1 = -1;
+      if (p2) *p2 = -1;
+      return warp_extra_visits(s, n, lane);
+    }
+    tab = reinterpret_cast<int2*>(c.pool + o);
   }
-  o = __shfl_sync(kFull, o, 0);
-  if (o < 0) {  // pool exhausted: quadratic fallback
-    if (lane == 0) report(c.st, K_POOL, -1);
-    if (p1) *p1 = -1;
-    if (p2) *p2 = -1;
-    return warp_extra_visits(s, n, lane);
-  }
-  int2* tab = reinterpret_cast<int2*>(c.pool + o);
   for (int k = lane; k < cap; k += 32) tab[k] = make_int2(-1, 0x7FFFFFFF);
   __syncwarp();
   for (int p = lane; p < n; p += 32) {
@@ -792,7 +800,7 @@ __device__ int warp_dup_scan(const RepairCtx& c, const int32_t* s, int n, int la
       int32_t x = s[p];
       uint32_t slot = ((uint32_t)x * 0x9E3779B1u) & (cap - 1);
       for (;;) {
-        int2 e = __ldcg(&tab[slot]);
+        int2 e = shared ? tab[slot] : __ldcg(&tab[slot]);
         if (e.x == x) { first = e.y; break; }
         slot = (slot + 1) & (cap - 1);
       }
@@ -982,9 +990,11 @@ __device__ int32_t trivertex_he(const RepairCtx& c, int32_t v, int guard) {
 // reference order, each trial-split until one keeps.  Every lane runs the
 // (identical) candidate enumeration so the trials stay warp-convergent.
 __device__ int warp_pinch_split(const RepairCtx& c, const int32_t* X, int L, int32_t poly, int lane, int32_t** A,
-                                int* la, int32_t** B, int* lb) {
+                                int* la, int32_t** B, int* lb, int2* stab) {
+  long long ck0 = clock64();
   int p1 = -1, p2 = -1;  // first repeated vertex (reparation.py:184-189)
-  warp_dup_scan(c, X, L, lane, &p1, &p2);
+  warp_dup_scan(c, X, L, lane, &p1, &p2, stab, kPinchDupCap);
+  if (c.dbg && lane == 0) { atomicAdd(c.dbg + 64, (unsigned long long)(clock64() - ck0)); atomicMax(c.dbg + 70, (unsigned long long)L); }
   if (p2 < 0) return 0;
   const int32_t v = X[p2];
   const int guard = (int)(3 * c.T + 3 < (1LL << 30) ? 3 * c.T + 3 : (1LL << 30));
@@ -1031,7 +1041,9 @@ __device__ int warp_pinch_split(const RepairCtx& c, const int32_t* X, int L, int
       if (ord == mid) continue;
       int32_t cand = gout;
       for (int st = 0; st <= idx; st++) cand = fan_step(c.hw, cand, guard);
+      long long ckt = clock64();
       int r = warp_try_pinch_arc(c, cand, X, L, poly, lane, A, la, B, lb);
+      if (c.dbg && lane == 0) { atomicAdd(c.dbg + 65, (unsigned long long)(clock64() - ckt)); atomicAdd(c.dbg + 66, 1ull); }
       if (r != 0) return r;
     }
   }
@@ -1046,7 +1058,9 @@ __device__ int warp_pinch_split(const RepairCtx& c, const int32_t* X, int L, int
     int cnt = 0;
     do {
       if (!hw_front(c.hw[g])) {
+        long long ckt = clock64();
         int r = warp_try_pinch_arc(c, g, X, L, poly, lane, A, la, B, lb);
+        if (c.dbg && lane == 0) { atomicAdd(c.dbg + 65, (unsigned long long)(clock64() - ckt)); atomicAdd(c.dbg + 67, 1ull); }
         if (r != 0) return r;
       }
       g = fan_step(c.hw, g, guard);
@@ -1060,12 +1074,22 @@ __device__ int warp_pinch_split(const RepairCtx& c, const int32_t* X, int L, int
 }
 
 // Pinch rounds of item w (record list in the pool) and its output totals.
+// Rounds r0, r0+1, ... of item w under `guard`.  With `park`, guard is only a
+// lower bound of the global one (the extra visits summed so far): reaching it
+// with pinched pieces left parks the item (state 4, next round in item_depth)
+// for the final pass instead of ending its loop.
+struct PinchPark {
+  int32_t* item_state = nullptr;
+  int32_t* item_depth = nullptr;
+  int32_t* list = nullptr;
+  unsigned int* n = nullptr;
+};
 __device__ void warp_finish_pinch(const RepairCtx& c, int64_t w, int32_t poly, long long list, int n, int lane,
                                   int64_t* item_list, int32_t* item_n, int64_t* item_slots,
-                                  unsigned long long* stats, long long guard) {
-  const int n0 = n;
+                                  unsigned long long* stats, long long guard, int2* stab, long long r0 = 0,
+                                  PinchPark park = PinchPark()) {
   bool ok = true, truncated = false;
-  for (long long r = 0; ok; r++) {
+  for (long long r = r0; ok; r++) {
     int elig = 0;
     for (int k0 = 0; k0 < n; k0 += 32) {
       int k = k0 + lane;
@@ -1077,8 +1101,18 @@ __device__ void warp_finish_pinch(const RepairCtx& c, int64_t w, int32_t poly, l
       elig += __popc(__ballot_sync(kFull, e));
     }
     if (elig == 0) break;
-    if (r >= guard) {  // the reference's loop ends here with pinched polygons left
-      truncated = true;
+    if (r >= guard) {
+      if (park.list) {  // whether the global guard allows round r is not known yet
+        if (lane == 0) {
+          item_list[w] = list;
+          item_n[w] = n;
+          park.item_depth[w] = (int32_t)r;
+          park.item_state[w] = 4;
+          park.list[atomicAdd(park.n, 1u)] = (int32_t)w;
+        }
+        return;
+      }
+      truncated = true;  // the reference's loop ends here with pinched polygons left
       break;
     }
     long long nl = 0;
@@ -1095,11 +1129,15 @@ __device__ void warp_finish_pinch(const RepairCtx& c, int64_t w, int32_t poly, l
       if ((rl & F_REP) && !(rl & F_TIP) && !(rl & F_FAIL)) {
         int32_t *A, *B;
         int al, bl;
-        int res = warp_pinch_split(c, c.pool + ro, (int)(rl & LEN_MASK), poly, lane, &A, &al, &B, &bl);
+        long long cks = clock64();
+        int res = warp_pinch_split(c, c.pool + ro, (int)(rl & LEN_MASK), poly, lane, &A, &al, &B, &bl, stab);
+        if (c.dbg && lane == 0) { atomicAdd(c.dbg + 68, (unsigned long long)(clock64() - cks)); atomicAdd(c.dbg + 69, 1ull); }
         if (res < 0) { ok = false; break; }
         if (res == 1) {
-          uint32_t fa = warp_tip_flag(A, al, lane) | (warp_dup_scan(c, A, al, lane, nullptr, nullptr) > 0 ? F_REP : 0u);
-          uint32_t fb = warp_tip_flag(B, bl, lane) | (warp_dup_scan(c, B, bl, lane, nullptr, nullptr) > 0 ? F_REP : 0u);
+          long long ckf = clock64();
+          uint32_t fa = warp_tip_flag(A, al, lane) | (warp_dup_scan(c, A, al, lane, nullptr, nullptr, stab, kPinchDupCap) > 0 ? F_REP : 0u);
+          uint32_t fb = warp_tip_flag(B, bl, lane) | (warp_dup_scan(c, B, bl, lane, nullptr, nullptr, stab, kPinchDupCap) > 0 ? F_REP : 0u);
+          if (c.dbg && lane == 0) atomicAdd(c.dbg + 71, (unsigned long long)(clock64() - ckf));
           if (lane == 0) {
             c.pool[nl + 2 * m] = (int32_t)(A - c.pool);
             c.pool[nl + 2 * m + 1] = (int32_t)((uint32_t)al | fa);
@@ -1122,6 +1160,7 @@ __device__ void warp_finish_pinch(const RepairCtx& c, int64_t w, int32_t poly, l
     if (!ok) break;
     list = nl;
     n = m;
+    if (did && lane == 0) atomicAdd(stats + 4, (unsigned long long)did);
     if (did == 0) break;
   }
   if (!ok) {
@@ -1147,7 +1186,6 @@ __device__ void warp_finish_pinch(const RepairCtx& c, int64_t w, int32_t poly, l
     item_n[w] = n;
     item_slots[w] = slots;
     if (unrep) atomicAdd(stats + 3, unrep);
-    if (n != n0) atomicAdd(stats + 4, (unsigned long long)(n - n0));
     if (truncated) atomicAdd(stats + 7, 1ull);
   }
 }
@@ -1157,12 +1195,12 @@ __device__ void warp_finish_pinch(const RepairCtx& c, int64_t w, int32_t poly, l
 // memory kernel, 2 = resume from item_list/item_n/item_depth in the pool.
 
 __device__ void finish_item(const RepairCtx& c, int64_t w, long long list, int n, long long depth, long long splits,
-                            int lane, int64_t* item_list, int32_t* item_n, unsigned long long* stats) {
+                            int lane, int64_t* item_list, int32_t* item_n, unsigned long long* stats, int2* stab) {
   // repeated flags and extra visits of the leaves (pinch guard, reparation.py:322)
   unsigned long long ex_sum = 0;
   for (int r = 0; r < n; r++) {
     uint32_t ro = (uint32_t)c.pool[list + 2 * r], rl = (uint32_t)c.pool[list + 2 * r + 1];
-    int ex = warp_dup_scan(c, c.pool + ro, (int)(rl & LEN_MASK), lane, nullptr, nullptr);
+    int ex = warp_dup_scan(c, c.pool + ro, (int)(rl & LEN_MASK), lane, nullptr, nullptr, stab);
     if (ex > 0 && lane == 0) c.pool[list + 2 * r + 1] = (int32_t)(rl | F_REP);
     ex_sum += ex;
   }
@@ -1190,6 +1228,7 @@ __global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, con
                                                                 unsigned long long* stats, LongQueue q, int mode) {
   __shared__ int32_t s_fan[kTipWarps][kFanCap];
   __shared__ int32_t s_back[kTipWarps][kFanCap];
+  __shared__ int2 s_dup[kTipWarps][kDupCap];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   int32_t* fan = s_fan[wib];
   int32_t* back = s_back[wib];
@@ -1294,7 +1333,7 @@ __global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, con
       if (lane == 0) { item_list[w] = -1; item_n[w] = 0; item_slots[w] = 0; }
       continue;
     }
-    finish_item(c, w, list, n, depth, splits, lane, item_list, item_n, stats);
+    finish_item(c, w, list, n, depth, splits, lane, item_list, item_n, stats, s_dup[wib]);
   }
 }
 
@@ -2060,21 +2099,44 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
 
 // ------------------------------------------------------------ pinch pass
 __global__ void __launch_bounds__(128) k_repair_pinch(RepairCtx c, const int32_t* __restrict__ items,
-                                                      const unsigned int* n_items, int64_t* __restrict__ item_list,
-                                                      int32_t* __restrict__ item_n, int64_t* __restrict__ item_slots,
-                                                      unsigned long long* stats) {
+                                                      const unsigned int* n_items, const int64_t* __restrict__ off,
+                                                      int64_t* __restrict__ item_list, int32_t* __restrict__ item_n,
+                                                      int64_t* __restrict__ item_slots,
+                                                      int32_t* __restrict__ item_state,
+                                                      int32_t* __restrict__ item_depth, LongQueue q,
+                                                      unsigned long long* stats, int mode) {
+  extern __shared__ int2 s_pdup[];  // [4][kPinchDupCap]
   const int lane = threadIdx.x & 31;
-  const unsigned int ni = *n_items;
-  const long long guard = (long long)stats[5] + 1;
+  int2* stab = s_pdup + (threadIdx.x >> 5) * kPinchDupCap;
+  const long long guard = (long long)*(volatile unsigned long long*)(stats + 5) + 1;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t w = warp; w < ni; w += nwarps) {
+  if (mode == 0) {
+    PinchPark park{item_state, item_depth, q.parked, q.n_parked};
+    const unsigned int ni = *n_items;
+    for (int64_t w = warp; w < ni; w += nwarps) {
+      const int32_t i = items[w];
+      if (off[i + 1] - off[i] > kLongMin) continue;  // long item: mode 1
+      const long long list = item_list[w];
+      if (list < 0) {
+        if (lane == 0) item_slots[w] = 0;
+        continue;
+      }
+      warp_finish_pinch(c, w, i, list, item_n[w], lane, item_list, item_n, item_slots, stats, guard, stab, 0, park);
+    }
+    return;
+  }
+  const unsigned int nh = *q.n_huge, nl = *q.n_long, np = *q.n_parked;
+  for (int64_t k = warp; k < nh + nl + np; k += nwarps) {
+    const int64_t w = k < nh ? q.huge[k] : k < nh + nl ? q.longq[k - nh] : q.parked[k - nh - nl];
+    const bool parked = k >= nh + nl;
     const long long list = item_list[w];
     if (list < 0) {
       if (lane == 0) item_slots[w] = 0;
       continue;
     }
-    warp_finish_pinch(c, w, items[w], list, item_n[w], lane, item_list, item_n, item_slots, stats, guard);
+    warp_finish_pinch(c, w, items[w], list, item_n[w], lane, item_list, item_n, item_slots, stats, guard, stab,
+                      parked ? item_depth[w] : 0);
   }
 }
 
@@ -2231,7 +2293,8 @@ void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, in
 }
 
 void launch_repair_tips_long(const RepairArgs& a, cudaStream_t s) {
-  RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st, a.tv_exact};
+  RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st, a.tv_exact,
+              a.dbg};
   static bool attr = false;
   size_t smem = seg_smem_bytes();
   if (!attr) {
@@ -2257,16 +2320,26 @@ void launch_repair_tips_long(const RepairArgs& a, cudaStream_t s) {
 }
 
 void launch_repair_tips(const RepairArgs& a, int mode, cudaStream_t s) {
-  RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st, a.tv_exact};
+  RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st, a.tv_exact,
+              a.dbg};
   k_repair_tips<<<mode ? kNumSMs : kNumSMs * 8, 32 * kTipWarps, 0, s>>>(
       c, a.items, a.n_items, a.off, a.v, a.item_list, a.item_n, a.item_state, a.item_depth, a.item_slots, a.stats,
       a.q, mode);
   note_launch(1);
 }
 
-void launch_repair_pinch(const RepairArgs& a, cudaStream_t s) {
-  RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st, a.tv_exact};
-  k_repair_pinch<<<kNumSMs * 4, 128, 0, s>>>(c, a.items, a.n_items, a.item_list, a.item_n, a.item_slots, a.stats);
+void launch_repair_pinch(const RepairArgs& a, int mode, cudaStream_t s) {
+  RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st, a.tv_exact,
+              a.dbg};
+  static bool attr = false;
+  const size_t smem = 4 * kPinchDupCap * sizeof(int2);
+  if (!attr) {
+    cudaFuncSetAttribute(k_repair_pinch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_repair_pinch<<<mode ? kNumSMs : kNumSMs * 2, 128, smem, s>>>(c, a.items, a.n_items, a.off, a.item_list, a.item_n,
+                                                                  a.item_slots, a.item_state, a.item_depth, a.q,
+                                                                  a.stats, mode);
   note_launch(1);
 }
 

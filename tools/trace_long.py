@@ -41,6 +41,9 @@ if __name__ == "__main__":
         qi, depth, dur = slow & 0xFFFF, (slow >> 16) & 0xFFFF, (slow >> 32) / 10.0
         print(f"slowest long item: qi={qi} depth={depth} {dur:.1f} us; split infos stale={d[61]} reused={d[62]} "
               f"re-walk fallbacks={d[63]}")
+        print(f"pinch kernel: slowest item {d[48]} cycles, all items {d[49]} cycles")
+        print(f"  pinch splits attempted {d[69]} ({d[68]} cyc), first-repeat scans {d[64]} cyc (max L {d[70]}), "
+              f"trials wedge {d[66]} + inner {d[67]} ({d[65]} cyc), piece flags {d[71]} cyc")
         env = dict(os.environ, TERMESH_TRACE_QI=str(qi))
         subprocess.run([sys.executable, __file__, "--child"], env=env, check=True)
     else:
