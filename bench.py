@@ -124,8 +124,8 @@ def algorithmic_bytes(n, T, F, P, Fp, Pp):
     array touched once in its device dtype.  R = rulers = seeds + F/8."""
     R = P + F // 8
     return {
-        # pass A: tri i64 in, xy gathers, tri32 + max_edge + trivertex out, 1.5 ascending keys (8 B) in the twin table
-        "label_a_tri_pass": 24 * T + 16 * n + 12 * T + 1 * T + 4 * n + 12 * T,
+        # pass A: tri i64 in, xy gathers, tri32 + max_edge out, 1.5 ascending keys (8 B) into the twin table
+        "label_a_tri_pass": 24 * T + 16 * n + 12 * T + 1 * T + 12 * T,
         # pass B: tri32 + max_edge in, 1.5 key probes, packed half-edge words + seeds out
         "label_b_edges": 12 * T + 1 * T + 12 * T + 12 * T + 1 * T,
         "select_seeds": 1 * T + 4 * P,
@@ -238,8 +238,20 @@ def run_gpu(args, rank, world, local_rank):
     dom_hbm = max(hbm_kernels, key=lambda k: kernels[k]["ms"]) if hbm_kernels else None
     d = kernels.get(dom_hbm, {})
     achieved = d.get("gbs") or 0.0
+    # DRAM bytes per launch of the roofline kernel from the committed ncu --set full capture
+    # (tools/ncu_summary.py -> profiles/ncu_traffic.json), same workload, or null
+    traffic, traffic_src = None, None
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[args.workload][dom_hbm]
+        traffic, traffic_src = t["dram_bytes"], f"profiles/{t['source']} (ncu, {t['kernel']})"
+    except Exception:
+        pass
+    dram_gbs = round(traffic / (d["ms"] / 1e3) / 1e9, 1) if traffic and d.get("ms") else None
     roofline = {"bound": "hbm", "kernel": dom_hbm, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4) if peak else None, "traffic": None,
+                "frac": round(achieved / peak, 4) if peak else None, "traffic": traffic,
+                "algorithmic_bytes": d.get("alg_bytes"), "traffic_source": traffic_src,
+                # the DRAM bytes the kernel actually moves (random sectors of the gathers) over its time
+                "dram_achieved": dram_gbs, "dram_frac": round(dram_gbs / peak, 4) if dram_gbs and peak else None,
                 "peak_source": peak_src, "dominant_by_time": dom,
                 "note": "dominant HBM kernel; repair_tips is latency-bound (no byte roofline)"}
 
@@ -319,7 +331,7 @@ def run_reference(args, rank, world):
     s = statistics.mean(times)
     v = round(tri.n_triangles / s, 1)
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(s * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": round(s * 1e3, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "int64/f64", "data": "synthetic",
             "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"],
                        "triangles": tri.n_triangles},

@@ -61,6 +61,8 @@ struct Counters {
   unsigned long long dbg[128];  // optional kernel timestamps / counters (tm_ctx_debug)
 };
 
+constexpr int kUploadChunks = 8;  // triangle upload chunks of tm_mesh_to_polygons_host
+
 enum Seg {
   S_LABEL_A, S_LABEL_B, S_SEEDS, S_TRAV_START, S_TRAV_RULERS, S_TRAV_LEN, S_TRAV_SCAN, S_TRAV_WRITE,
   S_CLASSIFY, S_REPAIR_TIPS, S_REPAIR_PINCH, S_STITCH, S_NUM
@@ -85,11 +87,11 @@ struct GraphKey {
   void* off = nullptr;
   void* v = nullptr;
   int64_t n = -1, T = -1, tb = 0, te = 0;
-  int bits = 0, check = 0;
+  int bits = 0, check = 0, ext = 0;
   unsigned long long pool_cap = 0;
   bool operator==(const GraphKey& o) const {
     return xy == o.xy && tri == o.tri && off == o.off && v == o.v && n == o.n && T == o.T && tb == o.tb &&
-           te == o.te && bits == o.bits && check == o.check && pool_cap == o.pool_cap;
+           te == o.te && bits == o.bits && check == o.check && ext == o.ext && pool_cap == o.pool_cap;
   }
 };
 
@@ -132,6 +134,11 @@ struct tm_ctx {
   // whole-path runs: the traversal records each slot's boundary half-edge
   // (hv) and repair derives its fan starts from it instead of a trivertex
   int32_t* path_hv = nullptr;
+  // host-array runs: counters reset and label pass A were enqueued by the
+  // caller, chunk by chunk behind the triangle upload (copy/compute overlap)
+  bool label_a_external = false;
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t chunk_ev[kUploadChunks] = {};
   long long graph_kernels = 0;  // kernels per graph replay (counted at capture)
 };
 
@@ -349,7 +356,7 @@ static int enqueue_label(tm_ctx* ctx, const double* d_xy, int64_t n, const void*
                          int check, int32_t* d_tri32, int32_t* d_hw, int8_t* d_me, uint8_t* d_seed, int32_t* d_tv,
                          cudaStream_t s) {
   Counters* dc = dc_of(ctx);
-  {
+  if (!ctx->label_a_external) {
     SegTimer t_(ctx, S_LABEL_A, s);
     launch_label_a(d_xy, n, d_tri, tri_bits == 64, T, check, d_tri32, d_hw, d_me, d_seed, d_tv, ctx->slots.p,
                    &dc->st, s);
@@ -570,6 +577,9 @@ void tm_ctx_destroy(tm_ctx* ctx) {
   prof_flush(ctx);
   for (auto e : ctx->prof.free_ev) cudaEventDestroy(e);
   if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+  if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
+  for (auto e : ctx->chunk_ev)
+    if (e) cudaEventDestroy(e);
   if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
   delete ctx;
 }
@@ -744,9 +754,8 @@ int tm_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, const int32_t*
 // given set of pointers/sizes) on the context's stream, ordered after the
 // caller's stream by events.  With profiling on, launches go to the caller's
 // stream one by one so each kernel group can be timed.
-static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_tri, int tri_bits, int64_t T,
-                      int check, int64_t* d_off, int32_t* d_v, int64_t* n_polys, int64_t* n_slots, int64_t* stats,
-                      cudaStream_t user) {
+// scratch and whole-path buffers for a mesh of n vertices / T triangles
+static int path_buffers(tm_ctx* ctx, int64_t n, int64_t T) {
   int rc = check_sizes(ctx, n, T);
   if (rc || (rc = prepare(ctx, T, n))) return rc;
   int64_t Tn = T > 0 ? T : 1, nn = n > 0 ? n : 1;
@@ -758,6 +767,14 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
   ENSURE(off0, (Tn + 1) * sizeof(int64_t));
   ENSURE(v0, 3 * Tn * sizeof(int32_t));
   ENSURE(hv, 3 * Tn * sizeof(int32_t));
+  return TM_OK;
+}
+
+static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_tri, int tri_bits, int64_t T,
+                      int check, int64_t* d_off, int32_t* d_v, int64_t* n_polys, int64_t* n_slots, int64_t* stats,
+                      cudaStream_t user) {
+  int rc = path_buffers(ctx, n, T);
+  if (rc) return rc;
   if (!ctx->gstream) CK(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
   for (auto& e : ctx->ev)
     if (!e) CK(cudaEventCreate(&e));
@@ -777,7 +794,7 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
   };
   auto body = [&](cudaStream_t s) -> int {
     int r;
-    if ((r = enqueue_reset(ctx, s))) return r;
+    if (!ctx->label_a_external && (r = enqueue_reset(ctx, s))) return r;
     CK(rec(ctx->ev[0], s));
     if ((r = enqueue_label(ctx, d_xy, n, d_tri, tri_bits, T, check, tri32, hw, ctx->max_edge.as<int8_t>(),
                            ctx->seed.as<uint8_t>(), nullptr, s)))
@@ -796,7 +813,7 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
 
   cudaStream_t s = user;
   if (ctx->use_graph && !ctx->prof.on) {
-    GraphKey key{d_xy, d_tri, d_off, d_v, n, T, 0, 0, tri_bits, check, ctx->pool_cap};
+    GraphKey key{d_xy, d_tri, d_off, d_v, n, T, 0, 0, tri_bits, check, ctx->label_a_external ? 1 : 0, ctx->pool_cap};
     part_range(ctx, T, &key.tb, &key.te);
     if (!ctx->graph || !(key == ctx->gkey)) {
       if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
@@ -882,10 +899,34 @@ int tm_mesh_to_polygons_host(tm_ctx* ctx, const double* h_xy, int64_t n, const i
   ENSURE(tri, 3 * Tn * sizeof(int64_t));
   ENSURE(fin_off, (Tn + 1) * sizeof(int64_t));
   ENSURE(fin_v, 3 * Tn * sizeof(int32_t));
+  if ((rc = path_buffers(ctx, n, T))) return rc;
+  if (!ctx->cstream) CK(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
+  for (auto& e : ctx->chunk_ev)
+    if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // Upload overlap: the vertices first (pass A gathers them at random), then
+  // the triangles in chunks on a copy stream; label pass A runs on each chunk
+  // as soon as it lands, so only the last chunk's pass A is exposed.
   CK(cudaMemcpyAsync(ctx->xy.p, h_xy, 2 * n * sizeof(double), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(ctx->tri.p, h_tri, 3 * T * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  if ((rc = enqueue_reset(ctx, s))) return rc;
+  launch_label_a_prepare(n, T, nullptr, ctx->slots.p, s);
+  CK(cudaEventRecord(ctx->chunk_ev[0], s));
+  CK(cudaStreamWaitEvent(ctx->cstream, ctx->chunk_ev[0], 0));  // table reset before any chunk's pass A
+  for (int k = 0; k < kUploadChunks; k++) {
+    const int64_t t0 = T * k / kUploadChunks, t1 = T * (k + 1) / kUploadChunks;
+    if (t1 > t0)
+      CK(cudaMemcpyAsync(ctx->tri.as<int64_t>() + 3 * t0, h_tri + 3 * t0, 3 * (t1 - t0) * sizeof(int64_t),
+                         cudaMemcpyHostToDevice, ctx->cstream));
+    CK(cudaEventRecord(ctx->chunk_ev[k], ctx->cstream));
+    CK(cudaStreamWaitEvent(s, ctx->chunk_ev[k], 0));
+    launch_label_a_range(ctx->xy.as<double>(), n, ctx->tri.p, 1, T, t0, t1, check, ctx->tri32.as<int32_t>(),
+                         ctx->hw.as<int32_t>(), ctx->max_edge.as<int8_t>(), ctx->seed.as<uint8_t>(), nullptr,
+                         ctx->slots.p, &dc_of(ctx)->st, s);
+  }
+  CK(cudaGetLastError());
+  ctx->label_a_external = true;
   rc = run_device(ctx, ctx->xy.as<double>(), n, ctx->tri.p, 64, T, check, ctx->fin_off.as<int64_t>(),
                   ctx->fin_v.as<int32_t>(), n_polys, n_slots, stats, s);
+  ctx->label_a_external = false;
   if (rc) return rc;
   if (*n_polys > cap_polys || *n_slots > cap_slots)
     return set_err(ctx, TM_ERR_CAPACITY, "host output capacity too small (%lld polygons, %lld slots needed)",

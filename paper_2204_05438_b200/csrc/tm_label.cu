@@ -182,7 +182,8 @@ __device__ __forceinline__ int warp_compact3(unsigned flags, int lane, int32_t* 
 // dense lanes.
 template <typename TI>
 __global__ void __launch_bounds__(kLabelThreads) k_tri_pass(const double2* __restrict__ xy, int64_t n,
-                                                            const TI* __restrict__ tri, int64_t T,
+                                                            const TI* __restrict__ tri, int64_t t_begin,
+                                                            int64_t T,
                                                             int32_t* __restrict__ tri32, int8_t* __restrict__ max_edge,
                                                             TwinTable tb, int32_t* __restrict__ hw,
                                                             uint8_t* __restrict__ seed, int32_t* __restrict__ tv,
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(kLabelThreads) k_tri_pass(const double2* __res
   __shared__ int32_t sq[kLabelWarps][3][96];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t - lane < T; t += stride) {
+  for (int64_t t = t_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t - lane < T; t += stride) {
     unsigned flags = 0;
     int32_t hh[3], oo[3], gg[3];
     if (t < T) {
@@ -385,26 +386,36 @@ size_t hash_bytes(int64_t n, int64_t T) {
   return (size_t)(tb.nb_mask + 1) * 4 * sizeof(unsigned long long);
 }
 
-void launch_label_a(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int check,
-                    int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed, int32_t* tv, void* table,
-                    DevStatus* st, cudaStream_t s) {
-  TwinTable tb = table_geometry(n, T, table);
+void launch_label_a_prepare(int64_t n, int64_t T, int32_t* tv, void* table, cudaStream_t s) {
   cudaMemsetAsync(table, 0xFF, hash_bytes(n, T), s);
   if (n > 0 && tv != nullptr) {
     // sentinel 0x7F7F7F7F (> any triangle index), mapped to -1 by pass B
     cudaMemsetAsync(tv, 0x7F, (size_t)n * sizeof(int32_t), s);
   }
-  if (T > 0) {
+}
+
+void launch_label_a_range(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int64_t t_begin,
+                          int64_t t_end, int check, int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed,
+                          int32_t* tv, void* table, DevStatus* st, cudaStream_t s) {
+  TwinTable tb = table_geometry(n, T, table);
+  if (t_end > t_begin) {
     const int B = kLabelThreads;
+    const int g = grid_for(t_end - t_begin, B);
     if (tri_is64)
-      k_tri_pass<int64_t><<<grid_for(T, B), B, 0, s>>>((const double2*)xy, n, (const int64_t*)tri, T, tri32, max_edge,
-                                                       tb, hw, seed, tv, check, st);
+      k_tri_pass<int64_t><<<g, B, 0, s>>>((const double2*)xy, n, (const int64_t*)tri, t_begin, t_end, tri32,
+                                          max_edge, tb, hw, seed, tv, check, st);
     else
-      k_tri_pass<int32_t><<<grid_for(T, B), B, 0, s>>>((const double2*)xy, n, (const int32_t*)tri, T,
-                                                       tri32 == tri ? nullptr : tri32, max_edge, tb, hw, seed, tv,
-                                                       check, st);
+      k_tri_pass<int32_t><<<g, B, 0, s>>>((const double2*)xy, n, (const int32_t*)tri, t_begin, t_end,
+                                          tri32 == tri ? nullptr : tri32, max_edge, tb, hw, seed, tv, check, st);
     note_launch(1);
   }
+}
+
+void launch_label_a(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int check,
+                    int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed, int32_t* tv, void* table,
+                    DevStatus* st, cudaStream_t s) {
+  launch_label_a_prepare(n, T, tv, table, s);
+  launch_label_a_range(xy, n, tri, tri_is64, T, 0, T, check, tri32, hw, max_edge, seed, tv, table, st, s);
 }
 
 void launch_label_b(const int32_t* tri32, int64_t n, int64_t T, int32_t* hw, const int8_t* max_edge, uint8_t* seed,

@@ -114,6 +114,31 @@ def test_host_c_abi_one_call(cuda, name):
     assert list(stats)[:4] == g["stats"].tolist()
 
 
+def test_host_c_abi_u1m_hashes(cuda):
+    """The one-call host path at full size (chunked upload overlapped with label
+    pass A): final CSR byte-equal to the reference (hashes.json)."""
+    from paper_2204_05438_b200 import _capi
+    from paper_2204_05438_b200.io_formats import array_hash as H
+    h = load_hashes().get("u1m_unit")
+    if h is None:
+        pytest.skip("hashes.json has no u1m_unit entry")
+    tri = big_input("u1m_unit")
+    T = tri.n_triangles
+    off = np.zeros(T + 1, dtype=np.int64)
+    verts = np.zeros(3 * T, dtype=np.int32)
+    npol, nsl = ctypes.c_int64(), ctypes.c_int64()
+    stats = (ctypes.c_int64 * _capi.NUM_STATS)()
+    ctx = _capi.context()
+    for _ in range(2):  # second call replays the captured graph
+        rc = _capi.lib().tm_mesh_to_polygons_host(ctx.ptr, _capi.ptr(tri.vertices), tri.n_vertices,
+                                                  _capi.ptr(tri.triangles), T, 0, _capi.ptr(off), _capi.ptr(verts),
+                                                  T, 3 * T, ctypes.byref(npol), ctypes.byref(nsl), stats)
+        ctx.check(rc)
+        P, F = npol.value, nsl.value
+        assert H(off[: P + 1]) == h["final_off"]
+        assert H(verts[:F].astype(np.int64)) == h["final_verts"]
+
+
 def _gpu_vs_oracle(tri):
     r = oracle.execute(tri)
     lab = tm().label_all(tri, check=False)
