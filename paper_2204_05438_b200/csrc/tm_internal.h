@@ -44,13 +44,13 @@ void launch_trav_start(const int32_t* hw, const int32_t* seeds, const int64_t* P
 // rulers: starts of the selected seeds + sampled half-edges of triangles [t_begin, t_end)
 void launch_ruler_walk(const int32_t* hw, const uint32_t* bits, int64_t T, int64_t t_begin, int64_t t_end,
                        const int32_t* start, const int64_t* Pp, int64_t Pcap, int32_t* rnext, int32_t* rdist,
-                       DevStatus* st, cudaStream_t s);
+                       int32_t* rprev, DevStatus* st, cudaStream_t s);
 void launch_chain_count(const int32_t* seeds, const int32_t* start, const int64_t* Pp, int64_t Pcap, int64_t T,
-                        const int32_t* rnext, const int32_t* rdist, int64_t* len, int64_t* nrul, DevStatus* st,
-                        cudaStream_t s);
+                        const int32_t* rnext, const int32_t* rdist, const int32_t* rprev, int64_t* len, int64_t* nrul,
+                        DevStatus* st, cudaStream_t s);
 void launch_chain_emit(const int32_t* start, const int64_t* Pp, int64_t Pcap, const int32_t* rnext,
-                       const int32_t* rdist, const int64_t* offsets, const int64_t* eoff, int32_t* ent_r,
-                       int64_t* ent_base, int64_t ecap, DevStatus* st, cudaStream_t s);
+                       const int32_t* rdist, const int32_t* rprev, const int64_t* offsets, const int64_t* eoff,
+                       int32_t* ent_r, int64_t* ent_base, int64_t ecap, DevStatus* st, cudaStream_t s);
 void launch_ruler_write(const int32_t* tri, const int32_t* hw, const int64_t* n_entries, const int32_t* ent_r,
                         const int64_t* ent_base, const int32_t* rdist, int64_t T, int64_t ecap, int32_t* verts,
                         int32_t* hv, cudaStream_t s);

@@ -110,7 +110,8 @@ __global__ void k_bfs_slow(const int32_t* __restrict__ hw, const int32_t* __rest
 // (1) every ruler walks to the next ruler: rnext/rdist indexed by half-edge id
 __device__ __forceinline__ void walk_ruler(const int32_t* __restrict__ hw, const RulerSet& rs, int32_t h,
                                            long long limit, int32_t* __restrict__ rnext,
-                                           int32_t* __restrict__ rdist, DevStatus* st) {
+                                           int32_t* __restrict__ rdist, int32_t* __restrict__ rprev,
+                                           DevStatus* st) {
   int32_t g = h;
   long long d = 0;
   do {
@@ -120,15 +121,16 @@ __device__ __forceinline__ void walk_ruler(const int32_t* __restrict__ hw, const
   } while (!is_ruler(rs, g));
   rnext[h] = g;
   rdist[h] = (int32_t)d;
+  rprev[g] = h;  // every ruler is the successor of exactly one ruler of its cycle
 }
 
 __global__ void __launch_bounds__(256) k_ruler_walk(const int32_t* __restrict__ hw, RulerSet rs, long long limit,
                                                     int32_t* __restrict__ rnext, int32_t* __restrict__ rdist,
-                                                    DevStatus* st) {
+                                                    int32_t* __restrict__ rprev, DevStatus* st) {
   for (int64_t h = rs.hb + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < rs.he;
        h += (int64_t)gridDim.x * blockDim.x) {
     if (!hw_front(hw[h]) || !is_ruler(rs, (int32_t)h)) continue;
-    walk_ruler(hw, rs, (int32_t)h, limit, rnext, rdist, st);
+    walk_ruler(hw, rs, (int32_t)h, limit, rnext, rdist, rprev, st);
   }
 }
 
@@ -137,53 +139,74 @@ __global__ void __launch_bounds__(256) k_ruler_walk_starts(const int32_t* __rest
                                                            const int32_t* __restrict__ start,
                                                            const int64_t* __restrict__ Pp, long long limit,
                                                            int32_t* __restrict__ rnext, int32_t* __restrict__ rdist,
-                                                           DevStatus* st) {
+                                                           int32_t* __restrict__ rprev, DevStatus* st) {
   const int64_t P = *Pp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t h = start[i];
     if (h < 0 || (h >= rs.hb && h < rs.he)) continue;
-    walk_ruler(hw, rs, h, limit, rnext, rdist, st);
+    walk_ruler(hw, rs, h, limit, rnext, rdist, rprev, st);
   }
 }
 
-// (2a) polygon length and ruler count per seed (traversal.py:264-281)
+// (2a) polygon length and ruler count per seed (traversal.py:264-281).  Two
+// walkers per cycle -- forward over rnext, backward over rprev -- consume the
+// rulers from both ends, so the longest cycle costs half as many dependent hops.
 __global__ void __launch_bounds__(256) k_chain_count(const int32_t* __restrict__ seeds, const int32_t* __restrict__ start,
                                                      const int64_t* __restrict__ Pp, long long limit, const int32_t* __restrict__ rnext,
-                                                     const int32_t* __restrict__ rdist, int64_t* __restrict__ len,
-                                                     int64_t* __restrict__ nrul, DevStatus* st) {
+                                                     const int32_t* __restrict__ rdist, const int32_t* __restrict__ rprev,
+                                                     int64_t* __restrict__ len, int64_t* __restrict__ nrul,
+                                                     DevStatus* st) {
   const int64_t P = *Pp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t h0 = start[i], r = h0;
+    const int32_t h0 = start[i];
     long long L = 0, cnt = 0;
     if (h0 >= 0) {
-      do {
-        L += rdist[r];
+      int32_t f = h0, b = rprev[h0];  // next ruler to consume going forward / backward
+      for (;;) {
+        L += rdist[f];
         cnt++;
-        r = rnext[r];
+        if (f == b) break;
+        f = rnext[f];
+        L += rdist[b];
+        cnt++;
+        if (b == f) break;
+        b = rprev[b];
         if (L > limit) { report(st, K_WALK, seeds[i]); L = 0; cnt = 0; break; }
-      } while (r != h0);
+      }
     }
     len[i] = L;
     nrul[i] = cnt;
   }
 }
 
-// (2b) emit (ruler, absolute output offset) entries in chain order
+// (2b) emit (ruler, absolute output offset) entries in chain order, from both ends
 __global__ void __launch_bounds__(256) k_chain_emit(const int32_t* __restrict__ start, const int64_t* __restrict__ Pp,
                                                     const int32_t* __restrict__ rnext, const int32_t* __restrict__ rdist,
+                                                    const int32_t* __restrict__ rprev,
                                                     const int64_t* __restrict__ offsets, const int64_t* __restrict__ eoff,
                                                     int32_t* __restrict__ ent_r, int64_t* __restrict__ ent_base,
                                                     int64_t ecap, DevStatus* st) {
   const int64_t P = *Pp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t k = eoff[i], kend = eoff[i + 1], pos = offsets[i];
-    int32_t r = start[i];
-    if (kend > ecap) { report(st, K_STRUCT, i); continue; }
-    for (; k < kend; k++) {
-      ent_r[k] = r;
-      ent_base[k] = pos;
-      pos += rdist[r];
-      r = rnext[r];
+    const int32_t h0 = start[i];
+    int64_t kf = eoff[i], kb = eoff[i + 1] - 1;
+    if (h0 < 0 || kb < kf) continue;
+    if (kb >= ecap) { report(st, K_STRUCT, i); continue; }
+    int64_t pf = offsets[i], pb = offsets[i + 1];  // forward start / backward end offsets
+    int32_t f = h0, b = rprev[h0];
+    for (;;) {
+      ent_r[kf] = f;
+      ent_base[kf] = pf;
+      pf += rdist[f];
+      kf++;
+      if (f == b) break;
+      f = rnext[f];
+      pb -= rdist[b];
+      ent_r[kb] = b;
+      ent_base[kb] = pb;
+      kb--;
+      if (b == f) break;
+      b = rprev[b];
     }
   }
 }
@@ -228,29 +251,29 @@ void launch_trav_start(const int32_t* hw, const int32_t* seeds, const int64_t* P
 
 void launch_ruler_walk(const int32_t* hw, const uint32_t* bits, int64_t T, int64_t t_begin, int64_t t_end,
                        const int32_t* start, const int64_t* Pp, int64_t Pcap, int32_t* rnext, int32_t* rdist,
-                       DevStatus* st, cudaStream_t s) {
+                       int32_t* rprev, DevStatus* st, cudaStream_t s) {
   if (T <= 0) return;
   RulerSet rs{bits, (int32_t)(3 * t_begin), (int32_t)(3 * t_end)};
-  k_ruler_walk<<<grid_for(3 * (t_end - t_begin), 256), 256, 0, s>>>(hw, rs, 3 * T + 3, rnext, rdist, st);
+  k_ruler_walk<<<grid_for(3 * (t_end - t_begin), 256), 256, 0, s>>>(hw, rs, 3 * T + 3, rnext, rdist, rprev, st);
   note_launch(1);
   if (t_begin > 0 || t_end < T) {
-    k_ruler_walk_starts<<<grid_for(Pcap, 256), 256, 0, s>>>(hw, rs, start, Pp, 3 * T + 3, rnext, rdist, st);
+    k_ruler_walk_starts<<<grid_for(Pcap, 256), 256, 0, s>>>(hw, rs, start, Pp, 3 * T + 3, rnext, rdist, rprev, st);
     note_launch(1);
   }
 }
 
 void launch_chain_count(const int32_t* seeds, const int32_t* start, const int64_t* Pp, int64_t Pcap, int64_t T,
-                        const int32_t* rnext, const int32_t* rdist, int64_t* len, int64_t* nrul, DevStatus* st,
-                        cudaStream_t s) {
-  k_chain_count<<<grid_for(Pcap, 256), 256, 0, s>>>(seeds, start, Pp, 3 * T + 3, rnext, rdist, len, nrul, st);
+                        const int32_t* rnext, const int32_t* rdist, const int32_t* rprev, int64_t* len, int64_t* nrul,
+                        DevStatus* st, cudaStream_t s) {
+  k_chain_count<<<grid_for(Pcap, 256), 256, 0, s>>>(seeds, start, Pp, 3 * T + 3, rnext, rdist, rprev, len, nrul, st);
   note_launch(1);
 }
 
 void launch_chain_emit(const int32_t* start, const int64_t* Pp, int64_t Pcap, const int32_t* rnext,
-                       const int32_t* rdist, const int64_t* offsets, const int64_t* eoff, int32_t* ent_r,
-                       int64_t* ent_base, int64_t ecap, DevStatus* st, cudaStream_t s) {
-  k_chain_emit<<<grid_for(Pcap, 256), 256, 0, s>>>(start, Pp, rnext, rdist, offsets, eoff, ent_r, ent_base, ecap,
-                                                   st);
+                       const int32_t* rdist, const int32_t* rprev, const int64_t* offsets, const int64_t* eoff,
+                       int32_t* ent_r, int64_t* ent_base, int64_t ecap, DevStatus* st, cudaStream_t s) {
+  k_chain_emit<<<grid_for(Pcap, 256), 256, 0, s>>>(start, Pp, rnext, rdist, rprev, offsets, eoff, ent_r, ent_base,
+                                                   ecap, st);
   note_launch(1);
 }
 
