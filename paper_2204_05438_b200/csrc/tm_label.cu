@@ -29,13 +29,15 @@ namespace tmb {
 // (lo << b) | hi (K = 2b bits) goes through an invertible K-bit mix x; the top
 // q bits of x pick the home bucket, the low R = K - q bits ("remainder") plus
 // the bucket displacement d identify the key exactly, so a slot holds the
-// whole entry in 64 bits:  [ remainder | d (kDispBits) | half-edge (hb) ].
+// whole entry in 64 bits:  [ remainder | d (kDispBits) | half-edge | L ], where L
+// says the half-edge is its triangle's longest edge (pass B then needs no
+// gather of the partner's max_edge).
 // A bucket is 4 slots = one 32-byte sector, so a probe is one sector load.
 // Slots of a bucket fill in order and are never cleared, so a lookup may stop
 // at the first bucket with an empty slot.
 constexpr unsigned long long kEmptySlot = ~0ull;
 constexpr unsigned long long kClaimBit = 1ull << 63;
-constexpr int kDispBits = 6;
+constexpr int kDispBits = 5;
 constexpr int kMaxDisp = (1 << kDispBits) - 1;
 
 struct TwinTable {
@@ -82,12 +84,13 @@ __device__ __forceinline__ void load_bucket_nc(const unsigned long long* s, unsi
 
 // Insert ascending half-edge h = lo -> hi.  In a valid mesh each key has one
 // ascending half-edge; a second one is an orientation / reciprocity defect.
-__device__ __forceinline__ void table_insert(const TwinTable& tb, DevStatus* st, int32_t h, int32_t lo, int32_t hi) {
+__device__ __forceinline__ void table_insert(const TwinTable& tb, DevStatus* st, int32_t hl, int32_t lo, int32_t hi) {
+  const int32_t h = hl >> 1;  // hl = (h << 1) | L
   Probe p = probe_of(tb, lo, hi);
   for (int d = 0; d <= kMaxDisp; d++) {
     unsigned long long* bk = tb.slots + 4 * ((p.home + d) & tb.nb_mask);
     const uint64_t tag = p.tag | (uint64_t)d;
-    const unsigned long long mine = (tag << tb.hb) | (uint32_t)h;
+    const unsigned long long mine = (tag << tb.hb) | (uint32_t)hl;
     unsigned long long v[4];
     load_bucket_cg(bk, v);
     int s = 0;
@@ -102,10 +105,10 @@ __device__ __forceinline__ void table_insert(const TwinTable& tb, DevStatus* st,
       s++;
     }
   }
-  report(st, K_STRUCT, h / 3);  // displacement overflow (> 63 buckets): not seen at load <= 0.7
+  report(st, K_STRUCT, h / 3);  // displacement overflow (> 31 buckets): not seen at load <= 0.7
 }
 
-// Partner of descending half-edge o -> g (key (g, o)); -1 when border.
+// Partner of descending half-edge o -> g (key (g, o)) as (h << 1) | L; -1 when border.
 __device__ __forceinline__ int32_t table_lookup(const TwinTable& tb, DevStatus* st, int check, int32_t lo, int32_t hi,
                                                 int64_t elem) {
   Probe p = probe_of(tb, lo, hi);
@@ -212,7 +215,8 @@ __global__ void __launch_bounds__(kLabelThreads) k_tri_pass(const double2* __res
         }
         double2 pa = xy[a], pb = xy[b], pc = xy[c];
         // labeling.py:55-59: edge 0 joins corners 1-2, edge 1 joins 2-0, edge 2 joins 0-1
-        max_edge[t] = (int8_t)argmax3(sqlen(pb, pc), sqlen(pc, pa), sqlen(pa, pb));
+        const int me0 = argmax3(sqlen(pb, pc), sqlen(pc, pa), sqlen(pa, pb));
+        max_edge[t] = (int8_t)me0;
         if (check) {
           // mesh_core.signed_areas (160-168), sign only, unfused
           double d = __dsub_rn(__dmul_rn(__dsub_rn(pb.x, pa.x), __dsub_rn(pc.y, pa.y)),
@@ -225,11 +229,12 @@ __global__ void __launch_bounds__(kLabelThreads) k_tri_pass(const double2* __res
           atomicMin(tv + b, (int32_t)t);
           atomicMin(tv + c, (int32_t)t);
         }
-        // half-edge j: origin corner (j+1)%3, target corner (j+2)%3
+        // half-edge j: origin corner (j+1)%3, target corner (j+2)%3; queued as (h << 1) | longest
         const int32_t cv[3] = {(int32_t)a, (int32_t)b, (int32_t)c};
+        const int me = me0;
 #pragma unroll
         for (int j = 0; j < 3; j++) {
-          hh[j] = (int32_t)(3 * t + j);
+          hh[j] = (int32_t)(((3 * t + j) << 1) | (me == j ? 1 : 0));
           oo[j] = cv[(j + 1) % 3];
           gg[j] = cv[(j + 2) % 3];
           if (oo[j] < gg[j]) flags |= 1u << j;
@@ -276,11 +281,12 @@ __global__ void __launch_bounds__(kLabelThreads) k_pair_pass(const int32_t* __re
     int m = warp_compact3(flags, lane, sq[wid][0], sq[wid][1], sq[wid][2], hh, oo, gg);
     for (int i = lane; i < m; i += 32) {
       const int32_t h = sq[wid][0][i];
-      const int32_t hc = table_lookup(tb, st, check, sq[wid][2][i], sq[wid][1][i], h / 3);
-      if (hc < 0) continue;  // border
+      const int32_t pl = table_lookup(tb, st, check, sq[wid][2][i], sq[wid][1][i], h / 3);
+      if (pl < 0) continue;  // border
+      const int32_t hc = pl >> 1;
       const int32_t tt = h / 3, j = h - 3 * tt;
-      const int32_t tc = hc / 3, k = hc - 3 * tc;
-      const bool own = __ldg(max_edge + tt) == j, other = __ldg(max_edge + tc) == k;
+      const int32_t tc = hc / 3;
+      const bool own = __ldg(max_edge + tt) == j, other = (pl & 1) != 0;
       const int32_t fr = (!own && !other) ? 1 : 0;
       hw[h] = (hc << 1) | fr;
       hw[hc] = (h << 1) | fr;
@@ -368,13 +374,14 @@ static TwinTable table_geometry(int64_t n, int64_t T, void* mem) {
   TwinTable tb{};
   tb.b = bit_length((uint64_t)(n > 1 ? n - 1 : 1));
   tb.K = 2 * tb.b;
-  tb.hb = bit_length((uint64_t)(3 * (T > 0 ? T : 1)));  // 2^hb > 3T: the all-ones field is never a half-edge
+  // payload (h << 1) | L; 2^(hb-1) > 3T, so the all-ones field is never a half-edge
+  tb.hb = bit_length((uint64_t)(3 * (T > 0 ? T : 1))) + 1;
   // ascending half-edges <= 3T/2 + border; 4-slot buckets at load in [0.35, 0.7)
   // (measured: a fuller table costs more in probe/CAS conflicts than it saves in L2)
   uint64_t keys = (uint64_t)(3 * (T > 0 ? T : 1)) / 2 + 64;
   int q = bit_length((keys * 10 / 28) | 1);
   if (q > tb.K) q = tb.K;
-  while (tb.K - q + kDispBits + tb.hb > 63 && q < tb.K) q++;  // the slot must hold remainder|d|h in 63 bits
+  while (tb.K - q + kDispBits + tb.hb > 63 && q < tb.K) q++;  // the slot must hold remainder|d|h|L in 63 bits
   tb.R = tb.K - q;
   tb.nb_mask = (1ull << q) - 1;
   tb.slots = static_cast<unsigned long long*>(mem);
