@@ -1413,20 +1413,6 @@ __device__ __forceinline__ int pmap_lookup(const SegView& g, int32_t x, int32_t 
   return -1;
 }
 
-// first set bit of the cyclic index range [a, a + cnt) of bits (over L), as an offset, or -1
-__device__ int bits_first(const uint32_t* bits, int L, int a, int cnt) {
-  int d = 0;
-  while (d < cnt) {
-    int k = wrapL(a + d, L);
-    int bo = k & 31;
-    int span = min(min(32 - bo, cnt - d), L - k);
-    uint32_t word = bits[k >> 5] >> bo;
-    uint32_t m = span >= 32 ? word : (word & ((1u << span) - 1u));
-    if (m) return d + __ffs(m) - 1;
-    d += span;
-  }
-  return -1;
-}
 
 // first tip of P in the cyclic index range [a, a + cnt), as an offset, or -1
 // (O(1): nexttip[k] = smallest tip index >= k, 0xFFFF when none)
