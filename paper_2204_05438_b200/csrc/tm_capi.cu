@@ -112,7 +112,7 @@ struct tm_ctx {
   Counters* h_result = nullptr;  // pinned, D2H target
   int64_t* h_pin = nullptr;      // pinned scratch (host counts for tm_repair)
   // label
-  Buf slots;
+  Buf slots, lbscan;
   // traversal
   Buf seeds, start, len, overflow, queue, stamp, tiles, nrul, eoff, rnext, rdist, rprev, startbits, ent_r, ent_base;
   // repair
@@ -318,6 +318,7 @@ static int prepare(tm_ctx* ctx, int64_t T, int64_t n = -1) {
   ENSURE(queue, Tn * sizeof(int32_t));
   ENSURE(stamp, Tn * sizeof(int32_t));
   ENSURE(tiles, (scan_scratch_elems(3 * Tn) + 8) * sizeof(int64_t));
+  ENSURE(lbscan, scan_lookback_bytes(Tn));
   ENSURE(rnext, 3 * Tn * sizeof(int32_t));
   ENSURE(rdist, 3 * Tn * sizeof(int32_t));
   ENSURE(rprev, 3 * Tn * sizeof(int32_t));
@@ -415,8 +416,8 @@ static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* 
   }
   {
     SegTimer t_(ctx, S_TRAV_SCAN, s);
-    launch_scan_dev(ctx->len.as<int64_t>(), d_off, &dc->n_seeds, Tn, tiles, s);
-    launch_scan_dev(ctx->nrul.as<int64_t>(), ctx->eoff.as<int64_t>(), &dc->n_seeds, Tn, tiles, s);
+    launch_scan_lookback(ctx->len.as<int64_t>(), ctx->nrul.as<int64_t>(), d_off, ctx->eoff.as<int64_t>(), &dc->n_seeds,
+                         Tn, ctx->lbscan.p, s);
     launch_gather_at(d_off, &dc->n_seeds, &dc->n_slots0, s);
     launch_gather_at(ctx->eoff.as<int64_t>(), &dc->n_seeds, &dc->n_entries, s);
   }
@@ -487,8 +488,8 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
     launch_out_counts(d_off_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->item_n.as<int32_t>(),
                       ctx->item_slots.as<int64_t>(), ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), nullptr,
                       &dc->st, s);
-    launch_scan_dev(ctx->cnt.as<int64_t>(), ctx->pbase.as<int64_t>(), Pp, Tn, tiles, s);
-    launch_scan_dev(ctx->slotsz.as<int64_t>(), ctx->sbase.as<int64_t>(), Pp, Tn, tiles, s);
+    launch_scan_lookback(ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), ctx->pbase.as<int64_t>(),
+                         ctx->sbase.as<int64_t>(), Pp, Tn, ctx->lbscan.p, s);
     launch_finalize(Pp, ctx->pbase.as<int64_t>(), ctx->sbase.as<int64_t>(), d_off_out, &dc->p_out, &dc->f_out, s);
     launch_stitch(d_off_in, d_v_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(), &dc->n_items,
                   ctx->item_list.as<int64_t>(), ctx->item_n.as<int32_t>(), ctx->pool.as<int32_t>(),
@@ -569,7 +570,8 @@ void tm_ctx_destroy(tm_ctx* ctx) {
                  &ctx->ent_r, &ctx->ent_base, &ctx->item_of, &ctx->items, &ctx->long_list, &ctx->item_list,
                  &ctx->item_n, &ctx->item_slots, &ctx->item_state, &ctx->item_depth, &ctx->hugeq, &ctx->longq, &ctx->parked, &ctx->cnt, &ctx->slotsz, &ctx->pbase, &ctx->sbase, &ctx->pool,
                  &ctx->undo, &ctx->xy, &ctx->tri, &ctx->tri32, &ctx->hw, &ctx->max_edge, &ctx->seed, &ctx->tv,
-                 &ctx->off0, &ctx->v0, &ctx->fin_off, &ctx->fin_v, &ctx->hw_snap, &ctx->hv};
+                 &ctx->off0, &ctx->v0, &ctx->fin_off, &ctx->fin_v, &ctx->hw_snap, &ctx->hv,
+                 &ctx->lbscan};
   for (Buf* b : bufs) b->release();
   if (ctx->h_reset) cudaFreeHost(ctx->h_reset);
   for (auto& e : ctx->ev)

@@ -109,6 +109,105 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_final(const int64_t* __re
   }
 }
 
+// ---- single-pass exclusive scan of one or two int64 arrays over in[0..n]
+// (element n contributes 0, so out[n] = total; n read from the device),
+// decoupled look-back: each tile publishes its aggregate, then its inclusive
+// prefix; a tile's warp 0 sums predecessors' aggregates 32 at a time until it
+// meets a published prefix.  Tiles are numbered in launch order by an atomic
+// counter, so every predecessor is resident or done (no deadlock).
+struct ScanState {
+  unsigned int* counter;  // [1 + ntiles]: tile counter, then per-tile flags (0 none, 1 aggregate, 2 prefix)
+  int64_t* agg;           // [2][ntiles] aggregates
+  int64_t* pre;           // [2][ntiles] inclusive prefixes
+  int64_t ntiles;
+};
+
+template <int NV>
+__global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const int64_t* __restrict__ in0,
+                                                                const int64_t* __restrict__ in1,
+                                                                int64_t* __restrict__ out0, int64_t* __restrict__ out1,
+                                                                const int64_t* __restrict__ n_dev, ScanState ss) {
+  __shared__ unsigned int s_tile;
+  __shared__ int64_t s_pre[NV], s_tot[NV];
+  if (threadIdx.x == 0) s_tile = atomicAdd(ss.counter, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t n = *n_dev;
+  const int64_t base = tile * kTile;
+  if (base > n) return;  // tiles beyond the data never publish: nobody looks that far ahead
+  volatile unsigned int* flags = ss.counter + 1;
+  const int64_t first = base + (int64_t)threadIdx.x * kScanItems;
+  const int64_t* in[2] = {in0, in1};
+  int64_t v[NV][kScanItems], ex[NV];
+#pragma unroll
+  for (int a = 0; a < NV; a++) {
+    int64_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+      const int64_t i = first + k;
+      v[a][k] = i < n ? in[a][i] : 0;
+      sum += v[a][k];
+    }
+    ex[a] = block_exclusive_scan<int64_t>(sum, &s_tot[a]);
+  }
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    int64_t tot[NV];
+#pragma unroll
+    for (int a = 0; a < NV; a++) tot[a] = s_tot[a];
+    if (lane == 0) {
+#pragma unroll
+      for (int a = 0; a < NV; a++) {
+        if (tile == 0) ss.pre[a * ss.ntiles] = tot[a];
+        else ss.agg[a * ss.ntiles + tile] = tot[a];
+      }
+      __threadfence();
+      flags[tile] = tile == 0 ? 2u : 1u;
+    }
+    int64_t prefix[NV] = {};
+    for (int64_t t_hi = tile - 1; t_hi >= 0; t_hi -= 32) {
+      const int64_t idx = t_hi - lane;  // lane 0 = nearest predecessor
+      unsigned f = idx >= 0 ? flags[idx] : 2u;
+      while (__any_sync(0xffffffffu, f == 0u))
+        if (f == 0u) f = flags[idx];
+      __threadfence();
+      const unsigned done = __ballot_sync(0xffffffffu, f == 2u);
+      const int stop = done ? __ffs(done) - 1 : 32;  // nearest predecessor with a prefix
+#pragma unroll
+      for (int a = 0; a < NV; a++) {
+        int64_t x = 0;
+        if (idx >= 0 && lane < stop) x = __ldcg(ss.agg + a * ss.ntiles + idx);
+        if (idx >= 0 && lane == stop) x = __ldcg(ss.pre + a * ss.ntiles + idx);
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        prefix[a] += x;
+      }
+      if (done) break;
+    }
+    if (lane == 0) {
+      if (tile > 0) {
+#pragma unroll
+        for (int a = 0; a < NV; a++) ss.pre[a * ss.ntiles + tile] = prefix[a] + tot[a];
+        __threadfence();
+        flags[tile] = 2u;
+      }
+#pragma unroll
+      for (int a = 0; a < NV; a++) s_pre[a] = prefix[a];
+    }
+  }
+  __syncthreads();
+  int64_t* out[2] = {out0, out1};
+#pragma unroll
+  for (int a = 0; a < NV; a++) {
+    int64_t run = s_pre[a] + ex[a];
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+      const int64_t i = first + k;
+      if (i <= n) out[a][i] = run;
+      run += v[a][k];
+    }
+  }
+}
+
 // ---- ascending indices base_index + t with flag[t] != 0 (seed compaction), count -> *n_out
 __global__ void __launch_bounds__(kScanThreads) k_flag_reduce(const uint8_t* __restrict__ flag, int64_t n,
                                                               int64_t* __restrict__ tile_sums) {
@@ -160,6 +259,28 @@ void launch_scan_dev(const int64_t* in, int64_t* out, const int64_t* n_dev, int6
   k_scan_tiles<<<1, kScanThreads, 0, s>>>(tile_sums, n_dev, 1);
   k_scan_final<<<nt, kScanThreads, 0, s>>>(in, n_dev, tile_sums, out);
   note_launch(3);
+}
+
+size_t scan_lookback_bytes(int64_t n_cap) {
+  const int64_t nt = n_cap / kTile + 2;
+  return (size_t)(nt + 2) * sizeof(unsigned int) + 4 * (size_t)nt * sizeof(int64_t) + 64;
+}
+
+void launch_scan_lookback(const int64_t* in0, const int64_t* in1, int64_t* out0, int64_t* out1,
+                          const int64_t* n_dev, int64_t n_cap, void* scratch, cudaStream_t s) {
+  const int64_t nt = n_cap / kTile + 2;  // tiles covering n_cap + 1 elements
+  ScanState ss;
+  ss.counter = static_cast<unsigned int*>(scratch);
+  const size_t head = (((size_t)(nt + 2) * sizeof(unsigned int)) + 63) & ~(size_t)63;
+  ss.agg = reinterpret_cast<int64_t*>(static_cast<char*>(scratch) + head);
+  ss.pre = ss.agg + 2 * nt;
+  ss.ntiles = nt;
+  cudaMemsetAsync(ss.counter, 0, (size_t)(nt + 1) * sizeof(unsigned int), s);
+  if (in1)
+    k_scan_lookback<2><<<(int)nt, kScanThreads, 0, s>>>(in0, in1, out0, out1, n_dev, ss);
+  else
+    k_scan_lookback<1><<<(int)nt, kScanThreads, 0, s>>>(in0, nullptr, out0, nullptr, n_dev, ss);
+  note_launch(1);
 }
 
 void launch_select_flags(const uint8_t* flag, int64_t n, int32_t* out, int64_t* n_out, int64_t* tile_sums,
