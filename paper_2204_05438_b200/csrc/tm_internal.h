@@ -46,7 +46,7 @@ void launch_trav_start(const int32_t* hw, const int32_t* seeds, const int64_t* P
                        int32_t* overflow, unsigned int* n_overflow, int32_t* queue, int32_t* stamp, uint32_t* bits,
                        DevStatus* st, cudaStream_t s);
 // rulers: starts of the selected seeds + sampled half-edges of triangles [t_begin, t_end)
-void launch_ruler_walk(const int32_t* hw, const uint32_t* bits, int64_t T, int64_t t_begin, int64_t t_end,
+void launch_ruler_walk(const int32_t* hw, uint32_t* bits, int64_t T, int64_t t_begin, int64_t t_end,
                        const int32_t* start, const int64_t* Pp, int64_t Pcap, int32_t* rnext, int32_t* rdist,
                        int32_t* rprev, DevStatus* st, cudaStream_t s);
 void launch_chain_count(const int32_t* seeds, const int32_t* start, const int64_t* Pp, int64_t Pcap, int64_t T,

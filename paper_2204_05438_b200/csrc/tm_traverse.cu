@@ -108,29 +108,45 @@ __global__ void k_bfs_slow(const int32_t* __restrict__ hw, const int32_t* __rest
 }
 
 // (1) every ruler walks to the next ruler: rnext/rdist indexed by half-edge id
+// Runs longer than kMaxRun boundary steps are cut by "virtual" rulers (marked
+// in the start bitmap, which only later kernels read): the gap between two
+// hash-sampled rulers is geometric with a ~100-step tail, and the write pass
+// walks each run on one thread, so bounding runs bounds its tail.  A virtual
+// ruler lies inside a gap that exactly one walk covers.
+constexpr int kMaxRun = 24;
 __device__ __forceinline__ void walk_ruler(const int32_t* __restrict__ hw, const RulerSet& rs, int32_t h,
                                            long long limit, int32_t* __restrict__ rnext,
                                            int32_t* __restrict__ rdist, int32_t* __restrict__ rprev,
-                                           DevStatus* st) {
-  int32_t g = h;
-  long long d = 0;
-  do {
+                                           uint32_t* __restrict__ vbits, DevStatus* st) {
+  int32_t cur = h, g = h;
+  long long d = 0, total = 0;
+  for (;;) {
     d++;
+    total++;
     g = walk_next(hw, g, limit);
-    if (g < 0 || d > limit) { report(st, K_WALK, h / 3); g = h; break; }
-  } while (!is_ruler(rs, g));
-  rnext[h] = g;
-  rdist[h] = (int32_t)d;
-  rprev[g] = h;  // every ruler is the successor of exactly one ruler of its cycle
+    if (g < 0 || total > limit) { report(st, K_WALK, h / 3); g = h; break; }
+    if (is_ruler(rs, g)) break;
+    if (d == kMaxRun) {
+      mark_start(vbits, g);
+      rnext[cur] = g;
+      rdist[cur] = (int32_t)d;
+      rprev[g] = cur;
+      cur = g;
+      d = 0;
+    }
+  }
+  rnext[cur] = g;
+  rdist[cur] = (int32_t)d;
+  rprev[g] = cur;  // every ruler is the successor of exactly one ruler of its cycle
 }
 
 __global__ void __launch_bounds__(256) k_ruler_walk(const int32_t* __restrict__ hw, RulerSet rs, long long limit,
                                                     int32_t* __restrict__ rnext, int32_t* __restrict__ rdist,
-                                                    int32_t* __restrict__ rprev, DevStatus* st) {
+                                                    int32_t* __restrict__ rprev, uint32_t* vbits, DevStatus* st) {
   for (int64_t h = rs.hb + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < rs.he;
        h += (int64_t)gridDim.x * blockDim.x) {
     if (!hw_front(hw[h]) || !is_ruler(rs, (int32_t)h)) continue;
-    walk_ruler(hw, rs, (int32_t)h, limit, rnext, rdist, rprev, st);
+    walk_ruler(hw, rs, (int32_t)h, limit, rnext, rdist, rprev, vbits, st);
   }
 }
 
@@ -139,12 +155,13 @@ __global__ void __launch_bounds__(256) k_ruler_walk_starts(const int32_t* __rest
                                                            const int32_t* __restrict__ start,
                                                            const int64_t* __restrict__ Pp, long long limit,
                                                            int32_t* __restrict__ rnext, int32_t* __restrict__ rdist,
-                                                           int32_t* __restrict__ rprev, DevStatus* st) {
+                                                           int32_t* __restrict__ rprev, uint32_t* vbits,
+                                                           DevStatus* st) {
   const int64_t P = *Pp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t h = start[i];
     if (h < 0 || (h >= rs.hb && h < rs.he)) continue;
-    walk_ruler(hw, rs, h, limit, rnext, rdist, rprev, st);
+    walk_ruler(hw, rs, h, limit, rnext, rdist, rprev, vbits, st);
   }
 }
 
@@ -249,15 +266,15 @@ void launch_trav_start(const int32_t* hw, const int32_t* seeds, const int64_t* P
   note_launch(2);
 }
 
-void launch_ruler_walk(const int32_t* hw, const uint32_t* bits, int64_t T, int64_t t_begin, int64_t t_end,
+void launch_ruler_walk(const int32_t* hw, uint32_t* bits, int64_t T, int64_t t_begin, int64_t t_end,
                        const int32_t* start, const int64_t* Pp, int64_t Pcap, int32_t* rnext, int32_t* rdist,
                        int32_t* rprev, DevStatus* st, cudaStream_t s) {
   if (T <= 0) return;
   RulerSet rs{bits, (int32_t)(3 * t_begin), (int32_t)(3 * t_end)};
-  k_ruler_walk<<<grid_for(3 * (t_end - t_begin), 256), 256, 0, s>>>(hw, rs, 3 * T + 3, rnext, rdist, rprev, st);
+  k_ruler_walk<<<grid_for(3 * (t_end - t_begin), 256), 256, 0, s>>>(hw, rs, 3 * T + 3, rnext, rdist, rprev, bits, st);
   note_launch(1);
   if (t_begin > 0 || t_end < T) {
-    k_ruler_walk_starts<<<grid_for(Pcap, 256), 256, 0, s>>>(hw, rs, start, Pp, 3 * T + 3, rnext, rdist, rprev, st);
+    k_ruler_walk_starts<<<grid_for(Pcap, 256), 256, 0, s>>>(hw, rs, start, Pp, 3 * T + 3, rnext, rdist, rprev, bits, st);
     note_launch(1);
   }
 }
