@@ -445,13 +445,12 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
   {
     SegTimer t_(ctx, S_CLASSIFY, s);
     launch_classify(d_off_in, d_v_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(), &dc->n_items,
-                    ctx->long_list.as<int32_t>(), &dc->n_long, dc->stats, q, s);
+                    ctx->long_list.as<int32_t>(), &dc->n_long, dc->stats, q, ctx->path_hv,
+                    const_cast<int32_t*>(d_tv), s);
   }
   CK(cudaMemsetAsync(ctx->item_state.p, 0, Tn * sizeof(int32_t), s));
   const int tv_exact = ctx->path_hv == nullptr;
-  if (!tv_exact)  // fan starts for the work items' vertices (d_tv is scratch here)
-    launch_tv_items(d_off_in, d_v_in, ctx->path_hv, ctx->items.as<int32_t>(), &dc->n_items, Tn,
-                    const_cast<int32_t*>(d_tv), s);
+
   RepairArgs a{d_tri32, d_hw, d_tv, tv_exact, T, ctx->pool.as<int32_t>(), ctx->pool_cap, &dc->pool_top, ctx->undo.as<int32_t>(),
                &dc->undo_top, (unsigned long long)Tn + 1024, &dc->st, ctx->items.as<int32_t>(), &dc->n_items,
                d_off_in, d_v_in, ctx->item_list.as<int64_t>(), ctx->item_n.as<int32_t>(),

@@ -98,9 +98,10 @@ struct RepairArgs {
 // tv[verts[k]] = hv[k] / 3 for every slot of the work items (any incident triangle)
 void launch_tv_items(const int64_t* off, const int32_t* v, const int32_t* hv, const int32_t* items,
                      const unsigned int* n_items, int64_t Pcap, int32_t* tv, cudaStream_t s);
+// hv (nullable): the traversal's slot half-edges -> tv[vertex] = an incident triangle for work items
 void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, int32_t* item_of,
                      int32_t* items, unsigned int* n_items, int32_t* long_list, unsigned int* n_long,
-                     unsigned long long* stats, LongQueue q, cudaStream_t s);
+                     unsigned long long* stats, LongQueue q, const int32_t* hv, int32_t* tv, cudaStream_t s);
 void launch_repair_tips_long(const RepairArgs& a, cudaStream_t s);
 // mode 0: items of length <= kLongMin; mode 1: long items handed back (state 2/3)
 void launch_repair_tips(const RepairArgs& a, int mode, cudaStream_t s);

@@ -200,7 +200,8 @@ __global__ void __launch_bounds__(256) k_classify(const int64_t* __restrict__ of
                                                   const int64_t* __restrict__ Pp, int32_t* __restrict__ item_of,
                                                   int32_t* __restrict__ items, unsigned int* n_items,
                                                   int32_t* __restrict__ long_list, unsigned int* n_long,
-                                                  unsigned long long* stats) {
+                                                  unsigned long long* stats, const int32_t* __restrict__ hv,
+                                                  int32_t* __restrict__ tv) {
   __shared__ int s_cnt;
   __shared__ unsigned int s_base;
   if (threadIdx.x == 0) s_cnt = 0;
@@ -231,6 +232,10 @@ __global__ void __launch_bounds__(256) k_classify(const int64_t* __restrict__ of
     if (is_item) {
       items[pi] = (int32_t)i;
       item_of[i] = pi;
+      if (hv) {  // whole path: fan start of every vertex of the work item (any incident triangle)
+        const int64_t b = off[i], e = off[i + 1];
+        for (int64_t k = b; k < e; k++) tv[v[k]] = hv[k] / 3;
+      }
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -250,7 +255,8 @@ __global__ void __launch_bounds__(256) k_classify_long(const int64_t* __restrict
                                                        const int32_t* __restrict__ long_list,
                                                        const unsigned int* n_long, int32_t* __restrict__ item_of,
                                                        int32_t* __restrict__ items, unsigned int* n_items,
-                                                       unsigned long long* stats, LongQueue q) {
+                                                       unsigned long long* stats, LongQueue q,
+                                                       const int32_t* __restrict__ hv, int32_t* __restrict__ tv) {
   __shared__ int32_t tab[kSetCap];
   __shared__ unsigned int dups;
   unsigned int nl = *n_long;
@@ -287,6 +293,8 @@ __global__ void __launch_bounds__(256) k_classify_long(const int64_t* __restrict
     }
     atomicAdd(&dups, my);
     __syncthreads();
+    if (dups > 0 && hv)
+      for (int p = threadIdx.x; p < n; p += blockDim.x) tv[s[p]] = hv[b + p] / 3;
     if (threadIdx.x == 0 && dups > 0) {
       unsigned int k = atomicAdd(n_items, 1u);
       items[k] = i;
@@ -2271,10 +2279,10 @@ void launch_tv_items(const int64_t* off, const int32_t* v, const int32_t* hv, co
 
 void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, int32_t* item_of,
                      int32_t* items, unsigned int* n_items, int32_t* long_list, unsigned int* n_long,
-                     unsigned long long* stats, LongQueue q, cudaStream_t s) {
-  k_classify<<<grid_for(Pcap, 256), 256, 0, s>>>(off, v, Pp, item_of, items, n_items, long_list, n_long, stats);
+                     unsigned long long* stats, LongQueue q, const int32_t* hv, int32_t* tv, cudaStream_t s) {
+  k_classify<<<grid_for(Pcap, 256), 256, 0, s>>>(off, v, Pp, item_of, items, n_items, long_list, n_long, stats, hv, tv);
   note_launch(1);
-  k_classify_long<<<kNumSMs * 4, 256, 0, s>>>(off, v, long_list, n_long, item_of, items, n_items, stats, q);
+  k_classify_long<<<kNumSMs * 4, 256, 0, s>>>(off, v, long_list, n_long, item_of, items, n_items, stats, q, hv, tv);
   note_launch(1);
 }
 
