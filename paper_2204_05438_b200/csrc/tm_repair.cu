@@ -101,62 +101,6 @@ __device__ __forceinline__ void demote(const RepairCtx& c, int32_t e, int32_t te
   c.hw[te] = e << 1;
 }
 
-// traversal.py:112-124 for one polygon
-__device__ bool poly_has_tip(const int32_t* s, int64_t n) {
-  for (int64_t pos = 0; pos < n; pos++) {
-    int64_t a = pos == 0 ? n - 1 : pos - 1, b = pos + 1 == n ? 0 : pos + 1;
-    if (s[a] == s[b]) return true;
-  }
-  return false;
-}
-
-// reparation.py:59-71
-__device__ int64_t first_tip(const int32_t* s, int64_t n) {
-  for (int64_t pos = 0; pos < n; pos++) {
-    int64_t a = pos == 0 ? n - 1 : pos - 1, b = pos + 1 == n ? 0 : pos + 1;
-    if (s[a] == s[b]) return pos;
-  }
-  return -1;
-}
-
-// (len - distinct) of one polygon (traversal.py:140-147).  Small polygons use a
-// quadratic scan; long ones an in-place heap sort of a scratch copy.
-__device__ void sift(int32_t* a, int64_t root, int64_t n) {
-  for (;;) {
-    int64_t ch = 2 * root + 1;
-    if (ch >= n) return;
-    if (ch + 1 < n && a[ch + 1] > a[ch]) ch++;
-    if (a[root] >= a[ch]) return;
-    int32_t t = a[root];
-    a[root] = a[ch];
-    a[ch] = t;
-    root = ch;
-  }
-}
-
-__device__ int64_t extra_visits(const int32_t* s, int64_t n, int32_t* scratch) {
-  if (n <= 48 || scratch == nullptr) {
-    int64_t extra = 0;
-    for (int64_t i = 1; i < n; i++) {
-      bool dup = false;
-      for (int64_t j = 0; j < i && !dup; j++) dup = s[j] == s[i];
-      extra += dup;
-    }
-    return extra;
-  }
-  for (int64_t i = 0; i < n; i++) scratch[i] = s[i];
-  for (int64_t r = n / 2 - 1; r >= 0; r--) sift(scratch, r, n);
-  for (int64_t e = n - 1; e > 0; e--) {
-    int32_t t = scratch[0];
-    scratch[0] = scratch[e];
-    scratch[e] = t;
-    sift(scratch, 0, e);
-  }
-  int64_t extra = 0;
-  for (int64_t i = 1; i < n; i++) extra += scratch[i] == scratch[i - 1];
-  return extra;
-}
-
 // ------------------------------------------------------------ classify
 // Per input polygon: tip flag, repeated flag, extra visits.  Work items are the
 // polygons with a repeated vertex (a tip implies one).
@@ -361,22 +305,6 @@ __device__ void walk_write(const RepairCtx& c, int32_t h0, int32_t* out) {
   } while (h != h0 && h >= 0);
 }
 
-// Re-walk split (reparation.py:216-229 after promotion).  Returns 1 on success
-// (pieces written), 0 when the length law fails (caller decides strictness),
-// -1 on error/capacity.
-__device__ int rewalk_split(const RepairCtx& c, int32_t e, int32_t te, int64_t plen, int32_t poly,
-                            int64_t* pa_off, int64_t* pa_len, int64_t* pb_off, int64_t* pb_len) {
-  int32_t ha = min_frontier_slot(c.hw, e / 3), hb = min_frontier_slot(c.hw, te / 3);
-  long long la = walk_len(c, ha), lb = walk_len(c, hb);
-  if (la < 0 || lb < 0) { report(c.st, K_STRUCT, poly); return -1; }
-  if (la + lb != plen + 2) return 0;
-  int64_t o = palloc(c, la + lb);
-  if (o < 0) { report(c.st, K_POOL, poly); return -1; }
-  walk_write(c, ha, c.pool + o);
-  walk_write(c, hb, c.pool + o + la);
-  *pa_off = o; *pa_len = la; *pb_off = o + la; *pb_len = lb;
-  return 1;
-}
 
 // ------------------------------------------------------------ warp helpers
 // One warp cooperates on one piece.  Lanes split O(len) scans and copies; the
