@@ -1509,13 +1509,17 @@ __device__ int emit_range_warp(const SegView& g, const SPiece& X, int start, int
   return n + count - (merge ? 1 : 0);
 }
 
-// Arc split of piece X at tip position pos with split info si
-// (not yet promoted).  On success the children are written (rotated to the
-// re-walk start pairs) and the edge is promoted; returns false without side
-// effects when a search fails (the caller falls back to the re-walk).
-__device__ bool seg_split_arcs(const RepairCtx& c, const SegView& g, const SPiece& X, int pos, int32_t v,
-                               const SplitInfo& si, int* s_stop, int seg_base, int seg_cap, int lane, SPiece* A,
-                               SPiece* B,
+// Arc split of piece X at tip position pos with split info si:
+// the cut, the children's lengths and rotations, their segment storage; the
+// edge is promoted.  Returns false without side effects when a search fails
+// (the caller falls back to the re-walk).  The children are then emitted by
+// seg_emit_child, pa and pb by the two warps of a pair.
+struct SplitPlan {
+  int j, la, lb, ka, kb, base_a, base_b;
+  int32_t v, u;
+};
+__device__ bool seg_split_plan(const RepairCtx& c, const SegView& g, const SPiece& X, int pos, int32_t v,
+                               const SplitInfo& si, int* s_stop, int seg_base, int seg_cap, int lane, SplitPlan* pl,
                                unsigned long long* prof) {
   const int Lx = X.len;
   if (si.a_in < 0) return false;
@@ -1547,45 +1551,47 @@ __device__ bool seg_split_arcs(const RepairCtx& c, const SegView& g, const SPiec
     }
   }
   if (ka < 0 || kb < 0) return false;
-  long long c2 = clock64();
   int base = 0;
   const int need = 2 * (X.nseg + 4);
   if (lane == 0) base = atomicAdd(s_stop, need);
   base = __shfl_sync(kFull, base, 0);
   if (base + need > seg_cap) return false;  // (capacity is checked per round; defensive)
   base += seg_base;
-  Seg* oa = g.segs + base;
-  Seg* ob = g.segs + base + X.nseg + 4;
-  int na = 0, nb = 0;
-  if (ka == 0) {
-    if (lane == 0) oa[0] = mkseg(~v, 1, 0);
-    na = emit_range_warp(g, X, j, la - 1, oa, 1, 1, lane);
-  } else {
-    na = emit_range_warp(g, X, wrapN(j + ka - 1, Lx), la - ka, oa, 0, 0, lane);
-    if (lane == 0) oa[na] = mkseg(~v, 1, la - ka);
-    na = emit_range_warp(g, X, j, ka - 1, oa, na + 1, la - ka + 1, lane);
-  }
-  nb = emit_range_warp(g, X, wrapN(pos + kb, Lx), lb - 1 - kb, ob, 0, 0, lane);
-  if (lane == 0) ob[nb] = mkseg(~si.u, 1, lb - 1 - kb);
-  nb = emit_range_warp(g, X, pos, kb, ob, nb + 1, lb - kb, lane);
   if (lane == 0) {
     promote(c, si.e, si.te);
-    A->soff = base; A->nseg = na; A->len = la;
-    B->soff = base + X.nseg + 4; B->nseg = nb; B->len = lb;
     if (prof) {
-      long long c3 = clock64();
       atomicAdd(prof + 0, (unsigned long long)(c1 - c0));
-      atomicAdd(prof + 1, (unsigned long long)(c2 - c1));
-      atomicAdd(prof + 2, (unsigned long long)(c3 - c2));
+      atomicAdd(prof + 1, (unsigned long long)(clock64() - c1));
       atomicAdd(prof + 3, (unsigned long long)X.nseg);
     }
   }
-  __syncwarp();
-  A->soff = __shfl_sync(kFull, A->soff, 0); A->nseg = __shfl_sync(kFull, A->nseg, 0);
-  A->len = __shfl_sync(kFull, A->len, 0);
-  B->soff = __shfl_sync(kFull, B->soff, 0); B->nseg = __shfl_sync(kFull, B->nseg, 0);
-  B->len = __shfl_sync(kFull, B->len, 0);
+  *pl = SplitPlan{j, la, lb, ka, kb, base, base + X.nseg + 4, v, si.u};
   return true;
+}
+
+// child 0 = pa = rotate([v] ++ X[j .. pos-1], ka), child 1 = pb = rotate(X[pos .. j-1] ++ [u], kb)
+__device__ SPiece seg_emit_child(const SegView& g, const SPiece& X, int pos, const SplitPlan& p, int which, int lane) {
+  const int Lx = X.len;
+  Seg* o = g.segs + (which ? p.base_b : p.base_a);
+  int nn;
+  if (which == 0) {
+    if (p.ka == 0) {
+      if (lane == 0) o[0] = mkseg(~p.v, 1, 0);
+      nn = emit_range_warp(g, X, p.j, p.la - 1, o, 1, 1, lane);
+    } else {
+      nn = emit_range_warp(g, X, wrapN(p.j + p.ka - 1, Lx), p.la - p.ka, o, 0, 0, lane);
+      if (lane == 0) o[nn] = mkseg(~p.v, 1, p.la - p.ka);
+      nn = emit_range_warp(g, X, p.j, p.ka - 1, o, nn + 1, p.la - p.ka + 1, lane);
+    }
+  } else {
+    nn = emit_range_warp(g, X, wrapN(pos + p.kb, Lx), p.lb - 1 - p.kb, o, 0, 0, lane);
+    if (lane == 0) o[nn] = mkseg(~p.u, 1, p.lb - 1 - p.kb);
+    nn = emit_range_warp(g, X, pos, p.kb, o, nn + 1, p.lb - p.kb, lane);
+  }
+  __syncwarp();
+  SPiece r{which ? p.base_b : p.base_a, nn, which ? p.lb : p.la, -1, -1};
+  r.ftip = seg_first_tip(g, r, lane, &r.fk);
+  return r;
 }
 
 __device__ __forceinline__ void tset_add(int32_t* set, int32_t x) {
@@ -1606,6 +1612,15 @@ __device__ __forceinline__ bool tset_has(const int32_t* set, int32_t x) {
   }
   return false;
 }
+
+// two warps of a pair meet (named barrier 1 + pair; 0 is __syncthreads)
+__device__ __forceinline__ void pair_sync(int pair) {
+  asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory");
+}
+struct PairMsg {
+  int mode;
+  SplitPlan plan;
+};
 
 __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c, const int32_t* __restrict__ items,
                                                                     const int64_t* __restrict__ off,
@@ -1636,6 +1651,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
   int* tlist = tipdeg + kSegTips;                              // tipped records of the round
   Seg* segs = reinterpret_cast<Seg*>(tlist + kSegRec);
   __shared__ int s_ntip, s_ntouch, s_stop, s_fail, s_ntips, s_need, s_tot;
+  __shared__ PairMsg pmsg[kSegWarps / 2];
   __shared__ long long s_base;
   __shared__ unsigned int s_w;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1820,89 +1836,109 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
       const bool tset_ok = s_ntouch <= kSegTouch / 2;  // else: always recompute
       for (int r = threadIdx.x; r < n; r += blockDim.x)
         if (in[r].ftip < 0) out[s_out[r]] = in[r];
-      for (int t = wib; t < ntips; t += kSegWarps) {
+      // Warp pairs share a split: the lead warp computes the split info, the
+      // cut and the rotations (promoting the edge), then the two warps emit
+      // pa and pb and find their first tips side by side.
+      const int pair = wib >> 1, hf = wib & 1;
+      for (int t = pair; t < ntips; t += kSegWarps / 2) {
         const int r = tlist[t];
         const SPiece X = in[r];
         const int pos = X.ftip;
-        long long ck0 = clock64();
-        const int32_t tv_ = selem(g, X, pos, lane), bv = selem(g, X, pos == 0 ? X.len - 1 : pos - 1, lane);
-        int k = -1;
-        if (X.fk >= 0) {  // the precomputed slot of this tip of P
-          uint32_t wbits = tipbits[X.fk >> 5];
-          k = tiprank[X.fk >> 5] + __popc(wbits & ((1u << (X.fk & 31)) - 1u));
-          if (k >= ntip_pre || tipv[k] != tv_) k = -1;
-        }
-        SplitInfo si;
-        bool use = k >= 0 && tset_ok;
-        if (use) {
-          si = tipinfo[k];
-          use = !tset_has(tset, tv_) && !tset_has(tset, si.u);  // no promotion touched v or u
-        }
-        if (lane == 0) atomicAdd(dbg + (use ? 62 : 61), 1ull);
-        FanCache fc;
-        if (k >= 0 && fcache && tipdeg[k] >= 0) { fc.in = fcache + (long long)k * kFanCap; fc.in_deg = tipdeg[k]; }
-        bool ok = use || warp_split_info(c, tv_, bv, i, fan, back, lane, false, false, &si, fc);
-        SPiece A{0, 0, 0, -1, -1}, B{0, 0, 0, -1, -1};
-        long long ck1 = clock64();
-        if (ok && !seg_split_arcs(c, g, X, pos, tv_, si, &s_stop, tb, half, lane, &A, &B,
+        if (hf == 0) {
+          long long ck0 = clock64();
+          const int32_t tv_ = selem(g, X, pos, lane), bv = selem(g, X, pos == 0 ? X.len - 1 : pos - 1, lane);
+          int k = -1;
+          if (X.fk >= 0) {  // the precomputed slot of this tip of P
+            uint32_t wbits = tipbits[X.fk >> 5];
+            k = tiprank[X.fk >> 5] + __popc(wbits & ((1u << (X.fk & 31)) - 1u));
+            if (k >= ntip_pre || tipv[k] != tv_) k = -1;
+          }
+          SplitInfo si;
+          bool use = k >= 0 && tset_ok;
+          if (use) {
+            si = tipinfo[k];
+            use = !tset_has(tset, tv_) && !tset_has(tset, si.u);  // no promotion touched v or u
+          }
+          if (lane == 0) atomicAdd(dbg + (use ? 62 : 61), 1ull);
+          FanCache fc;
+          if (k >= 0 && fcache && tipdeg[k] >= 0) { fc.in = fcache + (long long)k * kFanCap; fc.in_deg = tipdeg[k]; }
+          bool ok = use || warp_split_info(c, tv_, bv, i, fan, back, lane, false, false, &si, fc);
+          SplitPlan pl;
+          int mode = 0;  // 0 failed, 1 pair emission, 2 lead finished alone (re-walk fallback)
+          SPiece A{0, 0, 0, -1, -1}, B{0, 0, 0, -1, -1};
+          long long ck1 = clock64();
+          if (ok && seg_split_plan(c, g, X, pos, tv_, si, &s_stop, tb, half, lane, &pl,
                                    qi == trace_qi ? dbg + 52 : nullptr)) {
-          // re-walk fallback (reparation.py:216-229) with the strict length law;
-          // the pieces come back as one-vertex segments
-          if (lane == 0) { promote(c, si.e, si.te); atomicAdd(dbg + 63, 1ull); }
-          __syncwarp();
-          int32_t *pa = nullptr, *pb = nullptr;
-          int la = 0, lb = 0;
-          auto galloc = [&](long long m) -> int32_t* {
-            long long o = 0;
-            if (lane == 0) o = palloc(c, m);
-            o = __shfl_sync(kFull, o, 0);
-            return o < 0 ? nullptr : c.pool + o;
-          };
-          int rr = warp_rewalk_split(c, si.e, si.te, X.len, i, galloc, lane, &pa, &la, &pb, &lb);
-          if (rr == 0 && lane == 0) report(c.st, K_SPLIT_LAW, i);
-          ok = rr == 1;
-          if (ok) {
-            int sb = 0;
-            if (lane == 0) sb = atomicAdd(&s_stop, la + lb);
-            sb = __shfl_sync(kFull, sb, 0);
-            if (sb + la + lb > half) {
-              if (lane == 0) report(c.st, K_STRUCT, i);
-              ok = false;
-            } else {
-              sb += tb;
-              for (int x = lane; x < la; x += 32) segs[sb + x] = mkseg(~pa[x], 1, x);
-              for (int x = lane; x < lb; x += 32) segs[sb + la + x] = mkseg(~pb[x], 1, x);
-              A = SPiece{sb, la, la, -1, -1};
-              B = SPiece{sb + la, lb, lb, -1, -1};
+            mode = 1;
+          } else if (ok) {
+            // re-walk fallback (reparation.py:216-229) with the strict length law;
+            // the pieces come back as one-vertex segments
+            if (lane == 0) { promote(c, si.e, si.te); atomicAdd(dbg + 63, 1ull); }
+            __syncwarp();
+            int32_t *pa = nullptr, *pb = nullptr;
+            int la = 0, lb = 0;
+            auto galloc = [&](long long m) -> int32_t* {
+              long long o = 0;
+              if (lane == 0) o = palloc(c, m);
+              o = __shfl_sync(kFull, o, 0);
+              return o < 0 ? nullptr : c.pool + o;
+            };
+            int rr = warp_rewalk_split(c, si.e, si.te, X.len, i, galloc, lane, &pa, &la, &pb, &lb);
+            if (rr == 0 && lane == 0) report(c.st, K_SPLIT_LAW, i);
+            if (rr == 1) {
+              int sb = 0;
+              if (lane == 0) sb = atomicAdd(&s_stop, la + lb);
+              sb = __shfl_sync(kFull, sb, 0);
+              if (sb + la + lb > half) {
+                if (lane == 0) report(c.st, K_STRUCT, i);
+              } else {
+                sb += tb;
+                for (int x = lane; x < la; x += 32) segs[sb + x] = mkseg(~pa[x], 1, x);
+                for (int x = lane; x < lb; x += 32) segs[sb + la + x] = mkseg(~pb[x], 1, x);
+                __syncwarp();
+                A = SPiece{sb, la, la, -1, -1};
+                B = SPiece{sb + la, lb, lb, -1, -1};
+                A.ftip = seg_first_tip(g, A, lane, &A.fk);
+                B.ftip = seg_first_tip(g, B, lane, &B.fk);
+                mode = 2;
+              }
             }
           }
+          if (mode == 0 && lane == 0) atomicCAS(&s_fail, 0, 1);
+          if (mode != 0 && lane == 0) {
+            atomicAdd(&s_ntouch, 2);
+            tset_add(tset, tv_);
+            tset_add(tset, si.u);
+          }
+          if (lane == 0) {
+            pmsg[pair].mode = mode;
+            pmsg[pair].plan = pl;
+          }
+          if (mode == 2 && lane == 0) {
+            const int o = s_out[r];
+            out[o] = A;
+            out[o + 1] = B;
+            atomicAdd(&s_ntips, (A.ftip >= 0 ? 1 : 0) + (B.ftip >= 0 ? 1 : 0));
+          }
+          if (qi == trace_qi && lane == 0) {
+            atomicAdd(dbg + 56, (unsigned long long)(ck1 - ck0));
+            atomicAdd(dbg + 57, (unsigned long long)(clock64() - ck1));
+            atomicAdd(dbg + 59, 1ull);
+          }
         }
-        __syncwarp();
-        if (!ok) {
-          if (lane == 0) atomicCAS(&s_fail, 0, 1);
-          continue;
+        pair_sync(pair);  // the lead's message is ready
+        const int mode = pmsg[pair].mode;
+        if (mode == 1) {
+          const SplitPlan pl = pmsg[pair].plan;
+          const long long ck2 = clock64();
+          const SPiece C = seg_emit_child(g, X, pos, pl, hf, lane);
+          if (lane == 0) {
+            out[s_out[r] + hf] = C;
+            if (C.ftip >= 0) atomicAdd(&s_ntips, 1);
+            if (hf == 0 && qi == trace_qi) atomicAdd(dbg + 58, (unsigned long long)(clock64() - ck2));
+          }
         }
-        if (lane == 0) {
-          atomicAdd(&s_ntouch, 2);
-          tset_add(tset, tv_);
-          tset_add(tset, si.u);
-        }
-        long long ck2 = clock64();
-        A.ftip = seg_first_tip(g, A, lane, &A.fk);
-        B.ftip = seg_first_tip(g, B, lane, &B.fk);
-        long long ck3 = clock64();
-        if (qi == trace_qi && lane == 0) {
-          atomicAdd(dbg + 56, (unsigned long long)(ck1 - ck0));
-          atomicAdd(dbg + 57, (unsigned long long)(ck2 - ck1));
-          atomicAdd(dbg + 58, (unsigned long long)(ck3 - ck2));
-          atomicAdd(dbg + 59, 1ull);
-        }
-        if (lane == 0) {
-          int o = s_out[r];
-          out[o] = A;
-          out[o + 1] = B;
-          atomicAdd(&s_ntips, (A.ftip >= 0 ? 1 : 0) + (B.ftip >= 0 ? 1 : 0));
-        }
+        pair_sync(pair);  // message slot free again
       }
       __syncthreads();
       splits += ntips;

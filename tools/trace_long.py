@@ -50,10 +50,10 @@ if __name__ == "__main__":
         d = run()
         t0 = d[0]
         print("item L", d[2], "tips", d[3], "precompute us", (d[1] - t0) / 1e3)
-        print(f"splits {d[59]}: info {d[56] / max(d[59], 1):.0f} cyc, arcs {d[57] / max(d[59], 1):.0f} cyc, "
-              f"first tips {d[58] / max(d[59], 1):.0f} cyc per split")
+        print(f"splits {d[59]}: info {d[56] / max(d[59], 1):.0f} cyc, plan {d[57] / max(d[59], 1):.0f} cyc, "
+              f"emit + first tip of pa {d[58] / max(d[59], 1):.0f} cyc per split")
         ns = max(d[59], 1)
-        print(f"  arcs: cut {d[52] / ns:.0f} cyc, rotations {d[53] / ns:.0f} cyc, promote+emit {d[54] / ns:.0f} cyc, "
+        print(f"  plan: cut {d[52] / ns:.0f} cyc, rotations+alloc {d[53] / ns:.0f} cyc, "
               f"mean parent segments {d[55] / ns:.1f}")
         prev = d[1]
         for r in range(1, 48):
