@@ -1613,8 +1613,10 @@ __device__ __forceinline__ bool tset_has(const int32_t* set, int32_t x) {
   return false;
 }
 
-// two warps of a pair meet (named barrier 1 + pair; 0 is __syncthreads)
+// two warps of a pair meet (named barrier 1 + pair; 0 is __syncthreads); the
+// warp reconverges first (bar.sync is the .aligned form)
 __device__ __forceinline__ void pair_sync(int pair) {
+  __syncwarp();
   asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory");
 }
 struct PairMsg {

@@ -139,6 +139,40 @@ def test_host_c_abi_u1m_hashes(cuda):
         assert H(verts[:F].astype(np.int64)) == h["final_verts"]
 
 
+def test_graph_replay_soak_u1m(cuda):
+    """60 replays of the captured whole-path graph (device buffers) plus
+    profiled (non-graph) runs: every result byte-equal to the reference.
+    Guards the concurrent repair kernels (forked streams, warp-pair barriers,
+    look-back scans) against timing-dependent races and hangs."""
+    import torch
+    from paper_2204_05438_b200 import _capi
+    from paper_2204_05438_b200.io_formats import array_hash as H
+    h = load_hashes().get("u1m_unit")
+    if h is None:
+        pytest.skip("hashes.json has no u1m_unit entry")
+    tri = big_input("u1m_unit")
+    n, T = tri.n_vertices, tri.n_triangles
+    xy = torch.from_numpy(tri.vertices).to(cuda)
+    tr = torch.from_numpy(tri.triangles).to(cuda)
+    off = torch.empty(T + 1, dtype=torch.int64, device=cuda)
+    v = torch.empty(3 * T, dtype=torch.int32, device=cuda)
+    ctx = _capi.context(cuda)
+    npol, nsl = ctypes.c_int64(), ctypes.c_int64()
+    st = (ctypes.c_int64 * _capi.NUM_STATS)()
+    for k in range(66):
+        ctx.set_profiling(k >= 60)
+        rc = _capi.lib().tm_mesh_to_polygons(ctx.ptr, _capi.ptr(xy), n, _capi.ptr(tr), 64, T, 0, _capi.ptr(off),
+                                             _capi.ptr(v), T, 3 * T, ctypes.byref(npol), ctypes.byref(nsl), st,
+                                             _capi.stream_ptr(cuda))
+        ctx.check(rc)
+        if k % 10 == 0 or k >= 60:
+            P, F = npol.value, nsl.value
+            assert H(off[: P + 1].cpu().numpy()) == h["final_off"], k
+            assert H(v[:F].cpu().numpy().astype(np.int64)) == h["final_verts"], k
+    ctx.set_profiling(False)
+    ctx.segments(reset=True)
+
+
 def _gpu_vs_oracle(tri):
     r = oracle.execute(tri)
     lab = tm().label_all(tri, check=False)
