@@ -178,13 +178,40 @@ __device__ __forceinline__ int warp_compact3(unsigned flags, int lane, int32_t* 
   return base;
 }
 
+// Block-local twin matching (pass A).  Qhull emits the facets of one cone
+// together, so most twins sit a few indices apart (1M uniform: median distance
+// 4; 57% of the pairs inside one aligned 256-triangle block).  Each block
+// matches its own half-edges in a shared-memory table first and labels those
+// pairs on the spot; only the rest go through the global table.
+constexpr int kLocalBits = 10;
+constexpr int kLocalSlots = 1 << kLocalBits;  // >= 2 x the block's ascending half-edges (<= 2 per triangle)
+constexpr int32_t kLocalMatched = (int32_t)0x80000000;
+
+__device__ __forceinline__ uint32_t local_slot(int32_t lo, int32_t hi) {
+  return ((uint32_t)lo * 0x9E3779B1u + (uint32_t)hi * 0x85EBCA77u) >> (32 - kLocalBits);
+}
+
+// label the edge pair h (descending, own triangle tt, own longest-edge flag `own`)
+// + hc (partner, its longest-edge flag `other`): labeling.py:65-115
+__device__ __forceinline__ void label_pair(int32_t* __restrict__ hw, uint8_t* __restrict__ seed, int32_t h, bool own,
+                                           int32_t hc, bool other) {
+  const int32_t tt = h / 3, tc = hc / 3;
+  const int32_t fr = (!own && !other) ? 1 : 0;
+  hw[h] = (hc << 1) | fr;
+  hw[hc] = (h << 1) | fr;
+  if (own) seed[tt] = (other && tt < tc) ? 1 : 0;
+  if (other) seed[tc] = (own && tc < tt) ? 1 : 0;
+}
+
 // Pass A (K1 + first half of K0), one thread per triangle: corners -> tri32,
 // fp64 longest edge -> max_edge, orientation check, trivertex (atomicMin, a
-// fire-and-forget RED), provisional labels (hw = border, seed = 1); then the
-// warp's ascending half-edges (origin < target) go into the twin table on
-// dense lanes.
+// fire-and-forget RED), provisional labels (hw = border, seed = 1); the
+// block-local pairs are matched and labelled (not in check mode, where every
+// ascending half-edge goes to the global table so that the claim bits see all
+// partners); then the warp's remaining ascending half-edges (origin < target)
+// go into the twin table on dense lanes.
 template <typename TI>
-__global__ void __launch_bounds__(kLabelThreads) k_tri_pass(const double2* __restrict__ xy, int64_t n,
+__global__ void __launch_bounds__(kLabelThreads, 4) k_tri_pass(const double2* __restrict__ xy, int64_t n,
                                                             const TI* __restrict__ tri, int64_t t_begin,
                                                             int64_t T,
                                                             int32_t* __restrict__ tri32, int8_t* __restrict__ max_edge,
@@ -192,10 +219,19 @@ __global__ void __launch_bounds__(kLabelThreads) k_tri_pass(const double2* __res
                                                             uint8_t* __restrict__ seed, int32_t* __restrict__ tv,
                                                             int check, DevStatus* st) {
   __shared__ int32_t sq[kLabelWarps][3][96];
+  __shared__ unsigned long long lkey[kLocalSlots];
+  __shared__ int32_t lval[kLocalSlots];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool local = !check;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t t = t_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t - lane < T; t += stride) {
-    unsigned flags = 0;
+  for (int64_t base = t_begin + blockIdx.x * (int64_t)blockDim.x; base < T; base += stride) {
+    const int64_t t = base + threadIdx.x;
+    if (local) {
+      for (int i = threadIdx.x; i < kLocalSlots; i += kLabelThreads) lkey[i] = kEmptySlot;
+      __syncthreads();
+    }
+    unsigned flags = 0, desc = 0;
+    int me0 = -1;
     int32_t hh[3], oo[3], gg[3];
     if (t < T) {
       int64_t a = (int64_t)__ldg(tri + 3 * t), b = (int64_t)__ldg(tri + 3 * t + 1), c = (int64_t)__ldg(tri + 3 * t + 2);
@@ -215,7 +251,7 @@ __global__ void __launch_bounds__(kLabelThreads) k_tri_pass(const double2* __res
         }
         double2 pa = xy[a], pb = xy[b], pc = xy[c];
         // labeling.py:55-59: edge 0 joins corners 1-2, edge 1 joins 2-0, edge 2 joins 0-1
-        const int me0 = argmax3(sqlen(pb, pc), sqlen(pc, pa), sqlen(pa, pb));
+        me0 = argmax3(sqlen(pb, pc), sqlen(pc, pa), sqlen(pa, pb));
         max_edge[t] = (int8_t)me0;
         if (check) {
           // mesh_core.signed_areas (160-168), sign only, unfused
@@ -231,19 +267,60 @@ __global__ void __launch_bounds__(kLabelThreads) k_tri_pass(const double2* __res
         }
         // half-edge j: origin corner (j+1)%3, target corner (j+2)%3; queued as (h << 1) | longest
         const int32_t cv[3] = {(int32_t)a, (int32_t)b, (int32_t)c};
-        const int me = me0;
 #pragma unroll
         for (int j = 0; j < 3; j++) {
-          hh[j] = (int32_t)(((3 * t + j) << 1) | (me == j ? 1 : 0));
+          hh[j] = (int32_t)(((3 * t + j) << 1) | (me0 == j ? 1 : 0));
           oo[j] = cv[(j + 1) % 3];
           gg[j] = cv[(j + 2) % 3];
           if (oo[j] < gg[j]) flags |= 1u << j;
+          else if (oo[j] > gg[j]) desc |= 1u << j;
         }
       }
+    }
+    if (local) {
+      int lslot[3] = {-1, -1, -1};
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        if (!((flags >> j) & 1u)) continue;
+        const unsigned long long key = ((unsigned long long)(uint32_t)oo[j] << 32) | (uint32_t)gg[j];
+        uint32_t sl = local_slot(oo[j], gg[j]);
+        for (;;) {
+          unsigned long long prev = atomicCAS(&lkey[sl], kEmptySlot, key);
+          if (prev == kEmptySlot) {
+            lval[sl] = hh[j];
+            lslot[j] = (int)sl;
+            break;
+          }
+          if (prev == key) break;  // duplicate ascending key: left to the global table, which reports it
+          sl = (sl + 1) & (kLocalSlots - 1);
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        if (!((desc >> j) & 1u)) continue;
+        const unsigned long long key = ((unsigned long long)(uint32_t)gg[j] << 32) | (uint32_t)oo[j];
+        uint32_t sl = local_slot(gg[j], oo[j]);
+        for (;;) {
+          const unsigned long long k = lkey[sl];
+          if (k == kEmptySlot) break;
+          if (k == key) {
+            const int32_t pl = atomicOr(&lval[sl], kLocalMatched);
+            if (!(pl & kLocalMatched)) label_pair(hw, seed, (int32_t)(3 * t + j), me0 == j, pl >> 1, (pl & 1) != 0);
+            break;
+          }
+          sl = (sl + 1) & (kLocalSlots - 1);
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 3; j++)
+        if (lslot[j] >= 0 && (lval[lslot[j]] & kLocalMatched)) flags &= ~(1u << j);
     }
     int m = warp_compact3(flags, lane, sq[wid][0], sq[wid][1], sq[wid][2], hh, oo, gg);
     for (int i = lane; i < m; i += 32) table_insert(tb, st, sq[wid][0][i], sq[wid][1][i], sq[wid][2][i]);
     __syncwarp();
+    if (local) __syncthreads();  // lkey/lval are reset at the top of the next chunk
   }
 }
 
@@ -269,12 +346,14 @@ __global__ void __launch_bounds__(kLabelThreads) k_pair_pass(const int32_t* __re
     if (t < T) {
       const int32_t cv[3] = {__ldg(tri32 + 3 * t), __ldg(tri32 + 3 * t + 1), __ldg(tri32 + 3 * t + 2)};
       if ((uint32_t)cv[0] < (uint32_t)n && (uint32_t)cv[1] < (uint32_t)n && (uint32_t)cv[2] < (uint32_t)n) {
+        // a descending half-edge pass A already paired inside its block is no longer border
+        const int32_t w[3] = {hw[3 * t], hw[3 * t + 1], hw[3 * t + 2]};
 #pragma unroll
         for (int j = 0; j < 3; j++) {
           hh[j] = (int32_t)(3 * t + j);
           oo[j] = cv[(j + 1) % 3];
           gg[j] = cv[(j + 2) % 3];
-          if (oo[j] > gg[j]) flags |= 1u << j;
+          if (oo[j] > gg[j] && w[j] == -1) flags |= 1u << j;
         }
       }
     }
@@ -283,15 +362,8 @@ __global__ void __launch_bounds__(kLabelThreads) k_pair_pass(const int32_t* __re
       const int32_t h = sq[wid][0][i];
       const int32_t pl = table_lookup(tb, st, check, sq[wid][2][i], sq[wid][1][i], h / 3);
       if (pl < 0) continue;  // border
-      const int32_t hc = pl >> 1;
       const int32_t tt = h / 3, j = h - 3 * tt;
-      const int32_t tc = hc / 3;
-      const bool own = __ldg(max_edge + tt) == j, other = (pl & 1) != 0;
-      const int32_t fr = (!own && !other) ? 1 : 0;
-      hw[h] = (hc << 1) | fr;
-      hw[hc] = (h << 1) | fr;
-      if (own) seed[tt] = (other && tt < tc) ? 1 : 0;
-      if (other) seed[tc] = (own && tc < tt) ? 1 : 0;
+      label_pair(hw, seed, h, __ldg(max_edge + tt) == j, pl >> 1, (pl & 1) != 0);
     }
     __syncwarp();
   }
