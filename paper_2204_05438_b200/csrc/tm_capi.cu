@@ -54,7 +54,7 @@ struct Counters {
   int64_t p_in;        // repair input polygon count (tm_repair called with a host count)
   int64_t p_out;       // P': polygons after repair
   int64_t f_out;       // F': vertex slots after repair
-  unsigned int n_overflow, n_items, n_long, pad;
+  unsigned int n_overflow, n_items, n_long, n_pinch;
   unsigned int q_huge, q_long, q_next, n_parked;
   unsigned long long pool_top, undo_top;
   unsigned long long stats[8];
@@ -117,7 +117,7 @@ struct tm_ctx {
   Buf seeds, start, len, overflow, queue, stamp, tiles, nrul, eoff, rnext, rdist, rprev, startbits, ent_r, ent_base;
   // repair
   Buf item_of, items, long_list, item_list, item_n, item_slots, item_state, item_depth, cnt, slotsz, pbase, sbase, pool,
-      undo, hugeq, longq, parked;
+      undo, hugeq, longq, parked, pinchq;
   // whole-path buffers
   Buf xy, tri, tri32, hw, max_edge, seed, tv, off0, v0, fin_off, fin_v, hw_snap, hv;
   cudaStream_t gstream = nullptr;
@@ -337,6 +337,7 @@ static int prepare(tm_ctx* ctx, int64_t T, int64_t n = -1) {
   ENSURE(item_depth, Tn * sizeof(int32_t));
   ENSURE(hugeq, Tn * sizeof(int32_t));
   ENSURE(parked, Tn * sizeof(int32_t));
+  ENSURE(pinchq, Tn * sizeof(int32_t));
   ENSURE(longq, Tn * sizeof(int32_t));
   ENSURE(cnt, (Tn + 1) * sizeof(int64_t));
   ENSURE(slotsz, (Tn + 1) * sizeof(int64_t));
@@ -441,7 +442,8 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
   int64_t Tn = T > 0 ? T : 1;
   int64_t* tiles = ctx->tiles.as<int64_t>();
   LongQueue q{ctx->hugeq.as<int32_t>(), ctx->longq.as<int32_t>(), &dc->q_huge,        &dc->q_long,
-              &dc->q_next,           ctx->parked.as<int32_t>(), &dc->n_parked};
+              &dc->q_next,           ctx->parked.as<int32_t>(), &dc->n_parked,
+              ctx->pinchq.as<int32_t>(), &dc->n_pinch};
   {
     SegTimer t_(ctx, S_CLASSIFY, s);
     launch_classify(d_off_in, d_v_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(), &dc->n_items,
@@ -538,7 +540,7 @@ static int retry_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, cons
     ENSURE(pool, ctx->pool_cap * sizeof(int32_t));
     // reset the repair-side counters and the status; keep the traversal counts
     CK(cudaMemcpyAsync(&dc->st, &ctx->h_reset->st, sizeof(DevStatus), cudaMemcpyHostToDevice, s));
-    CK(cudaMemsetAsync(&dc->n_items, 0, 2 * sizeof(unsigned int), s));
+    CK(cudaMemsetAsync(&dc->n_items, 0, 3 * sizeof(unsigned int), s));  // n_items, n_long, n_pinch
     CK(cudaMemsetAsync(&dc->q_huge, 0, 4 * sizeof(unsigned int), s));
     CK(cudaMemsetAsync(&dc->pool_top, 0, 10 * sizeof(unsigned long long), s));
     r = enqueue_repair(ctx, d_tri32, d_hw, d_tv, T, d_off_in, d_v_in, Pp, d_off_out, d_v_out, s);
@@ -567,7 +569,7 @@ void tm_ctx_destroy(tm_ctx* ctx) {
   Buf* bufs[] = {&ctx->counters, &ctx->slots, &ctx->seeds, &ctx->start, &ctx->len, &ctx->overflow, &ctx->queue,
                  &ctx->stamp, &ctx->tiles, &ctx->nrul, &ctx->eoff, &ctx->rnext, &ctx->rdist, &ctx->rprev, &ctx->startbits,
                  &ctx->ent_r, &ctx->ent_base, &ctx->item_of, &ctx->items, &ctx->long_list, &ctx->item_list,
-                 &ctx->item_n, &ctx->item_slots, &ctx->item_state, &ctx->item_depth, &ctx->hugeq, &ctx->longq, &ctx->parked, &ctx->cnt, &ctx->slotsz, &ctx->pbase, &ctx->sbase, &ctx->pool,
+                 &ctx->item_n, &ctx->item_slots, &ctx->item_state, &ctx->item_depth, &ctx->hugeq, &ctx->longq, &ctx->parked, &ctx->pinchq, &ctx->cnt, &ctx->slotsz, &ctx->pbase, &ctx->sbase, &ctx->pool,
                  &ctx->undo, &ctx->xy, &ctx->tri, &ctx->tri32, &ctx->hw, &ctx->max_edge, &ctx->seed, &ctx->tv,
                  &ctx->off0, &ctx->v0, &ctx->fin_off, &ctx->fin_v, &ctx->hw_snap, &ctx->hv,
                  &ctx->lbscan};

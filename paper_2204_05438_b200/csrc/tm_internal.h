@@ -68,6 +68,8 @@ struct LongQueue {       // work items longer than kLongMin, longest class first
   unsigned int* next;
   int32_t* parked;         // short items whose pinch pass waits for the global guard
   unsigned int* n_parked;
+  int32_t* pinchq;         // short items with a pinch candidate left after the tip phase
+  unsigned int* n_pinch;
 };
 struct RepairArgs {
   const int32_t* tri;

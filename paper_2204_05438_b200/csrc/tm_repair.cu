@@ -1130,20 +1130,32 @@ __device__ void warp_finish_pinch(const RepairCtx& c, int64_t w, int32_t poly, l
 // Item states (item_state[w]): 0 = not started, 1 = finished by the shared-
 // memory kernel, 2 = resume from item_list/item_n/item_depth in the pool.
 
+// With a pinch queue (short items, k_repair_tips mode 0): an item without a
+// pinch candidate (no repeated leaf; the tip phase left no tips) is complete
+// here and gets its output size; the others are queued for k_repair_pinch.
 __device__ void finish_item(const RepairCtx& c, int64_t w, long long list, int n, long long depth, long long splits,
-                            int lane, int64_t* item_list, int32_t* item_n, unsigned long long* stats, int2* stab) {
+                            int lane, int64_t* item_list, int32_t* item_n, unsigned long long* stats, int2* stab,
+                            int64_t* item_slots = nullptr, int32_t* pq = nullptr, unsigned int* n_pq = nullptr) {
   // repeated flags and extra visits of the leaves (pinch guard, reparation.py:322)
   unsigned long long ex_sum = 0;
+  long long slots = 0;
+  int elig = 0;
   for (int r = 0; r < n; r++) {
     uint32_t ro = (uint32_t)c.pool[list + 2 * r], rl = (uint32_t)c.pool[list + 2 * r + 1];
     int ex = warp_dup_scan(c, c.pool + ro, (int)(rl & LEN_MASK), lane, nullptr, nullptr, stab);
     if (ex > 0 && lane == 0) c.pool[list + 2 * r + 1] = (int32_t)(rl | F_REP);
     ex_sum += ex;
+    slots += rl & LEN_MASK;
+    elig += (ex > 0 && !(rl & (F_TIP | F_FAIL))) ? 1 : 0;
   }
   __syncwarp();
   if (lane == 0) {
     item_list[w] = list;
     item_n[w] = n;
+    if (pq) {
+      if (elig == 0) item_slots[w] = slots;
+      else pq[atomicAdd(n_pq, 1u)] = (int32_t)w;
+    }
     if (depth > 0) atomicMax(stats + 0, (unsigned long long)depth);
     if (splits) atomicAdd(stats + 1, (unsigned long long)splits);
     if (ex_sum) atomicAdd(stats + 5, ex_sum);
@@ -1269,7 +1281,9 @@ __global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, con
       if (lane == 0) { item_list[w] = -1; item_n[w] = 0; item_slots[w] = 0; }
       continue;
     }
-    finish_item(c, w, list, n, depth, splits, lane, item_list, item_n, stats, s_dup[wib]);
+    if (mode) finish_item(c, w, list, n, depth, splits, lane, item_list, item_n, stats, s_dup[wib]);
+    else finish_item(c, w, list, n, depth, splits, lane, item_list, item_n, stats, s_dup[wib], item_slots, q.pinchq,
+                     q.n_pinch);
   }
 }
 
@@ -2073,16 +2087,12 @@ __global__ void __launch_bounds__(128) k_repair_pinch(RepairCtx c, const int32_t
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   if (mode == 0) {
     PinchPark park{item_state, item_depth, q.parked, q.n_parked};
-    const unsigned int ni = *n_items;
-    for (int64_t w = warp; w < ni; w += nwarps) {
-      const int32_t i = items[w];
-      if (off[i + 1] - off[i] > kLongMin) continue;  // long item: mode 1
-      const long long list = item_list[w];
-      if (list < 0) {
-        if (lane == 0) item_slots[w] = 0;
-        continue;
-      }
-      warp_finish_pinch(c, w, i, list, item_n[w], lane, item_list, item_n, item_slots, stats, guard, stab, 0, park);
+    // the short items finish_item queued (the rest are complete or failed)
+    const unsigned int np = *q.n_pinch;
+    for (int64_t k = warp; k < np; k += nwarps) {
+      const int64_t w = q.pinchq[k];
+      warp_finish_pinch(c, w, items[w], item_list[w], item_n[w], lane, item_list, item_n, item_slots, stats, guard,
+                        stab, 0, park);
     }
     return;
   }
