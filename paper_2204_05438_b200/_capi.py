@@ -12,7 +12,8 @@ import threading
 from .errors import CapacityError, StructuralError, TermeshError, ValidationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtermesh_b200.so")
+# TERMESH_LIB_VARIANT: an alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("TERMESH_LIB_VARIANT") or os.path.join(_HERE, "libtermesh_b200.so")
 
 TM_OK, TM_ERR_STRUCTURAL, TM_ERR_VALIDATION, TM_ERR_CAPACITY, TM_ERR_CUDA, TM_ERR_ARGUMENT = range(6)
 NUM_KINDS = 16

@@ -56,6 +56,7 @@ struct Counters {
   int64_t f_out;       // F': vertex slots after repair
   unsigned int n_overflow, n_items, n_long, n_pinch;
   unsigned int q_huge, q_long, q_next, n_parked;
+  unsigned int tip_next, pad1, pad2, pad3;
   unsigned long long pool_top, undo_top;
   unsigned long long stats[8];
   unsigned long long dbg[128];  // optional kernel timestamps / counters (tm_ctx_debug)
@@ -443,7 +444,7 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
   int64_t* tiles = ctx->tiles.as<int64_t>();
   LongQueue q{ctx->hugeq.as<int32_t>(), ctx->longq.as<int32_t>(), &dc->q_huge,        &dc->q_long,
               &dc->q_next,           ctx->parked.as<int32_t>(), &dc->n_parked,
-              ctx->pinchq.as<int32_t>(), &dc->n_pinch};
+              ctx->pinchq.as<int32_t>(), &dc->n_pinch, &dc->tip_next};
   {
     SegTimer t_(ctx, S_CLASSIFY, s);
     launch_classify(d_off_in, d_v_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(), &dc->n_items,
@@ -541,7 +542,7 @@ static int retry_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, cons
     // reset the repair-side counters and the status; keep the traversal counts
     CK(cudaMemcpyAsync(&dc->st, &ctx->h_reset->st, sizeof(DevStatus), cudaMemcpyHostToDevice, s));
     CK(cudaMemsetAsync(&dc->n_items, 0, 3 * sizeof(unsigned int), s));  // n_items, n_long, n_pinch
-    CK(cudaMemsetAsync(&dc->q_huge, 0, 4 * sizeof(unsigned int), s));
+    CK(cudaMemsetAsync(&dc->q_huge, 0, 8 * sizeof(unsigned int), s));  // queues + tip_next
     CK(cudaMemsetAsync(&dc->pool_top, 0, 10 * sizeof(unsigned long long), s));
     r = enqueue_repair(ctx, d_tri32, d_hw, d_tv, T, d_off_in, d_v_in, Pp, d_off_out, d_v_out, s);
     if (r) return r;

@@ -70,6 +70,7 @@ struct LongQueue {       // work items longer than kLongMin, longest class first
   unsigned int* n_parked;
   int32_t* pinchq;         // short items with a pinch candidate left after the tip phase
   unsigned int* n_pinch;
+  unsigned int* tip_next;  // work counter of k_repair_tips mode 0 (persistent warps)
 };
 struct RepairArgs {
   const int32_t* tri;

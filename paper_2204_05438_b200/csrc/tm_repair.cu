@@ -1164,7 +1164,7 @@ __device__ void finish_item(const RepairCtx& c, int64_t w, long long list, int n
 
 // One warp per work item.  item_list[w] = pool offset of the item's record
 // list, item_n[w] = #records (leaves in the reference's raw order).
-__global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, const int32_t* __restrict__ items,
+__global__ void __launch_bounds__(32 * kTipWarps, 8) k_repair_tips(RepairCtx c, const int32_t* __restrict__ items,
                                                                 const unsigned int* n_items,
                                                                 const int64_t* __restrict__ off,
                                                                 const int32_t* __restrict__ v,
@@ -1186,7 +1186,13 @@ __global__ void __launch_bounds__(32 * kTipWarps) k_repair_tips(RepairCtx c, con
   long long max_rounds = (long long)stats[2] + 1;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t wq = warp; wq < ni; wq += nwarps) {
+  // mode 0: persistent warps pull items from a counter (item costs vary by 10x)
+  auto next_item = [&]() -> int64_t {
+    unsigned int x = 0;
+    if (lane == 0) x = atomicAdd(q.tip_next, 1u);
+    return (int64_t)__shfl_sync(kFull, x, 0);
+  };
+  for (int64_t wq = mode ? warp : next_item(); wq < ni; wq = mode ? wq + nwarps : next_item()) {
     const int64_t w = !mode ? wq : (wq < nh ? q.huge[wq] : q.longq[wq - nh]);
     int32_t i = items[w];
     int64_t b = off[i];
@@ -2282,7 +2288,19 @@ void launch_repair_tips_long(const RepairArgs& a, cudaStream_t s) {
     seg_cap = (e && *e) ? atoi(e) : kSegCap;
     if (seg_cap > kSegCap) seg_cap = kSegCap;
   }
-  k_repair_tips_seg<<<kNumSMs, 32 * kSegWarps, smem, s>>>(c, a.items, a.off, a.v, a.item_list, a.item_n,
+  // Blocks of this kernel fill an SM's shared memory, so every SM it holds is
+  // closed to the short-item kernel running beside it.  The long items are few
+  // (~17 per 1M triangles) and the longest runs first, so a small grid keeps the
+  // lineage on time and leaves the other SMs to the short items: 24 blocks up
+  // to 20M triangles (measured best at 1M and 10M, 16-24), proportionally more above.
+  static int env_blk = -1;
+  if (env_blk < 0) {  // tuning hook: TERMESH_SEG_BLOCKS
+    const char* e = getenv("TERMESH_SEG_BLOCKS");
+    env_blk = (e && *e) ? atoi(e) : 0;
+  }
+  long long nblk = env_blk > 0 ? env_blk : 24 * (a.T / 20000000 + 1);
+  if (nblk > kNumSMs) nblk = kNumSMs;
+  k_repair_tips_seg<<<(int)nblk, 32 * kSegWarps, smem, s>>>(c, a.items, a.off, a.v, a.item_list, a.item_n,
                                                            a.item_state, a.item_depth, a.item_slots, a.stats, a.q,
                                                            a.dbg,
                                                            (unsigned int)trace_qi, seg_cap);
@@ -2292,7 +2310,12 @@ void launch_repair_tips_long(const RepairArgs& a, cudaStream_t s) {
 void launch_repair_tips(const RepairArgs& a, int mode, cudaStream_t s) {
   RepairCtx c{a.tri, a.hw, a.tv, a.T, a.pool, a.pool_cap, a.pool_top, a.undo, a.undo_top, a.undo_cap, a.st, a.tv_exact,
               a.dbg};
-  k_repair_tips<<<mode ? kNumSMs : kNumSMs * 8, 32 * kTipWarps, 0, s>>>(
+  static int resident = 0;
+  if (!resident) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_repair_tips, 32 * kTipWarps, 0);
+    if (resident < 1) resident = 1;
+  }
+  k_repair_tips<<<mode ? kNumSMs : kNumSMs * resident, 32 * kTipWarps, 0, s>>>(
       c, a.items, a.n_items, a.off, a.v, a.item_list, a.item_n, a.item_state, a.item_depth, a.item_slots, a.stats,
       a.q, mode);
   note_launch(1);

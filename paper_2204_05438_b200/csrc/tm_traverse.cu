@@ -140,13 +140,33 @@ __device__ __forceinline__ void walk_ruler(const int32_t* __restrict__ hw, const
   rprev[g] = cur;  // every ruler is the successor of exactly one ruler of its cycle
 }
 
+// About one half-edge in nine starts a walk, so a warp first gathers the rulers
+// of a 256-half-edge tile into a shared queue and then walks them on all lanes
+// (a thread-per-half-edge loop keeps ~3 of 32 lanes walking).
+constexpr int kWalkTile = 8;  // 32-wide chunks per warp tile
 __global__ void __launch_bounds__(256) k_ruler_walk(const int32_t* __restrict__ hw, RulerSet rs, long long limit,
                                                     int32_t* __restrict__ rnext, int32_t* __restrict__ rdist,
                                                     int32_t* __restrict__ rprev, uint32_t* vbits, DevStatus* st) {
-  for (int64_t h = rs.hb + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < rs.he;
-       h += (int64_t)gridDim.x * blockDim.x) {
-    if (!hw_front(hw[h]) || !is_ruler(rs, (int32_t)h)) continue;
-    walk_ruler(hw, rs, (int32_t)h, limit, rnext, rdist, rprev, vbits, st);
+  __shared__ int32_t s_q[8][32 * kWalkTile];
+  const int lane = threadIdx.x & 31;
+  int32_t* q = s_q[threadIdx.x >> 5];
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t tile = 32 * kWalkTile;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = rs.hb + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * tile; base < rs.he;
+       base += nwarps * tile) {
+    int n = 0;
+#pragma unroll
+    for (int c = 0; c < kWalkTile; c++) {
+      const int64_t h = base + c * 32 + lane;
+      const bool r = h < rs.he && hw_front(hw[h]) && is_ruler(rs, (int32_t)h);
+      const unsigned m = __ballot_sync(0xffffffffu, r);
+      if (r) q[n + __popc(m & lt)] = (int32_t)h;
+      n += __popc(m);
+    }
+    __syncwarp();
+    for (int k = lane; k < n; k += 32) walk_ruler(hw, rs, q[k], limit, rnext, rdist, rprev, vbits, st);
+    __syncwarp();
   }
 }
 
