@@ -123,7 +123,10 @@ struct tm_ctx {
   Buf xy, tri, tri32, hw, max_edge, seed, tv, off0, v0, fin_off, fin_v, hw_snap, hv;
   cudaStream_t gstream = nullptr;
   cudaStream_t aux = nullptr;                            // long repair items run beside the short ones
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_cls = nullptr;
+  // whole-path runs: the long polygons are written, classified and repaired on
+  // ctx->aux right after the traversal's chain pass (enqueue_traverse)
+  bool early_long = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cudaGraphExec_t graph = nullptr;
@@ -308,6 +311,7 @@ static int prepare(tm_ctx* ctx, int64_t T, int64_t n = -1) {
   if (!ctx->aux) CK(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
   if (!ctx->ev_fork) CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
   if (!ctx->ev_join) CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  if (!ctx->ev_cls) CK(cudaEventCreateWithFlags(&ctx->ev_cls, cudaEventDisableTiming));
   int64_t Tn = T > 0 ? T : 1;
   if (n >= 0) ENSURE(slots, hash_bytes(n, Tn));
   ENSURE(seeds, Tn * sizeof(int32_t));
@@ -385,6 +389,25 @@ static void part_range(const tm_ctx* ctx, int64_t T, int64_t* tb, int64_t* te) {
   *te = e;
 }
 
+static LongQueue long_queue(tm_ctx* ctx) {
+  Counters* dc = dc_of(ctx);
+  return LongQueue{ctx->hugeq.as<int32_t>(), ctx->longq.as<int32_t>(), &dc->q_huge,      &dc->q_long,
+                   &dc->q_next,           ctx->parked.as<int32_t>(), &dc->n_parked, ctx->pinchq.as<int32_t>(),
+                   &dc->n_pinch,          &dc->tip_next};
+}
+
+static RepairArgs repair_args(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, const int32_t* d_tv, int64_t T,
+                              const int64_t* d_off_in, const int32_t* d_v_in) {
+  Counters* dc = dc_of(ctx);
+  const int64_t Tn = T > 0 ? T : 1;
+  const int tv_exact = ctx->path_hv == nullptr;
+  return RepairArgs{d_tri32, d_hw, d_tv, tv_exact, T, ctx->pool.as<int32_t>(), ctx->pool_cap, &dc->pool_top,
+                    ctx->undo.as<int32_t>(), &dc->undo_top, (unsigned long long)Tn + 1024, &dc->st,
+                    ctx->items.as<int32_t>(), &dc->n_items, d_off_in, d_v_in, ctx->item_list.as<int64_t>(),
+                    ctx->item_n.as<int32_t>(), ctx->item_slots.as<int64_t>(), ctx->item_state.as<int32_t>(),
+                    ctx->item_depth.as<int32_t>(), dc->stats, long_queue(ctx), dc->dbg};
+}
+
 static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* d_hw, const uint8_t* d_seed,
                             int64_t T, int64_t* d_off, int32_t* d_v, cudaStream_t s) {
   Counters* dc = dc_of(ctx);
@@ -413,8 +436,8 @@ static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* 
     SegTimer t_(ctx, S_TRAV_LEN, s);
     launch_chain_count(ctx->seeds.as<int32_t>(), ctx->start.as<int32_t>(), &dc->n_seeds, Tn, T,
                        ctx->rnext.as<int32_t>(), ctx->rdist.as<int32_t>(), ctx->rprev.as<int32_t>(),
-                       ctx->len.as<int64_t>(),
-                       ctx->nrul.as<int64_t>(), &dc->st, s);
+                       ctx->len.as<int64_t>(), ctx->nrul.as<int64_t>(),
+                       ctx->early_long ? ctx->long_list.as<int32_t>() : nullptr, &dc->n_long, &dc->st, s);
   }
   {
     SegTimer t_(ctx, S_TRAV_SCAN, s);
@@ -428,6 +451,24 @@ static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* 
     launch_chain_emit(ctx->start.as<int32_t>(), &dc->n_seeds, Tn, ctx->rnext.as<int32_t>(), ctx->rdist.as<int32_t>(),
                       ctx->rprev.as<int32_t>(), d_off, ctx->eoff.as<int64_t>(), ctx->ent_r.as<int32_t>(), ctx->ent_base.as<int64_t>(),
                       ctx->ecap, &dc->st, s);
+    if (ctx->early_long) {
+      // fork: the long polygons' runs -> their classification -> the long-item
+      // repair kernel, on ctx->aux beside the rest of the traversal and the short items
+      cudaStream_t a = ctx->aux;
+      CK(cudaEventRecord(ctx->ev_fork, s));
+      CK(cudaStreamWaitEvent(a, ctx->ev_fork, 0));
+      launch_ruler_write_list(d_tri32, d_hw, ctx->long_list.as<int32_t>(), &dc->n_long, ctx->eoff.as<int64_t>(),
+                              ctx->ent_r.as<int32_t>(), ctx->ent_base.as<int64_t>(), ctx->rdist.as<int32_t>(), T, Tn,
+                              d_v, ctx->path_hv, a);
+      launch_classify(d_off, d_v, &dc->n_seeds, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(),
+                      &dc->n_items, ctx->long_list.as<int32_t>(), &dc->n_long, dc->stats, long_queue(ctx),
+                      ctx->path_hv, ctx->tv.as<int32_t>(), 2, a);
+      CK(cudaEventRecord(ctx->ev_cls, a));
+      CK(cudaMemsetAsync(ctx->item_state.p, 0, Tn * sizeof(int32_t), a));
+      launch_repair_tips_long(repair_args(ctx, d_tri32, const_cast<int32_t*>(d_hw), ctx->tv.as<int32_t>(), T, d_off, d_v),
+                              a);
+      CK(cudaEventRecord(ctx->ev_join, a));
+    }
     launch_ruler_write(d_tri32, d_hw, &dc->n_entries, ctx->ent_r.as<int32_t>(), ctx->ent_base.as<int64_t>(),
                        ctx->rdist.as<int32_t>(), T, ctx->ecap, d_v, ctx->path_hv, s);
   }
@@ -441,44 +482,37 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
                           int32_t* d_v_out, cudaStream_t s) {
   Counters* dc = dc_of(ctx);
   int64_t Tn = T > 0 ? T : 1;
-  int64_t* tiles = ctx->tiles.as<int64_t>();
-  LongQueue q{ctx->hugeq.as<int32_t>(), ctx->longq.as<int32_t>(), &dc->q_huge,        &dc->q_long,
-              &dc->q_next,           ctx->parked.as<int32_t>(), &dc->n_parked,
-              ctx->pinchq.as<int32_t>(), &dc->n_pinch, &dc->tip_next};
+  LongQueue q = long_queue(ctx);
+  const bool early = ctx->early_long;  // the long items already run on ctx->aux (enqueue_traverse)
   {
     SegTimer t_(ctx, S_CLASSIFY, s);
     launch_classify(d_off_in, d_v_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(), &dc->n_items,
                     ctx->long_list.as<int32_t>(), &dc->n_long, dc->stats, q, ctx->path_hv,
-                    const_cast<int32_t*>(d_tv), s);
+                    const_cast<int32_t*>(d_tv), early ? 1 : 0, s);
   }
-  CK(cudaMemsetAsync(ctx->item_state.p, 0, Tn * sizeof(int32_t), s));
-  const int tv_exact = ctx->path_hv == nullptr;
-
-  RepairArgs a{d_tri32, d_hw, d_tv, tv_exact, T, ctx->pool.as<int32_t>(), ctx->pool_cap, &dc->pool_top, ctx->undo.as<int32_t>(),
-               &dc->undo_top, (unsigned long long)Tn + 1024, &dc->st, ctx->items.as<int32_t>(), &dc->n_items,
-               d_off_in, d_v_in, ctx->item_list.as<int64_t>(), ctx->item_n.as<int32_t>(),
-               ctx->item_slots.as<int64_t>(), ctx->item_state.as<int32_t>(), ctx->item_depth.as<int32_t>(),
-               dc->stats, q, dc->dbg};
+  if (early) CK(cudaStreamWaitEvent(s, ctx->ev_cls, 0));  // the item list is complete
+  else CK(cudaMemsetAsync(ctx->item_state.p, 0, Tn * sizeof(int32_t), s));
+  RepairArgs a = repair_args(ctx, d_tri32, d_hw, d_tv, T, d_off_in, d_v_in);
   {
     SegTimer t_(ctx, S_REPAIR_TIPS, s);
     // fork: the long items (one block each) on ctx->aux beside the short ones
     static int serial = -1;
     if (serial < 0) serial = getenv("TERMESH_SERIAL_REPAIR") != nullptr;  // debug: no fork
-    cudaStream_t sl = serial ? s : ctx->aux;
-    if (!serial) {
-      CK(cudaEventRecord(ctx->ev_fork, s));
-      CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
+    if (!early) {
+      cudaStream_t sl = serial ? s : ctx->aux;
+      if (!serial) {
+        CK(cudaEventRecord(ctx->ev_fork, s));
+        CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
+      }
+      launch_repair_tips_long(a, sl);
+      if (!serial) CK(cudaEventRecord(ctx->ev_join, ctx->aux));
     }
-    launch_repair_tips_long(a, sl);
     launch_repair_tips(a, 0, s);
     {
       SegTimer t_(ctx, S_REPAIR_PINCH, s);
       launch_repair_pinch(a, 0, s);  // short items' pinch pass, still beside the long items
     }
-    if (!serial) {
-      CK(cudaEventRecord(ctx->ev_join, ctx->aux));
-      CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
-    }
+    if (early || !serial) CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
     launch_repair_tips(a, 1, s);  // long items the shared-memory kernel handed back
   }
   {
@@ -488,7 +522,7 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
   {
     SegTimer t_(ctx, S_STITCH, s);
     launch_out_counts(d_off_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->item_n.as<int32_t>(),
-                      ctx->item_slots.as<int64_t>(), ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), nullptr,
+                      ctx->item_slots.as<int64_t>(), ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), dc->stats,
                       &dc->st, s);
     launch_scan_lookback(ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), ctx->pbase.as<int64_t>(),
                          ctx->sbase.as<int64_t>(), Pp, Tn, ctx->lbscan.p, s);
@@ -580,6 +614,8 @@ void tm_ctx_destroy(tm_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
   if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
+  for (cudaEvent_t e : {ctx->ev_fork, ctx->ev_join, ctx->ev_cls})
+    if (e) cudaEventDestroy(e);
   prof_flush(ctx);
   for (auto e : ctx->prof.free_ev) cudaEventDestroy(e);
   if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
@@ -587,6 +623,7 @@ void tm_ctx_destroy(tm_ctx* ctx) {
   for (auto e : ctx->chunk_ev)
     if (e) cudaEventDestroy(e);
   if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
   delete ctx;
 }
 
@@ -807,11 +844,15 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
       return r;
     CK(rec(ctx->ev[1], s));
     ctx->path_hv = ctx->hv.as<int32_t>();
+    static int no_early = -1;
+    if (no_early < 0) no_early = getenv("TERMESH_NO_EARLY") != nullptr;  // A/B switch
+    ctx->early_long = !no_early;
     r = enqueue_traverse(ctx, tri32, hw, ctx->seed.as<uint8_t>(), T, off0, v0, s);
-    if (r) { ctx->path_hv = nullptr; return r; }
+    if (r) { ctx->path_hv = nullptr; ctx->early_long = false; return r; }
     CK(rec(ctx->ev[2], s));
     r = enqueue_repair(ctx, tri32, hw, tv, T, off0, v0, &dc->n_seeds, d_off, d_v, s);
     ctx->path_hv = nullptr;
+    ctx->early_long = false;
     if (r) return r;
     CK(rec(ctx->ev[3], s));
     return enqueue_readback(ctx, s);

@@ -51,13 +51,17 @@ void launch_ruler_walk(const int32_t* hw, uint32_t* bits, int64_t T, int64_t t_b
                        int32_t* rprev, DevStatus* st, cudaStream_t s);
 void launch_chain_count(const int32_t* seeds, const int32_t* start, const int64_t* Pp, int64_t Pcap, int64_t T,
                         const int32_t* rnext, const int32_t* rdist, const int32_t* rprev, int64_t* len, int64_t* nrul,
-                        DevStatus* st, cudaStream_t s);
+                        int32_t* long_list, unsigned int* n_long, DevStatus* st, cudaStream_t s);
 void launch_chain_emit(const int32_t* start, const int64_t* Pp, int64_t Pcap, const int32_t* rnext,
                        const int32_t* rdist, const int32_t* rprev, const int64_t* offsets, const int64_t* eoff,
                        int32_t* ent_r, int64_t* ent_base, int64_t ecap, DevStatus* st, cudaStream_t s);
 void launch_ruler_write(const int32_t* tri, const int32_t* hw, const int64_t* n_entries, const int32_t* ent_r,
                         const int64_t* ent_base, const int32_t* rdist, int64_t T, int64_t ecap, int32_t* verts,
                         int32_t* hv, cudaStream_t s);
+// the runs of the listed (long) polygons only: entries eoff[i] .. eoff[i + 1]
+void launch_ruler_write_list(const int32_t* tri, const int32_t* hw, const int32_t* list, const unsigned int* n_list,
+                             const int64_t* eoff, const int32_t* ent_r, const int64_t* ent_base, const int32_t* rdist,
+                             int64_t T, int64_t Pcap, int32_t* verts, int32_t* hv, cudaStream_t s);
 
 // tm_repair.cu
 struct LongQueue {       // work items longer than kLongMin, longest class first
@@ -72,6 +76,10 @@ struct LongQueue {       // work items longer than kLongMin, longest class first
   unsigned int* n_pinch;
   unsigned int* tip_next;  // work counter of k_repair_tips mode 0 (persistent warps)
 };
+// polygons longer than this are classified by k_classify_long (one block each);
+// on the whole path the traversal's chain pass lists them
+constexpr int kClassifyShort = 48;
+
 struct RepairArgs {
   const int32_t* tri;
   int32_t* hw;
@@ -104,7 +112,8 @@ void launch_tv_items(const int64_t* off, const int32_t* v, const int32_t* hv, co
 // hv (nullable): the traversal's slot half-edges -> tv[vertex] = an incident triangle for work items
 void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, int32_t* item_of,
                      int32_t* items, unsigned int* n_items, int32_t* long_list, unsigned int* n_long,
-                     unsigned long long* stats, LongQueue q, const int32_t* hv, int32_t* tv, cudaStream_t s);
+                     unsigned long long* stats, LongQueue q, const int32_t* hv, int32_t* tv, int which,
+                     cudaStream_t s);  // which: 0 all, 1 short polygons only, 2 the listed long ones only
 void launch_repair_tips_long(const RepairArgs& a, cudaStream_t s);
 // mode 0: items of length <= kLongMin; mode 1: long items handed back (state 2/3)
 void launch_repair_tips(const RepairArgs& a, int mode, cudaStream_t s);

@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(256) k_classify(const int64_t* __restrict__ of
                                                   int32_t* __restrict__ items, unsigned int* n_items,
                                                   int32_t* __restrict__ long_list, unsigned int* n_long,
                                                   unsigned long long* stats, const int32_t* __restrict__ hv,
-                                                  int32_t* __restrict__ tv) {
+                                                  int32_t* __restrict__ tv, int append_long) {
   __shared__ int s_cnt;
   __shared__ unsigned int s_base;
   if (threadIdx.x == 0) s_cnt = 0;
@@ -157,10 +157,10 @@ __global__ void __launch_bounds__(256) k_classify(const int64_t* __restrict__ of
     bool is_long = false, is_item = false;
     if (i < P) {
       int64_t b = off[i], n = off[i + 1] - b;
-      item_of[i] = -1;
-      if (n > 48) {
-        is_long = true;
+      if (n > kClassifyShort) {
+        is_long = append_long;  // k_classify_long sets item_of[i]
       } else {
+        item_of[i] = -1;
         // registers: all loads in flight at once, compares without reloads
         const int64_t ex = n <= 16 ? extra_visits_reg<16>(v + b, (int)n) : extra_visits_reg<48>(v + b, (int)n);
         if (ex > 0) {
@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(256) k_classify_long(const int64_t* __restrict
     __syncthreads();
     if (dups > 0 && hv)
       for (int p = threadIdx.x; p < n; p += blockDim.x) tv[s[p]] = hv[b + p] / 3;
+    if (threadIdx.x == 0 && dups == 0) item_of[i] = -1;
     if (threadIdx.x == 0 && dups > 0) {
       unsigned int k = atomicAdd(n_items, 1u);
       items[k] = i;
@@ -1679,7 +1680,10 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   int32_t* fan = fans + wib * kFanCap;
   int32_t* back = fans + (kSegWarps + wib) * kFanCap;
-  const long long max_rounds = (long long)stats[2] + 1;
+  // reparation.py:354-364 bounds the rounds by initial + 1, initial = extra visits
+  // of mesh0: a global sum the short-item classification may still be adding to
+  // when this kernel starts early.  Per item a round splits a tip (depth <= L + 1);
+  // k_out_counts checks the global bound on the final maximum depth.
   const unsigned int nh = *q.n_huge, nq = nh + *q.n_long;
   for (;;) {
     __syncthreads();
@@ -1801,7 +1805,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
     long long depth = 0, splits = 0;
     bool bad = false, spill = false;
     while (ntips > 0) {
-      if (depth + 1 > max_rounds) {
+      if (depth + 1 > (long long)L + 1) {
         if (threadIdx.x == 0) report(c.st, K_NO_CONVERGE, i);
         bad = true;
         break;
@@ -2127,6 +2131,7 @@ __global__ void __launch_bounds__(256) k_out_counts(const int64_t* __restrict__ 
     if (i == P) {
       cnt[i] = 0;
       slots[i] = 0;
+      if (stats && stats[0] > stats[2] + 1) report(st, K_NO_CONVERGE, P);  // rounds > initial + 1
       continue;
     }
     int32_t it = item_of[i];
@@ -2261,9 +2266,14 @@ void launch_tv_items(const int64_t* off, const int32_t* v, const int32_t* hv, co
 
 void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, int32_t* item_of,
                      int32_t* items, unsigned int* n_items, int32_t* long_list, unsigned int* n_long,
-                     unsigned long long* stats, LongQueue q, const int32_t* hv, int32_t* tv, cudaStream_t s) {
-  k_classify<<<grid_for(Pcap, 256), 256, 0, s>>>(off, v, Pp, item_of, items, n_items, long_list, n_long, stats, hv, tv);
-  note_launch(1);
+                     unsigned long long* stats, LongQueue q, const int32_t* hv, int32_t* tv, int which,
+                     cudaStream_t s) {
+  if (which != 2) {  // short polygons (and with which == 0 the list of the long ones)
+    k_classify<<<grid_for(Pcap, 256), 256, 0, s>>>(off, v, Pp, item_of, items, n_items, long_list, n_long, stats, hv,
+                                                   tv, which == 0);
+    note_launch(1);
+  }
+  if (which == 1) return;
   k_classify_long<<<kNumSMs * 4, 256, 0, s>>>(off, v, long_list, n_long, item_of, items, n_items, stats, q, hv, tv);
   note_launch(1);
 }

@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(256) k_chain_count(const int32_t* __restrict__
                                                      const int64_t* __restrict__ Pp, long long limit, const int32_t* __restrict__ rnext,
                                                      const int32_t* __restrict__ rdist, const int32_t* __restrict__ rprev,
                                                      int64_t* __restrict__ len, int64_t* __restrict__ nrul,
+                                                     int32_t* __restrict__ long_list, unsigned int* n_long,
                                                      DevStatus* st) {
   const int64_t P = *Pp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
@@ -213,6 +214,8 @@ __global__ void __launch_bounds__(256) k_chain_count(const int32_t* __restrict__
     }
     len[i] = L;
     nrul[i] = cnt;
+    // whole path: the long polygons go to the early long-item repair (k_classify_long)
+    if (long_list && L > kClassifyShort) long_list[atomicAdd(n_long, 1u)] = (int32_t)i;
   }
 }
 
@@ -270,6 +273,31 @@ __global__ void __launch_bounds__(256) k_ruler_write(const int32_t* __restrict__
   }
 }
 
+// the runs of the listed polygons (one block per polygon, one thread per run)
+__global__ void __launch_bounds__(128) k_ruler_write_list(const int32_t* __restrict__ tri,
+                                                          const int32_t* __restrict__ hw,
+                                                          const int32_t* __restrict__ list, const unsigned int* n_list,
+                                                          const int64_t* __restrict__ eoff,
+                                                          const int32_t* __restrict__ ent_r,
+                                                          const int64_t* __restrict__ ent_base,
+                                                          const int32_t* __restrict__ rdist, long long limit,
+                                                          int32_t* __restrict__ verts, int32_t* __restrict__ hv) {
+  const unsigned int nl = *n_list;
+  for (unsigned int w = blockIdx.x; w < nl; w += gridDim.x) {
+    const int32_t i = list[w];
+    for (int64_t k = eoff[i] + threadIdx.x; k < eoff[i + 1]; k += blockDim.x) {
+      int32_t g = ent_r[k];
+      const int64_t b = ent_base[k];
+      const int d = rdist[g];
+      for (int s = 0; s < d; s++) {
+        verts[b + s] = he_origin(tri, g);
+        if (hv) hv[b + s] = g;
+        g = walk_next(hw, g, limit);
+      }
+    }
+  }
+}
+
 static inline int grid_for(int64_t n, int block) {
   int64_t g = (n + block - 1) / block;
   int64_t cap = (int64_t)kNumSMs * 16;
@@ -301,8 +329,9 @@ void launch_ruler_walk(const int32_t* hw, uint32_t* bits, int64_t T, int64_t t_b
 
 void launch_chain_count(const int32_t* seeds, const int32_t* start, const int64_t* Pp, int64_t Pcap, int64_t T,
                         const int32_t* rnext, const int32_t* rdist, const int32_t* rprev, int64_t* len, int64_t* nrul,
-                        DevStatus* st, cudaStream_t s) {
-  k_chain_count<<<grid_for(Pcap, 256), 256, 0, s>>>(seeds, start, Pp, 3 * T + 3, rnext, rdist, rprev, len, nrul, st);
+                        int32_t* long_list, unsigned int* n_long, DevStatus* st, cudaStream_t s) {
+  k_chain_count<<<grid_for(Pcap, 256), 256, 0, s>>>(seeds, start, Pp, 3 * T + 3, rnext, rdist, rprev, len, nrul,
+                                                    long_list, n_long, st);
   note_launch(1);
 }
 
@@ -318,6 +347,13 @@ void launch_ruler_write(const int32_t* tri, const int32_t* hw, const int64_t* n_
                         const int64_t* ent_base, const int32_t* rdist, int64_t T, int64_t ecap, int32_t* verts,
                         int32_t* hv, cudaStream_t s) {
   k_ruler_write<<<kNumSMs * 16, 256, 0, s>>>(tri, hw, n_entries, ent_r, ent_base, rdist, 3 * T + 3, ecap, verts, hv);
+  note_launch(1);
+}
+
+void launch_ruler_write_list(const int32_t* tri, const int32_t* hw, const int32_t* list, const unsigned int* n_list,
+                             const int64_t* eoff, const int32_t* ent_r, const int64_t* ent_base, const int32_t* rdist,
+                             int64_t T, int64_t Pcap, int32_t* verts, int32_t* hv, cudaStream_t s) {
+  k_ruler_write_list<<<kNumSMs, 128, 0, s>>>(tri, hw, list, n_list, eoff, ent_r, ent_base, rdist, 3 * T + 3, verts, hv);
   note_launch(1);
 }
 
