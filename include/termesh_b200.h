@@ -118,6 +118,10 @@ int tm_ctx_set_partition(tm_ctx *ctx, int64_t t_begin, int64_t t_end);
 int tm_shift_offsets(int64_t *d_offsets, int64_t n_polys, int64_t delta, void *stream);
 /* kernel debug timestamps (ns, %globaltimer) of the last run: repair lineage trace */
 int tm_ctx_debug(const tm_ctx *ctx, uint64_t *out, int n);
+/* Debug hook (determinism hunts): copy an internal buffer of the last whole-path
+   run to device memory dst -- which: 0 pre-repair offsets, 1 pre-repair
+   vertices, 2 packed half-edge words, 3 slot half-edges, 4 seed flags. */
+int tm_ctx_debug_copy(const tm_ctx *ctx, int which, void *dst, size_t bytes);
 
 /* Labels.  tri_bits = 32 or 64 (reference triangles are int64).  check != 0
  * also reports index_range / orientation / degenerate / edge_count /

@@ -62,6 +62,7 @@ def lib():
         L.tm_segment_name.restype = ctypes.c_char_p
         L.tm_launch_count.restype = ctypes.c_int64
         L.tm_ctx_debug.argtypes = [_P, ctypes.POINTER(ctypes.c_uint64), _I]
+        L.tm_ctx_debug_copy.argtypes = [_P, _I, _P, ctypes.c_size_t]
         L.tm_ctx_set_partition.argtypes = [_P, _I64, _I64]
         L.tm_shift_offsets.argtypes = [_P, _I64, _I64, _P]
         L.tm_label.argtypes = [_P, _P, _I64, _P, _I, _I64, _I, _P, _P, _P, _P, _P, _P]
@@ -76,6 +77,7 @@ def lib():
         L.tm_mesh_to_polygons_host.argtypes = [_P, _P, _I64, _P, _I64, _I, _P, _P, _I64, _I64, _PI64, _PI64,
                                                _PI64]
         for name in ("tm_ctx_create", "tm_ctx_defects", "tm_ctx_phase_ms", "tm_ctx_set_profiling", "tm_ctx_debug",
+                     "tm_ctx_debug_copy",
                      "tm_ctx_set_partition", "tm_shift_offsets", "tm_ctx_segment_ms", "tm_label", "tm_relabel",
                      "tm_check_neighbors",
                      "tm_unpack_halfedges", "tm_pack_frontier", "tm_traverse", "tm_repair",
@@ -89,7 +91,7 @@ def exported_symbols():
     """Names declared in include/termesh_b200.h (checked by the CPU tests)."""
     return ("tm_version", "tm_ctx_create", "tm_ctx_destroy", "tm_ctx_last_error", "tm_ctx_defects",
             "tm_ctx_phase_ms", "tm_ctx_set_profiling", "tm_ctx_segment_ms", "tm_segment_name", "tm_launch_count",
-            "tm_ctx_debug", "tm_ctx_set_partition", "tm_shift_offsets",
+            "tm_ctx_debug", "tm_ctx_debug_copy", "tm_ctx_set_partition", "tm_shift_offsets",
             "tm_label", "tm_relabel", "tm_check_neighbors", "tm_unpack_halfedges",
             "tm_pack_frontier",
             "tm_traverse", "tm_repair", "tm_mesh_to_polygons_host", "tm_mesh_to_polygons")

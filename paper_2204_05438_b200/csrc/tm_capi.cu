@@ -667,6 +667,16 @@ int tm_ctx_debug(const tm_ctx* ctx, uint64_t* out, int n) {
   return TM_OK;
 }
 
+int tm_ctx_debug_copy(const tm_ctx* ctx, int which, void* dst, size_t bytes) {
+  if (!ctx || !dst) return TM_ERR_ARGUMENT;
+  const Buf* b = which == 0 ? &ctx->off0 : which == 1 ? &ctx->v0 : which == 2 ? &ctx->hw : which == 3 ? &ctx->hv
+               : which == 4 ? &ctx->seed : nullptr;
+  if (!b || !b->p) return TM_ERR_ARGUMENT;
+  if (bytes > b->bytes) bytes = b->bytes;
+  if (cudaMemcpy(dst, b->p, bytes, cudaMemcpyDeviceToDevice) != cudaSuccess) return TM_ERR_CUDA;
+  return TM_OK;
+}
+
 int tm_ctx_set_partition(tm_ctx* ctx, int64_t t_begin, int64_t t_end) {
   if (!ctx) return TM_ERR_ARGUMENT;
   if (t_begin < 0 || (t_end >= 0 && t_end < t_begin)) return set_err(ctx, TM_ERR_ARGUMENT, "bad seed partition");

@@ -219,7 +219,8 @@ __global__ void __launch_bounds__(kLabelThreads, 4) k_tri_pass(const double2* __
                                                             uint8_t* __restrict__ seed, int32_t* __restrict__ tv,
                                                             int check, DevStatus* st) {
   __shared__ int32_t sq[kLabelWarps][3][96];
-  __shared__ unsigned long long lkey[kLocalSlots];
+  __shared__ int32_t lown[kLocalSlots];  // 0 = free, else the claiming (thread, slot j) + 1
+  __shared__ uint32_t lklo[kLocalSlots], lkhi[kLocalSlots];
   __shared__ int32_t lval[kLocalSlots];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const bool local = !check;
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(kLabelThreads, 4) k_tri_pass(const double2* __
   for (int64_t base = t_begin + blockIdx.x * (int64_t)blockDim.x; base < T; base += stride) {
     const int64_t t = base + threadIdx.x;
     if (local) {
-      for (int i = threadIdx.x; i < kLocalSlots; i += kLabelThreads) lkey[i] = kEmptySlot;
+      for (int i = threadIdx.x; i < kLocalSlots; i += kLabelThreads) lown[i] = 0;
       __syncthreads();
     }
     unsigned flags = 0, desc = 0;
@@ -282,16 +283,16 @@ __global__ void __launch_bounds__(kLabelThreads, 4) k_tri_pass(const double2* __
 #pragma unroll
       for (int j = 0; j < 3; j++) {
         if (!((flags >> j) & 1u)) continue;
-        const unsigned long long key = ((unsigned long long)(uint32_t)oo[j] << 32) | (uint32_t)gg[j];
         uint32_t sl = local_slot(oo[j], gg[j]);
+        const int me = (int)threadIdx.x * 4 + j + 1;
         for (;;) {
-          unsigned long long prev = atomicCAS(&lkey[sl], kEmptySlot, key);
-          if (prev == kEmptySlot) {
+          if (atomicCAS(&lown[sl], 0, me) == 0) {
+            lklo[sl] = (uint32_t)oo[j];
+            lkhi[sl] = (uint32_t)gg[j];
             lval[sl] = hh[j];
             lslot[j] = (int)sl;
             break;
           }
-          if (prev == key) break;  // duplicate ascending key: left to the global table, which reports it
           sl = (sl + 1) & (kLocalSlots - 1);
         }
       }
@@ -299,12 +300,10 @@ __global__ void __launch_bounds__(kLabelThreads, 4) k_tri_pass(const double2* __
 #pragma unroll
       for (int j = 0; j < 3; j++) {
         if (!((desc >> j) & 1u)) continue;
-        const unsigned long long key = ((unsigned long long)(uint32_t)gg[j] << 32) | (uint32_t)oo[j];
         uint32_t sl = local_slot(gg[j], oo[j]);
         for (;;) {
-          const unsigned long long k = lkey[sl];
-          if (k == kEmptySlot) break;
-          if (k == key) {
+          if (lown[sl] == 0) break;
+          if (lklo[sl] == (uint32_t)gg[j] && lkhi[sl] == (uint32_t)oo[j]) {
             const int32_t pl = atomicOr(&lval[sl], kLocalMatched);
             if (!(pl & kLocalMatched)) label_pair(hw, seed, (int32_t)(3 * t + j), me0 == j, pl >> 1, (pl & 1) != 0);
             break;

@@ -33,3 +33,34 @@ def test_10m_parity(cuda, workload):
     for k in ("rounds", "splits", "initial_tips", "unrepaired"):
         assert info[k] == ref["stats"][k], k
     print(workload, "T", tri.n_triangles, "polygons", off.size - 1, "stats", ref["stats"])
+
+
+@pytest.mark.parametrize("workload", ["u10m"])
+def test_10m_whole_path_replays_match_oracle(cuda, workload):
+    """40 graph replays of the whole device path at 10M, every one equal to the
+    oracle's final CSR (a shared-memory 64-bit CAS race once corrupted ~1 step in
+    50 here while every 1M check passed)."""
+    import ctypes
+    import torch
+    import bench
+    from paper_2204_05438_b200 import _capi
+    tri = bench.load_mesh(workload, 0)
+    ref = oracle.execute(tri)
+    n, T = tri.n_vertices, tri.n_triangles
+    xy = torch.from_numpy(tri.vertices).to(cuda)
+    tr = torch.from_numpy(tri.triangles).to(cuda)
+    off = torch.empty(T + 1, dtype=torch.int64, device=cuda)
+    v = torch.empty(3 * T, dtype=torch.int32, device=cuda)
+    ctx = _capi.context(cuda)
+    npol, nsl = ctypes.c_int64(), ctypes.c_int64()
+    st = (ctypes.c_int64 * _capi.NUM_STATS)()
+    ref_off = torch.from_numpy(ref["final"][0]).to(cuda)
+    ref_v = torch.from_numpy(ref["final"][1].astype(np.int32)).to(cuda)
+    for k in range(40):
+        rc = _capi.lib().tm_mesh_to_polygons(ctx.ptr, _capi.ptr(xy), n, _capi.ptr(tr), 64, T, 0, _capi.ptr(off),
+                                             _capi.ptr(v), T, 3 * T, ctypes.byref(npol), ctypes.byref(nsl), st,
+                                             _capi.stream_ptr(cuda))
+        ctx.check(rc)
+        P, F = npol.value, nsl.value
+        assert P + 1 == ref_off.numel() and F == ref_v.numel(), k
+        assert torch.equal(off[: P + 1], ref_off) and torch.equal(v[:F], ref_v), k

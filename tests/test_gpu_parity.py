@@ -165,7 +165,7 @@ def test_graph_replay_soak_u1m(cuda):
                                              _capi.ptr(v), T, 3 * T, ctypes.byref(npol), ctypes.byref(nsl), st,
                                              _capi.stream_ptr(cuda))
         ctx.check(rc)
-        if k % 10 == 0 or k >= 60:
+        if True:  # every replay: a rare label race once showed up as 1 bad step in ~50 at 10M
             P, F = npol.value, nsl.value
             assert H(off[: P + 1].cpu().numpy()) == h["final_off"], k
             assert H(v[:F].cpu().numpy().astype(np.int64)) == h["final_verts"], k
