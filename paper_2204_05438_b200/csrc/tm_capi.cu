@@ -465,8 +465,11 @@ static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* 
                       ctx->path_hv, ctx->tv.as<int32_t>(), 2, a);
       CK(cudaEventRecord(ctx->ev_cls, a));
       CK(cudaMemsetAsync(ctx->item_state.p, 0, Tn * sizeof(int32_t), a));
-      launch_repair_tips_long(repair_args(ctx, d_tri32, const_cast<int32_t*>(d_hw), ctx->tv.as<int32_t>(), T, d_off, d_v),
-                              a);
+      {
+        RepairArgs ra = repair_args(ctx, d_tri32, const_cast<int32_t*>(d_hw), ctx->tv.as<int32_t>(), T, d_off, d_v);
+        launch_repair_tips_long(ra, a);
+        launch_repair_pinch(ra, 2, a);  // the finished long items' pinch pass, still beside the short items
+      }
       CK(cudaEventRecord(ctx->ev_join, a));
     }
     launch_ruler_write(d_tri32, d_hw, &dc->n_entries, ctx->ent_r.as<int32_t>(), ctx->ent_base.as<int64_t>(),
@@ -505,6 +508,7 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
         CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
       }
       launch_repair_tips_long(a, sl);
+      launch_repair_pinch(a, 2, sl);
       if (!serial) CK(cudaEventRecord(ctx->ev_join, ctx->aux));
     }
     launch_repair_tips(a, 0, s);

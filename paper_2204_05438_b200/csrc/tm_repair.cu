@@ -2106,10 +2106,30 @@ __global__ void __launch_bounds__(128) k_repair_pinch(RepairCtx c, const int32_t
     }
     return;
   }
-  const unsigned int nh = *q.n_huge, nl = *q.n_long, np = *q.n_parked;
+  const unsigned int nh = *q.n_huge, nl = *q.n_long;
+  if (mode == 2) {
+    // right after the shared-memory kernel, on its stream: the long items it finished
+    // (state 1), under the guard known so far; items that reach it are parked
+    PinchPark park{item_state, item_depth, q.parked, q.n_parked};
+    for (int64_t k = warp; k < nh + nl; k += nwarps) {
+      const int64_t w = k < nh ? q.huge[k] : q.longq[k - nh];
+      if (item_state[w] != 1) continue;  // handed back to k_repair_tips (states 2, 3)
+      const long long list = item_list[w];
+      if (list < 0) {
+        if (lane == 0) item_slots[w] = 0;
+        continue;
+      }
+      warp_finish_pinch(c, w, items[w], list, item_n[w], lane, item_list, item_n, item_slots, stats, guard, stab, 0,
+                        park);
+    }
+    return;
+  }
+  // mode 1, final guard: the long items k_repair_tips resumed, then every parked item
+  const unsigned int np = *q.n_parked;
   for (int64_t k = warp; k < nh + nl + np; k += nwarps) {
     const int64_t w = k < nh ? q.huge[k] : k < nh + nl ? q.longq[k - nh] : q.parked[k - nh - nl];
     const bool parked = k >= nh + nl;
+    if (!parked && item_state[w] != 2 && item_state[w] != 3) continue;  // done by mode 2 (or parked)
     const long long list = item_list[w];
     if (list < 0) {
       if (lane == 0) item_slots[w] = 0;
@@ -2340,7 +2360,8 @@ void launch_repair_pinch(const RepairArgs& a, int mode, cudaStream_t s) {
     cudaFuncSetAttribute(k_repair_pinch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_repair_pinch<<<mode ? kNumSMs : kNumSMs * 2, 128, smem, s>>>(c, a.items, a.n_items, a.off, a.item_list, a.item_n,
+  // mode 2 runs beside the short-item kernels: a few blocks (128 KB of shared memory each)
+  k_repair_pinch<<<mode == 2 ? 16 : mode ? kNumSMs : kNumSMs * 2, 128, smem, s>>>(c, a.items, a.n_items, a.off, a.item_list, a.item_n,
                                                                   a.item_slots, a.item_state, a.item_depth, a.q,
                                                                   a.stats, mode);
   note_launch(1);
