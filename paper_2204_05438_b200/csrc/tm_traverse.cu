@@ -201,14 +201,16 @@ __global__ void __launch_bounds__(256) k_chain_count(const int32_t* __restrict__
     if (h0 >= 0) {
       int32_t f = h0, b = rprev[h0];  // next ruler to consume going forward / backward
       for (;;) {
-        L += rdist[f];
+        // both walkers' loads issued together: one memory round trip per step of the pair
+        const int32_t df = rdist[f], nf = rnext[f], db = rdist[b], pb = rprev[b];
+        L += df;
         cnt++;
         if (f == b) break;
-        f = rnext[f];
-        L += rdist[b];
+        f = nf;
+        L += db;
         cnt++;
         if (b == f) break;
-        b = rprev[b];
+        b = pb;
         if (L > limit) { report(st, K_WALK, seeds[i]); L = 0; cnt = 0; break; }
       }
     }
@@ -235,18 +237,19 @@ __global__ void __launch_bounds__(256) k_chain_emit(const int32_t* __restrict__ 
     int64_t pf = offsets[i], pb = offsets[i + 1];  // forward start / backward end offsets
     int32_t f = h0, b = rprev[h0];
     for (;;) {
+      const int32_t df = rdist[f], nf = rnext[f], db = rdist[b], nb = rprev[b];
       ent_r[kf] = f;
       ent_base[kf] = pf;
-      pf += rdist[f];
+      pf += df;
       kf++;
       if (f == b) break;
-      f = rnext[f];
-      pb -= rdist[b];
+      f = nf;
+      pb -= db;
       ent_r[kb] = b;
       ent_base[kb] = pb;
       kb--;
       if (b == f) break;
-      b = rprev[b];
+      b = nb;
     }
   }
 }
