@@ -442,9 +442,7 @@ static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* 
   {
     SegTimer t_(ctx, S_TRAV_SCAN, s);
     launch_scan_lookback(ctx->len.as<int64_t>(), ctx->nrul.as<int64_t>(), d_off, ctx->eoff.as<int64_t>(), &dc->n_seeds,
-                         Tn, ctx->lbscan.p, s);
-    launch_gather_at(d_off, &dc->n_seeds, &dc->n_slots0, s);
-    launch_gather_at(ctx->eoff.as<int64_t>(), &dc->n_seeds, &dc->n_entries, s);
+                         Tn, ctx->lbscan.p, s, &dc->n_slots0, &dc->n_entries);
   }
   {
     SegTimer t_(ctx, S_TRAV_WRITE, s);
@@ -529,8 +527,7 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
                       ctx->item_slots.as<int64_t>(), ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), dc->stats,
                       &dc->st, s);
     launch_scan_lookback(ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), ctx->pbase.as<int64_t>(),
-                         ctx->sbase.as<int64_t>(), Pp, Tn, ctx->lbscan.p, s);
-    launch_finalize(Pp, ctx->pbase.as<int64_t>(), ctx->sbase.as<int64_t>(), d_off_out, &dc->p_out, &dc->f_out, s);
+                         ctx->sbase.as<int64_t>(), Pp, Tn, ctx->lbscan.p, s, &dc->p_out, &dc->f_out, d_off_out);
     launch_stitch(d_off_in, d_v_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(), &dc->n_items,
                   ctx->item_list.as<int64_t>(), ctx->item_n.as<int32_t>(), ctx->pool.as<int32_t>(),
                   ctx->pbase.as<int64_t>(), ctx->sbase.as<int64_t>(), d_off_out, d_v_out, s);

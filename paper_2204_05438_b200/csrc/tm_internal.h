@@ -35,8 +35,10 @@ void launch_scan_dev(const int64_t* in, int64_t* out, const int64_t* n_dev, int6
 void launch_shift(int64_t* a, int64_t n, int64_t delta, cudaStream_t s);
 // single-pass (decoupled look-back) exclusive scan of one or two arrays; in1/out1 may be null
 size_t scan_lookback_bytes(int64_t n_cap);
+// tot0 / tot1 (optional) receive out0[n] / out1[n]; csr_end (optional) gets csr_end[out0[n]] = out1[n]
 void launch_scan_lookback(const int64_t* in0, const int64_t* in1, int64_t* out0, int64_t* out1,
-                          const int64_t* n_dev, int64_t n_cap, void* scratch, cudaStream_t s);
+                          const int64_t* n_dev, int64_t n_cap, void* scratch, cudaStream_t s, int64_t* tot0 = nullptr,
+                          int64_t* tot1 = nullptr, int64_t* csr_end = nullptr);
 void launch_gather_at(const int64_t* arr, const int64_t* idx, int64_t* dst, cudaStream_t s);
 void launch_select_flags(const uint8_t* flag, int64_t n, int32_t* out, int64_t* n_out, int64_t* tile_sums,
                          cudaStream_t s, int64_t base_index = 0);

@@ -115,6 +115,12 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_final(const int64_t* __re
 // prefix; a tile's warp 0 sums predecessors' aggregates 32 at a time until it
 // meets a published prefix.  Tiles are numbered in launch order by an atomic
 // counter, so every predecessor is resident or done (no deadlock).
+struct ScanTotals {
+  int64_t* tot0 = nullptr;     // out0[n]
+  int64_t* tot1 = nullptr;     // out1[n]
+  int64_t* csr_end = nullptr;  // csr_end[out0[n]] = out1[n] (final CSR offset)
+};
+
 struct ScanState {
   unsigned int* counter;  // [1 + ntiles]: tile counter, then per-tile flags (0 none, 1 aggregate, 2 prefix)
   int64_t* agg;           // [2][ntiles] aggregates
@@ -126,15 +132,19 @@ template <int NV>
 __global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const int64_t* __restrict__ in0,
                                                                 const int64_t* __restrict__ in1,
                                                                 int64_t* __restrict__ out0, int64_t* __restrict__ out1,
-                                                                const int64_t* __restrict__ n_dev, ScanState ss) {
+                                                                const int64_t* __restrict__ n_dev, ScanState ss,
+                                                                ScanTotals tt) {
   __shared__ unsigned int s_tile;
   __shared__ int64_t s_pre[NV], s_tot[NV];
+  const int64_t n = *n_dev;
+  // persistent blocks take tiles in counter order until past the data (the grid is
+  // sized by a host bound; tiles beyond the data never publish: nobody looks that far)
+  for (;;) {
   if (threadIdx.x == 0) s_tile = atomicAdd(ss.counter, 1u);
   __syncthreads();
   const int64_t tile = s_tile;
-  const int64_t n = *n_dev;
   const int64_t base = tile * kTile;
-  if (base > n) return;  // tiles beyond the data never publish: nobody looks that far ahead
+  if (base > n) break;
   volatile unsigned int* flags = ss.counter + 1;
   const int64_t first = base + (int64_t)threadIdx.x * kScanItems;
   const int64_t* in[2] = {in0, in1};
@@ -196,15 +206,25 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const int64_t* _
   }
   __syncthreads();
   int64_t* out[2] = {out0, out1};
+  int64_t total[NV];
 #pragma unroll
   for (int a = 0; a < NV; a++) {
     int64_t run = s_pre[a] + ex[a];
+    total[a] = -1;
 #pragma unroll
     for (int k = 0; k < kScanItems; k++) {
       const int64_t i = first + k;
       if (i <= n) out[a][i] = run;
+      if (i == n) total[a] = run;
       run += v[a][k];
     }
+  }
+  if (total[0] >= 0) {  // the thread holding element n: totals (and the CSR end) without extra launches
+    if (tt.tot0) *tt.tot0 = total[0];
+    if (NV > 1 && tt.tot1) *tt.tot1 = total[NV - 1];
+    if (NV > 1 && tt.csr_end) tt.csr_end[total[0]] = total[NV - 1];
+  }
+  __syncthreads();  // s_tile / s_pre / s_tot are reused by the next tile
   }
 }
 
@@ -267,7 +287,8 @@ size_t scan_lookback_bytes(int64_t n_cap) {
 }
 
 void launch_scan_lookback(const int64_t* in0, const int64_t* in1, int64_t* out0, int64_t* out1,
-                          const int64_t* n_dev, int64_t n_cap, void* scratch, cudaStream_t s) {
+                          const int64_t* n_dev, int64_t n_cap, void* scratch, cudaStream_t s, int64_t* tot0,
+                          int64_t* tot1, int64_t* csr_end) {
   const int64_t nt = n_cap / kTile + 2;  // tiles covering n_cap + 1 elements
   ScanState ss;
   ss.counter = static_cast<unsigned int*>(scratch);
@@ -276,10 +297,15 @@ void launch_scan_lookback(const int64_t* in0, const int64_t* in1, int64_t* out0,
   ss.pre = ss.agg + 2 * nt;
   ss.ntiles = nt;
   cudaMemsetAsync(ss.counter, 0, (size_t)(nt + 1) * sizeof(unsigned int), s);
+  ScanTotals tt;
+  tt.tot0 = tot0;
+  tt.tot1 = tot1;
+  tt.csr_end = csr_end;
+  const int grid = (int)(nt < (int64_t)kNumSMs * 4 ? nt : (int64_t)kNumSMs * 4);
   if (in1)
-    k_scan_lookback<2><<<(int)nt, kScanThreads, 0, s>>>(in0, in1, out0, out1, n_dev, ss);
+    k_scan_lookback<2><<<grid, kScanThreads, 0, s>>>(in0, in1, out0, out1, n_dev, ss, tt);
   else
-    k_scan_lookback<1><<<(int)nt, kScanThreads, 0, s>>>(in0, nullptr, out0, nullptr, n_dev, ss);
+    k_scan_lookback<1><<<grid, kScanThreads, 0, s>>>(in0, nullptr, out0, nullptr, n_dev, ss, tt);
   note_launch(1);
 }
 
