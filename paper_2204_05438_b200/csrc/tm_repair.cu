@@ -926,6 +926,32 @@ __device__ int32_t trivertex_he(const RepairCtx& c, int32_t v, int guard) {
 // _pinch_candidates (reparation.py:169-205) for one piece, candidates in the
 // reference order, each trial-split until one keeps.  Every lane runs the
 // (identical) candidate enumeration so the trials stay warp-convergent.
+// Fan of v collected once (two walkers) and rotated to the reference anchor,
+// the half-edge of the lowest incident triangle (_fan_at_vertex / trivertex,
+// reparation.py:91-124): returns deg (fan[(anchor + i) % deg] is the i-th
+// half-edge in fan_step order), or -1 when the fan does not fit kFanCap.
+__device__ int warp_anchored_fan(const RepairCtx& c, int32_t v, int32_t* fan, int32_t* back, int lane, int* anchor) {
+  const int deg = warp_collect_fan(c, v, fan, back, lane);
+  if (deg < 1 || deg > kFanCap) return -1;
+  int best_t = 0x7FFFFFFF, best_k = 0;
+  for (int k = lane; k < deg; k += 32) {
+    const int t = fan[k] / 3;
+    if (t < best_t) { best_t = t; best_k = k; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const int ot = __shfl_xor_sync(kFull, best_t, o), ok = __shfl_xor_sync(kFull, best_k, o);
+    if (ot < best_t || (ot == best_t && ok < best_k)) { best_t = ot; best_k = ok; }
+  }
+  *anchor = best_k;
+  return deg;
+}
+
+__device__ int warp_pinch_split_slow(const RepairCtx& c, const int32_t* X, int L, int32_t poly, int lane, int32_t** A,
+                                     int* la, int32_t** B, int* lb, int p1, int p2);
+
+// _pinch_candidates with the fans held in shared memory (the frontier bits are
+// read per candidate sweep: a failed trial is reverted before the next one).
+// Falls back to the rotation-by-rotation enumeration when a fan exceeds kFanCap.
 __device__ int warp_pinch_split(const RepairCtx& c, const int32_t* X, int L, int32_t poly, int lane, int32_t** A,
                                 int* la, int32_t** B, int* lb, int2* stab) {
   long long ck0 = clock64();
@@ -933,6 +959,71 @@ __device__ int warp_pinch_split(const RepairCtx& c, const int32_t* X, int L, int
   warp_dup_scan(c, X, L, lane, &p1, &p2, stab, kPinchDupCap);
   if (c.dbg && lane == 0) { atomicAdd(c.dbg + 64, (unsigned long long)(clock64() - ck0)); atomicMax(c.dbg + 70, (unsigned long long)L); }
   if (p2 < 0) return 0;
+  // the duplicate table is free until the caller scans the children: fan buffers
+  int32_t* fan = reinterpret_cast<int32_t*>(stab);
+  int32_t* back = fan + kFanCap;
+  int anc = 0;
+  int deg = warp_anchored_fan(c, X[p2], fan, back, lane, &anc);
+  if (deg < 0) return warp_pinch_split_slow(c, X, L, poly, lane, A, la, B, lb, p1, p2);
+  __syncwarp();
+  const int poss[2] = {p2, p1};
+  for (int q = 0; q < 2; q++) {  // wedge internal edges at the second, then the first visit
+    const int32_t outv = X[(poss[q] + 1) % L];
+    const int i_out = warp_find_first(deg, lane, [&](int i) {
+      const int32_t g = fan[(anc + i) % deg];
+      return hw_front(c.hw[g]) && he_target(c.tri, g) == outv;
+    });
+    if (i_out < 0) {
+      if (lane == 0) report(c.st, K_STRUCT, poly);
+      return -1;
+    }
+    const int j = warp_find_first(deg - 1, lane, [&](int t) { return hw_front(c.hw[fan[(anc + i_out + 1 + t) % deg]]); });
+    const int k = j < 0 ? deg - 1 : j;
+    if (k == 0) continue;
+    const int mid = (k - 1) / 2;
+    for (int ord = -1; ord < k; ord++) {  // middle edge first, then the rest in order
+      const int idx = ord < 0 ? mid : ord;
+      if (ord == mid) continue;
+      const int32_t cand = fan[(anc + i_out + 1 + idx) % deg];
+      long long ckt = clock64();
+      int r = warp_try_pinch_arc(c, cand, X, L, poly, lane, A, la, B, lb);
+      if (c.dbg && lane == 0) { atomicAdd(c.dbg + 65, (unsigned long long)(clock64() - ckt)); atomicAdd(c.dbg + 66, 1ull); }
+      if (r != 0) return r;
+    }
+  }
+  for (int idx = p1 + 1; idx < p2; idx++) {  // internal fan edges of the inner-loop vertices
+    deg = warp_anchored_fan(c, X[idx], fan, back, lane, &anc);
+    if (deg < 0) return warp_pinch_split_slow(c, X, L, poly, lane, A, la, B, lb, -idx - 2, p2);  // resume at idx
+    __syncwarp();
+    for (int base = 0; base < deg; base += 32) {
+      const int i = base + lane;
+      const bool inner = i < deg && !hw_front(c.hw[fan[(anc + i) % deg]]);
+      unsigned m = __ballot_sync(kFull, inner);
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        const int32_t g = fan[(anc + base + b) % deg];
+        long long ckt = clock64();
+        int r = warp_try_pinch_arc(c, g, X, L, poly, lane, A, la, B, lb);
+        if (c.dbg && lane == 0) { atomicAdd(c.dbg + 65, (unsigned long long)(clock64() - ckt)); atomicAdd(c.dbg + 67, 1ull); }
+        if (r != 0) return r;
+      }
+    }
+  }
+  return 0;
+}
+
+// The rotation-by-rotation enumeration (fans larger than kFanCap).  p1 < -1
+// encodes a resume at inner vertex idx = -p1 - 2 (the wedges are done).
+__device__ int warp_pinch_split_slow(const RepairCtx& c, const int32_t* X, int L, int32_t poly, int lane, int32_t** A,
+                                     int* la, int32_t** B, int* lb, int p1, int p2) {
+  int first_inner = -1;
+  if (p1 < -1) {
+    first_inner = -p1 - 2;
+    int q1 = -1, q2 = -1;
+    warp_dup_scan(c, X, L, lane, &q1, &q2);
+    p1 = q1;
+  }
   const int32_t v = X[p2];
   const int guard = (int)(3 * c.T + 3 < (1LL << 30) ? 3 * c.T + 3 : (1LL << 30));
   int32_t g0 = trivertex_he(c, v, guard);
@@ -953,7 +1044,7 @@ __device__ int warp_pinch_split(const RepairCtx& c, const int32_t* X, int L, int
     } while (g != g0);
   }
   const int poss[2] = {p2, p1};
-  for (int q = 0; q < 2; q++) {  // wedge internal edges at the second, then the first visit
+  for (int q = first_inner < 0 ? 0 : 2; q < 2; q++) {  // wedge internal edges at the second, then the first visit
     int32_t outv = X[(poss[q] + 1) % L];
     int32_t g = g0, gout = -1;
     for (int st = 0; st < deg; st++) {
@@ -984,7 +1075,7 @@ __device__ int warp_pinch_split(const RepairCtx& c, const int32_t* X, int L, int
       if (r != 0) return r;
     }
   }
-  for (int idx = p1 + 1; idx < p2; idx++) {  // internal fan edges of the inner-loop vertices
+  for (int idx = first_inner < 0 ? p1 + 1 : first_inner; idx < p2; idx++) {  // internal fan edges of the inner-loop vertices
     int32_t x = X[idx];
     int32_t gx0 = trivertex_he(c, x, guard);
     if (gx0 < 0) {
