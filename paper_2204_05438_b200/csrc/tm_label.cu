@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(kLabelThreads, 4) k_tri_pass(const double2* __
 // on the lower triangle).  k = twin % 3 replaces the reference's back-slot
 // searches.  A half-edge without a partner stays border as pass A wrote it
 // (an ascending one keeps its provisional seed flag).
-__global__ void __launch_bounds__(kLabelThreads) k_pair_pass(const int32_t* __restrict__ tri32, int64_t T,
+__global__ void __launch_bounds__(kLabelThreads, 6) k_pair_pass(const int32_t* __restrict__ tri32, int64_t T,
                                                              const int8_t* __restrict__ max_edge, TwinTable tb,
                                                              int32_t* __restrict__ hw, uint8_t* __restrict__ seed,
                                                              int32_t* __restrict__ tv, int64_t n, int check,
