@@ -56,7 +56,7 @@ struct Counters {
   int64_t f_out;       // F': vertex slots after repair
   unsigned int n_overflow, n_items, n_long, n_pinch;
   unsigned int q_huge, q_long, q_next, n_parked;
-  unsigned int tip_next, pad1, pad2, pad3;
+  unsigned int tip_next, table_ovf, pad2, pad3;
   unsigned long long pool_top, undo_top;
   unsigned long long stats[8];
   unsigned long long dbg[128];  // optional kernel timestamps / counters (tm_ctx_debug)
@@ -127,6 +127,10 @@ struct tm_ctx {
   // whole-path runs: the long polygons are written, classified and repaired on
   // ctx->aux right after the traversal's chain pass (enqueue_traverse)
   bool early_long = false;
+  // whole path: half-size twin table (block-local matching leaves ~43% of the keys
+  // to it); an overflow reruns the call at full size and keeps that for this ctx
+  int table_shrink = 1;
+  int label_shrink = 0;  // what the label kernels of the current call use
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cudaGraphExec_t graph = nullptr;
@@ -364,15 +368,16 @@ static int enqueue_label(tm_ctx* ctx, const double* d_xy, int64_t n, const void*
                          int check, int32_t* d_tri32, int32_t* d_hw, int8_t* d_me, uint8_t* d_seed, int32_t* d_tv,
                          cudaStream_t s) {
   Counters* dc = dc_of(ctx);
+  const int shrink = ctx->label_shrink && !check;  // check = 1 sends every key to the table
   if (!ctx->label_a_external) {
     SegTimer t_(ctx, S_LABEL_A, s);
     launch_label_a(d_xy, n, d_tri, tri_bits == 64, T, check, d_tri32, d_hw, d_me, d_seed, d_tv, ctx->slots.p,
-                   &dc->st, s);
+                   &dc->st, s, shrink, &dc->table_ovf);
   }
   {
     SegTimer t_(ctx, S_LABEL_B, s);
     launch_label_b(tri_bits == 32 && d_tri32 == nullptr ? (const int32_t*)d_tri : d_tri32, n, T, d_hw, d_me, d_seed,
-                   d_tv, ctx->slots.p, check, &dc->st, s);
+                   d_tv, ctx->slots.p, check, &dc->st, s, shrink);
   }
   CK(cudaGetLastError());
   return TM_OK;
@@ -713,6 +718,7 @@ int tm_label(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_tri, int 
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   if ((rc = prepare(ctx, T, n)) || (rc = enqueue_reset(ctx, s))) return rc;
+  ctx->label_shrink = 0;  // phase API: full-size twin table
   if ((rc = enqueue_label(ctx, d_xy, n, d_tri, tri_bits, T, check, d_tri32, d_hw, d_max_edge, d_seed, d_tv, s)))
     return rc;
   Counters h;
@@ -824,6 +830,8 @@ static int path_buffers(tm_ctx* ctx, int64_t n, int64_t T) {
   return TM_OK;
 }
 
+constexpr int kRetryTable = 100;  // internal: rerun the call with the full-size twin table
+
 static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_tri, int tri_bits, int64_t T,
                       int check, int64_t* d_off, int32_t* d_v, int64_t* n_polys, int64_t* n_slots, int64_t* stats,
                       cudaStream_t user) {
@@ -840,6 +848,7 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
   int64_t* off0 = ctx->off0.as<int64_t>();
   int32_t* v0 = ctx->v0.as<int32_t>();
   Counters* dc = dc_of(ctx);
+  ctx->label_shrink = ctx->table_shrink;
 
   bool capturing = false;
   // external event nodes inside a capture, plain records otherwise
@@ -908,6 +917,12 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
   CK(cudaStreamSynchronize(s));
   CK(cudaGetLastError());
   Counters h = *ctx->h_result;
+  if (h.table_ovf) {  // the half-size twin table overflowed: this call's labels are incomplete
+    ctx->table_shrink = 0;
+    if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+    ctx->graph = nullptr;
+    return kRetryTable;
+  }
   rc = decode_status(ctx, h);
   if (rc == TM_ERR_CAPACITY) {
     // labels are ours: relabeling restores the pre-repair frontier exactly
@@ -940,8 +955,12 @@ int tm_mesh_to_polygons(tm_ctx* ctx, const double* d_xy, int64_t n, const void* 
   if (tri_bits != 32 && tri_bits != 64) return set_err(ctx, TM_ERR_ARGUMENT, "tri_bits must be 32 or 64");
   if (cap_polys < T || cap_slots < 3 * T)
     return set_err(ctx, TM_ERR_ARGUMENT, "output capacities must be at least T polygons and 3T slots");
-  return run_device(ctx, d_xy, n, d_tri, tri_bits, T, check, d_off, d_v, n_polys, n_slots, stats,
+  int rc = run_device(ctx, d_xy, n, d_tri, tri_bits, T, check, d_off, d_v, n_polys, n_slots, stats,
+                      (cudaStream_t)stream);
+  if (rc == kRetryTable)  // now at full table size
+    rc = run_device(ctx, d_xy, n, d_tri, tri_bits, T, check, d_off, d_v, n_polys, n_slots, stats,
                     (cudaStream_t)stream);
+  return rc;
 }
 
 int tm_mesh_to_polygons_host(tm_ctx* ctx, const double* h_xy, int64_t n, const int64_t* h_tri, int64_t T, int check,
@@ -966,7 +985,8 @@ int tm_mesh_to_polygons_host(tm_ctx* ctx, const double* h_xy, int64_t n, const i
   // as soon as it lands, so only the last chunk's pass A is exposed.
   CK(cudaMemcpyAsync(ctx->xy.p, h_xy, 2 * n * sizeof(double), cudaMemcpyHostToDevice, s));
   if ((rc = enqueue_reset(ctx, s))) return rc;
-  launch_label_a_prepare(n, T, nullptr, ctx->slots.p, s);
+  const int shrink = ctx->table_shrink && !check;
+  launch_label_a_prepare(n, T, nullptr, ctx->slots.p, s, shrink);
   CK(cudaEventRecord(ctx->chunk_ev[0], s));
   CK(cudaStreamWaitEvent(ctx->cstream, ctx->chunk_ev[0], 0));  // table reset before any chunk's pass A
   for (int k = 0; k < kUploadChunks; k++) {
@@ -978,13 +998,16 @@ int tm_mesh_to_polygons_host(tm_ctx* ctx, const double* h_xy, int64_t n, const i
     CK(cudaStreamWaitEvent(s, ctx->chunk_ev[k], 0));
     launch_label_a_range(ctx->xy.as<double>(), n, ctx->tri.p, 1, T, t0, t1, check, ctx->tri32.as<int32_t>(),
                          ctx->hw.as<int32_t>(), ctx->max_edge.as<int8_t>(), ctx->seed.as<uint8_t>(), nullptr,
-                         ctx->slots.p, &dc_of(ctx)->st, s);
+                         ctx->slots.p, &dc_of(ctx)->st, s, shrink, &dc_of(ctx)->table_ovf);
   }
   CK(cudaGetLastError());
   ctx->label_a_external = true;
   rc = run_device(ctx, ctx->xy.as<double>(), n, ctx->tri.p, 64, T, check, ctx->fin_off.as<int64_t>(),
                   ctx->fin_v.as<int32_t>(), n_polys, n_slots, stats, s);
   ctx->label_a_external = false;
+  if (rc == kRetryTable)  // the half-size twin table overflowed: once more at full size
+    return tm_mesh_to_polygons_host(ctx, h_xy, n, h_tri, T, check, h_off, h_v, cap_polys, cap_slots, n_polys,
+                                    n_slots, stats);
   if (rc) return rc;
   if (*n_polys > cap_polys || *n_slots > cap_slots)
     return set_err(ctx, TM_ERR_CAPACITY, "host output capacity too small (%lld polygons, %lld slots needed)",

@@ -15,14 +15,16 @@ size_t hash_bytes(int64_t n, int64_t T);
 void note_launch(int k);
 void launch_label_a(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int check,
                     int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed, int32_t* tv, void* table,
-                    DevStatus* st, cudaStream_t s);
+                    DevStatus* st, cudaStream_t s, int shrink = 0, unsigned int* ovf = nullptr);
 // pass A split for copy overlap: prepare (table/trivertex init) once, then triangle ranges
-void launch_label_a_prepare(int64_t n, int64_t T, int32_t* tv, void* table, cudaStream_t s);
+// shrink = 1: half-size twin table (whole path; overflow sets *ovf, the host reruns at full size)
+void launch_label_a_prepare(int64_t n, int64_t T, int32_t* tv, void* table, cudaStream_t s, int shrink = 0);
 void launch_label_a_range(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int64_t t_begin,
                           int64_t t_end, int check, int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed,
-                          int32_t* tv, void* table, DevStatus* st, cudaStream_t s);
+                          int32_t* tv, void* table, DevStatus* st, cudaStream_t s, int shrink = 0,
+                          unsigned int* ovf = nullptr);
 void launch_label_b(const int32_t* tri32, int64_t n, int64_t T, int32_t* hw, const int8_t* max_edge, uint8_t* seed,
-                    int32_t* tv, void* table, int check, DevStatus* st, cudaStream_t s);
+                    int32_t* tv, void* table, int check, DevStatus* st, cudaStream_t s, int shrink = 0);
 void launch_relabel(const int8_t* max_edge, int64_t T, int32_t* hw, uint8_t* seed, cudaStream_t s);
 void launch_check_neighbors(const int32_t* hw, const void* nb, int nb_is64, int64_t T, DevStatus* st, cudaStream_t s);
 void launch_unpack(const int32_t* hw, int64_t T, int32_t* twin, uint8_t* fr, cudaStream_t s);

@@ -44,6 +44,7 @@ struct TwinTable {
   unsigned long long* slots;  // 4 * nb
   uint64_t nb_mask;           // nb - 1 (nb = 2^q buckets)
   int K, b, R, hb;
+  unsigned int* ovf;          // shrunken table: displacement overflow flag (host retries at full size)
 };
 
 __device__ __forceinline__ uint64_t mixK(uint64_t x, int K) {
@@ -105,7 +106,8 @@ __device__ __forceinline__ void table_insert(const TwinTable& tb, DevStatus* st,
       s++;
     }
   }
-  report(st, K_STRUCT, h / 3);  // displacement overflow (> 31 buckets): not seen at load <= 0.7
+  if (tb.ovf) atomicOr(tb.ovf, 1u);  // shrunken table full: the host reruns with the full-size one
+  else report(st, K_STRUCT, h / 3);  // displacement overflow (> 31 buckets): not seen at load <= 0.7
 }
 
 // Partner of descending half-edge o -> g (key (g, o)) as (h << 1) | L; -1 when border.
@@ -441,7 +443,11 @@ static int bit_length(uint64_t v) {
 }
 
 // Geometry of the twin table for a mesh of n vertices / T triangles.
-static TwinTable table_geometry(int64_t n, int64_t T, void* mem) {
+// shrink = 1 (whole path): half the buckets.  Block-local matching pairs ~57% of
+// the edges before the table (Qhull order), so the inserted keys load the half
+// table to ~0.3; a mesh without that locality overflows it, which sets *ovf and
+// the host reruns the path with shrink = 0.
+static TwinTable table_geometry(int64_t n, int64_t T, void* mem, int shrink = 0, unsigned int* ovf = nullptr) {
   TwinTable tb{};
   tb.b = bit_length((uint64_t)(n > 1 ? n - 1 : 1));
   tb.K = 2 * tb.b;
@@ -451,11 +457,13 @@ static TwinTable table_geometry(int64_t n, int64_t T, void* mem) {
   // (measured: a fuller table costs more in probe/CAS conflicts than it saves in L2)
   uint64_t keys = (uint64_t)(3 * (T > 0 ? T : 1)) / 2 + 64;
   int q = bit_length((keys * 10 / 28) | 1);
+  if (shrink && q > 8) q -= 1;
   if (q > tb.K) q = tb.K;
   while (tb.K - q + kDispBits + tb.hb > 63 && q < tb.K) q++;  // the slot must hold remainder|d|h|L in 63 bits
   tb.R = tb.K - q;
   tb.nb_mask = (1ull << q) - 1;
   tb.slots = static_cast<unsigned long long*>(mem);
+  tb.ovf = shrink ? ovf : nullptr;
   return tb;
 }
 
@@ -464,8 +472,9 @@ size_t hash_bytes(int64_t n, int64_t T) {
   return (size_t)(tb.nb_mask + 1) * 4 * sizeof(unsigned long long);
 }
 
-void launch_label_a_prepare(int64_t n, int64_t T, int32_t* tv, void* table, cudaStream_t s) {
-  cudaMemsetAsync(table, 0xFF, hash_bytes(n, T), s);
+void launch_label_a_prepare(int64_t n, int64_t T, int32_t* tv, void* table, cudaStream_t s, int shrink) {
+  const TwinTable tb = table_geometry(n, T, nullptr, shrink);
+  cudaMemsetAsync(table, 0xFF, (size_t)(tb.nb_mask + 1) * 4 * sizeof(unsigned long long), s);
   if (n > 0 && tv != nullptr) {
     // sentinel 0x7F7F7F7F (> any triangle index), mapped to -1 by pass B
     cudaMemsetAsync(tv, 0x7F, (size_t)n * sizeof(int32_t), s);
@@ -474,8 +483,8 @@ void launch_label_a_prepare(int64_t n, int64_t T, int32_t* tv, void* table, cuda
 
 void launch_label_a_range(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int64_t t_begin,
                           int64_t t_end, int check, int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed,
-                          int32_t* tv, void* table, DevStatus* st, cudaStream_t s) {
-  TwinTable tb = table_geometry(n, T, table);
+                          int32_t* tv, void* table, DevStatus* st, cudaStream_t s, int shrink, unsigned int* ovf) {
+  TwinTable tb = table_geometry(n, T, table, shrink, ovf);
   if (t_end > t_begin) {
     const int B = kLabelThreads;
     const int g = grid_for(t_end - t_begin, B);
@@ -491,14 +500,14 @@ void launch_label_a_range(const double* xy, int64_t n, const void* tri, int tri_
 
 void launch_label_a(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int check,
                     int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed, int32_t* tv, void* table,
-                    DevStatus* st, cudaStream_t s) {
-  launch_label_a_prepare(n, T, tv, table, s);
-  launch_label_a_range(xy, n, tri, tri_is64, T, 0, T, check, tri32, hw, max_edge, seed, tv, table, st, s);
+                    DevStatus* st, cudaStream_t s, int shrink, unsigned int* ovf) {
+  launch_label_a_prepare(n, T, tv, table, s, shrink);
+  launch_label_a_range(xy, n, tri, tri_is64, T, 0, T, check, tri32, hw, max_edge, seed, tv, table, st, s, shrink, ovf);
 }
 
 void launch_label_b(const int32_t* tri32, int64_t n, int64_t T, int32_t* hw, const int8_t* max_edge, uint8_t* seed,
-                    int32_t* tv, void* table, int check, DevStatus* st, cudaStream_t s) {
-  TwinTable tb = table_geometry(n, T, table);
+                    int32_t* tv, void* table, int check, DevStatus* st, cudaStream_t s, int shrink) {
+  TwinTable tb = table_geometry(n, T, table, shrink);
   int64_t m = (T > n || tv == nullptr) ? T : n;
   if (m > 0) {
     k_pair_pass<<<grid_for(m, kLabelThreads), kLabelThreads, 0, s>>>(tri32, T, max_edge, tb, hw, seed, tv, n, check,

@@ -294,3 +294,48 @@ def test_pool_overflow_retry_is_exact(cuda):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_shuffled_triangle_order_full_table_rerun(cuda):
+    """A triangle order without Qhull's locality: block-local matching pairs
+    almost nothing, the whole path's half-size twin table overflows, and the
+    call reruns at full size (host and device entry points).  The output must
+    equal the oracle's for the shuffled mesh."""
+    import torch
+    from paper_2204_05438_b200 import _capi
+    from paper_2204_05438_b200.mesh_core import Triangulation
+    tri0 = big_input("u100k_unit")
+    T = tri0.n_triangles
+    perm = np.random.default_rng(7).permutation(T)  # new triangle t = old perm[t]
+    inv = np.empty(T, np.int64)
+    inv[perm] = np.arange(T)
+    nb_old = tri0.neighbors.reshape(-1, 3)[perm]
+    nb = np.where(nb_old >= 0, inv[np.maximum(nb_old, 0)], -1)
+    tri = Triangulation(tri0.vertices.copy(), tri0.triangles.reshape(-1, 3)[perm].ravel(), nb.ravel())
+    ref = oracle.execute(tri)
+    npol, nsl = ctypes.c_int64(), ctypes.c_int64()
+    stats = (ctypes.c_int64 * _capi.NUM_STATS)()
+    # host entry point
+    ctx = _capi.context()
+    off = np.zeros(T + 1, dtype=np.int64)
+    verts = np.zeros(3 * T, dtype=np.int32)
+    rc = _capi.lib().tm_mesh_to_polygons_host(ctx.ptr, _capi.ptr(tri.vertices), tri.n_vertices,
+                                              _capi.ptr(tri.triangles), T, 0, _capi.ptr(off), _capi.ptr(verts),
+                                              T, 3 * T, ctypes.byref(npol), ctypes.byref(nsl), stats)
+    ctx.check(rc)
+    P, F = npol.value, nsl.value
+    assert np.array_equal(off[: P + 1], ref["final"][0]) and np.array_equal(verts[:F], ref["final"][1])
+    # device entry point, fresh context (starts with the half-size table again)
+    ctx2 = _capi.context(cuda)
+    xy = torch.from_numpy(tri.vertices).to(cuda)
+    tr = torch.from_numpy(tri.triangles).to(cuda)
+    doff = torch.empty(T + 1, dtype=torch.int64, device=cuda)
+    dv = torch.empty(3 * T, dtype=torch.int32, device=cuda)
+    for _ in range(2):  # the second call already runs at full size
+        rc = _capi.lib().tm_mesh_to_polygons(ctx2.ptr, _capi.ptr(xy), tri.n_vertices, _capi.ptr(tr), 64, T, 0,
+                                             _capi.ptr(doff), _capi.ptr(dv), T, 3 * T, ctypes.byref(npol),
+                                             ctypes.byref(nsl), stats, _capi.stream_ptr(cuda))
+        ctx2.check(rc)
+        P, F = npol.value, nsl.value
+        assert np.array_equal(doff[: P + 1].cpu().numpy(), ref["final"][0])
+        assert np.array_equal(dv[:F].cpu().numpy(), ref["final"][1])
