@@ -130,6 +130,7 @@ struct tm_ctx {
   // whole path: half-size twin table (block-local matching leaves ~43% of the keys
   // to it); an overflow reruns the call at full size and keeps that for this ctx
   int table_shrink = 1;
+  void* stamp_clean = nullptr;  // stamp buffer known to be all -1
   int label_shrink = 0;  // what the label kernels of the current call use
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
@@ -326,6 +327,11 @@ static int prepare(tm_ctx* ctx, int64_t T, int64_t n = -1) {
   ENSURE(overflow, Tn * sizeof(int32_t));
   ENSURE(queue, Tn * sizeof(int32_t));
   ENSURE(stamp, Tn * sizeof(int32_t));
+  if (ctx->stamp_clean != ctx->stamp.p) {  // all -1 once; k_bfs_slow restores what it stamps
+    CK(cudaMemset(ctx->stamp.p, 0xFF, ctx->stamp.bytes));
+    CK(cudaDeviceSynchronize());
+    ctx->stamp_clean = ctx->stamp.p;
+  }
   ENSURE(tiles, (scan_scratch_elems(3 * Tn) + 8) * sizeof(int64_t));
   ENSURE(lbscan, scan_lookback_bytes(Tn));
   ENSURE(rnext, 3 * Tn * sizeof(int32_t));
@@ -424,7 +430,6 @@ static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* 
     SegTimer t_(ctx, S_SEEDS, s);
     launch_select_flags(d_seed + tb, te - tb, ctx->seeds.as<int32_t>(), &dc->n_seeds, tiles, s, tb);
   }
-  CK(cudaMemsetAsync(ctx->stamp.p, 0xFF, Tn * sizeof(int32_t), s));
   CK(cudaMemsetAsync(ctx->startbits.p, 0, ((3 * Tn + 31) / 32) * sizeof(uint32_t), s));
   {
     SegTimer t_(ctx, S_TRAV_START, s);

@@ -25,7 +25,7 @@ constexpr int kBfsCap = 48;
 // of t, else the FIFO BFS of find_start_frontier (172-192) across non-frontier
 // edges, slots 0,1,2 in order.  The BFS queue doubles as the seen set (every
 // triangle is enqueued exactly when first seen).  Returns -2 on local overflow.
-__device__ int32_t seed_start(const int32_t* __restrict__ hw, int32_t t) {
+__device__ int32_t seed_start(const int32_t* __restrict__ hw, int32_t t, int cap = kBfsCap) {
   int32_t h = min_frontier_slot(hw, t);
   if (h >= 0) return h;
   int32_t q[kBfsCap];
@@ -40,7 +40,7 @@ __device__ int32_t seed_start(const int32_t* __restrict__ hw, int32_t t) {
       bool seen = false;
       for (int i = 0; i < tail; i++) seen |= (q[i] == nt);
       if (!seen) {
-        if (tail == kBfsCap) return -2;
+        if (tail == cap) return -2;
         q[tail++] = nt;
       }
     }
@@ -67,11 +67,11 @@ __device__ __forceinline__ bool is_ruler(const RulerSet& rs, int32_t h) {
 __global__ void __launch_bounds__(256) k_trav_start(const int32_t* __restrict__ hw, const int32_t* __restrict__ seeds,
                                                     const int64_t* __restrict__ Pp, int32_t* __restrict__ start,
                                                     int32_t* __restrict__ overflow, unsigned int* n_overflow,
-                                                    uint32_t* __restrict__ bits, DevStatus* st) {
+                                                    uint32_t* __restrict__ bits, DevStatus* st, int bfs_cap) {
   const int64_t P = *Pp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t t = seeds[i];
-    int32_t h = seed_start(hw, t);
+    int32_t h = seed_start(hw, t, bfs_cap);
     if (h == -2) overflow[atomicAdd(n_overflow, 1u)] = (int32_t)i;
     else if (h < 0) report(st, K_NO_FRONTIER, t);
     else mark_start(bits, h);
@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(256) k_trav_start(const int32_t* __restrict__ 
 
 // Slow path for BFS regions larger than the register queue: one thread, a
 // global FIFO and a stamp array for the seen set.  Rare (max 17 visited at 10M).
+// The stamps are all -1 between runs: set once at allocation, restored here.
 __global__ void k_bfs_slow(const int32_t* __restrict__ hw, const int32_t* __restrict__ seeds,
                            int32_t* __restrict__ start, const int32_t* __restrict__ overflow,
                            const unsigned int* n_overflow, int32_t* __restrict__ queue, int32_t* __restrict__ stamp,
@@ -104,6 +105,7 @@ __global__ void k_bfs_slow(const int32_t* __restrict__ hw, const int32_t* __rest
     if (res < 0) report(st, K_NO_FRONTIER, t);
     else mark_start(bits, res);
     start[i] = res;
+    for (int64_t j = 0; j < tail; j++) stamp[queue[j]] = -1;  // leave the stamps clean (no per-run memset)
   }
 }
 
@@ -312,7 +314,13 @@ static inline int grid_for(int64_t n, int block) {
 void launch_trav_start(const int32_t* hw, const int32_t* seeds, const int64_t* Pp, int64_t Pcap, int32_t* start,
                        int32_t* overflow, unsigned int* n_overflow, int32_t* queue, int32_t* stamp, uint32_t* bits,
                        DevStatus* st, cudaStream_t s) {
-  k_trav_start<<<grid_for(Pcap, 256), 256, 0, s>>>(hw, seeds, Pp, start, overflow, n_overflow, bits, st);
+  static int bfs_cap = -1;
+  if (bfs_cap < 0) {  // testing hook: TERMESH_BFS_CAP sends more seeds to the BFS slow path
+    const char* e = getenv("TERMESH_BFS_CAP");
+    bfs_cap = (e && *e) ? atoi(e) : kBfsCap;
+    if (bfs_cap < 1 || bfs_cap > kBfsCap) bfs_cap = kBfsCap;
+  }
+  k_trav_start<<<grid_for(Pcap, 256), 256, 0, s>>>(hw, seeds, Pp, start, overflow, n_overflow, bits, st, bfs_cap);
   k_bfs_slow<<<1, 32, 0, s>>>(hw, seeds, start, overflow, n_overflow, queue, stamp, bits, st);
   note_launch(2);
 }

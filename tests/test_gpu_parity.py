@@ -339,3 +339,30 @@ def test_shuffled_triangle_order_full_table_rerun(cuda):
         P, F = npol.value, nsl.value
         assert np.array_equal(doff[: P + 1].cpu().numpy(), ref["final"][0])
         assert np.array_equal(dv[:F].cpu().numpy(), ref["final"][1])
+
+
+def test_bfs_slow_path_is_exact(cuda):
+    """TERMESH_BFS_CAP=1 sends every seed whose start half-edge is not in its own
+    triangle to the single-thread BFS slow path (normally only regions larger
+    than 48 triangles); repeated runs in one process also check that the slow
+    path leaves its stamp array clean."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, 'tests'); sys.path.insert(0, '.')\n"
+        "from conftest import load_case, CASE_NAMES\n"
+        "import paper_2204_05438_b200 as tm\n"
+        "for rep in range(2):\n"
+        "  for name in CASE_NAMES:\n"
+        "    tri, g = load_case(name)\n"
+        "    lab = tm.label_all(tri, check=False); m0 = tm.build_polygon_mesh(tri, lab)\n"
+        "    off, v = m0.csr()\n"
+        "    assert np.array_equal(off, g['mesh0_off']) and np.array_equal(v, g['mesh0_verts']), name\n"
+        "    f2, st = tm.execute(tri)\n"
+        "    assert np.array_equal(f2.csr()[1], g['final_verts']), name\n"
+        "print('ok')\n")
+    env = dict(os.environ, TERMESH_BFS_CAP="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
