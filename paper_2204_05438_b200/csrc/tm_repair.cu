@@ -145,7 +145,8 @@ __global__ void __launch_bounds__(256) k_classify(const int64_t* __restrict__ of
                                                   int32_t* __restrict__ items, unsigned int* n_items,
                                                   int32_t* __restrict__ long_list, unsigned int* n_long,
                                                   unsigned long long* stats, const int32_t* __restrict__ hv,
-                                                  int32_t* __restrict__ tv, int append_long) {
+                                                  int32_t* __restrict__ tv, int append_long,
+                                                  int32_t* __restrict__ item_state) {
   __shared__ int s_cnt;
   __shared__ unsigned int s_base;
   if (threadIdx.x == 0) s_cnt = 0;
@@ -175,6 +176,7 @@ __global__ void __launch_bounds__(256) k_classify(const int64_t* __restrict__ of
     const int pi = block_append(is_item, n_items, &s_cnt, &s_base);
     if (is_item) {
       items[pi] = (int32_t)i;
+      item_state[pi] = 0;  // (no per-run memset of the state array)
       item_of[i] = pi;
       if (hv) {  // whole path: fan start of every vertex of the work item (any incident triangle)
         const int64_t b = off[i], e = off[i + 1];
@@ -200,7 +202,8 @@ __global__ void __launch_bounds__(256) k_classify_long(const int64_t* __restrict
                                                        const unsigned int* n_long, int32_t* __restrict__ item_of,
                                                        int32_t* __restrict__ items, unsigned int* n_items,
                                                        unsigned long long* stats, LongQueue q,
-                                                       const int32_t* __restrict__ hv, int32_t* __restrict__ tv) {
+                                                       const int32_t* __restrict__ hv, int32_t* __restrict__ tv,
+                                                       int32_t* __restrict__ item_state) {
   __shared__ int32_t tab[kSetCap];
   __shared__ unsigned int dups;
   unsigned int nl = *n_long;
@@ -243,6 +246,7 @@ __global__ void __launch_bounds__(256) k_classify_long(const int64_t* __restrict
     if (threadIdx.x == 0 && dups > 0) {
       unsigned int k = atomicAdd(n_items, 1u);
       items[k] = i;
+      item_state[k] = 0;
       item_of[i] = (int32_t)k;
       atomicAdd(stats + 2, (unsigned long long)dups);
       atomicAdd(stats + 6, 1ull);
@@ -2378,14 +2382,15 @@ void launch_tv_items(const int64_t* off, const int32_t* v, const int32_t* hv, co
 void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, int32_t* item_of,
                      int32_t* items, unsigned int* n_items, int32_t* long_list, unsigned int* n_long,
                      unsigned long long* stats, LongQueue q, const int32_t* hv, int32_t* tv, int which,
-                     cudaStream_t s) {
+                     int32_t* item_state, cudaStream_t s) {
   if (which != 2) {  // short polygons (and with which == 0 the list of the long ones)
     k_classify<<<grid_for(Pcap, 256), 256, 0, s>>>(off, v, Pp, item_of, items, n_items, long_list, n_long, stats, hv,
-                                                   tv, which == 0);
+                                                   tv, which == 0, item_state);
     note_launch(1);
   }
   if (which == 1) return;
-  k_classify_long<<<kNumSMs * 4, 256, 0, s>>>(off, v, long_list, n_long, item_of, items, n_items, stats, q, hv, tv);
+  k_classify_long<<<kNumSMs * 4, 256, 0, s>>>(off, v, long_list, n_long, item_of, items, n_items, stats, q, hv, tv,
+                                              item_state);
   note_launch(1);
 }
 
