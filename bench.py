@@ -1,11 +1,15 @@
 """Benchmark: mesh -> polygons throughput (input triangles/s) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload u1m]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload u10m]
 
 A step is one pass of the whole hot path -- twin build + labels (K0-K2),
 traversal (K3), repair + stitch (K4) -- over one synthetic Delaunay
-triangulation (BASELINE.json configs[1]: 1M uniform points in the unit square,
-scipy Qhull, seed 0; T = 1,999,963 triangles).
+triangulation.  Default workload: BASELINE.json configs[2], 10M uniform points
+in the unit square (scipy Qhull, seed 0; T = 19,999,954 triangles), the config
+SURVEY.md 8(d) quotes the roofline on (at 1M the vertex array fits in L2).
+--workload u1m | c10m | ... selects another config.  --gpus N without a
+torchrun environment re-launches this script under torch.distributed.run with
+N ranks (127.0.0.1); under torchrun, WORLD_SIZE wins.
 
 GPU arm (default):
   value  device-resident: inputs (xy f64, triangles i64) already in HBM, CUDA
@@ -26,8 +30,17 @@ ends with the exchange -- NCCL all-gather of the per-rank (polygons, slots)
 counts and the shift of the local CSR to its global base.  Strong scaling:
 value = T / (slowest rank's step time); barrier + max-over-ranks timing.
 
+Parity: the final CSR of the last timed step (gathered to rank 0 when N > 1)
+is hashed and compared with the reference's own output for this workload
+(tests/golden/hashes.json, produced by the Python reference); the line's
+"parity" object says whether it matched.
+
 Reference arm (--impl reference): the reference algorithm's CPU port (oracle/)
-on the box's host cores over the same workload, rank 0 only.
+on the box's host cores over the same workload, rank 0 only.  Each step is a
+bounded sample: labels of the whole mesh (OpenMP), then traversal + repair of
+the seeds of one 1/S slice of the triangles (slices rotate across steps);
+value = T / (t_label + S * t_slice), i.e. the whole mesh's throughput
+extrapolated from the sampled slice.
 """
 import argparse
 import ctypes
@@ -168,12 +181,15 @@ def run_gpu(args, rank, world, local_rank):
 
     ctx.check(L.tm_ctx_set_partition(ctx.ptr, t_begin, t_end))
 
+    shard = [None]
+
     def step():
         rc = L.tm_mesh_to_polygons(ctx.ptr, _capi.ptr(xy), n, _capi.ptr(tr), 64, T, 0, _capi.ptr(off),
                                    _capi.ptr(verts), T, 3 * T, ctypes.byref(npol), ctypes.byref(nsl), stats, sp)
         ctx.check(rc)
         if world > 1:  # the exchange step: all-gather counts (NCCL), shift to the global slot base
-            D.stitch(off, verts, npol.value, nsl.value, pinch=(stats[8], stats[9]))
+            shard[0] = D.stitch(off, verts, npol.value, nsl.value, pinch=(stats[8], stats[10]),
+                                resume=D.device_resume(ctx, off, verts, T, stats))
 
     for _ in range(args.warmup):
         step()
@@ -204,6 +220,7 @@ def run_gpu(args, rank, world, local_rank):
     value = T / (ms_per_step / 1e3)  # the one mesh's triangles over the slowest rank's time
     P_out, F_out = npol.value, nsl.value
     repair_stats = dict(zip(_capi.STAT_NAMES, list(stats)))
+    parity = check_parity(args.workload, off, verts, P_out, F_out, shard[0], world, rank)
 
     # per-kernel device time (separate profiled pass; not part of `value`)
     ctx.set_profiling(True)
@@ -266,7 +283,8 @@ def run_gpu(args, rank, world, local_rank):
                                         _capi.ptr(h_v), T, 3 * T, ctypes.byref(npol), ctypes.byref(nsl), stats)
         ctx.check(rc)
         if world > 1:
-            D.stitch(h_off, h_v, npol.value, nsl.value, pinch=(stats[8], stats[9]))
+            D.stitch(h_off, h_v, npol.value, nsl.value, pinch=(stats[8], stats[10]),
+                     resume=D.device_resume(ctx, h_off, h_v, T, stats))
 
     for _ in range(args.warmup):
         e2e_step()
@@ -284,7 +302,6 @@ def run_gpu(args, rank, world, local_rank):
     e2e = {"value": round(T / (e2e_ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(e2e_ms, 3),
            "h2d_bytes_per_step": 16 * n + 24 * T, "d2h_bytes_per_step": 8 * (npol.value + 1) + 4 * nsl.value,
            "api": "tm_mesh_to_polygons_host (C ABI, pinned host buffers)"}
-    # parity spot check of the timed output against the oracle-free golden counts
     out = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
@@ -294,50 +311,151 @@ def run_gpu(args, rank, world, local_rank):
                    "polygon_slots_rank0": F_out, "l2": "flushed (256 MiB write) between steps",
                    "parallelism": f"replicated mesh, seeds partitioned x{world}, NCCL all-gather of counts"},
         "e2e": e2e, "roofline": roofline, "kernels": kernels, "repair_stats": repair_stats,
-        "gpu_launches": int(launches), "clocks": clk.summary(),
+        "gpu_launches": int(launches), "clocks": clk.summary(), "parity": parity,
         "step_ms": {"min": round(min(step_ms), 4), "median": round(statistics.median(step_ms), 4),
                     "max": round(max(step_ms), 4)},
     }
     return out, tri
 
 
-def cpu_baseline(tri, budget_s=12.0):
+# reference outputs of the bench workloads (tests/golden/hashes.json, made by the Python reference)
+GOLDEN_KEY = {"u100k": "u100k_unit", "u1m": "u1m_unit", "u10m": "u10m_unit", "c10m": "c10m_clustered"}
+
+
+def _h16(a):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]
+
+
+def check_parity(workload, off, verts, P, F, shard, world, rank):
+    """Hash the timed path's final CSR (int64 offsets / int64 vertices, the
+    reference dtypes) and compare with the reference's hashes for this input.
+    With N > 1 the rank CSRs are gathered to rank 0 first (outside the timing)."""
+    from paper_2204_05438_b200 import distributed as D
+    if world > 1:
+        g = D.gather_csr(shard, 0)
+        if rank != 0:
+            return None
+        o, v = g
+    else:
+        o = off[: P + 1].cpu().numpy()
+        v = verts[:F].cpu().numpy()
+    got = {"final_off": _h16(o.astype(np.int64)), "final_verts": _h16(v.astype(np.int64)),
+           "final_polygons": int(o.size - 1)}
+    ref = {}
+    try:
+        ref = json.load(open(os.path.join(ROOT, "tests", "golden", "hashes.json"))).get(GOLDEN_KEY.get(workload), {})
+    except Exception:
+        pass
+    if not ref:
+        return {**got, "reference": None, "match": None}
+    match = all(got[k] == ref.get(k) for k in got)
+    return {**got, "reference": f"tests/golden/hashes.json[{GOLDEN_KEY[workload]}]", "match": bool(match)}
+
+
+def reference_sample(tri, k, slices):
+    """One bounded sample of the reference algorithm (CPU port, oracle/): labels
+    of the whole mesh, then traversal + repair of the seeds in slice k of S
+    equal triangle ranges.  Returns (t_label, t_slice) in seconds."""
     import oracle
-    oracle.execute(tri)  # warm (page-in)
+    T = tri.n_triangles
+    b, e = k * T // slices, (k + 1) * T // slices
+    th = host_threads()
+    t0 = time.perf_counter()
+    lab = oracle.label_all(tri, th)
+    t1 = time.perf_counter()
+    sd = lab.seed.copy()
+    sd[:b] = False
+    sd[e:] = False
+    sub = oracle.Labels(lab.max_edge, lab.frontier, sd)
+    m0 = oracle.build_polygon_mesh(tri, sub, th)
+    oracle.repair_all(tri, sub, m0)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1
+
+
+def host_threads():
+    """Every host thread (torchrun sets OMP_NUM_THREADS=1 per rank; the reference
+    arm runs on rank 0 alone and uses the whole host)."""
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
+def reference_slices(T):
+    """Slices per sample so that one step is a few seconds of 16-core CPU work
+    (the 10M mesh takes ~1 min per full pass: 16 slices)."""
+    return max(1, min(64, -(-T // 1_250_000)))
+
+
+def cpu_baseline(tri, budget_s=15.0):
+    S = reference_slices(tri.n_triangles)
+    reference_sample(tri, 0, S)  # warm (page-in)
     runs = []
     t_start = time.perf_counter()
-    while not runs or (time.perf_counter() - t_start < budget_s and len(runs) < 5):
-        t0 = time.perf_counter()
-        oracle.execute(tri)
-        runs.append(time.perf_counter() - t0)
-    s = statistics.mean(runs)
-    return {"value": round(tri.n_triangles / s, 1), "unit": UNIT, "cores": oracle.max_threads(), "kind": "port",
-            "sample": f"full workload mesh (T={tri.n_triangles}), {len(runs)} run(s), mean {s:.3f} s; "
-                      "OpenMP label+traversal, sequential repair (reference 'mixed' mode)"}
+    k = 0
+    while not runs or (time.perf_counter() - t_start < budget_s and len(runs) < 8):
+        runs.append(reference_sample(tri, k % S, S))
+        k += 1
+    est = [tl + S * ts for tl, ts in runs]
+    s = statistics.mean(est)
+    return {"value": round(tri.n_triangles / s, 1), "unit": UNIT, "cores": host_threads(), "kind": "port",
+            "sample": f"{len(runs)} sample(s) of the workload mesh (T={tri.n_triangles}): labels of the whole mesh "
+                      f"(OpenMP) + traversal and sequential repair of one 1/{S} seed slice each (the reference "
+                      f"'mixed' mode); full-mesh time extrapolated as t_label + {S} * t_slice = {s:.2f} s"}
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return None
-    import oracle
     tri = load_mesh(args.workload, 0)
-    for _ in range(args.warmup):
-        oracle.execute(tri)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        oracle.execute(tri)
-        times.append(time.perf_counter() - t0)
-    s = statistics.mean(times)
-    v = round(tri.n_triangles / s, 1)
+    T = tri.n_triangles
+    S = reference_slices(T)
+    for k in range(args.warmup):
+        reference_sample(tri, k % S, S)
+    est = []
+    for k in range(args.steps):
+        tl, ts = reference_sample(tri, (args.warmup + k) % S, S)
+        est.append(tl + S * ts)
+    s = statistics.mean(est)
+    v = round(T / s, 1)
+    sample = (f"per step: labels of the whole mesh (OpenMP) + traversal and sequential repair of the seeds of one "
+              f"1/{S} triangle slice (slices rotate); full-mesh time t_label + {S} * t_slice")
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(s * 1e3, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "int64/f64", "data": "synthetic",
-            "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"],
-                       "triangles": tri.n_triangles},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.max_threads(), "kind": "port",
-                             "sample": f"full workload mesh per step ({args.steps} steps)"},
+            "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"], "triangles": T,
+                       "n_vertices": tri.n_vertices},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": host_threads(), "kind": "port",
+                             "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def launch_command(argv, nproc, port):
+    """torch.distributed.run command that re-launches this script with nproc ranks."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *argv]
+
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def probe_launch(rank, world):
+    """--probe-launch: every rank joins a gloo group and rank 0 reports who joined
+    (the CPU test of the self-launch)."""
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo")
+    t = torch.tensor([rank], dtype=torch.int64)
+    allr = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(allr, t)
+    if rank == 0:
+        print(json.dumps({"probe": True, "world": world, "ranks": [int(x.item()) for x in allr]}), flush=True)
+    dist.destroy_process_group()
 
 
 def main():
@@ -346,13 +464,21 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
-    ap.add_argument("--workload", choices=tuple(WORKLOADS), default="u1m")
+    ap.add_argument("--workload", choices=tuple(WORKLOADS), default="u10m")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--probe-launch", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (the driver may also launch us that way)
+        r = subprocess.run(launch_command(sys.argv[1:], args.gpus, _free_port()))
+        sys.exit(r.returncode)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.probe_launch:
+        probe_launch(rank, world)
+        return
     if args.impl == "reference":
         out = run_reference(args, rank, world)
         if out is not None:

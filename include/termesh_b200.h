@@ -69,7 +69,7 @@ extern "C" {
 #define TM_KIND_STRUCT 15
 #define TM_NUM_KINDS 16
 
-/* repair statistics (tm_repair / tm_mesh_to_polygons_host `stats`, int64[8]);
+/* repair statistics (tm_repair / tm_mesh_to_polygons* `stats`, int64[TM_NUM_STATS]);
  * 0..3 are repair_all's stats_out keys (reparation.py:372-376) */
 #define TM_STAT_ROUNDS 0
 #define TM_STAT_SPLITS 1
@@ -80,13 +80,18 @@ extern "C" {
 #define TM_STAT_PINCH_SPLITS 6
 #define TM_STAT_WORK_ITEMS 7
 /* the pinch pass's round guard (reparation.py:322) is GLOBAL: extra visits of
- * the tip-phase output + 1.  A seed partition runs with its own share
- * (PINCH_EXTRA + 1) and counts the items the guard cut off with pinched
- * polygons left (PINCH_TRUNCATED); the ranks' results equal the single run
- * unless a rank truncated and the global guard is larger. */
+ * the tip-phase output + 1.  A seed partition (tm_ctx_set_partition) knows only
+ * its own share (PINCH_EXTRA): items that reach the local guard with pinched
+ * polygons left are parked (PINCH_DEFERRED); after the ranks exchange their
+ * PINCH_EXTRA, tm_resume_pinch finishes them under the global guard, so the
+ * stitched result equals the single-GPU one.  PINCH_TRUNCATED counts the items
+ * the (final) guard cut off. */
 #define TM_STAT_PINCH_EXTRA 8
 #define TM_STAT_PINCH_TRUNCATED 9
-#define TM_NUM_STATS 10
+/* seed partition only: items parked at the final LOCAL guard; when > 0 the
+ * call's output is provisional and tm_resume_pinch must follow */
+#define TM_STAT_PINCH_DEFERRED 10
+#define TM_NUM_STATS 11
 
 typedef struct tm_ctx tm_ctx;
 
@@ -113,6 +118,14 @@ int64_t tm_launch_count(void);
  * With ranks owning consecutive ranges, the concatenation of their outputs in
  * rank order is the single-GPU output (seed order = raw order, F13). */
 int tm_ctx_set_partition(tm_ctx *ctx, int64_t t_begin, int64_t t_end);
+/* Seed partition, second phase: finish the items the last tm_mesh_to_polygons*
+ * call parked at its local pinch guard, under the global guard
+ * extra_total + 1 (extra_total = sum of every rank's TM_STAT_PINCH_EXTRA), and
+ * rewrite the output CSR.  off_out / v_out are device buffers after
+ * tm_mesh_to_polygons, host buffers after tm_mesh_to_polygons_host; the
+ * capacities are those of the first call.  Reference: reparation.py:315-340. */
+int tm_resume_pinch(tm_ctx *ctx, int64_t extra_total, int64_t *off_out, int32_t *v_out, int64_t cap_polys,
+                    int64_t cap_slots, int64_t *n_polys, int64_t *n_slots, int64_t *stats, void *stream);
 /* d_offsets[0..n_polys] += delta: places a rank's CSR at its global slot base
  * (the exclusive prefix of the all-gathered per-rank slot counts). */
 int tm_shift_offsets(int64_t *d_offsets, int64_t n_polys, int64_t delta, void *stream);
@@ -146,15 +159,18 @@ int tm_unpack_halfedges(tm_ctx *ctx, const int32_t *d_halfedge, int64_t T, int32
 /* overwrite the frontier bits from a caller frontier array (bool/uint8 [3T]) */
 int tm_pack_frontier(tm_ctx *ctx, int32_t *d_halfedge, const uint8_t *d_frontier, int64_t T, void *stream);
 
-/* Traversal.  Capacities: cap_polys >= #seeds, cap_slots >= #frontier
- * half-edges (T and 3T always suffice).  *n_polys / *n_slots are host outputs;
+/* Traversal.  Capacities: cap_polys >= T and cap_slots >= 3T are REQUIRED
+ * (TM_ERR_ARGUMENT otherwise; the output sizes are only known on the device,
+ * #seeds <= T and #frontier half-edges <= 3T, and d_offsets needs cap_polys + 1
+ * entries).  *n_polys / *n_slots are host outputs;
  * the call synchronizes `stream` before returning them. */
 int tm_traverse(tm_ctx *ctx, const int32_t *d_tri32, const int32_t *d_halfedge, const uint8_t *d_seed, int64_t T,
                 int64_t *d_offsets, int32_t *d_verts, int64_t cap_polys, int64_t cap_slots, int64_t *n_polys,
                 int64_t *n_slots, void *stream);
 
 /* Repair.  Mutates the frontier bits of d_halfedge exactly as repair_all
- * mutates labels.frontier.  Capacities T and 3T always suffice.  stats: host
+ * mutates labels.frontier.  Capacities cap_polys >= T and cap_slots >= 3T are
+ * required (as for tm_traverse; the repaired output never exceeds them).  stats: host
  * int64[TM_NUM_STATS]. */
 int tm_repair(tm_ctx *ctx, const int32_t *d_tri32, int32_t *d_halfedge, const int32_t *d_trivertex, int64_t T,
               const int64_t *d_offsets_in, const int32_t *d_verts_in, int64_t n_polys, int64_t *d_offsets_out,

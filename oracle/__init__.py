@@ -35,7 +35,7 @@ def _load():
         lib.or_compute_trivertex.argtypes = [_P, _I64, _I64, _P]
         lib.or_label.argtypes = [_P, _P, _P, _I64, ctypes.c_int, _P, _P, _P]
         lib.or_traverse.argtypes = [_P, _P, _I64, _P, _P, ctypes.c_int, _P, _P, _I64, _I64, _P]
-        lib.or_repair.argtypes = [_P, _P, _P, _I64, _I64, _P, _P, _P, _I64, _P, _P, _I64, _I64, _P, _P]
+        lib.or_repair.argtypes = [_P, _P, _P, _I64, _I64, _P, _P, _P, _I64, _P, _P, _I64, _I64, _P, _P, _I64]
         lib.or_canonicalize.argtypes = [_P, _P, _I64, _P, _P]
         _lib = lib
     return _lib
@@ -110,10 +110,13 @@ def build_polygon_mesh(tri, labels: Labels, threads: int = 0):
     return off, verts[: off[-1]].copy()
 
 
-def repair_all(tri, labels: Labels, mesh):
+def repair_all(tri, labels: Labels, mesh, guard_extra: int = -1):
     """reparation.py:343-377 (round schedule).  Mutates labels.frontier.
 
-    Returns ((offsets, verts), stats dict rounds/splits/initial_tips/unrepaired).
+    guard_extra >= 0 replaces the extra-visit count of the pinch guard
+    (reparation.py:322) -- a seed-partitioned run uses the global one.
+    Returns ((offsets, verts), stats dict rounds/splits/initial_tips/unrepaired/
+    tip_extra), tip_extra = extra visits of the tip-phase output.
     """
     _, tr, nb = _arrays(tri)
     T = tr.size // 3
@@ -131,13 +134,13 @@ def repair_all(tri, labels: Labels, mesh):
     off = np.zeros(cap_p + 1, dtype=np.int64)
     verts = np.empty(cap_s, dtype=np.int64)
     cnt = np.zeros(1, dtype=np.int64)
-    stats = np.zeros(4, dtype=np.int64)
+    stats = np.zeros(5, dtype=np.int64)
     _check(_load().or_repair(_ptr(tr), _ptr(nb), _ptr(tv), T, n, _ptr(labels.frontier),
                              _ptr(off_in), _ptr(v_in), P, _ptr(off), _ptr(verts), cap_p, cap_s,
-                             _ptr(cnt), _ptr(stats)))
+                             _ptr(cnt), _ptr(stats), int(guard_extra)))
     c = int(cnt[0])
     off = off[: c + 1].copy()
-    s = dict(zip(("rounds", "splits", "initial_tips", "unrepaired"), (int(x) for x in stats)))
+    s = dict(zip(("rounds", "splits", "initial_tips", "unrepaired", "tip_extra"), (int(x) for x in stats)))
     return (off, verts[: off[-1]].copy()), s
 
 

@@ -549,10 +549,13 @@ static int has_repeat(const int64_t *s, int64_t n, int64_t *scratch) { return ex
 /* reparation.py:343-377 (repair_all) with the round structure of
  * repair_round (294-312), _execute_round (232-277) and _pinch_pass (315-340).
  * stats = {rounds, splits, initial_tips, unrepaired}. */
+/* guard_extra >= 0 replaces the pinch guard's extra-visit count (a seed
+ * partition runs under the GLOBAL guard: the extra visits summed over all
+ * ranks' tip-phase outputs); stats[4] = this call's tip-phase extra visits. */
 int or_repair(const int64_t *tr, const int64_t *nb, const int64_t *tv, int64_t T, int64_t nverts,
               uint8_t *frontier, const int64_t *off_in, const int64_t *v_in, int64_t P,
               int64_t *off_out, int64_t *v_out, int64_t cap_polys, int64_t cap_slots,
-              int64_t *n_out, int64_t *stats) {
+              int64_t *n_out, int64_t *stats, int64_t guard_extra) {
     Mesh m = {NULL, tr, nb, tv, nverts, T, frontier};
     Polys cur, nxtp;
     int rc = polys_init(&cur);
@@ -589,10 +592,11 @@ int or_repair(const int64_t *tr, const int64_t *nb, const int64_t *tv, int64_t T
         for (int64_t i = 0; i < pcount(&cur); i++) { const int64_t *s = pget(&cur, i, &l); tips += has_tip(s, l); }
         if (tips == 0) break;
     }
-    int64_t before = pcount(&cur);
+    int64_t before = pcount(&cur), tip_extra = 0;
     if (!rc) {
         /* _pinch_pass: reparation.py:315-340 */
-        int64_t guard = mesh_extra_visits(&cur) + 1;
+        tip_extra = mesh_extra_visits(&cur);
+        int64_t guard = (guard_extra >= 0 ? guard_extra : tip_extra) + 1;
         scr = (int64_t *)malloc((size_t)(max_len(&cur) + 2 * guard + 8) * sizeof(int64_t) * 2);
         for (int64_t r = 0; r < guard && !rc; r++) {
             int64_t any = 0, rs = 0;
@@ -634,6 +638,7 @@ int or_repair(const int64_t *tr, const int64_t *nb, const int64_t *tv, int64_t T
             stats[1] = splits + (cnt - before);
             stats[2] = initial;
             stats[3] = unrepaired;
+            stats[4] = tip_extra;
         }
     }
     free(scr);

@@ -17,12 +17,12 @@ LIB_PATH = os.environ.get("TERMESH_LIB_VARIANT") or os.path.join(_HERE, "libterm
 
 TM_OK, TM_ERR_STRUCTURAL, TM_ERR_VALIDATION, TM_ERR_CAPACITY, TM_ERR_CUDA, TM_ERR_ARGUMENT = range(6)
 NUM_KINDS = 16
-NUM_STATS = 10
+NUM_STATS = 11
 KIND_NAMES = ("index_range", "orientation", "degenerate", "duplicate", "reciprocity", "edge_count",
               "trivertex", "neighbors", "walk", "no_frontier", "no_converge", "split_law", "pool",
               "barrier", "no_internal", "structural")
 STAT_NAMES = ("rounds", "splits", "initial_tips", "unrepaired", "nonsimple", "tip_splits",
-              "pinch_splits", "work_items", "pinch_extra", "pinch_truncated")
+              "pinch_splits", "work_items", "pinch_extra", "pinch_truncated", "pinch_deferred")
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -76,12 +76,13 @@ def lib():
                                           _PI64, _P]
         L.tm_mesh_to_polygons_host.argtypes = [_P, _P, _I64, _P, _I64, _I, _P, _P, _I64, _I64, _PI64, _PI64,
                                                _PI64]
+        L.tm_resume_pinch.argtypes = [_P, _I64, _P, _P, _I64, _I64, _PI64, _PI64, _PI64, _P]
         for name in ("tm_ctx_create", "tm_ctx_defects", "tm_ctx_phase_ms", "tm_ctx_set_profiling", "tm_ctx_debug",
                      "tm_ctx_debug_copy",
                      "tm_ctx_set_partition", "tm_shift_offsets", "tm_ctx_segment_ms", "tm_label", "tm_relabel",
                      "tm_check_neighbors",
                      "tm_unpack_halfedges", "tm_pack_frontier", "tm_traverse", "tm_repair",
-                     "tm_mesh_to_polygons", "tm_mesh_to_polygons_host"):
+                     "tm_mesh_to_polygons", "tm_mesh_to_polygons_host", "tm_resume_pinch"):
             getattr(L, name).restype = _I
         _lib = L
     return _lib
@@ -94,7 +95,7 @@ def exported_symbols():
             "tm_ctx_debug", "tm_ctx_debug_copy", "tm_ctx_set_partition", "tm_shift_offsets",
             "tm_label", "tm_relabel", "tm_check_neighbors", "tm_unpack_halfedges",
             "tm_pack_frontier",
-            "tm_traverse", "tm_repair", "tm_mesh_to_polygons_host", "tm_mesh_to_polygons")
+            "tm_traverse", "tm_repair", "tm_mesh_to_polygons_host", "tm_mesh_to_polygons", "tm_resume_pinch")
 
 
 def _require_cuda():
@@ -155,7 +156,12 @@ class Context:
             raise ValidationError("refusing to run on an invalid triangulation: " + msg,
                                   ValidationReport(False, defects))
         if rc == TM_ERR_STRUCTURAL:
-            raise StructuralError(msg)  # message already carries the [phase] tag
+            # the library tags its messages "[phase] ..."; keep the tag as e.phase
+            # (the reference's _phase guarantees e.phase, pipeline.py:114-121)
+            if msg.startswith("[") and "] " in msg:
+                tag, rest = msg[1:].split("] ", 1)
+                raise StructuralError(rest, phase=tag)
+            raise StructuralError(msg, phase=phase)
         if rc == TM_ERR_CAPACITY:
             raise CapacityError(msg)
         if rc == TM_ERR_ARGUMENT:

@@ -23,14 +23,21 @@ using namespace tmb;
 
 namespace {
 
+// Every (re)allocation of a library buffer bumps this generation: a captured
+// graph and the "stamp buffer is all -1" fact are only valid for the
+// generation they were made in (cudaFree + cudaMalloc may return the same address).
+std::atomic<unsigned long long> g_alloc_gen{1};
+
 struct Buf {
   void* p = nullptr;
   size_t bytes = 0;
+  unsigned long long gen = 0;  // g_alloc_gen value of the current allocation
   bool ensure(size_t want) {
     if (want <= bytes && p) return true;
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
+    gen = g_alloc_gen.fetch_add(1) + 1;
     size_t b = want < 256 ? 256 : want;
     if (cudaMalloc(&p, b) != cudaSuccess) return false;
     bytes = b;
@@ -58,7 +65,12 @@ struct Counters {
   unsigned int q_huge, q_long, q_next, n_parked;
   unsigned int tip_next, table_ovf, pad2, pad3;
   unsigned long long pool_top, undo_top;
-  unsigned long long stats[8];
+  // stats[0..7]: repair statistics (fill_stats); stats[8]: extra visits of the
+  // other ranks (host-set before tm_resume_pinch); stats[9]: seed partition,
+  // park items at the final local pinch guard (host-set in the reset image);
+  // stats[10]: items parked there (deferred to tm_resume_pinch); stats[11]: local
+  // guard cap (testing hook TERMESH_PINCH_GUARD_CAP, partitions only)
+  unsigned long long stats[12];
   unsigned long long dbg[128];  // optional kernel timestamps / counters (tm_ctx_debug)
 };
 
@@ -90,9 +102,11 @@ struct GraphKey {
   int64_t n = -1, T = -1, tb = 0, te = 0;
   int bits = 0, check = 0, ext = 0;
   unsigned long long pool_cap = 0;
+  unsigned long long alloc_gen = 0;  // no library buffer reallocated since the capture
   bool operator==(const GraphKey& o) const {
     return xy == o.xy && tri == o.tri && off == o.off && v == o.v && n == o.n && T == o.T && tb == o.tb &&
-           te == o.te && bits == o.bits && check == o.check && ext == o.ext && pool_cap == o.pool_cap;
+           te == o.te && bits == o.bits && check == o.check && ext == o.ext && pool_cap == o.pool_cap &&
+           alloc_gen == o.alloc_gen;
   }
 };
 
@@ -130,7 +144,7 @@ struct tm_ctx {
   // whole path: half-size twin table (block-local matching leaves ~43% of the keys
   // to it); an overflow reruns the call at full size and keeps that for this ctx
   int table_shrink = 1;
-  void* stamp_clean = nullptr;  // stamp buffer known to be all -1
+  unsigned long long stamp_clean = 0;  // allocation generation of the stamp buffer known to be all -1
   int label_shrink = 0;  // what the label kernels of the current call use
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
@@ -149,6 +163,9 @@ struct tm_ctx {
   cudaStream_t cstream = nullptr;
   cudaEvent_t chunk_ev[kUploadChunks] = {};
   long long graph_kernels = 0;  // kernels per graph replay (counted at capture)
+  // the last whole-path call, for tm_resume_pinch
+  int64_t last_T = -1;
+  bool last_host = false;
 };
 
 static int set_err(tm_ctx* c, int code, const char* fmt, ...) {
@@ -327,10 +344,10 @@ static int prepare(tm_ctx* ctx, int64_t T, int64_t n = -1) {
   ENSURE(overflow, Tn * sizeof(int32_t));
   ENSURE(queue, Tn * sizeof(int32_t));
   ENSURE(stamp, Tn * sizeof(int32_t));
-  if (ctx->stamp_clean != ctx->stamp.p) {  // all -1 once; k_bfs_slow restores what it stamps
+  if (ctx->stamp_clean != ctx->stamp.gen) {  // all -1 once per allocation; k_bfs_slow restores what it stamps
     CK(cudaMemset(ctx->stamp.p, 0xFF, ctx->stamp.bytes));
     CK(cudaDeviceSynchronize());
-    ctx->stamp_clean = ctx->stamp.p;
+    ctx->stamp_clean = ctx->stamp.gen;
   }
   ENSURE(tiles, (scan_scratch_elems(3 * Tn) + 8) * sizeof(int64_t));
   ENSURE(lbscan, scan_lookback_bytes(Tn));
@@ -566,6 +583,7 @@ static void fill_stats(const Counters& h, int64_t* stats) {
   stats[TM_STAT_WORK_ITEMS] = (int64_t)h.n_items;
   stats[TM_STAT_PINCH_EXTRA] = (int64_t)h.stats[5];
   stats[TM_STAT_PINCH_TRUNCATED] = (int64_t)h.stats[7];
+  stats[TM_STAT_PINCH_DEFERRED] = (int64_t)h.stats[10];
 }
 
 // Pool overflow: restore the pre-repair frontier bits (restore()), grow the
@@ -587,6 +605,7 @@ static int retry_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, cons
     CK(cudaMemsetAsync(&dc->n_items, 0, 3 * sizeof(unsigned int), s));  // n_items, n_long, n_pinch
     CK(cudaMemsetAsync(&dc->q_huge, 0, 8 * sizeof(unsigned int), s));  // queues + tip_next
     CK(cudaMemsetAsync(&dc->pool_top, 0, 10 * sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(&dc->stats[10], 0, sizeof(unsigned long long), s));
     r = enqueue_repair(ctx, d_tri32, d_hw, d_tv, T, d_off_in, d_v_in, Pp, d_off_out, d_v_out, s);
     if (r) return r;
     rc = finish(ctx, s, h);
@@ -852,20 +871,35 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
   int32_t* v0 = ctx->v0.as<int32_t>();
   Counters* dc = dc_of(ctx);
   ctx->label_shrink = ctx->table_shrink;
+  {
+    // a seed partition parks the items its final LOCAL pinch guard would cut off
+    // (the guard is global, reparation.py:322); tm_resume_pinch finishes them
+    int64_t tb = 0, te = 0;
+    part_range(ctx, T, &tb, &te);
+    ctx->h_reset->stats[8] = 0;
+    ctx->h_reset->stats[9] = (tb > 0 || te < T) ? 1 : 0;
+    const char* cap = getenv("TERMESH_PINCH_GUARD_CAP");  // testing hook (partitions only)
+    ctx->h_reset->stats[11] = (ctx->h_reset->stats[9] && cap && *cap) ? strtoull(cap, nullptr, 10) : 0;
+  }
+  ctx->last_T = -1;
 
   bool capturing = false;
   // external event nodes inside a capture, plain records otherwise
   auto rec = [&](cudaEvent_t e, cudaStream_t s) {
     return capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s);
   };
-  auto body = [&](cudaStream_t s) -> int {
+  // part 1: reset + labels; part 2: traversal + repair + readback; 3: both
+  auto body = [&](cudaStream_t s, int part = 3) -> int {
     int r;
-    if (!ctx->label_a_external && (r = enqueue_reset(ctx, s))) return r;
-    CK(rec(ctx->ev[0], s));
-    if ((r = enqueue_label(ctx, d_xy, n, d_tri, tri_bits, T, check, tri32, hw, ctx->max_edge.as<int8_t>(),
-                           ctx->seed.as<uint8_t>(), nullptr, s)))
-      return r;
-    CK(rec(ctx->ev[1], s));
+    if (part & 1) {
+      if (!ctx->label_a_external && (r = enqueue_reset(ctx, s))) return r;
+      CK(rec(ctx->ev[0], s));
+      if ((r = enqueue_label(ctx, d_xy, n, d_tri, tri_bits, T, check, tri32, hw, ctx->max_edge.as<int8_t>(),
+                             ctx->seed.as<uint8_t>(), nullptr, s)))
+        return r;
+      CK(rec(ctx->ev[1], s));
+    }
+    if (!(part & 2)) return enqueue_readback(ctx, s);
     ctx->path_hv = ctx->hv.as<int32_t>();
     static int no_early = -1;
     if (no_early < 0) no_early = getenv("TERMESH_NO_EARLY") != nullptr;  // A/B switch
@@ -882,8 +916,19 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
   };
 
   cudaStream_t s = user;
-  if (ctx->use_graph && !ctx->prof.on) {
-    GraphKey key{d_xy, d_tri, d_off, d_v, n, T, 0, 0, tri_bits, check, ctx->label_a_external ? 1 : 0, ctx->pool_cap};
+  if (check) {
+    // Validation first: a defective mesh (e.g. an out-of-range corner) must not
+    // reach the traversal and repair kernels, which index by corner.  The label
+    // passes run on their own, the status is decoded, then the rest follows.
+    if ((rc = body(s, 1))) return rc;
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    if (ctx->h_result->table_ovf) return kRetryTable;  // (check mode uses the full table; defensive)
+    if ((rc = decode_status(ctx, *ctx->h_result))) return rc;
+    if ((rc = body(s, 2))) return rc;
+  } else if (ctx->use_graph && !ctx->prof.on) {
+    GraphKey key{d_xy, d_tri, d_off, d_v, n, T, 0, 0, tri_bits, check, ctx->label_a_external ? 1 : 0, ctx->pool_cap,
+                 g_alloc_gen.load()};
     part_range(ctx, T, &key.tb, &key.te);
     if (!ctx->graph || !(key == ctx->gkey)) {
       if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
@@ -948,6 +993,7 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
   *n_polys = h.p_out;
   *n_slots = h.f_out;
   fill_stats(h, stats);
+  ctx->last_T = T;
   return TM_OK;
 }
 
@@ -963,7 +1009,56 @@ int tm_mesh_to_polygons(tm_ctx* ctx, const double* d_xy, int64_t n, const void* 
   if (rc == kRetryTable)  // now at full table size
     rc = run_device(ctx, d_xy, n, d_tri, tri_bits, T, check, d_off, d_v, n_polys, n_slots, stats,
                     (cudaStream_t)stream);
+  ctx->last_host = false;
   return rc;
+}
+
+int tm_resume_pinch(tm_ctx* ctx, int64_t extra_total, int64_t* off_out, int32_t* v_out, int64_t cap_polys,
+                    int64_t cap_slots, int64_t* n_polys, int64_t* n_slots, int64_t* stats, void* stream) {
+  if (!ctx || !n_polys || !n_slots || !off_out || !v_out) return TM_ERR_ARGUMENT;
+  if (ctx->last_T < 0) return set_err(ctx, TM_ERR_ARGUMENT, "tm_resume_pinch needs a preceding whole-path call");
+  const int64_t T = ctx->last_T, Tn = T > 0 ? T : 1;
+  const unsigned long long local = ctx->h_result->stats[5];
+  if (extra_total < (int64_t)local)
+    return set_err(ctx, TM_ERR_ARGUMENT, "global extra visits %lld below this rank's %llu", (long long)extra_total,
+                   local);
+  if (cap_polys < T || cap_slots < 3 * T)
+    return set_err(ctx, TM_ERR_ARGUMENT, "output capacities must be at least T polygons and 3T slots");
+  const bool host = ctx->last_host;
+  cudaStream_t s = host ? ctx->gstream : (cudaStream_t)stream;
+  Counters* dc = dc_of(ctx);
+  int64_t* d_off = host ? ctx->fin_off.as<int64_t>() : off_out;
+  int32_t* d_v = host ? ctx->fin_v.as<int32_t>() : v_out;
+  const int64_t* off0 = ctx->off0.as<int64_t>();
+  const int32_t* v0 = ctx->v0.as<int32_t>();
+  *ctx->h_pin = extra_total - (int64_t)local;
+  CK(cudaMemcpyAsync(&dc->stats[8], ctx->h_pin, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  ctx->path_hv = ctx->hv.as<int32_t>();
+  RepairArgs a = repair_args(ctx, ctx->tri32.as<int32_t>(), ctx->hw.as<int32_t>(), ctx->tv.as<int32_t>(), T, off0,
+                             v0);
+  launch_repair_pinch(a, 3, s);
+  ctx->path_hv = nullptr;
+  launch_out_counts(off0, &dc->n_seeds, Tn, ctx->item_of.as<int32_t>(), ctx->item_n.as<int32_t>(),
+                    ctx->item_slots.as<int64_t>(), ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), dc->stats,
+                    &dc->st, s);
+  launch_scan_lookback(ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), ctx->pbase.as<int64_t>(),
+                       ctx->sbase.as<int64_t>(), &dc->n_seeds, Tn, ctx->lbscan.p, s, &dc->p_out, &dc->f_out, d_off);
+  launch_stitch(off0, v0, &dc->n_seeds, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(), &dc->n_items,
+                ctx->item_list.as<int64_t>(), ctx->item_n.as<int32_t>(), ctx->pool.as<int32_t>(),
+                ctx->pbase.as<int64_t>(), ctx->sbase.as<int64_t>(), d_off, d_v, s);
+  CK(cudaGetLastError());
+  Counters h;
+  int rc = finish(ctx, s, &h);
+  if (rc) return rc;  // (a pool overflow here is not retried: the pinch pass allocates little)
+  *n_polys = h.p_out;
+  *n_slots = h.f_out;
+  fill_stats(h, stats);
+  if (host) {
+    CK(cudaMemcpyAsync(off_out, d_off, (*n_polys + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(v_out, d_v, *n_slots * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  return TM_OK;
 }
 
 int tm_mesh_to_polygons_host(tm_ctx* ctx, const double* h_xy, int64_t n, const int64_t* h_tri, int64_t T, int check,
@@ -1008,6 +1103,7 @@ int tm_mesh_to_polygons_host(tm_ctx* ctx, const double* h_xy, int64_t n, const i
   rc = run_device(ctx, ctx->xy.as<double>(), n, ctx->tri.p, 64, T, check, ctx->fin_off.as<int64_t>(),
                   ctx->fin_v.as<int32_t>(), n_polys, n_slots, stats, s);
   ctx->label_a_external = false;
+  ctx->last_host = true;
   if (rc == kRetryTable)  // the half-size twin table overflowed: once more at full size
     return tm_mesh_to_polygons_host(ctx, h_xy, n, h_tri, T, check, h_off, h_v, cap_polys, cap_slots, n_polys,
                                     n_slots, stats);

@@ -1115,6 +1115,7 @@ struct PinchPark {
   int32_t* item_depth = nullptr;
   int32_t* list = nullptr;
   unsigned int* n = nullptr;
+  unsigned long long* deferred = nullptr;  // counts items parked at the FINAL local guard (seed partition)
 };
 __device__ void warp_finish_pinch(const RepairCtx& c, int64_t w, int32_t poly, long long list, int n, int lane,
                                   int64_t* item_list, int32_t* item_n, int64_t* item_slots,
@@ -1141,6 +1142,7 @@ __device__ void warp_finish_pinch(const RepairCtx& c, int64_t w, int32_t poly, l
           park.item_depth[w] = (int32_t)r;
           park.item_state[w] = 4;
           park.list[atomicAdd(park.n, 1u)] = (int32_t)w;
+          if (park.deferred) atomicAdd(park.deferred, 1ull);
         }
         return;
       }
@@ -2187,7 +2189,15 @@ __global__ void __launch_bounds__(128) k_repair_pinch(RepairCtx c, const int32_t
   extern __shared__ int2 s_pdup[];  // [4][kPinchDupCap]
   const int lane = threadIdx.x & 31;
   int2* stab = s_pdup + (threadIdx.x >> 5) * kPinchDupCap;
-  const long long guard = (long long)*(volatile unsigned long long*)(stats + 5) + 1;
+  // reparation.py:322: guard = extra visits of the tip-phase output + 1.  stats[5]
+  // sums this context's items; stats[8] adds the other ranks' share (seed
+  // partition, host-set before the resume pass, mode 3).
+  long long guard = (long long)*(volatile unsigned long long*)(stats + 5) + 1 +
+                    (long long)*(volatile unsigned long long*)(stats + 8);
+  // testing hook (seed partitions only, TERMESH_PINCH_GUARD_CAP): a smaller local
+  // guard parks more items, so tm_resume_pinch's path runs on small meshes
+  const long long cap = (long long)*(volatile unsigned long long*)(stats + 11);
+  if (cap > 0 && mode != 3 && guard > cap) guard = cap;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   if (mode == 0) {
@@ -2219,19 +2229,43 @@ __global__ void __launch_bounds__(128) k_repair_pinch(RepairCtx c, const int32_t
     }
     return;
   }
-  // mode 1, final guard: the long items k_repair_tips resumed, then every parked item
   const unsigned int np = *q.n_parked;
+  if (mode == 3) {
+    // seed partition, resume under the GLOBAL guard: the items the final local
+    // guard parked (state 4; the parked list may hold an item twice, the CAS claims it once)
+    for (int64_t k = warp; k < np; k += nwarps) {
+      const int64_t w = q.parked[k];
+      int claimed = 0;
+      if (lane == 0) claimed = atomicCAS(item_state + w, 4, 1) == 4;
+      if (!__shfl_sync(kFull, claimed, 0)) continue;
+      warp_finish_pinch(c, w, items[w], item_list[w], item_n[w], lane, item_list, item_n, item_slots, stats, guard,
+                        stab, item_depth[w]);
+    }
+    return;
+  }
+  // mode 1, final (local) guard: the long items k_repair_tips resumed, then every
+  // parked item.  Seed partition (stats[9] != 0): the global guard is not known
+  // yet, so an item reaching the local one is parked again for mode 3 instead of
+  // being cut off.
+  const bool defer = *(volatile unsigned long long*)(stats + 9) != 0;
+  PinchPark park;
+  if (defer) park = PinchPark{item_state, item_depth, q.parked, q.n_parked, stats + 10};
   for (int64_t k = warp; k < nh + nl + np; k += nwarps) {
     const int64_t w = k < nh ? q.huge[k] : k < nh + nl ? q.longq[k - nh] : q.parked[k - nh - nl];
     const bool parked = k >= nh + nl;
     if (!parked && item_state[w] != 2 && item_state[w] != 3) continue;  // done by mode 2 (or parked)
+    if (parked) {
+      int claimed = 0;
+      if (lane == 0) claimed = atomicCAS(item_state + w, 4, 1) == 4;
+      if (!__shfl_sync(kFull, claimed, 0)) continue;
+    }
     const long long list = item_list[w];
     if (list < 0) {
       if (lane == 0) item_slots[w] = 0;
       continue;
     }
     warp_finish_pinch(c, w, items[w], list, item_n[w], lane, item_list, item_n, item_slots, stats, guard, stab,
-                      parked ? item_depth[w] : 0);
+                      parked ? item_depth[w] : 0, park);
   }
 }
 

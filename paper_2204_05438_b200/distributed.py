@@ -12,8 +12,11 @@ the stitch are all restricted to that range).  Distinct polygons have
 disjoint interiors, so the ranks' frontier promotions never interact
  and no label exchange is needed afterwards.
 
-The one exchange step is an all-gather of each rank's (polygon count, slot
-count) -- 16 bytes per rank, NCCL over NVLink on GPUs, gloo in the CPU tests.
+The exchange step is an all-gather of each rank's (polygon count, slot count,
+pinch extra visits, deferred items) -- 32 bytes per rank, NCCL over NVLink on
+GPUs, gloo in the CPU tests.  The pinch pass's round guard is global
+(reparation.py:322); a rank that parked items at its local guard finishes them
+under the global one (tm_resume_pinch) and the counts go round once more.
 Its exclusive prefix gives every rank its global polygon / slot base; shifting
 the local CSR offsets by the slot base (tm_shift_offsets) stitches the global
 CSR, whose rank-ordered concatenation is exactly the single-GPU output
@@ -44,8 +47,8 @@ def exclusive_bases(counts) -> tuple[np.ndarray, np.ndarray]:
 
 
 def exchange_counts(n_polys: int, n_slots: int, device, group=None, pinch=(0, 0)) -> np.ndarray:
-    """All-gather (polygons, slots, pinch extra visits, pinch-truncated items) of every
-    rank: int64[world, 4] on every rank (32 bytes per rank)."""
+    """All-gather (polygons, slots, pinch extra visits, pinch-deferred items) of
+    every rank: int64[world, 4] on every rank (32 bytes per rank)."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
@@ -57,19 +60,17 @@ def exchange_counts(n_polys: int, n_slots: int, device, group=None, pinch=(0, 0)
     return allc.view(world, 4).cpu().numpy()
 
 
-def check_pinch_guard(table) -> None:
-    """The pinch pass's round guard is global (reparation.py:322: extra visits
-    of the whole tip-phase output + 1); each rank ran with its own share.  A
-    rank whose guard cut items off (truncated > 0) must have had the global
-    guard, else its output differs from the single-GPU run: fail loudly.
-    table rows: (polygons, slots, extra, truncated)."""
-    t = np.asarray(table, dtype=np.int64).reshape(-1, 4)
-    total = int(t[:, 2].sum())
-    bad = (t[:, 3] > 0) & (t[:, 2] != total)
-    if bad.any():
-        from .errors import StructuralError
-        raise StructuralError(f"pinch round guard binds on rank(s) {np.flatnonzero(bad).tolist()}: the "
-                              "partitioned result would differ from the single-GPU one", phase="reparation")
+def global_pinch_extra(table) -> int:
+    """The pinch guard's extra-visit count of the whole mesh (reparation.py:322:
+    extra_vertex_visits of the tip-phase output): the sum of every rank's share.
+    table rows: (polygons, slots, extra, deferred)."""
+    return int(np.asarray(table, dtype=np.int64).reshape(-1, 4)[:, 2].sum())
+
+
+def needs_resume(table) -> bool:
+    """Some rank parked items at its local pinch guard (TM_STAT_PINCH_DEFERRED):
+    those ranks resume under the global guard and the counts are exchanged again."""
+    return bool((np.asarray(table, dtype=np.int64).reshape(-1, 4)[:, 3] > 0).any())
 
 
 @dataclass
@@ -88,15 +89,30 @@ class ShardedCSR:
         return int(self.offsets.numel() - 1)
 
 
-def stitch(local_off, local_verts, n_polys: int, n_slots: int, group=None, shift=None, pinch=(0, 0)) -> ShardedCSR:
-    """Exchange counts and place this rank's CSR at its global base.  `shift`
-    adds the slot base to the offsets in place (default: the C ABI kernel on
-    a CUDA tensor, a plain add on CPU tensors); `pinch` = this rank's
-    (TM_STAT_PINCH_EXTRA, TM_STAT_PINCH_TRUNCATED) for the global guard check."""
+def stitch(local_off, local_verts, n_polys: int, n_slots: int, group=None, shift=None, pinch=(0, 0),
+           resume=None) -> ShardedCSR:
+    """Exchange counts and place this rank's CSR at its global base.
+
+    pinch = this rank's (TM_STAT_PINCH_EXTRA, TM_STAT_PINCH_DEFERRED).  The pinch
+    guard is global (reparation.py:322), so a rank that parked items at its local
+    guard must finish them under the global one before its counts are final:
+    `resume(extra_total) -> (n_polys, n_slots)` does that (tm_resume_pinch on the
+    device) and a second all-gather publishes the final counts.  Without deferred
+    items anywhere (the usual case) the first exchange is the only one.
+    `shift` adds the slot base to the offsets in place (default: the C ABI kernel
+    on a CUDA tensor, a plain add on CPU tensors)."""
     import torch.distributed as dist
     rank = dist.get_rank(group)
-    table = exchange_counts(n_polys, n_slots, local_off.device if local_off.is_cuda else "cpu", group, pinch)
-    check_pinch_guard(table)
+    dev = local_off.device if local_off.is_cuda else "cpu"
+    table = exchange_counts(n_polys, n_slots, dev, group, pinch)
+    if needs_resume(table):
+        if int(pinch[1]) > 0:
+            if resume is None:
+                from .errors import StructuralError
+                raise StructuralError("items parked at the local pinch guard and no resume step given",
+                                      phase="reparation")
+            n_polys, n_slots = resume(global_pinch_extra(table))
+        table = exchange_counts(n_polys, n_slots, dev, group, (int(pinch[0]), 0))
     counts = table[:, :2]
     pb, sb = exclusive_bases(counts)
     off = local_off[: n_polys + 1]
@@ -104,6 +120,22 @@ def stitch(local_off, local_verts, n_polys: int, n_slots: int, group=None, shift
         shift = _shift_device if off.is_cuda else _shift_host
     shift(off, n_polys, int(sb[rank]))
     return ShardedCSR(off, local_verts[:n_slots], int(pb[rank]), int(sb[rank]), counts)
+
+
+def device_resume(ctx, off, verts, T: int, stats=None):
+    """resume callable for stitch(): tm_resume_pinch on `ctx`'s last whole-path
+    call (device output buffers off / verts), stats updated in place."""
+    from . import _capi
+
+    def run(extra_total: int):
+        npol, nsl = ctypes.c_int64(), ctypes.c_int64()
+        st = stats if stats is not None else (ctypes.c_int64 * _capi.NUM_STATS)()
+        rc = _capi.lib().tm_resume_pinch(ctx.ptr, int(extra_total), _capi.ptr(off), _capi.ptr(verts), T, 3 * T,
+                                         ctypes.byref(npol), ctypes.byref(nsl), st,
+                                         _capi.stream_ptr(off.device) if off.is_cuda else None)
+        ctx.check(rc, "reparation")
+        return npol.value, nsl.value
+    return run
 
 
 def _shift_host(off, n_polys, delta):
@@ -170,6 +202,15 @@ def run_partition(xy, tri, n: int, T: int, t_begin: int, t_end: int, ctx=None, o
     return off, verts, npol.value, nsl.value, dict(zip(_capi.STAT_NAMES, list(stats)))
 
 
+def resume_partition(ctx, off, verts, T: int, extra_total: int):
+    """Second phase of a partition run whose stats report pinch_deferred > 0:
+    tm_resume_pinch under the global guard.  Returns (n_polys, n_slots, stats)."""
+    from . import _capi
+    stats = (ctypes.c_int64 * _capi.NUM_STATS)()
+    p, f = device_resume(ctx, off, verts, T, stats)(extra_total)
+    return p, f, dict(zip(_capi.STAT_NAMES, list(stats)))
+
+
 def execute_distributed(tri, group=None, gather: bool = True):
     """Drop-in multi-GPU execute: every rank passes the same Triangulation; the
     global final CSR comes back on rank 0 (gather=True) or as shards."""
@@ -181,8 +222,11 @@ def execute_distributed(tri, group=None, gather: bool = True):
     xy = torch.from_numpy(np.ascontiguousarray(tri.vertices)).to(dev)
     tr = torch.from_numpy(np.ascontiguousarray(tri.triangles)).to(dev)
     b, e = partition(T, world)[rank]
-    off, verts, p, f, stats = run_partition(xy, tr, n, T, b, e)
-    shard = stitch(off, verts, p, f, group, pinch=(stats["pinch_extra"], stats["pinch_truncated"]))
+    from . import _capi
+    ctx = _capi.context(dev)
+    off, verts, p, f, stats = run_partition(xy, tr, n, T, b, e, ctx=ctx)
+    shard = stitch(off, verts, p, f, group, pinch=(stats["pinch_extra"], stats["pinch_deferred"]),
+                   resume=device_resume(ctx, off, verts, T))
     if not gather:
         return shard, stats
     return gather_csr(shard, 0, group), stats

@@ -43,5 +43,6 @@ def repair_all(tri: Triangulation, labels, mesh: PolygonMesh, backend: Backend =
     if stats_out is not None:
         for k, name in enumerate(_capi.STAT_NAMES):
             stats_out[name] = int(stats[k])
+        stats_out["tip_extra"] = stats_out["pinch_extra"]  # extra visits of the tip-phase output
     Pn, Fn = n_polys.value, n_slots.value
     return PolygonMesh(count=Pn, offsets=off[: Pn + 1], verts=verts[:Fn])

@@ -119,6 +119,14 @@ def write_small():
               "stats", out["stats"].tolist(), flush=True)
 
 
+def clustered(n, clusters=64, sigma=0.002, seed=0):
+    """Gaussian clusters around uniform centres in the unit square."""
+    rng = np.random.default_rng(seed)
+    c = rng.uniform(0, 1, (clusters, 2))
+    lab = rng.integers(0, clusters, n)
+    return tri_from_points(c[lab] + rng.normal(0, sigma, (n, 2)))
+
+
 def big_case(name, tri):
     t0 = time.perf_counter()
     out = run_reference(tri)
@@ -149,6 +157,7 @@ def write_big(which):
         "u100k_unit": lambda: tm.generate_random_delaunay(100_000, (0, 0, 1, 1), 0),
         "u1m_unit": lambda: tm.generate_random_delaunay(1_000_000, (0, 0, 1, 1), 0),
         "u10m_unit": lambda: tm.generate_random_delaunay(10_000_000, (0, 0, 1, 1), 0),
+        "c10m_clustered": lambda: clustered(10_000_000),
     }
     for name in which:
         data[name] = big_case(name, gens[name]())

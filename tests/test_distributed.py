@@ -29,15 +29,17 @@ def _free_port():
     return p
 
 
-def oracle_partition(tri, b, e):
-    """The reference algorithm on the polygons whose seed lies in [b, e)."""
+def oracle_partition(tri, b, e, guard_extra=-1):
+    """The reference algorithm on the polygons whose seed lies in [b, e), pinch
+    guard from `guard_extra` (the global extra visits) or, with -1, from this
+    range alone.  Returns (offsets, verts, tip-phase extra visits)."""
     lab = oracle.label_all(tri)
     off, v = oracle.build_polygon_mesh(tri, lab)
     seeds = np.flatnonzero(lab.seed)
     i0, i1 = np.searchsorted(seeds, b), np.searchsorted(seeds, e)
     sub = (off[i0:i1 + 1] - off[i0], v[off[i0]:off[i1]])
-    (fo, fv), _ = oracle.repair_all(tri, lab, sub)
-    return fo, fv
+    (fo, fv), st = oracle.repair_all(tri, lab, sub, guard_extra)
+    return fo, fv, st["tip_extra"]
 
 
 def test_partition_covers_range():
@@ -63,9 +65,22 @@ def _worker(rank, world, port, names, q):
         for name in names:
             tri, g = load_case(name)
             b, e = D.partition(tri.n_triangles, world)[rank]
-            fo, fv = oracle_partition(tri, b, e)
+            fo, fv, extra = oracle_partition(tri, b, e)
             p, f = fo.size - 1, int(fo[-1])
-            shard = D.stitch(torch.from_numpy(fo.copy()), torch.from_numpy(fv.astype(np.int32)), p, f)
+            bufs = {"off": torch.from_numpy(np.zeros(tri.n_triangles + 1, np.int64)),
+                    "v": torch.from_numpy(np.zeros(3 * tri.n_triangles + 1, np.int32))}
+            bufs["off"][: p + 1] = torch.from_numpy(fo)
+            bufs["v"][:f] = torch.from_numpy(fv.astype(np.int32))
+
+            def resume(extra_total, tri=tri, b=b, e=e, bufs=bufs):
+                # second phase under the GLOBAL pinch guard (reparation.py:322)
+                ro, rv, _ = oracle_partition(tri, b, e, extra_total)
+                bufs["off"][: ro.size] = torch.from_numpy(ro)
+                bufs["v"][: rv.size] = torch.from_numpy(rv.astype(np.int32))
+                return ro.size - 1, int(ro[-1])
+
+            # every rank reports a deferred item, so the two-exchange protocol runs
+            shard = D.stitch(bufs["off"], bufs["v"], p, f, pinch=(extra, 1), resume=resume)
             assert shard.counts.shape == (world, 2)
             out = D.gather_csr(shard, 0)
             if rank == 0:
@@ -87,30 +102,40 @@ def test_stitch_gloo(world):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("cap", [None, "1"])
 @pytest.mark.parametrize("world", [2, 3, 8])
 @pytest.mark.parametrize("name", CASES)
-def test_partitioned_device_path(cuda, name, world):
+def test_partitioned_device_path(cuda, name, world, cap, monkeypatch):
+    """Logical ranks on one GPU (one context each), the two-phase pinch guard:
+    ranks that parked items at their local guard resume under the global one.
+    cap = "1" (TERMESH_PINCH_GUARD_CAP) forces the local guard down to one round,
+    so every pinch-prone item takes the park -> resume path."""
     import torch
+    from paper_2204_05438_b200 import _capi
+    if cap:
+        monkeypatch.setenv("TERMESH_PINCH_GUARD_CAP", cap)
     tri, g = load_case(name)
     n, T = tri.n_vertices, tri.n_triangles
     xy = torch.from_numpy(tri.vertices).to(cuda)
     tr = torch.from_numpy(tri.triangles).to(cuda)
-    locs, guard = [], []
+    ranks, table = [], []
     for b, e in D.partition(T, world):
-        off, v, p, f, st = D.run_partition(xy, tr, n, T, b, e)
-        locs.append((off[: p + 1].clone(), v[:f].clone(), p, f))
-        guard.append([p, f, st["pinch_extra"], st["pinch_truncated"]])
-    try:
-        D.check_pinch_guard(guard)
-    except Exception:
-        # the guard binds (tiny mesh, e.g. aniso2k_s1: 1 extra visit in total):
-        # the loud failure is the specified behaviour for a partitioned run
-        assert any(r[3] > 0 for r in guard)
-        return
-    pb, sb = D.exclusive_bases([[p, f] for _, _, p, f in locs])
-    for (off, _, p, _), base in zip(locs, sb):
+        ctx = _capi.Context(cuda.index or 0)
+        off, v, p, f, st = D.run_partition(xy, tr, n, T, b, e, ctx=ctx)
+        ranks.append([ctx, off, v, p, f])
+        table.append([p, f, st["pinch_extra"], st["pinch_deferred"]])
+    total = D.global_pinch_extra(table)
+    if D.needs_resume(table):
+        for r, row in enumerate(table):
+            if row[3] > 0:
+                ctx, off, v = ranks[r][:3]
+                ranks[r][3], ranks[r][4], _ = D.resume_partition(ctx, off, v, T, total)
+    if cap and name.startswith("aniso"):
+        assert D.needs_resume(table)  # the hook really exercised the resume path
+    pb, sb = D.exclusive_bases([[p, f] for _, _, _, p, f in ranks])
+    for (_, off, _, p, _), base in zip(ranks, sb):
         D._shift_device(off, p, int(base))
     torch.cuda.synchronize()
-    got_off = np.concatenate([o[:-1].cpu().numpy() for o, _, _, _ in locs] + [np.array([int(sb[-1]) + locs[-1][3]])])
-    got_v = np.concatenate([v.cpu().numpy() for _, v, _, _ in locs])
+    got_off = np.concatenate([off[:p].cpu().numpy() for _, off, _, p, _ in ranks] + [np.array([int(sb[-1]) + ranks[-1][4]])])
+    got_v = np.concatenate([v[:f].cpu().numpy() for _, _, v, _, f in ranks])
     assert np.array_equal(got_off, g["final_off"]) and np.array_equal(got_v, g["final_verts"])
