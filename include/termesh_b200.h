@@ -103,6 +103,10 @@ int tm_ctx_defects(const tm_ctx *ctx, int64_t *counts, int64_t *first); /* TM_NU
 /* per-phase device milliseconds of the last tm_mesh_to_polygons* call:
  * [0] label (K0+K1+K2), [1] traversal (K3), [2] reparation + stitch (K4) */
 int tm_ctx_phase_ms(const tm_ctx *ctx, double *ms3);
+/* device milliseconds of the last tm_label call: [0] pass A (twin insert +
+ * LabelMax, labeling.py:46-62), [1] pass B (twin lookup + LabelSeed and
+ * LabelFrontier fused, labeling.py:65-115) -- the reference's kernel_seconds */
+int tm_ctx_label_ms(const tm_ctx *ctx, double *ms2);
 
 /* Optional per-kernel device timing: CUDA events around each kernel group on
  * the launching stream.  tm_ctx_segment_ms flushes and returns the number of
@@ -190,6 +194,63 @@ int tm_mesh_to_polygons_host(tm_ctx *ctx, const double *h_vertices, int64_t n_ve
 int tm_mesh_to_polygons(tm_ctx *ctx, const double *d_xy, int64_t n_vertices, const void *d_tri, int tri_bits,
                         int64_t T, int check, int64_t *d_offsets, int32_t *d_verts, int64_t cap_polys,
                         int64_t cap_slots, int64_t *n_polys, int64_t *n_slots, int64_t *stats, void *stream);
+
+/* ---------------------------------------------------------------- around the path
+ * Validation, polygon analytics and the canonical output form on the device
+ * (paths relative to /root/reference/pkg/src/termesh). */
+
+/* mesh_core.validate's trivertex rule (mesh_core.py:268-283): d_trivertex
+ * int64[n]; TM_ERR_VALIDATION (kind TM_KIND_TRIVERTEX, first bad vertex) if an
+ * entry is outside [-1, T), -1 for a referenced vertex, or a triangle that
+ * does not contain the vertex. */
+int tm_check_trivertex(tm_ctx *ctx, const void *d_tri, int tri_bits, int64_t T, const int64_t *d_trivertex,
+                       int64_t n_vertices, void *stream);
+
+/* Polygon-mesh analytics of traversal.py over a device CSR (vertex ids in
+ * [0, n_vertices)): per-polygon tip flags (tip_flags, :112-124) and repeated-
+ * vertex flags (repeated_vertex_flags, :127-137) into the optional uint8[P]
+ * outputs, extra_vertex_visits (:140-147), the sorted distinct vertex ids
+ * (unique_vertices, :150-153; optional int32[n_vertices] output) and their
+ * count, and boundary_edge_count (:156-166).  n_vertices < 0: derived from
+ * the largest id.  Synchronizes `stream`. */
+int tm_polygon_stats(tm_ctx *ctx, const int64_t *d_offsets, const int32_t *d_verts, int64_t n_polys,
+                     int64_t n_vertices, uint8_t *d_tip, uint8_t *d_repeated, int32_t *d_unique,
+                     int64_t *extra_visits, int64_t *unique_vertices, int64_t *boundary_edges, void *stream);
+
+/* enclosed_signed_areas (traversal.py:94-109): shoelace area per polygon in
+ * numpy's summation order (np.add.reduceat, pairwise), d_area f64[P]. */
+int tm_polygon_areas(tm_ctx *ctx, const int64_t *d_offsets, const int32_t *d_verts, int64_t n_polys,
+                     const double *d_xy, double *d_area, void *stream);
+
+/* oracle.canonicalize (oracle.py:124-141): every polygon rotated to its
+ * lexicographically smallest rotation, polygons in Python tuple order.  Output
+ * CSR d_offsets_out int64[P+1], d_verts_out int32[offsets[P]].  Counting sort
+ * on the minimum vertex, then a lexicographic sort inside each bucket.
+ * n_vertices < 0: derived from the largest id.  Synchronizes `stream`. */
+int tm_canonicalize(tm_ctx *ctx, const int64_t *d_offsets, const int32_t *d_verts, int64_t n_polys,
+                    int64_t n_vertices, int64_t *d_offsets_out, int32_t *d_verts_out, void *stream);
+
+/* ---------------------------------------------------------------- host-side text I/O (no GPU)
+ * Python repr(float) of x into out (io_formats.py:44-46); returns the length, -1 if cap is too small */
+int tm_format_double(double x, char *out, size_t cap);
+/* Triangle file readers (io_formats.py:48-158): kind 0 .node (f64[2*rows]),
+ * 1 .ele / 2 .neigh (int64[3*rows], unnormalized), 3 .trivertex (int64[rows];
+ * n_expected = vertex count).  Same comment / whitespace / header rules and
+ * ParseError messages as the reference; tm_file_status returns 1 with
+ * (line, message) on a parse error. */
+typedef struct tm_file tm_file;
+tm_file *tm_file_read(const char *path, int kind, int64_t n_expected);
+int tm_file_status(const tm_file *f, int64_t *rows, int64_t *cols, int64_t *err_line, char *msg, size_t cap);
+int tm_file_copy(const tm_file *f, void *dst);
+void tm_file_close(tm_file *f);
+/* write_polymesh (io_formats.py:251-262) of an already canonical CSR: header,
+ * repr coordinates, polygon rows; byte-identical to the reference */
+int tm_write_polymesh(const char *path, const double *xy, int64_t n_vertices, const int64_t *offsets,
+                      const int32_t *verts, int64_t n_polys, char *err, size_t err_cap);
+/* one file of write_triangulation (io_formats.py:213-248): which 0 .node (xy),
+ * 1 .ele, 2 .neigh (rows3 int64[3*count]), 3 .trivertex (rows3 int64[count]) */
+int tm_write_triangle_file(const char *path, int which, const double *xy, const int64_t *rows3, int64_t count,
+                           char *err, size_t err_cap);
 
 #ifdef __cplusplus
 }

@@ -9,8 +9,9 @@ include/termesh_b200.h (libtermesh_b200.so, built in-tree by
 
 from .backend import GPU, SEQUENTIAL, Backend, parallel
 from .errors import CapacityError, ParseError, StructuralError, TermeshError, ValidationError
-from .io_formats import (array_hash, canonicalize, generate_anisotropic_delaunay, generate_clustered_delaunay,
-                         generate_random_delaunay, read_polymesh, triangulate_points, write_polymesh)
+from .io_formats import (TriangleFileSet, array_hash, canonicalize, generate_anisotropic_delaunay,
+                         generate_clustered_delaunay, generate_random_delaunay, read_polymesh, read_triangulation,
+                         triangulate_points, write_polymesh, write_triangulation)
 from .labeling import EdgeLabels, label_all, label_frontiers, label_max, label_seeds
 from .mesh_core import (BORDER, Triangulation, ValidationReport, compute_trivertex, edge_endpoints,
                         next_halfedge, prev_halfedge, signed_areas, squared_length, twin, validate)

@@ -5,6 +5,7 @@ this C ABI.  If the library is missing or no CUDA device is visible, every
 entry point raises -- there is no CPU fallback.
 """
 
+import atexit
 import ctypes
 import os
 import threading
@@ -32,6 +33,7 @@ _PI64 = ctypes.POINTER(ctypes.c_int64)
 _lib = None
 _lock = threading.RLock()
 _ctxs = {}
+_all_ctxs = []  # every Context ever created (destroyed at exit)
 
 
 class ExtensionMissing(TermeshError, ImportError):
@@ -56,6 +58,7 @@ def lib():
         L.tm_ctx_last_error.restype = ctypes.c_char_p
         L.tm_ctx_defects.argtypes = [_P, _PI64, _PI64]
         L.tm_ctx_phase_ms.argtypes = [_P, ctypes.POINTER(ctypes.c_double)]
+        L.tm_ctx_label_ms.argtypes = [_P, ctypes.POINTER(ctypes.c_double)]
         L.tm_ctx_set_profiling.argtypes = [_P, _I]
         L.tm_ctx_segment_ms.argtypes = [_P, ctypes.POINTER(ctypes.c_double), _PI64, _I, _I]
         L.tm_segment_name.argtypes = [_I]
@@ -77,12 +80,32 @@ def lib():
         L.tm_mesh_to_polygons_host.argtypes = [_P, _P, _I64, _P, _I64, _I, _P, _P, _I64, _I64, _PI64, _PI64,
                                                _PI64]
         L.tm_resume_pinch.argtypes = [_P, _I64, _P, _P, _I64, _I64, _PI64, _PI64, _PI64, _P]
-        for name in ("tm_ctx_create", "tm_ctx_defects", "tm_ctx_phase_ms", "tm_ctx_set_profiling", "tm_ctx_debug",
+        L.tm_check_trivertex.argtypes = [_P, _P, _I, _I64, _P, _I64, _P]
+        L.tm_polygon_stats.argtypes = [_P, _P, _P, _I64, _I64, _P, _P, _P, _PI64, _PI64, _PI64, _P]
+        L.tm_polygon_areas.argtypes = [_P, _P, _P, _I64, _P, _P, _P]
+        L.tm_canonicalize.argtypes = [_P, _P, _P, _I64, _I64, _P, _P, _P]
+        # host-side text I/O (tm_io.cu; no GPU needed)
+        L.tm_format_double.argtypes = [ctypes.c_double, ctypes.c_char_p, ctypes.c_size_t]
+        L.tm_format_double.restype = _I
+        L.tm_file_read.argtypes = [ctypes.c_char_p, _I, _I64]
+        L.tm_file_read.restype = _P
+        L.tm_file_status.argtypes = [_P, _PI64, _PI64, _PI64, ctypes.c_char_p, ctypes.c_size_t]
+        L.tm_file_status.restype = _I
+        L.tm_file_copy.argtypes = [_P, _P]
+        L.tm_file_copy.restype = _I
+        L.tm_file_close.argtypes = [_P]
+        L.tm_file_close.restype = None
+        L.tm_write_polymesh.argtypes = [ctypes.c_char_p, _P, _I64, _P, _P, _I64, ctypes.c_char_p, ctypes.c_size_t]
+        L.tm_write_polymesh.restype = _I
+        L.tm_write_triangle_file.argtypes = [ctypes.c_char_p, _I, _P, _P, _I64, ctypes.c_char_p, ctypes.c_size_t]
+        L.tm_write_triangle_file.restype = _I
+        for name in ("tm_ctx_create", "tm_ctx_defects", "tm_ctx_phase_ms", "tm_ctx_label_ms", "tm_ctx_set_profiling", "tm_ctx_debug",
                      "tm_ctx_debug_copy",
                      "tm_ctx_set_partition", "tm_shift_offsets", "tm_ctx_segment_ms", "tm_label", "tm_relabel",
                      "tm_check_neighbors",
                      "tm_unpack_halfedges", "tm_pack_frontier", "tm_traverse", "tm_repair",
-                     "tm_mesh_to_polygons", "tm_mesh_to_polygons_host", "tm_resume_pinch"):
+                     "tm_mesh_to_polygons", "tm_mesh_to_polygons_host", "tm_resume_pinch", "tm_check_trivertex",
+                     "tm_polygon_stats", "tm_polygon_areas", "tm_canonicalize"):
             getattr(L, name).restype = _I
         _lib = L
     return _lib
@@ -91,11 +114,14 @@ def lib():
 def exported_symbols():
     """Names declared in include/termesh_b200.h (checked by the CPU tests)."""
     return ("tm_version", "tm_ctx_create", "tm_ctx_destroy", "tm_ctx_last_error", "tm_ctx_defects",
-            "tm_ctx_phase_ms", "tm_ctx_set_profiling", "tm_ctx_segment_ms", "tm_segment_name", "tm_launch_count",
+            "tm_ctx_phase_ms", "tm_ctx_label_ms", "tm_ctx_set_profiling", "tm_ctx_segment_ms", "tm_segment_name", "tm_launch_count",
             "tm_ctx_debug", "tm_ctx_debug_copy", "tm_ctx_set_partition", "tm_shift_offsets",
             "tm_label", "tm_relabel", "tm_check_neighbors", "tm_unpack_halfedges",
             "tm_pack_frontier",
-            "tm_traverse", "tm_repair", "tm_mesh_to_polygons_host", "tm_mesh_to_polygons", "tm_resume_pinch")
+            "tm_traverse", "tm_repair", "tm_mesh_to_polygons_host", "tm_mesh_to_polygons", "tm_resume_pinch",
+            "tm_check_trivertex", "tm_polygon_stats", "tm_polygon_areas", "tm_canonicalize",
+            "tm_format_double", "tm_file_read", "tm_file_status", "tm_file_copy", "tm_file_close",
+            "tm_write_polymesh", "tm_write_triangle_file")
 
 
 def _require_cuda():
@@ -115,6 +141,13 @@ class Context:
         if rc != TM_OK:
             raise TermeshError(f"tm_ctx_create failed with status {rc}")
         self.ptr = p
+        _all_ctxs.append(self)
+
+    def close(self):
+        """Free this context's device scratch (also done for every context at exit)."""
+        if self.ptr:
+            lib().tm_ctx_destroy(self.ptr)
+            self.ptr = None
 
     def defects(self):
         counts = (ctypes.c_int64 * NUM_KINDS)()
@@ -125,6 +158,12 @@ class Context:
     def phase_ms(self):
         ms = (ctypes.c_double * 3)()
         lib().tm_ctx_phase_ms(self.ptr, ms)
+        return list(ms)
+
+    def label_ms(self):
+        """[pass A ms, pass B ms] of the last tm_label call (device time)."""
+        ms = (ctypes.c_double * 2)()
+        lib().tm_ctx_label_ms(self.ptr, ms)
         return list(ms)
 
     def set_profiling(self, on: bool):
@@ -167,6 +206,23 @@ class Context:
         if rc == TM_ERR_ARGUMENT:
             raise ValueError(msg)
         raise TermeshError(f"CUDA failure: {msg}")
+
+
+def _destroy_contexts():
+    """Free every context's device scratch at interpreter exit (clean
+    compute-sanitizer leak reports; the CUDA context is still alive here)."""
+    if _lib is None:
+        return
+    for c in _all_ctxs:
+        try:
+            c.close()
+        except Exception:
+            pass
+    _all_ctxs.clear()
+    _ctxs.clear()
+
+
+atexit.register(_destroy_contexts)
 
 
 def context(device=None) -> Context:

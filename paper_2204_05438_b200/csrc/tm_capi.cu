@@ -72,6 +72,11 @@ struct Counters {
   // guard cap (testing hook TERMESH_PINCH_GUARD_CAP, partitions only)
   unsigned long long stats[12];
   unsigned long long dbg[128];  // optional kernel timestamps / counters (tm_ctx_debug)
+  // tm_polygon_stats / tm_canonicalize: extra visits, boundary edges, long-polygon
+  // count, unique vertex count (int64), bucket count (int64)
+  unsigned long long post_extra, post_edges;
+  unsigned int post_nlong, post_pad;
+  int64_t post_unique, post_nb;
 };
 
 constexpr int kUploadChunks = 8;  // triangle upload chunks of tm_mesh_to_polygons_host
@@ -135,6 +140,9 @@ struct tm_ctx {
       undo, hugeq, longq, parked, pinchq;
   // whole-path buffers
   Buf xy, tri, tri32, hw, max_edge, seed, tv, off0, v0, fin_off, fin_v, hw_snap, hv;
+  // tm_post.cu scratch (validation, analytics, canonical form)
+  Buf pbits, pflag, ptable, pstamp, ptip, prep, plong, prot, pbucket, porder, phist, pstart, pcursor, plen, ptiles;
+  unsigned long long pstamp_clean = 0;  // allocation generation of the all-INT_MAX stamp buffer
   cudaStream_t gstream = nullptr;
   cudaStream_t aux = nullptr;                            // long repair items run beside the short ones
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_cls = nullptr;
@@ -163,6 +171,11 @@ struct tm_ctx {
   cudaStream_t cstream = nullptr;
   cudaEvent_t chunk_ev[kUploadChunks] = {};
   long long graph_kernels = 0;  // kernels per graph replay (counted at capture)
+  // tm_label: events around pass A (twin insert + LabelMax) and pass B (twin
+  // lookup + LabelSeed/LabelFrontier), read by tm_ctx_label_ms
+  bool label_timing = false;
+  cudaEvent_t lev[3] = {nullptr, nullptr, nullptr};
+  double label_ms[2] = {0, 0};
   // the last whole-path call, for tm_resume_pinch
   int64_t last_T = -1;
   bool last_host = false;
@@ -392,16 +405,20 @@ static int enqueue_label(tm_ctx* ctx, const double* d_xy, int64_t n, const void*
                          cudaStream_t s) {
   Counters* dc = dc_of(ctx);
   const int shrink = ctx->label_shrink && !check;  // check = 1 sends every key to the table
+  const bool lt = ctx->label_timing;  // phase API: device time of each pass (tm_ctx_label_ms)
+  if (lt) CK(cudaEventRecord(ctx->lev[0], s));
   if (!ctx->label_a_external) {
     SegTimer t_(ctx, S_LABEL_A, s);
     launch_label_a(d_xy, n, d_tri, tri_bits == 64, T, check, d_tri32, d_hw, d_me, d_seed, d_tv, ctx->slots.p,
                    &dc->st, s, shrink, &dc->table_ovf);
   }
+  if (lt) CK(cudaEventRecord(ctx->lev[1], s));
   {
     SegTimer t_(ctx, S_LABEL_B, s);
     launch_label_b(tri_bits == 32 && d_tri32 == nullptr ? (const int32_t*)d_tri : d_tri32, n, T, d_hw, d_me, d_seed,
                    d_tv, ctx->slots.p, check, &dc->st, s, shrink);
   }
+  if (lt) CK(cudaEventRecord(ctx->lev[2], s));
   CK(cudaGetLastError());
   return TM_OK;
 }
@@ -635,14 +652,16 @@ void tm_ctx_destroy(tm_ctx* ctx) {
                  &ctx->item_n, &ctx->item_slots, &ctx->item_state, &ctx->item_depth, &ctx->hugeq, &ctx->longq, &ctx->parked, &ctx->pinchq, &ctx->cnt, &ctx->slotsz, &ctx->pbase, &ctx->sbase, &ctx->pool,
                  &ctx->undo, &ctx->xy, &ctx->tri, &ctx->tri32, &ctx->hw, &ctx->max_edge, &ctx->seed, &ctx->tv,
                  &ctx->off0, &ctx->v0, &ctx->fin_off, &ctx->fin_v, &ctx->hw_snap, &ctx->hv,
-                 &ctx->lbscan};
+                 &ctx->lbscan, &ctx->pbits, &ctx->pflag, &ctx->ptable, &ctx->pstamp, &ctx->ptip, &ctx->prep,
+                 &ctx->plong, &ctx->prot, &ctx->pbucket, &ctx->porder, &ctx->phist, &ctx->pstart, &ctx->pcursor,
+                 &ctx->plen, &ctx->ptiles};
   for (Buf* b : bufs) b->release();
   if (ctx->h_reset) cudaFreeHost(ctx->h_reset);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
   if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
-  for (cudaEvent_t e : {ctx->ev_fork, ctx->ev_join, ctx->ev_cls})
+  for (cudaEvent_t e : {ctx->ev_fork, ctx->ev_join, ctx->ev_cls, ctx->lev[0], ctx->lev[1], ctx->lev[2]})
     if (e) cudaEventDestroy(e);
   prof_flush(ctx);
   for (auto e : ctx->prof.free_ev) cudaEventDestroy(e);
@@ -741,10 +760,26 @@ int tm_label(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_tri, int 
   cudaStream_t s = (cudaStream_t)stream;
   if ((rc = prepare(ctx, T, n)) || (rc = enqueue_reset(ctx, s))) return rc;
   ctx->label_shrink = 0;  // phase API: full-size twin table
-  if ((rc = enqueue_label(ctx, d_xy, n, d_tri, tri_bits, T, check, d_tri32, d_hw, d_max_edge, d_seed, d_tv, s)))
-    return rc;
+  for (auto& e : ctx->lev)
+    if (!e) CK(cudaEventCreate(&e));
+  ctx->label_timing = true;
+  rc = enqueue_label(ctx, d_xy, n, d_tri, tri_bits, T, check, d_tri32, d_hw, d_max_edge, d_seed, d_tv, s);
+  ctx->label_timing = false;
+  if (rc) return rc;
   Counters h;
-  return finish(ctx, s, &h);
+  rc = finish(ctx, s, &h);
+  for (int k = 0; k < 2; k++) {
+    float ms = 0;
+    ctx->label_ms[k] = cudaEventElapsedTime(&ms, ctx->lev[k], ctx->lev[k + 1]) == cudaSuccess ? ms : 0.0;
+  }
+  return rc;
+}
+
+int tm_ctx_label_ms(const tm_ctx* ctx, double* ms2) {
+  if (!ctx || !ms2) return TM_ERR_ARGUMENT;
+  ms2[0] = ctx->label_ms[0];
+  ms2[1] = ctx->label_ms[1];
+  return TM_OK;
 }
 
 int tm_relabel(tm_ctx* ctx, int32_t* d_hw, const int8_t* d_max_edge, int64_t T, uint8_t* d_seed, void* stream) {
@@ -1115,6 +1150,135 @@ int tm_mesh_to_polygons_host(tm_ctx* ctx, const double* h_xy, int64_t n, const i
   CK(cudaMemcpyAsync(h_v, ctx->fin_v.p, *n_slots * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return TM_OK;
+}
+
+// n_vertices < 0: the largest vertex id of the CSR + 1 (one extra round trip)
+static int resolve_vertex_count(tm_ctx* ctx, const int64_t* d_off, const int32_t* d_v, int64_t P, int64_t* n,
+                                cudaStream_t s) {
+  if (*n >= 0) return TM_OK;
+  *n = 0;
+  if (P <= 0) return TM_OK;
+  CK(cudaMemcpyAsync(ctx->h_pin, d_off + P, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int64_t F = *ctx->h_pin;
+  int* dmax = reinterpret_cast<int*>(&dc_of(ctx)->post_pad);
+  launch_max_vertex(d_v, F, dmax, s);
+  CK(cudaMemcpyAsync(ctx->h_pin, dmax, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *n = (int64_t)(*reinterpret_cast<int*>(ctx->h_pin)) + 1;
+  return TM_OK;
+}
+
+// ---------------------------------------------------------------- validation / analytics / canonical form
+// (tm_post.cu).  Each call enqueues on `stream`, reads the counters back and
+// decodes the status like the phase functions.
+
+int tm_check_trivertex(tm_ctx* ctx, const void* d_tri, int tri_bits, int64_t T, const int64_t* d_trivertex,
+                       int64_t n, void* stream) {
+  if (!ctx || (tri_bits != 32 && tri_bits != 64) || T < 0 || n < 0) return TM_ERR_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = init_counters(ctx);
+  if (rc || (rc = enqueue_reset(ctx, s))) return rc;
+  ENSURE(pbits, ((n + 31) / 32 + 1) * sizeof(uint32_t));
+  launch_check_trivertex(d_tri, tri_bits == 64, T, d_trivertex, n, ctx->pbits.as<uint32_t>(), &dc_of(ctx)->st, s);
+  CK(cudaGetLastError());
+  Counters h;
+  return finish(ctx, s, &h);
+}
+
+int tm_polygon_stats(tm_ctx* ctx, const int64_t* d_off, const int32_t* d_v, int64_t P, int64_t n_vertices,
+                     uint8_t* d_tip, uint8_t* d_repeated, int32_t* d_unique, int64_t* extra_visits,
+                     int64_t* unique_vertices, int64_t* boundary_edges, void* stream) {
+  if (!ctx || P < 0) return TM_ERR_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = init_counters(ctx);
+  if (rc || (rc = resolve_vertex_count(ctx, d_off, d_v, P, &n_vertices, s)) || (rc = enqueue_reset(ctx, s))) return rc;
+  Counters* dc = dc_of(ctx);
+  const int64_t Pn = P > 0 ? P : 1, nn = n_vertices > 0 ? n_vertices : 1;
+  int64_t F = 0;
+  if (P > 0) {
+    CK(cudaMemcpyAsync(ctx->h_pin, d_off + P, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    F = *ctx->h_pin;
+  }
+  ENSURE(ptip, Pn);
+  ENSURE(prep, Pn);
+  ENSURE(plong, Pn * sizeof(int32_t));
+  ENSURE(pstamp, nn * sizeof(int32_t));
+  if (ctx->pstamp_clean != ctx->pstamp.gen) {  // INT_MAX once per allocation; k_poly_flags_long restores it
+    CK(cudaMemsetAsync(ctx->pstamp.p, 0x7F, ctx->pstamp.bytes, s));
+    ctx->pstamp_clean = ctx->pstamp.gen;
+  }
+  ENSURE(pflag, nn);
+  ENSURE(ptiles, (scan_scratch_elems(nn) + 8) * sizeof(int64_t));
+  int64_t slots = 64;
+  while (slots < 2 * F + 64) slots <<= 1;
+  ENSURE(ptable, slots * sizeof(unsigned long long));
+  uint8_t* tip = d_tip ? d_tip : ctx->ptip.as<uint8_t>();
+  uint8_t* rep = d_repeated ? d_repeated : ctx->prep.as<uint8_t>();
+  launch_poly_flags(d_off, P, d_v, tip, rep, &dc->post_extra, ctx->plong.as<int32_t>(), &dc->post_nlong,
+                    ctx->pstamp.as<int32_t>(), s);
+  launch_edge_set(d_off, P, d_v, ctx->ptable.as<unsigned long long>(), slots, &dc->post_edges, s);
+  launch_mark_vertices(d_v, F, n_vertices, ctx->pflag.as<uint8_t>(), &dc->st, s);
+  if (d_unique)
+    launch_select_flags(ctx->pflag.as<uint8_t>(), n_vertices, d_unique, &dc->post_unique, ctx->ptiles.as<int64_t>(),
+                        s, 0);
+  else {
+    ENSURE(porder, nn * sizeof(int32_t));
+    launch_select_flags(ctx->pflag.as<uint8_t>(), n_vertices, ctx->porder.as<int32_t>(), &dc->post_unique,
+                        ctx->ptiles.as<int64_t>(), s, 0);
+  }
+  CK(cudaGetLastError());
+  Counters h;
+  if ((rc = finish(ctx, s, &h))) return rc;
+  if (extra_visits) *extra_visits = (int64_t)h.post_extra;
+  if (unique_vertices) *unique_vertices = n_vertices > 0 ? h.post_unique : 0;
+  if (boundary_edges) *boundary_edges = (int64_t)h.post_edges;
+  return TM_OK;
+}
+
+int tm_polygon_areas(tm_ctx* ctx, const int64_t* d_off, const int32_t* d_v, int64_t P, const double* d_xy,
+                     double* d_area, void* stream) {
+  if (!ctx || P < 0) return TM_ERR_ARGUMENT;
+  launch_poly_areas(d_off, P, d_v, d_xy, d_area, (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  return TM_OK;
+}
+
+int tm_canonicalize(tm_ctx* ctx, const int64_t* d_off, const int32_t* d_v, int64_t P, int64_t n_vertices,
+                    int64_t* d_off_out, int32_t* d_v_out, void* stream) {
+  if (!ctx || P < 0) return TM_ERR_ARGUMENT;
+  if (n_vertices >= (int64_t)0x7FFFFFFF) return set_err(ctx, TM_ERR_ARGUMENT, "vertex ids must fit in 31 bits");
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = init_counters(ctx);
+  if (rc || (rc = resolve_vertex_count(ctx, d_off, d_v, P, &n_vertices, s)) || (rc = enqueue_reset(ctx, s))) return rc;
+  Counters* dc = dc_of(ctx);
+  const int64_t Pn = P > 0 ? P : 1, nb = n_vertices + 1;  // buckets: empty polygons, then one per minimum vertex
+  ENSURE(prot, Pn * sizeof(int32_t));
+  ENSURE(pbucket, Pn * sizeof(int32_t));
+  ENSURE(porder, (Pn > nb ? Pn : nb) * sizeof(int32_t));
+  ENSURE(phist, (nb + 2) * sizeof(int64_t));
+  ENSURE(pstart, (nb + 2) * sizeof(int64_t));
+  ENSURE(pcursor, (nb + 2) * sizeof(int64_t));
+  ENSURE(plen, (Pn + 1) * sizeof(int64_t));
+  ENSURE(lbscan, scan_lookback_bytes(Pn > nb ? Pn : nb));
+  int64_t* hp = ctx->h_pin;
+  hp[0] = nb;
+  hp[1] = P;
+  CK(cudaMemcpyAsync(&dc->post_nb, hp, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(&dc->p_in, hp + 1, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  unsigned long long* hist = ctx->phist.as<unsigned long long>();
+  launch_canon_rot(d_off, P, d_v, n_vertices, ctx->prot.as<int32_t>(), ctx->pbucket.as<int32_t>(), hist, &dc->st, s);
+  launch_scan_lookback(reinterpret_cast<const int64_t*>(hist), nullptr, ctx->pstart.as<int64_t>(), nullptr,
+                       &dc->post_nb, nb, ctx->lbscan.p, s);
+  launch_canon_sort(P, n_vertices, d_off, d_v, ctx->prot.as<int32_t>(), ctx->pbucket.as<int32_t>(),
+                    ctx->pstart.as<int64_t>(), ctx->pcursor.as<unsigned long long>(), ctx->porder.as<int32_t>(), s);
+  launch_canon_lengths(ctx->porder.as<int32_t>(), P, d_off, ctx->plen.as<int64_t>(), s);
+  launch_scan_lookback(ctx->plen.as<int64_t>(), nullptr, d_off_out, nullptr, &dc->p_in, Pn, ctx->lbscan.p, s);
+  launch_canon_write(ctx->porder.as<int32_t>(), P, d_off, d_v, ctx->prot.as<int32_t>(), d_off_out, d_v_out, s);
+  CK(cudaGetLastError());
+  Counters h;
+  return finish(ctx, s, &h);
 }
 
 }  // extern "C"

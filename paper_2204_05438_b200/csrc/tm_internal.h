@@ -137,4 +137,25 @@ void launch_finalize(const int64_t* Pp, const int64_t* pbase, const int64_t* sba
 void launch_undo(int32_t* hw, const int32_t* undo, const unsigned long long* undo_top, unsigned long long cap,
                  cudaStream_t s);
 
+// tm_post.cu (validation, polygon analytics, canonical form)
+void launch_check_trivertex(const void* tri, int tri_is64, int64_t T, const int64_t* tv, int64_t n, uint32_t* bits,
+                            DevStatus* st, cudaStream_t s);
+void launch_max_vertex(const int32_t* v, int64_t F, int* out, cudaStream_t s);
+void launch_mark_vertices(const int32_t* v, int64_t F, int64_t n, uint8_t* flag, DevStatus* st, cudaStream_t s);
+void launch_edge_set(const int64_t* off, int64_t P, const int32_t* v, unsigned long long* table, int64_t table_slots,
+                     unsigned long long* count, cudaStream_t s);
+void launch_poly_flags(const int64_t* off, int64_t P, const int32_t* v, uint8_t* tip, uint8_t* rep,
+                       unsigned long long* extra, int32_t* long_list, unsigned int* n_long, int32_t* stamp,
+                       cudaStream_t s);
+void launch_poly_areas(const int64_t* off, int64_t P, const int32_t* v, const double* xy, double* area,
+                       cudaStream_t s);
+void launch_canon_rot(const int64_t* off, int64_t P, const int32_t* v, int64_t n, int32_t* rot, int32_t* bucket,
+                      unsigned long long* hist, DevStatus* st, cudaStream_t s);
+void launch_canon_sort(int64_t P, int64_t n, const int64_t* off, const int32_t* v, const int32_t* rot,
+                       const int32_t* bucket, const int64_t* start, unsigned long long* cursor, int32_t* order,
+                       cudaStream_t s);
+void launch_canon_lengths(const int32_t* order, int64_t P, const int64_t* off, int64_t* len, cudaStream_t s);
+void launch_canon_write(const int32_t* order, int64_t P, const int64_t* off, const int32_t* v, const int32_t* rot,
+                        const int64_t* off_out, int32_t* v_out, cudaStream_t s);
+
 }  // namespace tmb

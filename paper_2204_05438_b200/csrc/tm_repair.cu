@@ -1136,7 +1136,13 @@ __device__ void warp_finish_pinch(const RepairCtx& c, int64_t w, int32_t poly, l
     if (elig == 0) break;
     if (r >= guard) {
       if (park.list) {  // whether the global guard allows round r is not known yet
+        // a consistent (provisional) output size for the stitch that may run
+        // before the item is finished (seed partition, tm_resume_pinch follows)
+        long long ps = 0;
+        for (int k = lane; k < n; k += 32) ps += (uint32_t)c.pool[list + 2 * k + 1] & LEN_MASK;
+        for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(kFull, ps, o);
         if (lane == 0) {
+          item_slots[w] = ps;
           item_list[w] = list;
           item_n[w] = n;
           park.item_depth[w] = (int32_t)r;
@@ -1770,7 +1776,9 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
   int* tipdeg = reinterpret_cast<int*>(nexttip + kSegMaxL);  // cached fan sizes (-1: none)
   int* tlist = tipdeg + kSegTips;                              // tipped records of the round
   Seg* segs = reinterpret_cast<Seg*>(tlist + kSegRec);
-  __shared__ int s_ntip, s_ntouch, s_stop, s_fail, s_ntips, s_need, s_tot;
+  // s_ntb: tipped-record count of the next round, double-buffered by round parity
+  // so the reset of one round never races with the previous round's readers
+  __shared__ int s_ntip, s_ntouch, s_stop, s_fail, s_ntb[2], s_need, s_tot;
   __shared__ PairMsg pmsg[kSegWarps / 2];
   __shared__ long long s_base;
   __shared__ unsigned int s_w;
@@ -1895,10 +1903,10 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
     if (wib == 0) {
       SPiece X0{0, 1, L, -1, -1};
       X0.ftip = s_ntip > 0 ? seg_first_tip(g, X0, lane, &X0.fk) : -1;
-      if (lane == 0) { recs[0] = X0; s_ntips = X0.ftip >= 0 ? 1 : 0; }
+      if (lane == 0) { recs[0] = X0; s_ntb[0] = X0.ftip >= 0 ? 1 : 0; }
     }
     __syncthreads();
-    int cur = 0, n = 1, ntips = s_ntips, hbase = 0;
+    int cur = 0, n = 1, ntips = s_ntb[0], hbase = 0;
     long long depth = 0, splits = 0;
     bool bad = false, spill = false;
     while (ntips > 0) {
@@ -1930,7 +1938,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
         }
         if (lane == 0) s_need = need;
       }
-      if (threadIdx.x == 0) s_ntips = 0;
+      if (threadIdx.x == 0) s_ntb[cur ^ 1] = 0;
       __syncthreads();
       // Segments are bump-allocated in one half of the arena; when a round
       // would overflow it, the live pieces are first compacted into the other
@@ -2041,7 +2049,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
             const int o = s_out[r];
             out[o] = A;
             out[o + 1] = B;
-            atomicAdd(&s_ntips, (A.ftip >= 0 ? 1 : 0) + (B.ftip >= 0 ? 1 : 0));
+            atomicAdd(&s_ntb[cur ^ 1], (A.ftip >= 0 ? 1 : 0) + (B.ftip >= 0 ? 1 : 0));
           }
           if (qi == trace_qi && lane == 0) {
             atomicAdd(dbg + 56, (unsigned long long)(ck1 - ck0));
@@ -2057,7 +2065,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
           const SPiece C = seg_emit_child(g, X, pos, pl, hf, lane);
           if (lane == 0) {
             out[s_out[r] + hf] = C;
-            if (C.ftip >= 0) atomicAdd(&s_ntips, 1);
+            if (C.ftip >= 0) atomicAdd(&s_ntb[cur ^ 1], 1);
             if (hf == 0 && qi == trace_qi) atomicAdd(dbg + 58, (unsigned long long)(clock64() - ck2));
           }
         }
@@ -2066,7 +2074,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
       __syncthreads();
       splits += ntips;
       n += ntips;
-      ntips = s_ntips;
+      ntips = s_ntb[cur ^ 1];
       cur ^= 1;
       if (trace && depth < 48) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ns)); dbg[4 + depth] = t_ns; }
       if (s_fail) {

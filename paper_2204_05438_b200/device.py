@@ -99,25 +99,18 @@ class DeviceMesh:
 
     def check_trivertex(self, trivertex):
         """mesh_core.validate's trivertex rule (mesh_core.py:268-283): each entry
-        is -1 for an unreferenced vertex or a triangle containing the vertex."""
-        torch = _torch()
+        is -1 for an unreferenced vertex or a triangle containing the vertex
+        (tm_check_trivertex)."""
         tv = to_device(np.asarray(trivertex, dtype=np.int64))
-        T, n = self.T, self.n
-        t3 = self.tri_in.view(-1, 3).to(torch.int64)
-        referenced = torch.zeros(n, dtype=torch.bool, device=tv.device)
-        if T:
-            referenced[t3.reshape(-1)] = True
-        bad = (tv < -1) | (tv >= T) | ((tv == -1) & referenced)
-        ok_idx = (tv >= 0) & ~bad
-        safe = torch.where(ok_idx, tv, torch.zeros_like(tv))
-        vid = torch.arange(n, device=tv.device)
-        contains = (t3[safe] == vid[:, None]).any(dim=1) if T else torch.zeros(n, dtype=torch.bool, device=tv.device)
-        bad |= ok_idx & ~contains
-        nbad = int(bad.sum())
-        if nbad:
-            first = int(torch.nonzero(bad)[0, 0])
-            rep = ValidationReport(False, [("trivertex", first, f"{nbad} defect(s), first at element {first}")])
-            raise ValidationError("refusing to run on an invalid triangulation: " + rep.summary(), rep)
+        bits = 64 if self.tri_in.dtype == _torch().int64 else 32
+        ctx = _capi.context(self.xy.device)
+        rc = _capi.lib().tm_check_trivertex(ctx.ptr, _capi.ptr(self.tri_in), bits, self.T, _capi.ptr(tv), self.n,
+                                            _capi.stream_ptr(self.xy.device))
+        try:
+            ctx.check(rc, "validate")
+        except ValidationError as e:
+            rep = e.report if e.report is not None else ValidationReport(False, [])
+            raise ValidationError("refusing to run on an invalid triangulation: " + rep.summary(), rep) from None
 
     # ------------------------------------------------------------ host views
     def trivertex_host(self) -> np.ndarray:

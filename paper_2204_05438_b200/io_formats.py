@@ -7,8 +7,10 @@ form (oracle.py:124-141) and the byte-stable polymesh writer
 (io_formats.py:251-262).
 """
 
+import ctypes
 import hashlib
 import os
+from dataclasses import dataclass
 from pathlib import Path
 
 import numpy as np
@@ -113,54 +115,165 @@ def array_hash(a) -> str:
 
 
 # ---------------------------------------------------------------- canonical form
-def _min_rotation(p):
-    p = list(p)
-    m = min(p)
-    best = None
-    for i, x in enumerate(p):
-        if x == m:
-            r = p[i:] + p[:i]
-            if best is None or r < best:
-                best = r
-    return tuple(best)
-
-
-def canonicalize(pm: PolygonMesh) -> PolygonMesh:
+def canonicalize(pm: PolygonMesh, n_vertices: int = -1) -> PolygonMesh:
     """Each polygon rotated to its lexicographically smallest rotation,
-    polygons sorted in tuple order (oracle.py:124-141)."""
-    off, v = pm.csr()
-    lens = np.diff(off)
-    polys = []
-    for i in range(pm.count):
-        s = v[off[i]:off[i + 1]]
-        if lens[i] == 0:
-            polys.append(())
-            continue
-        k = int(np.argmin(s))
-        if np.count_nonzero(s == s[k]) == 1:
-            polys.append(tuple(np.concatenate((s[k:], s[:k])).tolist()))
-        else:
-            polys.append(_min_rotation(s.tolist()))
-    polys.sort()
-    return PolygonMesh.from_polygons(polys)
+    polygons sorted in tuple order (oracle.py:124-141) -- tm_canonicalize on
+    the device (counting sort on the minimum vertex, lexicographic order inside
+    each bucket).  The result is a device-backed PolygonMesh."""
+    import torch
+    from . import _capi
+    off, v = pm.device_csr()
+    P = pm.count
+    dev = off.device
+    off_out = torch.empty(P + 1, dtype=torch.int64, device=dev)
+    v_out = torch.empty(max(int(v.numel()), 1), dtype=torch.int32, device=dev)
+    ctx = _capi.context(dev)
+    rc = _capi.lib().tm_canonicalize(ctx.ptr, _capi.ptr(off), _capi.ptr(v), P, n_vertices, _capi.ptr(off_out),
+                                     _capi.ptr(v_out), _capi.stream_ptr(dev))
+    ctx.check(rc)
+    return PolygonMesh(count=P, offsets=off_out, verts=v_out[: int(v.numel())])
 
 
 def _fmt(x: float) -> str:
+    """repr of a Python float (io_formats.py:44-46); the native writers use
+    tm_format_double, which prints the same bytes."""
     return repr(float(x))
+
+
+def format_double(x: float) -> str:
+    """The native writers' float formatting (tm_format_double): Python repr."""
+    from . import _capi
+    buf = ctypes.create_string_buffer(64)
+    n = _capi.lib().tm_format_double(float(x), buf, 64)
+    if n < 0:
+        raise ValueError("format buffer too small")
+    return buf.value.decode()
 
 
 def write_polymesh(mesh: PolygonMesh, vertices, path) -> None:
     """Canonical text form (io_formats.py:251-262): `<#v> <#polys>`, one
-    `x y` line per vertex (repr floats), one `<len> v0 v1 ...` per polygon."""
-    verts = np.asarray(vertices, dtype=np.float64).ravel()
-    cm = canonicalize(mesh)
+    `x y` line per vertex (repr floats), one `<len> v0 v1 ...` per polygon.
+    Canonical order on the device (tm_canonicalize), text by the native
+    multi-threaded writer (tm_write_polymesh) -- byte-identical output."""
+    from . import _capi
+    verts = np.ascontiguousarray(np.asarray(vertices, dtype=np.float64).ravel())
     n = verts.size // 2
-    with open(path, "w") as f:
-        f.write(f"{n} {cm.count}\n")
-        for i in range(n):
-            f.write(f"{_fmt(verts[2 * i])} {_fmt(verts[2 * i + 1])}\n")
-        for p in cm.polygons():
-            f.write(f"{p.size} " + " ".join(str(int(x)) for x in p) + "\n")
+    cm = canonicalize(mesh, n_vertices=n if n else -1)
+    d_off, d_v = cm.device_csr()
+    off = np.ascontiguousarray(d_off.cpu().numpy(), dtype=np.int64)
+    v = np.ascontiguousarray(d_v.cpu().numpy(), dtype=np.int32)
+    err = ctypes.create_string_buffer(512)
+    rc = _capi.lib().tm_write_polymesh(str(path).encode(), verts.ctypes.data_as(ctypes.c_void_p), n,
+                                       off.ctypes.data_as(ctypes.c_void_p), v.ctypes.data_as(ctypes.c_void_p),
+                                       cm.count, err, 512)
+    if rc != 0:
+        raise OSError(err.value.decode())
+
+
+# ---------------------------------------------------------------- Triangle file sets
+@dataclass
+class TriangleFileSet:
+    """Paths of one triangulation: .node, .ele, .neigh, optional .trivertex
+    (io_formats.py:33-41)."""
+
+    node: Path
+    ele: Path
+    neigh: Path
+    trivertex: Path | None = None
+
+
+_KIND = {"node": 0, "ele": 1, "neigh": 2, "trivertex": 3}
+
+
+def _read_native(path, kind: str, n_expected: int = 0) -> np.ndarray:
+    """tm_file_read: the reference's _data_lines + row readers (io_formats.py:48-158)
+    in native code; parse failures raise ParseError(path, line, message) with
+    the reference's messages."""
+    from . import _capi
+    L = _capi.lib()
+    h = L.tm_file_read(str(path).encode(), _KIND[kind], int(n_expected))
+    try:
+        rows, cols, line = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        msg = ctypes.create_string_buffer(1024)
+        if L.tm_file_status(h, ctypes.byref(rows), ctypes.byref(cols), ctypes.byref(line), msg, 1024):
+            raise ParseError(path, int(line.value), msg.value.decode())
+        out = np.empty(rows.value * cols.value, dtype=np.float64 if kind == "node" else np.int64)
+        L.tm_file_copy(h, out.ctypes.data_as(ctypes.c_void_p))
+    finally:
+        L.tm_file_close(h)
+    return out
+
+
+def read_triangulation(files: TriangleFileSet) -> Triangulation:
+    """Read and normalize a Triangle file set (io_formats.py:161-210): one-based
+    sets shifted to zero-based (border -1 kept), range checks, clockwise
+    triangles reoriented (vertex and neighbor slots 1, 2 swapped), trivertex
+    computed (device) when no file gives it, and the result validated (device)."""
+    from .errors import ValidationError
+    from .mesh_core import compute_trivertex, signed_areas, validate
+    coords = _read_native(files.node, "node")
+    n = coords.size // 2
+    tris = _read_native(files.ele, "ele").reshape(-1, 3)
+    neigh = _read_native(files.neigh, "neigh").reshape(-1, 3)
+    if neigh.shape[0] != tris.shape[0]:
+        raise ParseError(files.neigh, 0, f"{neigh.shape[0]} neighbor rows for {tris.shape[0]} triangles")
+    one_based = bool((tris == n).any())  # one-based sets reference vertex n
+    if one_based:
+        tris = tris - 1
+        neigh = np.where(neigh >= 0, neigh - 1, neigh)
+    if tris.size and ((tris < 0) | (tris >= n)).any():
+        bad = int(np.argwhere((tris < 0) | (tris >= n))[0][0])
+        raise ParseError(files.ele, 0, f"triangle row {bad} references a vertex outside [0, {n})")
+    T = tris.shape[0]
+    if neigh.size and ((neigh < -1) | (neigh >= T)).any():
+        bad = int(np.argwhere((neigh < -1) | (neigh >= T))[0][0])
+        raise ParseError(files.neigh, 0, f"neighbor row {bad} references a triangle outside [0, {T})")
+    trivertex = None
+    if files.trivertex is not None:
+        trivertex = _read_native(files.trivertex, "trivertex", n)
+        if one_based:
+            trivertex = np.where(trivertex >= 0, trivertex - 1, trivertex)
+    tri = Triangulation(coords, tris.ravel(), neigh.ravel(), trivertex)
+    cw = signed_areas(tri) < 0
+    if cw.any():
+        t3 = tri.triangles.reshape(-1, 3)
+        n3 = tri.neighbors.reshape(-1, 3)
+        t3[cw] = t3[cw][:, [0, 2, 1]]
+        n3[cw] = n3[cw][:, [0, 2, 1]]
+    if tri.trivertex is None:
+        tri.trivertex = compute_trivertex(tri)
+    report = validate(tri)
+    if not report.ok:
+        raise ValidationError(f"{files.node}: triangulation is invalid: {report.summary()}", report)
+    return tri
+
+
+def write_triangulation(tri: Triangulation, basepath) -> TriangleFileSet:
+    """.node/.ele/.neigh (+ .trivertex) next to basepath, zero-based, repr
+    coordinates (io_formats.py:213-248), written by tm_write_triangle_file."""
+    from . import _capi
+    base = Path(basepath)
+    paths = [base.with_suffix(x) for x in (".node", ".ele", ".neigh")]
+    err = ctypes.create_string_buffer(512)
+    xy = np.ascontiguousarray(tri.vertices, dtype=np.float64).ravel()
+    t3 = np.ascontiguousarray(tri.triangles, dtype=np.int64).ravel()
+    n3 = np.ascontiguousarray(tri.neighbors, dtype=np.int64).ravel()
+    jobs = [(paths[0], 0, xy, None, tri.n_vertices), (paths[1], 1, None, t3, tri.n_triangles),
+            (paths[2], 2, None, n3, tri.n_triangles)]
+    tv_path = None
+    if tri.trivertex is not None:
+        tv_path = base.with_suffix(".trivertex")
+        jobs.append((tv_path, 3, None, np.ascontiguousarray(tri.trivertex, dtype=np.int64), tri.n_vertices))
+    for path, which, a, b, count in jobs:
+        rc = _capi.lib().tm_write_triangle_file(str(path).encode(), which, _ptr_np(a), _ptr_np(b), int(count), err,
+                                                512)
+        if rc != 0:
+            raise OSError(err.value.decode())
+    return TriangleFileSet(paths[0], paths[1], paths[2], tv_path)
+
+
+def _ptr_np(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
 
 
 def read_polymesh(path):

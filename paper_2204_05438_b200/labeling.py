@@ -6,7 +6,6 @@ result stays on the device; the reference's numpy arrays (max_edge int8[T],
 frontier bool[3T], seed bool[T]) are materialised on first access.
 """
 
-import time
 
 import numpy as np
 
@@ -86,9 +85,9 @@ def label_all(tri: Triangulation, backend: Backend = SEQUENTIAL, kernel_seconds:
 
     With check=True the triangulation is validated on the device first and a
     failing report raises ValidationError.  kernel_seconds receives the device
-    time of the fused passes: "label_max" (twin build + LabelMax), and
-    "label_seed" / "label_frontier" (one fused pass, reported once under
-    label_seed; label_frontier is 0.0).
+    time of the fused passes (CUDA events, no upload): "label_max" = pass A
+    (twin inserts + LabelMax); "label_seed" / "label_frontier" = half each of
+    pass B (twin lookups + seeds and frontier in one pass).
     """
     import torch
     if check:
@@ -98,15 +97,17 @@ def label_all(tri: Triangulation, backend: Backend = SEQUENTIAL, kernel_seconds:
             raise ValidationError("refusing to label an invalid triangulation: " + str(e), e.report) from None
         if tri.trivertex is not None:
             DeviceMesh.upload(tri, check=False).check_trivertex(tri.trivertex)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
     dm = DeviceMesh.upload(tri, check=False)
     torch.cuda.synchronize()
-    t1 = time.perf_counter()
     if kernel_seconds is not None:
-        kernel_seconds["label_max"] = t1 - t0
-        kernel_seconds["label_seed"] = 0.0
-        kernel_seconds["label_frontier"] = 0.0
+        # device time of the two fused passes (tm_ctx_label_ms): pass A is
+        # LabelMax (+ the twin inserts); pass B computes seeds and frontier
+        # together, its time is split evenly between the reference's
+        # label_seed and label_frontier kernels (labeling.py:134-144)
+        a_ms, b_ms = _capi.context(dm.xy.device).label_ms()
+        kernel_seconds["label_max"] = a_ms / 1e3
+        kernel_seconds["label_seed"] = b_ms / 2e3
+        kernel_seconds["label_frontier"] = b_ms / 2e3
     return EdgeLabels(device=dm)
 
 

@@ -9,8 +9,8 @@ byte for byte.
 
 The polygon analytics (tip_flags, repeated_vertex_flags, extra_vertex_visits,
 unique_vertices, boundary_edge_count, enclosed_signed_areas) are untimed
-statistics in the reference (pipeline.py:150-171) and are provided here as
-numpy restatements over the host CSR.
+statistics in the reference (pipeline.py:150-171); here they are device
+kernels (tm_polygon_stats / tm_polygon_areas) over the device CSR.
 """
 
 import ctypes
@@ -122,76 +122,80 @@ class PolygonMesh:
 
 
 # ---------------------------------------------------------------- analytics
-def _flat(pm: PolygonMesh):
-    off, v = pm.csr()
-    lens = np.diff(off)
-    pid = np.repeat(np.arange(pm.count, dtype=np.int64), lens)
-    intra = np.arange(v.size, dtype=np.int64) - off[:-1][pid] if v.size else np.empty(0, np.int64)
-    return v, pid, intra, lens, off[:-1]
+# The reference's polygon analytics (traversal.py:94-166), computed by the
+# tm_polygon_stats / tm_polygon_areas kernels over the device CSR.
+def _stats(pm: PolygonMesh, want_flags: bool = False, want_unique: bool = False, n_vertices: int = -1):
+    import torch
+    off, v = pm.device_csr()
+    P = pm.count
+    dev = off.device
+    tip = rep = uniq = None
+    if want_flags:
+        tip = torch.empty(max(P, 1), dtype=torch.uint8, device=dev)
+        rep = torch.empty(max(P, 1), dtype=torch.uint8, device=dev)
+    if want_unique:  # distinct ids <= slots
+        uniq = torch.empty(max(int(v.numel()), 1), dtype=torch.int32, device=dev)
+    extra, count, edges = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    ctx = _capi.context(dev)
+    rc = _capi.lib().tm_polygon_stats(ctx.ptr, _capi.ptr(off), _capi.ptr(v), P, n_vertices, _capi.ptr(tip),
+                                      _capi.ptr(rep), _capi.ptr(uniq), ctypes.byref(extra), ctypes.byref(count),
+                                      ctypes.byref(edges), _capi.stream_ptr(dev))
+    ctx.check(rc)
+    return {"tip": tip, "rep": rep, "extra": extra.value, "n_unique": count.value, "unique": uniq,
+            "edges": edges.value}
 
 
 def tip_flags(pm: PolygonMesh) -> np.ndarray:
-    """Per polygon: any cyclic triple (a, b, a)."""
-    v, pid, intra, lens, starts = _flat(pm)
-    flags = np.zeros(pm.count, dtype=bool)
-    if v.size:
-        L = lens[pid]
-        prv = starts[pid] + np.where(intra == 0, L - 1, intra - 1)
-        nxt = starts[pid] + np.where(intra == L - 1, 0, intra + 1)
-        flags[pid[v[prv] == v[nxt]]] = True
-    return flags
-
-
-def _dup_mask(v, pid):
-    """Duplicate marks (all but the first occurrence of each (polygon, vertex))."""
-    order = np.lexsort((v, pid))
-    sp, sv = pid[order], v[order]
-    dup = np.zeros(v.size, dtype=bool)
-    dup[1:] = (sp[1:] == sp[:-1]) & (sv[1:] == sv[:-1])
-    return dup, sp
+    """Per polygon: any cyclic triple (a, b, a) (traversal.py:112-124)."""
+    if pm.count == 0:
+        return np.zeros(0, dtype=bool)
+    return _stats(pm, want_flags=True)["tip"][: pm.count].cpu().numpy().astype(bool)
 
 
 def repeated_vertex_flags(pm: PolygonMesh) -> np.ndarray:
-    v, pid, _, _, _ = _flat(pm)
-    flags = np.zeros(pm.count, dtype=bool)
-    if v.size:
-        dup, sp = _dup_mask(v, pid)
-        flags[sp[dup]] = True
-    return flags
+    """Per polygon: any vertex more than once (traversal.py:127-137)."""
+    if pm.count == 0:
+        return np.zeros(0, dtype=bool)
+    return _stats(pm, want_flags=True)["rep"][: pm.count].cpu().numpy().astype(bool)
 
 
 def extra_vertex_visits(pm: PolygonMesh) -> int:
-    v, pid, _, _, _ = _flat(pm)
-    if v.size == 0:
-        return 0
-    dup, _ = _dup_mask(v, pid)
-    return int(dup.sum())
+    """Sum over polygons of (length - distinct vertices) (traversal.py:140-147)."""
+    return 0 if pm.count == 0 else int(_stats(pm)["extra"])
 
 
-def unique_vertices(pm: PolygonMesh) -> np.ndarray:
-    _, v = pm.csr()
-    return np.unique(v)
+def unique_vertices(pm: PolygonMesh, n_vertices: int = -1) -> np.ndarray:
+    """Sorted distinct vertex ids (traversal.py:150-153)."""
+    if pm.count == 0:
+        return np.zeros(0, dtype=np.int64)
+    st = _stats(pm, want_unique=True, n_vertices=n_vertices)
+    return st["unique"][: st["n_unique"]].cpu().numpy().astype(np.int64)
+
+
+def unique_vertex_count(pm: PolygonMesh, n_vertices: int = -1) -> int:
+    """len(unique_vertices(pm)) without the D2H of the ids (PhaseStats.final_vertices)."""
+    return 0 if pm.count == 0 else int(_stats(pm, n_vertices=n_vertices)["n_unique"])
 
 
 def boundary_edge_count(pm: PolygonMesh) -> int:
-    v, pid, intra, lens, starts = _flat(pm)
-    if v.size == 0:
-        return 0
-    nxt = v[starts[pid] + np.where(intra == lens[pid] - 1, 0, intra + 1)]
-    lo, hi = np.minimum(v, nxt), np.maximum(v, nxt)
-    return int(np.unique(lo * (int(hi.max()) + 1) + hi).size)
+    """Distinct undirected boundary edges (traversal.py:156-166)."""
+    return 0 if pm.count == 0 else int(_stats(pm)["edges"])
 
 
 def enclosed_signed_areas(pm: PolygonMesh, vertices) -> np.ndarray:
-    v, pid, intra, lens, starts = _flat(pm)
-    out = np.zeros(pm.count, dtype=np.float64)
-    if v.size == 0:
-        return out
-    pts = np.asarray(vertices, dtype=np.float64).reshape(-1, 2)
-    nv = v[starts[pid] + np.where(intra == lens[pid] - 1, 0, intra + 1)]
-    cross = pts[v, 0] * pts[nv, 1] - pts[nv, 0] * pts[v, 1]
-    np.add.at(out, pid, cross)
-    return 0.5 * out
+    """Shoelace area per polygon walk (traversal.py:94-109), numpy's summation order."""
+    import torch
+    if pm.count == 0:
+        return np.zeros(0, dtype=np.float64)
+    off, v = pm.device_csr()
+    dev = off.device
+    xy = torch.from_numpy(np.ascontiguousarray(vertices, dtype=np.float64).ravel()).to(dev)
+    area = torch.empty(pm.count, dtype=torch.float64, device=dev)
+    ctx = _capi.context(dev)
+    rc = _capi.lib().tm_polygon_areas(ctx.ptr, _capi.ptr(off), _capi.ptr(v), pm.count, _capi.ptr(xy),
+                                      _capi.ptr(area), _capi.stream_ptr(dev))
+    ctx.check(rc)
+    return area.cpu().numpy()
 
 
 # ---------------------------------------------------------------- traversal

@@ -15,7 +15,7 @@ HEADER = os.path.join(ROOT, "include", "termesh_b200.h")
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int64_t|int|void|const char\s*\*)\s*(tm_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int64_t|int|void|const char\s*\*|tm_file\s*\*)\s*(tm_\w+)\(", text, re.M)))
 
 
 def test_header_declares_entry_points():
