@@ -80,6 +80,8 @@ struct Counters {
 };
 
 constexpr int kUploadChunks = 8;  // triangle upload chunks of tm_mesh_to_polygons_host
+constexpr int kRetryTable = 100;  // internal: rerun the call with a twin table twice the size
+constexpr int kMinShrink = -3;    // twin table at most 8x the full size
 
 enum Seg {
   S_LABEL_A, S_LABEL_B, S_SEEDS, S_TRAV_START, S_TRAV_RULERS, S_TRAV_LEN, S_TRAV_SCAN, S_TRAV_WRITE,
@@ -151,7 +153,7 @@ struct tm_ctx {
   bool early_long = false;
   // whole path: half-size twin table (block-local matching leaves ~43% of the keys
   // to it); an overflow reruns the call at full size and keeps that for this ctx
-  int table_shrink = 1;
+  int table_shrink = 1;  // 2^-s buckets; lowered by one on every displacement overflow
   unsigned long long stamp_clean = 0;  // allocation generation of the stamp buffer known to be all -1
   int label_shrink = 0;  // what the label kernels of the current call use
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -348,7 +350,7 @@ static int prepare(tm_ctx* ctx, int64_t T, int64_t n = -1) {
   if (!ctx->ev_join) CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
   if (!ctx->ev_cls) CK(cudaEventCreateWithFlags(&ctx->ev_cls, cudaEventDisableTiming));
   int64_t Tn = T > 0 ? T : 1;
-  if (n >= 0) ENSURE(slots, hash_bytes(n, Tn));
+  if (n >= 0) ENSURE(slots, hash_bytes(n, Tn, std::min(ctx->table_shrink, ctx->label_shrink)));
   ENSURE(seeds, Tn * sizeof(int32_t));
   ENSURE(start, Tn * sizeof(int32_t));
   ENSURE(len, (Tn + 1) * sizeof(int64_t));
@@ -404,7 +406,8 @@ static int enqueue_label(tm_ctx* ctx, const double* d_xy, int64_t n, const void*
                          int check, int32_t* d_tri32, int32_t* d_hw, int8_t* d_me, uint8_t* d_seed, int32_t* d_tv,
                          cudaStream_t s) {
   Counters* dc = dc_of(ctx);
-  const int shrink = ctx->label_shrink && !check;  // check = 1 sends every key to the table
+  // check = 1 sends every key to the table: never the half-size one
+  const int shrink = check && ctx->label_shrink > 0 ? 0 : ctx->label_shrink;
   const bool lt = ctx->label_timing;  // phase API: device time of each pass (tm_ctx_label_ms)
   if (lt) CK(cudaEventRecord(ctx->lev[0], s));
   if (!ctx->label_a_external) {
@@ -641,6 +644,8 @@ int tm_ctx_create(tm_ctx** out) {
   *out = new tm_ctx();
   const char* g = getenv("TERMESH_NO_GRAPH");
   if (g && *g && *g != '0') (*out)->use_graph = 0;
+  const char* ts = getenv("TERMESH_TABLE_SHRINK");  // testing hook: start with a 2^-s table (overflow/growth path)
+  if (ts && *ts) (*out)->table_shrink = atoi(ts);
   return TM_OK;
 }
 
@@ -758,16 +763,21 @@ int tm_label(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_tri, int 
   int rc = check_sizes(ctx, n, T);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  if ((rc = prepare(ctx, T, n)) || (rc = enqueue_reset(ctx, s))) return rc;
-  ctx->label_shrink = 0;  // phase API: full-size twin table
   for (auto& e : ctx->lev)
     if (!e) CK(cudaEventCreate(&e));
-  ctx->label_timing = true;
-  rc = enqueue_label(ctx, d_xy, n, d_tri, tri_bits, T, check, d_tri32, d_hw, d_max_edge, d_seed, d_tv, s);
-  ctx->label_timing = false;
-  if (rc) return rc;
   Counters h;
-  rc = finish(ctx, s, &h);
+  // phase API: full-size twin table, twice the buckets after a displacement overflow
+  for (ctx->label_shrink = std::min(0, ctx->table_shrink);; ctx->label_shrink--) {
+    if ((rc = prepare(ctx, T, n)) || (rc = enqueue_reset(ctx, s))) return rc;
+    ctx->label_timing = true;
+    rc = enqueue_label(ctx, d_xy, n, d_tri, tri_bits, T, check, d_tri32, d_hw, d_max_edge, d_seed, d_tv, s);
+    ctx->label_timing = false;
+    if (rc) return rc;
+    rc = finish(ctx, s, &h);
+    if (!h.table_ovf) break;
+    if (ctx->label_shrink <= kMinShrink)
+      return set_err(ctx, TM_ERR_CAPACITY, "twin table displacement overflow at 8x size (degenerate keys?)");
+  }
   for (int k = 0; k < 2; k++) {
     float ms = 0;
     ctx->label_ms[k] = cudaEventElapsedTime(&ms, ctx->lev[k], ctx->lev[k + 1]) == cudaSuccess ? ms : 0.0;
@@ -887,7 +897,6 @@ static int path_buffers(tm_ctx* ctx, int64_t n, int64_t T) {
   return TM_OK;
 }
 
-constexpr int kRetryTable = 100;  // internal: rerun the call with the full-size twin table
 
 static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_tri, int tri_bits, int64_t T,
                       int check, int64_t* d_off, int32_t* d_v, int64_t* n_polys, int64_t* n_slots, int64_t* stats,
@@ -1001,9 +1010,12 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
   CK(cudaGetLastError());
   Counters h = *ctx->h_result;
   if (h.table_ovf) {  // the half-size twin table overflowed: this call's labels are incomplete
-    ctx->table_shrink = 0;
+    // rerun with twice the buckets (full size after the half-size table)
+    ctx->table_shrink = std::min(ctx->table_shrink, ctx->label_shrink) - 1;
     if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
     ctx->graph = nullptr;
+    if (ctx->table_shrink < kMinShrink)
+      return set_err(ctx, TM_ERR_CAPACITY, "twin table displacement overflow at 8x size (degenerate keys?)");
     return kRetryTable;
   }
   rc = decode_status(ctx, h);
@@ -1041,7 +1053,7 @@ int tm_mesh_to_polygons(tm_ctx* ctx, const double* d_xy, int64_t n, const void* 
     return set_err(ctx, TM_ERR_ARGUMENT, "output capacities must be at least T polygons and 3T slots");
   int rc = run_device(ctx, d_xy, n, d_tri, tri_bits, T, check, d_off, d_v, n_polys, n_slots, stats,
                       (cudaStream_t)stream);
-  if (rc == kRetryTable)  // now at full table size
+  while (rc == kRetryTable)  // displacement overflow: again with twice the buckets
     rc = run_device(ctx, d_xy, n, d_tri, tri_bits, T, check, d_off, d_v, n_polys, n_slots, stats,
                     (cudaStream_t)stream);
   ctx->last_host = false;
@@ -1118,7 +1130,7 @@ int tm_mesh_to_polygons_host(tm_ctx* ctx, const double* h_xy, int64_t n, const i
   // as soon as it lands, so only the last chunk's pass A is exposed.
   CK(cudaMemcpyAsync(ctx->xy.p, h_xy, 2 * n * sizeof(double), cudaMemcpyHostToDevice, s));
   if ((rc = enqueue_reset(ctx, s))) return rc;
-  const int shrink = ctx->table_shrink && !check;
+  const int shrink = check && ctx->table_shrink > 0 ? 0 : ctx->table_shrink;
   launch_label_a_prepare(n, T, nullptr, ctx->slots.p, s, shrink);
   CK(cudaEventRecord(ctx->chunk_ev[0], s));
   CK(cudaStreamWaitEvent(ctx->cstream, ctx->chunk_ev[0], 0));  // table reset before any chunk's pass A

@@ -10,7 +10,7 @@ namespace tmb {
 struct DevStatus;
 
 // tm_label.cu
-size_t hash_bytes(int64_t n, int64_t T);
+size_t hash_bytes(int64_t n, int64_t T, int shrink = 0);  // bytes of the table at scale 2^-min(shrink, 0)
 // counts kernels of this library launched (bench.py's gpu_launches)
 void note_launch(int k);
 void launch_label_a(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int check,

@@ -106,8 +106,11 @@ __device__ __forceinline__ void table_insert(const TwinTable& tb, DevStatus* st,
       s++;
     }
   }
-  if (tb.ovf) atomicOr(tb.ovf, 1u);  // shrunken table full: the host reruns with the full-size one
-  else report(st, K_STRUCT, h / 3);  // displacement overflow (> 31 buckets): not seen at load <= 0.7
+  // displacement overflow (> 31 buckets; the half-size table without Qhull
+  // locality, or adversarial keys): the host reruns the call with a table twice
+  // the size
+  if (tb.ovf) atomicOr(tb.ovf, 1u);
+  else report(st, K_STRUCT, h / 3);
 }
 
 // Partner of descending half-edge o -> g (key (g, o)) as (h << 1) | L; -1 when border.
@@ -443,10 +446,11 @@ static int bit_length(uint64_t v) {
 }
 
 // Geometry of the twin table for a mesh of n vertices / T triangles.
-// shrink = 1 (whole path): half the buckets.  Block-local matching pairs ~57% of
-// the edges before the table (Qhull order), so the inserted keys load the half
-// table to ~0.3; a mesh without that locality overflows it, which sets *ovf and
-// the host reruns the path with shrink = 0.
+// shrink = s scales the bucket count by 2^-s.  s = 1 (whole path): half the
+// buckets -- block-local matching pairs ~57% of the edges before the table
+// (Qhull order), so the inserted keys load the half table to ~0.3; a mesh
+// without that locality overflows it, which sets *ovf and the host reruns the
+// call with s - 1 (full size, then 2x, 4x, 8x).
 static TwinTable table_geometry(int64_t n, int64_t T, void* mem, int shrink = 0, unsigned int* ovf = nullptr) {
   TwinTable tb{};
   tb.b = bit_length((uint64_t)(n > 1 ? n - 1 : 1));
@@ -457,18 +461,19 @@ static TwinTable table_geometry(int64_t n, int64_t T, void* mem, int shrink = 0,
   // (measured: a fuller table costs more in probe/CAS conflicts than it saves in L2)
   uint64_t keys = (uint64_t)(3 * (T > 0 ? T : 1)) / 2 + 64;
   int q = bit_length((keys * 10 / 28) | 1);
-  if (shrink && q > 8) q -= 1;
+  if (shrink > 0) q = q - shrink > 8 ? q - shrink : (q > 8 ? 8 : q);
+  if (shrink < 0) q -= shrink;
   if (q > tb.K) q = tb.K;
   while (tb.K - q + kDispBits + tb.hb > 63 && q < tb.K) q++;  // the slot must hold remainder|d|h|L in 63 bits
   tb.R = tb.K - q;
   tb.nb_mask = (1ull << q) - 1;
   tb.slots = static_cast<unsigned long long*>(mem);
-  tb.ovf = shrink ? ovf : nullptr;
+  tb.ovf = ovf;
   return tb;
 }
 
-size_t hash_bytes(int64_t n, int64_t T) {
-  TwinTable tb = table_geometry(n, T, nullptr);
+size_t hash_bytes(int64_t n, int64_t T, int shrink) {
+  TwinTable tb = table_geometry(n, T, nullptr, shrink < 0 ? shrink : 0);
   return (size_t)(tb.nb_mask + 1) * 4 * sizeof(unsigned long long);
 }
 

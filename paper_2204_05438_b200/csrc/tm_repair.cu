@@ -396,6 +396,7 @@ __device__ int warp_extra_visits(const int32_t* s, int n, int lane) {
 // failure, or kFanCap + 1 when the fan does not fit (caller falls back).
 __device__ int warp_collect_fan(const RepairCtx& c, int32_t v, int32_t* fan, int32_t* back, int lane) {
   int32_t g0 = -1;
+  __syncwarp();  // the buffers may still be read by every lane of a previous use (racecheck)
   if (lane == 0) {
     int32_t t0 = c.tv[v];
     g0 = t0 < 0 ? -1 : he_with_origin(c.tri, t0, v);
@@ -1956,6 +1957,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
           if (lane == 0) rel = atomicAdd(&s_stop, X.nseg);
           rel = __shfl_sync(kFull, rel, 0);
           for (int k = lane; k < X.nseg; k += 32) segs[nb + rel + k] = segs[X.soff + k];
+          __syncwarp();  // every lane has read in[r] before lane 0 rewrites it
           if (lane == 0) in[r].soff = nb + rel;
         }
         hbase = nb;
