@@ -65,6 +65,12 @@ WORKLOADS = {
                 desc="1M points in 64 Gaussian clusters (sigma 0.002) in the unit square, scipy Delaunay (seed 0)"),
     "c10m": dict(n=10_000_000, gen="clustered",
                  desc="10M points in 64 Gaussian clusters (sigma 0.002) in the unit square, scipy Delaunay (seed 0)"),
+    # BASELINE.json configs[3]: one Qhull call would take ~1 h and ~150 GB on the
+    # host, so the same points go through the tile-parallel exact Delaunay
+    # (tools/tiled_delaunay.py: the identical triangle set as Qhull, checked at
+    # 300k / 1M / 10M; tile-major triangle order)
+    "u100m": dict(n=100_000_000, gen="tiled",
+                  desc="100M uniform random points in the unit square, exact Delaunay (tile-parallel Qhull, seed 0)"),
 }
 METRIC = "triangles/sec end-to-end mesh->polygons"
 UNIT = "triangles/s"
@@ -75,6 +81,10 @@ def load_mesh(workload, seed):
     w = WORKLOADS[workload]
     if w["gen"] == "clustered":
         return io.cached(f"{workload}_s{seed}_clustered", lambda: io.generate_clustered_delaunay(w["n"], seed=seed))
+    if w["gen"] == "tiled":
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import tiled_delaunay
+        return io.cached(f"{workload}_s{seed}_tiled", lambda: tiled_delaunay.triangulation(w["n"], seed)[0])
     return io.cached(f"{workload}_s{seed}_unit", lambda: io.generate_random_delaunay(w["n"], (0.0, 0.0, 1.0, 1.0), seed))
 
 

@@ -31,13 +31,13 @@ tr = torch.from_numpy(tri.triangles).to(dev)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 L = _capi.lib()
 res = {}
+off = torch.empty(T + 1, dtype=torch.int64, device=dev)
+v = torch.empty(3 * T, dtype=torch.int32, device=dev)
 for G in [int(x) for x in a.gpus.split(",")]:
     per = []
     for b, e in D.partition(T, G):
-        ctx = _capi.Context(0)
+        ctx = _capi.Context(0)  # one rank's context (its scratch is freed after the rank: 100M fits one at a time)
         ctx.check(L.tm_ctx_set_partition(ctx.ptr, b, e))
-        off = torch.empty(T + 1, dtype=torch.int64, device=dev)
-        v = torch.empty(3 * T, dtype=torch.int32, device=dev)
         npol, nsl = ctypes.c_int64(), ctypes.c_int64()
         st = (ctypes.c_int64 * _capi.NUM_STATS)()
         sp = _capi.stream_ptr(dev)
@@ -57,7 +57,7 @@ for G in [int(x) for x in a.gpus.split(",")]:
             torch.cuda.synchronize()
             ms.append(e0.elapsed_time(e1))
         per.append(sorted(ms)[len(ms) // 2])
-        del ctx
+        ctx.close()
     res[G] = {"rank_ms": [round(x, 4) for x in per], "step_ms": round(max(per), 4),
               "triangles_per_s": round(T / (max(per) / 1e3), 1)}
 base = res[min(res)]["step_ms"]
