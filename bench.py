@@ -192,6 +192,7 @@ def run_gpu(args, rank, world, local_rank):
     ctx.check(L.tm_ctx_set_partition(ctx.ptr, t_begin, t_end))
 
     shard = [None]
+    comm = D.Comm() if world > 1 else None  # the library's NCCL communicator (tm_comm_*, C ABI)
 
     def step():
         rc = L.tm_mesh_to_polygons(ctx.ptr, _capi.ptr(xy), n, _capi.ptr(tr), 64, T, 0, _capi.ptr(off),
@@ -199,7 +200,7 @@ def run_gpu(args, rank, world, local_rank):
         ctx.check(rc)
         if world > 1:  # the exchange step: all-gather counts (NCCL), shift to the global slot base
             shard[0] = D.stitch(off, verts, npol.value, nsl.value, pinch=(stats[8], stats[10]),
-                                resume=D.device_resume(ctx, off, verts, T, stats))
+                                resume=D.device_resume(ctx, off, verts, T, stats), comm=comm)
 
     for _ in range(args.warmup):
         step()
@@ -294,7 +295,7 @@ def run_gpu(args, rank, world, local_rank):
         ctx.check(rc)
         if world > 1:
             D.stitch(h_off, h_v, npol.value, nsl.value, pinch=(stats[8], stats[10]),
-                     resume=D.device_resume(ctx, h_off, h_v, T, stats))
+                     resume=D.device_resume(ctx, h_off, h_v, T, stats), comm=comm)
 
     for _ in range(args.warmup):
         e2e_step()
@@ -319,7 +320,8 @@ def run_gpu(args, rank, world, local_rank):
         "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"], "n_vertices": n,
                    "triangles": T, "seed_range_rank0": [t_begin, t_end], "polygons_rank0": P_out,
                    "polygon_slots_rank0": F_out, "l2": "flushed (256 MiB write) between steps",
-                   "parallelism": f"replicated mesh, seeds partitioned x{world}, NCCL all-gather of counts"},
+                   "parallelism": f"replicated mesh, seeds partitioned x{world}, NCCL all-gather of counts "
+                                  f"(tm_comm_allgather)"},
         "e2e": e2e, "roofline": roofline, "kernels": kernels, "repair_stats": repair_stats,
         "gpu_launches": int(launches), "clocks": clk.summary(), "parity": parity,
         "step_ms": {"min": round(min(step_ms), 4), "median": round(statistics.median(step_ms), 4),

@@ -230,6 +230,22 @@ int tm_polygon_areas(tm_ctx *ctx, const int64_t *d_offsets, const int32_t *d_ver
 int tm_canonicalize(tm_ctx *ctx, const int64_t *d_offsets, const int32_t *d_verts, int64_t n_polys,
                     int64_t n_vertices, int64_t *d_offsets_out, int32_t *d_verts_out, void *stream);
 
+/* ---------------------------------------------------------------- multi-GPU exchange
+ * One NCCL communicator per rank (one process per GPU).  Rank 0 makes the
+ * unique id (tm_comm_id_bytes() bytes), the host broadcasts it, every rank
+ * calls tm_comm_init.  NCCL is bound at run time (libnccl.so.2).  The
+ * seed-partitioned path exchanges each rank's (polygons, slots, pinch extra
+ * visits, deferred items) with tm_comm_allgather and places its CSR at the
+ * exclusive prefix (tm_shift_offsets). */
+typedef struct tm_comm tm_comm;
+int tm_comm_id_bytes(void);
+int tm_comm_unique_id(void *id_out);
+int tm_comm_init(tm_comm **out, int rank, int world, const void *id, int device);
+/* d_recv[r * bytes_per_rank ...] = rank r's d_send (device buffers, on `stream`) */
+int tm_comm_allgather(tm_comm *comm, const void *d_send, void *d_recv, size_t bytes_per_rank, void *stream);
+void tm_comm_destroy(tm_comm *comm);
+const char *tm_comm_last_error(void);
+
 /* ---------------------------------------------------------------- host-side text I/O (no GPU)
  * Python repr(float) of x into out (io_formats.py:44-46); returns the length, -1 if cap is too small */
 int tm_format_double(double x, char *out, size_t cap);

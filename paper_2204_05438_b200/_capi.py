@@ -84,6 +84,17 @@ def lib():
         L.tm_polygon_stats.argtypes = [_P, _P, _P, _I64, _I64, _P, _P, _P, _PI64, _PI64, _PI64, _P]
         L.tm_polygon_areas.argtypes = [_P, _P, _P, _I64, _P, _P, _P]
         L.tm_canonicalize.argtypes = [_P, _P, _P, _I64, _I64, _P, _P, _P]
+        # multi-GPU exchange (tm_comm.cu; NCCL bound at run time)
+        L.tm_comm_id_bytes.restype = _I
+        L.tm_comm_unique_id.argtypes = [_P]
+        L.tm_comm_unique_id.restype = _I
+        L.tm_comm_init.argtypes = [ctypes.POINTER(_P), _I, _I, _P, _I]
+        L.tm_comm_init.restype = _I
+        L.tm_comm_allgather.argtypes = [_P, _P, _P, ctypes.c_size_t, _P]
+        L.tm_comm_allgather.restype = _I
+        L.tm_comm_destroy.argtypes = [_P]
+        L.tm_comm_destroy.restype = None
+        L.tm_comm_last_error.restype = ctypes.c_char_p
         # host-side text I/O (tm_io.cu; no GPU needed)
         L.tm_format_double.argtypes = [ctypes.c_double, ctypes.c_char_p, ctypes.c_size_t]
         L.tm_format_double.restype = _I
@@ -120,7 +131,8 @@ def exported_symbols():
             "tm_pack_frontier",
             "tm_traverse", "tm_repair", "tm_mesh_to_polygons_host", "tm_mesh_to_polygons", "tm_resume_pinch",
             "tm_check_trivertex", "tm_polygon_stats", "tm_polygon_areas", "tm_canonicalize",
-            "tm_format_double", "tm_file_read", "tm_file_status", "tm_file_copy", "tm_file_close",
+            "tm_comm_id_bytes", "tm_comm_unique_id", "tm_comm_init", "tm_comm_allgather", "tm_comm_destroy",
+            "tm_comm_last_error", "tm_format_double", "tm_file_read", "tm_file_status", "tm_file_copy", "tm_file_close",
             "tm_write_polymesh", "tm_write_triangle_file")
 
 

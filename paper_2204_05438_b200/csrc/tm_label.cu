@@ -71,20 +71,32 @@ __device__ __forceinline__ Probe probe_of(const TwinTable& tb, int32_t lo, int32
   return p;
 }
 
-__device__ __forceinline__ void load_bucket_cg(const unsigned long long* s, unsigned long long (&v)[4]) {
-  ulonglong2 a = __ldcg(reinterpret_cast<const ulonglong2*>(s));
-  ulonglong2 b = __ldcg(reinterpret_cast<const ulonglong2*>(s) + 1);
-  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+// A bucket's 4 slots as two 16-byte loads into registers (no local-memory
+// array: the slot loops below are fully unrolled over named values).
+struct Bucket {
+  unsigned long long s0, s1, s2, s3;
+  __device__ __forceinline__ unsigned long long at(int k) const {
+    return k == 0 ? s0 : k == 1 ? s1 : k == 2 ? s2 : s3;  // k is a compile-time constant after unrolling
+  }
+};
+
+__device__ __forceinline__ Bucket load_bucket_cg(const unsigned long long* s) {
+  const ulonglong2 a = __ldcg(reinterpret_cast<const ulonglong2*>(s));
+  const ulonglong2 b = __ldcg(reinterpret_cast<const ulonglong2*>(s) + 1);
+  return Bucket{a.x, a.y, b.x, b.y};
 }
 
-__device__ __forceinline__ void load_bucket_nc(const unsigned long long* s, unsigned long long (&v)[4]) {
-  ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(s));
-  ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(s) + 1);
-  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+__device__ __forceinline__ Bucket load_bucket_nc(const unsigned long long* s) {
+  const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(s));
+  const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(s) + 1);
+  return Bucket{a.x, a.y, b.x, b.y};
 }
 
 // Insert ascending half-edge h = lo -> hi.  In a valid mesh each key has one
 // ascending half-edge; a second one is an orientation / reciprocity defect.
+// Slots fill in order and are never cleared: an empty slot is claimed with a
+// CAS; a lost race leaves the slot occupied by the winner, which is then
+// examined like any occupied slot.
 __device__ __forceinline__ void table_insert(const TwinTable& tb, DevStatus* st, int32_t hl, int32_t lo, int32_t hi) {
   const int32_t h = hl >> 1;  // hl = (h << 1) | L
   Probe p = probe_of(tb, lo, hi);
@@ -92,18 +104,18 @@ __device__ __forceinline__ void table_insert(const TwinTable& tb, DevStatus* st,
     unsigned long long* bk = tb.slots + 4 * ((p.home + d) & tb.nb_mask);
     const uint64_t tag = p.tag | (uint64_t)d;
     const unsigned long long mine = (tag << tb.hb) | (uint32_t)hl;
-    unsigned long long v[4];
-    load_bucket_cg(bk, v);
-    int s = 0;
-    while (s < 4) {
-      if (v[s] == kEmptySlot) {
-        unsigned long long prev = atomicCAS(bk + s, kEmptySlot, mine);
-        if (prev == kEmptySlot) return;
-        v[s] = prev;  // lost the race: examine the winner, stay on this slot
-        continue;
+    const Bucket b = load_bucket_cg(bk);
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      unsigned long long cur = b.at(k);
+      if (cur == kEmptySlot) {
+        cur = atomicCAS(bk + k, kEmptySlot, mine);
+        if (cur == kEmptySlot) return;
       }
-      if (((v[s] & ~kClaimBit) >> tb.hb) == tag) { report(st, K_RECIPROCITY, h / 3); return; }
-      s++;
+      if (((cur & ~kClaimBit) >> tb.hb) == tag) {
+        report(st, K_RECIPROCITY, h / 3);
+        return;
+      }
     }
   }
   // displacement overflow (> 31 buckets; the half-size table without Qhull
@@ -121,17 +133,17 @@ __device__ __forceinline__ int32_t table_lookup(const TwinTable& tb, DevStatus* 
   for (int d = 0; d <= kMaxDisp; d++) {
     unsigned long long* bk = tb.slots + 4 * ((p.home + d) & tb.nb_mask);
     const uint64_t tag = p.tag | (uint64_t)d;
-    unsigned long long v[4];
-    load_bucket_nc(bk, v);
+    const Bucket b = load_bucket_nc(bk);
 #pragma unroll
-    for (int s = 0; s < 4; s++) {
-      if (v[s] == kEmptySlot) return -1;
-      if (((v[s] & ~kClaimBit) >> tb.hb) == tag) {
+    for (int k = 0; k < 4; k++) {
+      const unsigned long long cur = b.at(k);
+      if (cur == kEmptySlot) return -1;
+      if (((cur & ~kClaimBit) >> tb.hb) == tag) {
         if (check) {  // a second descending partner: edge shared by > 2 triangles
-          unsigned long long old = atomicOr(bk + s, kClaimBit);
+          unsigned long long old = atomicOr(bk + k, kClaimBit);
           if (old & kClaimBit) report(st, K_EDGE_COUNT, elem);
         }
-        return (int32_t)(v[s] & hmask);
+        return (int32_t)(cur & hmask);
       }
     }
   }

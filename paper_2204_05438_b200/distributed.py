@@ -46,11 +46,58 @@ def exclusive_bases(counts) -> tuple[np.ndarray, np.ndarray]:
     return pb, sb
 
 
-def exchange_counts(n_polys: int, n_slots: int, device, group=None, pinch=(0, 0)) -> np.ndarray:
+class Comm:
+    """The library's own NCCL communicator for this rank (tm_comm_init, C ABI):
+    rank 0's unique id goes round once through torch.distributed, then every
+    exchange of the path is a tm_comm_allgather on the device stream."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+        from . import _capi
+        L = _capi.lib()
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        uid = ctypes.create_string_buffer(L.tm_comm_id_bytes())
+        if self.rank == 0 and L.tm_comm_unique_id(uid) != 0:
+            raise _capi.TermeshError(L.tm_comm_last_error().decode())
+        obj = [uid.raw]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        self.device = torch.cuda.current_device()
+        p = ctypes.c_void_p()
+        idbuf = ctypes.create_string_buffer(obj[0], len(obj[0]))
+        if L.tm_comm_init(ctypes.byref(p), self.rank, self.world, idbuf, self.device) != 0:
+            raise _capi.TermeshError(L.tm_comm_last_error().decode())
+        self.ptr = p
+
+    def allgather(self, send, recv):
+        """recv (device, world x send.nbytes) <- every rank's send (device)."""
+        from . import _capi
+        L = _capi.lib()
+        rc = L.tm_comm_allgather(self.ptr, _capi.ptr(send), _capi.ptr(recv), send.numel() * send.element_size(),
+                                 _capi.stream_ptr(send.device))
+        if rc != 0:
+            raise _capi.TermeshError(L.tm_comm_last_error().decode())
+
+    def close(self):
+        if self.ptr:
+            from . import _capi
+            _capi.lib().tm_comm_destroy(self.ptr)
+            self.ptr = None
+
+
+def exchange_counts(n_polys: int, n_slots: int, device, group=None, pinch=(0, 0), comm: Comm | None = None) -> np.ndarray:
     """All-gather (polygons, slots, pinch extra visits, pinch-deferred items) of
-    every rank: int64[world, 4] on every rank (32 bytes per rank)."""
+    every rank: int64[world, 4] on every rank (32 bytes per rank) -- through the
+    library's NCCL communicator when one is given, else torch.distributed
+    (gloo in the CPU tests)."""
     import torch
     import torch.distributed as dist
+    if comm is not None:
+        dev = torch.device("cuda", comm.device)
+        mine = torch.tensor([n_polys, n_slots, int(pinch[0]), int(pinch[1])], dtype=torch.int64, device=dev)
+        allc = torch.empty(comm.world * 4, dtype=torch.int64, device=dev)
+        comm.allgather(mine, allc)
+        return allc.view(comm.world, 4).cpu().numpy()
     world = dist.get_world_size(group)
     if dist.get_backend(group) == "nccl":
         device = torch.device("cuda", torch.cuda.current_device())
@@ -90,7 +137,7 @@ class ShardedCSR:
 
 
 def stitch(local_off, local_verts, n_polys: int, n_slots: int, group=None, shift=None, pinch=(0, 0),
-           resume=None) -> ShardedCSR:
+           resume=None, comm: Comm | None = None) -> ShardedCSR:
     """Exchange counts and place this rank's CSR at its global base.
 
     pinch = this rank's (TM_STAT_PINCH_EXTRA, TM_STAT_PINCH_DEFERRED).  The pinch
@@ -100,11 +147,12 @@ def stitch(local_off, local_verts, n_polys: int, n_slots: int, group=None, shift
     device) and a second all-gather publishes the final counts.  Without deferred
     items anywhere (the usual case) the first exchange is the only one.
     `shift` adds the slot base to the offsets in place (default: the C ABI kernel
-    on a CUDA tensor, a plain add on CPU tensors)."""
+    on a CUDA tensor, a plain add on CPU tensors).  comm: the library's NCCL
+    communicator (Comm) for the exchange, else torch.distributed."""
     import torch.distributed as dist
     rank = dist.get_rank(group)
     dev = local_off.device if local_off.is_cuda else "cpu"
-    table = exchange_counts(n_polys, n_slots, dev, group, pinch)
+    table = exchange_counts(n_polys, n_slots, dev, group, pinch, comm)
     if needs_resume(table):
         if int(pinch[1]) > 0:
             if resume is None:
@@ -112,7 +160,7 @@ def stitch(local_off, local_verts, n_polys: int, n_slots: int, group=None, shift
                 raise StructuralError("items parked at the local pinch guard and no resume step given",
                                       phase="reparation")
             n_polys, n_slots = resume(global_pinch_extra(table))
-        table = exchange_counts(n_polys, n_slots, dev, group, (int(pinch[0]), 0))
+        table = exchange_counts(n_polys, n_slots, dev, group, (int(pinch[0]), 0), comm)
     counts = table[:, :2]
     pb, sb = exclusive_bases(counts)
     off = local_off[: n_polys + 1]
@@ -211,7 +259,7 @@ def resume_partition(ctx, off, verts, T: int, extra_total: int):
     return p, f, dict(zip(_capi.STAT_NAMES, list(stats)))
 
 
-def execute_distributed(tri, group=None, gather: bool = True):
+def execute_distributed(tri, group=None, gather: bool = True, comm: Comm | None = None):
     """Drop-in multi-GPU execute: every rank passes the same Triangulation; the
     global final CSR comes back on rank 0 (gather=True) or as shards."""
     import torch
@@ -225,8 +273,10 @@ def execute_distributed(tri, group=None, gather: bool = True):
     from . import _capi
     ctx = _capi.context(dev)
     off, verts, p, f, stats = run_partition(xy, tr, n, T, b, e, ctx=ctx)
+    if comm is None and dist.get_backend(group) == "nccl":
+        comm = Comm(group)  # the library's own communicator for the exchange
     shard = stitch(off, verts, p, f, group, pinch=(stats["pinch_extra"], stats["pinch_deferred"]),
-                   resume=device_resume(ctx, off, verts, T))
+                   resume=device_resume(ctx, off, verts, T), comm=comm)
     if not gather:
         return shard, stats
     return gather_csr(shard, 0, group), stats

@@ -139,3 +139,32 @@ def test_partitioned_device_path(cuda, name, world, cap, monkeypatch):
     got_off = np.concatenate([off[:p].cpu().numpy() for _, off, _, p, _ in ranks] + [np.array([int(sb[-1]) + ranks[-1][4]])])
     got_v = np.concatenate([v[:f].cpu().numpy() for _, _, v, _, f in ranks])
     assert np.array_equal(got_off, g["final_off"]) and np.array_equal(got_v, g["final_verts"])
+
+
+@pytest.mark.gpu
+def test_library_nccl_comm_single_rank(cuda):
+    """The C-ABI communicator (tm_comm_*: NCCL bound at run time) on a
+    one-rank group: the counts exchange and the stitch go through it."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = D.Comm()
+        send = torch.arange(8, dtype=torch.int64, device=cuda)
+        recv = torch.empty(8, dtype=torch.int64, device=cuda)
+        comm.allgather(send, recv)
+        torch.cuda.synchronize()
+        assert torch.equal(send, recv)
+        table = D.exchange_counts(5, 17, cuda, pinch=(3, 0), comm=comm)
+        assert table.tolist() == [[5, 17, 3, 0]]
+        tri, g = load_case("aniso2k_s1")
+        xy = torch.from_numpy(tri.vertices).to(cuda)
+        tr = torch.from_numpy(tri.triangles).to(cuda)
+        off, v, p, f, st = D.run_partition(xy, tr, tri.n_vertices, tri.n_triangles, 0, tri.n_triangles)
+        shard = D.stitch(off, v, p, f, pinch=(st["pinch_extra"], st["pinch_deferred"]), comm=comm)
+        assert np.array_equal(shard.offsets.cpu().numpy(), g["final_off"])
+        assert np.array_equal(shard.verts.cpu().numpy(), g["final_verts"])
+        comm.close()
+    finally:
+        dist.destroy_process_group()
