@@ -507,7 +507,8 @@ static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* 
                               d_v, ctx->path_hv, a);
       launch_classify(d_off, d_v, &dc->n_seeds, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(),
                       &dc->n_items, ctx->long_list.as<int32_t>(), &dc->n_long, dc->stats, long_queue(ctx),
-                      ctx->path_hv, ctx->tv.as<int32_t>(), 2, ctx->item_state.as<int32_t>(), a);
+                      ctx->path_hv, ctx->tv.as<int32_t>(), 2, ctx->item_state.as<int32_t>(), ctx->pool.as<int32_t>(),
+                      &dc->pool_top, ctx->pool_cap, a);
       CK(cudaEventRecord(ctx->ev_cls, a));
       {
         RepairArgs ra = repair_args(ctx, d_tri32, const_cast<int32_t*>(d_hw), ctx->tv.as<int32_t>(), T, d_off, d_v);
@@ -535,7 +536,8 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
     SegTimer t_(ctx, S_CLASSIFY, s);
     launch_classify(d_off_in, d_v_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(), &dc->n_items,
                     ctx->long_list.as<int32_t>(), &dc->n_long, dc->stats, q, ctx->path_hv,
-                    const_cast<int32_t*>(d_tv), early ? 1 : 0, ctx->item_state.as<int32_t>(), s);
+                    const_cast<int32_t*>(d_tv), early ? 1 : 0, ctx->item_state.as<int32_t>(), ctx->pool.as<int32_t>(),
+                    &dc->pool_top, ctx->pool_cap, s);
   }
   if (early) CK(cudaStreamWaitEvent(s, ctx->ev_cls, 0));  // the item list is complete
   RepairArgs a = repair_args(ctx, d_tri32, d_hw, d_tv, T, d_off_in, d_v_in);

@@ -117,7 +117,8 @@ void launch_tv_items(const int64_t* off, const int32_t* v, const int32_t* hv, co
 void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, int32_t* item_of,
                      int32_t* items, unsigned int* n_items, int32_t* long_list, unsigned int* n_long,
                      unsigned long long* stats, LongQueue q, const int32_t* hv, int32_t* tv, int which,
-                     int32_t* item_state, cudaStream_t s);  // item_state[k] = 0 for every item k created  // which: 0 all, 1 short polygons only, 2 the listed long ones only
+                     int32_t* item_state, int32_t* pool, unsigned long long* pool_top, unsigned long long pool_cap,
+                     cudaStream_t s);  // item_state[k] = 0 for every item k created  // which: 0 all, 1 short polygons only, 2 the listed long ones only
 void launch_repair_tips_long(const RepairArgs& a, cudaStream_t s);
 // mode 0: items of length <= kLongMin; mode 1: long items handed back (state 2/3)
 void launch_repair_tips(const RepairArgs& a, int mode, cudaStream_t s);

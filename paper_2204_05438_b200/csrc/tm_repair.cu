@@ -194,8 +194,11 @@ __global__ void __launch_bounds__(256) k_classify(const int64_t* __restrict__ of
   }
 }
 
-// long polygons: one block each; distinct vertices counted with a shared-memory
-// open-addressing set (len <= kSetCap/2), else a block-parallel quadratic scan.
+// long polygons: one block each; distinct vertices counted with an
+// open-addressing set -- in shared memory (len <= kSetCap/2), else in a
+// block-private region bump-allocated from the repair pool (the polygon of the
+// hull sliver reaches ~10^4 vertices at 100M points), else (pool exhausted)
+// a block-parallel quadratic scan.
 constexpr int kSetCap = 8192;
 __global__ void __launch_bounds__(256) k_classify_long(const int64_t* __restrict__ off, const int32_t* __restrict__ v,
                                                        const int32_t* __restrict__ long_list,
@@ -203,20 +206,31 @@ __global__ void __launch_bounds__(256) k_classify_long(const int64_t* __restrict
                                                        int32_t* __restrict__ items, unsigned int* n_items,
                                                        unsigned long long* stats, LongQueue q,
                                                        const int32_t* __restrict__ hv, int32_t* __restrict__ tv,
-                                                       int32_t* __restrict__ item_state) {
-  __shared__ int32_t tab[kSetCap];
+                                                       int32_t* __restrict__ item_state, int32_t* pool,
+                                                       unsigned long long* pool_top, unsigned long long pool_cap) {
+  __shared__ int32_t s_tab[kSetCap];
   __shared__ unsigned int dups;
+  __shared__ long long s_gbase;
   unsigned int nl = *n_long;
   for (unsigned int w = blockIdx.x; w < nl; w += gridDim.x) {
     int32_t i = long_list[w];
     int64_t b = off[i];
     int n = (int)(off[i + 1] - b);
     const int32_t* s = v + b;
-    if (threadIdx.x == 0) dups = 0;
+    int cap = 64;
+    while (cap < 2 * n) cap <<= 1;
+    if (threadIdx.x == 0) {
+      dups = 0;
+      s_gbase = -1;
+      if (cap > kSetCap) {
+        const unsigned long long o = atomicAdd(pool_top, (unsigned long long)cap);
+        if (o + (unsigned long long)cap <= pool_cap) s_gbase = (long long)o;
+      }
+    }
+    __syncthreads();
     unsigned int my = 0;
-    if (2 * n <= kSetCap) {
-      int cap = 64;
-      while (cap < 2 * n) cap <<= 1;
+    if (cap <= kSetCap || s_gbase >= 0) {
+      int32_t* tab = cap <= kSetCap ? s_tab : pool + s_gbase;
       for (int k = threadIdx.x; k < cap; k += blockDim.x) tab[k] = -1;
       __syncthreads();
       for (int p = threadIdx.x; p < n; p += blockDim.x) {
@@ -1417,7 +1431,16 @@ __global__ void __launch_bounds__(32 * kTipWarps, 8) k_repair_tips(RepairCtx c, 
 // or the record list would overflow, the current pieces go to the pool and the
 // warp kernel resumes the item (item_state = 2).
 constexpr int kSegWarps = 16;
-constexpr int kSegMaxL = 8192;   // longer items: the warp kernel from scratch (state 3)
+constexpr int kSegMaxL = 8192;   // longer items keep their per-item arrays in global memory (below)
+// Items longer than kSegMaxL (the hull-sliver polygon passes 10^4 vertices at
+// 100M points) keep P, its tip bitmap / ranks, the pair map and nexttip in a
+// block-private region of the repair pool instead of shared memory (the
+// segment lists and piece records stay in shared memory); longer than
+// kSegMaxG: the warp kernel from scratch (state 3).  3 kSegMaxG < 2^16 keeps
+// the 16-bit piece lengths and nexttip entries valid.
+constexpr int kSegMaxG = 21760;
+constexpr int kGPairCap = 65536;  // >= 2 kSegMaxG, power of two
+constexpr long long kGStride = (long long)kSegMaxG + 3 * (kSegMaxG / 32 + 1) + kGPairCap + (kSegMaxG + 1) / 2 + 64;
 constexpr int kPairCap = 16384;  // pair-map slots (>= 2 kSegMaxL); reused as leaf hash sets
 constexpr int kSegRec = 1024;    // piece records per round list
 constexpr int kSegTips = 512;    // precomputed tips per item
@@ -1759,22 +1782,28 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
                                                                     int64_t* __restrict__ item_slots,
                                                                     unsigned long long* stats, LongQueue q,
                                                                     unsigned long long* dbg, unsigned int trace_qi,
-                                                                    int seg_cap) {
+                                                                    int seg_cap, int smem_max_l) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  int32_t* P = reinterpret_cast<int32_t*>(smem_raw);
-  uint32_t* tipbits = reinterpret_cast<uint32_t*>(P + kSegMaxL);
-  int32_t* pmap = reinterpret_cast<int32_t*>(tipbits + kSegMaxL / 32);
-  SPiece* recs = reinterpret_cast<SPiece*>(pmap + kPairCap);  // [2][kSegRec]
+  int32_t* const sP = reinterpret_cast<int32_t*>(smem_raw);
+  uint32_t* const stipbits = reinterpret_cast<uint32_t*>(sP + kSegMaxL);
+  int32_t* const spmap = reinterpret_cast<int32_t*>(stipbits + kSegMaxL / 32);
+  SPiece* recs = reinterpret_cast<SPiece*>(spmap + kPairCap);  // [2][kSegRec]
   int32_t* s_out = reinterpret_cast<int32_t*>(recs + 2 * kSegRec);
   int32_t* fans = s_out + kSegRec;
   int32_t* tipv = fans + 2 * kSegWarps * kFanCap;  // tip vertex (or -1 when its info is unusable)
   int32_t* tipb = tipv + kSegTips;                 // barrier vertex
   SplitInfo* tipinfo = reinterpret_cast<SplitInfo*>(tipb + kSegTips);
   int32_t* tset = reinterpret_cast<int32_t*>(tipinfo + kSegTips);  // promoted-edge endpoints (hash set)
-  int32_t* tiprank = tset + kSegTouch;                              // tips of P before word w
-  int32_t* nextw = tiprank + kSegMaxL / 32 + 1;                      // first non-empty tip word >= w
-  uint16_t* nexttip = reinterpret_cast<uint16_t*>(nextw + kSegMaxL / 32 + 1);
-  int* tipdeg = reinterpret_cast<int*>(nexttip + kSegMaxL);  // cached fan sizes (-1: none)
+  int32_t* const stiprank = tset + kSegTouch;                         // tips of P before word w
+  int32_t* const snextw = stiprank + kSegMaxL / 32 + 1;                // first non-empty tip word >= w
+  uint16_t* const snexttip = reinterpret_cast<uint16_t*>(snextw + kSegMaxL / 32 + 1);
+  int* tipdeg = reinterpret_cast<int*>(snexttip + kSegMaxL);  // cached fan sizes (-1: none)
+  // the per-item arrays: shared memory, or the block's pool region for items over kSegMaxL
+  int32_t *P, *pmap, *tiprank, *nextw;
+  uint32_t* tipbits;
+  uint16_t* nexttip;
+  __shared__ long long s_gscr;  // pool offset of the block's global region (-1: not allocated)
+  if (threadIdx.x == 0) s_gscr = -1;
   int* tlist = tipdeg + kSegTips;                              // tipped records of the round
   Seg* segs = reinterpret_cast<Seg*>(tlist + kSegRec);
   // s_ntb: tipped-record count of the next round, double-buffered by round parity
@@ -1808,9 +1837,31 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
     const int32_t i = items[w];
     const int64_t b0 = off[i];
     const int L = (int)(off[i + 1] - b0);
-    if (L > kSegMaxL || L < 3) {
+    if (L > kSegMaxG || L < 3) {
       if (threadIdx.x == 0) item_state[w] = 3;
       continue;
+    }
+    if (L > smem_max_l) {  // smem_max_l = kSegMaxL (lower only as a testing hook)
+      if (threadIdx.x == 0 && s_gscr < 0) s_gscr = palloc(c, kGStride);
+      __syncthreads();
+      if (s_gscr < 0) {  // pool exhausted: the warp kernel from scratch
+        if (threadIdx.x == 0) item_state[w] = 3;
+        continue;
+      }
+      int32_t* gb = c.pool + s_gscr;
+      P = gb;
+      tipbits = reinterpret_cast<uint32_t*>(P + kSegMaxG);
+      tiprank = reinterpret_cast<int32_t*>(tipbits + kSegMaxG / 32 + 1);
+      nextw = tiprank + kSegMaxG / 32 + 1;
+      pmap = nextw + kSegMaxG / 32 + 1;
+      nexttip = reinterpret_cast<uint16_t*>(pmap + kGPairCap);
+    } else {
+      P = sP;
+      tipbits = stipbits;
+      tiprank = stiprank;
+      nextw = snextw;
+      pmap = spmap;
+      nexttip = snexttip;
     }
     int pcap = 64;
     while (pcap < 2 * L) pcap <<= 1;
@@ -2426,7 +2477,8 @@ void launch_tv_items(const int64_t* off, const int32_t* v, const int32_t* hv, co
 void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, int64_t Pcap, int32_t* item_of,
                      int32_t* items, unsigned int* n_items, int32_t* long_list, unsigned int* n_long,
                      unsigned long long* stats, LongQueue q, const int32_t* hv, int32_t* tv, int which,
-                     int32_t* item_state, cudaStream_t s) {
+                     int32_t* item_state, int32_t* pool, unsigned long long* pool_top, unsigned long long pool_cap,
+                     cudaStream_t s) {
   if (which != 2) {  // short polygons (and with which == 0 the list of the long ones)
     k_classify<<<grid_for(Pcap, 256), 256, 0, s>>>(off, v, Pp, item_of, items, n_items, long_list, n_long, stats, hv,
                                                    tv, which == 0, item_state);
@@ -2434,7 +2486,7 @@ void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, in
   }
   if (which == 1) return;
   k_classify_long<<<kNumSMs * 4, 256, 0, s>>>(off, v, long_list, n_long, item_of, items, n_items, stats, q, hv, tv,
-                                              item_state);
+                                              item_state, pool, pool_top, pool_cap);
   note_launch(1);
 }
 
@@ -2468,12 +2520,18 @@ void launch_repair_tips_long(const RepairArgs& a, cudaStream_t s) {
     const char* e = getenv("TERMESH_SEG_BLOCKS");
     env_blk = (e && *e) ? atoi(e) : 0;
   }
+  static int smem_max_l = -1;
+  if (smem_max_l < 0) {  // testing hook: TERMESH_SEG_SMEM_MAXL sends shorter items to the global-memory mode
+    const char* e = getenv("TERMESH_SEG_SMEM_MAXL");
+    smem_max_l = (e && *e) ? atoi(e) : kSegMaxL;
+    if (smem_max_l > kSegMaxL) smem_max_l = kSegMaxL;
+  }
   long long nblk = env_blk > 0 ? env_blk : 24 * (a.T / 20000000 + 1);
   if (nblk > kNumSMs) nblk = kNumSMs;
   k_repair_tips_seg<<<(int)nblk, 32 * kSegWarps, smem, s>>>(c, a.items, a.off, a.v, a.item_list, a.item_n,
                                                            a.item_state, a.item_depth, a.item_slots, a.stats, a.q,
                                                            a.dbg,
-                                                           (unsigned int)trace_qi, seg_cap);
+                                                           (unsigned int)trace_qi, seg_cap, smem_max_l);
   note_launch(1);
 }
 

@@ -296,6 +296,37 @@ def test_pool_overflow_retry_is_exact(cuda):
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
+def test_long_items_global_memory_mode(cuda):
+    """TERMESH_SEG_SMEM_MAXL=128 sends every long item over 128 vertices to the
+    long-item kernel's global-memory mode (used for real above 8192 vertices,
+    the hull-sliver polygon at 100M points); results must not change -- also
+    whole path at 200k anisotropic points against the oracle."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, 'tests'); sys.path.insert(0, '.')\n"
+        "from conftest import load_case\n"
+        "import oracle\n"
+        "import paper_2204_05438_b200 as tm\n"
+        "for name in ('aniso2k_s1', 'aniso2k_s2', 'aniso2k_s7', 'clust5k_s0', 'u1k_unit'):\n"
+        "    tri, g = load_case(name)\n"
+        "    f, st = tm.execute(tri)\n"
+        "    off, v = f.csr()\n"
+        "    assert np.array_equal(off, g['final_off']) and np.array_equal(v, g['final_verts']), name\n"
+        "tri = tm.generate_anisotropic_delaunay(200_000, seed=3)\n"
+        "f, st = tm.execute(tri)\n"
+        "ref = oracle.execute(tri)\n"
+        "off, v = f.csr()\n"
+        "assert np.array_equal(off, ref['final'][0]) and np.array_equal(v, ref['final'][1])\n"
+        "assert st.reparation_rounds == ref['stats']['rounds']\n"
+        "print('ok', st.reparation_rounds)\n")
+    env = dict(os.environ, TERMESH_SEG_SMEM_MAXL="128")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
 def test_shuffled_triangle_order_full_table_rerun(cuda):
     """A triangle order without Qhull's locality: block-local matching pairs
     almost nothing, the whole path's half-size twin table overflows, and the
