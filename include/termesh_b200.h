@@ -230,6 +230,18 @@ int tm_polygon_areas(tm_ctx *ctx, const int64_t *d_offsets, const int32_t *d_ver
 int tm_canonicalize(tm_ctx *ctx, const int64_t *d_offsets, const int32_t *d_verts, int64_t n_polys,
                     int64_t n_vertices, int64_t *d_offsets_out, int32_t *d_verts_out, void *stream);
 
+/* ---------------------------------------------------------------- GPU Delaunay (input generation)
+ * Delaunay triangulation of n points inside box = {x0, y0, x1, y1}, which
+ * must lie on the 2^-53 grid of [0, 1) (numpy uniform draws) for the exact
+ * predicates (the reference uses Qhull,
+ * io_formats.py:351-388).  Writes the CCW triangles whose smallest-index
+ * vertex has a certified star (d_tri int32[3 * cap_tris]) and lists the points
+ * whose star could not be certified locally (d_open int32[n]: the hull
+ * region, triangulated by the caller).  *n_degenerate counts cocircular /
+ * collinear ties (no unique triangulation). */
+int tm_delaunay(tm_ctx *ctx, const double *d_xy, int64_t n, const double *box, int32_t *d_tri, int64_t cap_tris,
+                int64_t *n_tris, int32_t *d_open, int64_t *n_open, int64_t *n_degenerate, void *stream);
+
 /* ---------------------------------------------------------------- multi-GPU exchange
  * One NCCL communicator per rank (one process per GPU).  Rank 0 makes the
  * unique id (tm_comm_id_bytes() bytes), the host broadcasts it, every rank

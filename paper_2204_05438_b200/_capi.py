@@ -84,6 +84,8 @@ def lib():
         L.tm_polygon_stats.argtypes = [_P, _P, _P, _I64, _I64, _P, _P, _P, _PI64, _PI64, _PI64, _P]
         L.tm_polygon_areas.argtypes = [_P, _P, _P, _I64, _P, _P, _P]
         L.tm_canonicalize.argtypes = [_P, _P, _P, _I64, _I64, _P, _P, _P]
+        L.tm_delaunay.argtypes = [_P, _P, _I64, _P, _P, _I64, _PI64, _P, _PI64, _PI64, _P]
+        L.tm_delaunay.restype = _I
         # multi-GPU exchange (tm_comm.cu; NCCL bound at run time)
         L.tm_comm_id_bytes.restype = _I
         L.tm_comm_unique_id.argtypes = [_P]
@@ -131,7 +133,7 @@ def exported_symbols():
             "tm_pack_frontier",
             "tm_traverse", "tm_repair", "tm_mesh_to_polygons_host", "tm_mesh_to_polygons", "tm_resume_pinch",
             "tm_check_trivertex", "tm_polygon_stats", "tm_polygon_areas", "tm_canonicalize",
-            "tm_comm_id_bytes", "tm_comm_unique_id", "tm_comm_init", "tm_comm_allgather", "tm_comm_destroy",
+            "tm_delaunay", "tm_comm_id_bytes", "tm_comm_unique_id", "tm_comm_init", "tm_comm_allgather", "tm_comm_destroy",
             "tm_comm_last_error", "tm_format_double", "tm_file_read", "tm_file_status", "tm_file_copy", "tm_file_close",
             "tm_write_polymesh", "tm_write_triangle_file")
 

@@ -77,6 +77,9 @@ struct Counters {
   unsigned long long post_extra, post_edges;
   unsigned int post_nlong, post_pad;
   int64_t post_unique, post_nb;
+  // tm_delaunay: cell count, point count, triangle total, open / degenerate stars
+  int64_t dl_ncell, dl_n, dl_ntri;
+  unsigned int dl_open, dl_degen;
 };
 
 constexpr int kUploadChunks = 8;  // triangle upload chunks of tm_mesh_to_polygons_host
@@ -144,6 +147,8 @@ struct tm_ctx {
   Buf xy, tri, tri32, hw, max_edge, seed, tv, off0, v0, fin_off, fin_v, hw_snap, hv;
   // tm_post.cu scratch (validation, analytics, canonical form)
   Buf pbits, pflag, ptable, pstamp, ptip, prep, plong, prot, pbucket, porder, phist, pstart, pcursor, plen, ptiles;
+  // tm_delaunay scratch
+  Buf dcell, dhist, dstart, dcursor, dids, dsxy, dcnt, doff;
   unsigned long long pstamp_clean = 0;  // allocation generation of the all-INT_MAX stamp buffer
   cudaStream_t gstream = nullptr;
   cudaStream_t aux = nullptr;                            // long repair items run beside the short ones
@@ -661,7 +666,8 @@ void tm_ctx_destroy(tm_ctx* ctx) {
                  &ctx->off0, &ctx->v0, &ctx->fin_off, &ctx->fin_v, &ctx->hw_snap, &ctx->hv,
                  &ctx->lbscan, &ctx->pbits, &ctx->pflag, &ctx->ptable, &ctx->pstamp, &ctx->ptip, &ctx->prep,
                  &ctx->plong, &ctx->prot, &ctx->pbucket, &ctx->porder, &ctx->phist, &ctx->pstart, &ctx->pcursor,
-                 &ctx->plen, &ctx->ptiles};
+                 &ctx->plen, &ctx->ptiles, &ctx->dcell, &ctx->dhist, &ctx->dstart, &ctx->dcursor, &ctx->dids,
+                 &ctx->dsxy, &ctx->dcnt, &ctx->doff};
   for (Buf* b : bufs) b->release();
   if (ctx->h_reset) cudaFreeHost(ctx->h_reset);
   for (auto& e : ctx->ev)
@@ -1293,6 +1299,59 @@ int tm_canonicalize(tm_ctx* ctx, const int64_t* d_off, const int32_t* d_v, int64
   CK(cudaGetLastError());
   Counters h;
   return finish(ctx, s, &h);
+}
+
+// ---------------------------------------------------------------- GPU Delaunay (tm_delaunay.cu)
+int tm_delaunay(tm_ctx* ctx, const double* d_xy, int64_t n, const double* box, int32_t* d_tri, int64_t cap_tris,
+                int64_t* n_tris, int32_t* d_open, int64_t* n_open, int64_t* n_degenerate, void* stream) {
+  if (!ctx || !box || !n_tris || !n_open || n < 0 || n >= (int64_t)0x7FFFFFFF) return TM_ERR_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = init_counters(ctx);
+  if (rc || (rc = enqueue_reset(ctx, s))) return rc;
+  Counters* dc = dc_of(ctx);
+  const double x0 = box[0], y0 = box[1], x1 = box[2], y1 = box[3];
+  if (!(x1 > x0 && y1 > y0)) return set_err(ctx, TM_ERR_ARGUMENT, "empty box");
+  int64_t G = 1;
+  while ((G + 1) * (G + 1) * 2 <= n) G++;  // ~2 points per cell
+  if (G > 46000) G = 46000;
+  const int64_t nc = G * G, nn = n > 0 ? n : 1;
+  ENSURE(dcell, nn * sizeof(int32_t));
+  ENSURE(dhist, (nc + 2) * sizeof(int64_t));
+  ENSURE(dstart, (nc + 2) * sizeof(int64_t));
+  ENSURE(dcursor, (nc + 2) * sizeof(int64_t));
+  ENSURE(dids, nn * sizeof(int32_t));
+  ENSURE(dsxy, 2 * nn * sizeof(double));
+  ENSURE(dcnt, (nn + 1) * sizeof(int64_t));
+  ENSURE(doff, (nn + 1) * sizeof(int64_t));
+  ENSURE(lbscan, scan_lookback_bytes(nc > nn ? nc : nn));
+  int64_t* hp = ctx->h_pin;
+  hp[0] = nc;
+  hp[1] = n;
+  CK(cudaMemcpyAsync(&dc->dl_ncell, hp, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  launch_delaunay_cells(d_xy, n, x0, y0, x1, y1, (int)G, ctx->dcell.as<int32_t>(),
+                        ctx->dhist.as<unsigned long long>(), s);
+  launch_scan_lookback(ctx->dhist.as<int64_t>(), nullptr, ctx->dstart.as<int64_t>(), nullptr, &dc->dl_ncell, nc,
+                       ctx->lbscan.p, s);
+  launch_delaunay_scatter(d_xy, n, (int)G, ctx->dcell.as<int32_t>(), ctx->dstart.as<int64_t>(),
+                          ctx->dcursor.as<unsigned long long>(), ctx->dids.as<int32_t>(), ctx->dsxy.as<double>(), s);
+  launch_delaunay_stars(ctx->dstart.as<int64_t>(), ctx->dids.as<int32_t>(), ctx->dsxy.as<double>(), n, x0, y0, x1, y1,
+                        (int)G, 0, ctx->dcnt.as<int64_t>(), nullptr, nullptr, d_open, &dc->dl_open, &dc->dl_degen, s);
+  launch_scan_lookback(ctx->dcnt.as<int64_t>(), nullptr, ctx->doff.as<int64_t>(), nullptr, &dc->dl_n, nn,
+                       ctx->lbscan.p, s, &dc->dl_ntri);
+  Counters h;
+  if ((rc = finish(ctx, s, &h))) return rc;
+  *n_tris = h.dl_ntri;
+  *n_open = h.dl_open;
+  if (n_degenerate) *n_degenerate = h.dl_degen;
+  if (h.dl_ntri > cap_tris)
+    return set_err(ctx, TM_ERR_CAPACITY, "triangle capacity %lld below %lld", (long long)cap_tris,
+                   (long long)h.dl_ntri);
+  launch_delaunay_stars(ctx->dstart.as<int64_t>(), ctx->dids.as<int32_t>(), ctx->dsxy.as<double>(), n, x0, y0, x1, y1,
+                        (int)G, 1, ctx->dcnt.as<int64_t>(), ctx->doff.as<int64_t>(), d_tri, nullptr, nullptr, nullptr,
+                        s);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  return TM_OK;
 }
 
 }  // extern "C"

@@ -159,4 +159,14 @@ void launch_canon_lengths(const int32_t* order, int64_t P, const int64_t* off, i
 void launch_canon_write(const int32_t* order, int64_t P, const int64_t* off, const int32_t* v, const int32_t* rot,
                         const int64_t* off_out, int32_t* v_out, cudaStream_t s);
 
+// tm_delaunay.cu (GPU Delaunay input generation)
+void launch_delaunay_cells(const double* xy, int64_t n, double x0, double y0, double x1, double y1, int G,
+                           int32_t* cell, unsigned long long* hist, cudaStream_t s);
+void launch_delaunay_scatter(const double* xy, int64_t n, int G, const int32_t* cell, const int64_t* start,
+                             unsigned long long* cursor, int32_t* ids, double* sxy, cudaStream_t s);
+void launch_delaunay_stars(const int64_t* start, const int32_t* ids, const double* sxy, int64_t n, double x0,
+                           double y0, double x1, double y1, int G, int mode, int64_t* cnt, const int64_t* off,
+                           int32_t* tri, int32_t* open_list, unsigned int* n_open, unsigned int* n_degenerate,
+                           cudaStream_t s);
+
 }  // namespace tmb
