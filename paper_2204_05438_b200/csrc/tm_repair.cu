@@ -1440,7 +1440,10 @@ constexpr int kSegMaxL = 8192;   // longer items keep their per-item arrays in g
 // the 16-bit piece lengths and nexttip entries valid.
 constexpr int kSegMaxG = 21760;
 constexpr int kGPairCap = 65536;  // >= 2 kSegMaxG, power of two
-constexpr long long kGStride = (long long)kSegMaxG + 3 * (kSegMaxG / 32 + 1) + kGPairCap + (kSegMaxG + 1) / 2 + 64;
+constexpr int kGRec = 8192;       // piece records per round list (very long items)
+constexpr int kGSegCap = 262144;  // segment arena (very long items)
+constexpr long long kGStride = (long long)kSegMaxG + 3 * (kSegMaxG / 32 + 1) + kGPairCap + (kSegMaxG + 1) / 2 + 16 +
+                               2 * (long long)kGRec + 2 * (long long)kGRec * 5 + 2 * (long long)kGSegCap + 64;
 constexpr int kPairCap = 16384;  // pair-map slots (>= 2 kSegMaxL); reused as leaf hash sets
 constexpr int kSegRec = 1024;    // piece records per round list
 constexpr int kSegTips = 512;    // precomputed tips per item
@@ -1787,9 +1790,9 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
   int32_t* const sP = reinterpret_cast<int32_t*>(smem_raw);
   uint32_t* const stipbits = reinterpret_cast<uint32_t*>(sP + kSegMaxL);
   int32_t* const spmap = reinterpret_cast<int32_t*>(stipbits + kSegMaxL / 32);
-  SPiece* recs = reinterpret_cast<SPiece*>(spmap + kPairCap);  // [2][kSegRec]
-  int32_t* s_out = reinterpret_cast<int32_t*>(recs + 2 * kSegRec);
-  int32_t* fans = s_out + kSegRec;
+  SPiece* const srecs = reinterpret_cast<SPiece*>(spmap + kPairCap);  // [2][kSegRec]
+  int32_t* const ss_out = reinterpret_cast<int32_t*>(srecs + 2 * kSegRec);
+  int32_t* fans = ss_out + kSegRec;
   int32_t* tipv = fans + 2 * kSegWarps * kFanCap;  // tip vertex (or -1 when its info is unusable)
   int32_t* tipb = tipv + kSegTips;                 // barrier vertex
   SplitInfo* tipinfo = reinterpret_cast<SplitInfo*>(tipb + kSegTips);
@@ -1804,8 +1807,14 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
   uint16_t* nexttip;
   __shared__ long long s_gscr;  // pool offset of the block's global region (-1: not allocated)
   if (threadIdx.x == 0) s_gscr = -1;
-  int* tlist = tipdeg + kSegTips;                              // tipped records of the round
-  Seg* segs = reinterpret_cast<Seg*>(tlist + kSegRec);
+  int* const stlist = tipdeg + kSegTips;                       // tipped records of the round
+  Seg* const ssegs = reinterpret_cast<Seg*>(stlist + kSegRec);
+  // piece records, their output slots, the round's tipped records and the
+  // segment arena: shared memory, or the block's pool region (very long items)
+  SPiece* recs;
+  int32_t *s_out, *tlist;
+  Seg* segs;
+  int rec_cap, scap;
   // s_ntb: tipped-record count of the next round, double-buffered by round parity
   // so the reset of one round never races with the previous round's readers
   __shared__ int s_ntip, s_ntouch, s_stop, s_fail, s_ntb[2], s_need, s_tot;
@@ -1855,6 +1864,12 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
       nextw = tiprank + kSegMaxG / 32 + 1;
       pmap = nextw + kSegMaxG / 32 + 1;
       nexttip = reinterpret_cast<uint16_t*>(pmap + kGPairCap);
+      s_out = reinterpret_cast<int32_t*>(nexttip) + (kSegMaxG + 1) / 2 + 16;
+      tlist = s_out + kGRec;
+      recs = reinterpret_cast<SPiece*>(tlist + kGRec);  // [2][kGRec]
+      segs = reinterpret_cast<Seg*>(recs + 2 * kGRec);
+      rec_cap = kGRec;
+      scap = kGSegCap;
     } else {
       P = sP;
       tipbits = stipbits;
@@ -1862,6 +1877,12 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
       nextw = snextw;
       pmap = spmap;
       nexttip = snexttip;
+      recs = srecs;
+      s_out = ss_out;
+      tlist = stlist;
+      segs = ssegs;
+      rec_cap = kSegRec;
+      scap = seg_cap;
     }
     int pcap = 64;
     while (pcap < 2 * L) pcap <<= 1;
@@ -1967,8 +1988,8 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
         bad = true;
         break;
       }
-      SPiece* in = recs + cur * kSegRec;
-      SPiece* out = recs + (cur ^ 1) * kSegRec;
+      SPiece* in = recs + cur * rec_cap;
+      SPiece* out = recs + (cur ^ 1) * rec_cap;
       // output slot of every input record (prefix over tip flags) and the
       // segments the round may need, warp 0
       if (wib == 0) {
@@ -1995,8 +2016,8 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
       // Segments are bump-allocated in one half of the arena; when a round
       // would overflow it, the live pieces are first compacted into the other
       // half, so the arena only ever has to hold the live pieces.
-      const int half = seg_cap / 2;
-      if (n + ntips > kSegRec) { spill = true; break; }  // uniform
+      const int half = scap / 2;
+      if (n + ntips > rec_cap) { spill = true; break; }  // uniform
       if (s_stop + s_need > half) {
         const int nb = hbase == 0 ? half : 0;
         __syncthreads();
@@ -2140,7 +2161,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
       continue;
     }
     // leaves (or the pieces before an unsplit round) -> global pool
-    const SPiece* fin = recs + cur * kSegRec;
+    const SPiece* fin = recs + cur * rec_cap;
     if (threadIdx.x == 0) {
       int tot = 0;
       for (int r = 0; r < n; r++) tot += fin[r].len;

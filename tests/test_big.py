@@ -1,20 +1,102 @@
 """Full-size parity (BASELINE.json configs 3 and 5): 10M uniform and 10M
-clustered points, GPU output vs the CPU oracle, raw polygon order + rotation,
-post-repair frontier and repair stats bit-exact.  Opt-in (TERMESH_BIG=1):
-generating each input with Qhull takes minutes."""
+clustered points.
+
+Default (-m gpu): the GPU path's labels, traversal output and final CSR
+against the hashes the Python reference itself produced for the same inputs
+(tests/golden/hashes.json, tests/golden/make_golden.py --big; ~21 / ~10 min of
+reference CPU time each), and 10 graph replays of the whole path.  The inputs
+are regenerated with scipy on the box (~1.5 min each) and their hashes checked
+first.  Opt-in (TERMESH_BIG=1): the same against the CPU oracle incl. the
+post-repair frontier, and a 40-replay soak."""
+import hashlib
 import os
 
 import numpy as np
 import pytest
 
 import oracle
+from conftest import load_hashes
 
-pytestmark = [pytest.mark.gpu, pytest.mark.slow,
-              pytest.mark.skipif(not os.environ.get("TERMESH_BIG"), reason="set TERMESH_BIG=1 (10M meshes)")]
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+big_only = pytest.mark.skipif(not os.environ.get("TERMESH_BIG"), reason="set TERMESH_BIG=1 (oracle at 10M)")
+KEYS = {"u10m": "u10m_unit", "c10m": "c10m_clustered"}
+
+
+def h16(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]
 
 
 @pytest.mark.parametrize("workload", ["u10m", "c10m"])
-def test_10m_parity(cuda, workload):
+def test_10m_matches_reference_hashes(cuda, workload):
+    import bench
+    import paper_2204_05438_b200 as tm
+    ref = load_hashes()[KEYS[workload]]
+    tri = bench.load_mesh(workload, 0)
+    assert h16(tri.vertices) == ref["input"]["vertices"] and h16(tri.triangles) == ref["input"]["triangles"], \
+        "input differs from the reference's (scipy/Qhull version?)"
+    lab = tm.label_all(tri, check=False)
+    assert h16(lab.max_edge) == ref["max_edge"] and h16(lab.seed) == ref["seed"]
+    assert h16(lab.frontier) == ref["frontier_pre"]
+    m0 = tm.build_polygon_mesh(tri, lab)
+    off0, v0 = m0.csr()
+    assert h16(off0) == ref["mesh0_off"] and h16(v0) == ref["mesh0_verts"]
+    info = {}
+    fin = tm.repair_all(tri, lab, m0, stats_out=info)
+    off, v = fin.csr()
+    assert h16(off) == ref["final_off"] and h16(v) == ref["final_verts"]
+    assert h16(lab.frontier) == ref["frontier_post"]
+    assert [info[k] for k in ("rounds", "splits", "initial_tips", "unrepaired")] == ref["stats"]
+    c_off, c_v = tm.canonicalize(fin, n_vertices=tri.n_vertices).csr()
+    assert h16(c_off) == ref["canon_off"] and h16(c_v) == ref["canon_verts"]
+
+
+@pytest.mark.parametrize("workload,replays", [("u10m", 10)])
+def test_10m_whole_path_replays(cuda, workload, replays):
+    """Graph replays of the whole device path at 10M, every one equal to the
+    reference's final CSR (a shared-memory 64-bit CAS race once corrupted ~1
+    step in 50 here while every 1M check passed)."""
+    _replays(cuda, workload, replays)
+
+
+@big_only
+@pytest.mark.parametrize("workload", ["u10m"])
+def test_10m_whole_path_replays_soak(cuda, workload):
+    _replays(cuda, workload, 40)
+
+
+def _replays(cuda, workload, replays):
+    import ctypes
+    import torch
+    import bench
+    from paper_2204_05438_b200 import _capi
+    ref = load_hashes()[KEYS[workload]]
+    tri = bench.load_mesh(workload, 0)
+    n, T = tri.n_vertices, tri.n_triangles
+    xy = torch.from_numpy(tri.vertices).to(cuda)
+    tr = torch.from_numpy(tri.triangles).to(cuda)
+    off = torch.empty(T + 1, dtype=torch.int64, device=cuda)
+    v = torch.empty(3 * T, dtype=torch.int32, device=cuda)
+    ctx = _capi.context(cuda)
+    npol, nsl = ctypes.c_int64(), ctypes.c_int64()
+    st = (ctypes.c_int64 * _capi.NUM_STATS)()
+    first = None
+    for k in range(replays):
+        rc = _capi.lib().tm_mesh_to_polygons(ctx.ptr, _capi.ptr(xy), n, _capi.ptr(tr), 64, T, 0, _capi.ptr(off),
+                                             _capi.ptr(v), T, 3 * T, ctypes.byref(npol), ctypes.byref(nsl), st,
+                                             _capi.stream_ptr(cuda))
+        ctx.check(rc)
+        P, F = npol.value, nsl.value
+        if first is None:
+            o, vv = off[: P + 1].cpu().numpy(), v[:F].cpu().numpy().astype(np.int64)
+            assert h16(o) == ref["final_off"] and h16(vv) == ref["final_verts"]
+            first = (off[: P + 1].clone(), v[:F].clone())
+        else:
+            assert torch.equal(off[: P + 1], first[0]) and torch.equal(v[:F], first[1]), k
+
+
+@big_only
+@pytest.mark.parametrize("workload", ["u10m", "c10m"])
+def test_10m_parity_vs_oracle(cuda, workload):
     import bench
     import paper_2204_05438_b200 as tm
     tri = bench.load_mesh(workload, 0)
@@ -32,35 +114,3 @@ def test_10m_parity(cuda, workload):
     assert np.array_equal(lab.frontier, ref["labels"].frontier)
     for k in ("rounds", "splits", "initial_tips", "unrepaired"):
         assert info[k] == ref["stats"][k], k
-    print(workload, "T", tri.n_triangles, "polygons", off.size - 1, "stats", ref["stats"])
-
-
-@pytest.mark.parametrize("workload", ["u10m"])
-def test_10m_whole_path_replays_match_oracle(cuda, workload):
-    """40 graph replays of the whole device path at 10M, every one equal to the
-    oracle's final CSR (a shared-memory 64-bit CAS race once corrupted ~1 step in
-    50 here while every 1M check passed)."""
-    import ctypes
-    import torch
-    import bench
-    from paper_2204_05438_b200 import _capi
-    tri = bench.load_mesh(workload, 0)
-    ref = oracle.execute(tri)
-    n, T = tri.n_vertices, tri.n_triangles
-    xy = torch.from_numpy(tri.vertices).to(cuda)
-    tr = torch.from_numpy(tri.triangles).to(cuda)
-    off = torch.empty(T + 1, dtype=torch.int64, device=cuda)
-    v = torch.empty(3 * T, dtype=torch.int32, device=cuda)
-    ctx = _capi.context(cuda)
-    npol, nsl = ctypes.c_int64(), ctypes.c_int64()
-    st = (ctypes.c_int64 * _capi.NUM_STATS)()
-    ref_off = torch.from_numpy(ref["final"][0]).to(cuda)
-    ref_v = torch.from_numpy(ref["final"][1].astype(np.int32)).to(cuda)
-    for k in range(40):
-        rc = _capi.lib().tm_mesh_to_polygons(ctx.ptr, _capi.ptr(xy), n, _capi.ptr(tr), 64, T, 0, _capi.ptr(off),
-                                             _capi.ptr(v), T, 3 * T, ctypes.byref(npol), ctypes.byref(nsl), st,
-                                             _capi.stream_ptr(cuda))
-        ctx.check(rc)
-        P, F = npol.value, nsl.value
-        assert P + 1 == ref_off.numel() and F == ref_v.numel(), k
-        assert torch.equal(off[: P + 1], ref_off) and torch.equal(v[:F], ref_v), k
