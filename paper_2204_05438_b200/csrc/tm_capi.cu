@@ -149,6 +149,9 @@ struct tm_ctx {
   Buf pbits, pflag, ptable, pstamp, ptip, prep, plong, prot, pbucket, porder, phist, pstart, pcursor, plen, ptiles;
   // tm_delaunay scratch
   Buf dcell, dhist, dstart, dcursor, dids, dsxy, dcnt, doff;
+  // fp32 copy of the coordinates for the LabelMax prefilter (TERMESH_NO_XY32=1 disables it)
+  Buf xy32;
+  int use_xy32 = 1;
   unsigned long long pstamp_clean = 0;  // allocation generation of the all-INT_MAX stamp buffer
   cudaStream_t gstream = nullptr;
   cudaStream_t aux = nullptr;                            // long repair items run beside the short ones
@@ -356,6 +359,7 @@ static int prepare(tm_ctx* ctx, int64_t T, int64_t n = -1) {
   if (!ctx->ev_cls) CK(cudaEventCreateWithFlags(&ctx->ev_cls, cudaEventDisableTiming));
   int64_t Tn = T > 0 ? T : 1;
   if (n >= 0) ENSURE(slots, hash_bytes(n, Tn, std::min(ctx->table_shrink, ctx->label_shrink)));
+  if (n >= 0 && ctx->use_xy32) ENSURE(xy32, (n > 0 ? n : 1) * 2 * sizeof(float));
   ENSURE(seeds, Tn * sizeof(int32_t));
   ENSURE(start, Tn * sizeof(int32_t));
   ENSURE(len, (Tn + 1) * sizeof(int64_t));
@@ -418,7 +422,7 @@ static int enqueue_label(tm_ctx* ctx, const double* d_xy, int64_t n, const void*
   if (!ctx->label_a_external) {
     SegTimer t_(ctx, S_LABEL_A, s);
     launch_label_a(d_xy, n, d_tri, tri_bits == 64, T, check, d_tri32, d_hw, d_me, d_seed, d_tv, ctx->slots.p,
-                   &dc->st, s, shrink, &dc->table_ovf);
+                   &dc->st, s, shrink, &dc->table_ovf, ctx->use_xy32 ? ctx->xy32.as<float>() : nullptr);
   }
   if (lt) CK(cudaEventRecord(ctx->lev[1], s));
   {
@@ -651,6 +655,8 @@ int tm_ctx_create(tm_ctx** out) {
   *out = new tm_ctx();
   const char* g = getenv("TERMESH_NO_GRAPH");
   if (g && *g && *g != '0') (*out)->use_graph = 0;
+  const char* x32 = getenv("TERMESH_NO_XY32");  // A/B switch
+  if (x32 && *x32 && *x32 != '0') (*out)->use_xy32 = 0;
   const char* ts = getenv("TERMESH_TABLE_SHRINK");  // testing hook: start with a 2^-s table (overflow/growth path)
   if (ts && *ts) (*out)->table_shrink = atoi(ts);
   return TM_OK;
@@ -667,7 +673,7 @@ void tm_ctx_destroy(tm_ctx* ctx) {
                  &ctx->lbscan, &ctx->pbits, &ctx->pflag, &ctx->ptable, &ctx->pstamp, &ctx->ptip, &ctx->prep,
                  &ctx->plong, &ctx->prot, &ctx->pbucket, &ctx->porder, &ctx->phist, &ctx->pstart, &ctx->pcursor,
                  &ctx->plen, &ctx->ptiles, &ctx->dcell, &ctx->dhist, &ctx->dstart, &ctx->dcursor, &ctx->dids,
-                 &ctx->dsxy, &ctx->dcnt, &ctx->doff};
+                 &ctx->dsxy, &ctx->dcnt, &ctx->doff, &ctx->xy32};
   for (Buf* b : bufs) b->release();
   if (ctx->h_reset) cudaFreeHost(ctx->h_reset);
   for (auto& e : ctx->ev)
@@ -1140,6 +1146,8 @@ int tm_mesh_to_polygons_host(tm_ctx* ctx, const double* h_xy, int64_t n, const i
   if ((rc = enqueue_reset(ctx, s))) return rc;
   const int shrink = check && ctx->table_shrink > 0 ? 0 : ctx->table_shrink;
   launch_label_a_prepare(n, T, nullptr, ctx->slots.p, s, shrink);
+  float* xy32 = (ctx->use_xy32 && !check) ? ctx->xy32.as<float>() : nullptr;
+  if (xy32) launch_xy32(ctx->xy.as<double>(), n, xy32, s);
   CK(cudaEventRecord(ctx->chunk_ev[0], s));
   CK(cudaStreamWaitEvent(ctx->cstream, ctx->chunk_ev[0], 0));  // table reset before any chunk's pass A
   for (int k = 0; k < kUploadChunks; k++) {
@@ -1151,7 +1159,7 @@ int tm_mesh_to_polygons_host(tm_ctx* ctx, const double* h_xy, int64_t n, const i
     CK(cudaStreamWaitEvent(s, ctx->chunk_ev[k], 0));
     launch_label_a_range(ctx->xy.as<double>(), n, ctx->tri.p, 1, T, t0, t1, check, ctx->tri32.as<int32_t>(),
                          ctx->hw.as<int32_t>(), ctx->max_edge.as<int8_t>(), ctx->seed.as<uint8_t>(), nullptr,
-                         ctx->slots.p, &dc_of(ctx)->st, s, shrink, &dc_of(ctx)->table_ovf);
+                         ctx->slots.p, &dc_of(ctx)->st, s, shrink, &dc_of(ctx)->table_ovf, xy32);
   }
   CK(cudaGetLastError());
   ctx->label_a_external = true;

@@ -13,16 +13,19 @@ struct DevStatus;
 size_t hash_bytes(int64_t n, int64_t T, int shrink = 0);  // bytes of the table at scale 2^-min(shrink, 0)
 // counts kernels of this library launched (bench.py's gpu_launches)
 void note_launch(int k);
+// xy32 (nullable): scratch float2[n] for the fp32 LabelMax prefilter (not used with check)
 void launch_label_a(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int check,
                     int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed, int32_t* tv, void* table,
-                    DevStatus* st, cudaStream_t s, int shrink = 0, unsigned int* ovf = nullptr);
+                    DevStatus* st, cudaStream_t s, int shrink = 0, unsigned int* ovf = nullptr,
+                    float* xy32 = nullptr);
+void launch_xy32(const double* xy, int64_t n, float* xy32, cudaStream_t s);
 // pass A split for copy overlap: prepare (table/trivertex init) once, then triangle ranges
 // shrink = 1: half-size twin table (whole path; overflow sets *ovf, the host reruns at full size)
 void launch_label_a_prepare(int64_t n, int64_t T, int32_t* tv, void* table, cudaStream_t s, int shrink = 0);
 void launch_label_a_range(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int64_t t_begin,
                           int64_t t_end, int check, int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed,
                           int32_t* tv, void* table, DevStatus* st, cudaStream_t s, int shrink = 0,
-                          unsigned int* ovf = nullptr);
+                          unsigned int* ovf = nullptr, const float* xy32 = nullptr);
 void launch_label_b(const int32_t* tri32, int64_t n, int64_t T, int32_t* hw, const int8_t* max_edge, uint8_t* seed,
                     int32_t* tv, void* table, int check, DevStatus* st, cudaStream_t s, int shrink = 0);
 void launch_relabel(const int8_t* max_edge, int64_t T, int32_t* hw, uint8_t* seed, cudaStream_t s);

@@ -170,6 +170,52 @@ __device__ __forceinline__ int argmax3(double l0, double l1, double l2) {
   return m;
 }
 
+// ---- single-precision prefilter of LabelMax.  The three squared lengths
+// are first computed from an fp32 copy of the coordinates (8 bytes per vertex
+// instead of 16: the copy of a 10M-point mesh stays mostly in L2), each with a
+// bound on its distance to the exact squared length; when the largest one
+// exceeds every other by more than their bounds, the fp64 argmax (any
+// rounding of the reference's dx*dx + dy*dy) has the same winner.  Otherwise
+// (near-ties, exact ties, non-finite values) the fp64 coordinates are read and
+// the reference formula decides.
+//   x32 = x(1+e), |e| <= u = 2^-24; dx32 = (x32a - x32b)(1+e'):
+//   |dx32 - dx| <= u (|xa| + |xb| + |dx|)(1 + u) =: d, |dx32^2 - dx^2| <= d (2|dx| + d),
+//   and two more roundings (square, sum) of at most u each.
+struct Sq32 {
+  float L, E;
+};
+__device__ __forceinline__ Sq32 sqlen32(float2 p, float2 q) {
+  const float u = 5.9604645e-08f;  // 2^-24
+  const float dx = __fsub_rn(p.x, q.x), dy = __fsub_rn(p.y, q.y);
+  const float L = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+  const float ax = fabsf(p.x) + fabsf(q.x) + fabsf(dx), ay = fabsf(p.y) + fabsf(q.y) + fabsf(dy);
+  const float dxe = 1.01f * u * ax, dye = 1.01f * u * ay;  // |dx32 - dx|, |dy32 - dy| bounds (with slack)
+  // 2 (safety) x [first-order + second-order + the roundings of the square and the sum]
+  const float E = 2.0f * (dxe * (2.0f * fabsf(dx) + dxe) + dye * (2.0f * fabsf(dy) + dye) + 3.0f * u * L) + 1e-37f;
+  return Sq32{L, E};
+}
+// winner of numpy's first-max argmax when the fp32 bounds separate it, else -1
+__device__ __forceinline__ int argmax3_32(float2 a, float2 b, float2 c) {
+  const Sq32 l0 = sqlen32(b, c), l1 = sqlen32(c, a), l2 = sqlen32(a, b);
+  if (!(isfinite(l0.L + l0.E) && isfinite(l1.L + l1.E) && isfinite(l2.L + l2.E))) return -1;
+  int m = 0;
+  Sq32 best = l0;
+  if (l1.L > best.L) { best = l1; m = 1; }
+  if (l2.L > best.L) { best = l2; m = 2; }
+  const float lo = best.L - best.E;
+  if (m != 0 && !(lo > l0.L + l0.E)) return -1;
+  if (m != 1 && !(lo > l1.L + l1.E)) return -1;
+  if (m != 2 && !(lo > l2.L + l2.E)) return -1;
+  return m;
+}
+
+__global__ void k_xy32(const double2* __restrict__ xy, int64_t n, float2* __restrict__ xy32) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 p = xy[i];
+    xy32[i] = make_float2(__double2float_rn(p.x), __double2float_rn(p.y));
+  }
+}
+
 constexpr int kLabelThreads = 256;
 constexpr int kLabelWarps = kLabelThreads / 32;
 
@@ -228,7 +274,8 @@ __device__ __forceinline__ void label_pair(int32_t* __restrict__ hw, uint8_t* __
 // partners); then the warp's remaining ascending half-edges (origin < target)
 // go into the twin table on dense lanes.
 template <typename TI>
-__global__ void __launch_bounds__(kLabelThreads, 4) k_tri_pass(const double2* __restrict__ xy, int64_t n,
+__global__ void __launch_bounds__(kLabelThreads, 4) k_tri_pass(const double2* __restrict__ xy,
+                                                            const float2* __restrict__ xy32, int64_t n,
                                                             const TI* __restrict__ tri, int64_t t_begin,
                                                             int64_t T,
                                                             int32_t* __restrict__ tri32, int8_t* __restrict__ max_edge,
@@ -267,11 +314,16 @@ __global__ void __launch_bounds__(kLabelThreads, 4) k_tri_pass(const double2* __
           tri32[3 * t + 1] = (int32_t)b;
           tri32[3 * t + 2] = (int32_t)c;
         }
-        double2 pa = xy[a], pb = xy[b], pc = xy[c];
         // labeling.py:55-59: edge 0 joins corners 1-2, edge 1 joins 2-0, edge 2 joins 0-1
-        me0 = argmax3(sqlen(pb, pc), sqlen(pc, pa), sqlen(pa, pb));
+        me0 = -1;
+        if (xy32 != nullptr) me0 = argmax3_32(xy32[a], xy32[b], xy32[c]);
+        if (me0 < 0) {
+          const double2 pa = xy[a], pb = xy[b], pc = xy[c];
+          me0 = argmax3(sqlen(pb, pc), sqlen(pc, pa), sqlen(pa, pb));
+        }
         max_edge[t] = (int8_t)me0;
         if (check) {
+          const double2 pa = xy[a], pb = xy[b], pc = xy[c];
           // mesh_core.signed_areas (160-168), sign only, unfused
           double d = __dsub_rn(__dmul_rn(__dsub_rn(pb.x, pa.x), __dsub_rn(pc.y, pa.y)),
                                __dmul_rn(__dsub_rn(pb.y, pa.y), __dsub_rn(pc.x, pa.x)));
@@ -498,28 +550,35 @@ void launch_label_a_prepare(int64_t n, int64_t T, int32_t* tv, void* table, cuda
   }
 }
 
+void launch_xy32(const double* xy, int64_t n, float* xy32, cudaStream_t s) {
+  if (n > 0) k_xy32<<<grid_for(n, 256), 256, 0, s>>>((const double2*)xy, n, (float2*)xy32), note_launch(1);
+}
+
 void launch_label_a_range(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int64_t t_begin,
                           int64_t t_end, int check, int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed,
-                          int32_t* tv, void* table, DevStatus* st, cudaStream_t s, int shrink, unsigned int* ovf) {
+                          int32_t* tv, void* table, DevStatus* st, cudaStream_t s, int shrink, unsigned int* ovf,
+                          const float* xy32) {
   TwinTable tb = table_geometry(n, T, table, shrink, ovf);
   if (t_end > t_begin) {
     const int B = kLabelThreads;
     const int g = grid_for(t_end - t_begin, B);
     if (tri_is64)
-      k_tri_pass<int64_t><<<g, B, 0, s>>>((const double2*)xy, n, (const int64_t*)tri, t_begin, t_end, tri32,
-                                          max_edge, tb, hw, seed, tv, check, st);
+      k_tri_pass<int64_t><<<g, B, 0, s>>>((const double2*)xy, (const float2*)xy32, n, (const int64_t*)tri, t_begin,
+                                          t_end, tri32, max_edge, tb, hw, seed, tv, check, st);
     else
-      k_tri_pass<int32_t><<<g, B, 0, s>>>((const double2*)xy, n, (const int32_t*)tri, t_begin, t_end,
-                                          tri32 == tri ? nullptr : tri32, max_edge, tb, hw, seed, tv, check, st);
+      k_tri_pass<int32_t><<<g, B, 0, s>>>((const double2*)xy, (const float2*)xy32, n, (const int32_t*)tri, t_begin,
+                                          t_end, tri32 == tri ? nullptr : tri32, max_edge, tb, hw, seed, tv, check, st);
     note_launch(1);
   }
 }
 
 void launch_label_a(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int check,
                     int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed, int32_t* tv, void* table,
-                    DevStatus* st, cudaStream_t s, int shrink, unsigned int* ovf) {
+                    DevStatus* st, cudaStream_t s, int shrink, unsigned int* ovf, float* xy32) {
   launch_label_a_prepare(n, T, tv, table, s, shrink);
-  launch_label_a_range(xy, n, tri, tri_is64, T, 0, T, check, tri32, hw, max_edge, seed, tv, table, st, s, shrink, ovf);
+  if (xy32 && !check) launch_xy32(xy, n, xy32, s);
+  launch_label_a_range(xy, n, tri, tri_is64, T, 0, T, check, tri32, hw, max_edge, seed, tv, table, st, s, shrink, ovf,
+                       check ? nullptr : xy32);
 }
 
 void launch_label_b(const int32_t* tri32, int64_t n, int64_t T, int32_t* hw, const int8_t* max_edge, uint8_t* seed,
