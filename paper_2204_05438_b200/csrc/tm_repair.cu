@@ -1785,7 +1785,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
                                                                     int64_t* __restrict__ item_slots,
                                                                     unsigned long long* stats, LongQueue q,
                                                                     unsigned long long* dbg, unsigned int trace_qi,
-                                                                    int seg_cap, int smem_max_l) {
+                                                                    int seg_cap, int smem_max_l, int rec_limit) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int32_t* const sP = reinterpret_cast<int32_t*>(smem_raw);
   uint32_t* const stipbits = reinterpret_cast<uint32_t*>(sP + kSegMaxL);
@@ -1817,7 +1817,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
   int rec_cap, scap;
   // s_ntb: tipped-record count of the next round, double-buffered by round parity
   // so the reset of one round never races with the previous round's readers
-  __shared__ int s_ntip, s_ntouch, s_stop, s_fail, s_ntb[2], s_need, s_tot;
+  __shared__ int s_ntip, s_ntouch, s_stop, s_fail, s_ntb[2], s_need, s_tot, s_reloc;
   __shared__ PairMsg pmsg[kSegWarps / 2];
   __shared__ long long s_base;
   __shared__ unsigned int s_w;
@@ -1850,7 +1850,8 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
       if (threadIdx.x == 0) item_state[w] = 3;
       continue;
     }
-    if (L > smem_max_l) {  // smem_max_l = kSegMaxL (lower only as a testing hook)
+    bool gmode = L > smem_max_l;  // smem_max_l = kSegMaxL (lower only as a testing hook)
+    if (gmode) {
       if (threadIdx.x == 0 && s_gscr < 0) s_gscr = palloc(c, kGStride);
       __syncthreads();
       if (s_gscr < 0) {  // pool exhausted: the warp kernel from scratch
@@ -1881,7 +1882,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
       s_out = ss_out;
       tlist = stlist;
       segs = ssegs;
-      rec_cap = kSegRec;
+      rec_cap = rec_limit;  // kSegRec (lower only as a testing hook)
       scap = seg_cap;
     }
     int pcap = 64;
@@ -1892,7 +1893,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
     for (int k = threadIdx.x; k < kSegTouch; k += blockDim.x) tset[k] = -1;
     if (threadIdx.x == 0) { s_ntip = 0; s_ntouch = 0; s_fail = 0; s_stop = 1; }  // segs[0]: the item
     __syncthreads();
-    const SegView g{P, L, tipbits, nexttip, pmap, pcap - 1, segs};
+    SegView g{P, L, tipbits, nexttip, pmap, pcap - 1, segs};
     // tips of P (bitmap) and the pair map
     for (int k = threadIdx.x; k < L; k += blockDim.x) {
       int32_t a = P[k == 0 ? L - 1 : k - 1], y = P[k];
@@ -1982,12 +1983,75 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
     int cur = 0, n = 1, ntips = s_ntb[0], hbase = 0;
     long long depth = 0, splits = 0;
     bool bad = false, spill = false;
+    // The piece records or the segment arena outgrow shared memory (hull
+    // slivers with thousands of splits at 100M points): move the item's state
+    // to the block's pool region and continue there (uniform; false if the
+    // pool is exhausted -- the caller then spills to the warp kernel).
+    auto to_global = [&]() -> bool {
+      if (threadIdx.x == 0 && s_gscr < 0) s_gscr = palloc(c, kGStride);
+      if (threadIdx.x == 0) s_reloc = 0;
+      __syncthreads();
+      if (s_gscr < 0) return false;
+      int32_t* gP = c.pool + s_gscr;
+      uint32_t* gtb = reinterpret_cast<uint32_t*>(gP + kSegMaxG);
+      int32_t* gtr = reinterpret_cast<int32_t*>(gtb + kSegMaxG / 32 + 1);
+      int32_t* gnw = gtr + kSegMaxG / 32 + 1;
+      int32_t* gpm = gnw + kSegMaxG / 32 + 1;
+      uint16_t* gnt = reinterpret_cast<uint16_t*>(gpm + kGPairCap);
+      int32_t* gso = reinterpret_cast<int32_t*>(gnt) + (kSegMaxG + 1) / 2 + 16;
+      int32_t* gtl = gso + kGRec;
+      SPiece* grec = reinterpret_cast<SPiece*>(gtl + kGRec);
+      Seg* gsg = reinterpret_cast<Seg*>(grec + 2 * kGRec);
+      const int nw = (L + 31) / 32;
+      for (int k = threadIdx.x; k < L; k += blockDim.x) {
+        gP[k] = P[k];
+        gnt[k] = nexttip[k];
+      }
+      for (int k = threadIdx.x; k < nw; k += blockDim.x) {
+        gtb[k] = tipbits[k];
+        gtr[k] = tiprank[k];
+        gnw[k] = nextw[k];
+      }
+      for (int k = threadIdx.x; k < pcap; k += blockDim.x) gpm[k] = pmap[k];
+      // the current record list, its segments packed from 0 (hbase = 0)
+      const SPiece* cin = recs + cur * rec_cap;
+      SPiece* gin = grec + cur * kGRec;
+      for (int r = wib; r < n; r += kSegWarps) {
+        SPiece X = cin[r];
+        int rel = 0;
+        if (lane == 0) rel = atomicAdd(&s_reloc, X.nseg);
+        rel = __shfl_sync(kFull, rel, 0);
+        for (int k = lane; k < X.nseg; k += 32) gsg[rel + k] = segs[X.soff + k];
+        X.soff = rel;
+        if (lane == 0) gin[r] = X;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) s_stop = s_reloc;
+      P = gP;
+      tipbits = gtb;
+      tiprank = gtr;
+      nextw = gnw;
+      pmap = gpm;
+      nexttip = gnt;
+      s_out = gso;
+      tlist = gtl;
+      recs = grec;
+      segs = gsg;
+      rec_cap = kGRec;
+      scap = kGSegCap;
+      hbase = 0;
+      g = SegView{P, L, tipbits, nexttip, pmap, pcap - 1, segs};
+      gmode = true;
+      __syncthreads();
+      return true;
+    };
     while (ntips > 0) {
       if (depth + 1 > (long long)L + 1) {
         if (threadIdx.x == 0) report(c.st, K_NO_CONVERGE, i);
         bad = true;
         break;
       }
+      if (n + ntips > rec_cap && !gmode && L <= kSegMaxG) to_global();  // uniform
       SPiece* in = recs + cur * rec_cap;
       SPiece* out = recs + (cur ^ 1) * rec_cap;
       // output slot of every input record (prefix over tip flags) and the
@@ -2016,7 +2080,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
       // Segments are bump-allocated in one half of the arena; when a round
       // would overflow it, the live pieces are first compacted into the other
       // half, so the arena only ever has to hold the live pieces.
-      const int half = scap / 2;
+      int half = scap / 2;
       if (n + ntips > rec_cap) { spill = true; break; }  // uniform
       if (s_stop + s_need > half) {
         const int nb = hbase == 0 ? half : 0;
@@ -2034,6 +2098,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
         }
         hbase = nb;
         __syncthreads();
+        if (s_stop + s_need > half && !gmode && L <= kSegMaxG && to_global()) half = scap / 2;  // uniform
         if (s_stop + s_need > half) { spill = true; break; }  // uniform
       }
       const int tb = hbase;
@@ -2547,12 +2612,18 @@ void launch_repair_tips_long(const RepairArgs& a, cudaStream_t s) {
     smem_max_l = (e && *e) ? atoi(e) : kSegMaxL;
     if (smem_max_l > kSegMaxL) smem_max_l = kSegMaxL;
   }
+  static int rec_limit = -1;
+  if (rec_limit < 0) {  // testing hook: TERMESH_SEG_REC_CAP moves items to the pool region after fewer pieces
+    const char* e = getenv("TERMESH_SEG_REC_CAP");
+    rec_limit = (e && *e) ? atoi(e) : kSegRec;
+    if (rec_limit > kSegRec || rec_limit < 8) rec_limit = kSegRec;
+  }
   long long nblk = env_blk > 0 ? env_blk : 24 * (a.T / 20000000 + 1);
   if (nblk > kNumSMs) nblk = kNumSMs;
   k_repair_tips_seg<<<(int)nblk, 32 * kSegWarps, smem, s>>>(c, a.items, a.off, a.v, a.item_list, a.item_n,
                                                            a.item_state, a.item_depth, a.item_slots, a.stats, a.q,
                                                            a.dbg,
-                                                           (unsigned int)trace_qi, seg_cap, smem_max_l);
+                                                           (unsigned int)trace_qi, seg_cap, smem_max_l, rec_limit);
   note_launch(1);
 }
 

@@ -296,11 +296,15 @@ def test_pool_overflow_retry_is_exact(cuda):
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
-def test_long_items_global_memory_mode(cuda):
-    """TERMESH_SEG_SMEM_MAXL=128 sends every long item over 128 vertices to the
-    long-item kernel's global-memory mode (used for real above 8192 vertices,
-    the hull-sliver polygon at 100M points); results must not change -- also
-    whole path at 200k anisotropic points against the oracle."""
+@pytest.mark.parametrize("env", [{"TERMESH_SEG_SMEM_MAXL": "128"}, {"TERMESH_SEG_REC_CAP": "12"},
+                                 {"TERMESH_SEG_CAP": "48"}])
+def test_long_items_global_memory_mode(cuda, env):
+    """The long-item kernel's pool-region mode (used for real above 8192
+    vertices and for items whose pieces outgrow shared memory -- the hull
+    slivers at 100M points), forced from the start (TERMESH_SEG_SMEM_MAXL) or
+    mid-lineage by a small record list (TERMESH_SEG_REC_CAP) or segment arena
+    (TERMESH_SEG_CAP); results must not change -- goldens and the whole path at
+    200k anisotropic points against the oracle."""
     import os
     import subprocess
     import sys
@@ -321,7 +325,7 @@ def test_long_items_global_memory_mode(cuda):
         "assert np.array_equal(off, ref['final'][0]) and np.array_equal(v, ref['final'][1])\n"
         "assert st.reparation_rounds == ref['stats']['rounds']\n"
         "print('ok', st.reparation_rounds)\n")
-    env = dict(os.environ, TERMESH_SEG_SMEM_MAXL="128")
+    env = dict(os.environ, **env)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
