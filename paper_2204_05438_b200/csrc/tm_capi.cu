@@ -63,7 +63,7 @@ struct Counters {
   int64_t f_out;       // F': vertex slots after repair
   unsigned int n_overflow, n_items, n_long, n_pinch;
   unsigned int q_huge, q_long, q_next, n_parked;
-  unsigned int tip_next, table_ovf, pad2, pad3;
+  unsigned int tip_next, table_ovf, gm_next, pad3;
   unsigned long long pool_top, undo_top;
   // stats[0..7]: repair statistics (fill_stats); stats[8]: extra visits of the
   // other ranks (host-set before tm_resume_pinch); stats[9]: seed partition,
@@ -450,7 +450,7 @@ static LongQueue long_queue(tm_ctx* ctx) {
   Counters* dc = dc_of(ctx);
   return LongQueue{ctx->hugeq.as<int32_t>(), ctx->longq.as<int32_t>(), &dc->q_huge,      &dc->q_long,
                    &dc->q_next,           ctx->parked.as<int32_t>(), &dc->n_parked, ctx->pinchq.as<int32_t>(),
-                   &dc->n_pinch,          &dc->tip_next};
+                   &dc->n_pinch,          &dc->tip_next,         &dc->gm_next};
 }
 
 static RepairArgs repair_args(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, const int32_t* d_tv, int64_t T,
@@ -517,7 +517,7 @@ static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* 
       launch_classify(d_off, d_v, &dc->n_seeds, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(),
                       &dc->n_items, ctx->long_list.as<int32_t>(), &dc->n_long, dc->stats, long_queue(ctx),
                       ctx->path_hv, ctx->tv.as<int32_t>(), 2, ctx->item_state.as<int32_t>(), ctx->pool.as<int32_t>(),
-                      &dc->pool_top, ctx->pool_cap, a);
+                      &dc->pool_top, ctx->pool_cap, ctx->item_depth.as<int32_t>(), a);
       CK(cudaEventRecord(ctx->ev_cls, a));
       {
         RepairArgs ra = repair_args(ctx, d_tri32, const_cast<int32_t*>(d_hw), ctx->tv.as<int32_t>(), T, d_off, d_v);
@@ -546,7 +546,7 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
     launch_classify(d_off_in, d_v_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(), &dc->n_items,
                     ctx->long_list.as<int32_t>(), &dc->n_long, dc->stats, q, ctx->path_hv,
                     const_cast<int32_t*>(d_tv), early ? 1 : 0, ctx->item_state.as<int32_t>(), ctx->pool.as<int32_t>(),
-                    &dc->pool_top, ctx->pool_cap, s);
+                    &dc->pool_top, ctx->pool_cap, ctx->item_depth.as<int32_t>(), s);
   }
   if (early) CK(cudaStreamWaitEvent(s, ctx->ev_cls, 0));  // the item list is complete
   RepairArgs a = repair_args(ctx, d_tri32, d_hw, d_tv, T, d_off_in, d_v_in);

@@ -82,6 +82,7 @@ struct LongQueue {       // work items longer than kLongMin, longest class first
   int32_t* pinchq;         // short items with a pinch candidate left after the tip phase
   unsigned int* n_pinch;
   unsigned int* tip_next;  // work counter of k_repair_tips mode 0 (persistent warps)
+  unsigned int* gm_next;   // work counter of k_repair_tips_seg's pool-region blocks
 };
 // polygons longer than this are classified by k_classify_long (one block each);
 // on the whole path the traversal's chain pass lists them
@@ -121,7 +122,7 @@ void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, in
                      int32_t* items, unsigned int* n_items, int32_t* long_list, unsigned int* n_long,
                      unsigned long long* stats, LongQueue q, const int32_t* hv, int32_t* tv, int which,
                      int32_t* item_state, int32_t* pool, unsigned long long* pool_top, unsigned long long pool_cap,
-                     cudaStream_t s);  // item_state[k] = 0 for every item k created  // which: 0 all, 1 short polygons only, 2 the listed long ones only
+                     int32_t* item_depth, cudaStream_t s);  // item_state[k] = 0 for every item k created  // which: 0 all, 1 short polygons only, 2 the listed long ones only
 void launch_repair_tips_long(const RepairArgs& a, cudaStream_t s);
 // mode 0: items of length <= kLongMin; mode 1: long items handed back (state 2/3)
 void launch_repair_tips(const RepairArgs& a, int mode, cudaStream_t s);

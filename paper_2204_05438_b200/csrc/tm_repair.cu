@@ -207,7 +207,8 @@ __global__ void __launch_bounds__(256) k_classify_long(const int64_t* __restrict
                                                        unsigned long long* stats, LongQueue q,
                                                        const int32_t* __restrict__ hv, int32_t* __restrict__ tv,
                                                        int32_t* __restrict__ item_state, int32_t* pool,
-                                                       unsigned long long* pool_top, unsigned long long pool_cap) {
+                                                       unsigned long long* pool_top, unsigned long long pool_cap,
+                                                       int32_t* __restrict__ item_depth) {
   __shared__ int32_t s_tab[kSetCap];
   __shared__ unsigned int dups;
   __shared__ long long s_gbase;
@@ -261,6 +262,7 @@ __global__ void __launch_bounds__(256) k_classify_long(const int64_t* __restrict
       unsigned int k = atomicAdd(n_items, 1u);
       items[k] = i;
       item_state[k] = 0;
+      item_depth[k] = (int32_t)dups;  // hint for k_repair_tips_seg: ~ the item's splits (pool-region blocks above gm_dups)
       item_of[i] = (int32_t)k;
       atomicAdd(stats + 2, (unsigned long long)dups);
       atomicAdd(stats + 6, 1ull);
@@ -1441,6 +1443,7 @@ constexpr int kSegMaxL = 8192;   // longer items keep their per-item arrays in g
 constexpr int kSegMaxG = 21760;
 constexpr int kGPairCap = 65536;  // >= 2 kSegMaxG, power of two
 constexpr int kGRec = 8192;       // piece records per round list (very long items)
+constexpr int kGmBlocks = 2;      // blocks of k_repair_tips_seg that take the pool-region items
 constexpr int kGSegCap = 262144;  // segment arena (very long items)
 constexpr long long kGStride = (long long)kSegMaxG + 3 * (kSegMaxG / 32 + 1) + kGPairCap + (kSegMaxG + 1) / 2 + 16 +
                                2 * (long long)kGRec + 2 * (long long)kGRec * 5 + 2 * (long long)kGSegCap + 64;
@@ -1775,17 +1778,20 @@ struct PairMsg {
   SplitPlan plan;
 };
 
-__global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c, const int32_t* __restrict__ items,
-                                                                    const int64_t* __restrict__ off,
-                                                                    const int32_t* __restrict__ v,
-                                                                    int64_t* __restrict__ item_list,
-                                                                    int32_t* __restrict__ item_n,
-                                                                    int32_t* __restrict__ item_state,
-                                                                    int32_t* __restrict__ item_depth,
-                                                                    int64_t* __restrict__ item_slots,
-                                                                    unsigned long long* stats, LongQueue q,
-                                                                    unsigned long long* dbg, unsigned int trace_qi,
-                                                                    int seg_cap, int smem_max_l, int rec_limit) {
+// G = false: items kept in shared memory; G = true: items whose P exceeds
+// smem_max_l or whose classification predicts more pieces than the shared
+// record list holds (extra visits > gm_dups) keep their per-item arrays,
+// records and segments in a block-private pool region (the hull slivers of
+// 100M-point meshes: 10^4 vertices, thousands of splits).  Two instantiations,
+// so the shared-memory path keeps its shared-memory loads.
+template <bool G>
+__device__ __forceinline__ void seg_body(RepairCtx c, const int32_t* __restrict__ items,
+                                         const int64_t* __restrict__ off, const int32_t* __restrict__ v,
+                                         int64_t* __restrict__ item_list, int32_t* __restrict__ item_n,
+                                         int32_t* __restrict__ item_state, int32_t* __restrict__ item_depth,
+                                         int64_t* __restrict__ item_slots, unsigned long long* stats, LongQueue q,
+                                         unsigned long long* dbg, unsigned int trace_qi, int seg_cap, int smem_max_l,
+                                         int rec_limit, int gm_dups) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int32_t* const sP = reinterpret_cast<int32_t*>(smem_raw);
   uint32_t* const stipbits = reinterpret_cast<uint32_t*>(sP + kSegMaxL);
@@ -1801,23 +1807,22 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
   int32_t* const snextw = stiprank + kSegMaxL / 32 + 1;                // first non-empty tip word >= w
   uint16_t* const snexttip = reinterpret_cast<uint16_t*>(snextw + kSegMaxL / 32 + 1);
   int* tipdeg = reinterpret_cast<int*>(snexttip + kSegMaxL);  // cached fan sizes (-1: none)
-  // the per-item arrays: shared memory, or the block's pool region for items over kSegMaxL
-  int32_t *P, *pmap, *tiprank, *nextw;
-  uint32_t* tipbits;
-  uint16_t* nexttip;
-  __shared__ long long s_gscr;  // pool offset of the block's global region (-1: not allocated)
+  // the per-item arrays: shared memory (G = false) or the block's pool region (G = true)
+  int32_t *P = sP, *pmap = spmap, *tiprank = stiprank, *nextw = snextw;
+  uint32_t* tipbits = stipbits;
+  uint16_t* nexttip = snexttip;
+  __shared__ long long s_gscr;  // pool offset of the block's region (-1: not allocated)
   if (threadIdx.x == 0) s_gscr = -1;
   int* const stlist = tipdeg + kSegTips;                       // tipped records of the round
   Seg* const ssegs = reinterpret_cast<Seg*>(stlist + kSegRec);
-  // piece records, their output slots, the round's tipped records and the
-  // segment arena: shared memory, or the block's pool region (very long items)
-  SPiece* recs;
-  int32_t *s_out, *tlist;
-  Seg* segs;
-  int rec_cap, scap;
+  // piece records, their output slots, the round's tipped records and the segment arena
+  SPiece* recs = srecs;
+  int32_t *s_out = ss_out, *tlist = stlist;
+  Seg* segs = ssegs;
+  int rec_cap = rec_limit, scap = seg_cap;  // (rec_limit = kSegRec, lower only as a testing hook)
   // s_ntb: tipped-record count of the next round, double-buffered by round parity
   // so the reset of one round never races with the previous round's readers
-  __shared__ int s_ntip, s_ntouch, s_stop, s_fail, s_ntb[2], s_need, s_tot, s_reloc;
+  __shared__ int s_ntip, s_ntouch, s_stop, s_fail, s_ntb[2], s_need, s_tot;
   __shared__ PairMsg pmsg[kSegWarps / 2];
   __shared__ long long s_base;
   __shared__ unsigned int s_w;
@@ -1831,7 +1836,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
   const unsigned int nh = *q.n_huge, nq = nh + *q.n_long;
   for (;;) {
     __syncthreads();
-    if (threadIdx.x == 0) s_w = atomicAdd(q.next, 1u);
+    if (threadIdx.x == 0) s_w = atomicAdd(G ? q.gm_next : q.next, 1u);
     __syncthreads();
     const unsigned int qi = s_w;
     if (qi >= nq) break;
@@ -1846,12 +1851,16 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
     const int32_t i = items[w];
     const int64_t b0 = off[i];
     const int L = (int)(off[i + 1] - b0);
-    if (L > kSegMaxG || L < 3) {
+    if (L < 3) {
       if (threadIdx.x == 0) item_state[w] = 3;
       continue;
     }
-    bool gmode = L > smem_max_l;  // smem_max_l = kSegMaxL (lower only as a testing hook)
-    if (gmode) {
+    if ((L > smem_max_l || item_depth[w] > gm_dups) != G) continue;  // the other instantiation's item
+    if constexpr (G) {
+      if (L > kSegMaxG) {
+        if (threadIdx.x == 0) item_state[w] = 3;  // the warp kernel from scratch
+        continue;
+      }
       if (threadIdx.x == 0 && s_gscr < 0) s_gscr = palloc(c, kGStride);
       __syncthreads();
       if (s_gscr < 0) {  // pool exhausted: the warp kernel from scratch
@@ -1871,19 +1880,6 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
       segs = reinterpret_cast<Seg*>(recs + 2 * kGRec);
       rec_cap = kGRec;
       scap = kGSegCap;
-    } else {
-      P = sP;
-      tipbits = stipbits;
-      tiprank = stiprank;
-      nextw = snextw;
-      pmap = spmap;
-      nexttip = snexttip;
-      recs = srecs;
-      s_out = ss_out;
-      tlist = stlist;
-      segs = ssegs;
-      rec_cap = rec_limit;  // kSegRec (lower only as a testing hook)
-      scap = seg_cap;
     }
     int pcap = 64;
     while (pcap < 2 * L) pcap <<= 1;
@@ -1983,75 +1979,12 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
     int cur = 0, n = 1, ntips = s_ntb[0], hbase = 0;
     long long depth = 0, splits = 0;
     bool bad = false, spill = false;
-    // The piece records or the segment arena outgrow shared memory (hull
-    // slivers with thousands of splits at 100M points): move the item's state
-    // to the block's pool region and continue there (uniform; false if the
-    // pool is exhausted -- the caller then spills to the warp kernel).
-    auto to_global = [&]() -> bool {
-      if (threadIdx.x == 0 && s_gscr < 0) s_gscr = palloc(c, kGStride);
-      if (threadIdx.x == 0) s_reloc = 0;
-      __syncthreads();
-      if (s_gscr < 0) return false;
-      int32_t* gP = c.pool + s_gscr;
-      uint32_t* gtb = reinterpret_cast<uint32_t*>(gP + kSegMaxG);
-      int32_t* gtr = reinterpret_cast<int32_t*>(gtb + kSegMaxG / 32 + 1);
-      int32_t* gnw = gtr + kSegMaxG / 32 + 1;
-      int32_t* gpm = gnw + kSegMaxG / 32 + 1;
-      uint16_t* gnt = reinterpret_cast<uint16_t*>(gpm + kGPairCap);
-      int32_t* gso = reinterpret_cast<int32_t*>(gnt) + (kSegMaxG + 1) / 2 + 16;
-      int32_t* gtl = gso + kGRec;
-      SPiece* grec = reinterpret_cast<SPiece*>(gtl + kGRec);
-      Seg* gsg = reinterpret_cast<Seg*>(grec + 2 * kGRec);
-      const int nw = (L + 31) / 32;
-      for (int k = threadIdx.x; k < L; k += blockDim.x) {
-        gP[k] = P[k];
-        gnt[k] = nexttip[k];
-      }
-      for (int k = threadIdx.x; k < nw; k += blockDim.x) {
-        gtb[k] = tipbits[k];
-        gtr[k] = tiprank[k];
-        gnw[k] = nextw[k];
-      }
-      for (int k = threadIdx.x; k < pcap; k += blockDim.x) gpm[k] = pmap[k];
-      // the current record list, its segments packed from 0 (hbase = 0)
-      const SPiece* cin = recs + cur * rec_cap;
-      SPiece* gin = grec + cur * kGRec;
-      for (int r = wib; r < n; r += kSegWarps) {
-        SPiece X = cin[r];
-        int rel = 0;
-        if (lane == 0) rel = atomicAdd(&s_reloc, X.nseg);
-        rel = __shfl_sync(kFull, rel, 0);
-        for (int k = lane; k < X.nseg; k += 32) gsg[rel + k] = segs[X.soff + k];
-        X.soff = rel;
-        if (lane == 0) gin[r] = X;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) s_stop = s_reloc;
-      P = gP;
-      tipbits = gtb;
-      tiprank = gtr;
-      nextw = gnw;
-      pmap = gpm;
-      nexttip = gnt;
-      s_out = gso;
-      tlist = gtl;
-      recs = grec;
-      segs = gsg;
-      rec_cap = kGRec;
-      scap = kGSegCap;
-      hbase = 0;
-      g = SegView{P, L, tipbits, nexttip, pmap, pcap - 1, segs};
-      gmode = true;
-      __syncthreads();
-      return true;
-    };
     while (ntips > 0) {
       if (depth + 1 > (long long)L + 1) {
         if (threadIdx.x == 0) report(c.st, K_NO_CONVERGE, i);
         bad = true;
         break;
       }
-      if (n + ntips > rec_cap && !gmode && L <= kSegMaxG) to_global();  // uniform
       SPiece* in = recs + cur * rec_cap;
       SPiece* out = recs + (cur ^ 1) * rec_cap;
       // output slot of every input record (prefix over tip flags) and the
@@ -2080,7 +2013,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
       // Segments are bump-allocated in one half of the arena; when a round
       // would overflow it, the live pieces are first compacted into the other
       // half, so the arena only ever has to hold the live pieces.
-      int half = scap / 2;
+      const int half = scap / 2;
       if (n + ntips > rec_cap) { spill = true; break; }  // uniform
       if (s_stop + s_need > half) {
         const int nb = hbase == 0 ? half : 0;
@@ -2098,7 +2031,6 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
         }
         hbase = nb;
         __syncthreads();
-        if (s_stop + s_need > half && !gmode && L <= kSegMaxG && to_global()) half = scap / 2;  // uniform
         if (s_stop + s_need > half) { spill = true; break; }  // uniform
       }
       const int tb = hbase;
@@ -2323,6 +2255,20 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_repair_tips_seg(RepairCtx c,
       atomicMax(dbg + 60, (dur << 32) | ((unsigned long long)(depth & 0xFFFF) << 16) | (qi & 0xFFFF));
     }
   }
+}
+
+__global__ void __launch_bounds__(32 * kSegWarps, 1) k_repair_tips_seg(
+    RepairCtx c, const int32_t* __restrict__ items, const int64_t* __restrict__ off, const int32_t* __restrict__ v,
+    int64_t* __restrict__ item_list, int32_t* __restrict__ item_n, int32_t* __restrict__ item_state,
+    int32_t* __restrict__ item_depth, int64_t* __restrict__ item_slots, unsigned long long* stats, LongQueue q,
+    unsigned long long* dbg, unsigned int trace_qi, int seg_cap, int smem_max_l, int rec_limit, int gm_dups,
+    int gm_blocks) {
+  if ((int)blockIdx.x < gm_blocks)
+    seg_body<true>(c, items, off, v, item_list, item_n, item_state, item_depth, item_slots, stats, q, dbg, trace_qi,
+                   seg_cap, smem_max_l, rec_limit, gm_dups);
+  else
+    seg_body<false>(c, items, off, v, item_list, item_n, item_state, item_depth, item_slots, stats, q, dbg, trace_qi,
+                    seg_cap, smem_max_l, rec_limit, gm_dups);
 }
 
 // ------------------------------------------------------------ pinch pass
@@ -2564,7 +2510,7 @@ void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, in
                      int32_t* items, unsigned int* n_items, int32_t* long_list, unsigned int* n_long,
                      unsigned long long* stats, LongQueue q, const int32_t* hv, int32_t* tv, int which,
                      int32_t* item_state, int32_t* pool, unsigned long long* pool_top, unsigned long long pool_cap,
-                     cudaStream_t s) {
+                     int32_t* item_depth, cudaStream_t s) {
   if (which != 2) {  // short polygons (and with which == 0 the list of the long ones)
     k_classify<<<grid_for(Pcap, 256), 256, 0, s>>>(off, v, Pp, item_of, items, n_items, long_list, n_long, stats, hv,
                                                    tv, which == 0, item_state);
@@ -2572,7 +2518,7 @@ void launch_classify(const int64_t* off, const int32_t* v, const int64_t* Pp, in
   }
   if (which == 1) return;
   k_classify_long<<<kNumSMs * 4, 256, 0, s>>>(off, v, long_list, n_long, item_of, items, n_items, stats, q, hv, tv,
-                                              item_state, pool, pool_top, pool_cap);
+                                              item_state, pool, pool_top, pool_cap, item_depth);
   note_launch(1);
 }
 
@@ -2618,12 +2564,19 @@ void launch_repair_tips_long(const RepairArgs& a, cudaStream_t s) {
     rec_limit = (e && *e) ? atoi(e) : kSegRec;
     if (rec_limit > kSegRec || rec_limit < 8) rec_limit = kSegRec;
   }
+  static int gm_dups = -1;
+  if (gm_dups < 0) {  // items with more extra visits than this go to the pool-region blocks
+    const char* e = getenv("TERMESH_SEG_GM_DUPS");
+    gm_dups = (e && *e) ? atoi(e) : 3 * kSegRec / 4;
+  }
   long long nblk = env_blk > 0 ? env_blk : 24 * (a.T / 20000000 + 1);
-  if (nblk > kNumSMs) nblk = kNumSMs;
+  if (nblk > kNumSMs - kGmBlocks) nblk = kNumSMs - kGmBlocks;
+  nblk += kGmBlocks;  // blocks [0, kGmBlocks) take the pool-region items
   k_repair_tips_seg<<<(int)nblk, 32 * kSegWarps, smem, s>>>(c, a.items, a.off, a.v, a.item_list, a.item_n,
                                                            a.item_state, a.item_depth, a.item_slots, a.stats, a.q,
                                                            a.dbg,
-                                                           (unsigned int)trace_qi, seg_cap, smem_max_l, rec_limit);
+                                                           (unsigned int)trace_qi, seg_cap, smem_max_l, rec_limit,
+                                                           gm_dups, kGmBlocks);
   note_launch(1);
 }
 

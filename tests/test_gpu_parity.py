@@ -296,15 +296,16 @@ def test_pool_overflow_retry_is_exact(cuda):
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("env", [{"TERMESH_SEG_SMEM_MAXL": "128"}, {"TERMESH_SEG_REC_CAP": "12"},
-                                 {"TERMESH_SEG_CAP": "48"}])
+@pytest.mark.parametrize("env", [{"TERMESH_SEG_SMEM_MAXL": "128"}, {"TERMESH_SEG_GM_DUPS": "2"},
+                                 {"TERMESH_SEG_REC_CAP": "12"}, {"TERMESH_SEG_CAP": "48"}])
 def test_long_items_global_memory_mode(cuda, env):
-    """The long-item kernel's pool-region mode (used for real above 8192
-    vertices and for items whose pieces outgrow shared memory -- the hull
-    slivers at 100M points), forced from the start (TERMESH_SEG_SMEM_MAXL) or
-    mid-lineage by a small record list (TERMESH_SEG_REC_CAP) or segment arena
-    (TERMESH_SEG_CAP); results must not change -- goldens and the whole path at
-    200k anisotropic points against the oracle."""
+    """The long-item kernel's pool-region blocks (used for real above 8192
+    vertices and for items whose classification predicts more pieces than the
+    shared record list holds -- the hull slivers at 100M points), forced by a
+    low length limit (TERMESH_SEG_SMEM_MAXL) or extra-visit threshold
+    (TERMESH_SEG_GM_DUPS), and the spill of shared-memory items to the warp
+    kernel (TERMESH_SEG_REC_CAP, TERMESH_SEG_CAP); results must not change --
+    goldens and the whole path at 200k anisotropic points against the oracle."""
     import os
     import subprocess
     import sys
