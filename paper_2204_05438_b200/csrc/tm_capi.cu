@@ -149,9 +149,11 @@ struct tm_ctx {
   Buf pbits, pflag, ptable, pstamp, ptip, prep, plong, prot, pbucket, porder, phist, pstart, pcursor, plen, ptiles;
   // tm_delaunay scratch
   Buf dcell, dhist, dstart, dcursor, dids, dsxy, dcnt, doff;
-  // fp32 copy of the coordinates for the LabelMax prefilter (TERMESH_NO_XY32=1 disables it)
+  // fp32 copy of the coordinates for the LabelMax prefilter: measured neutral to
+  // slightly slower at 1M / 10M (the label pass is not bound by the coordinate
+  // gathers), so off unless TERMESH_XY32=1
   Buf xy32;
-  int use_xy32 = 1;
+  int use_xy32 = 0;
   unsigned long long pstamp_clean = 0;  // allocation generation of the all-INT_MAX stamp buffer
   cudaStream_t gstream = nullptr;
   cudaStream_t aux = nullptr;                            // long repair items run beside the short ones
@@ -655,8 +657,8 @@ int tm_ctx_create(tm_ctx** out) {
   *out = new tm_ctx();
   const char* g = getenv("TERMESH_NO_GRAPH");
   if (g && *g && *g != '0') (*out)->use_graph = 0;
-  const char* x32 = getenv("TERMESH_NO_XY32");  // A/B switch
-  if (x32 && *x32 && *x32 != '0') (*out)->use_xy32 = 0;
+  const char* x32 = getenv("TERMESH_XY32");  // A/B switch
+  if (x32 && *x32 && *x32 != '0') (*out)->use_xy32 = 1;
   const char* ts = getenv("TERMESH_TABLE_SHRINK");  // testing hook: start with a 2^-s table (overflow/growth path)
   if (ts && *ts) (*out)->table_shrink = atoi(ts);
   return TM_OK;
