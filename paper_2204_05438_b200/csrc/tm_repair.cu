@@ -1285,7 +1285,10 @@ __device__ void finish_item(const RepairCtx& c, int64_t w, long long list, int n
 
 // One warp per work item.  item_list[w] = pool offset of the item's record
 // list, item_n[w] = #records (leaves in the reference's raw order).
-__global__ void __launch_bounds__(32 * kTipWarps, 8) k_repair_tips(RepairCtx c, const int32_t* __restrict__ items,
+#ifndef TM_TIP_MINB
+#define TM_TIP_MINB 8  // resident blocks per SM the register budget is cut for (A/B builds vary it)
+#endif
+__global__ void __launch_bounds__(32 * kTipWarps, TM_TIP_MINB) k_repair_tips(RepairCtx c, const int32_t* __restrict__ items,
                                                                 const unsigned int* n_items,
                                                                 const int64_t* __restrict__ off,
                                                                 const int32_t* __restrict__ v,
@@ -2200,6 +2203,12 @@ __device__ __forceinline__ void seg_body(RepairCtx c, const int32_t* __restrict_
     __syncthreads();
     if (spill) {
       // record list or segment arena too small: the warp kernel continues
+      // (debug counters: spills of the shared / pool-region bodies, the last
+      // spilled item's length, pieces and depth)
+      if (threadIdx.x == 0) {
+        atomicAdd(dbg + (G ? 73 : 72), 1ull);
+        dbg[74] = ((unsigned long long)L << 40) | ((unsigned long long)(n & 0xFFFFF) << 20) | (depth & 0xFFFFF);
+      }
       if (threadIdx.x == 0) { item_state[w] = 2; item_list[w] = list; item_n[w] = n; item_depth[w] = (int)depth; }
       if (threadIdx.x == 0 && splits) atomicAdd(stats + 1, (unsigned long long)splits);
       continue;
