@@ -1858,7 +1858,10 @@ __device__ __forceinline__ void seg_body(RepairCtx c, const int32_t* __restrict_
       if (threadIdx.x == 0) item_state[w] = 3;
       continue;
     }
-    if ((L > smem_max_l || item_depth[w] > gm_dups) != G) continue;  // the other instantiation's item
+    // the other instantiation's item?  Pool-region blocks take P over smem_max_l,
+    // more predicted pieces than the shared record list (extra visits > gm_dups),
+    // and P over half of it (the shared segment arena runs out first there)
+    if ((L > smem_max_l || L > smem_max_l / 2 + 1 || item_depth[w] > gm_dups) != G) continue;
     if constexpr (G) {
       if (L > kSegMaxG) {
         if (threadIdx.x == 0) item_state[w] = 3;  // the warp kernel from scratch
