@@ -1448,8 +1448,9 @@ constexpr int kGPairCap = 65536;  // >= 2 kSegMaxG, power of two
 constexpr int kGRec = 8192;       // piece records per round list (very long items)
 constexpr int kGmBlocks = 2;      // blocks of k_repair_tips_seg that take the pool-region items
 constexpr int kGSegCap = 262144;  // segment arena (very long items)
-constexpr long long kGStride = (long long)kSegMaxG + 3 * (kSegMaxG / 32 + 1) + kGPairCap + (kSegMaxG + 1) / 2 + 16 +
-                               2 * (long long)kGRec + 2 * (long long)kGRec * 5 + 2 * (long long)kGSegCap + 64;
+// pool region of a pool-region block: pair map, round lists, records, segment arena (ints)
+constexpr long long kGStride = (long long)kGPairCap + 2 * (long long)kGRec + 2 * (long long)kGRec * 5 +
+                               2 * (long long)kGSegCap + 64;
 constexpr int kPairCap = 16384;  // pair-map slots (>= 2 kSegMaxL); reused as leaf hash sets
 constexpr int kSegRec = 1024;    // piece records per round list
 constexpr int kSegTips = 512;    // precomputed tips per item
@@ -1474,6 +1475,11 @@ constexpr size_t kSegFixed = (size_t)kSegMaxL * 4 + (kSegMaxL / 32) * 4 + (size_
                              (size_t)kSegRec * 4 + 128;
 constexpr int kSegCap = (int)((kSmemMax - kSegFixed) / sizeof(Seg));
 size_t seg_smem_bytes() { return kSegFixed + (size_t)kSegCap * sizeof(Seg); }
+// the pool-region instantiation's shared layout (P, tip bitmap / ranks, nexttip for kSegMaxG, fans, tips)
+constexpr size_t kSegGFixed = (size_t)kSegMaxG * 4 + 3 * (size_t)(kSegMaxG / 32 + 1) * 4 + (size_t)kSegMaxG * 2 +
+                              2 * (size_t)kSegWarps * kFanCap * 4 + 2 * (size_t)kSegTips * 4 +
+                              (size_t)kSegTips * sizeof(SplitInfo) + (size_t)kSegTouch * 4 + (size_t)kSegTips * 4;
+static_assert(kSegGFixed <= kSmemMax, "pool-region layout exceeds the dynamic shared memory");
 
 struct SegView {
   const int32_t* P;
@@ -1796,33 +1802,55 @@ __device__ __forceinline__ void seg_body(RepairCtx c, const int32_t* __restrict_
                                          unsigned long long* dbg, unsigned int trace_qi, int seg_cap, int smem_max_l,
                                          int rec_limit, int gm_dups) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  int32_t* const sP = reinterpret_cast<int32_t*>(smem_raw);
-  uint32_t* const stipbits = reinterpret_cast<uint32_t*>(sP + kSegMaxL);
-  int32_t* const spmap = reinterpret_cast<int32_t*>(stipbits + kSegMaxL / 32);
-  SPiece* const srecs = reinterpret_cast<SPiece*>(spmap + kPairCap);  // [2][kSegRec]
-  int32_t* const ss_out = reinterpret_cast<int32_t*>(srecs + 2 * kSegRec);
-  int32_t* fans = ss_out + kSegRec;
-  int32_t* tipv = fans + 2 * kSegWarps * kFanCap;  // tip vertex (or -1 when its info is unusable)
-  int32_t* tipb = tipv + kSegTips;                 // barrier vertex
-  SplitInfo* tipinfo = reinterpret_cast<SplitInfo*>(tipb + kSegTips);
-  int32_t* tset = reinterpret_cast<int32_t*>(tipinfo + kSegTips);  // promoted-edge endpoints (hash set)
-  int32_t* const stiprank = tset + kSegTouch;                         // tips of P before word w
-  int32_t* const snextw = stiprank + kSegMaxL / 32 + 1;                // first non-empty tip word >= w
-  uint16_t* const snexttip = reinterpret_cast<uint16_t*>(snextw + kSegMaxL / 32 + 1);
-  int* tipdeg = reinterpret_cast<int*>(snexttip + kSegMaxL);  // cached fan sizes (-1: none)
-  // the per-item arrays: shared memory (G = false) or the block's pool region (G = true)
-  int32_t *P = sP, *pmap = spmap, *tiprank = stiprank, *nextw = snextw;
-  uint32_t* tipbits = stipbits;
-  uint16_t* nexttip = snexttip;
+  // G = false: everything in shared memory.  G = true: P, its tip bitmap /
+  // ranks and nexttip in shared memory sized for kSegMaxG (the pair map,
+  // piece records, round lists and segment arena move to the block's pool
+  // region), so the lineage's most frequent reads stay shared.
+  int32_t *P, *pmap, *tiprank, *nextw, *fans, *tipv, *tipb, *tset, *s_out, *tlist;
+  uint32_t* tipbits;
+  uint16_t* nexttip;
+  SplitInfo* tipinfo;
+  int* tipdeg;
+  SPiece* recs;
+  Seg* segs;
+  int rec_cap, scap;
+  constexpr int kMaxP = G ? kSegMaxG : kSegMaxL;
+  P = reinterpret_cast<int32_t*>(smem_raw);
+  tipbits = reinterpret_cast<uint32_t*>(P + kMaxP);
+  if constexpr (!G) {
+    pmap = reinterpret_cast<int32_t*>(tipbits + kSegMaxL / 32);
+    recs = reinterpret_cast<SPiece*>(pmap + kPairCap);  // [2][kSegRec]
+    s_out = reinterpret_cast<int32_t*>(recs + 2 * kSegRec);
+    fans = s_out + kSegRec;
+  } else {
+    tiprank = reinterpret_cast<int32_t*>(tipbits + kSegMaxG / 32 + 1);
+    nextw = tiprank + kSegMaxG / 32 + 1;
+    nexttip = reinterpret_cast<uint16_t*>(nextw + kSegMaxG / 32 + 1);
+    fans = reinterpret_cast<int32_t*>(nexttip + kSegMaxG);
+    pmap = s_out = tlist = nullptr;  // in the pool region (per block, below)
+    recs = nullptr;
+    segs = nullptr;
+  }
+  tipv = fans + 2 * kSegWarps * kFanCap;  // tip vertex (or -1 when its info is unusable)
+  tipb = tipv + kSegTips;                 // barrier vertex
+  tipinfo = reinterpret_cast<SplitInfo*>(tipb + kSegTips);
+  tset = reinterpret_cast<int32_t*>(tipinfo + kSegTips);  // promoted-edge endpoints (hash set)
+  if constexpr (!G) {
+    tiprank = tset + kSegTouch;                                  // tips of P before word w
+    nextw = tiprank + kSegMaxL / 32 + 1;                         // first non-empty tip word >= w
+    nexttip = reinterpret_cast<uint16_t*>(nextw + kSegMaxL / 32 + 1);
+    tipdeg = reinterpret_cast<int*>(nexttip + kSegMaxL);  // cached fan sizes (-1: none)
+    tlist = tipdeg + kSegTips;                             // tipped records of the round
+    segs = reinterpret_cast<Seg*>(tlist + kSegRec);
+    rec_cap = rec_limit;  // kSegRec (lower only as a testing hook)
+    scap = seg_cap;
+  } else {
+    tipdeg = reinterpret_cast<int*>(tset + kSegTouch);
+    rec_cap = kGRec;
+    scap = kGSegCap;
+  }
   __shared__ long long s_gscr;  // pool offset of the block's region (-1: not allocated)
   if (threadIdx.x == 0) s_gscr = -1;
-  int* const stlist = tipdeg + kSegTips;                       // tipped records of the round
-  Seg* const ssegs = reinterpret_cast<Seg*>(stlist + kSegRec);
-  // piece records, their output slots, the round's tipped records and the segment arena
-  SPiece* recs = srecs;
-  int32_t *s_out = ss_out, *tlist = stlist;
-  Seg* segs = ssegs;
-  int rec_cap = rec_limit, scap = seg_cap;  // (rec_limit = kSegRec, lower only as a testing hook)
   // s_ntb: tipped-record count of the next round, double-buffered by round parity
   // so the reset of one round never races with the previous round's readers
   __shared__ int s_ntip, s_ntouch, s_stop, s_fail, s_ntb[2], s_need, s_tot;
@@ -1873,19 +1901,11 @@ __device__ __forceinline__ void seg_body(RepairCtx c, const int32_t* __restrict_
         if (threadIdx.x == 0) item_state[w] = 3;
         continue;
       }
-      int32_t* gb = c.pool + s_gscr;
-      P = gb;
-      tipbits = reinterpret_cast<uint32_t*>(P + kSegMaxG);
-      tiprank = reinterpret_cast<int32_t*>(tipbits + kSegMaxG / 32 + 1);
-      nextw = tiprank + kSegMaxG / 32 + 1;
-      pmap = nextw + kSegMaxG / 32 + 1;
-      nexttip = reinterpret_cast<uint16_t*>(pmap + kGPairCap);
-      s_out = reinterpret_cast<int32_t*>(nexttip) + (kSegMaxG + 1) / 2 + 16;
+      pmap = c.pool + s_gscr;
+      s_out = pmap + kGPairCap;
       tlist = s_out + kGRec;
       recs = reinterpret_cast<SPiece*>(tlist + kGRec);  // [2][kGRec]
       segs = reinterpret_cast<Seg*>(recs + 2 * kGRec);
-      rec_cap = kGRec;
-      scap = kGSegCap;
     }
     int pcap = 64;
     while (pcap < 2 * L) pcap <<= 1;
