@@ -130,6 +130,32 @@ int tm_ctx_set_partition(tm_ctx *ctx, int64_t t_begin, int64_t t_end);
  * capacities are those of the first call.  Reference: reparation.py:315-340. */
 int tm_resume_pinch(tm_ctx *ctx, int64_t extra_total, int64_t *off_out, int32_t *v_out, int64_t cap_polys,
                     int64_t cap_slots, int64_t *n_polys, int64_t *n_slots, int64_t *stats, void *stream);
+/* Seed-partitioned labels ("each GPU labels its own edge
+ * range").  tm_label_range labels triangles [t_begin, t_end) into the
+ * context's own buffers with a range-local twin table (and converts the
+ * corners of the whole mesh) and lists the range's still-unpaired half-edges
+ * -- border or partner in another range -- as boundary entries (key
+ * (lo << 32) | hi, value (h << 1) | longest-edge flag, into caller buffers of
+ * `cap` entries; a padding key ~0 is ignored by tm_label_resolve).  After the ranks all-gather their entries
+ * (this rank's at [own_begin, own_begin + own_count) of the concatenation),
+ * tm_label_resolve labels the cross-range pairs of this rank's half-edges.
+ * Once the ranks' hw / seed / max_edge chunks are all-gathered into the
+ * context buffers, tm_polygons_from_labels runs the traversal, repair and
+ * stitch of the context's seed partition (no label phase). */
+int tm_label_range(tm_ctx *ctx, const double *d_xy, int64_t n_vertices, const void *d_tri, int tri_bits, int64_t T,
+                   int64_t t_begin, int64_t t_end, uint64_t *d_boundary_keys, int32_t *d_boundary_vals, int64_t cap,
+                   int64_t *n_boundary, void *stream);
+int tm_ctx_label_buffers(tm_ctx *ctx, int32_t **d_tri32, int32_t **d_halfedge, int8_t **d_max_edge, uint8_t **d_seed);
+/* copy the label state of triangles [t_begin, t_end) between caller arrays of
+ * the whole mesh (hw int32[3T], seed uint8[T], max_edge int8[T]; any may be
+ * NULL) and the context's: to_ctx = 1 caller -> context, 0 context -> caller */
+int tm_ctx_copy_labels(tm_ctx *ctx, int to_ctx, int32_t *d_halfedge, uint8_t *d_seed, int8_t *d_max_edge,
+                       int64_t t_begin, int64_t t_end, void *stream);
+int tm_label_resolve(tm_ctx *ctx, const uint64_t *d_keys_all, const int32_t *d_vals_all, int64_t n_all,
+                     int64_t own_begin, int64_t own_count, void *stream);
+int tm_polygons_from_labels(tm_ctx *ctx, int64_t n_vertices, int64_t T, int64_t *d_offsets, int32_t *d_verts,
+                            int64_t cap_polys, int64_t cap_slots, int64_t *n_polys, int64_t *n_slots, int64_t *stats,
+                            void *stream);
 /* d_offsets[0..n_polys] += delta: places a rank's CSR at its global slot base
  * (the exclusive prefix of the all-gathered per-rank slot counts). */
 int tm_shift_offsets(int64_t *d_offsets, int64_t n_polys, int64_t delta, void *stream);

@@ -85,6 +85,14 @@ def lib():
         L.tm_polygon_areas.argtypes = [_P, _P, _P, _I64, _P, _P, _P]
         L.tm_canonicalize.argtypes = [_P, _P, _P, _I64, _I64, _P, _P, _P]
         L.tm_delaunay.argtypes = [_P, _P, _I64, _P, _P, _I64, _PI64, _P, _PI64, _PI64, _P]
+        L.tm_label_range.argtypes = [_P, _P, _I64, _P, _I, _I64, _I64, _I64, _P, _P, _I64, _PI64, _P]
+        L.tm_ctx_label_buffers.argtypes = [_P] + [ctypes.POINTER(_P)] * 4
+        L.tm_ctx_copy_labels.argtypes = [_P, _I, _P, _P, _P, _I64, _I64, _P]
+        L.tm_ctx_copy_labels.restype = _I
+        L.tm_label_resolve.argtypes = [_P, _P, _P, _I64, _I64, _I64, _P]
+        L.tm_polygons_from_labels.argtypes = [_P, _I64, _I64, _P, _P, _I64, _I64, _PI64, _PI64, _PI64, _P]
+        for name in ("tm_label_range", "tm_ctx_label_buffers", "tm_label_resolve", "tm_polygons_from_labels"):
+            getattr(L, name).restype = _I
         L.tm_delaunay.restype = _I
         # multi-GPU exchange (tm_comm.cu; NCCL bound at run time)
         L.tm_comm_id_bytes.restype = _I
@@ -133,7 +141,8 @@ def exported_symbols():
             "tm_pack_frontier",
             "tm_traverse", "tm_repair", "tm_mesh_to_polygons_host", "tm_mesh_to_polygons", "tm_resume_pinch",
             "tm_check_trivertex", "tm_polygon_stats", "tm_polygon_areas", "tm_canonicalize",
-            "tm_delaunay", "tm_comm_id_bytes", "tm_comm_unique_id", "tm_comm_init", "tm_comm_allgather", "tm_comm_destroy",
+            "tm_delaunay", "tm_label_range", "tm_ctx_label_buffers", "tm_ctx_copy_labels", "tm_label_resolve",
+            "tm_polygons_from_labels", "tm_comm_id_bytes", "tm_comm_unique_id", "tm_comm_init", "tm_comm_allgather", "tm_comm_destroy",
             "tm_comm_last_error", "tm_format_double", "tm_file_read", "tm_file_status", "tm_file_copy", "tm_file_close",
             "tm_write_polymesh", "tm_write_triangle_file")
 

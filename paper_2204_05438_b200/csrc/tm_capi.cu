@@ -80,6 +80,7 @@ struct Counters {
   // tm_delaunay: cell count, point count, triangle total, open / degenerate stars
   int64_t dl_ncell, dl_n, dl_ntri;
   unsigned int dl_open, dl_degen;
+  unsigned long long n_boundary;  // tm_label_range: boundary entries of the rank
 };
 
 constexpr int kUploadChunks = 8;  // triangle upload chunks of tm_mesh_to_polygons_host
@@ -180,6 +181,10 @@ struct tm_ctx {
   // host-array runs: counters reset and label pass A were enqueued by the
   // caller, chunk by chunk behind the triangle upload (copy/compute overlap)
   bool label_a_external = false;
+  // seed-partitioned labels: tri32 / hw / max_edge / seed of the whole mesh were
+  // filled by tm_label_range + tm_label_resolve + the ranks' all-gather
+  bool labels_external = false;
+  Buf btab;  // boundary-entry resolution table
   cudaStream_t cstream = nullptr;
   cudaEvent_t chunk_ev[kUploadChunks] = {};
   long long graph_kernels = 0;  // kernels per graph replay (counted at capture)
@@ -675,7 +680,7 @@ void tm_ctx_destroy(tm_ctx* ctx) {
                  &ctx->lbscan, &ctx->pbits, &ctx->pflag, &ctx->ptable, &ctx->pstamp, &ctx->ptip, &ctx->prep,
                  &ctx->plong, &ctx->prot, &ctx->pbucket, &ctx->porder, &ctx->phist, &ctx->pstart, &ctx->pcursor,
                  &ctx->plen, &ctx->ptiles, &ctx->dcell, &ctx->dhist, &ctx->dstart, &ctx->dcursor, &ctx->dids,
-                 &ctx->dsxy, &ctx->dcnt, &ctx->doff, &ctx->xy32};
+                 &ctx->dsxy, &ctx->dcnt, &ctx->doff, &ctx->xy32, &ctx->btab};
   for (Buf* b : bufs) b->release();
   if (ctx->h_reset) cudaFreeHost(ctx->h_reset);
   for (auto& e : ctx->ev)
@@ -954,7 +959,8 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
     if (part & 1) {
       if (!ctx->label_a_external && (r = enqueue_reset(ctx, s))) return r;
       CK(rec(ctx->ev[0], s));
-      if ((r = enqueue_label(ctx, d_xy, n, d_tri, tri_bits, T, check, tri32, hw, ctx->max_edge.as<int8_t>(),
+      if (!ctx->labels_external &&
+          (r = enqueue_label(ctx, d_xy, n, d_tri, tri_bits, T, check, tri32, hw, ctx->max_edge.as<int8_t>(),
                              ctx->seed.as<uint8_t>(), nullptr, s)))
         return r;
       CK(rec(ctx->ev[1], s));
@@ -987,7 +993,8 @@ static int run_device(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_
     if ((rc = decode_status(ctx, *ctx->h_result))) return rc;
     if ((rc = body(s, 2))) return rc;
   } else if (ctx->use_graph && !ctx->prof.on) {
-    GraphKey key{d_xy, d_tri, d_off, d_v, n, T, 0, 0, tri_bits, check, ctx->label_a_external ? 1 : 0, ctx->pool_cap,
+    GraphKey key{d_xy, d_tri, d_off, d_v, n, T, 0, 0, tri_bits, check,
+                 (ctx->label_a_external ? 1 : 0) | (ctx->labels_external ? 2 : 0), ctx->pool_cap,
                  g_alloc_gen.load()};
     part_range(ctx, T, &key.tb, &key.te);
     if (!ctx->graph || !(key == ctx->gkey)) {
@@ -1362,6 +1369,90 @@ int tm_delaunay(tm_ctx* ctx, const double* d_xy, int64_t n, const double* box, i
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s));
   return TM_OK;
+}
+
+// ---------------------------------------------------------------- seed-partitioned labels (multi-GPU)
+int tm_label_range(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_tri, int tri_bits, int64_t T,
+                   int64_t t_begin, int64_t t_end, uint64_t* d_keys, int32_t* d_vals, int64_t cap,
+                   int64_t* n_boundary, void* stream) {
+  if (!ctx || !n_boundary || !d_keys || !d_vals || (tri_bits != 32 && tri_bits != 64)) return TM_ERR_ARGUMENT;
+  if (t_begin < 0 || t_end > T || t_end < t_begin) return set_err(ctx, TM_ERR_ARGUMENT, "bad triangle range");
+  int rc = path_buffers(ctx, n, T);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  ENSURE(slots, hash_bytes_range(n, T, t_end - t_begin));
+  if ((rc = enqueue_reset(ctx, s))) return rc;
+  Counters* dc = dc_of(ctx);
+  int32_t* tri32 = ctx->tri32.as<int32_t>();
+  launch_tri32(d_tri, tri_bits == 64, T, tri32, s);  // corners of the whole mesh (walks leave the range)
+  launch_label_range(d_xy, n, d_tri, tri_bits == 64, T, t_begin, t_end, tri32, ctx->hw.as<int32_t>(),
+                     ctx->max_edge.as<int8_t>(), ctx->seed.as<uint8_t>(), ctx->slots.p, &dc->st, &dc->table_ovf, s);
+  launch_boundary_extract(tri32, ctx->max_edge.as<int8_t>(), ctx->hw.as<int32_t>(), t_begin, t_end,
+                          reinterpret_cast<unsigned long long*>(d_keys), d_vals, &dc->n_boundary, cap, s);
+  CK(cudaGetLastError());
+  Counters h;
+  if ((rc = finish(ctx, s, &h))) return rc;
+  if (h.table_ovf) return set_err(ctx, TM_ERR_CAPACITY, "range twin table displacement overflow");
+  *n_boundary = (int64_t)h.n_boundary;
+  if (*n_boundary > cap)
+    return set_err(ctx, TM_ERR_CAPACITY, "%lld boundary entries, capacity %lld", (long long)*n_boundary,
+                   (long long)cap);
+  return TM_OK;
+}
+
+int tm_ctx_label_buffers(tm_ctx* ctx, int32_t** tri32, int32_t** hw, int8_t** max_edge, uint8_t** seed) {
+  if (!ctx) return TM_ERR_ARGUMENT;
+  if (tri32) *tri32 = ctx->tri32.as<int32_t>();
+  if (hw) *hw = ctx->hw.as<int32_t>();
+  if (max_edge) *max_edge = ctx->max_edge.as<int8_t>();
+  if (seed) *seed = ctx->seed.as<uint8_t>();
+  return TM_OK;
+}
+
+int tm_ctx_copy_labels(tm_ctx* ctx, int to_ctx, int32_t* d_hw, uint8_t* d_seed, int8_t* d_max_edge, int64_t t_begin,
+                       int64_t t_end, void* stream) {
+  if (!ctx || t_begin < 0 || t_end < t_begin || !ctx->hw.p) return TM_ERR_ARGUMENT;
+  if ((size_t)t_end * 3 * sizeof(int32_t) > ctx->hw.bytes) return set_err(ctx, TM_ERR_ARGUMENT, "range beyond T");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t m = t_end - t_begin;
+  int32_t* hw = ctx->hw.as<int32_t>() + 3 * t_begin;
+  uint8_t* sd = ctx->seed.as<uint8_t>() + t_begin;
+  int8_t* me = ctx->max_edge.as<int8_t>() + t_begin;
+  if (to_ctx) {
+    if (d_hw) CK(cudaMemcpyAsync(hw, d_hw + 3 * t_begin, 3 * m * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    if (d_seed) CK(cudaMemcpyAsync(sd, d_seed + t_begin, m, cudaMemcpyDeviceToDevice, s));
+    if (d_max_edge) CK(cudaMemcpyAsync(me, d_max_edge + t_begin, m, cudaMemcpyDeviceToDevice, s));
+  } else {
+    if (d_hw) CK(cudaMemcpyAsync(d_hw + 3 * t_begin, hw, 3 * m * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    if (d_seed) CK(cudaMemcpyAsync(d_seed + t_begin, sd, m, cudaMemcpyDeviceToDevice, s));
+    if (d_max_edge) CK(cudaMemcpyAsync(d_max_edge + t_begin, me, m, cudaMemcpyDeviceToDevice, s));
+  }
+  return TM_OK;
+}
+
+int tm_label_resolve(tm_ctx* ctx, const uint64_t* d_keys_all, const int32_t* d_vals_all, int64_t n_all,
+                     int64_t own_begin, int64_t own_count, void* stream) {
+  if (!ctx || n_all < 0 || own_begin < 0 || own_count < 0 || own_begin + own_count > n_all) return TM_ERR_ARGUMENT;
+  int64_t slots = 64;
+  while (slots < 2 * n_all + 64) slots <<= 1;
+  ENSURE(btab, slots * sizeof(int32_t));
+  launch_boundary_resolve(reinterpret_cast<const unsigned long long*>(d_keys_all), d_vals_all, n_all, own_begin,
+                          own_begin + own_count, ctx->btab.as<int32_t>(), slots, ctx->hw.as<int32_t>(),
+                          ctx->seed.as<uint8_t>(), (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  return TM_OK;
+}
+
+int tm_polygons_from_labels(tm_ctx* ctx, int64_t n, int64_t T, int64_t* d_off, int32_t* d_v, int64_t cap_polys,
+                            int64_t cap_slots, int64_t* n_polys, int64_t* n_slots, int64_t* stats, void* stream) {
+  if (!ctx || !n_polys || !n_slots) return TM_ERR_ARGUMENT;
+  if (cap_polys < T || cap_slots < 3 * T)
+    return set_err(ctx, TM_ERR_ARGUMENT, "output capacities must be at least T polygons and 3T slots");
+  ctx->labels_external = true;
+  int rc = run_device(ctx, nullptr, n, nullptr, 32, T, 0, d_off, d_v, n_polys, n_slots, stats, (cudaStream_t)stream);
+  ctx->labels_external = false;
+  ctx->last_host = false;
+  return rc;
 }
 
 }  // extern "C"

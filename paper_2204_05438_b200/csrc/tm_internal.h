@@ -29,6 +29,18 @@ void launch_label_a_range(const double* xy, int64_t n, const void* tri, int tri_
 void launch_label_b(const int32_t* tri32, int64_t n, int64_t T, int32_t* hw, const int8_t* max_edge, uint8_t* seed,
                     int32_t* tv, void* table, int check, DevStatus* st, cudaStream_t s, int shrink = 0);
 void launch_relabel(const int8_t* max_edge, int64_t T, int32_t* hw, uint8_t* seed, cudaStream_t s);
+// seed-partitioned labels (range-local twin table + boundary exchange)
+size_t hash_bytes_range(int64_t n, int64_t T, int64_t keyT);
+void launch_label_range(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int64_t b, int64_t e,
+                        int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed, void* table, DevStatus* st,
+                        unsigned int* ovf, cudaStream_t s);
+void launch_tri32(const void* tri, int tri_is64, int64_t T, int32_t* tri32, cudaStream_t s);
+void launch_boundary_extract(const int32_t* tri32, const int8_t* max_edge, const int32_t* hw, int64_t b, int64_t e,
+                             unsigned long long* keys, int32_t* vals, unsigned long long* count, int64_t cap,
+                             cudaStream_t s);
+void launch_boundary_resolve(const unsigned long long* keys, const int32_t* vals, int64_t n_all, int64_t own0,
+                             int64_t own1, int32_t* tab, int64_t tab_slots, int32_t* hw, uint8_t* seed,
+                             cudaStream_t s);
 void launch_check_neighbors(const int32_t* hw, const void* nb, int nb_is64, int64_t T, DevStatus* st, cudaStream_t s);
 void launch_unpack(const int32_t* hw, int64_t T, int32_t* twin, uint8_t* fr, cudaStream_t s);
 void launch_pack_frontier(int32_t* hw, int64_t T, const uint8_t* fr, cudaStream_t s);

@@ -400,7 +400,8 @@ __global__ void __launch_bounds__(kLabelThreads, 4) k_tri_pass(const double2* __
 // on the lower triangle).  k = twin % 3 replaces the reference's back-slot
 // searches.  A half-edge without a partner stays border as pass A wrote it
 // (an ascending one keeps its provisional seed flag).
-__global__ void __launch_bounds__(kLabelThreads, 6) k_pair_pass(const int32_t* __restrict__ tri32, int64_t T,
+__global__ void __launch_bounds__(kLabelThreads, 6) k_pair_pass(const int32_t* __restrict__ tri32, int64_t t_begin,
+                                                             int64_t T,
                                                              const int8_t* __restrict__ max_edge, TwinTable tb,
                                                              int32_t* __restrict__ hw, uint8_t* __restrict__ seed,
                                                              int32_t* __restrict__ tv, int64_t n, int check,
@@ -408,7 +409,7 @@ __global__ void __launch_bounds__(kLabelThreads, 6) k_pair_pass(const int32_t* _
   __shared__ int32_t sq[kLabelWarps][3][96];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t - lane < T; t += stride) {
+  for (int64_t t = t_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t - lane < T; t += stride) {
     unsigned flags = 0;
     int32_t hh[3], oo[3], gg[3];
     if (t < T) {
@@ -515,7 +516,9 @@ static int bit_length(uint64_t v) {
 // (Qhull order), so the inserted keys load the half table to ~0.3; a mesh
 // without that locality overflows it, which sets *ovf and the host reruns the
 // call with s - 1 (full size, then 2x, 4x, 8x).
-static TwinTable table_geometry(int64_t n, int64_t T, void* mem, int shrink = 0, unsigned int* ovf = nullptr) {
+static TwinTable table_geometry(int64_t n, int64_t T, void* mem, int shrink = 0, unsigned int* ovf = nullptr,
+                                int64_t keyT = -1) {
+  // keyT: triangles whose keys go in (a rank's range), T: half-edge ids < 3T
   TwinTable tb{};
   tb.b = bit_length((uint64_t)(n > 1 ? n - 1 : 1));
   tb.K = 2 * tb.b;
@@ -523,7 +526,8 @@ static TwinTable table_geometry(int64_t n, int64_t T, void* mem, int shrink = 0,
   tb.hb = bit_length((uint64_t)(3 * (T > 0 ? T : 1))) + 1;
   // ascending half-edges <= 3T/2 + border; 4-slot buckets at load in [0.35, 0.7)
   // (measured: a fuller table costs more in probe/CAS conflicts than it saves in L2)
-  uint64_t keys = (uint64_t)(3 * (T > 0 ? T : 1)) / 2 + 64;
+  const int64_t KT = keyT >= 0 ? keyT : T;
+  uint64_t keys = (uint64_t)(3 * (KT > 0 ? KT : 1)) / 2 + 64;
   int q = bit_length((keys * 10 / 28) | 1);
   if (shrink > 0) q = q - shrink > 8 ? q - shrink : (q > 8 ? 8 : q);
   if (shrink < 0) q -= shrink;
@@ -586,10 +590,145 @@ void launch_label_b(const int32_t* tri32, int64_t n, int64_t T, int32_t* hw, con
   TwinTable tb = table_geometry(n, T, table, shrink);
   int64_t m = (T > n || tv == nullptr) ? T : n;
   if (m > 0) {
-    k_pair_pass<<<grid_for(m, kLabelThreads), kLabelThreads, 0, s>>>(tri32, T, max_edge, tb, hw, seed, tv, n, check,
-                                                                     st);
+    k_pair_pass<<<grid_for(m, kLabelThreads), kLabelThreads, 0, s>>>(tri32, 0, T, max_edge, tb, hw, seed, tv, n,
+                                                                     check, st);
     note_launch(1);
   }
+}
+
+// ------------------------------------------------------------ seed-partitioned labels
+// A rank labels its triangle range [b, e) with a range-local twin table
+// (passes A and B restricted to the range); half-edges still unpaired are
+// either true border or have their partner in another rank's range: they are
+// listed as boundary entries (key (lo << 32) | hi, value (h << 1) | longest)
+// for the exchange, after which k_boundary_resolve labels the cross pairs.
+size_t hash_bytes_range(int64_t n, int64_t T, int64_t keyT) {
+  TwinTable tb = table_geometry(n, T, nullptr, 0, nullptr, keyT);
+  return (size_t)(tb.nb_mask + 1) * 4 * sizeof(unsigned long long);
+}
+
+void launch_label_range(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int64_t b, int64_t e,
+                        int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed, void* table, DevStatus* st,
+                        unsigned int* ovf, cudaStream_t s) {
+  const TwinTable tb = table_geometry(n, T, table, 0, ovf, e - b);
+  cudaMemsetAsync(table, 0xFF, (size_t)(tb.nb_mask + 1) * 4 * sizeof(unsigned long long), s);
+  if (e <= b) return;
+  const int g = grid_for(e - b, kLabelThreads);
+  if (tri_is64)
+    k_tri_pass<int64_t><<<g, kLabelThreads, 0, s>>>((const double2*)xy, nullptr, n, (const int64_t*)tri, b, e, tri32,
+                                                    max_edge, tb, hw, seed, nullptr, 0, st);
+  else
+    k_tri_pass<int32_t><<<g, kLabelThreads, 0, s>>>((const double2*)xy, nullptr, n, (const int32_t*)tri, b, e,
+                                                    tri32 == tri ? nullptr : tri32, max_edge, tb, hw, seed, nullptr, 0,
+                                                    st);
+  k_pair_pass<<<g, kLabelThreads, 0, s>>>(tri32, b, e, max_edge, tb, hw, seed, nullptr, n, 0, st);
+  note_launch(2);
+}
+
+template <typename TI>
+__global__ void k_tri32(const TI* __restrict__ tri, int64_t n3, int32_t* __restrict__ tri32) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n3; k += (int64_t)gridDim.x * blockDim.x)
+    tri32[k] = (int32_t)tri[k];
+}
+
+void launch_tri32(const void* tri, int tri_is64, int64_t T, int32_t* tri32, cudaStream_t s) {
+  if (T <= 0) return;
+  if (tri_is64) k_tri32<int64_t><<<grid_for(3 * T, 256), 256, 0, s>>>((const int64_t*)tri, 3 * T, tri32);
+  else k_tri32<int32_t><<<grid_for(3 * T, 256), 256, 0, s>>>((const int32_t*)tri, 3 * T, tri32);
+  note_launch(1);
+}
+
+__global__ void k_boundary_extract(const int32_t* __restrict__ tri32, const int8_t* __restrict__ max_edge,
+                                   const int32_t* __restrict__ hw, int64_t b, int64_t e,
+                                   unsigned long long* __restrict__ keys, int32_t* __restrict__ vals,
+                                   unsigned long long* count, int64_t cap) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t h0 = 3 * b + (blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane); h0 < 3 * e;
+       h0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t h = h0 + lane;
+    bool want = false;
+    unsigned long long key = 0;
+    int32_t val = 0;
+    if (h < 3 * e && hw[h] == -1) {
+      const int64_t t = h / 3;
+      const int j = (int)(h - 3 * t);
+      const uint32_t o = (uint32_t)tri32[3 * t + (j + 1) % 3], g = (uint32_t)tri32[3 * t + (j + 2) % 3];
+      key = ((unsigned long long)min(o, g) << 32) | max(o, g);
+      val = (int32_t)((h << 1) | (max_edge[t] == j ? 1 : 0));
+      want = true;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, want);
+    unsigned long long base = 0;
+    if (lane == 0 && m) base = atomicAdd(count, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (want) {
+      const unsigned long long k = base + __popc(m & ((1u << lane) - 1u));
+      if ((int64_t)k < cap) {
+        keys[k] = key;
+        vals[k] = val;
+      }
+    }
+  }
+}
+
+void launch_boundary_extract(const int32_t* tri32, const int8_t* max_edge, const int32_t* hw, int64_t b, int64_t e,
+                             unsigned long long* keys, int32_t* vals, unsigned long long* count, int64_t cap,
+                             cudaStream_t s) {
+  if (e > b)
+    k_boundary_extract<<<grid_for(3 * (e - b), 256), 256, 0, s>>>(tri32, max_edge, hw, b, e, keys, vals, count, cap),
+        note_launch(1);
+}
+
+__device__ __forceinline__ uint64_t bhash(unsigned long long key, uint64_t mask) {
+  return ((key * 0x9E3779B97F4A7C15ull) >> 17) & mask;
+}
+
+__global__ void k_boundary_insert(const unsigned long long* __restrict__ keys, int64_t n_all, int32_t* __restrict__ tab,
+                                  uint64_t mask) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n_all; k += (int64_t)gridDim.x * blockDim.x) {
+    if (keys[k] == ~0ull) continue;  // padding of a fixed-size all-gather
+    uint64_t h = bhash(keys[k], mask);
+    while (atomicCAS(tab + h, -1, (int32_t)k) != -1) h = (h + 1) & mask;
+  }
+}
+
+// own entries [own0, own1) of the concatenated list: find the entry with the
+// same key from another range, label this side of the pair (labeling.py:65-115)
+__global__ void k_boundary_resolve(const unsigned long long* __restrict__ keys, const int32_t* __restrict__ vals,
+                                   int64_t own0, int64_t own1, const int32_t* __restrict__ tab, uint64_t mask,
+                                   int32_t* __restrict__ hw, uint8_t* __restrict__ seed) {
+  for (int64_t k = own0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < own1;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long key = keys[k];
+    uint64_t h = bhash(key, mask);
+    int32_t partner = -1;
+    for (;;) {
+      const int32_t x = tab[h];
+      if (x < 0) break;
+      if (x != k && keys[x] == key) { partner = x; break; }
+      h = (h + 1) & mask;
+    }
+    if (partner < 0) continue;  // true border: stays -1 (frontier), provisional seed stays
+    const int32_t me = vals[k], pv = vals[partner];
+    const int32_t he = me >> 1, hp = pv >> 1;
+    const bool own = me & 1, other = pv & 1;
+    hw[he] = (hp << 1) | ((!own && !other) ? 1 : 0);
+    if (own) {
+      const int32_t tt = he / 3, tc = hp / 3;
+      seed[tt] = (other && tt < tc) ? 1 : 0;
+    }
+  }
+}
+
+void launch_boundary_resolve(const unsigned long long* keys, const int32_t* vals, int64_t n_all, int64_t own0,
+                             int64_t own1, int32_t* tab, int64_t tab_slots, int32_t* hw, uint8_t* seed,
+                             cudaStream_t s) {
+  cudaMemsetAsync(tab, 0xFF, (size_t)tab_slots * sizeof(int32_t), s);
+  if (n_all > 0) k_boundary_insert<<<grid_for(n_all, 256), 256, 0, s>>>(keys, n_all, tab, (uint64_t)(tab_slots - 1));
+  if (own1 > own0)
+    k_boundary_resolve<<<grid_for(own1 - own0, 256), 256, 0, s>>>(keys, vals, own0, own1, tab,
+                                                                  (uint64_t)(tab_slots - 1), hw, seed);
+  note_launch(2);
 }
 
 void launch_relabel(const int8_t* max_edge, int64_t T, int32_t* hw, uint8_t* seed, cudaStream_t s) {

@@ -259,7 +259,82 @@ def resume_partition(ctx, off, verts, T: int, extra_total: int):
     return p, f, dict(zip(_capi.STAT_NAMES, list(stats)))
 
 
-def execute_distributed(tri, group=None, gather: bool = True, comm: Comm | None = None):
+def partition_chunks(T: int, world: int) -> list[tuple[int, int]]:
+    """Equal chunks of ceil(T / world) triangles (the last one shorter): the
+    split-label mode's ranges, so the label all-gathers have one size per rank."""
+    C = -(-T // world) if world else 0
+    return [(min(r * C, T), min((r + 1) * C, T)) for r in range(world)]
+
+
+def split_labels(ctx, xy, tri, n: int, T: int, comm: Comm, rank: int, world: int):
+    """SURVEY.md 8(e) "each GPU labels its own edge range": this rank labels its
+    chunk with a range-local twin table (tm_label_range), the ranks all-gather
+    their boundary entries (half-edges whose partner may lie in another chunk),
+    tm_label_resolve pairs this chunk's cross-chunk half-edges, and an in-place
+    all-gather of the packed half-edge words, seeds and longest edges (14 B per
+    triangle) gives every rank the labels of the whole mesh in its context."""
+    import torch
+    from . import _capi
+    L = _capi.lib()
+    dev = xy.device
+    sp = _capi.stream_ptr(dev)
+    C = -(-T // world)
+    b, e = partition_chunks(T, world)[rank]
+    cap = 3 * (e - b) + 1
+    keys = torch.empty(cap, dtype=torch.int64, device=dev)
+    vals = torch.empty(cap, dtype=torch.int32, device=dev)
+    nb = ctypes.c_int64()
+    ctx.check(L.tm_label_range(ctx.ptr, _capi.ptr(xy), n, _capi.ptr(tri), 64 if tri.dtype == torch.int64 else 32, T,
+                               b, e, _capi.ptr(keys), _capi.ptr(vals), cap, ctypes.byref(nb), sp), "label")
+    cnt = torch.tensor([nb.value], dtype=torch.int64, device=dev)
+    cnts = torch.empty(world, dtype=torch.int64, device=dev)
+    comm.allgather(cnt, cnts)
+    counts = cnts.cpu().tolist()
+    maxc = max(1, max(counts))
+    kp = torch.full((maxc,), -1, dtype=torch.int64, device=dev)  # padding key ~0
+    vp = torch.full((maxc,), -1, dtype=torch.int32, device=dev)
+    kp[: nb.value] = keys[: nb.value]
+    vp[: nb.value] = vals[: nb.value]
+    k_all = torch.empty(world * maxc, dtype=torch.int64, device=dev)
+    v_all = torch.empty(world * maxc, dtype=torch.int32, device=dev)
+    comm.allgather(kp, k_all)
+    comm.allgather(vp, v_all)
+    ctx.check(L.tm_label_resolve(ctx.ptr, _capi.ptr(k_all), _capi.ptr(v_all), world * maxc, rank * maxc, nb.value,
+                                 sp), "label")
+    hw = torch.empty(3 * world * C, dtype=torch.int32, device=dev)
+    sd = torch.empty(world * C, dtype=torch.uint8, device=dev)
+    me = torch.empty(world * C, dtype=torch.int8, device=dev)
+    ctx.check(L.tm_ctx_copy_labels(ctx.ptr, 0, _capi.ptr(hw), _capi.ptr(sd), _capi.ptr(me), b, e, sp))
+    comm.allgather(hw[3 * rank * C: 3 * (rank + 1) * C], hw)  # in place: rank r's chunk at r * C
+    comm.allgather(sd[rank * C: (rank + 1) * C], sd)
+    comm.allgather(me[rank * C: (rank + 1) * C], me)
+    ctx.check(L.tm_ctx_copy_labels(ctx.ptr, 1, _capi.ptr(hw), _capi.ptr(sd), _capi.ptr(me), 0, T, sp))
+    return b, e
+
+
+def polygons_from_labels(ctx, n: int, T: int, t_begin: int, t_end: int, off=None, verts=None):
+    """Traversal, repair and stitch of the seeds in [t_begin, t_end) from the
+    labels already in the context (tm_polygons_from_labels).  Returns
+    (offsets, verts, n_polys, n_slots, stats) with LOCAL offsets."""
+    import torch
+    from . import _capi
+    dev = torch.device("cuda", ctx.device_index)
+    off = off if off is not None else torch.empty(T + 1, dtype=torch.int64, device=dev)
+    verts = verts if verts is not None else torch.empty(max(3 * T, 1), dtype=torch.int32, device=dev)
+    L = _capi.lib()
+    ctx.check(L.tm_ctx_set_partition(ctx.ptr, t_begin, t_end))
+    npol, nsl = ctypes.c_int64(), ctypes.c_int64()
+    stats = (ctypes.c_int64 * _capi.NUM_STATS)()
+    try:
+        ctx.check(L.tm_polygons_from_labels(ctx.ptr, n, T, _capi.ptr(off), _capi.ptr(verts), T, 3 * T,
+                                            ctypes.byref(npol), ctypes.byref(nsl), stats, _capi.stream_ptr(dev)),
+                  "traversal")
+    finally:
+        L.tm_ctx_set_partition(ctx.ptr, 0, -1)
+    return off, verts, npol.value, nsl.value, dict(zip(_capi.STAT_NAMES, list(stats)))
+
+
+def execute_distributed(tri, group=None, gather: bool = True, comm: Comm | None = None, split_labels_mode=False):
     """Drop-in multi-GPU execute: every rank passes the same Triangulation; the
     global final CSR comes back on rank 0 (gather=True) or as shards."""
     import torch
@@ -269,12 +344,16 @@ def execute_distributed(tri, group=None, gather: bool = True, comm: Comm | None 
     dev = torch.device("cuda", torch.cuda.current_device())
     xy = torch.from_numpy(np.ascontiguousarray(tri.vertices)).to(dev)
     tr = torch.from_numpy(np.ascontiguousarray(tri.triangles)).to(dev)
-    b, e = partition(T, world)[rank]
     from . import _capi
     ctx = _capi.context(dev)
-    off, verts, p, f, stats = run_partition(xy, tr, n, T, b, e, ctx=ctx)
-    if comm is None and dist.get_backend(group) == "nccl":
+    if comm is None and (split_labels_mode or dist.get_backend(group) == "nccl"):
         comm = Comm(group)  # the library's own communicator for the exchange
+    if split_labels_mode:
+        b, e = split_labels(ctx, xy, tr, n, T, comm, rank, world)
+        off, verts, p, f, stats = polygons_from_labels(ctx, n, T, b, e)
+    else:
+        b, e = partition(T, world)[rank]
+        off, verts, p, f, stats = run_partition(xy, tr, n, T, b, e, ctx=ctx)
     shard = stitch(off, verts, p, f, group, pinch=(stats["pinch_extra"], stats["pinch_deferred"]),
                    resume=device_resume(ctx, off, verts, T), comm=comm)
     if not gather:

@@ -168,3 +168,47 @@ def test_library_nccl_comm_single_rank(cuda):
         comm.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("name", CASES + ("aniso2k_s2", "clust5k_s3", "grid6x5", "tie5"))
+def test_split_labels_logical_ranks(cuda, name, world):
+    """Seed-partitioned LABELS (tm_label_range + boundary exchange +
+    tm_label_resolve + label all-gather) on logical ranks of one GPU: every
+    rank's labels equal the single-GPU ones and the stitched output equals the
+    reference golden."""
+    import sys
+    import torch
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import split_emulation
+    tri, g = load_case(name)
+    n, T = tri.n_vertices, tri.n_triangles
+    xy = torch.from_numpy(tri.vertices).to(cuda)
+    tr = torch.from_numpy(tri.triangles).to(cuda)
+    parts, out, _ = split_emulation.run(xy, tr, n, T, world)
+    offs, verts, base = [], [], 0
+    for off, v, p, f, st in out:
+        offs.append(off[:p].cpu().numpy() + base)
+        verts.append(v[:f].cpu().numpy())
+        base += f
+    got_off = np.concatenate(offs + [np.array([base])])
+    got_v = np.concatenate(verts)
+    assert np.array_equal(got_off, g["final_off"]) and np.array_equal(got_v, g["final_verts"])
+
+
+@pytest.mark.gpu
+def test_split_labels_single_rank_nccl(cuda):
+    """The real split-label path (distributed.split_labels over the library's
+    NCCL communicator) on a one-rank group."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        for name in ("aniso2k_s1", "u1k_unit"):
+            tri, g = load_case(name)
+            csr, stats = D.execute_distributed(tri, split_labels_mode=True)
+            assert np.array_equal(csr[0], g["final_off"]) and np.array_equal(csr[1], g["final_verts"])
+    finally:
+        dist.destroy_process_group()
