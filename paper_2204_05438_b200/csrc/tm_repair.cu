@@ -1446,7 +1446,7 @@ constexpr int kSegMaxL = 8192;   // longer items keep their per-item arrays in g
 constexpr int kSegMaxG = 21760;
 constexpr int kGPairCap = 65536;  // >= 2 kSegMaxG, power of two
 constexpr int kGRec = 8192;       // piece records per round list (very long items)
-constexpr int kGmBlocks = 2;      // blocks of k_repair_tips_seg that take the pool-region items
+constexpr int kGmBlocks = 6;      // blocks of k_repair_tips_seg that take the pool-region items (several huge hull slivers at 100M)
 constexpr int kGSegCap = 262144;  // segment arena (very long items)
 // pool region of a pool-region block: pair map, round lists, records, segment arena (ints)
 constexpr long long kGStride = (long long)kGPairCap + 2 * (long long)kGRec + 2 * (long long)kGRec * 5 +

@@ -44,6 +44,7 @@ if a.split:
     res = {}
     ctx = _capi.Context(0)
     for G in [int(x) for x in a.gpus.split(",")]:
+        split_emulation.run(xy, tr, n, T, G, flush=flush, ctx=ctx)  # warm-up: scratch sizes for this G, graphs
         runs = [split_emulation.run(xy, tr, n, T, G, flush=flush, ctx=ctx)[2] for _ in range(max(1, a.steps // 3))]
         ranks = []
         for r in range(G):
