@@ -194,10 +194,20 @@ def run_gpu(args, rank, world, local_rank):
     shard = [None]
     comm = D.Comm() if world > 1 else None  # the library's NCCL communicator (tm_comm_*, C ABI)
 
+    split = args.split_labels and world > 1
+    if split:  # seed-partitioned labels: chunk ranges, labels exchanged (distributed.split_labels)
+        t_begin, t_end = D.partition_chunks(T, world)[rank]
+        ctx.check(L.tm_ctx_set_partition(ctx.ptr, t_begin, t_end))
+
     def step():
-        rc = L.tm_mesh_to_polygons(ctx.ptr, _capi.ptr(xy), n, _capi.ptr(tr), 64, T, 0, _capi.ptr(off),
-                                   _capi.ptr(verts), T, 3 * T, ctypes.byref(npol), ctypes.byref(nsl), stats, sp)
-        ctx.check(rc)
+        if split:
+            D.split_labels(ctx, xy, tr, n, T, comm, rank, world)
+            ctx.check(L.tm_polygons_from_labels(ctx.ptr, n, T, _capi.ptr(off), _capi.ptr(verts), T, 3 * T,
+                                                ctypes.byref(npol), ctypes.byref(nsl), stats, sp))
+        else:
+            rc = L.tm_mesh_to_polygons(ctx.ptr, _capi.ptr(xy), n, _capi.ptr(tr), 64, T, 0, _capi.ptr(off),
+                                       _capi.ptr(verts), T, 3 * T, ctypes.byref(npol), ctypes.byref(nsl), stats, sp)
+            ctx.check(rc)
         if world > 1:  # the exchange step: all-gather counts (NCCL), shift to the global slot base
             shard[0] = D.stitch(off, verts, npol.value, nsl.value, pinch=(stats[8], stats[10]),
                                 resume=D.device_resume(ctx, off, verts, T, stats), comm=comm)
@@ -290,6 +300,15 @@ def run_gpu(args, rank, world, local_rank):
     h_v = torch.empty(3 * T, dtype=torch.int32).pin_memory()
 
     def e2e_step():
+        if split:  # host arrays in, the split path, the rank's CSR out
+            xy.copy_(h_xy, non_blocking=True)
+            tr.copy_(h_tr, non_blocking=True)
+            step()
+            P, F = shard[0].n_polys, int(shard[0].verts.numel())
+            h_off[: P + 1].copy_(shard[0].offsets, non_blocking=True)
+            h_v[:F].copy_(shard[0].verts, non_blocking=True)
+            torch.cuda.synchronize()
+            return
         rc = L.tm_mesh_to_polygons_host(ctx.ptr, _capi.ptr(h_xy), n, _capi.ptr(h_tr), T, 0, _capi.ptr(h_off),
                                         _capi.ptr(h_v), T, 3 * T, ctypes.byref(npol), ctypes.byref(nsl), stats)
         ctx.check(rc)
@@ -321,7 +340,7 @@ def run_gpu(args, rank, world, local_rank):
                    "triangles": T, "seed_range_rank0": [t_begin, t_end], "polygons_rank0": P_out,
                    "polygon_slots_rank0": F_out, "l2": "flushed (256 MiB write) between steps",
                    "parallelism": f"replicated mesh, seeds partitioned x{world}, NCCL all-gather of counts "
-                                  f"(tm_comm_allgather)"},
+                                  f"(tm_comm_allgather)" + (", labels partitioned" if split else "")},
         "e2e": e2e, "roofline": roofline, "kernels": kernels, "repair_stats": repair_stats,
         "gpu_launches": int(launches), "clocks": clk.summary(), "parity": parity,
         "step_ms": {"min": round(min(step_ms), 4), "median": round(statistics.median(step_ms), 4),
@@ -478,6 +497,8 @@ def main():
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--workload", choices=tuple(WORKLOADS), default="u10m")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--split-labels", action="store_true",
+                    help="N > 1: each rank labels its own triangle chunk (distributed.split_labels)")
     ap.add_argument("--probe-launch", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup

@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -181,6 +182,10 @@ struct tm_ctx {
   // host-array runs: counters reset and label pass A were enqueued by the
   // caller, chunk by chunk behind the triangle upload (copy/compute overlap)
   bool label_a_external = false;
+  // host-array entry: pinned int32 staging of the triangles (host-side narrowing)
+  int32_t* h_tri32 = nullptr;
+  int64_t h_tri32_cap = 0;
+  bool host_narrow = true;  // TERMESH_NO_NARROW=1: upload the int64 triangles as they are (A/B)
   // seed-partitioned labels: tri32 / hw / max_edge / seed of the whole mesh were
   // filled by tm_label_range + tm_label_resolve + the ranks' all-gather
   bool labels_external = false;
@@ -197,6 +202,15 @@ struct tm_ctx {
   int64_t last_T = -1;
   bool last_host = false;
 };
+
+// host threads for a host-side pass over `work` elements
+static int host_workers(int64_t work) {
+  unsigned hc = std::thread::hardware_concurrency();
+  int t = hc ? (int)hc : 1;
+  if (t > 16) t = 16;
+  const int64_t need = work / (1 << 20) + 1;
+  return (int)(need < t ? need : t);
+}
 
 static int set_err(tm_ctx* c, int code, const char* fmt, ...) {
   char buf[1024];
@@ -662,6 +676,8 @@ int tm_ctx_create(tm_ctx** out) {
   *out = new tm_ctx();
   const char* g = getenv("TERMESH_NO_GRAPH");
   if (g && *g && *g != '0') (*out)->use_graph = 0;
+  const char* nn = getenv("TERMESH_NO_NARROW");  // A/B switch
+  if (nn && *nn && *nn != '0') (*out)->host_narrow = false;
   const char* x32 = getenv("TERMESH_XY32");  // A/B switch
   if (x32 && *x32 && *x32 != '0') (*out)->use_xy32 = 1;
   const char* ts = getenv("TERMESH_TABLE_SHRINK");  // testing hook: start with a 2^-s table (overflow/growth path)
@@ -683,6 +699,7 @@ void tm_ctx_destroy(tm_ctx* ctx) {
                  &ctx->dsxy, &ctx->dcnt, &ctx->doff, &ctx->xy32, &ctx->btab};
   for (Buf* b : bufs) b->release();
   if (ctx->h_reset) cudaFreeHost(ctx->h_reset);
+  if (ctx->h_tri32) cudaFreeHost(ctx->h_tri32);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
@@ -1150,7 +1167,19 @@ int tm_mesh_to_polygons_host(tm_ctx* ctx, const double* h_xy, int64_t n, const i
     if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   // Upload overlap: the vertices first (pass A gathers them at random), then
   // the triangles in chunks on a copy stream; label pass A runs on each chunk
-  // as soon as it lands, so only the last chunk's pass A is exposed.
+  // as soon as it lands, so only the last chunk's pass A is exposed.  The
+  // triangles are narrowed int64 -> int32 on the host first (host threads,
+  // chunk k+1 while chunk k is in flight) into a pinned staging buffer: half
+  // the PCIe bytes; an index outside [0, n) becomes -1, which the label pass
+  // reports as index_range exactly like the int64 value.
+  const bool narrow = ctx->host_narrow && T > 0;
+  if (narrow && ctx->h_tri32_cap < 3 * Tn) {
+    if (ctx->h_tri32) cudaFreeHost(ctx->h_tri32);
+    ctx->h_tri32 = nullptr;
+    ctx->h_tri32_cap = 0;
+    CK(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_tri32), 3 * Tn * sizeof(int32_t)));
+    ctx->h_tri32_cap = 3 * Tn;
+  }
   CK(cudaMemcpyAsync(ctx->xy.p, h_xy, 2 * n * sizeof(double), cudaMemcpyHostToDevice, s));
   if ((rc = enqueue_reset(ctx, s))) return rc;
   const int shrink = check && ctx->table_shrink > 0 ? 0 : ctx->table_shrink;
@@ -1159,21 +1188,58 @@ int tm_mesh_to_polygons_host(tm_ctx* ctx, const double* h_xy, int64_t n, const i
   if (xy32) launch_xy32(ctx->xy.as<double>(), n, xy32, s);
   CK(cudaEventRecord(ctx->chunk_ev[0], s));
   CK(cudaStreamWaitEvent(ctx->cstream, ctx->chunk_ev[0], 0));  // table reset before any chunk's pass A
-  for (int k = 0; k < kUploadChunks; k++) {
+  // host narrowing workers: worker w converts its slice of every chunk in
+  // order and counts chunk k done; the main thread enqueues chunk k's copy as
+  // soon as all workers have passed it
+  std::vector<std::thread> workers;
+  std::atomic<int> done[kUploadChunks];
+  for (auto& d : done) d.store(0);
+  const int nw = narrow ? host_workers(3 * T) : 0;
+  int32_t* st32 = ctx->h_tri32;
+  for (int w = 0; w < nw; w++)
+    workers.emplace_back([&, w] {
+      for (int k = 0; k < kUploadChunks; k++) {
+        const int64_t a = 3 * (T * k / kUploadChunks), b = 3 * (T * (k + 1) / kUploadChunks);
+        const int64_t x0 = a + (b - a) * w / nw, x1 = a + (b - a) * (w + 1) / nw;
+        for (int64_t i = x0; i < x1; i++) {
+          const int64_t x = h_tri[i];
+          st32[i] = (x >= 0 && x < n) ? (int32_t)x : -1;
+        }
+        done[k].fetch_add(1, std::memory_order_release);
+      }
+    });
+  int crc = TM_OK;
+  for (int k = 0; k < kUploadChunks && crc == TM_OK; k++) {
     const int64_t t0 = T * k / kUploadChunks, t1 = T * (k + 1) / kUploadChunks;
-    if (t1 > t0)
-      CK(cudaMemcpyAsync(ctx->tri.as<int64_t>() + 3 * t0, h_tri + 3 * t0, 3 * (t1 - t0) * sizeof(int64_t),
-                         cudaMemcpyHostToDevice, ctx->cstream));
-    CK(cudaEventRecord(ctx->chunk_ev[k], ctx->cstream));
-    CK(cudaStreamWaitEvent(s, ctx->chunk_ev[k], 0));
-    launch_label_a_range(ctx->xy.as<double>(), n, ctx->tri.p, 1, T, t0, t1, check, ctx->tri32.as<int32_t>(),
-                         ctx->hw.as<int32_t>(), ctx->max_edge.as<int8_t>(), ctx->seed.as<uint8_t>(), nullptr,
-                         ctx->slots.p, &dc_of(ctx)->st, s, shrink, &dc_of(ctx)->table_ovf, xy32);
+    if (narrow) {
+      while (done[k].load(std::memory_order_acquire) < nw) std::this_thread::yield();
+      if (t1 > t0 && cudaMemcpyAsync(ctx->tri32.as<int32_t>() + 3 * t0, st32 + 3 * t0,
+                                     3 * (t1 - t0) * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                     ctx->cstream) != cudaSuccess)
+        crc = TM_ERR_CUDA;
+    } else if (t1 > t0 && cudaMemcpyAsync(ctx->tri.as<int64_t>() + 3 * t0, h_tri + 3 * t0,
+                                          3 * (t1 - t0) * sizeof(int64_t), cudaMemcpyHostToDevice,
+                                          ctx->cstream) != cudaSuccess) {
+      crc = TM_ERR_CUDA;
+    }
+    if (crc) break;
+    cudaEventRecord(ctx->chunk_ev[k], ctx->cstream);
+    cudaStreamWaitEvent(s, ctx->chunk_ev[k], 0);
+    if (narrow)
+      launch_label_a_range(ctx->xy.as<double>(), n, ctx->tri32.p, 0, T, t0, t1, check, ctx->tri32.as<int32_t>(),
+                           ctx->hw.as<int32_t>(), ctx->max_edge.as<int8_t>(), ctx->seed.as<uint8_t>(), nullptr,
+                           ctx->slots.p, &dc_of(ctx)->st, s, shrink, &dc_of(ctx)->table_ovf, xy32);
+    else
+      launch_label_a_range(ctx->xy.as<double>(), n, ctx->tri.p, 1, T, t0, t1, check, ctx->tri32.as<int32_t>(),
+                           ctx->hw.as<int32_t>(), ctx->max_edge.as<int8_t>(), ctx->seed.as<uint8_t>(), nullptr,
+                           ctx->slots.p, &dc_of(ctx)->st, s, shrink, &dc_of(ctx)->table_ovf, xy32);
   }
+  for (auto& t : workers) t.join();
+  if (crc) return set_err(ctx, crc, "triangle upload failed");
   CK(cudaGetLastError());
   ctx->label_a_external = true;
-  rc = run_device(ctx, ctx->xy.as<double>(), n, ctx->tri.p, 64, T, check, ctx->fin_off.as<int64_t>(),
-                  ctx->fin_v.as<int32_t>(), n_polys, n_slots, stats, s);
+  rc = run_device(ctx, ctx->xy.as<double>(), n, narrow ? ctx->tri32.p : ctx->tri.p, narrow ? 32 : 64, T, check,
+                  ctx->fin_off.as<int64_t>(), ctx->fin_v.as<int32_t>(), n_polys, n_slots, stats, s);
   ctx->label_a_external = false;
   ctx->last_host = true;
   if (rc == kRetryTable)  // the half-size twin table overflowed: once more at full size

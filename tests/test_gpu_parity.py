@@ -114,6 +114,44 @@ def test_host_c_abi_one_call(cuda, name):
     assert list(stats)[:4] == g["stats"].tolist()
 
 
+@pytest.mark.parametrize("narrow", ["1", "0"])
+def test_host_c_abi_invalid_and_narrowing(cuda, narrow, monkeypatch):
+    """The host entry narrows the int64 triangles on the host (default) or
+    uploads them as they are (TERMESH_NO_NARROW=1): same output, and with
+    check=1 an out-of-range corner (also one beyond int32) is a validation error
+    on both paths, raised before any traversal."""
+    from paper_2204_05438_b200 import _capi
+    from paper_2204_05438_b200.errors import ValidationError
+    if narrow == "0":
+        monkeypatch.setenv("TERMESH_NO_NARROW", "1")
+    ctx = _capi.Context(cuda.index or 0)
+    for name in ("aniso2k_s1", "u1k_unit"):
+        tri, g = load_case(name)
+        T = tri.n_triangles
+        off = np.zeros(T + 1, dtype=np.int64)
+        verts = np.zeros(3 * T, dtype=np.int32)
+        npol, nsl = ctypes.c_int64(), ctypes.c_int64()
+        stats = (ctypes.c_int64 * _capi.NUM_STATS)()
+        for check in (0, 1):
+            rc = _capi.lib().tm_mesh_to_polygons_host(ctx.ptr, _capi.ptr(tri.vertices), tri.n_vertices,
+                                                      _capi.ptr(tri.triangles), T, check, _capi.ptr(off),
+                                                      _capi.ptr(verts), T, 3 * T, ctypes.byref(npol),
+                                                      ctypes.byref(nsl), stats)
+            ctx.check(rc)
+            assert np.array_equal(off[: npol.value + 1], g["final_off"])
+            assert np.array_equal(verts[: nsl.value].astype(np.int64), g["final_verts"])
+        for bad in (tri.n_vertices, -5, 1 << 40):
+            t2 = tri.triangles.copy()
+            t2[3 * (T // 2) + 1] = bad
+            rc = _capi.lib().tm_mesh_to_polygons_host(ctx.ptr, _capi.ptr(tri.vertices), tri.n_vertices,
+                                                      _capi.ptr(t2), T, 1, _capi.ptr(off), _capi.ptr(verts), T,
+                                                      3 * T, ctypes.byref(npol), ctypes.byref(nsl), stats)
+            with pytest.raises(ValidationError) as ei:
+                ctx.check(rc)
+            assert "index_range" in str(ei.value)
+    ctx.close()
+
+
 def test_host_c_abi_u1m_hashes(cuda):
     """The one-call host path at full size (chunked upload overlapped with label
     pass A): final CSR byte-equal to the reference (hashes.json)."""
