@@ -185,7 +185,9 @@ struct tm_ctx {
   // host-array entry: pinned int32 staging of the triangles (host-side narrowing)
   int32_t* h_tri32 = nullptr;
   int64_t h_tri32_cap = 0;
-  bool host_narrow = true;  // TERMESH_NO_NARROW=1: upload the int64 triangles as they are (A/B)
+  // measured: no gain at 10M (19.2 vs 19.4 ms e2e), +0.6 ms at 1M (thread start-up): the
+  // host-side narrowing pass costs about what it saves on PCIe.  Off unless TERMESH_NARROW=1.
+  bool host_narrow = false;
   // seed-partitioned labels: tri32 / hw / max_edge / seed of the whole mesh were
   // filled by tm_label_range + tm_label_resolve + the ranks' all-gather
   bool labels_external = false;
@@ -676,8 +678,8 @@ int tm_ctx_create(tm_ctx** out) {
   *out = new tm_ctx();
   const char* g = getenv("TERMESH_NO_GRAPH");
   if (g && *g && *g != '0') (*out)->use_graph = 0;
-  const char* nn = getenv("TERMESH_NO_NARROW");  // A/B switch
-  if (nn && *nn && *nn != '0') (*out)->host_narrow = false;
+  const char* nn = getenv("TERMESH_NARROW");  // A/B switch
+  if (nn && *nn && *nn != '0') (*out)->host_narrow = true;
   const char* x32 = getenv("TERMESH_XY32");  // A/B switch
   if (x32 && *x32 && *x32 != '0') (*out)->use_xy32 = 1;
   const char* ts = getenv("TERMESH_TABLE_SHRINK");  // testing hook: start with a 2^-s table (overflow/growth path)

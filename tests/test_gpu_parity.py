@@ -116,14 +116,14 @@ def test_host_c_abi_one_call(cuda, name):
 
 @pytest.mark.parametrize("narrow", ["1", "0"])
 def test_host_c_abi_invalid_and_narrowing(cuda, narrow, monkeypatch):
-    """The host entry narrows the int64 triangles on the host (default) or
-    uploads them as they are (TERMESH_NO_NARROW=1): same output, and with
+    """The host entry uploads the int64 triangles as they are (default) or
+    narrows them to int32 on host threads first (TERMESH_NARROW=1): same output, and with
     check=1 an out-of-range corner (also one beyond int32) is a validation error
     on both paths, raised before any traversal."""
     from paper_2204_05438_b200 import _capi
     from paper_2204_05438_b200.errors import ValidationError
-    if narrow == "0":
-        monkeypatch.setenv("TERMESH_NO_NARROW", "1")
+    if narrow == "1":
+        monkeypatch.setenv("TERMESH_NARROW", "1")
     ctx = _capi.Context(cuda.index or 0)
     for name in ("aniso2k_s1", "u1k_unit"):
         tri, g = load_case(name)
