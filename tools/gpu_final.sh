@@ -26,9 +26,14 @@ timeout 1500 ncu --set full --metrics $EXTRA --clock-control none --import-sourc
    -o gpurun_out/prof_u10m python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full_u10m.log 2>&1
 ncu -i gpurun_out/prof_u10m.ncu-rep --page raw --csv > gpurun_out/prof_u10m_raw.csv 2>&1
 timeout 900 python tools/partition_scaling.py --workload u10m --steps 10 > gpurun_out/scaling_u10m.json 2>&1
+timeout 900 python tools/partition_scaling.py --workload u10m --steps 6 --split > gpurun_out/scaling_split_u10m.json 2>&1
+timeout 900 python tools/delaunay_check.py 10000000 --against qhull > gpurun_out/delaunay_10m.log 2>&1
+TRACE_WORKLOAD=u1m timeout 600 python tools/trace_long.py > gpurun_out/trace_u1m.log 2>&1
 ( time python -c "import bench; t = bench.load_mesh('u100m', 0)" ) > gpurun_out/gen_u100m.log 2>&1
 timeout 1200 python bench.py --workload u100m --steps 10 --warmup 3 > gpurun_out/bench_u100m.json 2> gpurun_out/bench_u100m.err
 timeout 1800 python tools/partition_scaling.py --workload u100m --steps 5 > gpurun_out/scaling_u100m.json 2>&1
+timeout 2400 python tools/partition_scaling.py --workload u100m --steps 3 --split > gpurun_out/scaling_split_u100m.json 2>&1
+timeout 1800 python tools/delaunay_check.py 100000000 --against tiled > gpurun_out/delaunay_100m.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches_u100m.csv \
    python bench.py --workload u100m --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_launch_u100m.log 2>&1
 timeout 2400 python tools/check_100m.py --workload u100m > gpurun_out/check_u100m.log 2>&1
