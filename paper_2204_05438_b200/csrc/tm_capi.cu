@@ -1501,8 +1501,8 @@ int tm_ctx_copy_labels(tm_ctx* ctx, int to_ctx, int32_t* d_hw, uint8_t* d_seed, 
 int tm_label_resolve(tm_ctx* ctx, const uint64_t* d_keys_all, const int32_t* d_vals_all, int64_t n_all,
                      int64_t own_begin, int64_t own_count, void* stream) {
   if (!ctx || n_all < 0 || own_begin < 0 || own_count < 0 || own_begin + own_count > n_all) return TM_ERR_ARGUMENT;
-  int64_t slots = 64;
-  while (slots < 2 * n_all + 64) slots <<= 1;
+  int64_t slots = 64;  // a table of this rank's entries only (k_boundary_insert / k_boundary_match)
+  while (slots < 2 * own_count + 64) slots <<= 1;
   ENSURE(btab, slots * sizeof(int32_t));
   launch_boundary_resolve(reinterpret_cast<const unsigned long long*>(d_keys_all), d_vals_all, n_all, own_begin,
                           own_begin + own_count, ctx->btab.as<int32_t>(), slots, ctx->hw.as<int32_t>(),

@@ -601,7 +601,7 @@ void launch_label_b(const int32_t* tri32, int64_t n, int64_t T, int32_t* hw, con
 // (passes A and B restricted to the range); half-edges still unpaired are
 // either true border or have their partner in another rank's range: they are
 // listed as boundary entries (key (lo << 32) | hi, value (h << 1) | longest)
-// for the exchange, after which k_boundary_resolve labels the cross pairs.
+// for the exchange, after which k_boundary_insert / k_boundary_match label the cross pairs.
 size_t hash_bytes_range(int64_t n, int64_t T, int64_t keyT) {
   TwinTable tb = table_geometry(n, T, nullptr, 0, nullptr, keyT);
   return (size_t)(tb.nb_mask + 1) * 4 * sizeof(unsigned long long);
@@ -683,33 +683,37 @@ __device__ __forceinline__ uint64_t bhash(unsigned long long key, uint64_t mask)
   return ((key * 0x9E3779B97F4A7C15ull) >> 17) & mask;
 }
 
-__global__ void k_boundary_insert(const unsigned long long* __restrict__ keys, int64_t n_all, int32_t* __restrict__ tab,
-                                  uint64_t mask) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n_all; k += (int64_t)gridDim.x * blockDim.x) {
+// own entries [own0, own1) go into a small table (this rank's share); every
+// other rank's entry probes it, and a hit labels this side of the pair
+// (labeling.py:65-115).  Reads of a small table instead of every rank
+// inserting every entry.
+__global__ void k_boundary_insert(const unsigned long long* __restrict__ keys, int64_t own0, int64_t own1,
+                                  int32_t* __restrict__ tab, uint64_t mask) {
+  for (int64_t k = own0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < own1;
+       k += (int64_t)gridDim.x * blockDim.x) {
     if (keys[k] == ~0ull) continue;  // padding of a fixed-size all-gather
     uint64_t h = bhash(keys[k], mask);
     while (atomicCAS(tab + h, -1, (int32_t)k) != -1) h = (h + 1) & mask;
   }
 }
 
-// own entries [own0, own1) of the concatenated list: find the entry with the
-// same key from another range, label this side of the pair (labeling.py:65-115)
-__global__ void k_boundary_resolve(const unsigned long long* __restrict__ keys, const int32_t* __restrict__ vals,
-                                   int64_t own0, int64_t own1, const int32_t* __restrict__ tab, uint64_t mask,
-                                   int32_t* __restrict__ hw, uint8_t* __restrict__ seed) {
-  for (int64_t k = own0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < own1;
-       k += (int64_t)gridDim.x * blockDim.x) {
+__global__ void k_boundary_match(const unsigned long long* __restrict__ keys, const int32_t* __restrict__ vals,
+                                 int64_t n_all, int64_t own0, int64_t own1, const int32_t* __restrict__ tab,
+                                 uint64_t mask, int32_t* __restrict__ hw, uint8_t* __restrict__ seed) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n_all; k += (int64_t)gridDim.x * blockDim.x) {
+    if (k >= own0 && k < own1) continue;
     const unsigned long long key = keys[k];
+    if (key == ~0ull) continue;
     uint64_t h = bhash(key, mask);
-    int32_t partner = -1;
+    int32_t mine = -1;
     for (;;) {
       const int32_t x = tab[h];
       if (x < 0) break;
-      if (x != k && keys[x] == key) { partner = x; break; }
+      if (keys[x] == key) { mine = x; break; }
       h = (h + 1) & mask;
     }
-    if (partner < 0) continue;  // true border: stays -1 (frontier), provisional seed stays
-    const int32_t me = vals[k], pv = vals[partner];
+    if (mine < 0) continue;
+    const int32_t me = vals[mine], pv = vals[k];
     const int32_t he = me >> 1, hp = pv >> 1;
     const bool own = me & 1, other = pv & 1;
     hw[he] = (hp << 1) | ((!own && !other) ? 1 : 0);
@@ -724,31 +728,12 @@ void launch_boundary_resolve(const unsigned long long* keys, const int32_t* vals
                              int64_t own1, int32_t* tab, int64_t tab_slots, int32_t* hw, uint8_t* seed,
                              cudaStream_t s) {
   cudaMemsetAsync(tab, 0xFF, (size_t)tab_slots * sizeof(int32_t), s);
-  if (n_all > 0) k_boundary_insert<<<grid_for(n_all, 256), 256, 0, s>>>(keys, n_all, tab, (uint64_t)(tab_slots - 1));
   if (own1 > own0)
-    k_boundary_resolve<<<grid_for(own1 - own0, 256), 256, 0, s>>>(keys, vals, own0, own1, tab,
-                                                                  (uint64_t)(tab_slots - 1), hw, seed);
+    k_boundary_insert<<<grid_for(own1 - own0, 256), 256, 0, s>>>(keys, own0, own1, tab, (uint64_t)(tab_slots - 1));
+  if (n_all > own1 - own0)
+    k_boundary_match<<<grid_for(n_all, 256), 256, 0, s>>>(keys, vals, n_all, own0, own1, tab,
+                                                          (uint64_t)(tab_slots - 1), hw, seed);
   note_launch(2);
-}
-
-void launch_relabel(const int8_t* max_edge, int64_t T, int32_t* hw, uint8_t* seed, cudaStream_t s) {
-  if (T > 0) k_label_edges<<<grid_for(T, 256), 256, 0, s>>>(max_edge, T, hw, seed, 1), note_launch(1);
-}
-
-void launch_check_neighbors(const int32_t* hw, const void* nb, int nb_is64, int64_t T, DevStatus* st, cudaStream_t s) {
-  if (T <= 0) return;
-  if (nb_is64)
-    k_check_neighbors<int64_t><<<grid_for(3 * T, 256), 256, 0, s>>>(hw, (const int64_t*)nb, 3 * T, st);
-  else
-    k_check_neighbors<int32_t><<<grid_for(3 * T, 256), 256, 0, s>>>(hw, (const int32_t*)nb, 3 * T, st);
-}
-
-void launch_unpack(const int32_t* hw, int64_t T, int32_t* twin, uint8_t* fr, cudaStream_t s) {
-  if (T > 0) k_unpack<<<grid_for(3 * T, 256), 256, 0, s>>>(hw, 3 * T, twin, fr);
-}
-
-void launch_pack_frontier(int32_t* hw, int64_t T, const uint8_t* fr, cudaStream_t s) {
-  if (T > 0) k_pack_frontier<<<grid_for(3 * T, 256), 256, 0, s>>>(hw, 3 * T, fr);
 }
 
 }  // namespace tmb
