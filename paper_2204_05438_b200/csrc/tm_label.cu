@@ -736,4 +736,24 @@ void launch_boundary_resolve(const unsigned long long* keys, const int32_t* vals
   note_launch(2);
 }
 
+void launch_relabel(const int8_t* max_edge, int64_t T, int32_t* hw, uint8_t* seed, cudaStream_t s) {
+  if (T > 0) k_label_edges<<<grid_for(T, 256), 256, 0, s>>>(max_edge, T, hw, seed, 1), note_launch(1);
+}
+
+void launch_check_neighbors(const int32_t* hw, const void* nb, int nb_is64, int64_t T, DevStatus* st, cudaStream_t s) {
+  if (T <= 0) return;
+  if (nb_is64)
+    k_check_neighbors<int64_t><<<grid_for(3 * T, 256), 256, 0, s>>>(hw, (const int64_t*)nb, 3 * T, st);
+  else
+    k_check_neighbors<int32_t><<<grid_for(3 * T, 256), 256, 0, s>>>(hw, (const int32_t*)nb, 3 * T, st);
+}
+
+void launch_unpack(const int32_t* hw, int64_t T, int32_t* twin, uint8_t* fr, cudaStream_t s) {
+  if (T > 0) k_unpack<<<grid_for(3 * T, 256), 256, 0, s>>>(hw, 3 * T, twin, fr);
+}
+
+void launch_pack_frontier(int32_t* hw, int64_t T, const uint8_t* fr, cudaStream_t s) {
+  if (T > 0) k_pack_frontier<<<grid_for(3 * T, 256), 256, 0, s>>>(hw, 3 * T, fr);
+}
+
 }  // namespace tmb
