@@ -318,8 +318,12 @@ __global__ void __launch_bounds__(kLabelThreads, 4) k_tri_pass(const double2* __
         me0 = -1;
         if (xy32 != nullptr) me0 = argmax3_32(xy32[a], xy32[b], xy32[c]);
         if (me0 < 0) {
+#ifdef TM_AB_NO_XY  // A/B timing builds only (wrong labels): what the coordinate gathers cost
+          me0 = (int)(t % 3);
+#else
           const double2 pa = xy[a], pb = xy[b], pc = xy[c];
           me0 = argmax3(sqlen(pb, pc), sqlen(pc, pa), sqlen(pa, pb));
+#endif
         }
         max_edge[t] = (int8_t)me0;
         if (check) {
@@ -386,7 +390,9 @@ __global__ void __launch_bounds__(kLabelThreads, 4) k_tri_pass(const double2* __
         if (lslot[j] >= 0 && (lval[lslot[j]] & kLocalMatched)) flags &= ~(1u << j);
     }
     int m = warp_compact3(flags, lane, sq[wid][0], sq[wid][1], sq[wid][2], hh, oo, gg);
+#ifndef TM_AB_NO_TABLE  // A/B timing builds only (wrong labels): what the table inserts cost
     for (int i = lane; i < m; i += 32) table_insert(tb, st, sq[wid][0][i], sq[wid][1][i], sq[wid][2][i]);
+#endif
     __syncwarp();
     if (local) __syncthreads();  // lkey/lval are reset at the top of the next chunk
   }
