@@ -22,6 +22,8 @@
 #include "tm_common.cuh"
 #include "tm_internal.h"
 
+#include <utility>
+
 namespace tmb {
 
 // ---------------------------------------------------------------- twin table
@@ -273,8 +275,14 @@ __device__ __forceinline__ void label_pair(int32_t* __restrict__ hw, uint8_t* __
 // ascending half-edge goes to the global table so that the claim bits see all
 // partners); then the warp's remaining ascending half-edges (origin < target)
 // go into the twin table on dense lanes.
+#ifndef TM_TRI_MINB
+#define TM_TRI_MINB 4
+#endif
+#ifndef TM_PAIR_MINB
+#define TM_PAIR_MINB 6
+#endif
 template <typename TI>
-__global__ void __launch_bounds__(kLabelThreads, 4) k_tri_pass(const double2* __restrict__ xy,
+__global__ void __launch_bounds__(kLabelThreads, TM_TRI_MINB) k_tri_pass(const double2* __restrict__ xy,
                                                             const float2* __restrict__ xy32, int64_t n,
                                                             const TI* __restrict__ tri, int64_t t_begin,
                                                             int64_t T,
@@ -406,7 +414,7 @@ __global__ void __launch_bounds__(kLabelThreads, 4) k_tri_pass(const double2* __
 // on the lower triangle).  k = twin % 3 replaces the reference's back-slot
 // searches.  A half-edge without a partner stays border as pass A wrote it
 // (an ascending one keeps its provisional seed flag).
-__global__ void __launch_bounds__(kLabelThreads, 6) k_pair_pass(const int32_t* __restrict__ tri32, int64_t t_begin,
+__global__ void __launch_bounds__(kLabelThreads, TM_PAIR_MINB) k_pair_pass(const int32_t* __restrict__ tri32, int64_t t_begin,
                                                              int64_t T,
                                                              const int8_t* __restrict__ max_edge, TwinTable tb,
                                                              int32_t* __restrict__ hw, uint8_t* __restrict__ seed,
@@ -510,6 +518,32 @@ static inline int grid_for(int64_t n, int block) {
   return (int)(g < 1 ? 1 : g);
 }
 
+// Grid of a grid-stride label kernel: exactly the resident blocks (occupancy x
+// SMs) when the work spans more, so no partial last wave -- at 10M the former
+// 16-per-SM grid ran k_tri_pass in 3.2 waves of 5 resident blocks (the last
+// 0.2 wave at one block per SM) and k_pair_pass in 2.67 of 6.
+template <typename K>
+static int resident_grid(K* fn, int64_t n, int block) {
+#ifdef TM_GRID16  // A/B: the former grid
+  return grid_for(n, block);
+#endif
+  static thread_local std::pair<const void*, int> cache[8];
+  int per_sm = 0;
+  for (auto& c : cache)
+    if (c.first == (const void*)fn) per_sm = c.second;
+  if (per_sm == 0) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, 0) != cudaSuccess || per_sm < 1) per_sm = 4;
+    for (auto& c : cache)
+      if (c.first == nullptr) {
+        c = {(const void*)fn, per_sm};
+        break;
+      }
+  }
+  const int64_t need = (n + block - 1) / block, cap = (int64_t)kNumSMs * per_sm;
+  return (int)(need < 1 ? 1 : need < cap ? need : cap);
+}
+
 static int bit_length(uint64_t v) {
   int b = 0;
   while (v) { b++; v >>= 1; }
@@ -571,7 +605,8 @@ void launch_label_a_range(const double* xy, int64_t n, const void* tri, int tri_
   TwinTable tb = table_geometry(n, T, table, shrink, ovf);
   if (t_end > t_begin) {
     const int B = kLabelThreads;
-    const int g = grid_for(t_end - t_begin, B);
+    const int g = tri_is64 ? resident_grid(k_tri_pass<int64_t>, t_end - t_begin, B)
+                           : resident_grid(k_tri_pass<int32_t>, t_end - t_begin, B);
     if (tri_is64)
       k_tri_pass<int64_t><<<g, B, 0, s>>>((const double2*)xy, (const float2*)xy32, n, (const int64_t*)tri, t_begin,
                                           t_end, tri32, max_edge, tb, hw, seed, tv, check, st);
@@ -596,7 +631,7 @@ void launch_label_b(const int32_t* tri32, int64_t n, int64_t T, int32_t* hw, con
   TwinTable tb = table_geometry(n, T, table, shrink);
   int64_t m = (T > n || tv == nullptr) ? T : n;
   if (m > 0) {
-    k_pair_pass<<<grid_for(m, kLabelThreads), kLabelThreads, 0, s>>>(tri32, 0, T, max_edge, tb, hw, seed, tv, n,
+    k_pair_pass<<<resident_grid(k_pair_pass, m, kLabelThreads), kLabelThreads, 0, s>>>(tri32, 0, T, max_edge, tb, hw, seed, tv, n,
                                                                      check, st);
     note_launch(1);
   }
@@ -619,7 +654,8 @@ void launch_label_range(const double* xy, int64_t n, const void* tri, int tri_is
   const TwinTable tb = table_geometry(n, T, table, 0, ovf, e - b);
   cudaMemsetAsync(table, 0xFF, (size_t)(tb.nb_mask + 1) * 4 * sizeof(unsigned long long), s);
   if (e <= b) return;
-  const int g = grid_for(e - b, kLabelThreads);
+  const int g = tri_is64 ? resident_grid(k_tri_pass<int64_t>, e - b, kLabelThreads)
+                         : resident_grid(k_tri_pass<int32_t>, e - b, kLabelThreads);
   if (tri_is64)
     k_tri_pass<int64_t><<<g, kLabelThreads, 0, s>>>((const double2*)xy, nullptr, n, (const int64_t*)tri, b, e, tri32,
                                                     max_edge, tb, hw, seed, nullptr, 0, st);
@@ -627,7 +663,7 @@ void launch_label_range(const double* xy, int64_t n, const void* tri, int tri_is
     k_tri_pass<int32_t><<<g, kLabelThreads, 0, s>>>((const double2*)xy, nullptr, n, (const int32_t*)tri, b, e,
                                                     tri32 == tri ? nullptr : tri32, max_edge, tb, hw, seed, nullptr, 0,
                                                     st);
-  k_pair_pass<<<g, kLabelThreads, 0, s>>>(tri32, b, e, max_edge, tb, hw, seed, nullptr, n, 0, st);
+  k_pair_pass<<<resident_grid(k_pair_pass, e - b, kLabelThreads), kLabelThreads, 0, s>>>(tri32, b, e, max_edge, tb, hw, seed, nullptr, n, 0, st);
   note_launch(2);
 }
 
