@@ -188,6 +188,9 @@ struct tm_ctx {
   // measured: no gain at 10M (19.2 vs 19.4 ms e2e), +0.6 ms at 1M (thread start-up): the
   // host-side narrowing pass costs about what it saves on PCIe.  Off unless TERMESH_NARROW=1.
   bool host_narrow = false;
+  // single-pass labels (tm_label.cu single_pass): -1 host-array entry only
+  // (pass A overlaps the upload), 0 never, 1 every unchecked call (TERMESH_LABEL_ONE)
+  int label_one = -1;
   // seed-partitioned labels: tri32 / hw / max_edge / seed of the whole mesh were
   // filled by tm_label_range + tm_label_resolve + the ranks' all-gather
   bool labels_external = false;
@@ -434,6 +437,10 @@ static int prepare(tm_ctx* ctx, int64_t T, int64_t n = -1) {
 }
 
 // ---------------------------------------------------------------- enqueue (no host syncs)
+static int label_one(const tm_ctx* ctx) {
+  return ctx->label_one < 0 ? (ctx->label_a_external ? 1 : 0) : ctx->label_one;
+}
+
 static int enqueue_label(tm_ctx* ctx, const double* d_xy, int64_t n, const void* d_tri, int tri_bits, int64_t T,
                          int check, int32_t* d_tri32, int32_t* d_hw, int8_t* d_me, uint8_t* d_seed, int32_t* d_tv,
                          cudaStream_t s) {
@@ -445,13 +452,14 @@ static int enqueue_label(tm_ctx* ctx, const double* d_xy, int64_t n, const void*
   if (!ctx->label_a_external) {
     SegTimer t_(ctx, S_LABEL_A, s);
     launch_label_a(d_xy, n, d_tri, tri_bits == 64, T, check, d_tri32, d_hw, d_me, d_seed, d_tv, ctx->slots.p,
-                   &dc->st, s, shrink, &dc->table_ovf, ctx->use_xy32 ? ctx->xy32.as<float>() : nullptr);
+                   &dc->st, s, shrink, &dc->table_ovf, ctx->use_xy32 ? ctx->xy32.as<float>() : nullptr,
+                   label_one(ctx));
   }
   if (lt) CK(cudaEventRecord(ctx->lev[1], s));
   {
     SegTimer t_(ctx, S_LABEL_B, s);
     launch_label_b(tri_bits == 32 && d_tri32 == nullptr ? (const int32_t*)d_tri : d_tri32, n, T, d_hw, d_me, d_seed,
-                   d_tv, ctx->slots.p, check, &dc->st, s, shrink);
+                   d_tv, ctx->slots.p, check, &dc->st, s, shrink, label_one(ctx));
   }
   if (lt) CK(cudaEventRecord(ctx->lev[2], s));
   CK(cudaGetLastError());
@@ -680,6 +688,8 @@ int tm_ctx_create(tm_ctx** out) {
   if (g && *g && *g != '0') (*out)->use_graph = 0;
   const char* nn = getenv("TERMESH_NARROW");  // A/B switch
   if (nn && *nn && *nn != '0') (*out)->host_narrow = true;
+  const char* lo = getenv("TERMESH_LABEL_ONE");  // A/B switch / testing hook
+  if (lo && *lo) (*out)->label_one = atoi(lo) ? 1 : 0;
   const char* x32 = getenv("TERMESH_XY32");  // A/B switch
   if (x32 && *x32 && *x32 != '0') (*out)->use_xy32 = 1;
   const char* ts = getenv("TERMESH_TABLE_SHRINK");  // testing hook: start with a 2^-s table (overflow/growth path)
@@ -1230,11 +1240,11 @@ int tm_mesh_to_polygons_host(tm_ctx* ctx, const double* h_xy, int64_t n, const i
     if (narrow)
       launch_label_a_range(ctx->xy.as<double>(), n, ctx->tri32.p, 0, T, t0, t1, check, ctx->tri32.as<int32_t>(),
                            ctx->hw.as<int32_t>(), ctx->max_edge.as<int8_t>(), ctx->seed.as<uint8_t>(), nullptr,
-                           ctx->slots.p, &dc_of(ctx)->st, s, shrink, &dc_of(ctx)->table_ovf, xy32);
+                           ctx->slots.p, &dc_of(ctx)->st, s, shrink, &dc_of(ctx)->table_ovf, xy32, ctx->label_one != 0);
     else
       launch_label_a_range(ctx->xy.as<double>(), n, ctx->tri.p, 1, T, t0, t1, check, ctx->tri32.as<int32_t>(),
                            ctx->hw.as<int32_t>(), ctx->max_edge.as<int8_t>(), ctx->seed.as<uint8_t>(), nullptr,
-                           ctx->slots.p, &dc_of(ctx)->st, s, shrink, &dc_of(ctx)->table_ovf, xy32);
+                           ctx->slots.p, &dc_of(ctx)->st, s, shrink, &dc_of(ctx)->table_ovf, xy32, ctx->label_one != 0);
   }
   for (auto& t : workers) t.join();
   if (crc) return set_err(ctx, crc, "triangle upload failed");

@@ -17,7 +17,7 @@ void note_launch(int k);
 void launch_label_a(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int check,
                     int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed, int32_t* tv, void* table,
                     DevStatus* st, cudaStream_t s, int shrink = 0, unsigned int* ovf = nullptr,
-                    float* xy32 = nullptr);
+                    float* xy32 = nullptr, int one = 0);
 void launch_xy32(const double* xy, int64_t n, float* xy32, cudaStream_t s);
 // pass A split for copy overlap: prepare (table/trivertex init) once, then triangle ranges
 // shrink = 1: half-size twin table (whole path; overflow sets *ovf, the host reruns at full size)
@@ -25,9 +25,12 @@ void launch_label_a_prepare(int64_t n, int64_t T, int32_t* tv, void* table, cuda
 void launch_label_a_range(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int64_t t_begin,
                           int64_t t_end, int check, int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed,
                           int32_t* tv, void* table, DevStatus* st, cudaStream_t s, int shrink = 0,
-                          unsigned int* ovf = nullptr, const float* xy32 = nullptr);
+                          unsigned int* ovf = nullptr, const float* xy32 = nullptr, int one = 0);
 void launch_label_b(const int32_t* tri32, int64_t n, int64_t T, int32_t* hw, const int8_t* max_edge, uint8_t* seed,
-                    int32_t* tv, void* table, int check, DevStatus* st, cudaStream_t s, int shrink = 0);
+                    int32_t* tv, void* table, int check, DevStatus* st, cudaStream_t s, int shrink = 0,
+                    int one = 0);
+// one = 1 (unchecked): single-pass labels -- pass A pairs every far edge in
+// the table, pass B only scans it for border half-edges
 void launch_relabel(const int8_t* max_edge, int64_t T, int32_t* hw, uint8_t* seed, cudaStream_t s);
 // seed-partitioned labels (range-local twin table + boundary exchange)
 size_t hash_bytes_range(int64_t n, int64_t T, int64_t keyT);

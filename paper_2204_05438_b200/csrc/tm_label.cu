@@ -152,6 +152,57 @@ __device__ __forceinline__ int32_t table_lookup(const TwinTable& tb, DevStatus* 
   return -1;
 }
 
+// label the edge pair h (own triangle tt, own longest-edge flag `own`) + hc
+// (partner, its longest-edge flag `other`): labeling.py:65-115
+__device__ __forceinline__ void label_pair(int32_t* __restrict__ hw, uint8_t* __restrict__ seed, int32_t h, bool own,
+                                           int32_t hc, bool other) {
+  const int32_t tt = h / 3, tc = hc / 3;
+  const int32_t fr = (!own && !other) ? 1 : 0;
+  hw[h] = (hc << 1) | fr;
+  hw[hc] = (h << 1) | fr;
+  if (own) seed[tt] = (other && tt < tc) ? 1 : 0;
+  if (other) seed[tc] = (own && tc < tt) ? 1 : 0;
+}
+
+// Single-pass rendezvous (unchecked labels): the two half-edges of an edge both
+// probe under the undirected key (lo, hi).  The first to arrive claims an empty
+// slot with its (h << 1) | L; the second finds it, marks the slot paired
+// (claim bit, a fire-and-forget RED) and labels both sides at once.  Two
+// arrivals racing for the same empty slot: the CAS loser reads the winner's
+// entry, i.e. its partner.  Entries left unpaired are border half-edges
+// (k_border_scan).  A third half-edge on one key finds a paired slot: edge_count.
+__device__ __forceinline__ void table_meet(const TwinTable& tb, DevStatus* st, int32_t* __restrict__ hw,
+                                           uint8_t* __restrict__ seed, int32_t hl, int32_t lo, int32_t hi) {
+  Probe p = probe_of(tb, lo, hi);
+  const uint64_t hmask = (1ull << tb.hb) - 1;
+  for (int d = 0; d <= kMaxDisp; d++) {
+    unsigned long long* bk = tb.slots + 4 * ((p.home + d) & tb.nb_mask);
+    const uint64_t tag = p.tag | (uint64_t)d;
+    const unsigned long long mine = (tag << tb.hb) | (uint32_t)hl;
+    const Bucket b = load_bucket_cg(bk);
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      unsigned long long cur = b.at(k);
+      if (cur == kEmptySlot) {
+        cur = atomicCAS(bk + k, kEmptySlot, mine);
+        if (cur == kEmptySlot) return;
+      }
+      if (((cur & ~kClaimBit) >> tb.hb) == tag) {
+        if (cur & kClaimBit) {
+          report(st, K_EDGE_COUNT, (hl >> 1) / 3);
+          return;
+        }
+        atomicOr(bk + k, kClaimBit);
+        const int32_t pl = (int32_t)(cur & hmask);
+        label_pair(hw, seed, hl >> 1, (hl & 1) != 0, pl >> 1, (pl & 1) != 0);
+        return;
+      }
+    }
+  }
+  if (tb.ovf) atomicOr(tb.ovf, 1u);
+  else report(st, K_STRUCT, (hl >> 1) / 3);
+}
+
 __device__ __forceinline__ double sqlen(double2 p, double2 q) {
   double dx = __dsub_rn(p.x, q.x);
   double dy = __dsub_rn(p.y, q.y);
@@ -256,17 +307,6 @@ __device__ __forceinline__ uint32_t local_slot(int32_t lo, int32_t hi) {
   return ((uint32_t)lo * 0x9E3779B1u + (uint32_t)hi * 0x85EBCA77u) >> (32 - kLocalBits);
 }
 
-// label the edge pair h (descending, own triangle tt, own longest-edge flag `own`)
-// + hc (partner, its longest-edge flag `other`): labeling.py:65-115
-__device__ __forceinline__ void label_pair(int32_t* __restrict__ hw, uint8_t* __restrict__ seed, int32_t h, bool own,
-                                           int32_t hc, bool other) {
-  const int32_t tt = h / 3, tc = hc / 3;
-  const int32_t fr = (!own && !other) ? 1 : 0;
-  hw[h] = (hc << 1) | fr;
-  hw[hc] = (h << 1) | fr;
-  if (own) seed[tt] = (other && tt < tc) ? 1 : 0;
-  if (other) seed[tc] = (own && tc < tt) ? 1 : 0;
-}
 
 // Pass A (K1 + first half of K0), one thread per triangle: corners -> tri32,
 // fp64 longest edge -> max_edge, orientation check, trivertex (atomicMin, a
@@ -281,7 +321,7 @@ __device__ __forceinline__ void label_pair(int32_t* __restrict__ hw, uint8_t* __
 #ifndef TM_PAIR_MINB
 #define TM_PAIR_MINB 6
 #endif
-template <typename TI>
+template <typename TI, bool ONE>
 __global__ void __launch_bounds__(kLabelThreads, TM_TRI_MINB) k_tri_pass(const double2* __restrict__ xy,
                                                             const float2* __restrict__ xy32, int64_t n,
                                                             const TI* __restrict__ tri, int64_t t_begin,
@@ -308,11 +348,14 @@ __global__ void __launch_bounds__(kLabelThreads, TM_TRI_MINB) k_tri_pass(const d
     int32_t hh[3], oo[3], gg[3];
     if (t < T) {
       int64_t a = (int64_t)__ldg(tri + 3 * t), b = (int64_t)__ldg(tri + 3 * t + 1), c = (int64_t)__ldg(tri + 3 * t + 2);
-      hw[3 * t] = -1;
-      hw[3 * t + 1] = -1;
-      hw[3 * t + 2] = -1;
-      seed[t] = 1;
-      if (a < 0 || a >= n || b < 0 || b >= n || c < 0 || c >= n) {
+      const bool bad = a < 0 || a >= n || b < 0 || b >= n || c < 0 || c >= n;
+      if (!ONE || bad) {  // provisional border labels (ONE: every half-edge is labelled by whoever resolves it)
+        hw[3 * t] = -1;
+        hw[3 * t + 1] = -1;
+        hw[3 * t + 2] = -1;
+        seed[t] = 1;
+      }
+      if (bad) {
         report(st, K_INDEX_RANGE, t);
         max_edge[t] = 0;
         if (tri32 != nullptr) tri32[3 * t] = tri32[3 * t + 1] = tri32[3 * t + 2] = -1;
@@ -356,6 +399,10 @@ __global__ void __launch_bounds__(kLabelThreads, TM_TRI_MINB) k_tri_pass(const d
           gg[j] = cv[(j + 2) % 3];
           if (oo[j] < gg[j]) flags |= 1u << j;
           else if (oo[j] > gg[j]) desc |= 1u << j;
+          else if (ONE) {  // a zero-length edge (o == g) has no partner: border
+            hw[3 * t + j] = -1;
+            if (me0 == j) seed[t] = 1;
+          }
         }
       }
     }
@@ -387,6 +434,8 @@ __global__ void __launch_bounds__(kLabelThreads, TM_TRI_MINB) k_tri_pass(const d
           if (lklo[sl] == (uint32_t)gg[j] && lkhi[sl] == (uint32_t)oo[j]) {
             const int32_t pl = atomicOr(&lval[sl], kLocalMatched);
             if (!(pl & kLocalMatched)) label_pair(hw, seed, (int32_t)(3 * t + j), me0 == j, pl >> 1, (pl & 1) != 0);
+            else if (ONE) report(st, K_EDGE_COUNT, t);
+            if (ONE) desc &= ~(1u << j);  // resolved here: not sent to the table
             break;
           }
           sl = (sl + 1) & (kLocalSlots - 1);
@@ -397,9 +446,22 @@ __global__ void __launch_bounds__(kLabelThreads, TM_TRI_MINB) k_tri_pass(const d
       for (int j = 0; j < 3; j++)
         if (lslot[j] >= 0 && (lval[lslot[j]] & kLocalMatched)) flags &= ~(1u << j);
     }
+    if (ONE) {  // descending half-edges still unpaired meet their partner in the table too, under (g, o)
+#pragma unroll
+      for (int j = 0; j < 3; j++)
+        if ((desc >> j) & 1u) {
+          const int32_t x = oo[j];
+          oo[j] = gg[j];
+          gg[j] = x;
+        }
+      flags |= desc;
+    }
     int m = warp_compact3(flags, lane, sq[wid][0], sq[wid][1], sq[wid][2], hh, oo, gg);
 #ifndef TM_AB_NO_TABLE  // A/B timing builds only (wrong labels): what the table inserts cost
-    for (int i = lane; i < m; i += 32) table_insert(tb, st, sq[wid][0][i], sq[wid][1][i], sq[wid][2][i]);
+    for (int i = lane; i < m; i += 32) {
+      if (ONE) table_meet(tb, st, hw, seed, sq[wid][0][i], sq[wid][1][i], sq[wid][2][i]);
+      else table_insert(tb, st, sq[wid][0][i], sq[wid][1][i], sq[wid][2][i]);
+    }
 #endif
     __syncwarp();
     if (local) __syncthreads();  // lkey/lval are reset at the top of the next chunk
@@ -452,6 +514,33 @@ __global__ void __launch_bounds__(kLabelThreads, TM_PAIR_MINB) k_pair_pass(const
   }
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride)
     if (tv != nullptr && tv[v] == 0x7F7F7F7F) tv[v] = -1;
+}
+
+// Pass B of the single-pass labels: the table entries left unpaired are the
+// border half-edges (twin -1, frontier; a border longest edge seeds its
+// triangle, labeling.py:76-80), plus the trivertex sentinel.  One sequential
+// read of the table.
+__global__ void __launch_bounds__(256) k_border_scan(TwinTable tb, int32_t* __restrict__ hw, uint8_t* __restrict__ seed,
+                                                     int32_t* __restrict__ tv, int64_t n) {
+  const uint64_t hmask = (1ull << tb.hb) - 1;
+  const int64_t nb = (int64_t)tb.nb_mask + 1;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const ulonglong2* sl = reinterpret_cast<const ulonglong2*>(tb.slots);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * nb; i += stride) {
+    const ulonglong2 q = __ldcs(sl + i);
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      const unsigned long long cur = k ? q.y : q.x;
+      if (!(cur & kClaimBit)) {  // occupied (empty = all ones) and never paired
+        const int32_t pl = (int32_t)(cur & hmask), h = pl >> 1;
+        hw[h] = -1;
+        if (pl & 1) seed[h / 3] = 1;
+      }
+    }
+  }
+  if (tv != nullptr)
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride)
+      if (tv[v] == 0x7F7F7F7F) tv[v] = -1;
 }
 
 // labeling.py:65-115 fused.  k = twin % 3 replaces the back-slot search.
@@ -518,6 +607,22 @@ static inline int grid_for(int64_t n, int block) {
   return (int)(g < 1 ? 1 : g);
 }
 
+// Single-pass labels (`one`, unchecked only): both half-edges of a far edge
+// meet in pass A (table_meet) and pass B is a scan of the table
+// (k_border_scan).  Used where pass A overlaps the triangle upload (the
+// host-array entry): the table work then hides under PCIe and only the scan
+// follows the last chunk.  Device-resident runs keep insert (pass A) + lookup
+// (pass B): measured 2.04 vs 2.11 ms of label time at 10M (the lookups' read-only
+// probes are cheaper than the second arrivals' coherent ones).  Checked labels
+// always use two passes: the claim bits must see every partner.
+static inline bool single_pass(int one, int check) {
+#ifdef TM_TWO_PASS  // A/B: insert + lookup passes everywhere
+  return false;
+#else
+  return one && !check;
+#endif
+}
+
 // Grid of a grid-stride label kernel: exactly the resident blocks (occupancy x
 // SMs) when the work spans more, so no partial last wave -- at 10M the former
 // 16-per-SM grid ran k_tri_pass in 3.2 waves of 5 resident blocks (the last
@@ -532,7 +637,9 @@ static int resident_grid(K* fn, int64_t n, int block) {
   for (auto& c : cache)
     if (c.first == (const void*)fn) per_sm = c.second;
   if (per_sm == 0) {
+#ifdef TM_CARVEOUT  // A/B: maximum shared-memory carveout (measured: halves L1 and slows both passes ~50%)
     cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+#endif
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, 0) != cudaSuccess || per_sm < 1) per_sm = 4;
     for (auto& c : cache)
       if (c.first == nullptr) {
@@ -601,34 +708,55 @@ void launch_xy32(const double* xy, int64_t n, float* xy32, cudaStream_t s) {
 void launch_label_a_range(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int64_t t_begin,
                           int64_t t_end, int check, int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed,
                           int32_t* tv, void* table, DevStatus* st, cudaStream_t s, int shrink, unsigned int* ovf,
-                          const float* xy32) {
+                          const float* xy32, int one) {
   TwinTable tb = table_geometry(n, T, table, shrink, ovf);
   if (t_end > t_begin) {
     const int B = kLabelThreads;
-    const int g = tri_is64 ? resident_grid(k_tri_pass<int64_t>, t_end - t_begin, B)
-                           : resident_grid(k_tri_pass<int32_t>, t_end - t_begin, B);
-    if (tri_is64)
-      k_tri_pass<int64_t><<<g, B, 0, s>>>((const double2*)xy, (const float2*)xy32, n, (const int64_t*)tri, t_begin,
-                                          t_end, tri32, max_edge, tb, hw, seed, tv, check, st);
-    else
-      k_tri_pass<int32_t><<<g, B, 0, s>>>((const double2*)xy, (const float2*)xy32, n, (const int32_t*)tri, t_begin,
-                                          t_end, tri32 == tri ? nullptr : tri32, max_edge, tb, hw, seed, tv, check, st);
+    const int64_t m = t_end - t_begin;
+    const int g = single_pass(one, check)
+                      ? (tri_is64 ? resident_grid(k_tri_pass<int64_t, true>, m, B)
+                                  : resident_grid(k_tri_pass<int32_t, true>, m, B))
+                      : (tri_is64 ? resident_grid(k_tri_pass<int64_t, false>, m, B)
+                                  : resident_grid(k_tri_pass<int32_t, false>, m, B));
+    const double2* p = (const double2*)xy;
+    const float2* p32 = (const float2*)xy32;
+    int32_t* t32 = tri_is64 || tri32 != tri ? tri32 : nullptr;
+    if (single_pass(one, check)) {
+      if (tri_is64)
+        k_tri_pass<int64_t, true><<<g, B, 0, s>>>(p, p32, n, (const int64_t*)tri, t_begin, t_end, t32, max_edge, tb,
+                                                  hw, seed, tv, 0, st);
+      else
+        k_tri_pass<int32_t, true><<<g, B, 0, s>>>(p, p32, n, (const int32_t*)tri, t_begin, t_end, t32, max_edge, tb,
+                                                  hw, seed, tv, 0, st);
+    } else if (tri_is64) {
+      k_tri_pass<int64_t, false><<<g, B, 0, s>>>(p, p32, n, (const int64_t*)tri, t_begin, t_end, t32, max_edge, tb, hw,
+                                                 seed, tv, check, st);
+    } else {
+      k_tri_pass<int32_t, false><<<g, B, 0, s>>>(p, p32, n, (const int32_t*)tri, t_begin, t_end, t32, max_edge, tb, hw,
+                                                 seed, tv, check, st);
+    }
     note_launch(1);
   }
 }
 
 void launch_label_a(const double* xy, int64_t n, const void* tri, int tri_is64, int64_t T, int check,
                     int32_t* tri32, int32_t* hw, int8_t* max_edge, uint8_t* seed, int32_t* tv, void* table,
-                    DevStatus* st, cudaStream_t s, int shrink, unsigned int* ovf, float* xy32) {
+                    DevStatus* st, cudaStream_t s, int shrink, unsigned int* ovf, float* xy32, int one) {
   launch_label_a_prepare(n, T, tv, table, s, shrink);
   if (xy32 && !check) launch_xy32(xy, n, xy32, s);
   launch_label_a_range(xy, n, tri, tri_is64, T, 0, T, check, tri32, hw, max_edge, seed, tv, table, st, s, shrink, ovf,
-                       check ? nullptr : xy32);
+                       check ? nullptr : xy32, one);
 }
 
 void launch_label_b(const int32_t* tri32, int64_t n, int64_t T, int32_t* hw, const int8_t* max_edge, uint8_t* seed,
-                    int32_t* tv, void* table, int check, DevStatus* st, cudaStream_t s, int shrink) {
+                    int32_t* tv, void* table, int check, DevStatus* st, cudaStream_t s, int shrink, int one) {
   TwinTable tb = table_geometry(n, T, table, shrink);
+  if (single_pass(one, check)) {
+    const int64_t m = (int64_t)(tb.nb_mask + 1) * 2;
+    k_border_scan<<<grid_for(m > n ? m : n, 256), 256, 0, s>>>(tb, hw, seed, tv, n);
+    note_launch(1);
+    return;
+  }
   int64_t m = (T > n || tv == nullptr) ? T : n;
   if (m > 0) {
     k_pair_pass<<<resident_grid(k_pair_pass, m, kLabelThreads), kLabelThreads, 0, s>>>(tri32, 0, T, max_edge, tb, hw, seed, tv, n,
@@ -654,13 +782,13 @@ void launch_label_range(const double* xy, int64_t n, const void* tri, int tri_is
   const TwinTable tb = table_geometry(n, T, table, 0, ovf, e - b);
   cudaMemsetAsync(table, 0xFF, (size_t)(tb.nb_mask + 1) * 4 * sizeof(unsigned long long), s);
   if (e <= b) return;
-  const int g = tri_is64 ? resident_grid(k_tri_pass<int64_t>, e - b, kLabelThreads)
-                         : resident_grid(k_tri_pass<int32_t>, e - b, kLabelThreads);
+  const int g = tri_is64 ? resident_grid(k_tri_pass<int64_t, false>, e - b, kLabelThreads)
+                         : resident_grid(k_tri_pass<int32_t, false>, e - b, kLabelThreads);
   if (tri_is64)
-    k_tri_pass<int64_t><<<g, kLabelThreads, 0, s>>>((const double2*)xy, nullptr, n, (const int64_t*)tri, b, e, tri32,
+    k_tri_pass<int64_t, false><<<g, kLabelThreads, 0, s>>>((const double2*)xy, nullptr, n, (const int64_t*)tri, b, e, tri32,
                                                     max_edge, tb, hw, seed, nullptr, 0, st);
   else
-    k_tri_pass<int32_t><<<g, kLabelThreads, 0, s>>>((const double2*)xy, nullptr, n, (const int32_t*)tri, b, e,
+    k_tri_pass<int32_t, false><<<g, kLabelThreads, 0, s>>>((const double2*)xy, nullptr, n, (const int32_t*)tri, b, e,
                                                     tri32 == tri ? nullptr : tri32, max_edge, tb, hw, seed, nullptr, 0,
                                                     st);
   k_pair_pass<<<resident_grid(k_pair_pass, e - b, kLabelThreads), kLabelThreads, 0, s>>>(tri32, b, e, max_edge, tb, hw, seed, nullptr, n, 0, st);

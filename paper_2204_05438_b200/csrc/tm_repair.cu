@@ -338,7 +338,10 @@ __device__ __forceinline__ int wrap_idx(int x, int n) { return x >= n ? x - n : 
 
 // Smallest p in [0, n) with pred(p), or -1.  Eight 32-wide chunks per round
 // so their loads are in flight together (one memory round trip per 256).
-constexpr int kScanUnroll = 8;
+#ifndef TM_SCAN_UNROLL
+#define TM_SCAN_UNROLL 8
+#endif
+constexpr int kScanUnroll = TM_SCAN_UNROLL;
 template <typename Pred>
 __device__ __forceinline__ int warp_find_first(int n, int lane, Pred pred) {
   for (int base = 0; base < n; base += 32 * kScanUnroll) {

@@ -79,3 +79,42 @@ def test_permuted_vertex_ids(cuda, name):
     final, _ = tm.execute(t2)
     off, v = final.csr()
     assert np.array_equal(off, g["final_off"]) and np.array_equal(v, perm[g["final_verts"]])
+
+
+
+@pytest.mark.parametrize("name", ["u1k_unit", "aniso2k_s1", "clust5k_s0", "sun", "tie5", "single", "grid2x2", "u1k_box"])
+def test_single_pass_labels(cuda, name, monkeypatch):
+    """Single-pass labels (both half-edges of a far edge meet in pass A,
+    table_meet; pass B scans the table for borders) -- the host-array entry's
+    default, and every unchecked call with TERMESH_LABEL_ONE=1: the
+    reference's final polygons through both entries."""
+    from paper_2204_05438_b200 import _capi
+    tri, g = load_case(name)
+    ctx = _capi.Context(cuda.index or 0)  # default: single pass on the host entry only
+    off, v = _host_path(ctx, tri)
+    assert np.array_equal(off, g["final_off"]) and np.array_equal(v, g["final_verts"])
+    ctx.close()
+    monkeypatch.setenv("TERMESH_LABEL_ONE", "1")
+    ctx = _capi.Context(cuda.index or 0)
+    off, v = _whole_path(ctx, tri, cuda)
+    assert np.array_equal(off, g["final_off"]) and np.array_equal(v, g["final_verts"])
+    ctx.close()
+
+
+def test_single_pass_labels_repeatable(cuda, monkeypatch):
+    """The rendezvous races (two arrivals on one empty slot, pairs labelled from
+    either side) on a 300k-point mesh, ten runs of each entry: every output
+    equals the two-pass device path's."""
+    import paper_2204_05438_b200 as tm
+    from paper_2204_05438_b200 import _capi
+    tri = tm.generate_random_delaunay(300_000, seed=5)
+    monkeypatch.setenv("TERMESH_LABEL_ONE", "0")
+    ctx = _capi.Context(cuda.index or 0)
+    ref = _whole_path(ctx, tri, cuda)
+    ctx.close()
+    monkeypatch.setenv("TERMESH_LABEL_ONE", "1")
+    ctx = _capi.Context(cuda.index or 0)
+    for _ in range(10):
+        for off, v in (_whole_path(ctx, tri, cuda), _host_path(ctx, tri)):
+            assert np.array_equal(off, ref[0]) and np.array_equal(v, ref[1])
+    ctx.close()
