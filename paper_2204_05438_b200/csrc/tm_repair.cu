@@ -336,10 +336,14 @@ constexpr int kTipWarps = 4;  // warps per block of k_repair_tips
 
 __device__ __forceinline__ int wrap_idx(int x, int n) { return x >= n ? x - n : (x < 0 ? x + n : x); }
 
-// Smallest p in [0, n) with pred(p), or -1.  Eight 32-wide chunks per round
-// so their loads are in flight together (one memory round trip per 256).
+// Smallest p in [0, n) with pred(p), or -1.  kScanUnroll 32-wide chunks per
+// round (their loads in flight together).  1, not 8: k_repair_tips is
+// instruction-fetch bound (ncu at 10M: "no instruction" is the top stall, 28%
+// of the samples) and every unrolled copy of an inlined predicate adds code;
+// 8 -> 2 cut its SASS from 7.3 k to 5.2 k instructions and the 10M step by
+// 0.24 ms, 2 -> 1 another 0.05 ms (tools/ab_lib.sh).
 #ifndef TM_SCAN_UNROLL
-#define TM_SCAN_UNROLL 8
+#define TM_SCAN_UNROLL 1
 #endif
 constexpr int kScanUnroll = TM_SCAN_UNROLL;
 template <typename Pred>
@@ -380,6 +384,15 @@ __device__ __forceinline__ void warp_copy(int32_t* dst, int n, int lane, Src src
 
 // first position p (cyclic triple s[p-1] == s[p+1]) or -1 (reparation.py:59-71)
 __device__ int warp_first_tip(const int32_t* s, int n, int lane) {
+#ifndef TM_NO_SHFL_SCAN
+  if (n <= 32) {  // one load per lane, cyclic neighbours by shuffle
+    const int32_t x = lane < n ? s[lane] : 0;
+    const int32_t pv = __shfl_sync(kFull, x, lane == 0 ? n - 1 : lane - 1);
+    const int32_t nx = __shfl_sync(kFull, x, lane + 1 >= n ? 0 : lane + 1);
+    const unsigned m = __ballot_sync(kFull, lane < n && pv == nx);
+    return m ? __ffs(m) - 1 : -1;
+  }
+#endif
   return warp_find_first(n, lane, [&](int p) { return s[p == 0 ? n - 1 : p - 1] == s[p + 1 == n ? 0 : p + 1]; });
 }
 
@@ -701,6 +714,7 @@ constexpr int kDupCap = 512;         // per-warp shared table in k_repair_tips (
 constexpr int kPinchDupCap = 4096;   // per-warp shared table in k_repair_pinch (pieces up to 2048 vertices)
 __device__ int warp_dup_scan(const RepairCtx& c, const int32_t* s, int n, int lane, int* p1, int* p2,
                              int2* stab = nullptr, int scap = kDupCap) {
+#ifdef TM_NO_SHFL_SCAN
   if (n <= 64) {
     int extra = 0, q2 = -1, q1 = -1;
     for (int pb = 0; pb < n; pb += 32) {
@@ -722,6 +736,33 @@ __device__ int warp_dup_scan(const RepairCtx& c, const int32_t* s, int n, int la
     if (p2) *p2 = q2;
     return extra;
   }
+#else
+  if (n <= 64) {  // in registers: lane l holds s[l] and s[32 + l]; first occurrences by match / shuffle
+    // vertex ids are >= 0: unused lanes hold distinct negatives that match nothing
+    const int32_t x0 = lane < n ? s[lane] : -1 - lane;
+    const int32_t x1 = lane + 32 < n ? s[lane + 32] : -33 - lane;
+    const int f0 = __ffs(__match_any_sync(kFull, x0)) - 1;  // first position of s[lane] (within 0..31)
+    int f1 = -1;
+    if (n > 32) {
+      for (int q = 0; q < 32; q++)
+        if (__shfl_sync(kFull, x0, q) == x1 && f1 < 0) f1 = q;
+      if (f1 < 0) f1 = 32 + __ffs(__match_any_sync(kFull, x1)) - 1;
+    }
+    const unsigned m0 = __ballot_sync(kFull, f0 < lane), m1 = __ballot_sync(kFull, n > 32 && f1 < lane + 32);
+    int q2 = -1, q1 = -1;
+    if (m0) {
+      q2 = __ffs(m0) - 1;
+      q1 = __shfl_sync(kFull, f0, q2);
+    } else if (m1) {
+      const int l = __ffs(m1) - 1;
+      q2 = 32 + l;
+      q1 = __shfl_sync(kFull, f1, l);
+    }
+    if (p1) *p1 = q1;
+    if (p2) *p2 = q2;
+    return __popc(m0) + __popc(m1);
+  }
+#endif
   int cap = 64;
   while (cap < 2 * n) cap <<= 1;
   const bool shared = stab != nullptr && cap <= scap;
