@@ -106,7 +106,19 @@ __device__ __forceinline__ void table_insert(const TwinTable& tb, DevStatus* st,
     unsigned long long* bk = tb.slots + 4 * ((p.home + d) & tb.nb_mask);
     const uint64_t tag = p.tag | (uint64_t)d;
     const unsigned long long mine = (tag << tb.hb) | (uint32_t)hl;
+#ifdef TM_CAS_FIRST  // A/B: claim slot 0 of the home bucket without reading the bucket first
+    Bucket b;
+    if (d == 0) {
+      const unsigned long long c0 = atomicCAS(bk, kEmptySlot, mine);
+      if (c0 == kEmptySlot) return;
+      b = load_bucket_cg(bk);
+      b.s0 = c0;
+    } else {
+      b = load_bucket_cg(bk);
+    }
+#else
     const Bucket b = load_bucket_cg(bk);
+#endif
 #pragma unroll
     for (int k = 0; k < 4; k++) {
       unsigned long long cur = b.at(k);

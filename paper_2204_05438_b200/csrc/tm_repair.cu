@@ -384,7 +384,7 @@ __device__ __forceinline__ void warp_copy(int32_t* dst, int n, int lane, Src src
 
 // first position p (cyclic triple s[p-1] == s[p+1]) or -1 (reparation.py:59-71)
 __device__ int warp_first_tip(const int32_t* s, int n, int lane) {
-#ifndef TM_NO_SHFL_SCAN
+#if !defined(TM_NO_SHFL_SCAN) && !defined(TM_NO_SHFL_TIP)
   if (n <= 32) {  // one load per lane, cyclic neighbours by shuffle
     const int32_t x = lane < n ? s[lane] : 0;
     const int32_t pv = __shfl_sync(kFull, x, lane == 0 ? n - 1 : lane - 1);
@@ -714,7 +714,7 @@ constexpr int kDupCap = 512;         // per-warp shared table in k_repair_tips (
 constexpr int kPinchDupCap = 4096;   // per-warp shared table in k_repair_pinch (pieces up to 2048 vertices)
 __device__ int warp_dup_scan(const RepairCtx& c, const int32_t* s, int n, int lane, int* p1, int* p2,
                              int2* stab = nullptr, int scap = kDupCap) {
-#ifdef TM_NO_SHFL_SCAN
+#if defined(TM_NO_SHFL_SCAN) || defined(TM_NO_SHFL_DUP)
   if (n <= 64) {
     int extra = 0, q2 = -1, q1 = -1;
     for (int pb = 0; pb < n; pb += 32) {
@@ -738,17 +738,21 @@ __device__ int warp_dup_scan(const RepairCtx& c, const int32_t* s, int n, int la
   }
 #else
   if (n <= 64) {  // in registers: lane l holds s[l] and s[32 + l]; first occurrences by match / shuffle
-    // vertex ids are >= 0: unused lanes hold distinct negatives that match nothing
+    // unused lanes (>= n) lie above every used one, so they never lower a used lane's
+    // first occurrence; their own flags are masked off below (a piece may hold
+    // negative values, so no sentinel is safe to count on)
     const int32_t x0 = lane < n ? s[lane] : -1 - lane;
     const int32_t x1 = lane + 32 < n ? s[lane + 32] : -33 - lane;
     const int f0 = __ffs(__match_any_sync(kFull, x0)) - 1;  // first position of s[lane] (within 0..31)
     int f1 = -1;
-    if (n > 32) {
+    if (n > 32) {  // (warp-uniform; the match runs on every lane, outside the per-lane branch)
+      const unsigned m1x = __match_any_sync(kFull, x1);
       for (int q = 0; q < 32; q++)
         if (__shfl_sync(kFull, x0, q) == x1 && f1 < 0) f1 = q;
-      if (f1 < 0) f1 = 32 + __ffs(__match_any_sync(kFull, x1)) - 1;
+      if (f1 < 0) f1 = 32 + __ffs(m1x) - 1;
     }
-    const unsigned m0 = __ballot_sync(kFull, f0 < lane), m1 = __ballot_sync(kFull, n > 32 && f1 < lane + 32);
+    const unsigned m0 = __ballot_sync(kFull, lane < n && f0 < lane);
+    const unsigned m1 = __ballot_sync(kFull, lane + 32 < n && f1 < lane + 32);
     int q2 = -1, q1 = -1;
     if (m0) {
       q2 = __ffs(m0) - 1;
