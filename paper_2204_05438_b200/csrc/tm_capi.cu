@@ -141,7 +141,7 @@ struct tm_ctx {
   // label
   Buf slots, lbscan;
   // traversal
-  Buf seeds, start, len, overflow, queue, stamp, tiles, nrul, eoff, rnext, rdist, rprev, startbits, ent_r, ent_base;
+  Buf seeds, start, len, overflow, queue, stamp, tiles, nrul, eoff, rulers, startbits, ent_r, ent_base;
   // repair
   Buf item_of, items, long_list, item_list, item_n, item_slots, item_state, item_depth, cnt, slotsz, pbase, sbase, pool,
       undo, hugeq, longq, parked, pinchq;
@@ -401,9 +401,7 @@ static int prepare(tm_ctx* ctx, int64_t T, int64_t n = -1) {
   }
   ENSURE(tiles, (scan_scratch_elems(3 * Tn) + 8) * sizeof(int64_t));
   ENSURE(lbscan, scan_lookback_bytes(Tn));
-  ENSURE(rnext, 3 * Tn * sizeof(int32_t));
-  ENSURE(rdist, 3 * Tn * sizeof(int32_t));
-  ENSURE(rprev, 3 * Tn * sizeof(int32_t));
+  ENSURE(rulers, (3 * Tn + 3) * sizeof(RulerRec));
   ENSURE(startbits, ((3 * Tn + 31) / 32) * sizeof(uint32_t));
   // ruler entries: seed starts + the 1/8 hash sample of half-edges (+ slack)
   ctx->ecap = Tn + (3 * Tn) / 8 + (3 * Tn) / 16 + 1024;
@@ -517,12 +515,12 @@ static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* 
   {
     SegTimer t_(ctx, S_TRAV_RULERS, s);
     launch_ruler_walk(d_hw, ctx->startbits.as<uint32_t>(), T, tb, te, ctx->start.as<int32_t>(), &dc->n_seeds, Tn,
-                      ctx->rnext.as<int32_t>(), ctx->rdist.as<int32_t>(), ctx->rprev.as<int32_t>(), &dc->st, s);
+                      ctx->rulers.as<RulerRec>(), &dc->st, s);
   }
   {
     SegTimer t_(ctx, S_TRAV_LEN, s);
     launch_chain_count(ctx->seeds.as<int32_t>(), ctx->start.as<int32_t>(), &dc->n_seeds, Tn, T,
-                       ctx->rnext.as<int32_t>(), ctx->rdist.as<int32_t>(), ctx->rprev.as<int32_t>(),
+                       ctx->rulers.as<RulerRec>(),
                        ctx->len.as<int64_t>(), ctx->nrul.as<int64_t>(),
                        ctx->early_long ? ctx->long_list.as<int32_t>() : nullptr, &dc->n_long, &dc->st, s);
   }
@@ -533,8 +531,7 @@ static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* 
   }
   {
     SegTimer t_(ctx, S_TRAV_WRITE, s);
-    launch_chain_emit(ctx->start.as<int32_t>(), &dc->n_seeds, Tn, ctx->rnext.as<int32_t>(), ctx->rdist.as<int32_t>(),
-                      ctx->rprev.as<int32_t>(), d_off, ctx->eoff.as<int64_t>(), ctx->ent_r.as<int32_t>(), ctx->ent_base.as<int64_t>(),
+    launch_chain_emit(ctx->start.as<int32_t>(), &dc->n_seeds, Tn, ctx->rulers.as<RulerRec>(), d_off, ctx->eoff.as<int64_t>(), ctx->ent_r.as<int32_t>(), ctx->ent_base.as<int64_t>(),
                       ctx->ecap, &dc->st, s);
     if (ctx->early_long) {
       // fork: the long polygons' runs -> their classification -> the long-item
@@ -543,7 +540,7 @@ static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* 
       CK(cudaEventRecord(ctx->ev_fork, s));
       CK(cudaStreamWaitEvent(a, ctx->ev_fork, 0));
       launch_ruler_write_list(d_tri32, d_hw, ctx->long_list.as<int32_t>(), &dc->n_long, ctx->eoff.as<int64_t>(),
-                              ctx->ent_r.as<int32_t>(), ctx->ent_base.as<int64_t>(), ctx->rdist.as<int32_t>(), T, Tn,
+                              ctx->ent_r.as<int32_t>(), ctx->ent_base.as<int64_t>(), ctx->rulers.as<RulerRec>(), T, Tn,
                               d_v, ctx->path_hv, a);
       launch_classify(d_off, d_v, &dc->n_seeds, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(),
                       &dc->n_items, ctx->long_list.as<int32_t>(), &dc->n_long, dc->stats, long_queue(ctx),
@@ -558,7 +555,7 @@ static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* 
       CK(cudaEventRecord(ctx->ev_join, a));
     }
     launch_ruler_write(d_tri32, d_hw, &dc->n_entries, ctx->ent_r.as<int32_t>(), ctx->ent_base.as<int64_t>(),
-                       ctx->rdist.as<int32_t>(), T, ctx->ecap, d_v, ctx->path_hv, s);
+                       ctx->rulers.as<RulerRec>(), T, ctx->ecap, d_v, ctx->path_hv, s);
   }
   CK(cudaGetLastError());
   return TM_OK;
@@ -700,7 +697,7 @@ int tm_ctx_create(tm_ctx** out) {
 void tm_ctx_destroy(tm_ctx* ctx) {
   if (!ctx) return;
   Buf* bufs[] = {&ctx->counters, &ctx->slots, &ctx->seeds, &ctx->start, &ctx->len, &ctx->overflow, &ctx->queue,
-                 &ctx->stamp, &ctx->tiles, &ctx->nrul, &ctx->eoff, &ctx->rnext, &ctx->rdist, &ctx->rprev, &ctx->startbits,
+                 &ctx->stamp, &ctx->tiles, &ctx->nrul, &ctx->eoff, &ctx->rulers, &ctx->startbits,
                  &ctx->ent_r, &ctx->ent_base, &ctx->item_of, &ctx->items, &ctx->long_list, &ctx->item_list,
                  &ctx->item_n, &ctx->item_slots, &ctx->item_state, &ctx->item_depth, &ctx->hugeq, &ctx->longq, &ctx->parked, &ctx->pinchq, &ctx->cnt, &ctx->slotsz, &ctx->pbase, &ctx->sbase, &ctx->pool,
                  &ctx->undo, &ctx->xy, &ctx->tri, &ctx->tri32, &ctx->hw, &ctx->max_edge, &ctx->seed, &ctx->tv,

@@ -67,22 +67,27 @@ void launch_select_flags(const uint8_t* flag, int64_t n, int32_t* out, int64_t* 
 void launch_trav_start(const int32_t* hw, const int32_t* seeds, const int64_t* Pp, int64_t Pcap, int32_t* start,
                        int32_t* overflow, unsigned int* n_overflow, int32_t* queue, int32_t* stamp, uint32_t* bits,
                        DevStatus* st, cudaStream_t s);
+// ruler record of half-edge h (a ruler): next ruler, run length (boundary steps to
+// it), previous ruler -- one 16-byte record so each chain step is one sector
+struct __align__(16) RulerRec {
+  int32_t next, dist, prev, pad;
+};
 // rulers: starts of the selected seeds + sampled half-edges of triangles [t_begin, t_end)
 void launch_ruler_walk(const int32_t* hw, uint32_t* bits, int64_t T, int64_t t_begin, int64_t t_end,
-                       const int32_t* start, const int64_t* Pp, int64_t Pcap, int32_t* rnext, int32_t* rdist,
-                       int32_t* rprev, DevStatus* st, cudaStream_t s);
+                       const int32_t* start, const int64_t* Pp, int64_t Pcap, RulerRec* R, DevStatus* st,
+                       cudaStream_t s);
 void launch_chain_count(const int32_t* seeds, const int32_t* start, const int64_t* Pp, int64_t Pcap, int64_t T,
-                        const int32_t* rnext, const int32_t* rdist, const int32_t* rprev, int64_t* len, int64_t* nrul,
+                        const RulerRec* R, int64_t* len, int64_t* nrul,
                         int32_t* long_list, unsigned int* n_long, DevStatus* st, cudaStream_t s);
-void launch_chain_emit(const int32_t* start, const int64_t* Pp, int64_t Pcap, const int32_t* rnext,
-                       const int32_t* rdist, const int32_t* rprev, const int64_t* offsets, const int64_t* eoff,
+void launch_chain_emit(const int32_t* start, const int64_t* Pp, int64_t Pcap, const RulerRec* R,
+                       const int64_t* offsets, const int64_t* eoff,
                        int32_t* ent_r, int64_t* ent_base, int64_t ecap, DevStatus* st, cudaStream_t s);
 void launch_ruler_write(const int32_t* tri, const int32_t* hw, const int64_t* n_entries, const int32_t* ent_r,
-                        const int64_t* ent_base, const int32_t* rdist, int64_t T, int64_t ecap, int32_t* verts,
+                        const int64_t* ent_base, const RulerRec* R, int64_t T, int64_t ecap, int32_t* verts,
                         int32_t* hv, cudaStream_t s);
 // the runs of the listed (long) polygons only: entries eoff[i] .. eoff[i + 1]
 void launch_ruler_write_list(const int32_t* tri, const int32_t* hw, const int32_t* list, const unsigned int* n_list,
-                             const int64_t* eoff, const int32_t* ent_r, const int64_t* ent_base, const int32_t* rdist,
+                             const int64_t* eoff, const int32_t* ent_r, const int64_t* ent_base, const RulerRec* R,
                              int64_t T, int64_t Pcap, int32_t* verts, int32_t* hv, cudaStream_t s);
 
 // tm_repair.cu

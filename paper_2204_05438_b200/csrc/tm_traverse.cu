@@ -109,7 +109,15 @@ __global__ void k_bfs_slow(const int32_t* __restrict__ hw, const int32_t* __rest
   }
 }
 
-// (1) every ruler walks to the next ruler: rnext/rdist indexed by half-edge id
+// (1) every ruler walks to the next ruler: R[h] = {next ruler, run length, previous ruler}
+// indexed by half-edge id, one 16-byte record (the chain passes read a ruler's
+// successor and distance, or predecessor and distance, with one sector each)
+__device__ __forceinline__ void set_next(RulerRec* R, int32_t h, int32_t g, int32_t d) {
+  *reinterpret_cast<int2*>(R + h) = make_int2(g, d);
+}
+__device__ __forceinline__ int4 ld_rec(const RulerRec* R, int32_t h) {
+  return __ldg(reinterpret_cast<const int4*>(R + h));
+}
 // Runs longer than kMaxRun boundary steps are cut by "virtual" rulers (marked
 // in the start bitmap, which only later kernels read): the gap between two
 // hash-sampled rulers is geometric with a ~100-step tail, and the write pass
@@ -117,8 +125,7 @@ __global__ void k_bfs_slow(const int32_t* __restrict__ hw, const int32_t* __rest
 // ruler lies inside a gap that exactly one walk covers.
 constexpr int kMaxRun = 24;
 __device__ __forceinline__ void walk_ruler(const int32_t* __restrict__ hw, const RulerSet& rs, int32_t h,
-                                           long long limit, int32_t* __restrict__ rnext,
-                                           int32_t* __restrict__ rdist, int32_t* __restrict__ rprev,
+                                           long long limit, RulerRec* __restrict__ R,
                                            uint32_t* __restrict__ vbits, DevStatus* st) {
   int32_t cur = h, g = h;
   long long d = 0, total = 0;
@@ -130,16 +137,14 @@ __device__ __forceinline__ void walk_ruler(const int32_t* __restrict__ hw, const
     if (is_ruler(rs, g)) break;
     if (d == kMaxRun) {
       mark_start(vbits, g);
-      rnext[cur] = g;
-      rdist[cur] = (int32_t)d;
-      rprev[g] = cur;
+      set_next(R, cur, g, (int32_t)d);
+      R[g].prev = cur;
       cur = g;
       d = 0;
     }
   }
-  rnext[cur] = g;
-  rdist[cur] = (int32_t)d;
-  rprev[g] = cur;  // every ruler is the successor of exactly one ruler of its cycle
+  set_next(R, cur, g, (int32_t)d);
+  R[g].prev = cur;  // every ruler is the successor of exactly one ruler of its cycle
 }
 
 // About one half-edge in nine starts a walk, so a warp first gathers the rulers
@@ -147,8 +152,7 @@ __device__ __forceinline__ void walk_ruler(const int32_t* __restrict__ hw, const
 // (a thread-per-half-edge loop keeps ~3 of 32 lanes walking).
 constexpr int kWalkTile = 8;  // 32-wide chunks per warp tile
 __global__ void __launch_bounds__(256) k_ruler_walk(const int32_t* __restrict__ hw, RulerSet rs, long long limit,
-                                                    int32_t* __restrict__ rnext, int32_t* __restrict__ rdist,
-                                                    int32_t* __restrict__ rprev, uint32_t* vbits, DevStatus* st) {
+                                                    RulerRec* __restrict__ R, uint32_t* vbits, DevStatus* st) {
   __shared__ int32_t s_q[8][32 * kWalkTile];
   const int lane = threadIdx.x & 31;
   int32_t* q = s_q[threadIdx.x >> 5];
@@ -167,7 +171,7 @@ __global__ void __launch_bounds__(256) k_ruler_walk(const int32_t* __restrict__ 
       n += __popc(m);
     }
     __syncwarp();
-    for (int k = lane; k < n; k += 32) walk_ruler(hw, rs, q[k], limit, rnext, rdist, rprev, vbits, st);
+    for (int k = lane; k < n; k += 32) walk_ruler(hw, rs, q[k], limit, R, vbits, st);
     __syncwarp();
   }
 }
@@ -176,23 +180,22 @@ __global__ void __launch_bounds__(256) k_ruler_walk(const int32_t* __restrict__ 
 __global__ void __launch_bounds__(256) k_ruler_walk_starts(const int32_t* __restrict__ hw, RulerSet rs,
                                                            const int32_t* __restrict__ start,
                                                            const int64_t* __restrict__ Pp, long long limit,
-                                                           int32_t* __restrict__ rnext, int32_t* __restrict__ rdist,
-                                                           int32_t* __restrict__ rprev, uint32_t* vbits,
+                                                           RulerRec* __restrict__ R, uint32_t* vbits,
                                                            DevStatus* st) {
   const int64_t P = *Pp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t h = start[i];
     if (h < 0 || (h >= rs.hb && h < rs.he)) continue;
-    walk_ruler(hw, rs, h, limit, rnext, rdist, rprev, vbits, st);
+    walk_ruler(hw, rs, h, limit, R, vbits, st);
   }
 }
 
 // (2a) polygon length and ruler count per seed (traversal.py:264-281).  Two
-// walkers per cycle -- forward over rnext, backward over rprev -- consume the
+// walkers per cycle -- forward over next, backward over prev -- consume the
 // rulers from both ends, so the longest cycle costs half as many dependent hops.
 __global__ void __launch_bounds__(256) k_chain_count(const int32_t* __restrict__ seeds, const int32_t* __restrict__ start,
-                                                     const int64_t* __restrict__ Pp, long long limit, const int32_t* __restrict__ rnext,
-                                                     const int32_t* __restrict__ rdist, const int32_t* __restrict__ rprev,
+                                                     const int64_t* __restrict__ Pp, long long limit,
+                                                     const RulerRec* __restrict__ R,
                                                      int64_t* __restrict__ len, int64_t* __restrict__ nrul,
                                                      int32_t* __restrict__ long_list, unsigned int* n_long,
                                                      DevStatus* st) {
@@ -201,10 +204,11 @@ __global__ void __launch_bounds__(256) k_chain_count(const int32_t* __restrict__
     const int32_t h0 = start[i];
     long long L = 0, cnt = 0;
     if (h0 >= 0) {
-      int32_t f = h0, b = rprev[h0];  // next ruler to consume going forward / backward
+      int32_t f = h0, b = R[h0].prev;  // next ruler to consume going forward / backward
       for (;;) {
-        // both walkers' loads issued together: one memory round trip per step of the pair
-        const int32_t df = rdist[f], nf = rnext[f], db = rdist[b], pb = rprev[b];
+        // both walkers' records loaded together: one memory round trip per step of the pair
+        const int4 rf = ld_rec(R, f), rb = ld_rec(R, b);
+        const int32_t df = rf.y, nf = rf.x, db = rb.y, pb = rb.z;
         L += df;
         cnt++;
         if (f == b) break;
@@ -225,8 +229,7 @@ __global__ void __launch_bounds__(256) k_chain_count(const int32_t* __restrict__
 
 // (2b) emit (ruler, absolute output offset) entries in chain order, from both ends
 __global__ void __launch_bounds__(256) k_chain_emit(const int32_t* __restrict__ start, const int64_t* __restrict__ Pp,
-                                                    const int32_t* __restrict__ rnext, const int32_t* __restrict__ rdist,
-                                                    const int32_t* __restrict__ rprev,
+                                                    const RulerRec* __restrict__ R,
                                                     const int64_t* __restrict__ offsets, const int64_t* __restrict__ eoff,
                                                     int32_t* __restrict__ ent_r, int64_t* __restrict__ ent_base,
                                                     int64_t ecap, DevStatus* st) {
@@ -237,9 +240,10 @@ __global__ void __launch_bounds__(256) k_chain_emit(const int32_t* __restrict__ 
     if (h0 < 0 || kb < kf) continue;
     if (kb >= ecap) { report(st, K_STRUCT, i); continue; }
     int64_t pf = offsets[i], pb = offsets[i + 1];  // forward start / backward end offsets
-    int32_t f = h0, b = rprev[h0];
+    int32_t f = h0, b = R[h0].prev;
     for (;;) {
-      const int32_t df = rdist[f], nf = rnext[f], db = rdist[b], nb = rprev[b];
+      const int4 rf = ld_rec(R, f), rb = ld_rec(R, b);
+      const int32_t df = rf.y, nf = rf.x, db = rb.y, nb = rb.z;
       ent_r[kf] = f;
       ent_base[kf] = pf;
       pf += df;
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(256) k_ruler_write(const int32_t* __restrict__
                                                      const int64_t* __restrict__ n_entries,
                                                      const int32_t* __restrict__ ent_r,
                                                      const int64_t* __restrict__ ent_base,
-                                                     const int32_t* __restrict__ rdist, long long limit,
+                                                     const RulerRec* __restrict__ R, long long limit,
                                                      int64_t ecap, int32_t* __restrict__ verts,
                                                      int32_t* __restrict__ hv) {
   int64_t E = *n_entries;
@@ -269,7 +273,7 @@ __global__ void __launch_bounds__(256) k_ruler_write(const int32_t* __restrict__
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < E; k += (int64_t)gridDim.x * blockDim.x) {
     int32_t g = ent_r[k];
     int64_t w = ent_base[k];
-    int d = rdist[g];
+    int d = R[g].dist;
     for (int s = 0; s < d; s++) {
       verts[w + s] = he_origin(tri, g);
       if (hv) hv[w + s] = g;  // the boundary half-edge of each slot (fan starts for repair)
@@ -285,7 +289,7 @@ __global__ void __launch_bounds__(128) k_ruler_write_list(const int32_t* __restr
                                                           const int64_t* __restrict__ eoff,
                                                           const int32_t* __restrict__ ent_r,
                                                           const int64_t* __restrict__ ent_base,
-                                                          const int32_t* __restrict__ rdist, long long limit,
+                                                          const RulerRec* __restrict__ R, long long limit,
                                                           int32_t* __restrict__ verts, int32_t* __restrict__ hv) {
   const unsigned int nl = *n_list;
   for (unsigned int w = blockIdx.x; w < nl; w += gridDim.x) {
@@ -293,7 +297,7 @@ __global__ void __launch_bounds__(128) k_ruler_write_list(const int32_t* __restr
     for (int64_t k = eoff[i] + threadIdx.x; k < eoff[i + 1]; k += blockDim.x) {
       int32_t g = ent_r[k];
       const int64_t b = ent_base[k];
-      const int d = rdist[g];
+      const int d = R[g].dist;
       for (int s = 0; s < d; s++) {
         verts[b + s] = he_origin(tri, g);
         if (hv) hv[b + s] = g;
@@ -326,45 +330,45 @@ void launch_trav_start(const int32_t* hw, const int32_t* seeds, const int64_t* P
 }
 
 void launch_ruler_walk(const int32_t* hw, uint32_t* bits, int64_t T, int64_t t_begin, int64_t t_end,
-                       const int32_t* start, const int64_t* Pp, int64_t Pcap, int32_t* rnext, int32_t* rdist,
-                       int32_t* rprev, DevStatus* st, cudaStream_t s) {
+                       const int32_t* start, const int64_t* Pp, int64_t Pcap, RulerRec* R, DevStatus* st,
+                       cudaStream_t s) {
   if (T <= 0) return;
   RulerSet rs{bits, (int32_t)(3 * t_begin), (int32_t)(3 * t_end)};
-  k_ruler_walk<<<grid_for(3 * (t_end - t_begin), 256), 256, 0, s>>>(hw, rs, 3 * T + 3, rnext, rdist, rprev, bits, st);
+  k_ruler_walk<<<grid_for(3 * (t_end - t_begin), 256), 256, 0, s>>>(hw, rs, 3 * T + 3, R, bits, st);
   note_launch(1);
   if (t_begin > 0 || t_end < T) {
-    k_ruler_walk_starts<<<grid_for(Pcap, 256), 256, 0, s>>>(hw, rs, start, Pp, 3 * T + 3, rnext, rdist, rprev, bits, st);
+    k_ruler_walk_starts<<<grid_for(Pcap, 256), 256, 0, s>>>(hw, rs, start, Pp, 3 * T + 3, R, bits, st);
     note_launch(1);
   }
 }
 
 void launch_chain_count(const int32_t* seeds, const int32_t* start, const int64_t* Pp, int64_t Pcap, int64_t T,
-                        const int32_t* rnext, const int32_t* rdist, const int32_t* rprev, int64_t* len, int64_t* nrul,
+                        const RulerRec* R, int64_t* len, int64_t* nrul,
                         int32_t* long_list, unsigned int* n_long, DevStatus* st, cudaStream_t s) {
-  k_chain_count<<<grid_for(Pcap, 256), 256, 0, s>>>(seeds, start, Pp, 3 * T + 3, rnext, rdist, rprev, len, nrul,
+  k_chain_count<<<grid_for(Pcap, 256), 256, 0, s>>>(seeds, start, Pp, 3 * T + 3, R, len, nrul,
                                                     long_list, n_long, st);
   note_launch(1);
 }
 
-void launch_chain_emit(const int32_t* start, const int64_t* Pp, int64_t Pcap, const int32_t* rnext,
-                       const int32_t* rdist, const int32_t* rprev, const int64_t* offsets, const int64_t* eoff,
+void launch_chain_emit(const int32_t* start, const int64_t* Pp, int64_t Pcap, const RulerRec* R,
+                       const int64_t* offsets, const int64_t* eoff,
                        int32_t* ent_r, int64_t* ent_base, int64_t ecap, DevStatus* st, cudaStream_t s) {
-  k_chain_emit<<<grid_for(Pcap, 256), 256, 0, s>>>(start, Pp, rnext, rdist, rprev, offsets, eoff, ent_r, ent_base,
+  k_chain_emit<<<grid_for(Pcap, 256), 256, 0, s>>>(start, Pp, R, offsets, eoff, ent_r, ent_base,
                                                    ecap, st);
   note_launch(1);
 }
 
 void launch_ruler_write(const int32_t* tri, const int32_t* hw, const int64_t* n_entries, const int32_t* ent_r,
-                        const int64_t* ent_base, const int32_t* rdist, int64_t T, int64_t ecap, int32_t* verts,
+                        const int64_t* ent_base, const RulerRec* R, int64_t T, int64_t ecap, int32_t* verts,
                         int32_t* hv, cudaStream_t s) {
-  k_ruler_write<<<kNumSMs * 16, 256, 0, s>>>(tri, hw, n_entries, ent_r, ent_base, rdist, 3 * T + 3, ecap, verts, hv);
+  k_ruler_write<<<kNumSMs * 16, 256, 0, s>>>(tri, hw, n_entries, ent_r, ent_base, R, 3 * T + 3, ecap, verts, hv);
   note_launch(1);
 }
 
 void launch_ruler_write_list(const int32_t* tri, const int32_t* hw, const int32_t* list, const unsigned int* n_list,
-                             const int64_t* eoff, const int32_t* ent_r, const int64_t* ent_base, const int32_t* rdist,
+                             const int64_t* eoff, const int32_t* ent_r, const int64_t* ent_base, const RulerRec* R,
                              int64_t T, int64_t Pcap, int32_t* verts, int32_t* hv, cudaStream_t s) {
-  k_ruler_write_list<<<kNumSMs, 128, 0, s>>>(tri, hw, list, n_list, eoff, ent_r, ent_base, rdist, 3 * T + 3, verts, hv);
+  k_ruler_write_list<<<kNumSMs, 128, 0, s>>>(tri, hw, list, n_list, eoff, ent_r, ent_base, R, 3 * T + 3, verts, hv);
   note_launch(1);
 }
 
