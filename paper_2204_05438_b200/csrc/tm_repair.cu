@@ -121,6 +121,25 @@ __device__ __forceinline__ int extra_visits_reg(const int32_t* __restrict__ s, i
   return ex;
 }
 
+__device__ __forceinline__ int lane_id() { return (int)(threadIdx.x & 31); }
+
+// (n - distinct) of s[0..n), n <= 64, one warp: lane l holds s[l] and s[32 + l];
+// unused lanes hold distinct negatives (and are masked from the count).  The
+// matches run on every lane (warp-uniform code, full mask).
+__device__ __forceinline__ int warp_extra_64(const int32_t* __restrict__ s, int n, int lane) {
+  const int32_t x0 = lane < n ? __ldg(s + lane) : -1 - lane;
+  const int32_t x1 = lane + 32 < n ? __ldg(s + lane + 32) : -33 - lane;
+  const int f0 = __ffs(__match_any_sync(kFull, x0)) - 1;
+  const unsigned m1x = __match_any_sync(kFull, x1);
+  int f1 = -1;
+  if (n > 32)
+    for (int q = 0; q < 32; q++)
+      if (__shfl_sync(kFull, x0, q) == x1 && f1 < 0) f1 = q;
+  if (f1 < 0) f1 = 32 + __ffs(m1x) - 1;
+  return __popc(__ballot_sync(kFull, lane < n && f0 < lane)) +
+         __popc(__ballot_sync(kFull, lane + 32 < n && f1 < lane + 32));
+}
+
 // Block-aggregated append: one global atomic per block and list instead of
 // one per element (a single hot counter serialises thousands of returning
 // atomics).  All threads of the block must call it.
@@ -155,21 +174,34 @@ __global__ void __launch_bounds__(256) k_classify(const int64_t* __restrict__ of
   unsigned long long extra_sum = 0, rep_cnt = 0;
   for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < P; i0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = i0 + threadIdx.x;
-    bool is_long = false, is_item = false;
+    bool is_long = false, is_item = false, mid = false;
+    int64_t b = 0, n = 0, ex = 0;
     if (i < P) {
-      int64_t b = off[i], n = off[i + 1] - b;
+      b = off[i];
+      n = off[i + 1] - b;
       if (n > kClassifyShort) {
         is_long = append_long;  // k_classify_long sets item_of[i]
       } else {
         item_of[i] = -1;
         // registers: all loads in flight at once, compares without reloads
-        const int64_t ex = n <= 16 ? extra_visits_reg<16>(v + b, (int)n) : extra_visits_reg<48>(v + b, (int)n);
-        if (ex > 0) {
-          extra_sum += ex;
-          rep_cnt++;
-          is_item = true;
-        }
+        if (n <= 16) ex = extra_visits_reg<16>(v + b, (int)n);
+        else mid = true;
       }
+    }
+    // 16 < n <= 48 (6% of the polygons, but in 85% of the warps): the whole warp
+    // per polygon, first occurrences by __match_any_sync / shuffles, instead of
+    // every lane of such a warp running the 48-wide quadratic compare
+    for (unsigned mm = __ballot_sync(kFull, mid); mm; mm &= mm - 1) {
+      const int src = __ffs(mm) - 1;
+      const int64_t bb = __shfl_sync(kFull, b, src);
+      const int nn = (int)__shfl_sync(kFull, n, src);
+      const int e = warp_extra_64(v + bb, nn, lane_id());
+      if ((int)(threadIdx.x & 31) == src) ex = e;
+    }
+    if (i < P && n <= kClassifyShort && ex > 0) {
+      extra_sum += ex;
+      rep_cnt++;
+      is_item = true;
     }
     const int pl = block_append(is_long, n_long, &s_cnt, &s_base);
     if (is_long) long_list[pl] = (int32_t)i;
