@@ -434,6 +434,14 @@ static int prepare(tm_ctx* ctx, int64_t T, int64_t n = -1) {
   return TM_OK;
 }
 
+// debug timeline (TERMESH_STAMPS=1): globaltimer when a stream reaches a point, in
+// dbg[100 + k] (tm_ctx_debug; tools/trace_step.py).  Off: no launches.
+static void stamp(tm_ctx* ctx, int k, cudaStream_t s) {
+  static int on = -1;
+  if (on < 0) on = getenv("TERMESH_STAMPS") != nullptr;
+  if (on) launch_stamp(dc_of(ctx)->dbg + 100 + k, s);
+}
+
 // ---------------------------------------------------------------- enqueue (no host syncs)
 static int label_one(const tm_ctx* ctx) {
   return ctx->label_one < 0 ? (ctx->label_a_external ? 1 : 0) : ctx->label_one;
@@ -447,6 +455,7 @@ static int enqueue_label(tm_ctx* ctx, const double* d_xy, int64_t n, const void*
   const int shrink = check && ctx->label_shrink > 0 ? 0 : ctx->label_shrink;
   const bool lt = ctx->label_timing;  // phase API: device time of each pass (tm_ctx_label_ms)
   if (lt) CK(cudaEventRecord(ctx->lev[0], s));
+  stamp(ctx, 0, s);
   if (!ctx->label_a_external) {
     SegTimer t_(ctx, S_LABEL_A, s);
     launch_label_a(d_xy, n, d_tri, tri_bits == 64, T, check, d_tri32, d_hw, d_me, d_seed, d_tv, ctx->slots.p,
@@ -460,6 +469,7 @@ static int enqueue_label(tm_ctx* ctx, const double* d_xy, int64_t n, const void*
                    d_tv, ctx->slots.p, check, &dc->st, s, shrink, label_one(ctx));
   }
   if (lt) CK(cudaEventRecord(ctx->lev[2], s));
+  stamp(ctx, 1, s);
   CK(cudaGetLastError());
   return TM_OK;
 }
@@ -524,11 +534,13 @@ static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* 
                        ctx->len.as<int64_t>(), ctx->nrul.as<int64_t>(),
                        ctx->early_long ? ctx->long_list.as<int32_t>() : nullptr, &dc->n_long, &dc->st, s);
   }
+  stamp(ctx, 2, s);
   {
     SegTimer t_(ctx, S_TRAV_SCAN, s);
     launch_scan_lookback(ctx->len.as<int64_t>(), ctx->nrul.as<int64_t>(), d_off, ctx->eoff.as<int64_t>(), &dc->n_seeds,
                          Tn, ctx->lbscan.p, s, &dc->n_slots0, &dc->n_entries);
   }
+  stamp(ctx, 3, s);
   {
     SegTimer t_(ctx, S_TRAV_WRITE, s);
     launch_chain_emit(ctx->start.as<int32_t>(), &dc->n_seeds, Tn, ctx->rulers.as<RulerRec>(), d_off, ctx->eoff.as<int64_t>(), ctx->ent_r.as<int32_t>(), ctx->ent_base.as<int64_t>(),
@@ -537,26 +549,33 @@ static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* 
       // fork: the long polygons' runs -> their classification -> the long-item
       // repair kernel, on ctx->aux beside the rest of the traversal and the short items
       cudaStream_t a = ctx->aux;
+      stamp(ctx, 4, s);
       CK(cudaEventRecord(ctx->ev_fork, s));
       CK(cudaStreamWaitEvent(a, ctx->ev_fork, 0));
+      stamp(ctx, 11, a);
       launch_ruler_write_list(d_tri32, d_hw, ctx->long_list.as<int32_t>(), &dc->n_long, ctx->eoff.as<int64_t>(),
                               ctx->ent_r.as<int32_t>(), ctx->ent_base.as<int64_t>(), ctx->rulers.as<RulerRec>(), T, Tn,
                               d_v, ctx->path_hv, a);
+      stamp(ctx, 12, a);
       launch_classify(d_off, d_v, &dc->n_seeds, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(),
                       &dc->n_items, ctx->long_list.as<int32_t>(), &dc->n_long, dc->stats, long_queue(ctx),
                       ctx->path_hv, ctx->tv.as<int32_t>(), 2, ctx->item_state.as<int32_t>(), ctx->pool.as<int32_t>(),
                       &dc->pool_top, ctx->pool_cap, ctx->item_depth.as<int32_t>(), a);
       CK(cudaEventRecord(ctx->ev_cls, a));
+      stamp(ctx, 13, a);
       {
         RepairArgs ra = repair_args(ctx, d_tri32, const_cast<int32_t*>(d_hw), ctx->tv.as<int32_t>(), T, d_off, d_v);
         launch_repair_tips_long(ra, a);
+        stamp(ctx, 14, a);
         launch_repair_pinch(ra, 2, a);  // the finished long items' pinch pass, still beside the short items
       }
+      stamp(ctx, 15, a);
       CK(cudaEventRecord(ctx->ev_join, a));
     }
     launch_ruler_write(d_tri32, d_hw, &dc->n_entries, ctx->ent_r.as<int32_t>(), ctx->ent_base.as<int64_t>(),
                        ctx->rulers.as<RulerRec>(), T, ctx->ecap, d_v, ctx->path_hv, s);
   }
+  stamp(ctx, 5, s);
   CK(cudaGetLastError());
   return TM_OK;
 }
@@ -576,6 +595,7 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
                     const_cast<int32_t*>(d_tv), early ? 1 : 0, ctx->item_state.as<int32_t>(), ctx->pool.as<int32_t>(),
                     &dc->pool_top, ctx->pool_cap, ctx->item_depth.as<int32_t>(), s);
   }
+  stamp(ctx, 6, s);
   if (early) CK(cudaStreamWaitEvent(s, ctx->ev_cls, 0));  // the item list is complete
   RepairArgs a = repair_args(ctx, d_tri32, d_hw, d_tv, T, d_off_in, d_v_in);
   {
@@ -593,18 +613,23 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
       launch_repair_pinch(a, 2, sl);
       if (!serial) CK(cudaEventRecord(ctx->ev_join, ctx->aux));
     }
+    stamp(ctx, 16, s);
     launch_repair_tips(a, 0, s);
+    stamp(ctx, 7, s);
     {
       SegTimer t_(ctx, S_REPAIR_PINCH, s);
       launch_repair_pinch(a, 0, s);  // short items' pinch pass, still beside the long items
     }
+    stamp(ctx, 17, s);
     if (early || !serial) CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
+    stamp(ctx, 8, s);
     launch_repair_tips(a, 1, s);  // long items the shared-memory kernel handed back
   }
   {
     SegTimer t_(ctx, S_REPAIR_PINCH, s);
     launch_repair_pinch(a, 1, s);
   }
+  stamp(ctx, 9, s);
   {
     SegTimer t_(ctx, S_STITCH, s);
     launch_out_counts(d_off_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->item_n.as<int32_t>(),
@@ -616,6 +641,7 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
                   ctx->item_list.as<int64_t>(), ctx->item_n.as<int32_t>(), ctx->pool.as<int32_t>(),
                   ctx->pbase.as<int64_t>(), ctx->sbase.as<int64_t>(), d_off_out, d_v_out, s);
   }
+  stamp(ctx, 10, s);
   CK(cudaGetLastError());
   return TM_OK;
 }

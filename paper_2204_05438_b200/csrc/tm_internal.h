@@ -91,6 +91,7 @@ void launch_ruler_write_list(const int32_t* tri, const int32_t* hw, const int32_
                              int64_t T, int64_t Pcap, int32_t* verts, int32_t* hv, cudaStream_t s);
 
 // tm_repair.cu
+void launch_stamp(unsigned long long* slot, cudaStream_t s);  // debug timeline (globaltimer)
 struct LongQueue {       // work items longer than kLongMin, longest class first
   int32_t* huge;
   int32_t* longq;

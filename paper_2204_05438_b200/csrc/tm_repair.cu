@@ -2744,6 +2744,15 @@ void launch_finalize(const int64_t* Pp, const int64_t* pbase, const int64_t* sba
   note_launch(1);
 }
 
+__global__ void k_stamp(unsigned long long* slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *slot = t;
+}
+
+// debug timeline (TERMESH_STAMPS): the time a stream reaches this point
+void launch_stamp(unsigned long long* slot, cudaStream_t s) { k_stamp<<<1, 1, 0, s>>>(slot); }
+
 void launch_undo(int32_t* hw, const int32_t* undo, const unsigned long long* undo_top, unsigned long long cap,
                  cudaStream_t s) {
   k_undo<<<kNumSMs, 256, 0, s>>>(hw, undo, undo_top, cap);
