@@ -2495,14 +2495,13 @@ __global__ void __launch_bounds__(256) k_out_counts(const int64_t* __restrict__ 
 }
 
 // untouched polygons: one thread each, up to 16 independent loads in flight
-__global__ void __launch_bounds__(256) k_stitch_plain(const int64_t* __restrict__ off, const int32_t* __restrict__ v,
-                                                      const int64_t* __restrict__ Pp,
-                                                      const int32_t* __restrict__ item_of,
-                                                      const int64_t* __restrict__ pbase,
-                                                      const int64_t* __restrict__ sbase,
-                                                      int64_t* __restrict__ off_out, int32_t* __restrict__ v_out) {
+__device__ __forceinline__ void stitch_plain(const int64_t* __restrict__ off, const int32_t* __restrict__ v,
+                                             const int64_t* __restrict__ Pp, const int32_t* __restrict__ item_of,
+                                             const int64_t* __restrict__ pbase, const int64_t* __restrict__ sbase,
+                                             int64_t* __restrict__ off_out, int32_t* __restrict__ v_out, int64_t blk,
+                                             int64_t nblk) {
   const int64_t P = *Pp;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t i = blk * blockDim.x + threadIdx.x; i < P; i += nblk * blockDim.x) {
     if (item_of[i] >= 0) continue;
     int64_t b = off[i], n = off[i + 1] - b, sb = sbase[i];
     off_out[pbase[i]] = sb;
@@ -2519,18 +2518,15 @@ __global__ void __launch_bounds__(256) k_stitch_plain(const int64_t* __restrict_
 }
 
 // repaired polygons: one warp per work item, leaves flattened across lanes
-__global__ void __launch_bounds__(256) k_stitch_items(const int32_t* __restrict__ items,
-                                                      const unsigned int* n_items,
-                                                      const int64_t* __restrict__ item_list,
-                                                      const int32_t* __restrict__ item_n,
-                                                      const int32_t* __restrict__ pool,
-                                                      const int64_t* __restrict__ pbase,
-                                                      const int64_t* __restrict__ sbase,
-                                                      int64_t* __restrict__ off_out, int32_t* __restrict__ v_out) {
+__device__ __forceinline__ void stitch_items(const int32_t* __restrict__ items, const unsigned int* n_items,
+                                             const int64_t* __restrict__ item_list, const int32_t* __restrict__ item_n,
+                                             const int32_t* __restrict__ pool, const int64_t* __restrict__ pbase,
+                                             const int64_t* __restrict__ sbase, int64_t* __restrict__ off_out,
+                                             int32_t* __restrict__ v_out, int64_t blk, int64_t nblk) {
   const int lane = threadIdx.x & 31;
   const unsigned int ni = *n_items;
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t warp = (blk * blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = (nblk * blockDim.x) >> 5;
   for (int64_t w = warp; w < ni; w += nwarps) {
     int32_t i = items[w];
     int64_t list = item_list[w];
@@ -2568,6 +2564,24 @@ __global__ void __launch_bounds__(256) k_stitch_items(const int32_t* __restrict_
       sb += total;
     }
   }
+}
+
+// The final CSR in one launch: every third block copies repaired items (one
+// warp per item), the others untouched polygons (one thread each) -- the two
+// parts are independent, and one after the other they were both on the tail
+// of the step.
+__global__ void __launch_bounds__(256) k_stitch(const int64_t* __restrict__ off, const int32_t* __restrict__ v,
+                                                const int64_t* __restrict__ Pp, const int32_t* __restrict__ item_of,
+                                                const int32_t* __restrict__ items, const unsigned int* n_items,
+                                                const int64_t* __restrict__ item_list,
+                                                const int32_t* __restrict__ item_n, const int32_t* __restrict__ pool,
+                                                const int64_t* __restrict__ pbase, const int64_t* __restrict__ sbase,
+                                                int64_t* __restrict__ off_out, int32_t* __restrict__ v_out) {
+  const int64_t b = blockIdx.x, g = gridDim.x;
+  if (b % 3 == 2)
+    stitch_items(items, n_items, item_list, item_n, pool, pbase, sbase, off_out, v_out, b / 3, g / 3);
+  else
+    stitch_plain(off, v, Pp, item_of, pbase, sbase, off_out, v_out, b - (b + 1) / 3, g - g / 3);
 }
 
 __global__ void k_finalize(const int64_t* __restrict__ Pp, const int64_t* __restrict__ pbase,
@@ -2733,9 +2747,9 @@ void launch_stitch(const int64_t* off, const int32_t* v, const int64_t* Pp, int6
                    const int32_t* items, const unsigned int* n_items, const int64_t* item_list, const int32_t* item_n,
                    const int32_t* pool, const int64_t* pbase, const int64_t* sbase, int64_t* off_out, int32_t* v_out,
                    cudaStream_t s) {
-  k_stitch_plain<<<grid_for(Pcap, 256), 256, 0, s>>>(off, v, Pp, item_of, pbase, sbase, off_out, v_out);
-  k_stitch_items<<<kNumSMs * 8, 256, 0, s>>>(items, n_items, item_list, item_n, pool, pbase, sbase, off_out, v_out);
-  note_launch(2);
+  k_stitch<<<kNumSMs * 12, 256, 0, s>>>(off, v, Pp, item_of, items, n_items, item_list, item_n, pool, pbase, sbase,
+                                        off_out, v_out);
+  note_launch(1);
 }
 
 void launch_finalize(const int64_t* Pp, const int64_t* pbase, const int64_t* sbase, int64_t* off_out,

@@ -22,13 +22,15 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --c
    python bench.py --workload u1m --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch_u1m.log 2>&1
 EXTRA=l1tex__m_l1tex2xbar_write_sectors_mem_global_op_atom.sum,l1tex__m_l1tex2xbar_write_sectors_mem_global_op_red.sum,smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio,dram__bytes_read.sum,dram__bytes_write.sum
 timeout 1500 ncu --set full --metrics $EXTRA --clock-control none --import-source on \
-   -k "regex:k_tri_pass|k_pair_pass|k_ruler_walk|k_ruler_write|k_repair_tips|k_stitch_plain|k_chain|k_classify" -s 26 -c 12 \
+   -k "regex:k_tri_pass|k_pair_pass|k_ruler_walk|k_ruler_write|k_repair_tips|k_stitch|k_chain|k_classify" -s 26 -c 12 \
    -o gpurun_out/prof_u10m python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full_u10m.log 2>&1
 ncu -i gpurun_out/prof_u10m.ncu-rep --page raw --csv > gpurun_out/prof_u10m_raw.csv 2>&1
 timeout 900 python tools/partition_scaling.py --workload u10m --steps 10 > gpurun_out/scaling_u10m.json 2>&1
 timeout 900 python tools/partition_scaling.py --workload u10m --steps 6 --split > gpurun_out/scaling_split_u10m.json 2>&1
 timeout 900 python tools/delaunay_check.py 10000000 --against qhull > gpurun_out/delaunay_10m.log 2>&1
 TRACE_WORKLOAD=u1m timeout 600 python tools/trace_long.py > gpurun_out/trace_u1m.log 2>&1
+TERMESH_STAMPS=1 timeout 600 python tools/trace_step.py u10m > gpurun_out/trace_step.log 2>&1
+timeout 300 python tools/pcie_probe.py > gpurun_out/pcie_probe.json 2>&1
 ( time python -c "import bench; t = bench.load_mesh('u100m', 0)" ) > gpurun_out/gen_u100m.log 2>&1
 timeout 1200 python bench.py --workload u100m --steps 10 --warmup 3 > gpurun_out/bench_u100m.json 2> gpurun_out/bench_u100m.err
 timeout 1800 python tools/partition_scaling.py --workload u100m --steps 5 > gpurun_out/scaling_u100m.json 2>&1

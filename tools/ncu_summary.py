@@ -39,7 +39,7 @@ COLUMNS = [
 ]
 SEGMENT = {"k_tri_pass": "label_a_tri_pass", "k_pair_pass": "label_b_edges", "k_ruler_walk": "trav_rulers",
            "k_ruler_write": "trav_write", "k_chain_count": "trav_chain", "k_repair_tips_seg": "repair_tips",
-           "k_repair_tips": "repair_tips_short", "k_stitch_plain": "repair_stitch"}
+           "k_repair_tips": "repair_tips_short", "k_stitch_plain": "repair_stitch", "k_stitch": "repair_stitch"}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1e-9, "us": 1e-6, "usecond": 1e-6,
          "ms": 1e-3, "msecond": 1e-3, "s": 1, "second": 1, "nsecond": 1e-9}
 
