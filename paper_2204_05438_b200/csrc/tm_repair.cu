@@ -2730,7 +2730,13 @@ void launch_repair_pinch(const RepairArgs& a, int mode, cudaStream_t s) {
     attr = true;
   }
   // mode 2 runs beside the short-item kernels: a few blocks (128 KB of shared memory each)
-  k_repair_pinch<<<mode == 2 ? 16 : mode ? kNumSMs : kNumSMs * 2, 128, smem, s>>>(c, a.items, a.n_items, a.off, a.item_list, a.item_n,
+  static int p2 = -1;
+  if (p2 < 0) {  // tuning hook: TERMESH_PINCH2_BLOCKS
+    const char* e = getenv("TERMESH_PINCH2_BLOCKS");
+    p2 = (e && *e) ? atoi(e) : 16;
+    if (p2 < 1) p2 = 16;
+  }
+  k_repair_pinch<<<mode == 2 ? p2 : mode ? kNumSMs : kNumSMs * 2, 128, smem, s>>>(c, a.items, a.n_items, a.off, a.item_list, a.item_n,
                                                                   a.item_slots, a.item_state, a.item_depth, a.q,
                                                                   a.stats, mode);
   note_launch(1);
