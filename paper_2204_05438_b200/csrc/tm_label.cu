@@ -333,6 +333,15 @@ __device__ __forceinline__ uint32_t local_slot(int32_t lo, int32_t hi) {
 #ifndef TM_PAIR_MINB
 #define TM_PAIR_MINB 6
 #endif
+// A/B switches (measured and rejected): software-pipelined
+// chunks -- the extra live registers cost a resident block per SM and the
+// passes are bound by random-sector throughput, not by a chunk's chain.
+#ifndef TM_TRI_PF
+#define TM_TRI_PF 0
+#endif
+#ifndef TM_PAIR_PF
+#define TM_PAIR_PF 0
+#endif
 template <typename TI, bool ONE>
 __global__ void __launch_bounds__(kLabelThreads, TM_TRI_MINB) k_tri_pass(const double2* __restrict__ xy,
                                                             const float2* __restrict__ xy32, int64_t n,
@@ -349,7 +358,28 @@ __global__ void __launch_bounds__(kLabelThreads, TM_TRI_MINB) k_tri_pass(const d
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const bool local = !check;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = t_begin + blockIdx.x * (int64_t)blockDim.x; base < T; base += stride) {
+  int64_t base = t_begin + blockIdx.x * (int64_t)blockDim.x;
+#if TM_TRI_PF >= 1
+  // Software pipeline over the grid-stride chunks: the next chunk's corners
+  // (and, TM_TRI_PF >= 2, its three coordinate records) are requested while the
+  // current chunk does its shared-memory matching and table inserts, so a
+  // chunk's dependent chain is bucket load -> CAS instead of corners -> coordinates
+  // -> bucket load -> CAS.
+  int64_t na = 0, nb = 0, nc = 0;
+  if (base + threadIdx.x < T) {
+    const int64_t t0 = base + threadIdx.x;
+    na = (int64_t)__ldg(tri + 3 * t0), nb = (int64_t)__ldg(tri + 3 * t0 + 1), nc = (int64_t)__ldg(tri + 3 * t0 + 2);
+  }
+#endif
+#if TM_TRI_PF >= 2
+  const bool pf_xy = xy32 == nullptr;
+  double2 qa = make_double2(0.0, 0.0), qb = qa, qc = qa;
+  if (pf_xy && base + threadIdx.x < T && (uint64_t)na < (uint64_t)n && (uint64_t)nb < (uint64_t)n &&
+      (uint64_t)nc < (uint64_t)n) {
+    qa = xy[na], qb = xy[nb], qc = xy[nc];
+  }
+#endif
+  for (; base < T; base += stride) {
     const int64_t t = base + threadIdx.x;
     if (local) {
       for (int i = threadIdx.x; i < kLocalSlots; i += kLabelThreads) lown[i] = 0;
@@ -358,8 +388,19 @@ __global__ void __launch_bounds__(kLabelThreads, TM_TRI_MINB) k_tri_pass(const d
     unsigned flags = 0, desc = 0;
     int me0 = -1;
     int32_t hh[3], oo[3], gg[3];
+#if TM_TRI_PF >= 2
+    const double2 ca = qa, cb = qb, cc = qc;  // this chunk's coordinates (valid when its corners are in range)
+#endif
     if (t < T) {
+#if TM_TRI_PF >= 1
+      const int64_t a = na, b = nb, c = nc;
+      if (t + stride < T) {
+        const int64_t tn = t + stride;
+        na = (int64_t)__ldg(tri + 3 * tn), nb = (int64_t)__ldg(tri + 3 * tn + 1), nc = (int64_t)__ldg(tri + 3 * tn + 2);
+      }
+#else
       int64_t a = (int64_t)__ldg(tri + 3 * t), b = (int64_t)__ldg(tri + 3 * t + 1), c = (int64_t)__ldg(tri + 3 * t + 2);
+#endif
       const bool bad = a < 0 || a >= n || b < 0 || b >= n || c < 0 || c >= n;
       if (!ONE || bad) {  // provisional border labels (ONE: every half-edge is labelled by whoever resolves it)
         hw[3 * t] = -1;
@@ -383,6 +424,10 @@ __global__ void __launch_bounds__(kLabelThreads, TM_TRI_MINB) k_tri_pass(const d
         if (me0 < 0) {
 #ifdef TM_AB_NO_XY  // A/B timing builds only (wrong labels): what the coordinate gathers cost
           me0 = (int)(t % 3);
+#elif TM_TRI_PF >= 2
+          double2 pa = ca, pb = cb, pc = cc;
+          if (!pf_xy) pa = xy[a], pb = xy[b], pc = xy[c];
+          me0 = argmax3(sqlen(pb, pc), sqlen(pc, pa), sqlen(pa, pb));
 #else
           const double2 pa = xy[a], pb = xy[b], pc = xy[c];
           me0 = argmax3(sqlen(pb, pc), sqlen(pc, pa), sqlen(pa, pb));
@@ -390,7 +435,12 @@ __global__ void __launch_bounds__(kLabelThreads, TM_TRI_MINB) k_tri_pass(const d
         }
         max_edge[t] = (int8_t)me0;
         if (check) {
+#if TM_TRI_PF >= 2
+          double2 pa = ca, pb = cb, pc = cc;
+          if (!pf_xy) pa = xy[a], pb = xy[b], pc = xy[c];
+#else
           const double2 pa = xy[a], pb = xy[b], pc = xy[c];
+#endif
           // mesh_core.signed_areas (160-168), sign only, unfused
           double d = __dsub_rn(__dmul_rn(__dsub_rn(pb.x, pa.x), __dsub_rn(pc.y, pa.y)),
                                __dmul_rn(__dsub_rn(pb.y, pa.y), __dsub_rn(pc.x, pa.x)));
@@ -468,6 +518,12 @@ __global__ void __launch_bounds__(kLabelThreads, TM_TRI_MINB) k_tri_pass(const d
         }
       flags |= desc;
     }
+#if TM_TRI_PF >= 2
+    if (pf_xy && t + stride < T && (uint64_t)na < (uint64_t)n && (uint64_t)nb < (uint64_t)n &&
+        (uint64_t)nc < (uint64_t)n) {
+      qa = xy[na], qb = xy[nb], qc = xy[nc];  // next chunk's coordinates, in flight during the inserts
+    }
+#endif
     int m = warp_compact3(flags, lane, sq[wid][0], sq[wid][1], sq[wid][2], hh, oo, gg);
 #ifndef TM_AB_NO_TABLE  // A/B timing builds only (wrong labels): what the table inserts cost
     for (int i = lane; i < m; i += 32) {
@@ -497,14 +553,39 @@ __global__ void __launch_bounds__(kLabelThreads, TM_PAIR_MINB) k_pair_pass(const
   __shared__ int32_t sq[kLabelWarps][3][96];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+#if TM_PAIR_PF
+  // the next chunk's corners and packed words are requested before this chunk's
+  // lookups (descending entries -- the only ones tested -- are written by their
+  // own thread alone, so the early read sees their final pass-A value)
+  int32_t nv0 = 0, nv1 = 0, nv2 = 0, nw0 = 0, nw1 = 0, nw2 = 0;
+  {
+    const int64_t t0 = t_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t0 < T) {
+      nv0 = __ldg(tri32 + 3 * t0), nv1 = __ldg(tri32 + 3 * t0 + 1), nv2 = __ldg(tri32 + 3 * t0 + 2);
+      nw0 = hw[3 * t0], nw1 = hw[3 * t0 + 1], nw2 = hw[3 * t0 + 2];
+    }
+  }
+#endif
   for (int64_t t = t_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t - lane < T; t += stride) {
     unsigned flags = 0;
     int32_t hh[3], oo[3], gg[3];
     if (t < T) {
+#if TM_PAIR_PF
+      const int32_t cv[3] = {nv0, nv1, nv2};
+      const int32_t w[3] = {nw0, nw1, nw2};
+      if (t + stride < T) {
+        const int64_t tn = t + stride;
+        nv0 = __ldg(tri32 + 3 * tn), nv1 = __ldg(tri32 + 3 * tn + 1), nv2 = __ldg(tri32 + 3 * tn + 2);
+        nw0 = hw[3 * tn], nw1 = hw[3 * tn + 1], nw2 = hw[3 * tn + 2];
+      }
+#else
       const int32_t cv[3] = {__ldg(tri32 + 3 * t), __ldg(tri32 + 3 * t + 1), __ldg(tri32 + 3 * t + 2)};
+#endif
       if ((uint32_t)cv[0] < (uint32_t)n && (uint32_t)cv[1] < (uint32_t)n && (uint32_t)cv[2] < (uint32_t)n) {
         // a descending half-edge pass A already paired inside its block is no longer border
+#if !TM_PAIR_PF
         const int32_t w[3] = {hw[3 * t], hw[3 * t + 1], hw[3 * t + 2]};
+#endif
 #pragma unroll
         for (int j = 0; j < 3; j++) {
           hh[j] = (int32_t)(3 * t + j);

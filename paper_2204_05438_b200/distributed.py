@@ -38,6 +38,38 @@ def partition(T: int, world: int) -> list[tuple[int, int]]:
     return [(r * T // world, (r + 1) * T // world) for r in range(world)]
 
 
+def balance_partition(bounds, rank_cost, damping: float = 1.0) -> list[tuple[int, int]]:
+    """Cost-balanced consecutive seed ranges for the next call on the same mesh.
+
+    bounds: the ranges just used (consecutive, covering [0, T)); rank_cost: the
+    cost each rank measured for its range (device ms of its traversal + repair).
+    Each range's cost is taken as spread evenly over its triangles; the new
+    boundaries cut the resulting piecewise-linear cumulative cost into G equal
+    parts (damping < 1 moves each boundary only part of the way).  Repeated
+    calls converge onto the measured cost profile -- e.g. the rank holding the
+    hull-sliver repair lineage (one dependent chain) ends up with a narrow
+    range.  Any consecutive ranges give the single-GPU output (the
+    rank-ordered concatenation is the ascending seed order), so balancing
+    never changes the result, only who does which seeds."""
+    G = len(bounds)
+    if G != len(rank_cost) or G == 0:
+        raise ValueError("one cost per range")
+    T = bounds[-1][1]
+    edges = np.array([b for b, _ in bounds] + [T], dtype=np.float64)
+    cost = np.maximum(np.asarray(rank_cost, dtype=np.float64), 0.0)
+    if G == 1 or T == 0 or cost.sum() <= 0:
+        return [tuple(map(int, x)) for x in bounds]
+    cum = np.concatenate([[0.0], np.cumsum(cost)])
+    targets = cum[-1] * np.arange(1, G) / G
+    cuts = np.interp(targets, cum, edges)  # inverse of the piecewise-linear cumulative cost
+    cuts = edges[1:-1] + damping * (cuts - edges[1:-1])
+    c = np.round(cuts).astype(np.int64)
+    c = np.clip(c, 0, T)
+    c = np.maximum.accumulate(c)  # monotone
+    out = [0] + c.tolist() + [T]
+    return [(int(out[r]), int(out[r + 1])) for r in range(G)]
+
+
 def exclusive_bases(counts) -> tuple[np.ndarray, np.ndarray]:
     """counts[r] = (polygons, slots) of rank r -> (polygon base, slot base) per rank."""
     c = np.asarray(counts, dtype=np.int64).reshape(-1, 2)
@@ -334,9 +366,12 @@ def polygons_from_labels(ctx, n: int, T: int, t_begin: int, t_end: int, off=None
     return off, verts, npol.value, nsl.value, dict(zip(_capi.STAT_NAMES, list(stats)))
 
 
-def execute_distributed(tri, group=None, gather: bool = True, comm: Comm | None = None, split_labels_mode=False):
+def execute_distributed(tri, group=None, gather: bool = True, comm: Comm | None = None, split_labels_mode=False,
+                        seed_ranges=None):
     """Drop-in multi-GPU execute: every rank passes the same Triangulation; the
-    global final CSR comes back on rank 0 (gather=True) or as shards."""
+    global final CSR comes back on rank 0 (gather=True) or as shards.
+    seed_ranges: consecutive per-rank seed ranges covering [0, T) (e.g. from
+    balance_partition after a previous call on the same mesh); default equal."""
     import torch
     import torch.distributed as dist
     rank, world = dist.get_rank(group), dist.get_world_size(group)
@@ -348,11 +383,16 @@ def execute_distributed(tri, group=None, gather: bool = True, comm: Comm | None 
     ctx = _capi.context(dev)
     if comm is None and (split_labels_mode or dist.get_backend(group) == "nccl"):
         comm = Comm(group)  # the library's own communicator for the exchange
+    if seed_ranges is not None and (len(seed_ranges) != world or seed_ranges[0][0] != 0 or seed_ranges[-1][1] != T
+                                    or any(seed_ranges[r][1] != seed_ranges[r + 1][0] for r in range(world - 1))):
+        raise ValueError("seed_ranges must be consecutive ranges covering [0, T), one per rank")
     if split_labels_mode:
         b, e = split_labels(ctx, xy, tr, n, T, comm, rank, world)
+        if seed_ranges is not None:
+            b, e = seed_ranges[rank]
         off, verts, p, f, stats = polygons_from_labels(ctx, n, T, b, e)
     else:
-        b, e = partition(T, world)[rank]
+        b, e = partition(T, world)[rank] if seed_ranges is None else seed_ranges[rank]
         off, verts, p, f, stats = run_partition(xy, tr, n, T, b, e, ctx=ctx)
     shard = stitch(off, verts, p, f, group, pinch=(stats["pinch_extra"], stats["pinch_deferred"]),
                    resume=device_resume(ctx, off, verts, T), comm=comm)

@@ -212,3 +212,56 @@ def test_split_labels_single_rank_nccl(cuda):
             assert np.array_equal(csr[0], g["final_off"]) and np.array_equal(csr[1], g["final_verts"])
     finally:
         dist.destroy_process_group()
+
+
+def test_balance_partition_properties():
+    """Measured-cost rebalancing: consecutive ranges covering [0, T), and on a
+    cost profile with one expensive point (a repair lineage) the iteration
+    converges to ranges of near-equal cost."""
+    T, G = 1_000_000, 8
+    dens = np.ones(T)
+    dens[T - 1000:T - 990] += 2e5 / 10  # a concentrated chain near the end (hull band last)
+    cum = np.concatenate([[0.0], np.cumsum(dens)])
+
+    def cost(bounds):
+        return [cum[e] - cum[b] for b, e in bounds]
+
+    bounds = D.partition(T, G)
+    first = max(cost(bounds))
+    for _ in range(6):
+        bounds = D.balance_partition(bounds, cost(bounds))
+        assert bounds[0][0] == 0 and bounds[-1][1] == T
+        assert all(b <= e for b, e in bounds) and all(bounds[r][1] == bounds[r + 1][0] for r in range(G - 1))
+    c = cost(bounds)
+    floor = max(2e5, cum[-1] / G)  # the chain cannot be split
+    assert max(c) <= 1.05 * floor < 0.7 * first
+    assert D.balance_partition([(0, 10)], [3.0]) == [(0, 10)]
+    assert D.balance_partition([(0, 5), (5, 10)], [0.0, 0.0]) == [(0, 5), (5, 10)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [3, 8])
+@pytest.mark.parametrize("name", CASES)
+def test_split_labels_rebalanced_seed_ranges(cuda, name, world):
+    """Seed ranges that differ from the label chunks (measured-cost
+    rebalancing, here from a skewed synthetic cost) give the same stitched
+    output: only the seed ranges decide who repairs what."""
+    import sys
+    import torch
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import split_emulation
+    tri, g = load_case(name)
+    n, T = tri.n_vertices, tri.n_triangles
+    xy = torch.from_numpy(tri.vertices).to(cuda)
+    tr = torch.from_numpy(tri.triangles).to(cuda)
+    seeds = D.balance_partition(D.partition_chunks(T, world), [1.0 + 5.0 * (r == world - 1) for r in range(world)])
+    assert seeds != D.partition_chunks(T, world)
+    _, out, _ = split_emulation.run(xy, tr, n, T, world, seeds=seeds, segments=True)
+    offs, verts, base = [], [], 0
+    for off, v, p, f, st in out:
+        offs.append(off[:p].cpu().numpy() + base)
+        verts.append(v[:f].cpu().numpy())
+        base += f
+    got_off = np.concatenate(offs + [np.array([base])])
+    got_v = np.concatenate(verts)
+    assert np.array_equal(got_off, g["final_off"]) and np.array_equal(got_v, g["final_verts"])

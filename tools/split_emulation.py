@@ -27,11 +27,16 @@ def _timed(fn, flush=None):
     return r, e0.elapsed_time(e1)
 
 
-def run(xy, tr, n, T, G, flush=None, ctx=None):
+def run(xy, tr, n, T, G, flush=None, ctx=None, seeds=None, segments=False):
+    """seeds: the ranks' seed ranges for traversal + repair (default: the label
+    chunks; D.balance_partition gives cost-balanced ones -- the label chunks stay
+    equal so the all-gathers have one size per rank).  segments: also collect
+    each rank's per-kernel device times (a separate profiled run)."""
     dev = xy.device
     L = _capi.lib()
     sp = _capi.stream_ptr(dev)
     parts = D.partition_chunks(T, G)
+    seeds = seeds or parts
     own = ctx is None
     ctx = ctx or _capi.Context(dev.index or 0)
     hw = torch.empty(3 * T, dtype=torch.int32, device=dev)  # the label all-gather's result
@@ -66,15 +71,25 @@ def run(xy, tr, n, T, G, flush=None, ctx=None):
     off = torch.empty(T + 1, dtype=torch.int64, device=dev)
     v = torch.empty(max(3 * T, 1), dtype=torch.int32, device=dev)
     extras = []
-    for r, (b, e) in enumerate(parts):
+    for r, (b, e) in enumerate(seeds):
         ctx.check(L.tm_ctx_copy_labels(ctx.ptr, 1, _capi.ptr(hw), _capi.ptr(sd), _capi.ptr(me), 0, T, sp))
         D.polygons_from_labels(ctx, n, T, b, e, off, v)  # graph capture / warm-up outside the timing
         ctx.check(L.tm_ctx_copy_labels(ctx.ptr, 1, _capi.ptr(hw), _capi.ptr(sd), _capi.ptr(me), 0, T, sp))
         res, t[r]["polygons"] = _timed(lambda: D.polygons_from_labels(ctx, n, T, b, e, off, v), flush)
         extras.append(res[4]["pinch_extra"])
+        if segments:
+            ctx.check(L.tm_ctx_copy_labels(ctx.ptr, 1, _capi.ptr(hw), _capi.ptr(sd), _capi.ptr(me), 0, T, sp))
+            ctx.set_profiling(True)
+            ctx.segments(reset=True)
+            if flush is not None:
+                flush.zero_()
+            D.polygons_from_labels(ctx, n, T, b, e, off, v)
+            torch.cuda.synchronize()
+            t[r]["segments"] = {k: round(ms, 4) for k, (ms, c) in ctx.segments(reset=True).items() if c}
+            ctx.set_profiling(False)
     total = sum(extras)
     out = []
-    for r, (b, e) in enumerate(parts):  # the outputs, with the global pinch guard's resume
+    for r, (b, e) in enumerate(seeds):  # the outputs, with the global pinch guard's resume
         ctx.check(L.tm_ctx_copy_labels(ctx.ptr, 1, _capi.ptr(hw), _capi.ptr(sd), _capi.ptr(me), 0, T, sp))
         o, vv, p, f, st = D.polygons_from_labels(ctx, n, T, b, e, off, v)
         if st["pinch_deferred"]:
@@ -82,4 +97,4 @@ def run(xy, tr, n, T, G, flush=None, ctx=None):
         out.append((off[: p + 1].clone(), v[:f].clone(), p, f, st))
     if own:
         ctx.close()
-    return parts, out, t
+    return seeds, out, t
