@@ -82,6 +82,7 @@ struct Counters {
   int64_t dl_ncell, dl_n, dl_ntri;
   unsigned int dl_open, dl_degen;
   unsigned long long n_boundary;  // tm_label_range: boundary entries of the rank
+  int64_t n_isrt, n_units;         // stitch: work items in polygon order, units (runs + items)
 };
 
 constexpr int kUploadChunks = 8;  // triangle upload chunks of tm_mesh_to_polygons_host
@@ -144,7 +145,7 @@ struct tm_ctx {
   Buf seeds, start, len, overflow, queue, stamp, tiles, nrul, eoff, rulers, startbits, ent_r, ent_base;
   // repair
   Buf item_of, items, long_list, item_list, item_n, item_slots, item_state, item_depth, cnt, slotsz, pbase, sbase, pool,
-      undo, hugeq, longq, parked, pinchq;
+      undo, hugeq, longq, parked, pinchq, iflag, isrt, itiles;
   // whole-path buffers
   Buf xy, tri, tri32, hw, max_edge, seed, tv, off0, v0, fin_off, fin_v, hw_snap, hv;
   // tm_post.cu scratch (validation, analytics, canonical form)
@@ -419,10 +420,13 @@ static int prepare(tm_ctx* ctx, int64_t T, int64_t n = -1) {
   ENSURE(parked, Tn * sizeof(int32_t));
   ENSURE(pinchq, Tn * sizeof(int32_t));
   ENSURE(longq, Tn * sizeof(int32_t));
-  ENSURE(cnt, (Tn + 1) * sizeof(int64_t));
-  ENSURE(slotsz, (Tn + 1) * sizeof(int64_t));
-  ENSURE(pbase, (Tn + 1) * sizeof(int64_t));
-  ENSURE(sbase, (Tn + 1) * sizeof(int64_t));
+  ENSURE(cnt, (Tn + 2) * sizeof(int64_t));  // per unit (<= items + 1) or per polygon, + the scan's end element
+  ENSURE(slotsz, (Tn + 2) * sizeof(int64_t));
+  ENSURE(pbase, (Tn + 2) * sizeof(int64_t));
+  ENSURE(sbase, (Tn + 2) * sizeof(int64_t));
+  ENSURE(iflag, Tn * sizeof(uint8_t));
+  ENSURE(isrt, Tn * sizeof(int32_t));
+  ENSURE(itiles, (scan_scratch_elems(Tn) + 8) * sizeof(int64_t));
   // item copies + pieces + per-warp arena slack
   unsigned long long want = 8ull * (unsigned long long)Tn + (1ull << 22);
   const char* forced = getenv("TERMESH_POOL_INIT");  // testing hook: start small, exercise the retry path
@@ -580,6 +584,39 @@ static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* 
   return TM_OK;
 }
 
+// The final CSR from the input CSR and the repaired items.  Default: by units
+// (runs of untouched polygons + the work item after each, tm_repair.cu); the
+// item order is built here when `sort` (else enqueue_repair built it before
+// waiting for the long items).
+static void enqueue_stitch(tm_ctx* ctx, const int64_t* d_off_in, const int32_t* d_v_in, const int64_t* Pp, int64_t Tn,
+                           int64_t* d_off_out, int32_t* d_v_out, bool sort, cudaStream_t s) {
+  Counters* dc = dc_of(ctx);
+#ifdef TM_OLD_STITCH  // A/B: per-polygon counts, scan and copy
+  (void)sort;
+  launch_out_counts(d_off_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->item_n.as<int32_t>(),
+                    ctx->item_slots.as<int64_t>(), ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), dc->stats,
+                    &dc->st, s);
+  launch_scan_lookback(ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), ctx->pbase.as<int64_t>(),
+                       ctx->sbase.as<int64_t>(), Pp, Tn, ctx->lbscan.p, s, &dc->p_out, &dc->f_out, d_off_out);
+  launch_stitch(d_off_in, d_v_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(), &dc->n_items,
+                ctx->item_list.as<int64_t>(), ctx->item_n.as<int32_t>(), ctx->pool.as<int32_t>(),
+                ctx->pbase.as<int64_t>(), ctx->sbase.as<int64_t>(), d_off_out, d_v_out, s);
+#else
+  if (sort)
+    launch_item_sort(ctx->item_of.as<int32_t>(), Pp, Tn, ctx->iflag.as<uint8_t>(), ctx->isrt.as<int32_t>(),
+                     &dc->n_isrt, ctx->itiles.as<int64_t>(), s);
+  launch_unit_counts(d_off_in, Pp, Tn, ctx->isrt.as<int32_t>(), &dc->n_isrt, ctx->item_of.as<int32_t>(),
+                     ctx->item_n.as<int32_t>(), ctx->item_slots.as<int64_t>(), ctx->cnt.as<int64_t>(),
+                     ctx->slotsz.as<int64_t>(), &dc->n_units, dc->stats, &dc->st, s);
+  launch_scan_lookback(ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), ctx->pbase.as<int64_t>(),
+                       ctx->sbase.as<int64_t>(), &dc->n_units, Tn, ctx->lbscan.p, s, &dc->p_out, &dc->f_out,
+                       d_off_out);
+  launch_stitch_units(d_off_in, d_v_in, Pp, ctx->isrt.as<int32_t>(), &dc->n_isrt, ctx->item_of.as<int32_t>(),
+                      ctx->item_list.as<int64_t>(), ctx->item_n.as<int32_t>(), ctx->pool.as<int32_t>(),
+                      ctx->pbase.as<int64_t>(), ctx->sbase.as<int64_t>(), d_off_out, d_v_out, s);
+#endif
+}
+
 // Repair phase.  Pp: device polygon count of the input CSR.
 static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, const int32_t* d_tv, int64_t T,
                           const int64_t* d_off_in, const int32_t* d_v_in, const int64_t* Pp, int64_t* d_off_out,
@@ -621,6 +658,11 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
       launch_repair_pinch(a, 0, s);  // short items' pinch pass, still beside the long items
     }
     stamp(ctx, 17, s);
+#ifndef TM_OLD_STITCH
+    // the work items in polygon order for the stitch, while the long items still run
+    launch_item_sort(ctx->item_of.as<int32_t>(), Pp, Tn, ctx->iflag.as<uint8_t>(), ctx->isrt.as<int32_t>(),
+                     &dc->n_isrt, ctx->itiles.as<int64_t>(), s);
+#endif
     if (early || !serial) CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
     stamp(ctx, 8, s);
     launch_repair_tips(a, 1, s);  // long items the shared-memory kernel handed back
@@ -632,14 +674,7 @@ static int enqueue_repair(tm_ctx* ctx, const int32_t* d_tri32, int32_t* d_hw, co
   stamp(ctx, 9, s);
   {
     SegTimer t_(ctx, S_STITCH, s);
-    launch_out_counts(d_off_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->item_n.as<int32_t>(),
-                      ctx->item_slots.as<int64_t>(), ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), dc->stats,
-                      &dc->st, s);
-    launch_scan_lookback(ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), ctx->pbase.as<int64_t>(),
-                         ctx->sbase.as<int64_t>(), Pp, Tn, ctx->lbscan.p, s, &dc->p_out, &dc->f_out, d_off_out);
-    launch_stitch(d_off_in, d_v_in, Pp, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(), &dc->n_items,
-                  ctx->item_list.as<int64_t>(), ctx->item_n.as<int32_t>(), ctx->pool.as<int32_t>(),
-                  ctx->pbase.as<int64_t>(), ctx->sbase.as<int64_t>(), d_off_out, d_v_out, s);
+    enqueue_stitch(ctx, d_off_in, d_v_in, Pp, Tn, d_off_out, d_v_out, false, s);
   }
   stamp(ctx, 10, s);
   CK(cudaGetLastError());
@@ -725,7 +760,7 @@ void tm_ctx_destroy(tm_ctx* ctx) {
   Buf* bufs[] = {&ctx->counters, &ctx->slots, &ctx->seeds, &ctx->start, &ctx->len, &ctx->overflow, &ctx->queue,
                  &ctx->stamp, &ctx->tiles, &ctx->nrul, &ctx->eoff, &ctx->rulers, &ctx->startbits,
                  &ctx->ent_r, &ctx->ent_base, &ctx->item_of, &ctx->items, &ctx->long_list, &ctx->item_list,
-                 &ctx->item_n, &ctx->item_slots, &ctx->item_state, &ctx->item_depth, &ctx->hugeq, &ctx->longq, &ctx->parked, &ctx->pinchq, &ctx->cnt, &ctx->slotsz, &ctx->pbase, &ctx->sbase, &ctx->pool,
+                 &ctx->item_n, &ctx->item_slots, &ctx->item_state, &ctx->item_depth, &ctx->hugeq, &ctx->longq, &ctx->parked, &ctx->pinchq, &ctx->iflag, &ctx->isrt, &ctx->itiles, &ctx->cnt, &ctx->slotsz, &ctx->pbase, &ctx->sbase, &ctx->pool,
                  &ctx->undo, &ctx->xy, &ctx->tri, &ctx->tri32, &ctx->hw, &ctx->max_edge, &ctx->seed, &ctx->tv,
                  &ctx->off0, &ctx->v0, &ctx->fin_off, &ctx->fin_v, &ctx->hw_snap, &ctx->hv,
                  &ctx->lbscan, &ctx->pbits, &ctx->pflag, &ctx->ptable, &ctx->pstamp, &ctx->ptip, &ctx->prep,
@@ -1160,14 +1195,7 @@ int tm_resume_pinch(tm_ctx* ctx, int64_t extra_total, int64_t* off_out, int32_t*
                              v0);
   launch_repair_pinch(a, 3, s);
   ctx->path_hv = nullptr;
-  launch_out_counts(off0, &dc->n_seeds, Tn, ctx->item_of.as<int32_t>(), ctx->item_n.as<int32_t>(),
-                    ctx->item_slots.as<int64_t>(), ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), dc->stats,
-                    &dc->st, s);
-  launch_scan_lookback(ctx->cnt.as<int64_t>(), ctx->slotsz.as<int64_t>(), ctx->pbase.as<int64_t>(),
-                       ctx->sbase.as<int64_t>(), &dc->n_seeds, Tn, ctx->lbscan.p, s, &dc->p_out, &dc->f_out, d_off);
-  launch_stitch(off0, v0, &dc->n_seeds, Tn, ctx->item_of.as<int32_t>(), ctx->items.as<int32_t>(), &dc->n_items,
-                ctx->item_list.as<int64_t>(), ctx->item_n.as<int32_t>(), ctx->pool.as<int32_t>(),
-                ctx->pbase.as<int64_t>(), ctx->sbase.as<int64_t>(), d_off, d_v, s);
+  enqueue_stitch(ctx, off0, v0, &dc->n_seeds, Tn, d_off, d_v, true, s);
   CK(cudaGetLastError());
   Counters h;
   int rc = finish(ctx, s, &h);

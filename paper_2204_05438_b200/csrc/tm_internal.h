@@ -158,6 +158,17 @@ void launch_stitch(const int64_t* off, const int32_t* v, const int64_t* Pp, int6
                    const int32_t* items, const unsigned int* n_items, const int64_t* item_list, const int32_t* item_n,
                    const int32_t* pool, const int64_t* pbase, const int64_t* sbase, int64_t* off_out, int32_t* v_out,
                    cudaStream_t s);
+// the final CSR by units (runs of untouched polygons + the work item after each)
+void launch_item_sort(const int32_t* item_of, const int64_t* Pp, int64_t Pcap, uint8_t* flag, int32_t* srt,
+                      int64_t* n_srt, int64_t* tiles, cudaStream_t s);
+void launch_unit_counts(const int64_t* off, const int64_t* Pp, int64_t Pcap, const int32_t* srt, const int64_t* n_srt,
+                        const int32_t* item_of, const int32_t* item_n, const int64_t* item_slots, int64_t* cnt,
+                        int64_t* slots, int64_t* n_units, const unsigned long long* stats, DevStatus* st,
+                        cudaStream_t s);
+void launch_stitch_units(const int64_t* off, const int32_t* v, const int64_t* Pp, const int32_t* srt,
+                         const int64_t* n_srt, const int32_t* item_of, const int64_t* item_list, const int32_t* item_n,
+                         const int32_t* pool, const int64_t* pbase, const int64_t* sbase, int64_t* off_out,
+                         int32_t* v_out, cudaStream_t s);
 void launch_finalize(const int64_t* Pp, const int64_t* pbase, const int64_t* sbase, int64_t* off_out,
                      int64_t* p_out, int64_t* f_out, cudaStream_t s);
 void launch_undo(int32_t* hw, const int32_t* undo, const unsigned long long* undo_top, unsigned long long cap,

@@ -2584,6 +2584,146 @@ __global__ void __launch_bounds__(256) k_stitch(const int64_t* __restrict__ off,
     stitch_plain(off, v, Pp, item_of, pbase, sbase, off_out, v_out, b - (b + 1) / 3, g - g / 3);
 }
 
+// ---- the final CSR by UNITS.  In polygon order the untouched polygons come in
+// runs between work items, and a run keeps its order and moves by one shift:
+// unit k = the run before the k-th work item (polygon order) + that item's
+// pieces; unit K = the trailing run.  So the per-unit counts, the scan and the
+// copy cost O(items) + a coalesced copy of the runs, not a count, scan and
+// per-polygon copy over every polygon.
+
+// polygons holding a work item (ordered compaction input); the item set is
+// final after classification
+__global__ void __launch_bounds__(256) k_item_flags(const int32_t* __restrict__ item_of, const int64_t* __restrict__ Pp,
+                                                    int64_t n, uint8_t* __restrict__ flag) {
+  const int64_t P = *Pp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = (i < P && item_of[i] >= 0) ? 1 : 0;
+}
+
+// unit k: run [rs, re) of untouched polygons, then (k < K) the item of polygon re
+__device__ __forceinline__ void unit_range(const int32_t* __restrict__ srt, int64_t K, int64_t P, int64_t k,
+                                           int64_t* rs, int64_t* re) {
+  *rs = k == 0 ? 0 : (int64_t)srt[k - 1] + 1;
+  *re = k < K ? (int64_t)srt[k] : P;
+}
+
+__global__ void __launch_bounds__(256) k_unit_counts(const int64_t* __restrict__ off, const int64_t* __restrict__ Pp,
+                                                     const int32_t* __restrict__ srt, const int64_t* __restrict__ Kp,
+                                                     const int32_t* __restrict__ item_of,
+                                                     const int32_t* __restrict__ item_n,
+                                                     const int64_t* __restrict__ item_slots, int64_t* __restrict__ cnt,
+                                                     int64_t* __restrict__ slots, int64_t* __restrict__ n_units,
+                                                     const unsigned long long* stats, DevStatus* st) {
+  const int64_t P = *Pp, K = *Kp;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= K + 1; k += (int64_t)gridDim.x * blockDim.x) {
+    if (k == K + 1) {  // the scan reads one element past the count
+      cnt[k] = 0;
+      slots[k] = 0;
+      *n_units = K + 1;
+      if (stats && stats[0] > stats[2] + 1) report(st, K_NO_CONVERGE, P);  // rounds > initial + 1
+      continue;
+    }
+    int64_t rs, re;
+    unit_range(srt, K, P, k, &rs, &re);
+    int64_t c = re - rs, s = off[re] - off[rs];
+    if (k < K) {
+      const int32_t it = item_of[re];
+      c += item_n[it];
+      s += item_slots[it];
+    }
+    cnt[k] = c;
+    slots[k] = s;
+  }
+}
+
+// one warp per unit: the run's offsets and vertices as coalesced copies (4
+// loads in flight per lane), then the item's pieces flattened across lanes.
+// (Measured: batching 32 unit headers per warp with the runs flattened across
+// lanes and items in a separate half of the grid was slower -- 0.31 vs 0.21 ms
+// at 10M: the per-element owner search is instruction-bound.)
+__global__ void __launch_bounds__(256) k_stitch_units(const int64_t* __restrict__ off, const int32_t* __restrict__ v,
+                                                      const int64_t* __restrict__ Pp, const int32_t* __restrict__ srt,
+                                                      const int64_t* __restrict__ Kp,
+                                                      const int32_t* __restrict__ item_of,
+                                                      const int64_t* __restrict__ item_list,
+                                                      const int32_t* __restrict__ item_n,
+                                                      const int32_t* __restrict__ pool,
+                                                      const int64_t* __restrict__ pbase,
+                                                      const int64_t* __restrict__ sbase, int64_t* __restrict__ off_out,
+                                                      int32_t* __restrict__ v_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t P = *Pp, K = *Kp;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k <= K; k += nw) {
+    int64_t rs, re;
+    unit_range(srt, K, P, k, &rs, &re);
+    int64_t pb = pbase[k], sb = sbase[k];
+    const int64_t o0 = off[rs], o1 = off[re];
+    for (int64_t i0 = rs; i0 < re; i0 += 128) {
+      int64_t b[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const int64_t i = i0 + q * 32 + lane;
+        if (i < re) b[q] = off[i];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const int64_t i = i0 + q * 32 + lane;
+        if (i < re) off_out[pb + (i - rs)] = sb + (b[q] - o0);
+      }
+    }
+    for (int64_t j0 = o0; j0 < o1; j0 += 128) {
+      int32_t b[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const int64_t j = j0 + q * 32 + lane;
+        if (j < o1) b[q] = v[j];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const int64_t j = j0 + q * 32 + lane;
+        if (j < o1) v_out[sb + (j - o0)] = b[q];
+      }
+    }
+    if (k == K) continue;
+    pb += re - rs;
+    sb += o1 - o0;
+    const int32_t w = item_of[re];
+    const int64_t list = item_list[w];
+    const int n = item_n[w];
+    if (list < 0) continue;
+    for (int c = 0; c < n; c += 32) {  // the item's pieces, flattened across lanes
+      const int r = c + lane;
+      uint32_t ro = 0;
+      int ln = 0;
+      if (r < n) {
+        ro = (uint32_t)pool[list + 2 * r];
+        ln = (int)((uint32_t)pool[list + 2 * r + 1] & LEN_MASK);
+      }
+      int inc = ln;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const int start = inc - ln, total = __shfl_sync(0xffffffffu, inc, 31);
+      if (r < n) off_out[pb + r] = sb + start;
+      for (int kb = 0; kb < total; kb += 32) {
+        const int e = kb + lane;
+        int lo = 0;
+        for (int step = 16; step > 0; step >>= 1) {
+          const int cand = lo + step;
+          const int cs = __shfl_sync(0xffffffffu, start, cand < 32 ? cand : 31);
+          if (cand < 32 && cand + c < n && cs <= e) lo = cand;
+        }
+        const uint32_t lro = __shfl_sync(0xffffffffu, ro, lo);
+        const int ls = __shfl_sync(0xffffffffu, start, lo);
+        if (e < total) v_out[sb + e] = pool[lro + (e - ls)];
+      }
+      sb += total;
+    }
+  }
+}
+
 __global__ void k_finalize(const int64_t* __restrict__ Pp, const int64_t* __restrict__ pbase,
                            const int64_t* __restrict__ sbase, int64_t* __restrict__ off_out, int64_t* p_out,
                            int64_t* f_out) {
@@ -2755,6 +2895,31 @@ void launch_stitch(const int64_t* off, const int32_t* v, const int64_t* Pp, int6
                    cudaStream_t s) {
   k_stitch<<<kNumSMs * 12, 256, 0, s>>>(off, v, Pp, item_of, items, n_items, item_list, item_n, pool, pbase, sbase,
                                         off_out, v_out);
+  note_launch(1);
+}
+
+void launch_item_sort(const int32_t* item_of, const int64_t* Pp, int64_t Pcap, uint8_t* flag, int32_t* srt,
+                      int64_t* n_srt, int64_t* tiles, cudaStream_t s) {
+  k_item_flags<<<grid_for(Pcap, 256), 256, 0, s>>>(item_of, Pp, Pcap, flag);
+  note_launch(1);
+  launch_select_flags(flag, Pcap, srt, n_srt, tiles, s, 0);
+}
+
+void launch_unit_counts(const int64_t* off, const int64_t* Pp, int64_t Pcap, const int32_t* srt, const int64_t* n_srt,
+                        const int32_t* item_of, const int32_t* item_n, const int64_t* item_slots, int64_t* cnt,
+                        int64_t* slots, int64_t* n_units, const unsigned long long* stats, DevStatus* st,
+                        cudaStream_t s) {
+  k_unit_counts<<<grid_for(Pcap / 8 + 2, 256), 256, 0, s>>>(off, Pp, srt, n_srt, item_of, item_n, item_slots, cnt,
+                                                             slots, n_units, stats, st);
+  note_launch(1);
+}
+
+void launch_stitch_units(const int64_t* off, const int32_t* v, const int64_t* Pp, const int32_t* srt,
+                         const int64_t* n_srt, const int32_t* item_of, const int64_t* item_list, const int32_t* item_n,
+                         const int32_t* pool, const int64_t* pbase, const int64_t* sbase, int64_t* off_out,
+                         int32_t* v_out, cudaStream_t s) {
+  k_stitch_units<<<kNumSMs * 8, 256, 0, s>>>(off, v, Pp, srt, n_srt, item_of, item_list, item_n, pool, pbase, sbase,
+                                             off_out, v_out);
   note_launch(1);
 }
 
