@@ -2641,7 +2641,10 @@ __global__ void __launch_bounds__(256) k_unit_counts(const int64_t* __restrict__
 // (Measured: batching 32 unit headers per warp with the runs flattened across
 // lanes and items in a separate half of the grid was slower -- 0.31 vs 0.21 ms
 // at 10M: the per-element owner search is instruction-bound.)
-__global__ void __launch_bounds__(256) k_stitch_units(const int64_t* __restrict__ off, const int32_t* __restrict__ v,
+#ifndef TM_STITCH_MINB
+#define TM_STITCH_MINB 1
+#endif
+__global__ void __launch_bounds__(256, TM_STITCH_MINB) k_stitch_units(const int64_t* __restrict__ off, const int32_t* __restrict__ v,
                                                       const int64_t* __restrict__ Pp, const int32_t* __restrict__ srt,
                                                       const int64_t* __restrict__ Kp,
                                                       const int32_t* __restrict__ item_of,
