@@ -142,7 +142,8 @@ struct tm_ctx {
   // label
   Buf slots, lbscan;
   // traversal
-  Buf seeds, start, len, overflow, queue, stamp, tiles, nrul, eoff, rulers, startbits, ent_r, ent_base;
+  Buf seeds, start, len, overflow, queue, stamp, tiles, nrul, eoff, rulers, startbits, ent_r, ent_base, ccache;
+  int64_t cc_cap = 0;  // seeds whose short chains k_chain_count caches for k_chain_emit
   // repair
   Buf item_of, items, long_list, item_list, item_n, item_slots, item_state, item_depth, cnt, slotsz, pbase, sbase, pool,
       undo, hugeq, longq, parked, pinchq, iflag, isrt, itiles;
@@ -408,6 +409,8 @@ static int prepare(tm_ctx* ctx, int64_t T, int64_t n = -1) {
   ctx->ecap = Tn + (3 * Tn) / 8 + (3 * Tn) / 16 + 1024;
   ENSURE(ent_r, ctx->ecap * sizeof(int32_t));
   ENSURE(ent_base, ctx->ecap * sizeof(int64_t));
+  ctx->cc_cap = Tn / 4 + 1024;  // seeds beyond it (never at Delaunay densities, P ~ 0.15 T) re-walk
+  ENSURE(ccache, ctx->cc_cap * 2 * sizeof(int4));
   ENSURE(item_of, Tn * sizeof(int32_t));
   ENSURE(items, Tn * sizeof(int32_t));
   ENSURE(long_list, Tn * sizeof(int32_t));
@@ -536,7 +539,8 @@ static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* 
     launch_chain_count(ctx->seeds.as<int32_t>(), ctx->start.as<int32_t>(), &dc->n_seeds, Tn, T,
                        ctx->rulers.as<RulerRec>(),
                        ctx->len.as<int64_t>(), ctx->nrul.as<int64_t>(),
-                       ctx->early_long ? ctx->long_list.as<int32_t>() : nullptr, &dc->n_long, &dc->st, s);
+                       ctx->early_long ? ctx->long_list.as<int32_t>() : nullptr, &dc->n_long,
+                       ctx->ccache.as<int4>(), ctx->cc_cap, &dc->st, s);
   }
   stamp(ctx, 2, s);
   {
@@ -548,7 +552,7 @@ static int enqueue_traverse(tm_ctx* ctx, const int32_t* d_tri32, const int32_t* 
   {
     SegTimer t_(ctx, S_TRAV_WRITE, s);
     launch_chain_emit(ctx->start.as<int32_t>(), &dc->n_seeds, Tn, ctx->rulers.as<RulerRec>(), d_off, ctx->eoff.as<int64_t>(), ctx->ent_r.as<int32_t>(), ctx->ent_base.as<int64_t>(),
-                      ctx->ecap, &dc->st, s);
+                      ctx->ecap, ctx->ccache.as<int4>(), ctx->cc_cap, &dc->st, s);
     if (ctx->early_long) {
       // fork: the long polygons' runs -> their classification -> the long-item
       // repair kernel, on ctx->aux beside the rest of the traversal and the short items
@@ -759,7 +763,7 @@ void tm_ctx_destroy(tm_ctx* ctx) {
   if (!ctx) return;
   Buf* bufs[] = {&ctx->counters, &ctx->slots, &ctx->seeds, &ctx->start, &ctx->len, &ctx->overflow, &ctx->queue,
                  &ctx->stamp, &ctx->tiles, &ctx->nrul, &ctx->eoff, &ctx->rulers, &ctx->startbits,
-                 &ctx->ent_r, &ctx->ent_base, &ctx->item_of, &ctx->items, &ctx->long_list, &ctx->item_list,
+                 &ctx->ent_r, &ctx->ent_base, &ctx->ccache, &ctx->item_of, &ctx->items, &ctx->long_list, &ctx->item_list,
                  &ctx->item_n, &ctx->item_slots, &ctx->item_state, &ctx->item_depth, &ctx->hugeq, &ctx->longq, &ctx->parked, &ctx->pinchq, &ctx->iflag, &ctx->isrt, &ctx->itiles, &ctx->cnt, &ctx->slotsz, &ctx->pbase, &ctx->sbase, &ctx->pool,
                  &ctx->undo, &ctx->xy, &ctx->tri, &ctx->tri32, &ctx->hw, &ctx->max_edge, &ctx->seed, &ctx->tv,
                  &ctx->off0, &ctx->v0, &ctx->fin_off, &ctx->fin_v, &ctx->hw_snap, &ctx->hv,

@@ -78,10 +78,12 @@ void launch_ruler_walk(const int32_t* hw, uint32_t* bits, int64_t T, int64_t t_b
                        cudaStream_t s);
 void launch_chain_count(const int32_t* seeds, const int32_t* start, const int64_t* Pp, int64_t Pcap, int64_t T,
                         const RulerRec* R, int64_t* len, int64_t* nrul,
-                        int32_t* long_list, unsigned int* n_long, DevStatus* st, cudaStream_t s);
+                        int32_t* long_list, unsigned int* n_long, int4* cc, int64_t cc_cap, DevStatus* st,
+                        cudaStream_t s);
 void launch_chain_emit(const int32_t* start, const int64_t* Pp, int64_t Pcap, const RulerRec* R,
                        const int64_t* offsets, const int64_t* eoff,
-                       int32_t* ent_r, int64_t* ent_base, int64_t ecap, DevStatus* st, cudaStream_t s);
+                       int32_t* ent_r, int64_t* ent_base, int64_t ecap, const int4* cc, int64_t cc_cap, DevStatus* st,
+                       cudaStream_t s);
 void launch_ruler_write(const int32_t* tri, const int32_t* hw, const int64_t* n_entries, const int32_t* ent_r,
                         const int64_t* ent_base, const RulerRec* R, int64_t T, int64_t ecap, int32_t* verts,
                         int32_t* hv, cudaStream_t s);

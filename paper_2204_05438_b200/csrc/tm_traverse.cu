@@ -198,21 +198,26 @@ __global__ void __launch_bounds__(256) k_chain_count(const int32_t* __restrict__
                                                      const RulerRec* __restrict__ R,
                                                      int64_t* __restrict__ len, int64_t* __restrict__ nrul,
                                                      int32_t* __restrict__ long_list, unsigned int* n_long,
-                                                     DevStatus* st) {
+                                                     int4* __restrict__ cc, int64_t cc_cap, DevStatus* st) {
   const int64_t P = *Pp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t h0 = start[i];
     long long L = 0, cnt = 0;
+    int4 c0 = make_int4(0, 0, 0, 0), c1 = c0;  // the first four visits (f0, df0, b0, db0), (f1, df1, b1, db1)
     if (h0 >= 0) {
       int32_t f = h0, b = R[h0].prev;  // next ruler to consume going forward / backward
       for (;;) {
         // both walkers' records loaded together: one memory round trip per step of the pair
         const int4 rf = ld_rec(R, f), rb = ld_rec(R, b);
         const int32_t df = rf.y, nf = rf.x, db = rb.y, pb = rb.z;
+        if (cnt == 0) c0.x = f, c0.y = df;
+        else if (cnt == 2) c1.x = f, c1.y = df;
         L += df;
         cnt++;
         if (f == b) break;
         f = nf;
+        if (cnt == 1) c0.z = b, c0.w = db;
+        else if (cnt == 3) c1.z = b, c1.w = db;
         L += db;
         cnt++;
         if (b == f) break;
@@ -222,6 +227,12 @@ __global__ void __launch_bounds__(256) k_chain_count(const int32_t* __restrict__
     }
     len[i] = L;
     nrul[i] = cnt;
+    // chains of <= 4 rulers (most polygons) hand their visits to k_chain_emit,
+    // which then reads 32 coalesced bytes per seed instead of re-walking R
+    if (cc != nullptr && i < cc_cap && cnt <= 4) {
+      cc[2 * i] = c0;
+      cc[2 * i + 1] = c1;
+    }
     // whole path: the long polygons go to the early long-item repair (k_classify_long)
     if (long_list && L > kClassifyShort) long_list[atomicAdd(n_long, 1u)] = (int32_t)i;
   }
@@ -232,7 +243,8 @@ __global__ void __launch_bounds__(256) k_chain_emit(const int32_t* __restrict__ 
                                                     const RulerRec* __restrict__ R,
                                                     const int64_t* __restrict__ offsets, const int64_t* __restrict__ eoff,
                                                     int32_t* __restrict__ ent_r, int64_t* __restrict__ ent_base,
-                                                    int64_t ecap, DevStatus* st) {
+                                                    int64_t ecap, const int4* __restrict__ cc, int64_t cc_cap,
+                                                    DevStatus* st) {
   const int64_t P = *Pp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t h0 = start[i];
@@ -240,6 +252,16 @@ __global__ void __launch_bounds__(256) k_chain_emit(const int32_t* __restrict__ 
     if (h0 < 0 || kb < kf) continue;
     if (kb >= ecap) { report(st, K_STRUCT, i); continue; }
     int64_t pf = offsets[i], pb = offsets[i + 1];  // forward start / backward end offsets
+    const int64_t cnt = kb - kf + 1;
+    if (cc != nullptr && i < cc_cap && cnt <= 4) {  // replay k_chain_count's visits: f0, b0, f1, b1
+      const int4 c0 = __ldg(cc + 2 * i), c1 = __ldg(cc + 2 * i + 1);
+      ent_r[kf] = c0.x;
+      ent_base[kf] = pf;
+      if (cnt >= 2) { pb -= c0.w; ent_r[kb] = c0.z; ent_base[kb] = pb; }
+      if (cnt >= 3) { pf += c0.y; ent_r[kf + 1] = c1.x; ent_base[kf + 1] = pf; }
+      if (cnt >= 4) { pb -= c1.w; ent_r[kb - 1] = c1.z; ent_base[kb - 1] = pb; }
+      continue;
+    }
     int32_t f = h0, b = R[h0].prev;
     for (;;) {
       const int4 rf = ld_rec(R, f), rb = ld_rec(R, b);
@@ -344,17 +366,25 @@ void launch_ruler_walk(const int32_t* hw, uint32_t* bits, int64_t T, int64_t t_b
 
 void launch_chain_count(const int32_t* seeds, const int32_t* start, const int64_t* Pp, int64_t Pcap, int64_t T,
                         const RulerRec* R, int64_t* len, int64_t* nrul,
-                        int32_t* long_list, unsigned int* n_long, DevStatus* st, cudaStream_t s) {
+                        int32_t* long_list, unsigned int* n_long, int4* cc, int64_t cc_cap, DevStatus* st,
+                        cudaStream_t s) {
+#ifdef TM_NO_CHAIN_CACHE  // A/B: k_chain_emit re-walks every chain
+  cc = nullptr;
+#endif
   k_chain_count<<<grid_for(Pcap, 256), 256, 0, s>>>(seeds, start, Pp, 3 * T + 3, R, len, nrul,
-                                                    long_list, n_long, st);
+                                                    long_list, n_long, cc, cc_cap, st);
   note_launch(1);
 }
 
 void launch_chain_emit(const int32_t* start, const int64_t* Pp, int64_t Pcap, const RulerRec* R,
                        const int64_t* offsets, const int64_t* eoff,
-                       int32_t* ent_r, int64_t* ent_base, int64_t ecap, DevStatus* st, cudaStream_t s) {
+                       int32_t* ent_r, int64_t* ent_base, int64_t ecap, const int4* cc, int64_t cc_cap, DevStatus* st,
+                       cudaStream_t s) {
+#ifdef TM_NO_CHAIN_CACHE
+  cc = nullptr;
+#endif
   k_chain_emit<<<grid_for(Pcap, 256), 256, 0, s>>>(start, Pp, R, offsets, eoff, ent_r, ent_base,
-                                                   ecap, st);
+                                                   ecap, cc, cc_cap, st);
   note_launch(1);
 }
 
