@@ -1935,6 +1935,7 @@ __device__ __forceinline__ void seg_body(RepairCtx c, const int32_t* __restrict_
   // so the reset of one round never races with the previous round's readers
   __shared__ int s_ntip, s_ntouch, s_stop, s_fail, s_ntb[2], s_need, s_tot;
   __shared__ PairMsg pmsg[kSegWarps / 2];
+  __shared__ int s_wcnt[kSegWarps], s_wneed[kSegWarps];
   __shared__ long long s_base;
   __shared__ unsigned int s_w;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -2094,7 +2095,8 @@ __device__ __forceinline__ void seg_body(RepairCtx c, const int32_t* __restrict_
       SPiece* in = recs + cur * rec_cap;
       SPiece* out = recs + (cur ^ 1) * rec_cap;
       // output slot of every input record (prefix over tip flags) and the
-      // segments the round may need, warp 0
+      // segments the round may need
+#ifdef TM_SEG_WARP0_SCAN  // A/B: warp 0 alone (n / 32 dependent steps per round)
       if (wib == 0) {
         int carry = 0, need = 0;
         for (int base = 0; base < n; base += 32) {
@@ -2116,6 +2118,46 @@ __device__ __forceinline__ void seg_body(RepairCtx c, const int32_t* __restrict_
       }
       if (threadIdx.x == 0) s_ntb[cur ^ 1] = 0;
       __syncthreads();
+#else
+      // the whole block, one record per thread per pass (the record list
+      // grows with the splits: hundreds of pieces in the late rounds)
+      {
+        int carry = 0, need = 0;  // block-uniform
+        for (int base = 0; base < n; base += blockDim.x) {
+          const int r = base + threadIdx.x;
+          const int t = (r < n && in[r].ftip >= 0) ? 1 : 0;
+          int inc = t;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, inc, o);
+            if (lane >= o) inc += y;
+          }
+          int nd = t ? 2 * (in[r].nseg + 4) : 0;
+          for (int o = 16; o > 0; o >>= 1) nd += __shfl_xor_sync(kFull, nd, o);
+          if (lane == 31) s_wcnt[wib] = inc;
+          if (lane == 0) s_wneed[wib] = nd;
+          __syncthreads();
+          int wpre = 0, tot = 0, ntot = 0;
+#pragma unroll
+          for (int w2 = 0; w2 < kSegWarps; w2++) {
+            const int x = s_wcnt[w2];
+            wpre += w2 < wib ? x : 0;
+            tot += x;
+            ntot += s_wneed[w2];
+          }
+          const int ex = carry + wpre + inc - t;
+          if (r < n) s_out[r] = r + ex;
+          if (t) tlist[ex] = r;  // the tipped records, in order
+          carry += tot;
+          need += ntot;
+          __syncthreads();  // s_wcnt / s_wneed reused by the next pass
+        }
+        if (threadIdx.x == 0) {
+          s_need = need;
+          s_ntb[cur ^ 1] = 0;
+        }
+        __syncthreads();
+      }
+#endif
       // Segments are bump-allocated in one half of the arena; when a round
       // would overflow it, the live pieces are first compacted into the other
       // half, so the arena only ever has to hold the live pieces.
