@@ -9,7 +9,6 @@ GPU: the same partitions run through the C ABI (tm_ctx_set_partition) as
 logical ranks on one device (the G-way partitioned path on one
 GPU), stitched with the same bases."""
 import os
-import socket
 
 import numpy as np
 import pytest
@@ -21,12 +20,13 @@ from paper_2204_05438_b200 import distributed as D
 CASES = ("aniso2k_s1", "clust5k_s0", "sun", "u1k_unit")
 
 
-def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
+def _store_path():
+    """A fresh file for a file:// rendezvous (no TCP port to race for)."""
+    import tempfile
+    fd, path = tempfile.mkstemp(prefix="termesh_pg_")
+    os.close(fd)
+    os.unlink(path)
+    return path
 
 
 def oracle_partition(tri, b, e, guard_extra=-1):
@@ -56,11 +56,10 @@ def test_exclusive_bases():
     assert pb.tolist() == [0, 3, 3] and sb.tolist() == [0, 10, 10]
 
 
-def _worker(rank, world, port, names, q):
+def _worker(rank, world, store, names, q):
     import torch
     import torch.distributed as dist
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", init_method=f"file://{store}", rank=rank, world_size=world)
     try:
         for name in names:
             tri, g = load_case(name)
@@ -95,7 +94,7 @@ def test_stitch_gloo(world):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
-    mp.start_processes(_worker, args=(world, _free_port(), CASES, q), nprocs=world, join=True,
+    mp.start_processes(_worker, args=(world, _store_path(), CASES, q), nprocs=world, join=True,
                        start_method="spawn")
     res = [q.get() for _ in CASES]
     assert all(ok for _, ok in res), res
@@ -147,8 +146,7 @@ def test_library_nccl_comm_single_rank(cuda):
     one-rank group: the counts exchange and the stitch go through it."""
     import torch
     import torch.distributed as dist
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
-    dist.init_process_group("gloo", rank=0, world_size=1)
+    dist.init_process_group("gloo", init_method=f"file://{_store_path()}", rank=0, world_size=1)
     try:
         comm = D.Comm()
         send = torch.arange(8, dtype=torch.int64, device=cuda)
@@ -203,8 +201,7 @@ def test_split_labels_single_rank_nccl(cuda):
     NCCL communicator) on a one-rank group."""
     import torch
     import torch.distributed as dist
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
-    dist.init_process_group("gloo", rank=0, world_size=1)
+    dist.init_process_group("gloo", init_method=f"file://{_store_path()}", rank=0, world_size=1)
     try:
         for name in ("aniso2k_s1", "u1k_unit"):
             tri, g = load_case(name)
